@@ -1,0 +1,54 @@
+// Drop-in serial RK entry point (ref/include/asyrk/kaczmarz.hpp:20-115, hot-path
+// subset). rk_solve runs on the GPU's deterministic worker and reproduces the
+// reference's iterates bit for bit.
+#pragma once
+
+#include <cstdint>
+#include <random>
+#include <span>
+#include <vector>
+
+#include "asyrk/csr.hpp"
+#include "asyrk/rng.hpp"
+#include "asyrk/trace.hpp"
+
+namespace asyrk {
+
+class SolutionProjector;  // dense oracle of the reference (not on the device path)
+
+inline constexpr index_t kAllComponents = -1;
+
+enum class UpdateVariant { single_component, full_row };
+
+/// Walker alias sampler over a fixed nonnegative weight vector
+/// (ref kaczmarz.hpp:32-41); the construction order matches the reference so
+/// seeded draws are identical.
+class AliasTable {
+  public:
+    explicit AliasTable(std::span<const double> weights);
+    index_t sample(std::mt19937_64& gen) const;
+    index_t size() const { return static_cast<index_t>(prob_.size()); }
+
+  private:
+    std::vector<double> prob_;
+    std::vector<index_t> alias_;
+};
+
+enum class Sampling {
+    uniform,            // rows equiprobable; requires normalized A
+    norm_proportional,  // P(i) proportional to ||a_i||^2, alias table
+    shuffle,            // per-epoch random permutation, each row once
+};
+
+struct RkConfig {
+    index_t max_epochs = 100;
+    double target_r_sq = 0.0;
+    std::uint64_t seed = 0;
+    Sampling sampling = Sampling::uniform;
+    const std::vector<double>* x_star = nullptr;
+    const SolutionProjector* projector = nullptr;
+};
+
+Trace rk_solve(const CsrMatrix& A, std::span<const double> b, std::span<const double> x0, const RkConfig& cfg);
+
+}  // namespace asyrk

@@ -1,0 +1,217 @@
+/*
+ * asyrk_cuda.h — the drop-in C ABI of the B200-native AsyRK hot path.
+ *
+ * Plain C: pointers, sizes and PODs only (no C++, no torch types); no
+ * function throws. Every entry point returns an asyrk_status whose values are
+ * the reference's ErrorCode ordinals + 1 (ref/include/asyrk/error.hpp:8-33),
+ * so a host wrapper can rethrow asyrk::Error{code, asyrk_last_error()}
+ * exactly as the reference does. Device failures map to the closest
+ * reference code (see ASYRK_E_* below and DESIGN.md §Errors).
+ *
+ * Entry points and the reference interface each one replaces:
+ *   asyrk_solve_parallel     solve_parallel          ref/include/asyrk/parallel.hpp:52-54
+ *                                                    (pybind: ref/bindings/module.cpp:173-200,297-303)
+ *   asyrk_rk_solve           rk_solve                ref/include/asyrk/kaczmarz.hpp:108-109
+ *                                                    (pybind: ref/bindings/module.cpp:156-171,292-296)
+ *   asyrk_sweep_threads      sweep_threads           ref/include/asyrk/parallel.hpp:73-75
+ *   asyrk_residuals          residuals               ref/include/asyrk/csr.hpp:89-90
+ *   asyrk_power_iteration_lambda_max
+ *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:131-132
+ *   asyrk_system_*           (new) device-resident CSR + b handle: the
+ *                            "device-CSR cache" the reference has no
+ *                            equivalent of (SURVEY.md §8b "Ownership").
+ *   asyrk_mrhs_*             (new) multi-right-hand-side AsyRK (config 5);
+ *                            the reference is single-RHS.
+ *
+ * Threading: calls are synchronous and blocking (the caller's thread is the
+ * coordinator, as in ref/src/parallel.cpp:388-408). A system handle must not
+ * be used by two threads at once.
+ */
+#ifndef ASYRK_CUDA_H
+#define ASYRK_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ASYRK_ABI_VERSION 1
+
+/* ErrorCode ordinal + 1 (ref/include/asyrk/error.hpp:8-33). */
+typedef enum {
+    ASYRK_OK = 0,
+    ASYRK_E_IndexOutOfRange = 1,
+    ASYRK_E_DuplicateEntry = 2,
+    ASYRK_E_ZeroRow = 3,
+    ASYRK_E_ZeroColumn = 4,
+    ASYRK_E_NotNormalized = 5,
+    ASYRK_E_DimensionMismatch = 6,
+    ASYRK_E_PowerIterationDiverged = 7,
+    ASYRK_E_NonFinite = 8,
+    ASYRK_E_ComponentNotInSupport = 9,
+    ASYRK_E_Inconsistent = 10,
+    ASYRK_E_TooLarge = 11,             /* also: device out of memory, index width overflow */
+    ASYRK_E_InvalidRho = 12,
+    ASYRK_E_MissingStats = 13,
+    ASYRK_E_StepTooLarge = 14,
+    ASYRK_E_ZeroLambdaMin = 15,
+    ASYRK_E_InvalidGamma = 16,
+    ASYRK_E_NonPositiveData = 17,
+    ASYRK_E_InsufficientData = 18,
+    ASYRK_E_NonPositiveSigma = 19,
+    ASYRK_E_SigmaUnavailable = 20,
+    ASYRK_E_InfeasibleSpec = 21,
+    ASYRK_E_ThreadSpawnFailure = 22,   /* also: kernel launch failure / no CUDA device */
+    ASYRK_E_IoError = 23,
+    ASYRK_E_InvalidArgument = 24,
+} asyrk_status;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* asyrk_last_error(void);
+int asyrk_abi_version(void);
+
+/* Host CSR, the reference CsrMatrix fields (ref/include/asyrk/csr.hpp:69-75).
+ * row_norm are the reference's cached norms (csr.cpp:53-61, recomputed by
+ * normalize_rows csr.cpp:130-134); they enter the projection coefficient
+ * gamma*res/(nrm*nrm) and so must be passed, not assumed to be 1. */
+typedef struct {
+    int64_t m, n, nnz;
+    const int64_t* row_ptr;  /* m+1 */
+    const int64_t* col_idx;  /* nnz, strictly increasing within a row */
+    const double* values;    /* nnz */
+    const double* row_norm;  /* m */
+    int32_t normalized;      /* CsrMatrix::is_normalized() */
+} asyrk_csr_view;
+
+/* UpdateVariant (kaczmarz.hpp:20) */
+enum { ASYRK_SINGLE_COMPONENT = 0, ASYRK_FULL_ROW = 1 };
+/* ParSampling (parallel.hpp:14-17) + device extension: norm_proportional
+ * (alias table over ||a_i||^2, only Sampling in rk_solve upstream). */
+enum { ASYRK_WITH_REPLACEMENT = 0, ASYRK_SLICE_SHUFFLE = 1, ASYRK_NORM_PROPORTIONAL = 2 };
+/* Sampling (kaczmarz.hpp:89-93) */
+enum { ASYRK_RK_UNIFORM = 0, ASYRK_RK_NORM_PROPORTIONAL = 1, ASYRK_RK_SHUFFLE = 2 };
+/* Device precision of the async path (values / x). fp64 is the reference's. */
+enum { ASYRK_F64 = 0, ASYRK_F32 = 1, ASYRK_F32_VALUES_F64_X = 2 };
+
+/* RunConfig (parallel.hpp:19-31) plus device extensions. threads maps to
+ * concurrent warp-workers; threads == 1 is the deterministic path that
+ * consumes the reference's mt19937_64 row sequence. */
+typedef struct {
+    int64_t threads;
+    double gamma;
+    int64_t epochs;
+    double target_r_sq;
+    int32_t variant;           /* ASYRK_FULL_ROW | ASYRK_SINGLE_COMPONENT */
+    int32_t sampling;          /* ASYRK_SLICE_SHUFFLE (reference default) | ... */
+    uint64_t seed;
+    int64_t snapshot_interval;
+    const double* x_star;      /* host, n entries, or NULL (dist_sq disabled) */
+    /* --- device extensions (zero = reference behaviour) --- */
+    int32_t precision;         /* ASYRK_F64 ... */
+    int32_t allow_unnormalized; /* 1: async/norm_proportional on raw rows (config 4) */
+} asyrk_run_config;
+
+/* RkConfig (kaczmarz.hpp:95-103) */
+typedef struct {
+    int64_t max_epochs;
+    double target_r_sq;
+    uint64_t seed;
+    int32_t sampling;          /* ASYRK_RK_* */
+    const double* x_star;
+} asyrk_rk_config;
+
+/* Trace (trace.hpp:11-37), caller-allocated. count receives the number of
+ * records produced; at most cap are written. dist_sq entries are -1 when
+ * x_star is NULL. final_x (n entries) may be NULL. */
+typedef struct {
+    int64_t cap;
+    int64_t count;
+    int64_t* epoch_index;
+    double* r_sq;
+    double* grad_sq;
+    double* dist_sq;
+    double* wall_seconds;
+    int64_t* updates_applied;
+    double* final_x;
+} asyrk_trace_out;
+
+/* InstrumentReport (parallel.hpp:36-42). */
+typedef struct {
+    int64_t row_updates;
+    int64_t increments;
+    double max_abs_error;
+    double tolerance;
+    int32_t consistent;
+} asyrk_instrument_out;
+
+/* Device-side timing of the last solve on a system (CUDA events on the
+ * launching stream). */
+typedef struct {
+    double solve_ms;           /* first to last kernel of the solve */
+    double worker_ms;          /* sum over projection-kernel launches */
+    double monitor_ms;         /* sum over residual-monitor launches */
+    int64_t worker_launches;
+    int64_t monitor_launches;
+    int64_t kernel_launches;   /* all kernels this library launched */
+    int64_t projections;       /* row projections applied */
+    int32_t resident_warps;    /* concurrent worker warps actually resident */
+    int32_t warps;             /* worker warps launched */
+} asyrk_solve_stats;
+
+/* ---- one-shot entry points: host buffers in, host buffers out ---------- */
+
+/* solve_parallel (parallel.hpp:52-54). instrument may be NULL. */
+asyrk_status asyrk_solve_parallel(const asyrk_csr_view* A, const double* b, const double* x0,
+                                  const asyrk_run_config* cfg, asyrk_trace_out* trace,
+                                  asyrk_instrument_out* instrument);
+
+/* rk_solve (kaczmarz.hpp:108-109) — deterministic, bit-identical iterates. */
+asyrk_status asyrk_rk_solve(const asyrk_csr_view* A, const double* b, const double* x0,
+                            const asyrk_rk_config* cfg, asyrk_trace_out* trace);
+
+/* residuals (csr.hpp:89-90): r_sq, grad_sq in the reference's summation order. */
+asyrk_status asyrk_residuals(const asyrk_csr_view* A, const double* x, const double* b, double* r_sq,
+                             double* grad_sq);
+
+/* power_iteration_lambda_max (stats.hpp:131-132), same start vector. */
+asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double tol, int64_t max_iters,
+                                              double* lambda_max);
+
+/* sweep_threads (parallel.hpp:73-75): one solve per entry of thread_list
+ * (must contain 1); out arrays have n_threads entries. */
+asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const double* x0,
+                                 const asyrk_run_config* cfg, const int64_t* thread_list,
+                                 int64_t n_threads, double* wall_seconds, int64_t* epochs,
+                                 double* final_r_sq, double* speedup);
+
+/* ---- device-resident system: upload once, solve many times ------------- */
+typedef struct asyrk_system asyrk_system;
+
+/* Uploads A (+ b) and packs the device layout (row records, CSC, alias).
+ * stream: a cudaStream_t or NULL for a library-owned stream. */
+asyrk_status asyrk_system_create(const asyrk_csr_view* A, const double* b, int32_t precision,
+                                 void* stream, asyrk_system** out);
+asyrk_status asyrk_system_destroy(asyrk_system* sys);
+/* x0 NULL means x0 = 0. */
+asyrk_status asyrk_system_solve(asyrk_system* sys, const double* x0, const asyrk_run_config* cfg,
+                                asyrk_trace_out* trace, asyrk_instrument_out* instrument);
+asyrk_status asyrk_system_rk_solve(asyrk_system* sys, const double* x0, const asyrk_rk_config* cfg,
+                                   asyrk_trace_out* trace);
+asyrk_status asyrk_system_residuals(asyrk_system* sys, const double* x, double* r_sq, double* grad_sq);
+/* Replace b (m entries) of a system in place (device re-pack of the record headers). */
+asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b);
+/* y = A x (m entries) and y = A^T x (n entries), reference summation order
+ * (CsrMatrix::multiply / multiply_transpose, ref/src/csr.cpp:72-92). */
+asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y);
+asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x, double* y);
+asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t max_iters, double* lambda_max,
+                                          int64_t* iterations);
+asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
+/* Largest number of worker warps that are co-resident for this system. */
+asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ASYRK_CUDA_H */

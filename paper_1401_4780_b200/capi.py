@@ -1,0 +1,316 @@
+"""ctypes view of the C ABI (include/asyrk_cuda.h, include/asyrk_datagen.h).
+
+This is the binding a ctypes-based host would write against the drop-in
+library (INTEGRATION.md shows the same for cgo/JNI-style hosts). bench.py and
+the GPU parity tests drive the hot path through it. Loading fails loudly if
+``libasyrk_b200.so`` has not been built; there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libasyrk_b200.so")
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_i32p = C.POINTER(C.c_int32)
+
+ERROR_NAMES = [
+    "IndexOutOfRange", "DuplicateEntry", "ZeroRow", "ZeroColumn", "NotNormalized",
+    "DimensionMismatch", "PowerIterationDiverged", "NonFinite", "ComponentNotInSupport",
+    "Inconsistent", "TooLarge", "InvalidRho", "MissingStats", "StepTooLarge", "ZeroLambdaMin",
+    "InvalidGamma", "NonPositiveData", "InsufficientData", "NonPositiveSigma", "SigmaUnavailable",
+    "InfeasibleSpec", "ThreadSpawnFailure", "IoError", "InvalidArgument",
+]
+
+F64, F32, F32X64 = 0, 1, 2
+SINGLE_COMPONENT, FULL_ROW = 0, 1
+WITH_REPLACEMENT, SLICE_SHUFFLE, NORM_PROPORTIONAL = 0, 1, 2
+RK_UNIFORM, RK_NORM_PROPORTIONAL, RK_SHUFFLE = 0, 1, 2
+
+
+class CsrView(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("nnz", C.c_int64), ("row_ptr", _i64p), ("col_idx", _i64p),
+                ("values", _f64p), ("row_norm", _f64p), ("normalized", C.c_int32)]
+
+
+class RunConfig(C.Structure):
+    _fields_ = [("threads", C.c_int64), ("gamma", C.c_double), ("epochs", C.c_int64), ("target_r_sq", C.c_double),
+                ("variant", C.c_int32), ("sampling", C.c_int32), ("seed", C.c_uint64),
+                ("snapshot_interval", C.c_int64), ("x_star", _f64p), ("precision", C.c_int32),
+                ("allow_unnormalized", C.c_int32)]
+
+
+class RkConfig(C.Structure):
+    _fields_ = [("max_epochs", C.c_int64), ("target_r_sq", C.c_double), ("seed", C.c_uint64),
+                ("sampling", C.c_int32), ("x_star", _f64p)]
+
+
+class TraceOut(C.Structure):
+    _fields_ = [("cap", C.c_int64), ("count", C.c_int64), ("epoch_index", _i64p), ("r_sq", _f64p),
+                ("grad_sq", _f64p), ("dist_sq", _f64p), ("wall_seconds", _f64p), ("updates_applied", _i64p),
+                ("final_x", _f64p)]
+
+
+class InstrumentOut(C.Structure):
+    _fields_ = [("row_updates", C.c_int64), ("increments", C.c_int64), ("max_abs_error", C.c_double),
+                ("tolerance", C.c_double), ("consistent", C.c_int32)]
+
+
+class SolveStats(C.Structure):
+    _fields_ = [("solve_ms", C.c_double), ("worker_ms", C.c_double), ("monitor_ms", C.c_double),
+                ("worker_launches", C.c_int64), ("monitor_launches", C.c_int64), ("kernel_launches", C.c_int64),
+                ("projections", C.c_int64), ("resident_warps", C.c_int32), ("warps", C.c_int32)]
+
+
+class AsyrkError(ValueError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.name = ERROR_NAMES[status - 1] if 1 <= status <= len(ERROR_NAMES) else f"status{status}"
+        super().__init__(f"{self.name}: {msg}")
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is not built; run __graft_entry__.build() (make -C "
+                              "paper_1401_4780_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.asyrk_last_error.restype = C.c_char_p
+        sp = C.c_void_p
+        L.asyrk_system_create.argtypes = [C.POINTER(CsrView), _f64p, C.c_int32, C.c_void_p, C.POINTER(sp)]
+        L.asyrk_system_destroy.argtypes = [sp]
+        L.asyrk_system_solve.argtypes = [sp, _f64p, C.POINTER(RunConfig), C.POINTER(TraceOut),
+                                         C.POINTER(InstrumentOut)]
+        L.asyrk_system_rk_solve.argtypes = [sp, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
+        L.asyrk_system_residuals.argtypes = [sp, _f64p, _f64p, _f64p]
+        L.asyrk_system_set_rhs.argtypes = [sp, _f64p]
+        L.asyrk_system_multiply.argtypes = [sp, _f64p, _f64p]
+        L.asyrk_system_multiply_transpose.argtypes = [sp, _f64p, _f64p]
+        L.asyrk_system_power_iteration.argtypes = [sp, C.c_double, C.c_int64, _f64p, _i64p]
+        L.asyrk_system_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
+        L.asyrk_system_max_resident_warps.argtypes = [sp, C.c_int32, _i32p]
+        L.asyrk_solve_parallel.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig),
+                                           C.POINTER(TraceOut), C.POINTER(InstrumentOut)]
+        L.asyrk_rk_solve.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
+        L.asyrk_residuals.argtypes = [C.POINTER(CsrView), _f64p, _f64p, _f64p, _f64p]
+        L.asyrk_power_iteration_lambda_max.argtypes = [C.POINTER(CsrView), C.c_double, C.c_int64, _f64p]
+        L.asyrk_sweep_threads.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig), _i64p, C.c_int64,
+                                          _f64p, _i64p, _f64p, _f64p]
+        L.asyrk_generate_fixed_theta.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int32, C.c_double,
+                                                 C.c_int64, C.c_int32, _i64p, _i64p, _f64p, _f64p, _f64p, _f64p,
+                                                 _i32p]
+        _lib = L
+    return _lib
+
+
+# every symbol include/asyrk_cuda.h and include/asyrk_datagen.h declare
+EXPORTED = [
+    "asyrk_last_error", "asyrk_abi_version", "asyrk_solve_parallel", "asyrk_rk_solve", "asyrk_residuals",
+    "asyrk_power_iteration_lambda_max", "asyrk_sweep_threads", "asyrk_system_create", "asyrk_system_destroy",
+    "asyrk_system_solve", "asyrk_system_rk_solve", "asyrk_system_residuals", "asyrk_system_set_rhs",
+    "asyrk_system_multiply", "asyrk_system_multiply_transpose", "asyrk_system_power_iteration",
+    "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
+]
+
+
+def check(status: int):
+    if status:
+        raise AsyrkError(status, lib().asyrk_last_error().decode())
+
+
+class HostCsr:
+    """Host CSR arrays in the reference's layout (int64 indices, fp64 values)."""
+
+    def __init__(self, m, n, row_ptr, col_idx, values, row_norm=None, normalized=None):
+        self.m, self.n = int(m), int(n)
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        if row_norm is None:
+            seg = np.add.reduceat(self.values * self.values, self.row_ptr[:-1]) if self.m else np.zeros(0)
+            row_norm = np.sqrt(seg)
+        self.row_norm = np.ascontiguousarray(row_norm, dtype=np.float64)
+        if normalized is None:
+            normalized = bool(np.all(np.abs(self.row_norm - 1.0) <= 1e-12))
+        self.normalized = bool(normalized)
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+    def view(self):
+        return CsrView(self.m, self.n, self.nnz, _ptr(self.row_ptr, _i64p), _ptr(self.col_idx, _i64p),
+                       _ptr(self.values, _f64p), _ptr(self.row_norm, _f64p), 1 if self.normalized else 0)
+
+
+def generate_fixed_theta(m, n, theta, seed, dist="normal", scale_decades=0.0, k=1, threads=0):
+    """Seeded fixed-theta system (include/asyrk_datagen.h). Returns (HostCsr, b, x_star)."""
+    nnz = m * theta
+    rp = np.zeros(m + 1, np.int64)
+    ci = np.zeros(nnz, np.int64)
+    v = np.zeros(nnz)
+    rn = np.zeros(m)
+    b = np.zeros(m * k)
+    xs = np.zeros(n * k)
+    norm = C.c_int32(0)
+    check(lib().asyrk_generate_fixed_theta(m, n, theta, seed, 1 if dist == "uniform" else 0, scale_decades, k,
+                                           threads, _ptr(rp, _i64p), _ptr(ci, _i64p), _ptr(v, _f64p),
+                                           _ptr(rn, _f64p), _ptr(b, _f64p), _ptr(xs, _f64p), C.byref(norm)))
+    A = HostCsr(m, n, rp, ci, v, rn, bool(norm.value))
+    if k > 1:
+        return A, b.reshape(m, k), xs.reshape(n, k)
+    return A, b, xs
+
+
+class _Trace:
+    def __init__(self, n, cap, want_x=True):
+        self.b = dict(epoch_index=np.zeros(cap, np.int64), r_sq=np.zeros(cap), grad_sq=np.zeros(cap),
+                      dist_sq=np.zeros(cap), wall_seconds=np.zeros(cap), updates_applied=np.zeros(cap, np.int64),
+                      final_x=np.zeros(n) if want_x else None)
+        b = self.b
+        self.out = TraceOut(cap, 0, _ptr(b["epoch_index"], _i64p), _ptr(b["r_sq"], _f64p),
+                            _ptr(b["grad_sq"], _f64p), _ptr(b["dist_sq"], _f64p), _ptr(b["wall_seconds"], _f64p),
+                            _ptr(b["updates_applied"], _i64p), _ptr(b["final_x"], _f64p))
+
+    def result(self, has_dist):
+        k = min(self.out.count, self.out.cap)
+        d = {key: (val[:k].copy() if key != "final_x" else val) for key, val in self.b.items()
+             if key != "dist_sq" or has_dist}
+        return d
+
+
+def _run_config(threads=1, gamma=1.0, epochs=100, target=0.0, variant=FULL_ROW, sampling=SLICE_SHUFFLE, seed=0,
+                snapshot_interval=1, x_star=None, precision=F64, allow_unnormalized=0):
+    return RunConfig(threads, gamma, epochs, target, variant, sampling, seed, snapshot_interval,
+                     _ptr(x_star, _f64p), precision, allow_unnormalized)
+
+
+class System:
+    """Device-resident A (+ b): asyrk_system_* of the C ABI."""
+
+    def __init__(self, A: HostCsr, b=None, precision=F64, stream=None):
+        self.A = A
+        self.m, self.n = A.m, A.n
+        self.precision = precision
+        self._b = np.ascontiguousarray(b, dtype=np.float64) if b is not None else None
+        h = C.c_void_p()
+        check(lib().asyrk_system_create(C.byref(A.view()), _ptr(self._b, _f64p), precision,
+                                        C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().asyrk_system_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_rhs(self, b):
+        self._b = np.ascontiguousarray(b, dtype=np.float64)
+        check(lib().asyrk_system_set_rhs(self.h, _ptr(self._b, _f64p)))
+
+    def solve(self, x0=None, instrument=False, want_x=True, **cfg):
+        xs = cfg.pop("x_star", None)
+        xs = np.ascontiguousarray(xs, dtype=np.float64) if xs is not None else None
+        c = _run_config(x_star=xs, **cfg)
+        cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
+        tr = _Trace(self.n, cap, want_x)
+        x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+        rep = InstrumentOut()
+        check(lib().asyrk_system_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out),
+                                       C.byref(rep) if instrument else None))
+        d = tr.result(xs is not None)
+        if instrument:
+            d["instrument"] = dict(row_updates=rep.row_updates, increments=rep.increments,
+                                   max_abs_error=rep.max_abs_error, tolerance=rep.tolerance,
+                                   consistent=bool(rep.consistent))
+        return d
+
+    def rk_solve(self, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):
+        xs = np.ascontiguousarray(x_star, dtype=np.float64) if x_star is not None else None
+        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+        tr = _Trace(self.n, max(max_epochs, 0) + 2)
+        x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+        check(lib().asyrk_system_rk_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out)))
+        return tr.result(xs is not None)
+
+    def residuals(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        rs, gs = C.c_double(), C.c_double()
+        check(lib().asyrk_system_residuals(self.h, _ptr(x, _f64p), C.byref(rs), C.byref(gs)))
+        return rs.value, gs.value
+
+    def multiply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.m)
+        check(lib().asyrk_system_multiply(self.h, _ptr(x, _f64p), _ptr(y, _f64p)))
+        return y
+
+    def multiply_transpose(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.zeros(self.n)
+        check(lib().asyrk_system_multiply_transpose(self.h, _ptr(x, _f64p), _ptr(y, _f64p)))
+        return y
+
+    def power_iteration(self, tol=1e-6, max_iters=200000):
+        lam, it = C.c_double(), C.c_int64()
+        check(lib().asyrk_system_power_iteration(self.h, tol, max_iters, C.byref(lam), C.byref(it)))
+        return lam.value, it.value
+
+    def stats(self):
+        s = SolveStats()
+        check(lib().asyrk_system_last_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in SolveStats._fields_}
+
+    def max_resident_warps(self, precision=None):
+        out = C.c_int32()
+        check(lib().asyrk_system_max_resident_warps(self.h, self.precision if precision is None else precision,
+                                                    C.byref(out)))
+        return out.value
+
+
+def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, **cfg):
+    """One-shot asyrk_solve_parallel with host buffers (upload, solve, download)."""
+    xs = cfg.pop("x_star", None)
+    xs = np.ascontiguousarray(xs, dtype=np.float64) if xs is not None else None
+    c = _run_config(x_star=xs, **cfg)
+    cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
+    tr = _Trace(A.n, cap, want_x)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+    rep = InstrumentOut()
+    check(lib().asyrk_solve_parallel(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0a, _f64p), C.byref(c),
+                                     C.byref(tr.out), C.byref(rep) if instrument else None))
+    d = tr.result(xs is not None)
+    if instrument:
+        d["instrument"] = dict(row_updates=rep.row_updates, increments=rep.increments,
+                               max_abs_error=rep.max_abs_error, tolerance=rep.tolerance,
+                               consistent=bool(rep.consistent))
+    return d
+
+
+def rk_solve_host(A: HostCsr, b, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):
+    xs = np.ascontiguousarray(x_star, dtype=np.float64) if x_star is not None else None
+    c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+    tr = _Trace(A.n, max(max_epochs, 0) + 2)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+    check(lib().asyrk_rk_solve(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out)))
+    return tr.result(xs is not None)

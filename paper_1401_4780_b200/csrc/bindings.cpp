@@ -1,0 +1,208 @@
+// pybind11 module `_asyrk` with the reference's Python signatures
+// (ref/bindings/module.cpp:281-318, hot-path subset): dict in / dict out,
+// triplets -> CSR -> normalize_rows inside, errors as
+// ValueError("<ErrorCodeName>: message") (module.cpp:271-279).
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "asyrk/error.hpp"
+#include "asyrk/kaczmarz.hpp"
+#include "asyrk/parallel.hpp"
+#include "asyrk/stats.hpp"
+#include "asyrk/stepsize.hpp"
+#include "asyrk/trace.hpp"
+
+namespace py = pybind11;
+using namespace asyrk;
+
+namespace {
+
+CsrMatrix triplets_to_csr(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                          const std::vector<double>& vals) {
+    if (rows.size() != cols.size() || rows.size() != vals.size())
+        fail(ErrorCode::DimensionMismatch, "triplet lists differ in length");
+    std::vector<Triplet> t(rows.size());
+    for (std::size_t k = 0; k < rows.size(); ++k) t[k] = Triplet{rows[k], cols[k], vals[k]};
+    return CsrMatrix::from_triplets(t, m, n);
+}
+
+py::dict to_dict(const Trace& tr) {
+    std::vector<index_t> ep, upd;
+    std::vector<double> rs, gs, wall, dist;
+    const bool has_dist = !tr.epochs.empty() && tr.epochs.front().dist_sq.has_value();
+    for (const EpochRecord& e : tr.epochs) {
+        ep.push_back(e.epoch_index);
+        rs.push_back(e.r_sq);
+        gs.push_back(e.grad_sq);
+        wall.push_back(e.wall_seconds);
+        upd.push_back(e.updates_applied);
+        if (has_dist && e.dist_sq) dist.push_back(*e.dist_sq);
+    }
+    py::dict d;
+    d["epoch_index"] = ep;
+    d["r_sq"] = rs;
+    d["grad_sq"] = gs;
+    if (has_dist) d["dist_sq"] = dist;
+    d["wall_seconds"] = wall;
+    d["updates_applied"] = upd;
+    d["final_x"] = tr.final_x;
+    d["config"] = tr.config_echo;
+    return d;
+}
+
+Sampling parse_sampling(const std::string& s) {
+    if (s == "uniform") return Sampling::uniform;
+    if (s == "norm" || s == "norm-proportional") return Sampling::norm_proportional;
+    if (s == "shuffle") return Sampling::shuffle;
+    fail(ErrorCode::InvalidArgument, "sampling: expected uniform|norm|shuffle");
+}
+
+UpdateVariant parse_variant(const std::string& s) {
+    if (s == "full-row" || s == "full_row") return UpdateVariant::full_row;
+    if (s == "single" || s == "single_component") return UpdateVariant::single_component;
+    fail(ErrorCode::InvalidArgument, "variant: expected full-row|single");
+}
+
+py::dict solve_rk_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                     const std::vector<double>& vals, const std::vector<double>& b, index_t epochs, double target,
+                     std::uint64_t seed, const std::string& sampling) {
+    CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
+    auto [A, bn] = normalize_rows(A0, b);
+    RkConfig cfg;
+    cfg.max_epochs = epochs;
+    cfg.target_r_sq = target;
+    cfg.seed = seed;
+    cfg.sampling = parse_sampling(sampling);
+    std::vector<double> x0(static_cast<std::size_t>(n), 0.0);
+    Trace tr;
+    {
+        py::gil_scoped_release nogil;
+        tr = rk_solve(A, bn, x0, cfg);
+    }
+    return to_dict(tr);
+}
+
+py::dict solve_parallel_core(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                             const std::vector<double>& vals, const std::vector<double>& b, index_t threads,
+                             double gamma, index_t epochs, double target, std::uint64_t seed,
+                             const std::string& variant, const std::string& sampling, index_t snapshot_interval,
+                             int precision, bool instrumented, const std::vector<double>* x_star) {
+    CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
+    DeviceOptions dev;
+    dev.precision = precision;
+    dev.norm_proportional = sampling == "norm" || sampling == "norm-proportional";
+    // the reference normalizes before every parallel solve (module.cpp:179);
+    // norm-proportional sampling is the device extension for raw rows
+    CsrMatrix A;
+    std::vector<double> bn;
+    if (dev.norm_proportional) {
+        A = std::move(A0);
+        bn = b;
+    } else {
+        auto pr = normalize_rows(A0, b);
+        A = std::move(pr.first);
+        bn = std::move(pr.second);
+    }
+    RunConfig cfg;
+    cfg.threads = threads;
+    cfg.gamma = gamma;
+    cfg.epochs = epochs;
+    cfg.target_r_sq = target;
+    cfg.seed = seed;
+    cfg.variant = parse_variant(variant);
+    cfg.sampling = (sampling == "slice" || sampling == "slice_shuffle") ? ParSampling::slice_shuffle
+                                                                       : ParSampling::with_replacement;
+    cfg.snapshot_interval = snapshot_interval;
+    cfg.x_star = x_star;
+    std::vector<double> x0(static_cast<std::size_t>(n), 0.0);
+    InstrumentReport rep;
+    Trace tr;
+    {
+        py::gil_scoped_release nogil;
+        tr = solve_parallel(A, bn, x0, cfg, instrumented ? &rep : nullptr, dev);
+    }
+    py::dict d = to_dict(tr);
+    if (instrumented)
+        d["instrument"] = py::dict(py::arg("row_updates") = rep.row_updates, py::arg("increments") = rep.increments,
+                                   py::arg("max_abs_error") = rep.max_abs_error, py::arg("tolerance") = rep.tolerance,
+                                   py::arg("consistent") = rep.consistent);
+    return d;
+}
+
+}  // namespace
+
+PYBIND11_MODULE(_asyrk, mod) {
+    mod.doc() = "B200-native AsyRK: sm_100a row-projection solvers behind the reference's signatures.";
+
+    py::register_exception_translator([](std::exception_ptr p) {
+        try {
+            if (p) std::rethrow_exception(p);
+        } catch (const Error& e) {
+            const std::string text = std::string(error_code_name(e.code())) + ": " + e.what();
+            PyErr_SetString(PyExc_ValueError, text.c_str());
+        }
+    });
+
+    mod.def("solve_rk", &solve_rk_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"),
+            py::arg("b"), py::arg("epochs") = 100, py::arg("target") = 0.0, py::arg("seed") = 0,
+            py::arg("sampling") = "uniform",
+            "Serial randomized row-projection solve from x0 = 0 (deterministic device worker, "
+            "bit-identical to the reference).");
+    mod.def(
+        "solve_parallel",
+        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+           const std::vector<double>& vals, const std::vector<double>& b, index_t threads, double gamma,
+           index_t epochs, double target, std::uint64_t seed, const std::string& variant) {
+            // reference: slice_shuffle, snapshot_interval 1, always instrumented (module.cpp:182-191)
+            return solve_parallel_core(m, n, rows, cols, vals, b, threads, gamma, epochs, target, seed, variant,
+                                       "slice", 1, 0, true, nullptr);
+        },
+        py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"), py::arg("b"),
+        py::arg("threads") = 1, py::arg("gamma") = 1.0, py::arg("epochs") = 100, py::arg("target") = 0.0,
+        py::arg("seed") = 0, py::arg("variant") = "full-row",
+        "Lock-free solve with `threads` warp-workers; returns the trace plus an instrument report.");
+    mod.def(
+        "solve_parallel_device",
+        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+           const std::vector<double>& vals, const std::vector<double>& b, index_t threads, double gamma,
+           index_t epochs, double target, std::uint64_t seed, const std::string& variant, const std::string& sampling,
+           index_t snapshot_interval, int precision, bool instrument, std::optional<std::vector<double>> x_star) {
+            return solve_parallel_core(m, n, rows, cols, vals, b, threads, gamma, epochs, target, seed, variant,
+                                       sampling, snapshot_interval, precision, instrument,
+                                       x_star ? &*x_star : nullptr);
+        },
+        py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"), py::arg("b"),
+        py::arg("threads") = 1, py::arg("gamma") = 1.0, py::arg("epochs") = 100, py::arg("target") = 0.0,
+        py::arg("seed") = 0, py::arg("variant") = "full-row", py::arg("sampling") = "slice",
+        py::arg("snapshot_interval") = 1, py::arg("precision") = 0, py::arg("instrument") = false,
+        py::arg("x_star") = py::none(),
+        "solve_parallel with the device options: sampling slice|replacement|norm, precision 0/1/2.");
+    mod.def(
+        "lambda_max",
+        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+           const std::vector<double>& vals, double tol, index_t max_iters) {
+            CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
+            auto [A, ignored] = normalize_rows(A0, {});
+            py::gil_scoped_release nogil;
+            return power_iteration_lambda_max(A, tol, max_iters);
+        },
+        py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"), py::arg("tol") = 1e-9,
+        py::arg("max_iters") = 200000, "lambda_max(A^T A) of the row-normalized matrix (device power iteration).");
+    mod.def(
+        "residuals",
+        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+           const std::vector<double>& vals, const std::vector<double>& b, const std::vector<double>& x) {
+            CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
+            Residuals r = residuals(A, x, b);
+            return py::dict(py::arg("r_sq") = r.r_sq, py::arg("grad_sq") = r.grad_sq);
+        },
+        py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"), py::arg("b"), py::arg("x"),
+        "||Ax-b||^2 and ||A^T(Ax-b)||^2 of the raw (unnormalized) system, reference summation order.");
+    mod.def(
+        "max_feasible_tau", [](index_t m, double lambda_max) { return max_feasible_tau(m, lambda_max); },
+        py::arg("m"), py::arg("lambda_max"), "Largest tau with 2e*lambda_max*(tau+1)/m <= 1.");
+}

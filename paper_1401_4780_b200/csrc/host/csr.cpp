@@ -1,0 +1,220 @@
+// Host side of the drop-in CSR (include/asyrk/csr.hpp): construction and
+// normalization semantics of ref/src/csr.cpp:9-63,103-138, with every
+// numeric pass (multiply, multiply_transpose, residuals) on the device.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+
+#include "asyrk/csr.hpp"
+#include "asyrk_cuda.h"
+
+namespace asyrk {
+
+const char* error_code_name(ErrorCode c) {
+    static const char* const names[] = {
+        "IndexOutOfRange", "DuplicateEntry", "ZeroRow", "ZeroColumn", "NotNormalized",
+        "DimensionMismatch", "PowerIterationDiverged", "NonFinite", "ComponentNotInSupport",
+        "Inconsistent", "TooLarge", "InvalidRho", "MissingStats", "StepTooLarge", "ZeroLambdaMin",
+        "InvalidGamma", "NonPositiveData", "InsufficientData", "NonPositiveSigma", "SigmaUnavailable",
+        "InfeasibleSpec", "ThreadSpawnFailure", "IoError", "InvalidArgument"};
+    const int k = static_cast<int>(c);
+    return (k >= 0 && k < static_cast<int>(sizeof(names) / sizeof(names[0]))) ? names[k] : "Unknown";
+}
+
+void throw_status(int status) {
+    if (status == ASYRK_OK) return;
+    throw Error(static_cast<ErrorCode>(status - 1), asyrk_last_error());
+}
+
+// ---- device cache: one asyrk_system per precision, built on first use
+struct CsrMatrix::DeviceCache {
+    std::mutex mu;
+    std::array<asyrk_system*, 3> sys{nullptr, nullptr, nullptr};
+    ~DeviceCache() {
+        for (auto* s : sys)
+            if (s) asyrk_system_destroy(s);
+    }
+};
+
+CsrMatrix::CsrMatrix(const CsrMatrix& o)
+    : m_(o.m_), n_(o.n_), row_ptr_(o.row_ptr_), col_idx_(o.col_idx_), values_(o.values_),
+      row_norm_(o.row_norm_), normalized_(o.normalized_) {}
+
+CsrMatrix& CsrMatrix::operator=(const CsrMatrix& o) {
+    if (this != &o) {
+        m_ = o.m_;
+        n_ = o.n_;
+        row_ptr_ = o.row_ptr_;
+        col_idx_ = o.col_idx_;
+        values_ = o.values_;
+        row_norm_ = o.row_norm_;
+        normalized_ = o.normalized_;
+        dev_.reset();
+    }
+    return *this;
+}
+
+CsrMatrix::~CsrMatrix() = default;
+
+asyrk_system* CsrMatrix::device(int precision) const {
+    if (precision < 0 || precision > 2) fail(ErrorCode::InvalidArgument, "unknown precision");
+    if (!dev_) dev_ = std::make_shared<DeviceCache>();
+    std::lock_guard<std::mutex> lk(dev_->mu);
+    auto*& s = dev_->sys[static_cast<std::size_t>(precision)];
+    if (!s) {
+        asyrk_csr_view v{m_, n_, nnz(), row_ptr_.data(), col_idx_.data(), values_.data(), row_norm_.data(),
+                         normalized_ ? 1 : 0};
+        throw_status(asyrk_system_create(&v, nullptr, precision, nullptr, &s));
+    }
+    return s;
+}
+
+void CsrMatrix::release_device() const { dev_.reset(); }
+
+void CsrMatrix::compute_norms() {
+    row_norm_.resize(static_cast<std::size_t>(m_));
+    for (index_t i = 0; i < m_; ++i) {
+        const index_t b = row_ptr_[static_cast<std::size_t>(i)], e = row_ptr_[static_cast<std::size_t>(i) + 1];
+        if (e == b) fail(ErrorCode::ZeroRow, "row " + std::to_string(i) + " has no nonzeros");
+        double ss = 0.0;  // storage order, like the reference (csr.cpp:53-61)
+        for (index_t k = b; k < e; ++k) ss += values_[static_cast<std::size_t>(k)] * values_[static_cast<std::size_t>(k)];
+        row_norm_[static_cast<std::size_t>(i)] = std::sqrt(ss);
+    }
+}
+
+CsrMatrix CsrMatrix::from_triplets(std::span<const Triplet> entries, index_t m, index_t n) {
+    if (m < 1 || n < 1) fail(ErrorCode::InvalidArgument, "matrix dimensions must be positive");
+    for (const Triplet& t : entries)
+        if (t.row < 0 || t.row >= m || t.col < 0 || t.col >= n)
+            fail(ErrorCode::IndexOutOfRange, "triplet (" + std::to_string(t.row) + "," + std::to_string(t.col) +
+                                                 ") outside " + std::to_string(m) + "x" + std::to_string(n));
+    // counting sort by row, then sort each row's columns: O(nnz + rows * theta log theta)
+    std::vector<index_t> start(static_cast<std::size_t>(m) + 1, 0);
+    for (const Triplet& t : entries) ++start[static_cast<std::size_t>(t.row) + 1];
+    for (index_t i = 0; i < m; ++i) start[static_cast<std::size_t>(i) + 1] += start[static_cast<std::size_t>(i)];
+    std::vector<std::size_t> order(entries.size());
+    {
+        std::vector<index_t> cur(start.begin(), start.end() - 1);
+        for (std::size_t k = 0; k < entries.size(); ++k)
+            order[static_cast<std::size_t>(cur[static_cast<std::size_t>(entries[k].row)]++)] = k;
+    }
+    CsrMatrix A;
+    A.m_ = m;
+    A.n_ = n;
+    A.row_ptr_.assign(static_cast<std::size_t>(m) + 1, 0);
+    A.col_idx_.reserve(entries.size());
+    A.values_.reserve(entries.size());
+    for (index_t i = 0; i < m; ++i) {
+        auto b = order.begin() + start[static_cast<std::size_t>(i)];
+        auto e = order.begin() + start[static_cast<std::size_t>(i) + 1];
+        std::stable_sort(b, e, [&](std::size_t x, std::size_t y) { return entries[x].col < entries[y].col; });
+        index_t kept = 0;
+        for (auto it = b; it != e; ++it) {
+            if (it != b && entries[*it].col == entries[*(it - 1)].col)
+                fail(ErrorCode::DuplicateEntry, "duplicate entry at (" + std::to_string(i) + "," +
+                                                    std::to_string(entries[*it].col) + ")");
+            if (entries[*it].value != 0.0) {
+                A.col_idx_.push_back(entries[*it].col);
+                A.values_.push_back(entries[*it].value);
+                ++kept;
+            }
+        }
+        A.row_ptr_[static_cast<std::size_t>(i) + 1] = A.row_ptr_[static_cast<std::size_t>(i)] + kept;
+    }
+    A.compute_norms();
+    return A;
+}
+
+CsrMatrix CsrMatrix::from_csr(index_t m, index_t n, std::vector<index_t> row_ptr, std::vector<index_t> col_idx,
+                              std::vector<double> values) {
+    if (m < 1 || n < 1) fail(ErrorCode::InvalidArgument, "matrix dimensions must be positive");
+    if (row_ptr.size() != static_cast<std::size_t>(m) + 1 || row_ptr.front() != 0 ||
+        row_ptr.back() != static_cast<index_t>(col_idx.size()) || col_idx.size() != values.size())
+        fail(ErrorCode::DimensionMismatch, "from_csr: inconsistent arrays");
+    CsrMatrix A;
+    A.m_ = m;
+    A.n_ = n;
+    A.row_ptr_ = std::move(row_ptr);
+    A.col_idx_ = std::move(col_idx);
+    A.values_ = std::move(values);
+    A.compute_norms();
+    return A;
+}
+
+double CsrMatrix::row_dot(index_t i, std::span<const double> x) const {
+    double s = 0.0;
+    for (index_t k = row_ptr_[static_cast<std::size_t>(i)]; k < row_ptr_[static_cast<std::size_t>(i) + 1]; ++k)
+        s += values_[static_cast<std::size_t>(k)] * x[static_cast<std::size_t>(col_idx_[static_cast<std::size_t>(k)])];
+    return s;
+}
+
+void CsrMatrix::multiply(std::span<const double> x, std::vector<double>& y) const {
+    if (static_cast<index_t>(x.size()) != n_) fail(ErrorCode::DimensionMismatch, "multiply: x has wrong length");
+    y.assign(static_cast<std::size_t>(m_), 0.0);
+    throw_status(asyrk_system_multiply(device(0), x.data(), y.data()));
+}
+
+void CsrMatrix::multiply_transpose(std::span<const double> x, std::vector<double>& y) const {
+    if (static_cast<index_t>(x.size()) != m_)
+        fail(ErrorCode::DimensionMismatch, "multiply_transpose: x has wrong length");
+    y.assign(static_cast<std::size_t>(n_), 0.0);
+    throw_status(asyrk_system_multiply_transpose(device(0), x.data(), y.data()));
+}
+
+std::vector<Triplet> CsrMatrix::to_triplets() const {
+    std::vector<Triplet> out;
+    out.reserve(values_.size());
+    for (index_t i = 0; i < m_; ++i)
+        for (index_t k = row_ptr_[static_cast<std::size_t>(i)]; k < row_ptr_[static_cast<std::size_t>(i) + 1]; ++k)
+            out.push_back({i, col_idx_[static_cast<std::size_t>(k)], values_[static_cast<std::size_t>(k)]});
+    return out;
+}
+
+void CsrMatrix::flag_normalized() {
+    for (index_t i = 0; i < m_; ++i)
+        if (std::abs(row_norm_[static_cast<std::size_t>(i)] - 1.0) > kNormTol)
+            fail(ErrorCode::NotNormalized, "row " + std::to_string(i) + " norm " +
+                                               std::to_string(row_norm_[static_cast<std::size_t>(i)]) +
+                                               " not within 1e-12 of 1");
+    normalized_ = true;
+    dev_.reset();
+}
+
+std::pair<CsrMatrix, std::vector<double>> normalize_rows(const CsrMatrix& A, std::span<const double> b) {
+    if (!b.empty() && static_cast<index_t>(b.size()) != A.rows())
+        fail(ErrorCode::DimensionMismatch, "normalize_rows: b has wrong length");
+    CsrMatrix N = A;
+    std::vector<double> nb(b.begin(), b.end());
+    for (index_t i = 0; i < A.rows(); ++i) {
+        const std::size_t si = static_cast<std::size_t>(i);
+        const double nrm = A.row_norm_[si];
+        if (nrm == 0.0) fail(ErrorCode::ZeroRow, "row " + std::to_string(i) + " has zero norm");
+        if (std::abs(nrm - 1.0) <= CsrMatrix::kNormTol) continue;  // unit rows stay bit-identical
+        double ss = 0.0;
+        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k) {
+            double& v = N.values_[static_cast<std::size_t>(k)];
+            v /= nrm;
+        }
+        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k)
+            ss += N.values_[static_cast<std::size_t>(k)] * N.values_[static_cast<std::size_t>(k)];
+        if (!nb.empty()) nb[si] /= nrm;
+        N.row_norm_[si] = std::sqrt(ss);  // recomputed, not assumed 1
+    }
+    N.flag_normalized();
+    return {std::move(N), std::move(nb)};
+}
+
+Residuals residuals(const CsrMatrix& A, std::span<const double> x, std::span<const double> b) {
+    if (static_cast<index_t>(x.size()) != A.cols() || static_cast<index_t>(b.size()) != A.rows())
+        fail(ErrorCode::DimensionMismatch, "residuals: dimension mismatch");
+    asyrk_system* s = A.device(0);
+    throw_status(asyrk_system_set_rhs(s, b.data()));
+    Residuals out;
+    throw_status(asyrk_system_residuals(s, x.data(), &out.r_sq, &out.grad_sq));
+    return out;
+}
+
+}  // namespace asyrk

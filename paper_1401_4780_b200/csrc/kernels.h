@@ -1,0 +1,113 @@
+// Launch wrappers of the sm_100a kernels (host-callable, no CUDA types
+// beyond cudaStream_t). Implemented in worker.cu, det.cu, monitor.cu, pack.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "layout.cuh"
+
+namespace ak {
+
+enum Precision { P_F64 = 0, P_F32 = 1, P_F32X64 = 2 };
+enum Sampling { S_UNIFORM = 0, S_SLICE = 1, S_ALIAS = 2 };
+
+struct AliasEntry {
+    float prob;
+    int32_t alias;
+};
+
+// ---- K2: asynchronous Hogwild worker (one warp = one AsyRK worker)
+struct WorkerArgs {
+    Layout L;
+    void* x;                      // X[n]
+    void* shadow;                 // X[n] or nullptr (instrumented run)
+    const AliasEntry* alias;      // m entries (S_ALIAS)
+    DevState* st;
+    unsigned long long* increments;
+    long long W;                  // worker warps
+    double gamma;
+    uint32_t key0, key1;          // seed
+    int sampling;
+    int full_row;
+};
+int worker_elems_per_lane(uint32_t max_len);  // 1, 2, 4 or 0 (looped)
+void launch_worker(const WorkerArgs& a, int precision, int E, cudaStream_t s);
+int worker_max_resident_warps(int precision, int E, int full_row);
+
+// ---- K1: deterministic single worker consuming a host-generated sequence
+struct DetArgs {
+    Layout L;
+    const double* row_norm;       // reference row norms (coefficient exactness)
+    double* x;
+    double* shadow;               // or nullptr
+    const int32_t* seq;           // rows of this chunk, in order
+    const int32_t* picks;         // single_component picks, or nullptr
+    long long count;              // rows in this chunk (0 = take span*m from st)
+    DevState* st;
+    double gamma;
+    int full_row;
+    int x_in_smem;
+};
+void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
+bool det_fits_smem(long long n);
+
+// ---- K3: residual monitor r = Ax - b, g = A^T r, dist = ||x - x*||^2
+struct CscDev {
+    const long long* col_ptr;     // n+1
+    const int32_t* row;           // nnz
+    const void* val;              // nnz (V)
+};
+struct MonitorArgs {
+    Layout L;
+    CscDev csc;
+    const void* x;                // X[n]
+    const double* x_star;         // or nullptr
+    double* r;                    // m
+    double* g;                    // n
+    double* part;                 // per-block partials [3][nblocks]
+    DevRecord* rec;               // trace records
+    long long rec_cap;
+    DevState* st;
+    int* host_flag;               // mapped pinned: stop seen by the host
+    int exact;                    // 1: reference summation order (bitwise)
+    int advance;                  // 0: initial record, 1: after a chunk
+    long long m_rows;
+};
+void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
+
+// ---- K4: power iteration building blocks (stats.cpp:15-50)
+void launch_spmv_rows(const Layout& L, int precision, const double* v, double* out, cudaStream_t s);
+void launch_spmv_cols(const CscDev& C, int precision, long long n, const double* r, double* out,
+                      cudaStream_t s);
+// dot/norm with a fixed-order tree; result in *out (device)
+void launch_dot(const double* a, const double* b, long long n, double* scratch, double* out, cudaStream_t s);
+void launch_power_update(double* v, const double* w, const double* wn_dot, long long n, cudaStream_t s);
+
+// ---- K0: packing
+void launch_pack_records(const long long* row_ptr, const long long* col, const double* val,
+                         const double* row_norm, const double* b, long long m, const uint2* row_info,
+                         uint32_t stride16, uint32_t uniform_len, int precision, unsigned char* rec,
+                         cudaStream_t s);
+void launch_row_ids(const long long* row_ptr, long long m, int32_t* row_id, cudaStream_t s);
+void launch_gather_csc(const int32_t* perm, const int32_t* row_id, const double* val, long long nnz,
+                       int precision, int32_t* csc_row, void* csc_val, cudaStream_t s);
+void launch_col_hist(const int32_t* sorted_cols, long long nnz, long long n, long long* col_ptr,
+                     cudaStream_t s);
+void launch_x_init(const double* x0, void* x, long long n, int precision, cudaStream_t s);
+void launch_x_export(const void* x, double* out, long long n, int precision, cudaStream_t s);
+void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target,
+                       cudaStream_t s);
+void launch_instrument_check(const void* x, const double* x0, const void* shadow, long long n,
+                             int precision, double* out_max, cudaStream_t s);
+
+}  // namespace ak
+
+namespace ak {
+size_t csc_sort_temp_bytes(long long nnz);
+void csc_sort(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out, const int32_t* vals_in,
+              int32_t* vals_out, long long nnz, int end_bit, cudaStream_t s);
+void launch_iota_cols(const long long* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s);
+int monitor_row_blocks(long long m);
+int monitor_col_blocks(long long n);
+void launch_set_rhs(const Layout& L, const double* b, cudaStream_t s);
+}  // namespace ak

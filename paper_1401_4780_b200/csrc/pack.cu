@@ -1,0 +1,197 @@
+// K0 — CSR upload and device layout packing (replaces the storage of
+// CsrMatrix, ref/include/asyrk/csr.hpp:69-75, as seen by the hot path).
+// The reference's int64 row_ptr/col_idx and fp64 values arrive in HBM as
+// uploaded; these kernels pack them into the row-record layout (layout.cuh)
+// and build the CSC copy the residual monitor reads.
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace ak {
+
+// one warp per row: header {b, 1/nrm^2}, values (converted), int32 columns
+template <class V>
+__global__ void pack_records_kernel(const long long* __restrict__ row_ptr, const long long* __restrict__ col,
+                                    const double* __restrict__ val, const double* __restrict__ row_norm,
+                                    const double* __restrict__ b, long long m, const uint2* __restrict__ row_info,
+                                    uint32_t stride16, unsigned char* __restrict__ rec) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= m) return;
+    const long long k0 = row_ptr[warp], len = row_ptr[warp + 1] - k0;
+    unsigned char* base = rec + (row_info ? (size_t)row_info[warp].x * 16u : (size_t)warp * stride16 * 16u);
+    if (lane == 0) {
+        const double nrm = row_norm[warp];
+        reinterpret_cast<double*>(base)[0] = b ? b[warp] : 0.0;
+        reinterpret_cast<double*>(base)[1] = 1.0 / (nrm * nrm);
+    }
+    V* vals = reinterpret_cast<V*>(base + 16);
+    int32_t* cols = reinterpret_cast<int32_t*>(base + 16 + (size_t)len * sizeof(V));
+    for (long long k = lane; k < len; k += 32) {
+        vals[k] = (V)val[k0 + k];
+        cols[k] = (int32_t)col[k0 + k];
+    }
+    // zero the pad so records are deterministic bytes
+    const size_t used = 16 + (size_t)len * (sizeof(V) + 4);
+    const size_t total = (size_t)rec_size16((uint32_t)len, (int)sizeof(V)) * 16u;
+    for (size_t p = used + lane; p < total; p += 32) base[p] = 0;
+}
+
+void launch_pack_records(const long long* row_ptr, const long long* col, const double* val, const double* row_norm,
+                         const double* b, long long m, const uint2* row_info, uint32_t stride16, uint32_t, int precision,
+                         unsigned char* rec, cudaStream_t s) {
+    const unsigned blocks = (unsigned)((m * 32 + 255) / 256);
+    if (precision == P_F64)
+        pack_records_kernel<double><<<blocks, 256, 0, s>>>(row_ptr, col, val, row_norm, b, m, row_info, stride16, rec);
+    else
+        pack_records_kernel<float><<<blocks, 256, 0, s>>>(row_ptr, col, val, row_norm, b, m, row_info, stride16, rec);
+}
+
+__global__ void row_ids_kernel(const long long* __restrict__ row_ptr, long long m, int32_t* __restrict__ row_id) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= m) return;
+    for (long long k = row_ptr[warp] + lane; k < row_ptr[warp + 1]; k += 32) row_id[k] = (int32_t)warp;
+}
+void launch_row_ids(const long long* row_ptr, long long m, int32_t* row_id, cudaStream_t s) {
+    row_ids_kernel<<<(unsigned)((m * 32 + 255) / 256), 256, 0, s>>>(row_ptr, m, row_id);
+}
+
+template <class V>
+__global__ void gather_csc_kernel(const int32_t* __restrict__ perm, const int32_t* __restrict__ row_id,
+                                  const double* __restrict__ val, long long nnz, int32_t* __restrict__ csc_row,
+                                  V* __restrict__ csc_val) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
+        const int32_t p = perm[e];
+        csc_row[e] = row_id[p];
+        csc_val[e] = (V)val[p];
+    }
+}
+void launch_gather_csc(const int32_t* perm, const int32_t* row_id, const double* val, long long nnz, int precision,
+                       int32_t* csc_row, void* csc_val, cudaStream_t s) {
+    if (nnz == 0) return;
+    const unsigned blocks = (unsigned)std::min<long long>((nnz + 255) / 256, 148 * 32);
+    if (precision == P_F64)
+        gather_csc_kernel<double><<<blocks, 256, 0, s>>>(perm, row_id, val, nnz, csc_row, static_cast<double*>(csc_val));
+    else
+        gather_csc_kernel<float><<<blocks, 256, 0, s>>>(perm, row_id, val, nnz, csc_row, static_cast<float*>(csc_val));
+}
+
+// col_ptr[j] = first position of column j in the column-sorted keys
+__global__ void col_ptr_kernel(const int32_t* __restrict__ sorted_cols, long long nnz, long long n,
+                               long long* __restrict__ col_ptr) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e <= nnz; e += (long long)gridDim.x * blockDim.x) {
+        const long long cur = e < nnz ? sorted_cols[e] : n;
+        const long long prev = e > 0 ? sorted_cols[e - 1] : -1;
+        for (long long j = prev + 1; j <= cur; ++j) col_ptr[j] = e;
+    }
+}
+void launch_col_hist(const int32_t* sorted_cols, long long nnz, long long n, long long* col_ptr, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((nnz + 256) / 256, 148 * 32);
+    col_ptr_kernel<<<blocks, 256, 0, s>>>(sorted_cols, nnz, n, col_ptr);
+}
+
+template <class X>
+__global__ void x_init_kernel(const double* __restrict__ x0, X* __restrict__ x, long long n) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        x[k] = x0 ? (X)x0[k] : X(0);
+}
+template <class X>
+__global__ void x_export_kernel(const X* __restrict__ x, double* __restrict__ out, long long n) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        out[k] = (double)x[k];
+}
+void launch_x_init(const double* x0, void* x, long long n, int precision, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+    if (precision == P_F32)
+        x_init_kernel<float><<<blocks, 256, 0, s>>>(x0, static_cast<float*>(x), n);
+    else
+        x_init_kernel<double><<<blocks, 256, 0, s>>>(x0, static_cast<double*>(x), n);
+}
+void launch_x_export(const void* x, double* out, long long n, int precision, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+    if (precision == P_F32)
+        x_export_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x), out, n);
+    else
+        x_export_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), out, n);
+}
+
+__global__ void state_init_kernel(DevState* st, long long epochs_cap, long long interval, double target) {
+    st->epoch = 0;
+    st->updates = 0;
+    st->nrec = 0;
+    st->epochs_cap = epochs_cap;
+    st->interval = interval;
+    st->target = target;
+    st->stop = 0;
+    st->status = 0;
+    st->increments = 0;
+    st->t0_ns = globaltimer_ns();
+}
+void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
+    state_init_kernel<<<1, 1, 0, s>>>(st, epochs_cap, interval, target);
+}
+
+// max_t |x_t - x0_t - shadow_t|  (finish_instrument, parallel.cpp:94-106)
+template <class X>
+__global__ void instrument_check_kernel(const X* __restrict__ x, const double* __restrict__ x0,
+                                        const X* __restrict__ shadow, long long n, unsigned long long* out) {
+    double mx = 0.0;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const double d = fabs((double)x[k] - x0[k] - (double)shadow[k]);
+        mx = d > mx ? d : mx;
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(FULL, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, __double_as_longlong(mx));
+}
+void launch_instrument_check(const void* x, const double* x0, const void* shadow, long long n, int precision,
+                             double* out_max, cudaStream_t s) {
+    cudaMemsetAsync(out_max, 0, sizeof(double), s);
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+    auto* o = reinterpret_cast<unsigned long long*>(out_max);
+    if (precision == P_F32)
+        instrument_check_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x), x0,
+                                                              static_cast<const float*>(shadow), n, o);
+    else
+        instrument_check_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), x0,
+                                                               static_cast<const double*>(shadow), n, o);
+}
+
+// CUB radix sort wrapper: stable sort of (col, nnz-index) pairs by column, so
+// each column lists its rows ascending (the order multiply_transpose adds in).
+size_t csc_sort_temp_bytes(long long nnz) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, (int)nnz);
+    return bytes;
+}
+void csc_sort(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out, const int32_t* vals_in,
+              int32_t* vals_out, long long nnz, int end_bit, cudaStream_t s) {
+    cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)nnz, 0, end_bit, s);
+}
+
+__global__ void iota_cols_kernel(const long long* __restrict__ col, long long nnz, int32_t* __restrict__ keys,
+                                 int32_t* __restrict__ idx) {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
+        keys[e] = (int32_t)col[e];
+        idx[e] = (int32_t)e;
+    }
+}
+void launch_iota_cols(const long long* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s) {
+    if (nnz == 0) return;
+    const unsigned blocks = (unsigned)std::min<long long>((nnz + 255) / 256, 148 * 32);
+    iota_cols_kernel<<<blocks, 256, 0, s>>>(col, nnz, keys, idx);
+}
+
+__global__ void set_rhs_kernel(Layout L, const double* __restrict__ b) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L.m; i += (long long)gridDim.x * blockDim.x) {
+        const RowRef r = row_ref(L, i);
+        *reinterpret_cast<double*>(const_cast<unsigned char*>(r.base)) = b[i];
+    }
+}
+void launch_set_rhs(const Layout& L, const double* b, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((L.m + 255) / 256, 148 * 8);
+    set_rhs_kernel<<<blocks, 256, 0, s>>>(L, b);
+}
+
+}  // namespace ak

@@ -1,0 +1,915 @@
+// The C ABI (include/asyrk_cuda.h): device-resident systems, the solve
+// driver (the reference's coordinator, ref/src/parallel.cpp:220-445, moved
+// onto the stream) and the one-shot host-buffer entry points.
+//
+// Solve driver. One "chunk" = span = min(snapshot_interval, epochs - e)
+// epochs of row events followed by the residual monitor and a finalize
+// kernel that writes the trace record and decides stop/NonFinite on the
+// device (DevState). The host only enqueues chunks ahead (bounded lookahead)
+// and polls a mapped pinned flag; chunks enqueued after the stop decision
+// exit at their first instruction. No host round trip sits between epochs.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/asyrk_cuda.h"
+#include "host_seq.h"
+#include "kernels.h"
+
+using namespace ak;
+
+namespace {
+
+thread_local std::string g_err;
+
+asyrk_status fail(asyrk_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+struct CudaFail {
+    asyrk_status st;
+};
+
+#define CK(call)                                                                                       \
+    do {                                                                                               \
+        cudaError_t e_ = (call);                                                                       \
+        if (e_ != cudaSuccess) {                                                                       \
+            g_err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;                     \
+            throw CudaFail{e_ == cudaErrorMemoryAllocation ? ASYRK_E_TooLarge : ASYRK_E_ThreadSpawnFailure}; \
+        }                                                                                              \
+    } while (0)
+
+template <class F>
+asyrk_status guarded(F&& f) {
+    try {
+        return f();
+    } catch (const CudaFail& c) {
+        return c.st;
+    } catch (const std::bad_alloc&) {
+        return fail(ASYRK_E_TooLarge, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(ASYRK_E_InvalidArgument, e.what());
+    }
+}
+
+template <class T>
+T* dalloc(size_t count) {
+    void* p = nullptr;
+    if (count == 0) count = 1;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+constexpr int kLookahead = 4;      // chunks in flight beyond the last confirmed one
+constexpr int kTimedLaunches = 1024;  // worker launches timed with event pairs per solve
+
+}  // namespace
+
+struct asyrk_system {
+    int64_t m = 0, n = 0, nnz = 0;
+    int precision = 0;
+    bool normalized = false;
+    bool uniform = true;
+    uint32_t max_len = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+
+    // layout
+    unsigned char* rec = nullptr;
+    uint2* row_info = nullptr;
+    uint32_t stride16 = 0, uniform_len = 0;
+    double* row_norm = nullptr;
+    long long* col_ptr = nullptr;
+    int32_t* csc_row = nullptr;
+    void* csc_val = nullptr;
+    AliasEntry* alias = nullptr;  // device alias table (async norm_proportional), built lazily
+
+    // host copies for sequence generation
+    std::vector<int32_t> h_len;
+    std::vector<double> h_norm;
+    std::unique_ptr<HostAlias> h_alias;
+
+    // solve state
+    void* x = nullptr;        // X[n]
+    double* xd = nullptr;     // fp64 staging (x0, export, det x)
+    void* shadow = nullptr;
+    double* x0d = nullptr;
+    double* xstar = nullptr;
+    double* r = nullptr;
+    double* g = nullptr;
+    double* part = nullptr;
+    DevRecord* recs = nullptr;
+    long long rec_cap = 0;
+    DevState* st = nullptr;
+    unsigned long long* incr = nullptr;
+    double* scratch = nullptr;
+    int* host_flag = nullptr;      // pinned mapped
+    int* host_flag_dev = nullptr;
+
+    // det staging ring
+    int32_t* seq_dev[kLookahead + 1] = {};
+    int32_t* pick_dev[kLookahead + 1] = {};
+    int32_t* seq_host[kLookahead + 1] = {};
+    int32_t* pick_host[kLookahead + 1] = {};
+    size_t seq_cap = 0;
+
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    std::vector<cudaEvent_t> ev_w;   // 2 per timed worker launch
+    std::vector<cudaEvent_t> ev_chunk;
+    asyrk_solve_stats stats{};
+
+    Layout layout() const {
+        Layout L;
+        L.rec = rec;
+        L.row_info = uniform ? nullptr : row_info;
+        L.stride16 = stride16;
+        L.uniform_len = uniform_len;
+        L.m = m;
+        L.n = n;
+        return L;
+    }
+    CscDev csc() const { return CscDev{col_ptr, csc_row, csc_val}; }
+    size_t xbytes() const { return precision == P_F32 ? 4 : 8; }
+};
+
+namespace {
+
+void free_all(asyrk_system* s) {
+    auto F = [](void* p) {
+        if (p) cudaFree(p);
+    };
+    F(s->rec);
+    F(s->row_info);
+    F(s->row_norm);
+    F(s->col_ptr);
+    F(s->csc_row);
+    F(s->csc_val);
+    F(s->alias);
+    F(s->x);
+    F(s->xd);
+    F(s->shadow);
+    F(s->x0d);
+    F(s->xstar);
+    F(s->r);
+    F(s->g);
+    F(s->part);
+    F(s->recs);
+    F(s->st);
+    F(s->incr);
+    F(s->scratch);
+    if (s->host_flag) cudaFreeHost(s->host_flag);
+    for (int k = 0; k <= kLookahead; ++k) {
+        F(s->seq_dev[k]);
+        F(s->pick_dev[k]);
+        if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
+        if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
+    }
+    if (s->ev_begin) cudaEventDestroy(s->ev_begin);
+    if (s->ev_end) cudaEventDestroy(s->ev_end);
+    for (auto e : s->ev_w) cudaEventDestroy(e);
+    for (auto e : s->ev_chunk) cudaEventDestroy(e);
+    if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
+}
+
+asyrk_status check_view(const asyrk_csr_view* A) {
+    if (!A || !A->row_ptr || !A->col_idx || !A->values || !A->row_norm)
+        return fail(ASYRK_E_InvalidArgument, "csr view has null arrays");
+    if (A->m < 1 || A->n < 1) return fail(ASYRK_E_InvalidArgument, "matrix dimensions must be positive");
+    if (A->row_ptr[0] != 0 || A->row_ptr[A->m] != A->nnz)
+        return fail(ASYRK_E_DimensionMismatch, "row_ptr does not span nnz");
+    if (A->m >= (int64_t)INT32_MAX || A->n >= (int64_t)INT32_MAX || A->nnz >= (int64_t)INT32_MAX)
+        return fail(ASYRK_E_TooLarge, "m, n and nnz must each be < 2^31 on the device layout");
+    return ASYRK_OK;
+}
+
+// Bind the per-solve buffers that depend on cap (records) lazily.
+void ensure_records(asyrk_system* s, long long cap) {
+    if (cap <= s->rec_cap) return;
+    if (s->recs) cudaFree(s->recs);
+    s->recs = dalloc<DevRecord>((size_t)cap);
+    s->rec_cap = cap;
+}
+
+void ensure_seq(asyrk_system* s, size_t count) {
+    if (count <= s->seq_cap) return;
+    for (int k = 0; k <= kLookahead; ++k) {
+        if (s->seq_dev[k]) cudaFree(s->seq_dev[k]);
+        if (s->pick_dev[k]) cudaFree(s->pick_dev[k]);
+        if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
+        if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
+        s->seq_dev[k] = dalloc<int32_t>(count);
+        s->pick_dev[k] = dalloc<int32_t>(count);
+        CK(cudaHostAlloc((void**)&s->seq_host[k], count * 4, cudaHostAllocDefault));
+        CK(cudaHostAlloc((void**)&s->pick_host[k], count * 4, cudaHostAllocDefault));
+    }
+    s->seq_cap = count;
+}
+
+void ensure_events(asyrk_system* s) {
+    if (!s->ev_begin) {
+        CK(cudaEventCreate(&s->ev_begin));
+        CK(cudaEventCreate(&s->ev_end));
+    }
+    if (s->ev_w.empty()) {
+        s->ev_w.resize(2 * kTimedLaunches);
+        for (auto& e : s->ev_w) CK(cudaEventCreate(&e));
+        s->ev_chunk.resize(kLookahead + 1);
+        for (auto& e : s->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+}
+
+void ensure_alias_dev(asyrk_system* s) {
+    if (s->alias) return;
+    if (!s->h_alias) {
+        std::vector<double> w(s->h_norm.size());
+        for (size_t i = 0; i < w.size(); ++i) w[i] = s->h_norm[i] * s->h_norm[i];
+        s->h_alias = std::make_unique<HostAlias>();
+        if (!s->h_alias->build(w)) throw CudaFail{fail(ASYRK_E_InvalidArgument, "alias weights invalid")};
+    }
+    std::vector<AliasEntry> t(s->h_alias->prob.size());
+    for (size_t i = 0; i < t.size(); ++i) t[i] = AliasEntry{(float)s->h_alias->prob[i], s->h_alias->alias[i]};
+    s->alias = dalloc<AliasEntry>(t.size());
+    CK(cudaMemcpyAsync(s->alias, t.data(), t.size() * sizeof(AliasEntry), cudaMemcpyHostToDevice, s->stream));
+    CK(cudaStreamSynchronize(s->stream));
+}
+
+asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t precision, void* stream,
+                         asyrk_system** out) {
+    asyrk_status v = check_view(A);
+    if (v) return v;
+    if (precision < 0 || precision > 2) return fail(ASYRK_E_InvalidArgument, "unknown precision");
+    auto s = std::make_unique<asyrk_system>();
+    s->m = A->m;
+    s->n = A->n;
+    s->nnz = A->nnz;
+    s->precision = precision;
+    s->normalized = A->normalized != 0;
+    if (stream) {
+        s->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+        s->own_stream = true;
+    }
+    const int vbytes = precision == P_F64 ? 8 : 4;
+    // row lengths, layout
+    s->h_len.resize((size_t)A->m);
+    s->h_norm.assign(A->row_norm, A->row_norm + A->m);
+    uint32_t maxl = 0, minl = UINT32_MAX;
+    for (int64_t i = 0; i < A->m; ++i) {
+        const int64_t l = A->row_ptr[i + 1] - A->row_ptr[i];
+        if (l <= 0) {
+            free_all(s.get());
+            return fail(ASYRK_E_ZeroRow, "row " + std::to_string(i) + " has no nonzeros");
+        }
+        s->h_len[(size_t)i] = (int32_t)l;
+        maxl = std::max<uint32_t>(maxl, (uint32_t)l);
+        minl = std::min<uint32_t>(minl, (uint32_t)l);
+    }
+    s->max_len = maxl;
+    s->uniform = maxl == minl;
+    size_t rec_bytes;
+    std::vector<uint2> info;
+    if (s->uniform) {
+        s->uniform_len = maxl;
+        s->stride16 = rec_size16(maxl, vbytes);
+        rec_bytes = (size_t)A->m * s->stride16 * 16u;
+    } else {
+        info.resize((size_t)A->m);
+        uint64_t off = 0;
+        for (int64_t i = 0; i < A->m; ++i) {
+            info[(size_t)i] = make_uint2((uint32_t)off, (uint32_t)s->h_len[(size_t)i]);
+            off += rec_size16((uint32_t)s->h_len[(size_t)i], vbytes);
+            if (off >= (1ull << 32)) {
+                free_all(s.get());
+                return fail(ASYRK_E_TooLarge, "row records exceed 64 GiB");
+            }
+        }
+        rec_bytes = (size_t)off * 16u;
+    }
+    cudaStream_t st = s->stream;
+    s->rec = dalloc<unsigned char>(rec_bytes);
+    if (!s->uniform) {
+        s->row_info = dalloc<uint2>(info.size());
+        CK(cudaMemcpyAsync(s->row_info, info.data(), info.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    }
+    // raw upload (the reference's int64/fp64 arrays), then pack on the device
+    long long* d_rp = dalloc<long long>((size_t)A->m + 1);
+    long long* d_col = dalloc<long long>((size_t)A->nnz);
+    double* d_val = dalloc<double>((size_t)A->nnz);
+    double* d_b = dalloc<double>((size_t)A->m);
+    s->row_norm = dalloc<double>((size_t)A->m);
+    CK(cudaMemcpyAsync(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_col, A->col_idx, (size_t)A->nnz * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_val, A->values, (size_t)A->nnz * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s->row_norm, A->row_norm, (size_t)A->m * 8, cudaMemcpyHostToDevice, st));
+    if (b) CK(cudaMemcpyAsync(d_b, b, (size_t)A->m * 8, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemsetAsync(d_b, 0, (size_t)A->m * 8, st));
+    launch_pack_records(d_rp, d_col, d_val, s->row_norm, d_b, A->m, s->uniform ? nullptr : s->row_info, s->stride16,
+                        s->uniform_len, precision, s->rec, st);
+    CK(cudaGetLastError());
+    // CSC (stable by column => rows ascending within each column)
+    int32_t* keys = dalloc<int32_t>((size_t)A->nnz);
+    int32_t* idx = dalloc<int32_t>((size_t)A->nnz);
+    int32_t* keys_s = dalloc<int32_t>((size_t)A->nnz);
+    int32_t* idx_s = dalloc<int32_t>((size_t)A->nnz);
+    int32_t* row_id = dalloc<int32_t>((size_t)A->nnz);
+    launch_iota_cols(d_col, A->nnz, keys, idx, st);
+    launch_row_ids(d_rp, A->m, row_id, st);
+    int end_bit = 1;
+    while ((1ll << end_bit) < A->n) ++end_bit;
+    const size_t tb = csc_sort_temp_bytes(A->nnz);
+    unsigned char* temp = dalloc<unsigned char>(tb);
+    csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, st);
+    s->col_ptr = dalloc<long long>((size_t)A->n + 1);
+    s->csc_row = dalloc<int32_t>((size_t)A->nnz);
+    s->csc_val = dalloc<unsigned char>((size_t)A->nnz * vbytes);
+    launch_gather_csc(idx_s, row_id, d_val, A->nnz, precision, s->csc_row, s->csc_val, st);
+    launch_col_hist(keys_s, A->nnz, A->n, s->col_ptr, st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
+                    (void*)idx_s, (void*)row_id, (void*)temp})
+        cudaFree(p);
+
+    // solve buffers
+    s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
+    s->xd = dalloc<double>((size_t)A->n);
+    s->x0d = dalloc<double>((size_t)A->n);
+    s->r = dalloc<double>((size_t)A->m);
+    s->g = dalloc<double>((size_t)A->n);
+    s->part = dalloc<double>((size_t)monitor_row_blocks(A->m) + 2 * (size_t)monitor_col_blocks(A->n) + 8);
+    s->st = dalloc<DevState>(1);
+    s->incr = dalloc<unsigned long long>(1);
+    s->scratch = dalloc<double>(4096);
+    CK(cudaHostAlloc((void**)&s->host_flag, sizeof(int), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&s->host_flag_dev, s->host_flag, 0));
+    ensure_records(s.get(), 256);
+    ensure_events(s.get());
+    *out = s.release();
+    return ASYRK_OK;
+}
+
+void write_trace(asyrk_system* s, const DevState& hs, asyrk_trace_out* trace, int precision) {
+    if (!trace) return;
+    const long long k = std::min<long long>(hs.nrec, s->rec_cap);
+    std::vector<DevRecord> recs((size_t)k);
+    if (k) CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
+    trace->count = hs.nrec;
+    const long long w = std::min<long long>(k, trace->cap);
+    for (long long i = 0; i < w; ++i) {
+        const DevRecord& r = recs[(size_t)i];
+        if (trace->epoch_index) trace->epoch_index[i] = r.epoch;
+        if (trace->r_sq) trace->r_sq[i] = r.r_sq;
+        if (trace->grad_sq) trace->grad_sq[i] = r.grad_sq;
+        if (trace->dist_sq) trace->dist_sq[i] = r.dist_sq;
+        if (trace->wall_seconds) trace->wall_seconds[i] = 1e-9 * (double)r.t_ns;
+        if (trace->updates_applied) trace->updates_applied[i] = r.updates;
+    }
+    if (trace->final_x) {
+        launch_x_export(s->x, s->xd, s->n, precision, s->stream);
+        CK(cudaMemcpyAsync(trace->final_x, s->xd, (size_t)s->n * 8, cudaMemcpyDeviceToHost, s->stream));
+        CK(cudaStreamSynchronize(s->stream));
+    }
+}
+
+MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xstar) {
+    MonitorArgs a{};
+    a.L = s->layout();
+    a.csc = s->csc();
+    a.x = s->x;
+    a.x_star = with_xstar ? s->xstar : nullptr;
+    a.r = s->r;
+    a.g = s->g;
+    a.part = s->part;
+    a.rec = s->recs;
+    a.rec_cap = s->rec_cap;
+    a.st = s->st;
+    a.host_flag = s->host_flag_dev;
+    a.exact = exact ? 1 : 0;
+    a.advance = advance;
+    a.m_rows = s->m;
+    return a;
+}
+
+struct SolveSpec {
+    int64_t threads;
+    double gamma;
+    int64_t epochs;
+    double target;
+    bool full_row;
+    int sampling;           // ASYRK_WITH_REPLACEMENT / SLICE / NORM_PROP
+    uint64_t seed;
+    int64_t interval;
+    const double* x_star;
+    int precision;
+    bool det;               // deterministic sequence path
+    int det_mode;           // SeqGen mode
+};
+
+asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
+                       asyrk_instrument_out* instr) {
+    cudaStream_t st = s->stream;
+    const int prec = sp.det ? P_F64 : sp.precision;
+    if (sp.det && s->precision != P_F64)
+        return fail(ASYRK_E_InvalidArgument, "the deterministic path needs an fp64 system");
+    if (!sp.det && sp.precision != s->precision)
+        return fail(ASYRK_E_InvalidArgument, "config precision differs from the system's");
+    const long long max_chunks = sp.epochs > 0 ? (sp.epochs + sp.interval - 1) / sp.interval : 0;
+    ensure_records(s, std::max<long long>(256, max_chunks + 2));
+    ensure_events(s);
+    s->stats = asyrk_solve_stats{};
+
+    // x0, x_star
+    if (x0) CK(cudaMemcpyAsync(s->x0d, x0, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemsetAsync(s->x0d, 0, (size_t)s->n * 8, st));
+    launch_x_init(s->x0d, s->x, s->n, prec, st);
+    if (sp.x_star) {
+        if (!s->xstar) s->xstar = dalloc<double>((size_t)s->n);
+        CK(cudaMemcpyAsync(s->xstar, sp.x_star, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
+    }
+    if (instr) {
+        if (!s->shadow) s->shadow = dalloc<unsigned char>((size_t)s->n * 8);
+        CK(cudaMemsetAsync(s->shadow, 0, (size_t)s->n * 8, st));
+        CK(cudaMemsetAsync(s->incr, 0, sizeof(unsigned long long), st));
+    }
+    *s->host_flag = 0;
+
+    CK(cudaEventRecord(s->ev_begin, st));
+    launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st);
+    long long launches = 1;
+    launch_monitor(monitor_args(s, sp.det, 0, sp.x_star != nullptr), prec, st);
+    launches += 3;
+    s->stats.monitor_launches++;
+
+    // worker setup
+    WorkerArgs wa{};
+    DetArgs da{};
+    int E = 0;
+    std::unique_ptr<SeqGen> gen;
+    std::vector<unsigned long long> chunk_incr;
+    if (sp.det) {
+        const bool picks = !sp.full_row;
+        if (sp.det_mode == 1 && !s->h_alias) {
+            std::vector<double> w(s->h_norm.size());
+            for (size_t i = 0; i < w.size(); ++i) w[i] = s->h_norm[i] * s->h_norm[i];
+            s->h_alias = std::make_unique<HostAlias>();
+            if (!s->h_alias->build(w)) {
+                s->h_alias.reset();
+                return fail(ASYRK_E_InvalidArgument, "alias weights invalid");
+            }
+        }
+        gen = std::make_unique<SeqGen>(sp.seed, sp.det_mode, s->m, &s->h_len, s->h_alias.get(), picks);
+        ensure_seq(s, (size_t)(std::min<int64_t>(sp.interval, std::max<int64_t>(sp.epochs, 1)) * s->m));
+        da.L = s->layout();
+        da.row_norm = s->row_norm;
+        da.x = static_cast<double*>(s->x);
+        da.shadow = instr ? static_cast<double*>(s->shadow) : nullptr;
+        da.st = s->st;
+        da.gamma = sp.gamma;
+        da.full_row = sp.full_row ? 1 : 0;
+        da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
+        s->stats.warps = 1;
+        s->stats.resident_warps = 1;
+    } else {
+        if (sp.sampling == ASYRK_NORM_PROPORTIONAL) ensure_alias_dev(s);
+        E = worker_elems_per_lane(s->max_len);
+        wa.L = s->layout();
+        wa.x = s->x;
+        wa.shadow = instr ? s->shadow : nullptr;
+        wa.alias = s->alias;
+        wa.st = s->st;
+        wa.increments = instr ? s->incr : nullptr;
+        wa.W = sp.threads;
+        wa.gamma = sp.gamma;
+        const uint64_t k = splitmix64(sp.seed ^ 0xA5A5A5A5DEADBEEFull);
+        wa.key0 = (uint32_t)k;
+        wa.key1 = (uint32_t)(k >> 32);
+        wa.sampling = sp.sampling == ASYRK_SLICE_SHUFFLE ? S_SLICE
+                      : sp.sampling == ASYRK_NORM_PROPORTIONAL ? S_ALIAS
+                                                                : S_UNIFORM;
+        wa.full_row = sp.full_row ? 1 : 0;
+        s->stats.warps = (int32_t)std::min<int64_t>(sp.threads, INT32_MAX);
+        s->stats.resident_warps =
+            (int32_t)std::min<int64_t>(sp.threads, worker_max_resident_warps(prec, E, wa.full_row));
+    }
+    CK(cudaGetLastError());
+
+    long long timed = 0;
+    long long k = 0;
+    for (; k < max_chunks; ++k) {
+        if (k >= kLookahead) {
+            CK(cudaEventSynchronize(s->ev_chunk[(size_t)(k % (kLookahead + 1))]));
+            if (*reinterpret_cast<volatile int*>(s->host_flag)) break;
+        }
+        const bool time_it = timed < kTimedLaunches;
+        if (sp.det) {
+            const long long e0 = k * sp.interval;
+            const long long span = std::min<long long>(sp.interval, sp.epochs - e0);
+            const int slot = (int)(k % (kLookahead + 1));
+            // slot reuse: the copy of chunk k-(L+1) completed before chunk k-L's event (synced above)
+            unsigned long long inc = 0;
+            for (long long e = 0; e < span; ++e) {
+                int32_t* sq = s->seq_host[slot] + e * s->m;
+                int32_t* pk = s->pick_host[slot] + e * s->m;
+                gen->epoch(sq, pk);
+                if (instr) {
+                    if (sp.full_row)
+                        for (int64_t q = 0; q < s->m; ++q) inc += (unsigned long long)s->h_len[(size_t)sq[q]];
+                    else
+                        inc += (unsigned long long)s->m;
+                }
+            }
+            chunk_incr.push_back(inc);
+            const size_t cnt = (size_t)(span * s->m);
+            CK(cudaMemcpyAsync(s->seq_dev[slot], s->seq_host[slot], cnt * 4, cudaMemcpyHostToDevice, st));
+            if (!sp.full_row)
+                CK(cudaMemcpyAsync(s->pick_dev[slot], s->pick_host[slot], cnt * 4, cudaMemcpyHostToDevice, st));
+            da.seq = s->seq_dev[slot];
+            da.picks = s->pick_dev[slot];
+            da.count = (long long)cnt;
+            if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
+            launch_det(da, 0, st);
+        } else {
+            if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
+            launch_worker(wa, prec, E, st);
+        }
+        if (time_it) {
+            CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed + 1)], st));
+            ++timed;
+        }
+        launches += 1;
+        s->stats.worker_launches++;
+        launch_monitor(monitor_args(s, sp.det, 1, sp.x_star != nullptr), prec, st);
+        launches += 3;
+        s->stats.monitor_launches++;
+        CK(cudaEventRecord(s->ev_chunk[(size_t)(k % (kLookahead + 1))], st));
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(s->ev_end, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+
+    DevState hs;
+    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+    s->stats.solve_ms = ms;
+    double wms = 0.0;
+    for (long long t = 0; t < timed; ++t) {
+        float w = 0.f;
+        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+        wms += w;
+    }
+    s->stats.worker_ms = wms;
+    s->stats.kernel_launches = launches;
+    s->stats.projections = hs.updates;
+    if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
+
+    write_trace(s, hs, trace, prec);
+    if (instr) {
+        instr->row_updates = hs.updates;
+        unsigned long long inc = 0;
+        if (sp.det) {
+            const long long done = sp.interval > 0 ? (hs.epoch + sp.interval - 1) / sp.interval : 0;
+            for (long long c = 0; c < done && c < (long long)chunk_incr.size(); ++c) inc += chunk_incr[(size_t)c];
+        } else {
+            CK(cudaMemcpy(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost));
+        }
+        instr->increments = (int64_t)inc;
+        launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
+        double mx = 0.0;
+        CK(cudaMemcpyAsync(&mx, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        instr->max_abs_error = mx;
+        instr->tolerance = 1e-9 * (double)std::max<int64_t>(instr->increments, 1);
+        instr->consistent = mx <= instr->tolerance ? 1 : 0;
+    }
+    return ASYRK_OK;
+}
+
+// validate_config, ref/src/parallel.cpp:56-80 (+ device extensions)
+asyrk_status validate_run(const asyrk_system* s, const asyrk_run_config* c) {
+    if (!c) return fail(ASYRK_E_InvalidArgument, "null config");
+    const bool raw_ok = c->allow_unnormalized || c->sampling == ASYRK_NORM_PROPORTIONAL;
+    if (!s->normalized && !raw_ok) return fail(ASYRK_E_NotNormalized, "solve_parallel requires normalized rows");
+    if (c->threads < 1) return fail(ASYRK_E_InvalidArgument, "threads must be >= 1");
+    if (!(c->gamma > 0.0)) return fail(ASYRK_E_InvalidGamma, "gamma must be positive");
+    if (c->epochs < 0 || c->snapshot_interval < 1)
+        return fail(ASYRK_E_InvalidArgument, "epochs must be >= 0 and snapshot_interval >= 1");
+    if (c->sampling == ASYRK_SLICE_SHUFFLE && s->m < c->threads)
+        return fail(ASYRK_E_InvalidArgument, "slice_shuffle needs at least one row per worker");
+    if (c->sampling < 0 || c->sampling > 2) return fail(ASYRK_E_InvalidArgument, "unknown sampling");
+    if (c->variant != ASYRK_FULL_ROW && c->variant != ASYRK_SINGLE_COMPONENT)
+        return fail(ASYRK_E_InvalidArgument, "unknown variant");
+    return ASYRK_OK;
+}
+
+asyrk_status system_solve_impl(asyrk_system* s, const double* x0, const asyrk_run_config* c,
+                               asyrk_trace_out* trace, asyrk_instrument_out* instr) {
+    asyrk_status v = validate_run(s, c);
+    if (v) return v;
+    SolveSpec sp{};
+    sp.threads = c->threads;
+    sp.gamma = c->gamma;
+    sp.epochs = c->epochs;
+    sp.target = c->target_r_sq;
+    sp.full_row = c->variant == ASYRK_FULL_ROW;
+    sp.sampling = c->sampling;
+    sp.seed = c->seed;
+    sp.interval = c->snapshot_interval;
+    sp.x_star = c->x_star;
+    sp.precision = c->precision;
+    sp.det = c->threads == 1;
+    sp.det_mode = c->sampling == ASYRK_SLICE_SHUFFLE ? 2 : (c->sampling == ASYRK_NORM_PROPORTIONAL ? 1 : 0);
+    return run_solve(s, x0, sp, trace, instr);
+}
+
+asyrk_status system_rk_impl(asyrk_system* s, const double* x0, const asyrk_rk_config* c, asyrk_trace_out* trace) {
+    if (!c) return fail(ASYRK_E_InvalidArgument, "null config");
+    if (c->sampling == ASYRK_RK_UNIFORM && !s->normalized)
+        return fail(ASYRK_E_NotNormalized,
+                    "uniform row sampling is only unbiased on normalized rows; use norm_proportional or normalize first");
+    if (c->max_epochs < 0) return fail(ASYRK_E_InvalidArgument, "max_epochs must be >= 0");
+    if (c->sampling < 0 || c->sampling > 2) return fail(ASYRK_E_InvalidArgument, "unknown sampling");
+    SolveSpec sp{};
+    sp.threads = 1;
+    sp.gamma = 1.0;
+    sp.epochs = c->max_epochs;
+    sp.target = c->target_r_sq;
+    sp.full_row = true;
+    sp.seed = c->seed;
+    sp.interval = 1;
+    sp.x_star = c->x_star;
+    sp.precision = P_F64;
+    sp.det = true;
+    sp.det_mode = c->sampling == ASYRK_RK_UNIFORM ? 0 : (c->sampling == ASYRK_RK_NORM_PROPORTIONAL ? 1 : 2);
+    return run_solve(s, x0, sp, trace, nullptr);
+}
+
+asyrk_status residuals_impl(asyrk_system* s, const double* x, double* r_sq, double* grad_sq) {
+    cudaStream_t st = s->stream;
+    CK(cudaMemcpyAsync(s->x0d, x, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
+    launch_x_init(s->x0d, s->x, s->n, s->precision, st);
+    launch_state_init(s->st, 0, 1, -1.0, st);
+    MonitorArgs a = monitor_args(s, s->precision == P_F64, 0, false);
+    a.host_flag = nullptr;
+    launch_monitor(a, s->precision, st);
+    CK(cudaGetLastError());
+    DevRecord rec;
+    DevState hs;
+    CK(cudaMemcpyAsync(&rec, s->recs, sizeof(rec), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hs, s->st, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hs.status) {
+        *r_sq = NAN;
+        *grad_sq = NAN;
+        return ASYRK_OK;
+    }
+    *r_sq = rec.r_sq;
+    *grad_sq = rec.grad_sq;
+    return ASYRK_OK;
+}
+
+// power_iteration_lambda_max, ref/src/stats.cpp:15-50
+asyrk_status power_impl(asyrk_system* s, double tol, int64_t max_iters, double* lambda, int64_t* iters) {
+    cudaStream_t st = s->stream;
+    const int64_t n = s->n;
+    RefStream gen(0x5ca1ab1eULL, 0);
+    std::vector<double> v((size_t)n);
+    for (auto& e : v) e = gen.normal();
+    double ss = 0.0;
+    for (double e : v) ss += e * e;
+    double vn = std::sqrt(ss);
+    if (vn == 0.0) v[0] = 1.0, vn = 1.0;
+    for (auto& e : v) e /= vn;
+    double* dv = s->xd;   // v
+    double* dav = s->r;   // A v
+    double* dw = s->g;    // A^T A v
+    double* dots = s->scratch + 2048;
+    CK(cudaMemcpyAsync(dv, v.data(), (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    double lam = 0.0;
+    double h[2];
+    for (int64_t it = 0; it < max_iters; ++it) {
+        launch_spmv_rows(s->layout(), s->precision, dv, dav, st);
+        launch_spmv_cols(s->csc(), s->precision, n, dav, dw, st);
+        launch_dot(dw, dw, n, s->scratch, dots, st);
+        launch_dot(dv, dw, n, s->scratch + 1024, dots + 1, st);
+        CK(cudaMemcpyAsync(h, dots, 16, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double wn = std::sqrt(h[0]);
+        if (wn == 0.0) {
+            *lambda = 0.0;
+            if (iters) *iters = it + 1;
+            return ASYRK_OK;
+        }
+        const double next = h[1];
+        launch_power_update(dv, dw, dots, n, st);
+        if (it > 0 && std::abs(next - lam) <= tol * std::max(1.0, std::abs(next))) {
+            *lambda = next;
+            if (iters) *iters = it + 1;
+            CK(cudaStreamSynchronize(st));
+            return ASYRK_OK;
+        }
+        lam = next;
+    }
+    return fail(ASYRK_E_PowerIterationDiverged,
+                "power iteration did not converge within " + std::to_string(max_iters) + " iterations");
+}
+
+struct SysGuard {
+    asyrk_system* s = nullptr;
+    ~SysGuard() {
+        if (s) {
+            free_all(s);
+            delete s;
+        }
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* asyrk_last_error(void) { return g_err.c_str(); }
+int asyrk_abi_version(void) { return ASYRK_ABI_VERSION; }
+
+asyrk_status asyrk_system_create(const asyrk_csr_view* A, const double* b, int32_t precision, void* stream,
+                                 asyrk_system** out) {
+    return guarded([&] { return create_impl(A, b, precision, stream, out); });
+}
+
+asyrk_status asyrk_system_destroy(asyrk_system* sys) {
+    if (!sys) return ASYRK_OK;
+    cudaStreamSynchronize(sys->stream);
+    free_all(sys);
+    delete sys;
+    return ASYRK_OK;
+}
+
+asyrk_status asyrk_system_solve(asyrk_system* sys, const double* x0, const asyrk_run_config* cfg,
+                                asyrk_trace_out* trace, asyrk_instrument_out* instrument) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return system_solve_impl(sys, x0, cfg, trace, instrument); });
+}
+
+asyrk_status asyrk_system_rk_solve(asyrk_system* sys, const double* x0, const asyrk_rk_config* cfg,
+                                   asyrk_trace_out* trace) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return system_rk_impl(sys, x0, cfg, trace); });
+}
+
+asyrk_status asyrk_system_residuals(asyrk_system* sys, const double* x, double* r_sq, double* grad_sq) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return residuals_impl(sys, x, r_sq, grad_sq); });
+}
+
+asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t max_iters, double* lambda_max,
+                                          int64_t* iterations) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return power_impl(sys, tol, max_iters, lambda_max, iterations); });
+}
+
+asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b) {
+    if (!sys || !b) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        CK(cudaMemcpyAsync(sys->r, b, (size_t)sys->m * 8, cudaMemcpyHostToDevice, sys->stream));
+        launch_set_rhs(sys->layout(), sys->r, sys->stream);
+        CK(cudaStreamSynchronize(sys->stream));
+        CK(cudaGetLastError());
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y) {
+    if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        CK(cudaMemcpyAsync(sys->xd, x, (size_t)sys->n * 8, cudaMemcpyHostToDevice, sys->stream));
+        launch_spmv_rows(sys->layout(), sys->precision, sys->xd, sys->r, sys->stream);
+        CK(cudaMemcpyAsync(y, sys->r, (size_t)sys->m * 8, cudaMemcpyDeviceToHost, sys->stream));
+        CK(cudaStreamSynchronize(sys->stream));
+        CK(cudaGetLastError());
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x, double* y) {
+    if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        CK(cudaMemcpyAsync(sys->r, x, (size_t)sys->m * 8, cudaMemcpyHostToDevice, sys->stream));
+        launch_spmv_cols(sys->csc(), sys->precision, sys->n, sys->r, sys->g, sys->stream);
+        CK(cudaMemcpyAsync(y, sys->g, (size_t)sys->n * 8, cudaMemcpyDeviceToHost, sys->stream));
+        CK(cudaStreamSynchronize(sys->stream));
+        CK(cudaGetLastError());
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out) {
+    if (!sys || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
+    *out = sys->stats;
+    return ASYRK_OK;
+}
+
+asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out) {
+    if (!sys || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        *out = worker_max_resident_warps(precision, worker_elems_per_lane(sys->max_len), 1);
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_solve_parallel(const asyrk_csr_view* A, const double* b, const double* x0,
+                                  const asyrk_run_config* cfg, asyrk_trace_out* trace,
+                                  asyrk_instrument_out* instrument) {
+    if (!cfg) return fail(ASYRK_E_InvalidArgument, "null config");
+    return guarded([&] {
+        SysGuard g;
+        const int prec = cfg->threads == 1 ? P_F64 : cfg->precision;
+        asyrk_status s = create_impl(A, b, prec, nullptr, &g.s);
+        if (s) return s;
+        return system_solve_impl(g.s, x0, cfg, trace, instrument);
+    });
+}
+
+asyrk_status asyrk_rk_solve(const asyrk_csr_view* A, const double* b, const double* x0, const asyrk_rk_config* cfg,
+                            asyrk_trace_out* trace) {
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, b, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return system_rk_impl(g.s, x0, cfg, trace);
+    });
+}
+
+asyrk_status asyrk_residuals(const asyrk_csr_view* A, const double* x, const double* b, double* r_sq,
+                             double* grad_sq) {
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, b, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return residuals_impl(g.s, x, r_sq, grad_sq);
+    });
+}
+
+asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double tol, int64_t max_iters,
+                                              double* lambda_max) {
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, nullptr, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return power_impl(g.s, tol, max_iters, lambda_max, nullptr);
+    });
+}
+
+// sweep_threads, ref/src/parallel.cpp:447-481
+asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const double* x0,
+                                 const asyrk_run_config* cfg, const int64_t* thread_list, int64_t n_threads,
+                                 double* wall_seconds, int64_t* epochs, double* final_r_sq, double* speedup) {
+    if (!cfg || !thread_list) return fail(ASYRK_E_InvalidArgument, "null argument");
+    if (n_threads <= 0) return fail(ASYRK_E_InvalidArgument, "thread list is empty");
+    if (std::find(thread_list, thread_list + n_threads, (int64_t)1) == thread_list + n_threads)
+        return fail(ASYRK_E_InvalidArgument, "thread list must contain 1 (the speedup reference)");
+    return guarded([&] {
+        SysGuard g64, g;
+        asyrk_status s = create_impl(A, b, P_F64, nullptr, &g64.s);
+        if (s) return s;
+        if (cfg->precision != P_F64) {
+            s = create_impl(A, b, cfg->precision, nullptr, &g.s);
+            if (s) return s;
+        }
+        const long long cap = 1 + (cfg->epochs + cfg->snapshot_interval - 1) / std::max<int64_t>(1, cfg->snapshot_interval);
+        std::vector<int64_t> ep((size_t)cap);
+        std::vector<double> rs((size_t)cap), wall((size_t)cap);
+        for (int64_t t = 0; t < n_threads; ++t) {
+            asyrk_run_config c = *cfg;
+            c.threads = thread_list[t];
+            asyrk_trace_out tr{};
+            tr.cap = cap;
+            tr.epoch_index = ep.data();
+            tr.r_sq = rs.data();
+            tr.wall_seconds = wall.data();
+            asyrk_system* sys = (c.threads == 1 || cfg->precision == P_F64) ? g64.s : g.s;
+            s = system_solve_impl(sys, x0, &c, &tr, nullptr);
+            if (s) return s;
+            const int64_t last = std::min<int64_t>(tr.count, cap) - 1;
+            wall_seconds[t] = wall[(size_t)last];
+            epochs[t] = ep[(size_t)last];
+            final_r_sq[t] = rs[(size_t)last];
+        }
+        double w1 = 0.0;
+        for (int64_t t = 0; t < n_threads; ++t)
+            if (thread_list[t] == 1) {
+                w1 = wall_seconds[t];
+                break;
+            }
+        for (int64_t t = 0; t < n_threads; ++t) speedup[t] = wall_seconds[t] > 0.0 ? w1 / wall_seconds[t] : 0.0;
+        return ASYRK_OK;
+    });
+}
+
+}  // extern "C"
