@@ -9,11 +9,12 @@
 //                   plus (x_j - x*_j)^2 when an x_star oracle is given
 // Finalize:         r_sq, grad_sq, dist_sq -> trace record, stop / NonFinite
 //
-// exact = 1 reproduces the reference's floating-point order bit for bit
-// (thread-per-row and thread-per-column serial sums, single-thread serial
-// norms); used by the deterministic path so its records are bit-identical.
-// exact = 0 (async path) uses warp-per-row tree reductions and fixed-order
-// block partials: deterministic run to run, within rounding of the reference.
+// r_i and g_j are always formed in the reference's floating-point order
+// (serial storage-order sums of rounded products), so they are bit-identical
+// to ref residuals(). exact = 1 (deterministic path) also sums r^2, g^2 and
+// (x - x*)^2 serially in index order, making every trace record
+// bit-identical; exact = 0 (async path) sums them as fixed-order block
+// partials: deterministic run to run, within a few ulps of the reference.
 #include "kernels.h"
 
 namespace ak {
@@ -25,23 +26,13 @@ __device__ __forceinline__ double ldx(const void* x, long long k) {
     return (double)__ldcg(static_cast<const X*>(x) + k);
 }
 
-// ---- pass 1, exact: one thread per row, storage order, mul then add
+// ---- pass 1: one warp per row. Lanes form the products v_k * x[c_k]
+// (rounded multiplies); lane 0 adds them in storage order starting from 0.0,
+// then subtracts b_i — exactly the reference's row_dot(i, x) - b_i
+// (csr.cpp:65-70,146), so r is bit-identical in both monitor flavours.
+// fast flavour: r^2 block partials (fixed order).
 template <class V, class X>
-__global__ void __launch_bounds__(kMonThreads) rows_exact_kernel(MonitorArgs a) {
-    if (a.st->stop) return;
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.L.m) return;
-    const RowRef r = row_ref(a.L, i);
-    const V* vals = rec_vals<V>(r);
-    const int32_t* cols = rec_cols<V>(r);
-    double s = 0.0;
-    for (int k = 0; k < r.len; ++k) s = __dadd_rn(s, __dmul_rn((double)__ldg(vals + k), ldx<X>(a.x, __ldg(cols + k))));
-    a.r[i] = __dsub_rn(s, rec_b(r));
-}
-
-// ---- pass 1, fast: one warp per row, tree reduction; r^2 block partials
-template <class V, class X>
-__global__ void __launch_bounds__(kMonThreads) rows_fast_kernel(MonitorArgs a) {
+__global__ void __launch_bounds__(kMonThreads) rows_kernel(MonitorArgs a) {
     if (a.st->stop) return;
     __shared__ double red[kMonThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -52,12 +43,21 @@ __global__ void __launch_bounds__(kMonThreads) rows_fast_kernel(MonitorArgs a) {
         const V* vals = rec_vals<V>(r);
         const int32_t* cols = rec_cols<V>(r);
         double s = 0.0;
-        for (int k = lane; k < r.len; k += 32) s += (double)__ldg(vals + k) * ldx<X>(a.x, __ldg(cols + k));
-        s = warp_sum(s);
-        const double ri = s - rec_b(r);
+        for (int c0 = 0; c0 < r.len; c0 += 32) {
+            const int k = c0 + lane;
+            double p = 0.0;
+            if (k < r.len) p = __dmul_rn((double)__ldg(vals + k), ldx<X>(a.x, __ldg(cols + k)));
+            const int lim = min(32, r.len - c0);
+            for (int t = 0; t < lim; ++t) {
+                const double pt = __shfl_sync(FULL, p, t);
+                s = __dadd_rn(s, pt);
+            }
+        }
+        const double ri = __dsub_rn(s, rec_b(r));
         if (lane == 0) a.r[i] = ri;
         mine += ri * ri;
     }
+    if (a.exact) return;
     if (lane == 0) red[wib] = mine;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -138,19 +138,33 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
     }
 }
 
-// ---- finalize, exact: serial sums in the reference's order (one thread)
+// ---- finalize, exact: serial sums in the reference's order (residuals
+// csr.cpp:147-158, dist oracle parallel.cpp:82-92). Lanes square 32 values at
+// a time; lane 0 accumulates them in index order.
+__device__ __forceinline__ double serial_sumsq(const double* v, const double* w, long long n, int lane) {
+    double s = 0.0;
+    for (long long c0 = 0; c0 < n; c0 += 32) {
+        const long long k = c0 + lane;
+        double q = 0.0;
+        if (k < n) {
+            const double d = w ? __dsub_rn(v[k], w[k]) : v[k];
+            q = __dmul_rn(d, d);
+        }
+        const int lim = (int)min(32ll, n - c0);
+        for (int t = 0; t < lim; ++t) s = __dadd_rn(s, __shfl_sync(FULL, q, t));
+    }
+    return s;
+}
+
 template <class X>
 __global__ void finalize_exact_kernel(MonitorArgs a) {
-    if (a.st->stop || threadIdx.x != 0) return;
-    double rs = 0.0, gs = 0.0, ds = 0.0;
-    for (long long i = 0; i < a.L.m; ++i) rs = __dadd_rn(rs, __dmul_rn(a.r[i], a.r[i]));
-    for (long long j = 0; j < a.L.n; ++j) gs = __dadd_rn(gs, __dmul_rn(a.g[j], a.g[j]));
-    if (a.x_star)
-        for (long long j = 0; j < a.L.n; ++j) {
-            const double d = __dsub_rn(ldx<X>(a.x, j), a.x_star[j]);
-            ds = __dadd_rn(ds, __dmul_rn(d, d));
-        }
-    commit_record(a, rs, gs, ds);
+    if (a.st->stop) return;
+    const int lane = threadIdx.x & 31;
+    const double rs = serial_sumsq(a.r, nullptr, a.L.m, lane);
+    const double gs = serial_sumsq(a.g, nullptr, a.L.n, lane);
+    double ds = 0.0;
+    if (a.x_star) ds = serial_sumsq(static_cast<const double*>(a.x), a.x_star, a.L.n, lane);  // exact mode is fp64
+    if (lane == 0) commit_record(a, rs, gs, ds);
 }
 
 // ---- finalize, fast: fixed-order sum of the block partials (one block)
@@ -194,15 +208,12 @@ template <class V, class X>
 static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
     const int nbr = monitor_row_blocks(a.L.m);
     const int nbc = monitor_col_blocks(a.L.n);
-    if (a.exact) {
-        rows_exact_kernel<V, X><<<(unsigned)((a.L.m + kMonThreads - 1) / kMonThreads), kMonThreads, 0, s>>>(a);
-        cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr);
+    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a);
+    cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr);
+    if (a.exact)
         finalize_exact_kernel<X><<<1, 32, 0, s>>>(a);
-    } else {
-        rows_fast_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a);
-        cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr);
+    else
         finalize_fast_kernel<<<1, kMonThreads, 0, s>>>(a, nbr, nbc);
-    }
 }
 
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s) {

@@ -1,0 +1,114 @@
+"""Generate tests/golden/golden.npz from the REFERENCE ITSELF (oracle/_ref,
+the unmodified /root/reference sources compiled by oracle/Makefile).
+
+Run here (where /root/reference exists):  python tests/golden/make_golden.py
+The fixtures travel with the repo, so the GPU box never needs the reference.
+
+Contents (all produced by reference code paths):
+  rng/*            make_stream raw outputs, uniform_below, normals, cumulative
+                   shuffles, alias draws (ref/include/asyrk/rng.hpp, kaczmarz.cpp:14-69)
+  inst/<name>/*    gen_sparse_gaussian instances used by the reference tests
+                   (CSR arrays after normalize_rows, b, x*)
+  rk/<name>/<s>/*  rk_solve traces (uniform / shuffle / norm) incl. final_x
+  par/<name>/<v>_<s>/*  solve_parallel(threads=1) traces + instrument reports
+  res/<name>/*     residuals at a fixed x
+  pow/<name>       power_iteration_lambda_max(tol=1e-10)
+  kat/*            known-answer vectors of the reference unit tests
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle import REF  # noqa: E402
+
+# (m, n, delta, seed) — instances of the reference's own tests
+INSTANCES = {
+    "par_shuffle_30x15": (30, 15, 0.25, 61),      # test_parallel.cpp:10-43
+    "snap_24x12": (24, 12, 0.3, 67),               # test_parallel.cpp:45-60
+    "instr_48x16": (48, 16, 0.3, 71),              # test_parallel.cpp:62-85
+    "repl_40x20": (40, 20, 0.25, 73),              # test_parallel.cpp:87-98
+    "diverge_20x10": (20, 10, 0.4, 79),            # test_parallel.cpp:100-109
+    "at_solution_20x10": (20, 10, 0.4, 83),        # test_parallel.cpp:111-119
+    "accept5_200x80": (200, 80, 0.1, 5150),        # acceptance.cpp:230-270 (C5)
+    "stats_200x120": (200, 120, 0.05, 29),         # test_stats.cpp:47-62
+    "seed_30x15": (30, 15, 0.25, 43),              # test_kaczmarz.cpp:94-106
+    "dist_40x20": (40, 20, 0.2, 47),               # test_kaczmarz.cpp:108-122
+    "delay0_20x12": (20, 12, 0.3, 7),              # test_delay_sim.cpp:28-52
+    "accept9_2000x1500": (2000, 1500, 0.01, 90210),  # acceptance.cpp:400-418 (C9)
+}
+
+
+def main():
+    out = {}
+    # ---- RNG known answers
+    for seed, stream in [(0, 0), (42, 0), (31337, 3), (0x5CA1AB1E, 0)]:
+        out[f"rng/raw/{seed}_{stream}"] = REF.stream_raw(seed, stream, 1000)
+    out["rng/below/7_3_20000"] = REF.uniform_below_seq(7, 3, 20000, 2000)
+    out["rng/below/9_0_3"] = REF.uniform_below_seq(9, 0, 3, 2000)
+    out["rng/normal/1_2"] = REF.normal_seq(1, 2, 500)
+    out["rng/shuffle/21_0_30x5"] = REF.shuffle_seq(21, 0, 30, 5)
+    w = np.array([1.0, 2.0, 3.0])
+    out["rng/alias/w"] = w
+    out["rng/alias/123"] = REF.alias_sample_seq(w, 123, 5000)
+    w2 = np.linspace(0.1, 4.0, 37) ** 2
+    out["rng/alias2/w"] = w2
+    out["rng/alias2/5"] = REF.alias_sample_seq(w2, 5, 5000)
+
+    # ---- instances + traces
+    for name, (m, n, delta, seed) in INSTANCES.items():
+        A, b, xs = REF.gen_sparse_gaussian(m, n, delta, seed)
+        e = A.export()
+        p = f"inst/{name}/"
+        out[p + "shape"] = np.array([m, n])
+        out[p + "row_ptr"] = e["row_ptr"]
+        out[p + "col_idx"] = e["col_idx"]
+        out[p + "values"] = e["values"]
+        out[p + "row_norm"] = e["row_norm"]
+        out[p + "b"] = b
+        out[p + "x_star"] = xs
+        x0 = np.zeros(n)
+        epochs = 40 if m <= 200 else 10
+        for s in ["uniform", "shuffle", "norm"]:
+            t = REF.rk_solve(A, b, x0, epochs, 0.0, 31337, s, xs)
+            q = f"rk/{name}/{s}/"
+            for k in ["epoch_index", "r_sq", "grad_sq", "dist_sq", "updates_applied", "final_x"]:
+                out[q + k] = t[k]
+        for v in ["full_row", "single"]:
+            for s in ["slice_shuffle", "with_replacement"]:
+                gamma = 1.0 if v == "full_row" else 0.05
+                t = REF.solve_parallel(A, b, x0, 1, gamma, 13, 0.0, v, s, 21, 3, xs, True)
+                q = f"par/{name}/{v}_{s}/"
+                for k in ["epoch_index", "r_sq", "grad_sq", "dist_sq", "updates_applied", "final_x"]:
+                    out[q + k] = t[k]
+                ins = t["instrument"]
+                out[q + "instrument"] = np.array([ins["row_updates"], ins["increments"], ins["max_abs_error"],
+                                                  ins["tolerance"], float(ins["consistent"])])
+        rng = np.random.default_rng(seed)
+        xr = rng.standard_normal(n)
+        out[f"res/{name}/x"] = xr
+        out[f"res/{name}/vals"] = np.array(REF.residuals(A, xr, b))
+        out[f"res/{name}/Ax"] = REF.multiply(A, xr)
+        out[f"res/{name}/ATr"] = REF.multiply_transpose(A, rng.standard_normal(m))
+        out[f"res/{name}/r_in"] = np.random.default_rng(seed).standard_normal(n + m)[n:]
+        out[f"res/{name}/ATr"] = REF.multiply_transpose(A, out[f"res/{name}/r_in"])
+        out[f"pow/{name}"] = np.array([REF.power_iteration(A, 1e-10, 200000)])
+
+    # ---- known answers of the reference unit tests
+    A, bn = REF.build(1, 2, [0, 0], [0, 1], [3.0, 4.0], True, np.array([10.0]))  # test_kaczmarz.cpp:21-30
+    out["kat/rk_step_34/x1"] = REF.rk_step(A, bn, np.zeros(2), 0)
+    s = np.sqrt(0.5)
+    A3, _ = REF.build(3, 2, [0, 1, 2, 2], [0, 1, 0, 1], [1.0, 1.0, s, s], False, None)
+    out["kat/asyrk_update/third_row"] = np.array([REF.asyrk_update(A3, np.zeros(3), 2, 1, 0.5, np.array([1.0, 0.0]))])
+    out["kat/asyrk_update/singleton"] = np.array([REF.asyrk_update(A3, np.array([4.0, 0.0, 0.0]), 0, 0, 1.0,
+                                                                   np.array([3.0, 0.0]))])
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
+    np.savez_compressed(path, **out)
+    print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e3:.0f} kB")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,149 @@
+"""Host-side checks that need no GPU: the C-ABI library loads and exports
+every symbol include/*.h declares, the pybind module mirrors the reference
+signatures and error convention, the config generator's contract holds, and
+the product fails loudly (no CPU fallback) when no device is present."""
+import inspect
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADERS = [os.path.join(ROOT, "include", "asyrk_cuda.h"), os.path.join(ROOT, "include", "asyrk_datagen.h")]
+
+
+def declared_functions():
+    names = set()
+    for h in HEADERS:
+        text = open(h).read()
+        text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+        for mt in re.finditer(r"\b(asyrk_[a-z0-9_]+)\s*\(", text):
+            names.add(mt.group(1))
+    return names
+
+
+def test_c_abi_exports_every_declared_symbol():
+    from paper_1401_4780_b200 import capi
+
+    L = capi.lib()
+    declared = declared_functions()
+    assert len(declared) >= 19
+    for name in declared:
+        assert hasattr(L, name), f"{name} declared in include/ but not exported"
+    assert set(capi.EXPORTED) <= declared
+    assert L.asyrk_abi_version() == 1
+
+
+def test_exported_symbols_via_nm():
+    import subprocess
+
+    out = subprocess.run(["nm", "-D", "--defined-only", os.path.join(ROOT, "paper_1401_4780_b200",
+                                                                     "libasyrk_b200.so")],
+                         capture_output=True, text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert declared_functions() <= exported
+
+
+def test_kernels_are_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", os.path.join(ROOT, "paper_1401_4780_b200",
+                                                                  "libasyrk_b200.so")],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_pybind_signatures_match_reference():
+    import paper_1401_4780_b200 as pkg
+
+    doc = pkg.solve_parallel.__doc__
+    for arg in ["m", "n", "rows", "cols", "vals", "b", "threads", "gamma", "epochs", "target", "seed", "variant"]:
+        assert f"{arg}:" in doc
+    for arg, default in [("threads", "1"), ("gamma", "1.0"), ("epochs", "100"), ("target", "0.0"), ("seed", "0"),
+                         ("variant", "'full-row'")]:
+        assert re.search(rf"\b{arg}: [^=]*= {re.escape(default)}[,)]", doc), arg
+    doc = pkg.solve_rk.__doc__
+    for arg, default in [("epochs", "100"), ("target", "0.0"), ("seed", "0"), ("sampling", "'uniform'")]:
+        assert re.search(rf"\b{arg}: [^=]*= {re.escape(default)}[,)]", doc), arg
+
+
+@pytest.mark.parametrize(
+    "rows,cols,vals,code",
+    [
+        ([0, 0], [1, 1], [1.0, 2.0], "DuplicateEntry"),
+        ([0, 2], [1, 1], [1.0, 2.0], "IndexOutOfRange"),
+        ([0], [1], [1.0], "ZeroRow"),
+        ([0, 1], [0], [1.0, 1.0], "DimensionMismatch"),
+    ],
+)
+def test_host_validation_errors_surface_as_value_error(rows, cols, vals, code):
+    import paper_1401_4780_b200 as pkg
+
+    with pytest.raises(ValueError, match=code):
+        pkg.solve_parallel(2, 2, rows, cols, vals, [1.0, 1.0], threads=2)
+    with pytest.raises(ValueError, match=code):
+        pkg.solve_rk(2, 2, rows, cols, vals, [1.0, 1.0])
+
+
+def test_bad_variant_and_sampling_names():
+    import paper_1401_4780_b200 as pkg
+
+    with pytest.raises(ValueError, match="InvalidArgument"):
+        pkg.solve_parallel(2, 2, [0, 1], [0, 1], [1.0, 1.0], [1.0, 1.0], variant="diagonal")
+    with pytest.raises(ValueError, match="InvalidArgument"):
+        pkg.solve_rk(2, 2, [0, 1], [0, 1], [1.0, 1.0], [1.0, 1.0], sampling="sorted")
+
+
+def test_no_silent_cpu_fallback():
+    from paper_1401_4780_b200 import capi
+
+    A, b, _ = capi.generate_fixed_theta(64, 32, 4, seed=1)
+    try:
+        s = capi.System(A, b)
+    except capi.AsyrkError as e:
+        assert e.name == "ThreadSpawnFailure" and "CUDA" in str(e)
+        return
+    s.close()
+    pytest.skip("a CUDA device is present; the GPU suite covers this path")
+
+
+def test_generator_contract():
+    from paper_1401_4780_b200 import capi
+
+    m, n, th = 3000, 1000, 20
+    A, b, xs = capi.generate_fixed_theta(m, n, th, seed=5, threads=4)
+    A2, b2, xs2 = capi.generate_fixed_theta(m, n, th, seed=5, threads=1)
+    assert np.array_equal(A.values, A2.values) and np.array_equal(b, b2)  # thread-count independent
+    assert np.array_equal(A.row_ptr, np.arange(m + 1) * th)
+    cols = A.col_idx.reshape(m, th)
+    assert np.all(np.diff(cols, axis=1) > 0) and cols.min() >= 0 and cols.max() < n
+    assert A.normalized and np.all(np.abs(A.row_norm - 1.0) <= 1e-12)
+    dense_b = (A.values.reshape(m, th) * xs[cols]).sum(axis=1)
+    assert np.allclose(b, dense_b, rtol=1e-12, atol=1e-12)
+    # config 4 style: log-uniform row scaling -> raw norms in [0.1, 10]
+    A4, b4, _ = capi.generate_fixed_theta(m, n, 25, seed=9, scale_decades=1.0)
+    assert not A4.normalized and A4.row_norm.min() >= 0.1 - 1e-12 and A4.row_norm.max() <= 10 + 1e-9
+    # uniform values, multi-RHS layout
+    A3, B3, X3 = capi.generate_fixed_theta(500, 200, 10, seed=3, dist="uniform", k=4)
+    assert B3.shape == (500, 4) and X3.shape == (200, 4)
+    v = A3.values.reshape(500, 10)
+    assert np.allclose(B3, np.einsum("it,itk->ik", v, X3[A3.col_idx.reshape(500, 10)]), rtol=1e-12, atol=1e-12)
+
+
+def test_generator_rejects_bad_shapes():
+    from paper_1401_4780_b200 import capi
+
+    with pytest.raises(capi.AsyrkError, match="InvalidArgument"):
+        capi.generate_fixed_theta(10, 5, 6, seed=1)
+
+
+def test_corollary_tau_bound():
+    import paper_1401_4780_b200 as pkg
+
+    # 2e*lambda*(tau+1)/m <= 1  (stepsize.cpp:64-69); SURVEY probe: cfg2 lambda 6.076 -> tau_max 6054
+    assert pkg.max_feasible_tau(200000, 6.076) == 6053  # m/(2e*lambda) - 1 = 6053.6
+    lam = 6.076
+    t = pkg.max_feasible_tau(200000, lam)
+    assert 2 * np.e * lam * (t + 1) / 200000 <= 1 < 2 * np.e * lam * (t + 2) / 200000

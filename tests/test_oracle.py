@@ -1,0 +1,139 @@
+"""Pins the C restatement (oracle/oracle.c) against the reference's own
+outputs (tests/golden/golden.npz, made by oracle/_ref from the unmodified
+reference sources) and known answers. CPU only."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import triplets
+
+C = oracle.C
+
+
+def test_mt19937_64_known_answer():
+    # std::mt19937_64 default seed 5489: the 10000th output is 9981545732273789042
+    # (C++ standard [rand.predef]/3)
+    import ctypes
+
+    out = np.zeros(10000, np.uint64)
+    # make_stream(seed, stream) seeds with splitmix64(seed^stream); find the raw generator via a
+    # seed whose splitmix64 image is 5489 is impractical, so exercise the generator directly:
+    lib = C.L
+    lib.oc_mt_seed.argtypes = [ctypes.c_void_p, ctypes.c_uint64]
+    lib.oc_mt_next.argtypes = [ctypes.c_void_p]
+    lib.oc_mt_next.restype = ctypes.c_uint64
+    state = ctypes.create_string_buffer(312 * 8 + 16)
+    lib.oc_mt_seed(state, 5489)
+    for k in range(10000):
+        out[k] = lib.oc_mt_next(state)
+    assert int(out[-1]) == 9981545732273789042
+
+
+def test_rng_streams_match_reference(golden):
+    for key in golden.files:
+        if key.startswith("rng/raw/"):
+            seed, stream = (int(v) for v in key.split("/")[-1].split("_"))
+            assert np.array_equal(C.stream_raw(seed, stream, 1000), golden[key])
+    assert np.array_equal(C.uniform_below_seq(7, 3, 20000, 2000), golden["rng/below/7_3_20000"])
+    assert np.array_equal(C.uniform_below_seq(9, 0, 3, 2000), golden["rng/below/9_0_3"])
+    assert np.array_equal(C.normal_seq(1, 2, 500), golden["rng/normal/1_2"])
+    assert np.array_equal(C.shuffle_seq(21, 0, 30, 5), golden["rng/shuffle/21_0_30x5"])
+    assert np.array_equal(C.alias_sample_seq(golden["rng/alias/w"], 123, 5000), golden["rng/alias/123"])
+    assert np.array_equal(C.alias_sample_seq(golden["rng/alias2/w"], 5, 5000), golden["rng/alias2/5"])
+
+
+def test_alias_frequencies():
+    # test_kaczmarz.cpp:153-169: within 0.005 of w_i / sum(w) over 2e5 draws
+    w = np.array([1.0, 2.0, 3.0])
+    draws = C.alias_sample_seq(w, 123, 200000)
+    freq = np.bincount(draws, minlength=3) / 200000
+    assert np.all(np.abs(freq - w / 6.0) < 0.005)
+    with pytest.raises(oracle.OracleError, match="InvalidArgument"):
+        C.alias_sample_seq(np.array([0.0, 0.0]), 1, 1)
+
+
+def _build(inst):
+    rows, cols, vals = triplets(inst)
+    A, _ = C.build(inst["m"], inst["n"], rows, cols, vals, normalize=True, b=inst["b"])
+    return A
+
+
+def test_csr_build_matches_reference(instances):
+    for nm, inst in instances.items():
+        A = _build(inst)
+        e = A.export()
+        assert np.array_equal(e["row_ptr"], inst["row_ptr"]), nm
+        assert np.array_equal(e["col_idx"], inst["col_idx"]), nm
+        assert np.array_equal(e["values"], inst["values"]), nm  # normalize_rows idempotent on unit rows
+        assert np.array_equal(e["row_norm"], inst["row_norm"]), nm
+
+
+@pytest.mark.parametrize("sampling", ["uniform", "shuffle", "norm"])
+def test_rk_solve_bitwise(golden, instances, sampling):
+    for nm, inst in instances.items():
+        A = _build(inst)
+        q = f"rk/{nm}/{sampling}/"
+        ep = int(golden[q + "epoch_index"][-1])
+        t = C.rk_solve(A, inst["b"], np.zeros(inst["n"]), 40 if inst["m"] <= 200 else 10, 0.0, 31337, sampling,
+                       inst["x_star"])
+        for k in ["epoch_index", "r_sq", "grad_sq", "dist_sq", "updates_applied", "final_x"]:
+            assert np.array_equal(t[k], golden[q + k]), (nm, k)
+        assert t["epoch_index"][-1] == ep
+
+
+@pytest.mark.parametrize("variant", ["full_row", "single"])
+@pytest.mark.parametrize("sampling", ["slice_shuffle", "with_replacement"])
+def test_solve_single_bitwise(golden, instances, variant, sampling):
+    for nm, inst in instances.items():
+        A = _build(inst)
+        gamma = 1.0 if variant == "full_row" else 0.05
+        t = C.solve_parallel(A, inst["b"], np.zeros(inst["n"]), 1, gamma, 13, 0.0, variant, sampling, 21, 3,
+                             inst["x_star"], True)
+        q = f"par/{nm}/{variant}_{sampling}/"
+        for k in ["epoch_index", "r_sq", "grad_sq", "dist_sq", "updates_applied", "final_x"]:
+            assert np.array_equal(t[k], golden[q + k]), (nm, k)
+        ins = t["instrument"]
+        got = np.array([ins["row_updates"], ins["increments"], ins["max_abs_error"], ins["tolerance"],
+                        float(ins["consistent"])])
+        assert np.array_equal(got, golden[q + "instrument"]), nm
+
+
+def test_residuals_spmv_power_bitwise(golden, instances):
+    for nm, inst in instances.items():
+        A = _build(inst)
+        x = golden[f"res/{nm}/x"]
+        assert np.array_equal(np.array(C.residuals(A, x, inst["b"])), golden[f"res/{nm}/vals"]), nm
+        assert np.array_equal(C.multiply(A, x), golden[f"res/{nm}/Ax"]), nm
+        assert np.array_equal(C.multiply_transpose(A, golden[f"res/{nm}/r_in"]), golden[f"res/{nm}/ATr"]), nm
+        assert C.power_iteration(A, 1e-10) == golden[f"pow/{nm}"][0], nm
+
+
+def test_known_answers(golden):
+    A, bn = C.build(1, 2, [0, 0], [0, 1], [3.0, 4.0], True, np.array([10.0]))
+    x1 = C.rk_step(A, bn, np.zeros(2), 0)
+    assert np.array_equal(x1, golden["kat/rk_step_34/x1"])
+    assert abs(x1[0] - 1.2) <= 1.2e-14 and abs(x1[1] - 1.6) <= 1.6e-14  # test_kaczmarz.cpp:21-30
+    assert abs(golden["kat/asyrk_update/third_row"][0] + 0.5) <= 1e-14  # test_kaczmarz.cpp:55-60
+    assert abs(golden["kat/asyrk_update/singleton"][0] - 1.0) <= 1e-15
+
+
+def test_csr_errors():
+    with pytest.raises(oracle.OracleError, match="DuplicateEntry"):
+        C.build(2, 2, [0, 0], [1, 1], [1.0, 2.0], False)
+    with pytest.raises(oracle.OracleError, match="IndexOutOfRange"):
+        C.build(2, 2, [0, 2], [1, 1], [1.0, 2.0], False)
+    with pytest.raises(oracle.OracleError, match="ZeroRow"):
+        C.build(2, 2, [0], [1], [1.0], False)
+
+
+@pytest.mark.skipif(oracle.REF is None, reason="oracle/_ref not built (no /root/reference here)")
+def test_restatement_matches_reference_random_seeds():
+    R = oracle.REF
+    for seed in range(3):
+        A, b, xs = R.gen_sparse_gaussian(60, 30, 0.2, 1000 + seed)
+        e = A.export()
+        Ac = C.from_arrays(60, 30, e["row_ptr"], e["col_idx"], e["values"])
+        for s in ["uniform", "shuffle", "norm"]:
+            t1 = R.rk_solve(A, b, np.zeros(30), 15, 0.0, seed, s, xs)
+            t2 = C.rk_solve(Ac, b, np.zeros(30), 15, 0.0, seed, s, xs)
+            assert np.array_equal(t1["final_x"], t2["final_x"]) and np.array_equal(t1["r_sq"], t2["r_sq"])
