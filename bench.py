@@ -1,0 +1,367 @@
+#!/usr/bin/env python3
+"""AsyRK hot-path benchmark (BASELINE.json metric on config 2).
+
+Workload (N=1, BASELINE.json configs[1]): m=200000, n=100000, 30 nonzeros per
+row at distinct uniform columns, N(0,1) values, rows normalized, fp64;
+x* ~ N(0,1), b = A x*, x0 = 0; asynchronous lock-free warp-workers with
+Philox with-replacement row sampling, gamma = 1, a residual snapshot every
+epoch (snapshot_interval = 1, the reference default), stop at
+||Ax-b|| / ||b|| < 1e-6. One "step" = one full solve to tolerance.
+
+  value  projections/s of the whole job: row projections applied by all ranks
+         / max-over-ranks device time (CUDA events on the solve stream), A and
+         b resident in HBM, L2 flushed (256 MiB write) before every step.
+  e2e    the same metric through the C ABI one-shot entry point
+         asyrk_solve_parallel with HOST buffers: CSR upload + device packing,
+         solve, trace + final_x download inside the timed region.
+  --impl reference  the reference's own multithreaded CPU solve_parallel
+         (oracle/_ref, the unmodified reference sources) on this host.
+
+Multi-GPU (torchrun, N > 1): each rank solves an independent system of the
+same shape (seed + rank) — replicas, no data-path collective ("scaling":
+"weak"); timing is the max over ranks.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Kaczmarz row projections/sec; time to ||Ax-b||/||b||<1e-6 vs CPU AsyRK"
+CFG2 = dict(m=200000, n=100000, theta=30, seed=1002)
+TOL = 1e-6
+BYTES_PER_PROJ_F64 = 864  # S_A 384 + x gather 240 + atomic payload 240
+L2_FLUSH_BYTES = 256 << 20
+
+
+def workload_config(W, extra=None):
+    c = {
+        "workload": "config2: m=200000 n=100000 theta=30 N(0,1) unit rows fp64, x0=0, async to ||r||/||b||<1e-6",
+        "sampling": "with_replacement (Philox per warp)",
+        "gamma": 1.0,
+        "snapshot_interval": 1,
+        "warps": W,
+        "l2": "flushed before every step (256 MiB write); A (75 MB records) re-read from HBM each step",
+        "x0": "zeros",
+    }
+    if extra:
+        c.update(extra)
+    return c
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram read+write bytes per worker launch from the committed ncu capture, or None."""
+    p = os.path.join(ROOT, "profiles", "worker_ncu_summary.json")
+    try:
+        d = json.load(open(p))
+        return d.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def gen_system(seed):
+    from paper_1401_4780_b200 import capi
+
+    return capi.generate_fixed_theta(CFG2["m"], CFG2["n"], CFG2["theta"], seed=seed)
+
+
+# --------------------------------------------------------------------------- reference arm
+def ref_solve_once(R, Ah, b, threads, target, epochs=10000):
+    x0 = np.zeros(Ah.n)
+    t = R.solve_parallel(Ah, b, x0, threads=threads, gamma=1.0, epochs=epochs, target=target,
+                         variant="full_row", sampling="with_replacement", seed=7, snapshot_interval=1, cap=epochs + 2)
+    return int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), t
+
+
+def load_ref():
+    import oracle
+
+    if oracle.REF is None:
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "ref"], check=False)
+        import importlib
+
+        importlib.reload(oracle)
+    return oracle.REF
+
+
+def ref_matrix(R, A):
+    rows = np.repeat(np.arange(A.m, dtype=np.int64), np.diff(A.row_ptr))
+    Ah, _ = R.build(A.m, A.n, rows, A.col_idx, A.values, normalize=True, b=None)
+    return Ah
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    R = load_ref()
+    if R is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built and reference sources absent"}))
+        return 0
+    A, b, xs = gen_system(CFG2["seed"])
+    Ah = ref_matrix(R, A)
+    target = TOL * TOL * float(b @ b)
+    cores = host_cores()
+    for _ in range(args.warmup):
+        ref_solve_once(R, Ah, b, cores, target)
+    proj, wall, ttt = 0, 0.0, []
+    for _ in range(args.steps):
+        p, w, t = ref_solve_once(R, Ah, b, cores, target)
+        proj += p
+        wall += w
+        ttt.append(w)
+    value = proj / wall
+    cpu = {"value": value, "unit": "proj/s", "cores": cores, "kind": "reference",
+           "sample": f"{args.steps} full config-2 solves to 1e-6 (reference solve_parallel, {cores} threads, "
+                     "with_replacement, gamma=1, snapshot_interval=1)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "config": workload_config(cores, {"threads": cores, "warps": None}),
+        "time_to_tolerance_ms": 1e3 * statistics.median(ttt), "epochs": int(t["epoch_index"][-1]),
+        "cpu_baseline": cpu, "e2e": {"value": value, "unit": "proj/s", "h2d_bytes_per_step": 0,
+                                     "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+
+    from paper_1401_4780_b200 import capi
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    capi.check(capi.lib().asyrk_set_device(local))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    A, b, xs = gen_system(CFG2["seed"] + rank)
+    bb = float(b @ b)
+    target = TOL * TOL * bb
+    stream = torch.cuda.Stream()
+    S = capi.System(A, b, stream=stream.cuda_stream)
+    W = args.warps or S.max_resident_warps()
+    lam, lam_iters = S.power_iteration(1e-6)  # stats.cpp:15-50 on the device; tau bound beside the warp count
+    flush =torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    solve_kw = dict(threads=W, gamma=1.0, epochs=2000, target=target, sampling=capi.WITH_REPLACEMENT,
+                    snapshot_interval=1, want_x=False)
+
+    for w in range(args.warmup):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        S.solve(seed=100 + w, **solve_kw)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    stats = []
+    epochs = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[k][0].record(stream)
+            r = S.solve(seed=1000 + k, **solve_kw)
+            ev[k][1].record(stream)
+            stats.append(S.stats())
+            epochs.append(int(r["epoch_index"][-1]))
+            rel = float(np.sqrt(r["r_sq"][-1] / bb))
+            if not rel < TOL:
+                raise RuntimeError(f"step {k} stopped at relative residual {rel} (epochs {epochs[-1]})")
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(c) for a, c in ev]
+    dev_ms = sum(step_ms)
+    proj = sum(s["projections"] for s in stats)
+    launches = sum(s["kernel_launches"] for s in stats)
+    w_ms = sum(s["worker_ms"] for s in stats)
+    w_launch = sum(s["worker_launches"] for s in stats)
+    if dist:
+        t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot = torch.tensor([float(proj)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        dev_ms_max, proj_all = float(t.item()), float(tot.item())
+    else:
+        dev_ms_max, proj_all = dev_ms, float(proj)
+    value = proj_all / (dev_ms_max * 1e-3)
+
+    # ---- e2e: one-shot C-ABI call with host buffers
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_wall = 0.0
+    e2e_proj = 0
+    for k in range(e2e_steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = capi.solve_parallel_host(A, b, threads=W, gamma=1.0, epochs=2000, target=target,
+                                     sampling=capi.WITH_REPLACEMENT, seed=2000 + k)
+        e2e_wall += time.perf_counter() - t0
+        e2e_proj += int(r["updates_applied"][-1])
+    if dist:
+        t = torch.tensor([e2e_wall], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_wall = float(t.item())
+        tot = torch.tensor([float(e2e_proj)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tot)
+        e2e_proj = float(tot.item())
+    h2d = 8 * (A.m + 1) + 16 * A.nnz + 8 * A.m + 8 * A.m  # row_ptr, col_idx+values, row_norm, b
+    d2h = 8 * A.n + 48 * (max(epochs) + 2)  # final_x + trace records
+
+    out = None
+    if rank == 0:
+        peak, peak_kind = measured_peak_hbm()
+        avg_launch_ms = w_ms / max(w_launch, 1)
+        proj_per_launch = CFG2["m"]
+        achieved = BYTES_PER_PROJ_F64 * proj_per_launch / (avg_launch_ms * 1e-3) / 1e9
+        traffic = ncu_traffic()
+        out = {
+            "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(W, {"resident_warps": stats[0]["resident_warps"],
+                                          "lambda_max": lam, "tau_max": CFG2["m"] / (2 * np.e * lam) - 1,
+                                          "parallelism": f"replicas x{world}"}),
+            "time_to_tolerance_ms": statistics.median(step_ms), "epochs": statistics.median(epochs),
+            "e2e": {"value": e2e_proj / e2e_wall, "unit": "proj/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_wall / e2e_steps},
+            "gpu_launches": launches,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "asyrk worker (K2)", "bytes_per_proj": BYTES_PER_PROJ_F64,
+                         "avg_launch_ms": avg_launch_ms, "peak_source": peak_kind,
+                         "worker_share_of_step": w_ms / dev_ms},
+            "worker_proj_per_s": proj / (w_ms * 1e-3),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(A, b)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    S.close()
+    if out is not None:
+        print(json.dumps(out))
+    return 0
+
+
+def cpu_baseline(A, b):
+    R = load_ref()
+    if R is None:
+        return None
+    Ah = ref_matrix(R, A)
+    cores = host_cores()
+    target = TOL * TOL * float(b @ b)
+    p, w, t = ref_solve_once(R, Ah, b, cores, target)
+    return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference",
+            "sample": f"1 full config-2 solve to 1e-6 ({int(t['epoch_index'][-1])} epochs, {w:.2f} s) with the "
+                      f"reference solve_parallel, {cores} threads, with_replacement",
+            "time_to_tolerance_ms": 1e3 * w}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = all resident)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -70,6 +70,8 @@ typedef enum {
 /* Message of the last failing call on this thread ("" if none). */
 const char* asyrk_last_error(void);
 int asyrk_abi_version(void);
+/* Select the CUDA device for this host thread (one process per GPU). */
+asyrk_status asyrk_set_device(int32_t device);
 
 /* Host CSR, the reference CsrMatrix fields (ref/include/asyrk/csr.hpp:69-75).
  * row_norm are the reference's cached norms (csr.cpp:53-61, recomputed by
@@ -210,6 +212,13 @@ asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
 /* Largest number of worker warps that are co-resident for this system. */
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
+
+/* ---- measurement ------------------------------------------------------- */
+/* x-side roofline R_x: theta random gathers of an n-element
+ * x, a warp reduction, theta random red.global.add per "projection", no A
+ * stream. mode 0 dependent gather->red, 1 gathers only, 2 reds only. */
+asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t precision, int32_t warps,
+                                    int64_t proj_per_warp, int32_t mode, double* proj_per_s, double* kernel_ms);
 
 #ifdef __cplusplus
 }

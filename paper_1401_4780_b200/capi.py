@@ -89,6 +89,7 @@ def lib():
                               "paper_1401_4780_b200/csrc)")
         L = C.CDLL(LIB_PATH)
         L.asyrk_last_error.restype = C.c_char_p
+        L.asyrk_set_device.argtypes = [C.c_int32]
         sp = C.c_void_p
         L.asyrk_system_create.argtypes = [C.POINTER(CsrView), _f64p, C.c_int32, C.c_void_p, C.POINTER(sp)]
         L.asyrk_system_destroy.argtypes = [sp]
@@ -109,6 +110,8 @@ def lib():
         L.asyrk_power_iteration_lambda_max.argtypes = [C.POINTER(CsrView), C.c_double, C.c_int64, _f64p]
         L.asyrk_sweep_threads.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig), _i64p, C.c_int64,
                                           _f64p, _i64p, _f64p, _f64p]
+        L.asyrk_microbench_xside.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
+                                             _f64p, _f64p]
         L.asyrk_generate_fixed_theta.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int32, C.c_double,
                                                  C.c_int64, C.c_int32, _i64p, _i64p, _f64p, _f64p, _f64p, _f64p,
                                                  _i32p]
@@ -118,12 +121,21 @@ def lib():
 
 # every symbol include/asyrk_cuda.h and include/asyrk_datagen.h declare
 EXPORTED = [
-    "asyrk_last_error", "asyrk_abi_version", "asyrk_solve_parallel", "asyrk_rk_solve", "asyrk_residuals",
+    "asyrk_last_error", "asyrk_abi_version", "asyrk_set_device", "asyrk_solve_parallel", "asyrk_rk_solve", "asyrk_residuals",
     "asyrk_power_iteration_lambda_max", "asyrk_sweep_threads", "asyrk_system_create", "asyrk_system_destroy",
     "asyrk_system_solve", "asyrk_system_rk_solve", "asyrk_system_residuals", "asyrk_system_set_rhs",
     "asyrk_system_multiply", "asyrk_system_multiply_transpose", "asyrk_system_power_iteration",
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
+    "asyrk_microbench_xside",
 ]
+
+
+def microbench_xside(n, theta, precision=F64, warps=4736, proj_per_warp=256, mode=0):
+    """R_x: projections/s of the x-side traffic alone (see asyrk_microbench_xside)."""
+    rate, ms = C.c_double(), C.c_double()
+    check(lib().asyrk_microbench_xside(n, theta, precision, warps, proj_per_warp, mode, C.byref(rate),
+                                       C.byref(ms)))
+    return rate.value
 
 
 def check(status: int):

@@ -52,10 +52,14 @@ void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
 
 // ---- K3: residual monitor r = Ax - b, g = A^T r, dist = ||x - x*||^2
+// Columns of A in SELL-32 order: the 32 columns of group g interleave their
+// entries, entry t of column 32g+l at grp_off[g] + 32t + l (rows ascending
+// within each column); slots past a column's length are padding.
 struct CscDev {
-    const long long* col_ptr;     // n+1
-    const int32_t* row;           // nnz
-    const void* val;              // nnz (V)
+    const long long* grp_off;     // ceil(n/32)+1
+    const int32_t* col_len;       // n
+    const int32_t* row;           // padded
+    const void* val;              // padded (V)
 };
 struct MonitorArgs {
     Layout L;
@@ -70,13 +74,22 @@ struct MonitorArgs {
     DevState* st;
     int* host_flag;               // mapped pinned: stop seen by the host
     int exact;                    // 1: reference summation order (bitwise)
+    int stage_bytes;              // pass-1 staged record bytes per warp
     int advance;                  // 0: initial record, 1: after a chunk
     long long m_rows;
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 
 // ---- K4: power iteration building blocks (stats.cpp:15-50)
-void launch_spmv_rows(const Layout& L, int precision, const double* v, double* out, cudaStream_t s);
+void launch_spmv_rows(const Layout& L, int precision, int stage, const double* v, double* out, cudaStream_t s);
+int monitor_stage_bytes(const Layout& L, uint32_t max_len, int vbytes);
+// SELL-32 columns from a column-sorted CSC: lengths + group sizes, then scatter
+void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s);
+void launch_sell_scatter(const long long* col_ptr, const int32_t* src_row, const void* src_val, const int32_t* col_len,
+                         const long long* grp_off, long long n, int precision, int32_t* dst_row, void* dst_val,
+                         cudaStream_t s);
+size_t scan_temp_bytes(long long count);
+void exclusive_scan(void* temp, size_t temp_bytes, const long long* in, long long* out, long long count, cudaStream_t s);
 void launch_spmv_cols(const CscDev& C, int precision, long long n, const double* r, double* out,
                       cudaStream_t s);
 // dot/norm with a fixed-order tree; result in *out (device)

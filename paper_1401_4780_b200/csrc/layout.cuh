@@ -28,6 +28,7 @@ struct Layout {
     uint32_t stride16;         // uniform record stride / 16 B
     uint32_t uniform_len;      // uniform nonzeros per row
     int64_t m, n;
+    size_t rec_bytes;          // total record bytes
 };
 
 struct RowRef {

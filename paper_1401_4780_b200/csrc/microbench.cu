@@ -1,0 +1,84 @@
+// x-side roofline microbenchmark (SURVEY.md §8d "R_x"): the x traffic of one
+// projection with no A stream — theta random L2-resident gathers of x, a warp
+// reduction, then theta random red.global.add — at a given warp count and x
+// footprint. Modes: 0 gather -> reduce -> red (the worker's dependent chain),
+// 1 gathers only, 2 reds only. Indices come from a counter hash, so no memory
+// other than x is touched. Used by bench.py to state the L2/atomic-bound
+// roofline beside the HBM one.
+#include "../../include/asyrk_cuda.h"
+#include "kernels.h"
+
+namespace ak {
+
+__device__ __forceinline__ uint32_t hash32(uint32_t a) {
+    a ^= a >> 16;
+    a *= 0x7feb352du;
+    a ^= a >> 15;
+    a *= 0x846ca68bu;
+    a ^= a >> 16;
+    return a;
+}
+
+template <class X>
+__global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta, long long per_warp, int mode,
+                                                    unsigned long long* sink) {
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    X acc_all = X(0);
+    for (long long q = 0; q < per_warp; ++q) {
+        const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)lane * 0xC2B2AE35u);
+        const uint32_t col = (uint32_t)(((uint64_t)h * n) >> 32);
+        const bool on = lane < theta;
+        X s = X(0);
+        if (mode != 2 && on) s = __ldcg(x + col);
+        if (mode == 0) {
+            s = warp_sum(s);
+            if (on) atomicAdd(x + col, X(1e-30) * s);
+        } else if (mode == 2) {
+            if (on) atomicAdd(x + col, X(1e-30));
+        } else {
+            acc_all += s;
+        }
+    }
+    if (mode == 1 && acc_all == X(12345.678)) atomicAdd(sink, 1ull);  // keep the gathers alive
+}
+
+}  // namespace ak
+
+extern "C" asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t precision, int32_t warps,
+                                               int64_t proj_per_warp, int32_t mode, double* proj_per_s,
+                                               double* kernel_ms) {
+    using namespace ak;
+    if (n < 1 || theta < 1 || theta > 32 || warps < 1 || proj_per_warp < 1) return ASYRK_E_InvalidArgument;
+    void* x = nullptr;
+    unsigned long long* sink = nullptr;
+    const size_t xb = (size_t)n * (precision == P_F32 ? 4 : 8);
+    if (cudaMalloc(&x, xb) != cudaSuccess) return ASYRK_E_TooLarge;
+    cudaMalloc(&sink, 8);
+    cudaMemset(x, 0, xb);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int threads = 256;
+    const int blocks = (warps * 32 + threads - 1) / threads;
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+        cudaEventRecord(e0);
+        if (precision == P_F32)
+            xside_kernel<float><<<blocks, threads>>>((float*)x, (uint32_t)n, theta, proj_per_warp, mode, sink);
+        else
+            xside_kernel<double><<<blocks, threads>>>((double*)x, (uint32_t)n, theta, proj_per_warp, mode, sink);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(x);
+    cudaFree(sink);
+    if (err != cudaSuccess) return ASYRK_E_ThreadSpawnFailure;
+    *proj_per_s = (double)blocks * threads / 32 * (double)proj_per_warp / (ms * 1e-3);
+    if (kernel_ms) *kernel_ms = ms;
+    return ASYRK_OK;
+}

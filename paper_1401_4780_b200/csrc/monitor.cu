@@ -4,106 +4,184 @@
 // coordinator's stop logic (parallel.cpp:388-408).
 //
 // Pass 1 (rows):    r_i = a_i^T x - b_i
-// Pass 2 (columns): g_j = sum_i a_ij r_i over the CSC copy, rows ascending
-//                   (the reference's multiply_transpose order, csr.cpp:80-92),
-//                   plus (x_j - x*_j)^2 when an x_star oracle is given
+// Pass 2 (columns): g_j = sum_i a_ij r_i, rows ascending (multiply_transpose
+//                   order, csr.cpp:80-92), plus (x_j - x*_j)^2 with an x* oracle
 // Finalize:         r_sq, grad_sq, dist_sq -> trace record, stop / NonFinite
 //
-// r_i and g_j are always formed in the reference's floating-point order
-// (serial storage-order sums of rounded products), so they are bit-identical
-// to ref residuals(). exact = 1 (deterministic path) also sums r^2, g^2 and
+// r_i and g_j are formed in the reference's floating-point order (serial
+// storage-order sums of rounded products) and are bit-identical to
+// ref residuals(). exact = 1 (deterministic path) also sums r^2, g^2 and
 // (x - x*)^2 serially in index order, making every trace record
 // bit-identical; exact = 0 (async path) sums them as fixed-order block
 // partials: deterministic run to run, within a few ulps of the reference.
+//
+// One lane per row / column keeps the serial order without any shuffle
+// chain; coalescing comes from the layouts: pass 1 stages 32 consecutive
+// row records (contiguous bytes) into shared memory with 16-byte loads;
+// pass 2 reads the SELL-32 column layout (entry t of the 32 columns of a
+// group stored contiguously, layout.cuh), so a warp's loads are contiguous.
+// x and r are read through the read-only path: the kernels run quiesced
+// (L1 is invalidated at every launch), unlike the workers.
 #include "kernels.h"
 
 namespace ak {
 
 constexpr int kMonThreads = 256;
+constexpr int kRowWarps = 8;            // warps per block, pass 1
+constexpr int kStageMax = 16384;        // staged record bytes per warp
 
-template <class X>
-__device__ __forceinline__ double ldx(const void* x, long long k) {
-    return (double)__ldcg(static_cast<const X*>(x) + k);
+static int sm_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
 }
 
-// ---- pass 1: one warp per row. Lanes form the products v_k * x[c_k]
-// (rounded multiplies); lane 0 adds them in storage order starting from 0.0,
-// then subtracts b_i — exactly the reference's row_dot(i, x) - b_i
-// (csr.cpp:65-70,146), so r is bit-identical in both monitor flavours.
-// fast flavour: r^2 block partials (fixed order).
+__device__ __forceinline__ size_t row_off(const Layout& L, long long i) {
+    if (L.row_info == nullptr) return (size_t)i * ((size_t)L.stride16 * 16u);
+    return i < L.m ? (size_t)__ldg(L.row_info + i).x * 16u : L.rec_bytes;
+}
+
+template <class X>
+__device__ __forceinline__ double ldro(const X* p) {
+    return (double)__ldg(p);
+}
+
+// Serial storage-order dot of one row: s = 0; s += v_k * x[c_k]  (csr.cpp:65-70)
 template <class V, class X>
-__global__ void __launch_bounds__(kMonThreads) rows_kernel(MonitorArgs a) {
-    if (a.st->stop) return;
-    __shared__ double red[kMonThreads / 32];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long warps_total = (long long)gridDim.x * (kMonThreads / 32);
-    double mine = 0.0;
-    for (long long i = (long long)blockIdx.x * (kMonThreads / 32) + wib; i < a.L.m; i += warps_total) {
-        const RowRef r = row_ref(a.L, i);
-        const V* vals = rec_vals<V>(r);
-        const int32_t* cols = rec_cols<V>(r);
-        double s = 0.0;
-        for (int c0 = 0; c0 < r.len; c0 += 32) {
-            const int k = c0 + lane;
-            double p = 0.0;
-            if (k < r.len) p = __dmul_rn((double)__ldg(vals + k), ldx<X>(a.x, __ldg(cols + k)));
-            const int lim = min(32, r.len - c0);
-            for (int t = 0; t < lim; ++t) {
-                const double pt = __shfl_sync(FULL, p, t);
-                s = __dadd_rn(s, pt);
-            }
-        }
-        const double ri = __dsub_rn(s, rec_b(r));
-        if (lane == 0) a.r[i] = ri;
-        mine += ri * ri;
+__device__ __forceinline__ double row_dot_serial(const unsigned char* base, int len, const X* __restrict__ x) {
+    const V* vals = reinterpret_cast<const V*>(base + 16);
+    const int32_t* cols = reinterpret_cast<const int32_t*>(base + 16 + (size_t)len * sizeof(V));
+    double s = 0.0;
+    int k = 0;
+    for (; k + 8 <= len; k += 8) {  // 8 independent gathers in flight per lane, then ordered adds
+        double xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = ldro(x + cols[k + u]);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn((double)vals[k + u], xv[u]));
     }
-    if (a.exact) return;
+    for (; k < len; ++k) s = __dadd_rn(s, __dmul_rn((double)vals[k], ldro(x + cols[k])));
+    return s;
+}
+
+// Pass 1 / SpMV rows. out[i] = a_i^T x (- b_i when sub_b). part: r^2 block partials or null.
+template <class V, class X>
+__global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(Layout L, const X* __restrict__ x, double* out,
+                                                             double* part, int stage_bytes, int sub_b,
+                                                             const DevState* st) {
+    if (st && st->stop) return;
+    extern __shared__ __align__(16) unsigned char stage_all[];
+    __shared__ double red[kRowWarps];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned char* stage = stage_all + (size_t)wib * stage_bytes;
+    const long long tiles = (L.m + 31) / 32;
+    const long long gw = (long long)blockIdx.x * kRowWarps + wib, nw = (long long)gridDim.x * kRowWarps;
+    double mine = 0.0;
+    for (long long t = gw; t < tiles; t += nw) {
+        const long long r0 = t * 32;
+        const int nr = (int)min(32ll, L.m - r0);
+        const size_t start = row_off(L, r0), end = row_off(L, r0 + nr);
+        const bool staged = end - start <= (size_t)stage_bytes;
+        if (staged) {
+            const uint4* src = reinterpret_cast<const uint4*>(L.rec + start);
+            uint4* dst = reinterpret_cast<uint4*>(stage);
+            const int n16 = (int)((end - start) / 16);
+            for (int o = lane; o < n16; o += 32) dst[o] = __ldg(src + o);
+        }
+        __syncwarp();
+        if (lane < nr) {
+            const long long i = r0 + lane;
+            const size_t off = row_off(L, i);
+            const int len = L.row_info ? (int)__ldg(L.row_info + i).y : (int)L.uniform_len;
+            // two call sites so each pointer keeps its address space (LDS vs LDG, not generic LD)
+            double s, bi;
+            if (staged) {
+                const unsigned char* base = stage + (off - start);
+                s = row_dot_serial<V, X>(base, len, x);
+                bi = *reinterpret_cast<const double*>(base);
+            } else {
+                const unsigned char* base = L.rec + off;
+                s = row_dot_serial<V, X>(base, len, x);
+                bi = __ldg(reinterpret_cast<const double*>(base));
+            }
+            if (sub_b) s = __dsub_rn(s, bi);
+            out[i] = s;
+            mine += s * s;
+        }
+        __syncwarp();
+    }
+    if (!part) return;
+    mine = warp_sum(mine);
     if (lane == 0) red[wib] = mine;
     __syncthreads();
     if (threadIdx.x == 0) {
         double t = 0.0;
-        for (int w = 0; w < kMonThreads / 32; ++w) t += red[w];
-        a.part[blockIdx.x] = t;
+        for (int w = 0; w < kRowWarps; ++w) t += red[w];
+        part[blockIdx.x] = t;
     }
 }
 
-// ---- pass 2: one thread per column over the CSC copy (rows ascending).
-// exact: g_j kept for the serial finalize; fast: g^2 and dist^2 block partials.
+// Pass 2 / SpMV columns over SELL-32: lane l of group g owns column 32g + l.
+// out: g (or null), part: {g^2, dist^2} block partials (or null).
 template <class V, class X>
-__global__ void __launch_bounds__(kMonThreads) cols_kernel(MonitorArgs a, int nblocks_rows) {
-    if (a.st->stop) return;
-    __shared__ double red_g[kMonThreads], red_d[kMonThreads];
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n, const double* __restrict__ r,
+                                                          double* out, double* part_g, double* part_d,
+                                                          const X* __restrict__ x, const double* __restrict__ x_star,
+                                                          const DevState* st) {
+    if (st && st->stop) return;
+    __shared__ double red_g[kMonThreads / 32], red_d[kMonThreads / 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const long long j = (long long)blockIdx.x * kMonThreads + threadIdx.x;
+    const long long grp = j >> 5;
     double g2 = 0.0, d2 = 0.0;
-    if (j < a.L.n) {
-        const long long e0 = __ldg(a.csc.col_ptr + j), e1 = __ldg(a.csc.col_ptr + j + 1);
-        const V* cv = static_cast<const V*>(a.csc.val);
+    if (j < n) {
+        const int len = __ldg(C.col_len + j);
+        const long long base = __ldg(C.grp_off + grp) + lane;
+        const V* cv = static_cast<const V*>(C.val);
         double g = 0.0;
-        for (long long e = e0; e < e1; ++e) g = __dadd_rn(g, __dmul_rn((double)__ldg(cv + e), a.r[__ldg(a.csc.row + e)]));
-        if (a.exact) {
-            a.g[j] = g;
-        } else {
-            g2 = g * g;
-            if (a.x_star) {
-                const double d = ldx<X>(a.x, j) - a.x_star[j];
-                d2 = d * d;
+        int t = 0;
+        for (; t + 8 <= len; t += 8) {  // 8 independent gathers in flight per lane
+            const long long e = base + 32ll * t;
+            double rv[8], av[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                rv[u] = __ldg(r + __ldg(C.row + e + 32 * u));
+                av[u] = (double)__ldg(cv + e + 32 * u);
             }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) g = __dadd_rn(g, __dmul_rn(av[u], rv[u]));
+        }
+        for (; t < len; ++t) {
+            const long long e = base + 32ll * t;
+            g = __dadd_rn(g, __dmul_rn((double)__ldg(cv + e), __ldg(r + __ldg(C.row + e))));
+        }
+        if (out) out[j] = g;
+        g2 = g * g;
+        if (x_star) {
+            const double d = ldro(x + j) - x_star[j];
+            d2 = d * d;
         }
     }
-    if (a.exact) return;
-    red_g[threadIdx.x] = g2;
-    red_d[threadIdx.x] = d2;
+    if (!part_g) return;
+    g2 = warp_sum(g2);
+    d2 = warp_sum(d2);
+    if (lane == 0) {
+        red_g[wib] = g2;
+        red_d[wib] = d2;
+    }
     __syncthreads();
-    for (int o = kMonThreads / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            red_g[threadIdx.x] += red_g[threadIdx.x + o];
-            red_d[threadIdx.x] += red_d[threadIdx.x + o];
-        }
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
-        a.part[nblocks_rows + blockIdx.x] = red_g[0];
-        a.part[nblocks_rows + gridDim.x + blockIdx.x] = red_d[0];
+        double a = 0.0, b = 0.0;
+        for (int w = 0; w < kMonThreads / 32; ++w) {
+            a += red_g[w];
+            b += red_d[w];
+        }
+        part_g[blockIdx.x] = a;
+        part_d[blockIdx.x] = b;
     }
 }
 
@@ -156,7 +234,6 @@ __device__ __forceinline__ double serial_sumsq(const double* v, const double* w,
     return s;
 }
 
-template <class X>
 __global__ void finalize_exact_kernel(MonitorArgs a) {
     if (a.st->stop) return;
     const int lane = threadIdx.x & 31;
@@ -187,31 +264,50 @@ __global__ void __launch_bounds__(kMonThreads) finalize_fast_kernel(MonitorArgs 
     if (threadIdx.x == 0) commit_record(a, red[0][0], red[1][0], red[2][0]);
 }
 
-static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+// ---- launch geometry
+int monitor_stage_bytes(const Layout& L, uint32_t max_len, int vbytes) {
+    const size_t rec = (size_t)rec_size16(max_len, vbytes) * 16u;
+    size_t s = 32 * rec;
+    if (s > (size_t)kStageMax) s = kStageMax;
+    return (int)((s + 15) / 16 * 16);
+}
+
+template <class V, class X>
+static void rows_launch(const Layout& L, const X* x, double* out, double* part, int stage, int sub_b,
+                        const DevState* st, int& nblocks, cudaStream_t s) {
+    const size_t smem = (size_t)stage * kRowWarps;
+    static size_t configured = 0;
+    if (smem > 48 * 1024 && smem > configured) {
+        cudaFuncSetAttribute((const void*)rows_kernel<V, X>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kRowWarps * kStageMax));
+        configured = (size_t)kRowWarps * kStageMax;
     }
-    return sms;
+    const long long tiles = (L.m + 31) / 32;
+    long long want = (tiles + kRowWarps - 1) / kRowWarps;
+    const long long cap = (long long)sm_count() * 4;
+    nblocks = (int)(want < cap ? want : cap);
+    rows_kernel<V, X><<<nblocks, 32 * kRowWarps, smem, s>>>(L, x, out, part, stage, sub_b, st);
 }
 
 int monitor_row_blocks(long long m) {
-    const long long want = (m + (kMonThreads / 32) - 1) / (kMonThreads / 32);
-    const long long cap = (long long)sm_count() * 8;
+    const long long tiles = (m + 31) / 32;
+    const long long want = (tiles + kRowWarps - 1) / kRowWarps;
+    const long long cap = (long long)sm_count() * 4;
     return (int)(want < cap ? want : cap);
 }
 int monitor_col_blocks(long long n) { return (int)((n + kMonThreads - 1) / kMonThreads); }
 
 template <class V, class X>
 static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
-    const int nbr = monitor_row_blocks(a.L.m);
+    int nbr = 0;
     const int nbc = monitor_col_blocks(a.L.n);
-    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a);
-    cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr);
+    const X* x = static_cast<const X*>(a.x);
+    rows_launch<V, X>(a.L, x, a.r, a.exact ? nullptr : a.part, a.stage_bytes, 1, a.st, nbr, s);
+    cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.exact ? a.g : nullptr,
+                                                  a.exact ? nullptr : a.part + nbr,
+                                                  a.exact ? nullptr : a.part + nbr + nbc, x, a.x_star, a.st);
     if (a.exact)
-        finalize_exact_kernel<X><<<1, 32, 0, s>>>(a);
+        finalize_exact_kernel<<<1, 32, 0, s>>>(a);
     else
         finalize_fast_kernel<<<1, kMonThreads, 0, s>>>(a, nbr, nbc);
 }
@@ -225,41 +321,22 @@ void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s) {
 }
 
 // ---- power iteration pieces (ref/src/stats.cpp:15-50): y = A v and
-// w = A^T y in the reference's order, fixed-order tree dots.
-template <class V>
-__global__ void __launch_bounds__(kMonThreads) spmv_rows_kernel(Layout L, const double* v, double* out) {
-    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= L.m) return;
-    const RowRef r = row_ref(L, i);
-    const V* vals = rec_vals<V>(r);
-    const int32_t* cols = rec_cols<V>(r);
-    double s = 0.0;
-    for (int k = 0; k < r.len; ++k) s = __dadd_rn(s, __dmul_rn((double)__ldg(vals + k), v[__ldg(cols + k)]));
-    out[i] = s;
-}
-template <class V>
-__global__ void __launch_bounds__(kMonThreads) spmv_cols_kernel(CscDev C, long long n, const double* r, double* out) {
-    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n) return;
-    const V* cv = static_cast<const V*>(C.val);
-    double g = 0.0;
-    for (long long e = C.col_ptr[j]; e < C.col_ptr[j + 1]; ++e) g = __dadd_rn(g, __dmul_rn((double)cv[e], r[C.row[e]]));
-    out[j] = g;
-}
-
-void launch_spmv_rows(const Layout& L, int precision, const double* v, double* out, cudaStream_t s) {
-    const unsigned nb = (unsigned)((L.m + kMonThreads - 1) / kMonThreads);
+// w = A^T y in the reference's order (CsrMatrix::multiply / multiply_transpose).
+void launch_spmv_rows(const Layout& L, int precision, int stage, const double* v, double* out, cudaStream_t s) {
+    int nb = 0;
     if (precision == P_F64)
-        spmv_rows_kernel<double><<<nb, kMonThreads, 0, s>>>(L, v, out);
+        rows_launch<double, double>(L, v, out, nullptr, stage, 0, nullptr, nb, s);
     else
-        spmv_rows_kernel<float><<<nb, kMonThreads, 0, s>>>(L, v, out);
+        rows_launch<float, double>(L, v, out, nullptr, stage, 0, nullptr, nb, s);
 }
 void launch_spmv_cols(const CscDev& C, int precision, long long n, const double* r, double* out, cudaStream_t s) {
     const unsigned nb = (unsigned)((n + kMonThreads - 1) / kMonThreads);
     if (precision == P_F64)
-        spmv_cols_kernel<double><<<nb, kMonThreads, 0, s>>>(C, n, r, out);
+        cols_kernel<double, double><<<nb, kMonThreads, 0, s>>>(C, n, r, out, nullptr, nullptr, nullptr, nullptr,
+                                                               nullptr);
     else
-        spmv_cols_kernel<float><<<nb, kMonThreads, 0, s>>>(C, n, r, out);
+        cols_kernel<float, double><<<nb, kMonThreads, 0, s>>>(C, n, r, out, nullptr, nullptr, nullptr, nullptr,
+                                                              nullptr);
 }
 
 __global__ void __launch_bounds__(kMonThreads) dot_part_kernel(const double* a, const double* b, long long n,

@@ -183,6 +183,65 @@ void launch_iota_cols(const long long* col, long long nnz, int32_t* keys, int32_
     iota_cols_kernel<<<blocks, 256, 0, s>>>(col, nnz, keys, idx);
 }
 
+// ---- SELL-32 column layout (see CscDev): one warp per group of 32 columns
+__global__ void sell_len_kernel(const long long* __restrict__ col_ptr, long long n, int32_t* __restrict__ col_len,
+                                long long* __restrict__ grp_size) {
+    const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long groups = (n + 31) / 32;
+    if (g >= groups) return;
+    const long long j = g * 32 + lane;
+    const int len = j < n ? (int)(col_ptr[j + 1] - col_ptr[j]) : 0;
+    if (j < n) col_len[j] = len;
+    int mx = len;
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
+    if (lane == 0) grp_size[g] = 32ll * mx;
+}
+void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s) {
+    const long long groups = (n + 31) / 32;
+    sell_len_kernel<<<(unsigned)((groups * 32 + 255) / 256), 256, 0, s>>>(col_ptr, n, col_len, grp_size);
+}
+
+template <class V>
+__global__ void sell_scatter_kernel(const long long* __restrict__ col_ptr, const int32_t* __restrict__ src_row,
+                                    const V* __restrict__ src_val, const int32_t* __restrict__ col_len,
+                                    const long long* __restrict__ grp_off, long long n, int32_t* __restrict__ dst_row,
+                                    V* __restrict__ dst_val) {
+    const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long j = g * 32 + lane;
+    if (g >= (n + 31) / 32 || j >= n) return;
+    const long long src = col_ptr[j], dst = grp_off[g] + lane;
+    const int len = col_len[j];
+    for (int t = 0; t < len; ++t) {
+        dst_row[dst + 32ll * t] = src_row[src + t];
+        dst_val[dst + 32ll * t] = src_val[src + t];
+    }
+}
+void launch_sell_scatter(const long long* col_ptr, const int32_t* src_row, const void* src_val, const int32_t* col_len,
+                         const long long* grp_off, long long n, int precision, int32_t* dst_row, void* dst_val,
+                         cudaStream_t s) {
+    const long long groups = (n + 31) / 32;
+    const unsigned blocks = (unsigned)((groups * 32 + 255) / 256);
+    if (precision == P_F64)
+        sell_scatter_kernel<double><<<blocks, 256, 0, s>>>(col_ptr, src_row, static_cast<const double*>(src_val),
+                                                           col_len, grp_off, n, dst_row,
+                                                           static_cast<double*>(dst_val));
+    else
+        sell_scatter_kernel<float><<<blocks, 256, 0, s>>>(col_ptr, src_row, static_cast<const float*>(src_val),
+                                                          col_len, grp_off, n, dst_row, static_cast<float*>(dst_val));
+}
+
+size_t scan_temp_bytes(long long count) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const long long*)nullptr, (long long*)nullptr, (int)count);
+    return bytes;
+}
+void exclusive_scan(void* temp, size_t temp_bytes, const long long* in, long long* out, long long count,
+                    cudaStream_t s) {
+    cub::DeviceScan::ExclusiveSum(temp, temp_bytes, in, out, (int)count, s);
+}
+
 __global__ void set_rhs_kernel(Layout L, const double* __restrict__ b) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L.m; i += (long long)gridDim.x * blockDim.x) {
         const RowRef r = row_ref(L, i);

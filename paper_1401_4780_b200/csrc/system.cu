@@ -84,9 +84,12 @@ struct asyrk_system {
     uint2* row_info = nullptr;
     uint32_t stride16 = 0, uniform_len = 0;
     double* row_norm = nullptr;
-    long long* col_ptr = nullptr;
-    int32_t* csc_row = nullptr;
-    void* csc_val = nullptr;
+    size_t rec_bytes = 0;
+    int stage_bytes = 0;           // monitor pass-1 staging per warp
+    long long* grp_off = nullptr;  // SELL-32 columns (CscDev)
+    int32_t* col_len = nullptr;
+    int32_t* sell_row = nullptr;
+    void* sell_val = nullptr;
     AliasEntry* alias = nullptr;  // device alias table (async norm_proportional), built lazily
 
     // host copies for sequence generation
@@ -131,9 +134,10 @@ struct asyrk_system {
         L.uniform_len = uniform_len;
         L.m = m;
         L.n = n;
+        L.rec_bytes = rec_bytes;
         return L;
     }
-    CscDev csc() const { return CscDev{col_ptr, csc_row, csc_val}; }
+    CscDev csc() const { return CscDev{grp_off, col_len, sell_row, sell_val}; }
     size_t xbytes() const { return precision == P_F32 ? 4 : 8; }
 };
 
@@ -146,9 +150,10 @@ void free_all(asyrk_system* s) {
     F(s->rec);
     F(s->row_info);
     F(s->row_norm);
-    F(s->col_ptr);
-    F(s->csc_row);
-    F(s->csc_val);
+    F(s->grp_off);
+    F(s->col_len);
+    F(s->sell_row);
+    F(s->sell_val);
     F(s->alias);
     F(s->x);
     F(s->xd);
@@ -293,6 +298,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     }
     cudaStream_t st = s->stream;
     s->rec = dalloc<unsigned char>(rec_bytes);
+    s->rec_bytes = rec_bytes;
     if (!s->uniform) {
         s->row_info = dalloc<uint2>(info.size());
         CK(cudaMemcpyAsync(s->row_info, info.data(), info.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
@@ -325,15 +331,35 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     const size_t tb = csc_sort_temp_bytes(A->nnz);
     unsigned char* temp = dalloc<unsigned char>(tb);
     csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, st);
-    s->col_ptr = dalloc<long long>((size_t)A->n + 1);
-    s->csc_row = dalloc<int32_t>((size_t)A->nnz);
-    s->csc_val = dalloc<unsigned char>((size_t)A->nnz * vbytes);
-    launch_gather_csc(idx_s, row_id, d_val, A->nnz, precision, s->csc_row, s->csc_val, st);
-    launch_col_hist(keys_s, A->nnz, A->n, s->col_ptr, st);
+    long long* col_ptr = dalloc<long long>((size_t)A->n + 1);
+    int32_t* csc_row = dalloc<int32_t>((size_t)A->nnz);
+    unsigned char* csc_val = dalloc<unsigned char>((size_t)A->nnz * vbytes);
+    launch_gather_csc(idx_s, row_id, d_val, A->nnz, precision, csc_row, csc_val, st);
+    launch_col_hist(keys_s, A->nnz, A->n, col_ptr, st);
+    // SELL-32 columns for the monitor's coalesced thread-per-column pass
+    const long long groups = (A->n + 31) / 32;
+    s->col_len = dalloc<int32_t>((size_t)A->n);
+    s->grp_off = dalloc<long long>((size_t)groups + 1);
+    long long* grp_size = dalloc<long long>((size_t)groups + 1);
+    CK(cudaMemsetAsync(grp_size, 0, ((size_t)groups + 1) * 8, st));
+    launch_sell_len(col_ptr, A->n, s->col_len, grp_size, st);
+    const size_t stb = scan_temp_bytes(groups + 1);
+    unsigned char* stemp = dalloc<unsigned char>(stb);
+    exclusive_scan(stemp, stb, grp_size, s->grp_off, groups + 1, st);
+    long long sell_total = 0;
+    CK(cudaMemcpyAsync(&sell_total, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    s->sell_row = dalloc<int32_t>((size_t)sell_total);
+    s->sell_val = dalloc<unsigned char>((size_t)sell_total * vbytes);
+    CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, st));
+    launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row, s->sell_val,
+                        st);
+    s->stage_bytes = monitor_stage_bytes(s->layout(), s->max_len, vbytes);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
-                    (void*)idx_s, (void*)row_id, (void*)temp})
+                    (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
+                    (void*)grp_size, (void*)stemp})
         cudaFree(p);
 
     // solve buffers
@@ -393,6 +419,7 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.exact = exact ? 1 : 0;
     a.advance = advance;
     a.m_rows = s->m;
+    a.stage_bytes = s->stage_bytes;
     return a;
 }
 
@@ -695,7 +722,7 @@ asyrk_status power_impl(asyrk_system* s, double tol, int64_t max_iters, double* 
     double lam = 0.0;
     double h[2];
     for (int64_t it = 0; it < max_iters; ++it) {
-        launch_spmv_rows(s->layout(), s->precision, dv, dav, st);
+        launch_spmv_rows(s->layout(), s->precision, s->stage_bytes, dv, dav, st);
         launch_spmv_cols(s->csc(), s->precision, n, dav, dw, st);
         launch_dot(dw, dw, n, s->scratch, dots, st);
         launch_dot(dv, dw, n, s->scratch + 1024, dots + 1, st);
@@ -737,6 +764,13 @@ extern "C" {
 
 const char* asyrk_last_error(void) { return g_err.c_str(); }
 int asyrk_abi_version(void) { return ASYRK_ABI_VERSION; }
+
+asyrk_status asyrk_set_device(int32_t device) {
+    return guarded([&] {
+        CK(cudaSetDevice(device));
+        return ASYRK_OK;
+    });
+}
 
 asyrk_status asyrk_system_create(const asyrk_csr_view* A, const double* b, int32_t precision, void* stream,
                                  asyrk_system** out) {
@@ -789,7 +823,7 @@ asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y
     if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
         CK(cudaMemcpyAsync(sys->xd, x, (size_t)sys->n * 8, cudaMemcpyHostToDevice, sys->stream));
-        launch_spmv_rows(sys->layout(), sys->precision, sys->xd, sys->r, sys->stream);
+        launch_spmv_rows(sys->layout(), sys->precision, sys->stage_bytes, sys->xd, sys->r, sys->stream);
         CK(cudaMemcpyAsync(y, sys->r, (size_t)sys->m * 8, cudaMemcpyDeviceToHost, sys->stream));
         CK(cudaStreamSynchronize(sys->stream));
         CK(cudaGetLastError());

@@ -21,9 +21,18 @@
 //    exact number of row events (span * m, split evenly over the warps), so
 //    epochs are exact and the per-launch records are quiesced snapshots;
 //  * no CAS retry loop: the L2 atomic unit performs the add.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace ak {
+
+// 3 blocks x 8 warps per SM (<= 85 registers, no spills with two rows in
+// flight per warp): 24 worker warps x 2 rows resident per SM.
+#ifndef ASYRK_WORKER_MIN_BLOCKS
+#define ASYRK_WORKER_MIN_BLOCKS 3
+#endif
+constexpr int kWorkerBlocksPerSM = ASYRK_WORKER_MIN_BLOCKS;
 
 template <class V, int E>
 struct Frag {
@@ -89,8 +98,11 @@ __device__ __forceinline__ Draw draw_row(const WorkerArgs& a, long long warp, lo
     return d;
 }
 
-template <class V, class X, int E, bool FULL_ROW>
-__global__ void __launch_bounds__(256) worker_kernel(WorkerArgs a) {
+// R rows are in flight per warp: their gathers are issued back to back, then
+// their reductions interleave, then their reds — R-fold memory-level
+// parallelism per warp without more resident warps (R workers per warp).
+template <class V, class X, int E, int R, bool FULL_ROW>
+__global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerArgs a) {
     using T = X;  // arithmetic type of the projection (x's precision)
     const DevState* st = a.st;
     if (st->stop) return;
@@ -122,58 +134,88 @@ __global__ void __launch_bounds__(256) worker_kernel(WorkerArgs a) {
     Draw B0 = draw_row(a, warp, epoch, lane, slice_lo, slice_len);
     Draw B1 = nb > 1 ? draw_row(a, warp, epoch, 32 + lane, slice_lo, slice_len) : B0;
 
-    Frag<V, E> cur;
-    load_frag<V, E>(a.L, __shfl_sync(FULL, B0.row, 0), lane, cur);
-    uint32_t pick_cur = __shfl_sync(FULL, B0.pick, 0);
+    Frag<V, E> cur[R];
+    uint32_t pick_cur[R];
+    bool ok_cur[R];
+    {
+        const int nq0 = (int)min(32ll, count);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ok_cur[r] = r < nq0;
+            const long long row = __shfl_sync(FULL, B0.row, r);
+            pick_cur[r] = __shfl_sync(FULL, B0.pick, r);
+            if (ok_cur[r]) load_frag<V, E>(a.L, row, lane, cur[r]);
+        }
+    }
 
     for (long long bi = 0; bi < nb; ++bi) {
         const int nq = (int)min(32ll, count - bi * 32);
-        for (int q = 0; q < nq; ++q) {
-            // ---- prefetch the next row's record (independent of x)
-            Frag<V, E> nxt;
-            uint32_t pick_nxt = 0;
-            const bool in_batch = q + 1 < nq;
-            if (in_batch || bi + 1 < nb) {
-                const long long nrow = __shfl_sync(FULL, in_batch ? B0.row : B1.row, in_batch ? q + 1 : 0);
-                pick_nxt = __shfl_sync(FULL, in_batch ? B0.pick : B1.pick, in_batch ? q + 1 : 0);
-                load_frag<V, E>(a.L, nrow, lane, nxt);
+        const int nq_next = bi + 1 < nb ? (int)min(32ll, count - (bi + 1) * 32) : 0;
+        for (int q0 = 0; q0 < nq; q0 += R) {
+            // ---- prefetch the next R rows' records (independent of x)
+            Frag<V, E> nxt[R];
+            uint32_t pick_nxt[R];
+            bool ok_nxt[R];
+            const bool in_batch = q0 + R < nq;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int qn = in_batch ? q0 + R + r : r;
+                ok_nxt[r] = in_batch ? (q0 + R + r < nq) : (r < nq_next);
+                const long long nrow = __shfl_sync(FULL, in_batch ? B0.row : B1.row, qn & 31);
+                pick_nxt[r] = __shfl_sync(FULL, in_batch ? B0.pick : B1.pick, qn & 31);
+                if (ok_nxt[r]) load_frag<V, E>(a.L, nrow, lane, nxt[r]);
             }
 
-            // ---- stale residual a_i^T x - b_i (relaxed, L1-bypassing reads)
-            T acc = T(0);
+            // ---- stale residuals a_i^T x - b_i (relaxed, L1-bypassing reads)
+            T acc[R];
 #pragma unroll
-            for (int e = 0; e < E; ++e)
-                if (cur.c[e] >= 0) acc += (T)cur.v[e] * (T)ld_x(x + cur.c[e]);
-            acc = warp_sum(acc);
-            const T res = acc - (T)cur.b;
-
-            if (FULL_ROW) {
-                // x -= gamma * res / ||a_i||^2 * a_i   (parallel.cpp:318-331)
-                const T c = gamma * res * (T)cur.inv;
+            for (int r = 0; r < R; ++r) {
+                acc[r] = T(0);
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if (cur.c[e] >= 0) {
-                        const T d = -c * (T)cur.v[e];
-                        atomicAdd(x + cur.c[e], d);
-                        if (shadow) atomicAdd(shadow + cur.c[e], d);
-                    }
-                }
-                incr += (unsigned long long)cur.len;
-            } else {
-                // one component t ~ U(supp a_i): x_t += -gamma*theta*a_it*res  (parallel.cpp:332-346)
-                const int t = (int)__umulhi(pick_cur, (uint32_t)cur.len);
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if (lane + 32 * e == t) {
-                        const T d = -gamma * (T)cur.len * (T)cur.v[e] * res;
-                        atomicAdd(x + cur.c[e], d);
-                        if (shadow) atomicAdd(shadow + cur.c[e], d);
-                    }
-                }
-                incr += 1;
+                for (int e = 0; e < E; ++e)
+                    if (ok_cur[r] && cur[r].c[e] >= 0) acc[r] += (T)cur[r].v[e] * (T)ld_x(x + cur[r].c[e]);
             }
-            cur = nxt;
-            pick_cur = pick_nxt;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] += __shfl_xor_sync(FULL, acc[r], o);
+
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!ok_cur[r]) continue;
+                const T res = acc[r] - (T)cur[r].b;
+                if (FULL_ROW) {
+                    // x -= gamma * res / ||a_i||^2 * a_i   (parallel.cpp:318-331)
+                    const T c = gamma * res * (T)cur[r].inv;
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        if (cur[r].c[e] >= 0) {
+                            const T d = -c * (T)cur[r].v[e];
+                            atomicAdd(x + cur[r].c[e], d);
+                            if (shadow) atomicAdd(shadow + cur[r].c[e], d);
+                        }
+                    }
+                    incr += (unsigned long long)cur[r].len;
+                } else {
+                    // one component t ~ U(supp a_i): x_t += -gamma*theta*a_it*res  (parallel.cpp:332-346)
+                    const int t = (int)__umulhi(pick_cur[r], (uint32_t)cur[r].len);
+#pragma unroll
+                    for (int e = 0; e < E; ++e) {
+                        if (lane + 32 * e == t) {
+                            const T d = -gamma * (T)cur[r].len * (T)cur[r].v[e] * res;
+                            atomicAdd(x + cur[r].c[e], d);
+                            if (shadow) atomicAdd(shadow + cur[r].c[e], d);
+                        }
+                    }
+                    incr += 1;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                cur[r] = nxt[r];
+                pick_cur[r] = pick_nxt[r];
+                ok_cur[r] = ok_nxt[r];
+            }
         }
         B0 = B1;
         if (bi + 2 < nb) B1 = draw_row(a, warp, epoch, (bi + 2) * 32 + lane, slice_lo, slice_len);
@@ -251,29 +293,35 @@ int worker_elems_per_lane(uint32_t max_len) {
     return 0;
 }
 
-template <class V, class X>
-static const void* pick_kernel(int E, int full_row) {
-    if (full_row) {
-        switch (E) {
-            case 1: return (const void*)worker_kernel<V, X, 1, true>;
-            case 2: return (const void*)worker_kernel<V, X, 2, true>;
-            case 4: return (const void*)worker_kernel<V, X, 4, true>;
-            default: return (const void*)worker_kernel_long<V, X, true>;
-        }
-    }
+template <class V, class X, bool F>
+static const void* pick_kernel_r(int E, int R) {
     switch (E) {
-        case 1: return (const void*)worker_kernel<V, X, 1, false>;
-        case 2: return (const void*)worker_kernel<V, X, 2, false>;
-        case 4: return (const void*)worker_kernel<V, X, 4, false>;
-        default: return (const void*)worker_kernel_long<V, X, false>;
+        case 1: return R == 2 ? (const void*)worker_kernel<V, X, 1, 2, F> : (const void*)worker_kernel<V, X, 1, 1, F>;
+        case 2: return R == 2 ? (const void*)worker_kernel<V, X, 2, 2, F> : (const void*)worker_kernel<V, X, 2, 1, F>;
+        case 4: return (const void*)worker_kernel<V, X, 4, 1, F>;
+        default: return (const void*)worker_kernel_long<V, X, F>;
     }
+}
+template <class V, class X>
+static const void* pick_kernel(int E, int full_row, int R) {
+    return full_row ? pick_kernel_r<V, X, true>(E, R) : pick_kernel_r<V, X, false>(E, R);
+}
+
+static int rows_per_warp() {
+    static int r = -1;
+    if (r < 0) {
+        const char* e = getenv("ASYRK_ROWS_PER_WARP");
+        r = (e && atoi(e) == 1) ? 1 : 2;
+    }
+    return r;
 }
 
 static const void* kernel_for(int precision, int E, int full_row) {
+    const int R = rows_per_warp();
     switch (precision) {
-        case P_F32: return pick_kernel<float, float>(E, full_row);
-        case P_F32X64: return pick_kernel<float, double>(E, full_row);
-        default: return pick_kernel<double, double>(E, full_row);
+        case P_F32: return pick_kernel<float, float>(E, full_row, R);
+        case P_F32X64: return pick_kernel<float, double>(E, full_row, R);
+        default: return pick_kernel<double, double>(E, full_row, R);
     }
 }
 
