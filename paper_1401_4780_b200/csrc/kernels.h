@@ -74,15 +74,15 @@ struct MonitorArgs {
     DevState* st;
     int* host_flag;               // mapped pinned: stop seen by the host
     int exact;                    // 1: reference summation order (bitwise)
-    int stage_bytes;              // pass-1 staged record bytes per warp
+    CscDev rows;                  // SELL-32 rows of A (pass 1)
+    const double* b;              // m
     int advance;                  // 0: initial record, 1: after a chunk
     long long m_rows;
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 
 // ---- K4: power iteration building blocks (stats.cpp:15-50)
-void launch_spmv_rows(const Layout& L, int precision, int stage, const double* v, double* out, cudaStream_t s);
-int monitor_stage_bytes(const Layout& L, uint32_t max_len, int vbytes);
+void launch_spmv_rows(const CscDev& R, int precision, long long m, const double* v, double* out, cudaStream_t s);
 // SELL-32 columns from a column-sorted CSC: lengths + group sizes, then scatter
 void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s);
 void launch_sell_scatter(const long long* col_ptr, const int32_t* src_row, const void* src_val, const int32_t* col_len,

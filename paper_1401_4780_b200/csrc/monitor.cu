@@ -16,19 +16,17 @@
 // partials: deterministic run to run, within a few ulps of the reference.
 //
 // One lane per row / column keeps the serial order without any shuffle
-// chain; coalescing comes from the layouts: pass 1 stages 32 consecutive
-// row records (contiguous bytes) into shared memory with 16-byte loads;
-// pass 2 reads the SELL-32 column layout (entry t of the 32 columns of a
-// group stored contiguously, layout.cuh), so a warp's loads are contiguous.
-// x and r are read through the read-only path: the kernels run quiesced
-// (L1 is invalidated at every launch), unlike the workers.
+// chain; coalescing comes from the layouts: both passes read SELL-32 copies
+// of A (entry t of the 32 rows / columns of a group stored contiguously,
+// kernels.h CscDev), so every load of a warp is contiguous, and each lane
+// keeps 8 independent gathers in flight. x and r are read through the
+// read-only path: the kernels run quiesced (L1 is invalidated at every
+// launch), unlike the workers.
 #include "kernels.h"
 
 namespace ak {
 
 constexpr int kMonThreads = 256;
-constexpr int kRowWarps = 8;            // warps per block, pass 1
-constexpr int kStageMax = 16384;        // staged record bytes per warp
 
 static int sm_count() {
     static int sms = 0;
@@ -40,88 +38,59 @@ static int sm_count() {
     return sms;
 }
 
-__device__ __forceinline__ size_t row_off(const Layout& L, long long i) {
-    if (L.row_info == nullptr) return (size_t)i * ((size_t)L.stride16 * 16u);
-    return i < L.m ? (size_t)__ldg(L.row_info + i).x * 16u : L.rec_bytes;
-}
 
 template <class X>
 __device__ __forceinline__ double ldro(const X* p) {
     return (double)__ldg(p);
 }
 
-// Serial storage-order dot of one row: s = 0; s += v_k * x[c_k]  (csr.cpp:65-70)
+// Pass 1 / SpMV rows over the SELL-32 row copy: lane l of group g owns row
+// 32g + l and adds v_k * x[c_k] in storage order starting from 0.0 — the
+// reference's serial row_dot (csr.cpp:65-70) — with every load of a warp
+// contiguous and 8 independent gathers in flight per lane.
+// out[i] = a_i^T x (- b_i when b); part: r^2 block partials or null.
 template <class V, class X>
-__device__ __forceinline__ double row_dot_serial(const unsigned char* base, int len, const X* __restrict__ x) {
-    const V* vals = reinterpret_cast<const V*>(base + 16);
-    const int32_t* cols = reinterpret_cast<const int32_t*>(base + 16 + (size_t)len * sizeof(V));
-    double s = 0.0;
-    int k = 0;
-    for (; k + 8 <= len; k += 8) {  // 8 independent gathers in flight per lane, then ordered adds
-        double xv[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = ldro(x + cols[k + u]);
-#pragma unroll
-        for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn((double)vals[k + u], xv[u]));
-    }
-    for (; k < len; ++k) s = __dadd_rn(s, __dmul_rn((double)vals[k], ldro(x + cols[k])));
-    return s;
-}
-
-// Pass 1 / SpMV rows. out[i] = a_i^T x (- b_i when sub_b). part: r^2 block partials or null.
-template <class V, class X>
-__global__ void __launch_bounds__(32 * kRowWarps) rows_kernel(Layout L, const X* __restrict__ x, double* out,
-                                                             double* part, int stage_bytes, int sub_b,
-                                                             const DevState* st) {
+__global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m, const X* __restrict__ x,
+                                                          const double* __restrict__ b, double* out, double* part,
+                                                          const DevState* st) {
     if (st && st->stop) return;
-    extern __shared__ __align__(16) unsigned char stage_all[];
-    __shared__ double red[kRowWarps];
+    __shared__ double red[kMonThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned char* stage = stage_all + (size_t)wib * stage_bytes;
-    const long long tiles = (L.m + 31) / 32;
-    const long long gw = (long long)blockIdx.x * kRowWarps + wib, nw = (long long)gridDim.x * kRowWarps;
-    double mine = 0.0;
-    for (long long t = gw; t < tiles; t += nw) {
-        const long long r0 = t * 32;
-        const int nr = (int)min(32ll, L.m - r0);
-        const size_t start = row_off(L, r0), end = row_off(L, r0 + nr);
-        const bool staged = end - start <= (size_t)stage_bytes;
-        if (staged) {
-            const uint4* src = reinterpret_cast<const uint4*>(L.rec + start);
-            uint4* dst = reinterpret_cast<uint4*>(stage);
-            const int n16 = (int)((end - start) / 16);
-            for (int o = lane; o < n16; o += 32) dst[o] = __ldg(src + o);
-        }
-        __syncwarp();
-        if (lane < nr) {
-            const long long i = r0 + lane;
-            const size_t off = row_off(L, i);
-            const int len = L.row_info ? (int)__ldg(L.row_info + i).y : (int)L.uniform_len;
-            // two call sites so each pointer keeps its address space (LDS vs LDG, not generic LD)
-            double s, bi;
-            if (staged) {
-                const unsigned char* base = stage + (off - start);
-                s = row_dot_serial<V, X>(base, len, x);
-                bi = *reinterpret_cast<const double*>(base);
-            } else {
-                const unsigned char* base = L.rec + off;
-                s = row_dot_serial<V, X>(base, len, x);
-                bi = __ldg(reinterpret_cast<const double*>(base));
+    const long long i = (long long)blockIdx.x * kMonThreads + threadIdx.x;
+    double r2 = 0.0;
+    if (i < m) {
+        const int len = __ldg(R.col_len + i);
+        const long long base = __ldg(R.grp_off + (i >> 5)) + lane;
+        const V* rv = static_cast<const V*>(R.val);
+        double s = 0.0;
+        int t = 0;
+        for (; t + 8 <= len; t += 8) {
+            const long long e = base + 32ll * t;
+            double xv[8], av[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                xv[u] = ldro(x + __ldg(R.row + e + 32 * u));
+                av[u] = (double)__ldg(rv + e + 32 * u);
             }
-            if (sub_b) s = __dsub_rn(s, bi);
-            out[i] = s;
-            mine += s * s;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(av[u], xv[u]));
         }
-        __syncwarp();
+        for (; t < len; ++t) {
+            const long long e = base + 32ll * t;
+            s = __dadd_rn(s, __dmul_rn((double)__ldg(rv + e), ldro(x + __ldg(R.row + e))));
+        }
+        if (b) s = __dsub_rn(s, b[i]);
+        out[i] = s;
+        r2 = s * s;
     }
     if (!part) return;
-    mine = warp_sum(mine);
-    if (lane == 0) red[wib] = mine;
+    r2 = warp_sum(r2);
+    if (lane == 0) red[wib] = r2;
     __syncthreads();
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < kRowWarps; ++w) t += red[w];
-        part[blockIdx.x] = t;
+        double tot = 0.0;
+        for (int w = 0; w < kMonThreads / 32; ++w) tot += red[w];
+        part[blockIdx.x] = tot;
     }
 }
 
@@ -265,44 +234,15 @@ __global__ void __launch_bounds__(kMonThreads) finalize_fast_kernel(MonitorArgs 
 }
 
 // ---- launch geometry
-int monitor_stage_bytes(const Layout& L, uint32_t max_len, int vbytes) {
-    const size_t rec = (size_t)rec_size16(max_len, vbytes) * 16u;
-    size_t s = 32 * rec;
-    if (s > (size_t)kStageMax) s = kStageMax;
-    return (int)((s + 15) / 16 * 16);
-}
-
-template <class V, class X>
-static void rows_launch(const Layout& L, const X* x, double* out, double* part, int stage, int sub_b,
-                        const DevState* st, int& nblocks, cudaStream_t s) {
-    const size_t smem = (size_t)stage * kRowWarps;
-    static size_t configured = 0;
-    if (smem > 48 * 1024 && smem > configured) {
-        cudaFuncSetAttribute((const void*)rows_kernel<V, X>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(kRowWarps * kStageMax));
-        configured = (size_t)kRowWarps * kStageMax;
-    }
-    const long long tiles = (L.m + 31) / 32;
-    long long want = (tiles + kRowWarps - 1) / kRowWarps;
-    const long long cap = (long long)sm_count() * 4;
-    nblocks = (int)(want < cap ? want : cap);
-    rows_kernel<V, X><<<nblocks, 32 * kRowWarps, smem, s>>>(L, x, out, part, stage, sub_b, st);
-}
-
-int monitor_row_blocks(long long m) {
-    const long long tiles = (m + 31) / 32;
-    const long long want = (tiles + kRowWarps - 1) / kRowWarps;
-    const long long cap = (long long)sm_count() * 4;
-    return (int)(want < cap ? want : cap);
-}
+int monitor_row_blocks(long long m) { return (int)((m + kMonThreads - 1) / kMonThreads); }
 int monitor_col_blocks(long long n) { return (int)((n + kMonThreads - 1) / kMonThreads); }
 
 template <class V, class X>
 static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
-    int nbr = 0;
+    const int nbr = monitor_row_blocks(a.L.m);
     const int nbc = monitor_col_blocks(a.L.n);
     const X* x = static_cast<const X*>(a.x);
-    rows_launch<V, X>(a.L, x, a.r, a.exact ? nullptr : a.part, a.stage_bytes, 1, a.st, nbr, s);
+    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, a.st);
     cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.exact ? a.g : nullptr,
                                                   a.exact ? nullptr : a.part + nbr,
                                                   a.exact ? nullptr : a.part + nbr + nbc, x, a.x_star, a.st);
@@ -322,12 +262,12 @@ void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s) {
 
 // ---- power iteration pieces (ref/src/stats.cpp:15-50): y = A v and
 // w = A^T y in the reference's order (CsrMatrix::multiply / multiply_transpose).
-void launch_spmv_rows(const Layout& L, int precision, int stage, const double* v, double* out, cudaStream_t s) {
-    int nb = 0;
+void launch_spmv_rows(const CscDev& R, int precision, long long m, const double* v, double* out, cudaStream_t s) {
+    const int nb = monitor_row_blocks(m);
     if (precision == P_F64)
-        rows_launch<double, double>(L, v, out, nullptr, stage, 0, nullptr, nb, s);
+        rows_kernel<double, double><<<nb, kMonThreads, 0, s>>>(R, m, v, nullptr, out, nullptr, nullptr);
     else
-        rows_launch<float, double>(L, v, out, nullptr, stage, 0, nullptr, nb, s);
+        rows_kernel<float, double><<<nb, kMonThreads, 0, s>>>(R, m, v, nullptr, out, nullptr, nullptr);
 }
 void launch_spmv_cols(const CscDev& C, int precision, long long n, const double* r, double* out, cudaStream_t s) {
     const unsigned nb = (unsigned)((n + kMonThreads - 1) / kMonThreads);

@@ -203,33 +203,34 @@ void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, lo
 }
 
 template <class V>
-__global__ void sell_scatter_kernel(const long long* __restrict__ col_ptr, const int32_t* __restrict__ src_row,
-                                    const V* __restrict__ src_val, const int32_t* __restrict__ col_len,
-                                    const long long* __restrict__ grp_off, long long n, int32_t* __restrict__ dst_row,
+__global__ void sell_scatter_kernel(const long long* __restrict__ ptr, const int32_t* __restrict__ src_idx,
+                                    const double* __restrict__ src_val, const int32_t* __restrict__ len_arr,
+                                    const long long* __restrict__ grp_off, long long n, int32_t* __restrict__ dst_idx,
                                     V* __restrict__ dst_val) {
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const long long j = g * 32 + lane;
     if (g >= (n + 31) / 32 || j >= n) return;
-    const long long src = col_ptr[j], dst = grp_off[g] + lane;
-    const int len = col_len[j];
+    const long long src = ptr[j], dst = grp_off[g] + lane;
+    const int len = len_arr[j];
     for (int t = 0; t < len; ++t) {
-        dst_row[dst + 32ll * t] = src_row[src + t];
-        dst_val[dst + 32ll * t] = src_val[src + t];
+        dst_idx[dst + 32ll * t] = src_idx[src + t];
+        dst_val[dst + 32ll * t] = (V)src_val[src + t];
     }
 }
-void launch_sell_scatter(const long long* col_ptr, const int32_t* src_row, const void* src_val, const int32_t* col_len,
-                         const long long* grp_off, long long n, int precision, int32_t* dst_row, void* dst_val,
+// src_val is fp64 (the reference's values); dst_val gets the device precision
+void launch_sell_scatter(const long long* ptr, const int32_t* src_idx, const void* src_val, const int32_t* len_arr,
+                         const long long* grp_off, long long n, int precision, int32_t* dst_idx, void* dst_val,
                          cudaStream_t s) {
     const long long groups = (n + 31) / 32;
     const unsigned blocks = (unsigned)((groups * 32 + 255) / 256);
+    const double* sv = static_cast<const double*>(src_val);
     if (precision == P_F64)
-        sell_scatter_kernel<double><<<blocks, 256, 0, s>>>(col_ptr, src_row, static_cast<const double*>(src_val),
-                                                           col_len, grp_off, n, dst_row,
+        sell_scatter_kernel<double><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, dst_idx,
                                                            static_cast<double*>(dst_val));
     else
-        sell_scatter_kernel<float><<<blocks, 256, 0, s>>>(col_ptr, src_row, static_cast<const float*>(src_val),
-                                                          col_len, grp_off, n, dst_row, static_cast<float*>(dst_val));
+        sell_scatter_kernel<float><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, dst_idx,
+                                                          static_cast<float*>(dst_val));
 }
 
 size_t scan_temp_bytes(long long count) {

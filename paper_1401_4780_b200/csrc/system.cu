@@ -85,11 +85,15 @@ struct asyrk_system {
     uint32_t stride16 = 0, uniform_len = 0;
     double* row_norm = nullptr;
     size_t rec_bytes = 0;
-    int stage_bytes = 0;           // monitor pass-1 staging per warp
     long long* grp_off = nullptr;  // SELL-32 columns (CscDev)
     int32_t* col_len = nullptr;
     int32_t* sell_row = nullptr;
     void* sell_val = nullptr;
+    long long* rgrp_off = nullptr;  // SELL-32 rows (monitor pass 1)
+    int32_t* row_len = nullptr;
+    int32_t* rsell_col = nullptr;
+    void* rsell_val = nullptr;
+    double* b = nullptr;            // right-hand side (also in the record headers)
     AliasEntry* alias = nullptr;  // device alias table (async norm_proportional), built lazily
 
     // host copies for sequence generation
@@ -138,6 +142,7 @@ struct asyrk_system {
         return L;
     }
     CscDev csc() const { return CscDev{grp_off, col_len, sell_row, sell_val}; }
+    CscDev rsell() const { return CscDev{rgrp_off, row_len, rsell_col, rsell_val}; }
     size_t xbytes() const { return precision == P_F32 ? 4 : 8; }
 };
 
@@ -154,6 +159,11 @@ void free_all(asyrk_system* s) {
     F(s->col_len);
     F(s->sell_row);
     F(s->sell_val);
+    F(s->rgrp_off);
+    F(s->row_len);
+    F(s->rsell_col);
+    F(s->rsell_val);
+    F(s->b);
     F(s->alias);
     F(s->x);
     F(s->xd);
@@ -333,8 +343,8 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, st);
     long long* col_ptr = dalloc<long long>((size_t)A->n + 1);
     int32_t* csc_row = dalloc<int32_t>((size_t)A->nnz);
-    unsigned char* csc_val = dalloc<unsigned char>((size_t)A->nnz * vbytes);
-    launch_gather_csc(idx_s, row_id, d_val, A->nnz, precision, csc_row, csc_val, st);
+    double* csc_val = dalloc<double>((size_t)A->nnz);
+    launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, st);
     launch_col_hist(keys_s, A->nnz, A->n, col_ptr, st);
     // SELL-32 columns for the monitor's coalesced thread-per-column pass
     const long long groups = (A->n + 31) / 32;
@@ -354,12 +364,30 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, st));
     launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row, s->sell_val,
                         st);
-    s->stage_bytes = monitor_stage_bytes(s->layout(), s->max_len, vbytes);
+    // SELL-32 rows for the monitor's coalesced thread-per-row pass (r = Ax - b)
+    const long long rgroups = (A->m + 31) / 32;
+    s->row_len = dalloc<int32_t>((size_t)A->m);
+    s->rgrp_off = dalloc<long long>((size_t)rgroups + 1);
+    long long* rgrp_size = dalloc<long long>((size_t)rgroups + 1);
+    CK(cudaMemsetAsync(rgrp_size, 0, ((size_t)rgroups + 1) * 8, st));
+    launch_sell_len(d_rp, A->m, s->row_len, rgrp_size, st);
+    const size_t rstb = scan_temp_bytes(rgroups + 1);
+    unsigned char* rstemp = dalloc<unsigned char>(rstb);
+    exclusive_scan(rstemp, rstb, rgrp_size, s->rgrp_off, rgroups + 1, st);
+    long long rsell_total = 0;
+    CK(cudaMemcpyAsync(&rsell_total, s->rgrp_off + rgroups, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    s->rsell_col = dalloc<int32_t>((size_t)rsell_total);
+    s->rsell_val = dalloc<unsigned char>((size_t)rsell_total * vbytes);
+    CK(cudaMemsetAsync(s->rsell_col, 0, (size_t)std::max<long long>(rsell_total, 1) * 4, st));
+    launch_sell_scatter(d_rp, keys, d_val, s->row_len, s->rgrp_off, A->m, precision, s->rsell_col, s->rsell_val, st);
+    s->b = dalloc<double>((size_t)A->m);
+    CK(cudaMemcpyAsync(s->b, d_b, (size_t)A->m * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
                     (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
-                    (void*)grp_size, (void*)stemp})
+                    (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
         cudaFree(p);
 
     // solve buffers
@@ -419,7 +447,8 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.exact = exact ? 1 : 0;
     a.advance = advance;
     a.m_rows = s->m;
-    a.stage_bytes = s->stage_bytes;
+    a.rows = s->rsell();
+    a.b = s->b;
     return a;
 }
 
@@ -722,7 +751,7 @@ asyrk_status power_impl(asyrk_system* s, double tol, int64_t max_iters, double* 
     double lam = 0.0;
     double h[2];
     for (int64_t it = 0; it < max_iters; ++it) {
-        launch_spmv_rows(s->layout(), s->precision, s->stage_bytes, dv, dav, st);
+        launch_spmv_rows(s->rsell(), s->precision, s->m, dv, dav, st);
         launch_spmv_cols(s->csc(), s->precision, n, dav, dw, st);
         launch_dot(dw, dw, n, s->scratch, dots, st);
         launch_dot(dv, dw, n, s->scratch + 1024, dots + 1, st);
@@ -813,6 +842,7 @@ asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b) {
     return guarded([&] {
         CK(cudaMemcpyAsync(sys->r, b, (size_t)sys->m * 8, cudaMemcpyHostToDevice, sys->stream));
         launch_set_rhs(sys->layout(), sys->r, sys->stream);
+        CK(cudaMemcpyAsync(sys->b, sys->r, (size_t)sys->m * 8, cudaMemcpyDeviceToDevice, sys->stream));
         CK(cudaStreamSynchronize(sys->stream));
         CK(cudaGetLastError());
         return ASYRK_OK;
@@ -823,7 +853,7 @@ asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y
     if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
         CK(cudaMemcpyAsync(sys->xd, x, (size_t)sys->n * 8, cudaMemcpyHostToDevice, sys->stream));
-        launch_spmv_rows(sys->layout(), sys->precision, sys->stage_bytes, sys->xd, sys->r, sys->stream);
+        launch_spmv_rows(sys->rsell(), sys->precision, sys->m, sys->xd, sys->r, sys->stream);
         CK(cudaMemcpyAsync(y, sys->r, (size_t)sys->m * 8, cudaMemcpyDeviceToHost, sys->stream));
         CK(cudaStreamSynchronize(sys->stream));
         CK(cudaGetLastError());
