@@ -295,7 +295,8 @@ def run_gpu(args):
         tot = torch.tensor([float(e2e_proj)], device="cuda", dtype=torch.float64)
         dist.all_reduce(tot)
         e2e_proj = float(tot.item())
-    h2d = 8 * (A.m + 1) + 16 * A.nnz + 8 * A.m + 8 * A.m  # row_ptr, col_idx+values, row_norm, b
+    # row_ptr (int64), col_idx (narrowed to int32 while staging), values (fp64), row_norm, b
+    h2d = 8 * (A.m + 1) + 12 * A.nnz + 8 * A.m + 8 * A.m
     d2h = 8 * A.n + 48 * (max(epochs) + 2)  # final_x + trace records
 
     out = None

@@ -97,7 +97,7 @@ void launch_dot(const double* a, const double* b, long long n, double* scratch, 
 void launch_power_update(double* v, const double* w, const double* wn_dot, long long n, cudaStream_t s);
 
 // ---- K0: packing
-void launch_pack_records(const long long* row_ptr, const long long* col, const double* val,
+void launch_pack_records(const long long* row_ptr, const int32_t* col, const double* val,
                          const double* row_norm, const double* b, long long m, const uint2* row_info,
                          uint32_t stride16, uint32_t uniform_len, int precision, unsigned char* rec,
                          cudaStream_t s);
@@ -119,7 +119,7 @@ namespace ak {
 size_t csc_sort_temp_bytes(long long nnz);
 void csc_sort(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* keys_out, const int32_t* vals_in,
               int32_t* vals_out, long long nnz, int end_bit, cudaStream_t s);
-void launch_iota_cols(const long long* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s);
+void launch_iota_cols(const int32_t* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s);
 int monitor_row_blocks(long long m);
 int monitor_col_blocks(long long n);
 void launch_set_rhs(const Layout& L, const double* b, cudaStream_t s);

@@ -11,7 +11,7 @@ namespace ak {
 
 // one warp per row: header {b, 1/nrm^2}, values (converted), int32 columns
 template <class V>
-__global__ void pack_records_kernel(const long long* __restrict__ row_ptr, const long long* __restrict__ col,
+__global__ void pack_records_kernel(const long long* __restrict__ row_ptr, const int32_t* __restrict__ col,
                                     const double* __restrict__ val, const double* __restrict__ row_norm,
                                     const double* __restrict__ b, long long m, const uint2* __restrict__ row_info,
                                     uint32_t stride16, unsigned char* __restrict__ rec) {
@@ -37,7 +37,7 @@ __global__ void pack_records_kernel(const long long* __restrict__ row_ptr, const
     for (size_t p = used + lane; p < total; p += 32) base[p] = 0;
 }
 
-void launch_pack_records(const long long* row_ptr, const long long* col, const double* val, const double* row_norm,
+void launch_pack_records(const long long* row_ptr, const int32_t* col, const double* val, const double* row_norm,
                          const double* b, long long m, const uint2* row_info, uint32_t stride16, uint32_t, int precision,
                          unsigned char* rec, cudaStream_t s) {
     const unsigned blocks = (unsigned)((m * 32 + 255) / 256);
@@ -170,14 +170,14 @@ void csc_sort(void* temp, size_t temp_bytes, const int32_t* keys_in, int32_t* ke
     cub::DeviceRadixSort::SortPairs(temp, temp_bytes, keys_in, keys_out, vals_in, vals_out, (int)nnz, 0, end_bit, s);
 }
 
-__global__ void iota_cols_kernel(const long long* __restrict__ col, long long nnz, int32_t* __restrict__ keys,
+__global__ void iota_cols_kernel(const int32_t* __restrict__ col, long long nnz, int32_t* __restrict__ keys,
                                  int32_t* __restrict__ idx) {
     for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x) {
         keys[e] = (int32_t)col[e];
         idx[e] = (int32_t)e;
     }
 }
-void launch_iota_cols(const long long* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s) {
+void launch_iota_cols(const int32_t* col, long long nnz, int32_t* keys, int32_t* idx, cudaStream_t s) {
     if (nnz == 0) return;
     const unsigned blocks = (unsigned)std::min<long long>((nnz + 255) / 256, 148 * 32);
     iota_cols_kernel<<<blocks, 256, 0, s>>>(col, nnz, keys, idx);

@@ -1,0 +1,179 @@
+// Host runtime of the C ABI (runtime.h).
+#include "runtime.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+
+namespace ak {
+
+ThreadPool::ThreadPool(int n) {
+    for (int t = 1; t < n; ++t) {
+        workers_.emplace_back([this, t] {
+            long long seen = 0;
+            for (;;) {
+                const std::function<void(int)>* task;
+                {
+                    std::unique_lock<std::mutex> lk(mu_);
+                    cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                    if (stop_) return;
+                    seen = gen_;
+                    task = task_;
+                }
+                (*task)(t);
+                std::lock_guard<std::mutex> lk(mu_);
+                if (--pending_ == 0) done_cv_.notify_one();
+            }
+        });
+    }
+}
+
+ThreadPool::~ThreadPool() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+}
+
+void ThreadPool::run(const std::function<void(int)>& f) {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        task_ = &f;
+        pending_ = (int)workers_.size();
+        ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return pending_ == 0; });
+}
+
+static int stager_threads() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    return (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+}
+
+Stager::Stager() : pool_(stager_threads()) {
+    for (int k = 0; k < kSlots; ++k) {
+        if (cudaHostAlloc((void**)&slot_[k], kChunk, cudaHostAllocDefault) != cudaSuccess)
+            throw std::runtime_error("pinned staging allocation failed");
+        cudaEventCreateWithFlags(&ev_[k], cudaEventDisableTiming);
+    }
+}
+
+Stager& Stager::get() {
+    static Stager* s = new Stager();  // process lifetime (pinned memory freed at exit)
+    return *s;
+}
+
+// Fill pinned chunks with fill(dst_chunk, first_elem, n_elems, thread, nthreads)
+// and DMA them to dst; out_elem = bytes per staged element.
+template <class F>
+void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* dst, F&& fill) {
+    std::lock_guard<std::mutex> lk(mu_);
+    const size_t per_chunk = kChunk / out_elem;
+    const size_t total = out_bytes / out_elem;
+    for (size_t e0 = 0; e0 < total; e0 += per_chunk) {
+        const size_t ne = std::min(per_chunk, total - e0);
+        const int k = next_;
+        next_ = (next_ + 1) % kSlots;
+        cudaEventSynchronize(ev_[k]);  // slot's previous DMA done
+        unsigned char* slot = slot_[k];
+        const int nt = pool_.size();
+        std::function<void(int)> task = [&](int t) {
+            const size_t a = ne * t / nt, b = ne * (t + 1) / nt;
+            if (b > a) fill(slot + a * out_elem, e0 + a, b - a);
+        };
+        if (ne * out_elem >= (1u << 20))
+            pool_.run(task);
+        else
+            fill(slot, e0, ne);
+        if (cudaMemcpyAsync(dst + e0 * out_elem, slot, ne * out_elem, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            throw std::runtime_error("staged upload failed");
+        cudaEventRecord(ev_[k], s);
+    }
+}
+
+void Stager::upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    const char* sp = static_cast<const char*>(src);
+    pipeline(bytes, 1, s, static_cast<char*>(dst),
+             [sp](unsigned char* out, size_t first, size_t n) { std::memcpy(out, sp + first, n); });
+}
+
+void Stager::upload_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s) {
+    pipeline(count * 4, 4, s, reinterpret_cast<char*>(dst), [src](unsigned char* out, size_t first, size_t n) {
+        int32_t* o = reinterpret_cast<int32_t*>(out);
+        const int64_t* in = src + first;
+        for (size_t k = 0; k < n; ++k) o[k] = (int32_t)in[k];
+    });
+}
+
+static bool pool_debug() {
+    static int d = -1;
+    if (d < 0) d = getenv("ASYRK_DEBUG_POOL") ? 1 : 0;
+    return d == 1;
+}
+
+static bool no_pool() {
+    static int d = -1;
+    if (d < 0) d = getenv("ASYRK_NO_POOL") ? 1 : 0;
+    return d == 1;
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static int configured = -1;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured != dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        configured = dev;
+    }
+    const cudaError_t e = no_pool() ? cudaMalloc(p, bytes ? bytes : 1) : cudaMallocAsync(p, bytes ? bytes : 1, s);
+    if (getenv("ASYRK_DEBUG_POOL")) fprintf(stderr, "[pool] alloc %p %zu\n", *p, bytes);
+    return e;
+}
+
+cudaError_t pool_free(void* p, cudaStream_t s) {
+    if (pool_debug() && p) fprintf(stderr, "[pool] free  %p\n", p);
+    if (no_pool()) return p ? cudaFree(p) : cudaSuccess;
+    return p ? cudaFreeAsync(p, s) : cudaSuccess;
+}
+
+namespace {
+std::mutex g_flag_mu;
+int* g_flag_host = nullptr;
+int* g_flag_dev = nullptr;
+std::vector<int> g_flag_free;
+constexpr int kFlags = 1024;
+}  // namespace
+
+int* flag_acquire(int** dev_ptr) {
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    if (!g_flag_host) {
+        if (cudaHostAlloc((void**)&g_flag_host, kFlags * sizeof(int), cudaHostAllocMapped) != cudaSuccess)
+            return nullptr;
+        cudaHostGetDevicePointer((void**)&g_flag_dev, g_flag_host, 0);
+        for (int k = kFlags - 1; k >= 0; --k) g_flag_free.push_back(k);
+    }
+    if (g_flag_free.empty()) return nullptr;
+    const int k = g_flag_free.back();
+    g_flag_free.pop_back();
+    *dev_ptr = g_flag_dev + k;
+    return g_flag_host + k;
+}
+
+void flag_release(int* host_ptr) {
+    if (!host_ptr) return;
+    std::lock_guard<std::mutex> lk(g_flag_mu);
+    g_flag_free.push_back((int)(host_ptr - g_flag_host));
+}
+
+}  // namespace ak

@@ -19,6 +19,7 @@
 #include "../../include/asyrk_cuda.h"
 #include "host_seq.h"
 #include "kernels.h"
+#include "runtime.h"
 
 using namespace ak;
 
@@ -39,7 +40,8 @@ struct CudaFail {
     do {                                                                                               \
         cudaError_t e_ = (call);                                                                       \
         if (e_ != cudaSuccess) {                                                                       \
-            g_err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call;                     \
+            g_err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call " (system.cu:" +    \
+                    std::to_string(__LINE__) + ")";                                                    \
             throw CudaFail{e_ == cudaErrorMemoryAllocation ? ASYRK_E_TooLarge : ASYRK_E_ThreadSpawnFailure}; \
         }                                                                                              \
     } while (0)
@@ -57,13 +59,23 @@ asyrk_status guarded(F&& f) {
     }
 }
 
+// Device allocations are stream-ordered pool allocations on the system's
+// stream (runtime.h), set per entry point.
+thread_local cudaStream_t g_alloc_stream = nullptr;
+
 template <class T>
 T* dalloc(size_t count) {
     void* p = nullptr;
     if (count == 0) count = 1;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    CK(pool_alloc(&p, count * sizeof(T), g_alloc_stream));
     return static_cast<T*>(p);
 }
+
+struct AllocStream {
+    cudaStream_t prev;
+    explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
+    ~AllocStream() { g_alloc_stream = prev; }
+};
 
 constexpr int kLookahead = 4;      // chunks in flight beyond the last confirmed one
 constexpr int kTimedLaunches = 1024;  // worker launches timed with event pairs per solve
@@ -149,9 +161,8 @@ struct asyrk_system {
 namespace {
 
 void free_all(asyrk_system* s) {
-    auto F = [](void* p) {
-        if (p) cudaFree(p);
-    };
+    cudaStream_t fs = s->stream;
+    auto F = [fs](void* p) { pool_free(p, fs); };
     F(s->rec);
     F(s->row_info);
     F(s->row_norm);
@@ -177,7 +188,7 @@ void free_all(asyrk_system* s) {
     F(s->st);
     F(s->incr);
     F(s->scratch);
-    if (s->host_flag) cudaFreeHost(s->host_flag);
+    flag_release(s->host_flag);
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
         F(s->pick_dev[k]);
@@ -188,6 +199,7 @@ void free_all(asyrk_system* s) {
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     for (auto e : s->ev_w) cudaEventDestroy(e);
     for (auto e : s->ev_chunk) cudaEventDestroy(e);
+    if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -205,16 +217,19 @@ asyrk_status check_view(const asyrk_csr_view* A) {
 // Bind the per-solve buffers that depend on cap (records) lazily.
 void ensure_records(asyrk_system* s, long long cap) {
     if (cap <= s->rec_cap) return;
-    if (s->recs) cudaFree(s->recs);
+    AllocStream as(s->stream);
+    CK(cudaGetLastError());
+    CK(pool_free(s->recs, s->stream));
     s->recs = dalloc<DevRecord>((size_t)cap);
     s->rec_cap = cap;
 }
 
 void ensure_seq(asyrk_system* s, size_t count) {
     if (count <= s->seq_cap) return;
+    AllocStream as(s->stream);
     for (int k = 0; k <= kLookahead; ++k) {
-        if (s->seq_dev[k]) cudaFree(s->seq_dev[k]);
-        if (s->pick_dev[k]) cudaFree(s->pick_dev[k]);
+        pool_free(s->seq_dev[k], s->stream);
+        pool_free(s->pick_dev[k], s->stream);
         if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
         if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
         s->seq_dev[k] = dalloc<int32_t>(count);
@@ -225,21 +240,26 @@ void ensure_seq(asyrk_system* s, size_t count) {
     s->seq_cap = count;
 }
 
-void ensure_events(asyrk_system* s) {
+// Events are created on demand: `timed` pairs for the worker launches of the
+// coming solve (capped at kTimedLaunches), plus the chunk ring.
+void ensure_events(asyrk_system* s, long long timed = 0) {
     if (!s->ev_begin) {
         CK(cudaEventCreate(&s->ev_begin));
         CK(cudaEventCreate(&s->ev_end));
-    }
-    if (s->ev_w.empty()) {
-        s->ev_w.resize(2 * kTimedLaunches);
-        for (auto& e : s->ev_w) CK(cudaEventCreate(&e));
         s->ev_chunk.resize(kLookahead + 1);
         for (auto& e : s->ev_chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const size_t want = (size_t)(2 * std::min<long long>(timed, kTimedLaunches));
+    while (s->ev_w.size() < want) {
+        cudaEvent_t e;
+        CK(cudaEventCreate(&e));
+        s->ev_w.push_back(e);
     }
 }
 
 void ensure_alias_dev(asyrk_system* s) {
     if (s->alias) return;
+    AllocStream as(s->stream);
     if (!s->h_alias) {
         std::vector<double> w(s->h_norm.size());
         for (size_t i = 0; i < w.size(); ++i) w[i] = s->h_norm[i] * s->h_norm[i];
@@ -270,6 +290,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
         s->own_stream = true;
     }
+    AllocStream alloc_on(s->stream);
     const int vbytes = precision == P_F64 ? 8 : 4;
     // row lengths, layout
     s->h_len.resize((size_t)A->m);
@@ -315,15 +336,17 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     }
     // raw upload (the reference's int64/fp64 arrays), then pack on the device
     long long* d_rp = dalloc<long long>((size_t)A->m + 1);
-    long long* d_col = dalloc<long long>((size_t)A->nnz);
+    int32_t* d_col = dalloc<int32_t>((size_t)A->nnz);
     double* d_val = dalloc<double>((size_t)A->nnz);
     double* d_b = dalloc<double>((size_t)A->m);
     s->row_norm = dalloc<double>((size_t)A->m);
-    CK(cudaMemcpyAsync(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_col, A->col_idx, (size_t)A->nnz * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_val, A->values, (size_t)A->nnz * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s->row_norm, A->row_norm, (size_t)A->m * 8, cudaMemcpyHostToDevice, st));
-    if (b) CK(cudaMemcpyAsync(d_b, b, (size_t)A->m * 8, cudaMemcpyHostToDevice, st));
+    // pinned, multithreaded staging; int64 columns cross PCIe as int32 (runtime.h)
+    Stager& up = Stager::get();
+    up.upload(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, st);
+    up.upload_narrow(d_col, A->col_idx, (size_t)A->nnz, st);
+    up.upload(d_val, A->values, (size_t)A->nnz * 8, st);
+    up.upload(s->row_norm, A->row_norm, (size_t)A->m * 8, st);
+    if (b) up.upload(d_b, b, (size_t)A->m * 8, st);
     else CK(cudaMemsetAsync(d_b, 0, (size_t)A->m * 8, st));
     launch_pack_records(d_rp, d_col, d_val, s->row_norm, d_b, A->m, s->uniform ? nullptr : s->row_info, s->stride16,
                         s->uniform_len, precision, s->rec, st);
@@ -388,7 +411,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
                     (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
                     (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
-        cudaFree(p);
+        pool_free(p, st);
 
     // solve buffers
     s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
@@ -400,10 +423,11 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     s->st = dalloc<DevState>(1);
     s->incr = dalloc<unsigned long long>(1);
     s->scratch = dalloc<double>(4096);
-    CK(cudaHostAlloc((void**)&s->host_flag, sizeof(int), cudaHostAllocMapped));
-    CK(cudaHostGetDevicePointer((void**)&s->host_flag_dev, s->host_flag, 0));
+    s->host_flag = flag_acquire(&s->host_flag_dev);
+    if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
+    CK(cudaStreamSynchronize(st));
     *out = s.release();
     return ASYRK_OK;
 }
@@ -470,6 +494,7 @@ struct SolveSpec {
 asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
                        asyrk_instrument_out* instr) {
     cudaStream_t st = s->stream;
+    AllocStream alloc_on(st);
     const int prec = sp.det ? P_F64 : sp.precision;
     if (sp.det && s->precision != P_F64)
         return fail(ASYRK_E_InvalidArgument, "the deterministic path needs an fp64 system");
@@ -477,7 +502,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         return fail(ASYRK_E_InvalidArgument, "config precision differs from the system's");
     const long long max_chunks = sp.epochs > 0 ? (sp.epochs + sp.interval - 1) / sp.interval : 0;
     ensure_records(s, std::max<long long>(256, max_chunks + 2));
-    ensure_events(s);
+    ensure_events(s, max_chunks);
     s->stats = asyrk_solve_stats{};
 
     // x0, x_star
