@@ -323,6 +323,10 @@ def run_gpu(args):
                          "avg_launch_ms": avg_launch_ms, "peak_source": peak_kind,
                          "worker_share_of_step": w_ms / dev_ms},
             "worker_proj_per_s": proj / (w_ms * 1e-3),
+            # R_proj = min(BW_HBM / S_A, R_x); R_x = the x-side traffic alone
+            # (30 random L2 gathers -> warp reduce -> 30 random red.add.f64 per projection),
+            # measured here at the same warp count and x footprint
+            "x_roofline": x_roofline(W, proj / (w_ms * 1e-3)),
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
@@ -334,6 +338,18 @@ def run_gpu(args):
     if out is not None:
         print(json.dumps(out))
     return 0
+
+
+def x_roofline(W, worker_rate):
+    from paper_1401_4780_b200 import capi
+
+    rx = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 0) for _ in range(3))
+    peak, _ = measured_peak_hbm()
+    r_hbm = peak * 1e9 / 384.0  # A stream: 16 B header + 30 x (8 B value + 4 B column), record-padded
+    r_proj = min(r_hbm, rx)
+    return {"R_x_proj_per_s": rx, "R_hbm_proj_per_s": r_hbm, "R_proj": r_proj,
+            "achieved_proj_per_s": worker_rate, "frac": worker_rate / r_proj,
+            "mode": "dependent gather->reduce->red.add.f64, theta=30, n=100000"}
 
 
 def cpu_baseline(A, b):
