@@ -191,7 +191,8 @@ asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const
 typedef struct asyrk_system asyrk_system;
 
 /* Uploads A (+ b) and packs the device layout (row records, CSC, alias).
- * stream: a cudaStream_t or NULL for a library-owned stream. */
+ * stream: a cudaStream_t (cudaStreamLegacy = (void*)1 for the legacy default
+ * stream) or NULL for a library-owned stream. */
 asyrk_status asyrk_system_create(const asyrk_csr_view* A, const double* b, int32_t precision,
                                  void* stream, asyrk_system** out);
 asyrk_status asyrk_system_destroy(asyrk_system* sys);
@@ -212,6 +213,36 @@ asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
 /* Largest number of worker warps that are co-resident for this system. */
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
+
+/* ---- multi-right-hand-side AsyRK (BASELINE config 5) -------------------- *
+ * k right-hand sides share A and the row sequence: one row projection
+ * updates every RHS column (X n x k row-major fp32, B m x k). A GPU owns the
+ * column shard [c0, c1) (a power of two, 2..64 columns). The reference is
+ * single-RHS: its oracle is k independent solves.
+ *
+ * Multi-GPU protocol (one process per GPU; the collective is the caller's,
+ * e.g. NCCL all-reduce on the system's stream):
+ *   begin -> [all-reduce(norms, sum)] -> commit(0) ->
+ *   loop { step -> [all-reduce(norms, sum)] -> commit(1) -> stopped? } -> finish
+ * norms is a device double[3] = this shard's {||R||_F^2, ||A^T R||_F^2,
+ * ||X - X*||_F^2}; after the all-reduce every rank takes the same global stop
+ * decision (r_sq <= target_r_sq) on the device. */
+typedef struct asyrk_mrhs asyrk_mrhs;
+asyrk_status asyrk_mrhs_create(const asyrk_csr_view* A, const float* B, int64_t k_total, int64_t c0, int64_t c1,
+                               void* stream, asyrk_mrhs** out);
+asyrk_status asyrk_mrhs_destroy(asyrk_mrhs* h);
+/* X0 (n x k_total fp32) and Xstar (n x k_total fp64) may be NULL. */
+asyrk_status asyrk_mrhs_begin(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar);
+asyrk_status asyrk_mrhs_norms(asyrk_mrhs* h, double** dev_norms);
+asyrk_status asyrk_mrhs_commit(asyrk_mrhs* h, int32_t advance);
+asyrk_status asyrk_mrhs_step(asyrk_mrhs* h);
+asyrk_status asyrk_mrhs_stopped(asyrk_mrhs* h, int32_t* stopped);
+/* X_out: n x (c1 - c0) fp32, this shard's columns. */
+asyrk_status asyrk_mrhs_finish(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out);
+/* single-process convenience: begin + loop + finish (no collective) */
+asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
+                              asyrk_trace_out* trace, float* X_out);
+asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out);
 
 /* ---- measurement ------------------------------------------------------- */
 /* x-side roofline R_x: theta random gathers of an n-element

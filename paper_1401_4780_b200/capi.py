@@ -110,6 +110,18 @@ def lib():
         L.asyrk_power_iteration_lambda_max.argtypes = [C.POINTER(CsrView), C.c_double, C.c_int64, _f64p]
         L.asyrk_sweep_threads.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig), _i64p, C.c_int64,
                                           _f64p, _i64p, _f64p, _f64p]
+        _f32p = C.POINTER(C.c_float)
+        L.asyrk_mrhs_create.argtypes = [C.POINTER(CsrView), _f32p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p,
+                                        C.POINTER(sp)]
+        L.asyrk_mrhs_destroy.argtypes = [sp]
+        L.asyrk_mrhs_begin.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p]
+        L.asyrk_mrhs_norms.argtypes = [sp, C.POINTER(C.c_void_p)]
+        L.asyrk_mrhs_commit.argtypes = [sp, C.c_int32]
+        L.asyrk_mrhs_step.argtypes = [sp]
+        L.asyrk_mrhs_stopped.argtypes = [sp, _i32p]
+        L.asyrk_mrhs_finish.argtypes = [sp, C.POINTER(TraceOut), _f32p]
+        L.asyrk_mrhs_solve.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p]
+        L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_microbench_xside.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
                                              _f64p, _f64p]
         L.asyrk_generate_fixed_theta.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int32, C.c_double,
@@ -126,8 +138,87 @@ EXPORTED = [
     "asyrk_system_solve", "asyrk_system_rk_solve", "asyrk_system_residuals", "asyrk_system_set_rhs",
     "asyrk_system_multiply", "asyrk_system_multiply_transpose", "asyrk_system_power_iteration",
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
-    "asyrk_microbench_xside",
+    "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
+    "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
+    "asyrk_mrhs_last_stats",
 ]
+
+
+class MultiRHS:
+    """Device-resident multi-RHS shard (asyrk_mrhs_*): A replicated, columns [c0, c1) of B/X."""
+
+    def __init__(self, A: "HostCsr", B, c0, c1, stream=None):
+        B = np.ascontiguousarray(B, dtype=np.float32)
+        self.m, self.n = A.m, A.n
+        self.k_total = B.shape[1]
+        self.c0, self.c1 = c0, c1
+        h = C.c_void_p()
+        check(lib().asyrk_mrhs_create(C.byref(A.view()), B.ctypes.data_as(C.POINTER(C.c_float)), self.k_total, c0,
+                                      c1, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().asyrk_mrhs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def begin(self, X0=None, X_star=None, **cfg):
+        self._cfg = _run_config(**cfg)
+        self._x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
+        self._xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        check(lib().asyrk_mrhs_begin(self.h, C.byref(self._cfg),
+                                     self._x0.ctypes.data_as(C.POINTER(C.c_float)) if self._x0 is not None else None,
+                                     _ptr(self._xs, _f64p)))
+        self._cap = max(self._cfg.epochs, 0) // max(self._cfg.snapshot_interval, 1) + 2
+
+    def norms_ptr(self):
+        p = C.c_void_p()
+        check(lib().asyrk_mrhs_norms(self.h, C.byref(p)))
+        return p.value
+
+    def commit(self, advance):
+        check(lib().asyrk_mrhs_commit(self.h, 1 if advance else 0))
+
+    def step(self):
+        check(lib().asyrk_mrhs_step(self.h))
+
+    def stopped(self):
+        s = C.c_int32()
+        check(lib().asyrk_mrhs_stopped(self.h, C.byref(s)))
+        return bool(s.value)
+
+    def finish(self):
+        tr = _Trace(0, self._cap, want_x=False)
+        X = np.zeros((self.n, self.c1 - self.c0), np.float32)
+        check(lib().asyrk_mrhs_finish(self.h, C.byref(tr.out), X.ctypes.data_as(C.POINTER(C.c_float))))
+        d = tr.result(self._xs is not None)
+        d["X"] = X
+        return d
+
+    def solve(self, X0=None, X_star=None, **cfg):
+        c = _run_config(**cfg)
+        cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
+        tr = _Trace(0, cap, want_x=False)
+        X = np.zeros((self.n, self.c1 - self.c0), np.float32)
+        x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
+        xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        check(lib().asyrk_mrhs_solve(self.h, C.byref(c), x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None
+                                     else None, _ptr(xs, _f64p), C.byref(tr.out),
+                                     X.ctypes.data_as(C.POINTER(C.c_float))))
+        d = tr.result(xs is not None)
+        d["X"] = X
+        return d
+
+    def stats(self):
+        s = SolveStats()
+        check(lib().asyrk_mrhs_last_stats(self.h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in SolveStats._fields_}
 
 
 def microbench_xside(n, theta, precision=F64, warps=4736, proj_per_warp=256, mode=0):

@@ -81,6 +81,34 @@ struct MonitorArgs {
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 
+// ---- K2b/K3b: multi-right-hand-side worker and monitor (mrhs.cu)
+struct MrhsArgs {
+    Layout L;                     // fp32 row records (b unused)
+    float* X;                     // n x KL row-major
+    const float* B;               // m x KL row-major
+    float* R;                     // m x KL residual scratch
+    const double* Xstar;          // n x KL or nullptr
+    const long long* col_ptr;     // plain CSC for G = A^T R
+    const int32_t* csc_row;
+    const double* csc_val;
+    double* part;                 // block partials
+    double* norms;                // {r_sq, g_sq, d_sq} of this shard (all-reduce target)
+    DevRecord* rec;
+    long long rec_cap;
+    DevState* st;
+    int* host_flag;
+    long long W;
+    double gamma;
+    uint32_t key0, key1;
+    int KL;
+};
+bool mrhs_supported_kl(long long kl);
+int mrhs_row_blocks(long long m);
+int mrhs_col_blocks(long long n);
+void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s);
+void launch_mrhs_monitor(const MrhsArgs& a, cudaStream_t s);
+void launch_mrhs_commit(const MrhsArgs& a, int advance, cudaStream_t s);
+
 // ---- K4: power iteration building blocks (stats.cpp:15-50)
 void launch_spmv_rows(const CscDev& R, int precision, long long m, const double* v, double* out, cudaStream_t s);
 // SELL-32 columns from a column-sorted CSC: lengths + group sizes, then scatter

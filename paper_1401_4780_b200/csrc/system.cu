@@ -16,66 +16,21 @@
 #include <string>
 #include <vector>
 
-#include "../../include/asyrk_cuda.h"
+#include "capi_common.h"
 #include "host_seq.h"
 #include "kernels.h"
-#include "runtime.h"
 
 using namespace ak;
 
-namespace {
-
-thread_local std::string g_err;
-
-asyrk_status fail(asyrk_status s, const std::string& msg) {
-    g_err = msg;
-    return s;
+namespace ak {
+std::string& err_buf() {
+    static thread_local std::string e;
+    return e;
 }
-
-struct CudaFail {
-    asyrk_status st;
-};
-
-#define CK(call)                                                                                       \
-    do {                                                                                               \
-        cudaError_t e_ = (call);                                                                       \
-        if (e_ != cudaSuccess) {                                                                       \
-            g_err = std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #call " (system.cu:" +    \
-                    std::to_string(__LINE__) + ")";                                                    \
-            throw CudaFail{e_ == cudaErrorMemoryAllocation ? ASYRK_E_TooLarge : ASYRK_E_ThreadSpawnFailure}; \
-        }                                                                                              \
-    } while (0)
-
-template <class F>
-asyrk_status guarded(F&& f) {
-    try {
-        return f();
-    } catch (const CudaFail& c) {
-        return c.st;
-    } catch (const std::bad_alloc&) {
-        return fail(ASYRK_E_TooLarge, "host allocation failed");
-    } catch (const std::exception& e) {
-        return fail(ASYRK_E_InvalidArgument, e.what());
-    }
-}
-
-// Device allocations are stream-ordered pool allocations on the system's
-// stream (runtime.h), set per entry point.
 thread_local cudaStream_t g_alloc_stream = nullptr;
+}  // namespace ak
 
-template <class T>
-T* dalloc(size_t count) {
-    void* p = nullptr;
-    if (count == 0) count = 1;
-    CK(pool_alloc(&p, count * sizeof(T), g_alloc_stream));
-    return static_cast<T*>(p);
-}
-
-struct AllocStream {
-    cudaStream_t prev;
-    explicit AllocStream(cudaStream_t s) : prev(g_alloc_stream) { g_alloc_stream = s; }
-    ~AllocStream() { g_alloc_stream = prev; }
-};
+namespace {
 
 constexpr int kLookahead = 4;      // chunks in flight beyond the last confirmed one
 constexpr int kTimedLaunches = 1024;  // worker launches timed with event pairs per solve
@@ -106,6 +61,9 @@ struct asyrk_system {
     int32_t* rsell_col = nullptr;
     void* rsell_val = nullptr;
     double* b = nullptr;            // right-hand side (also in the record headers)
+    long long* col_ptr = nullptr;   // plain CSC (kept only for multi-RHS systems)
+    int32_t* csc_row = nullptr;
+    double* csc_val = nullptr;
     AliasEntry* alias = nullptr;  // device alias table (async norm_proportional), built lazily
 
     // host copies for sequence generation
@@ -175,6 +133,9 @@ void free_all(asyrk_system* s) {
     F(s->rsell_col);
     F(s->rsell_val);
     F(s->b);
+    F(s->col_ptr);
+    F(s->csc_row);
+    F(s->csc_val);
     F(s->alias);
     F(s->x);
     F(s->xd);
@@ -274,7 +235,7 @@ void ensure_alias_dev(asyrk_system* s) {
 }
 
 asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t precision, void* stream,
-                         asyrk_system** out) {
+                         asyrk_system** out, bool keep_csc = false) {
     asyrk_status v = check_view(A);
     if (v) return v;
     if (precision < 0 || precision > 2) return fail(ASYRK_E_InvalidArgument, "unknown precision");
@@ -408,6 +369,14 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     CK(cudaMemcpyAsync(s->b, d_b, (size_t)A->m * 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
+    if (keep_csc) {  // plain CSC stays for the multi-RHS monitor (warp per column)
+        s->col_ptr = col_ptr;
+        s->csc_row = csc_row;
+        s->csc_val = csc_val;
+        col_ptr = nullptr;
+        csc_row = nullptr;
+        csc_val = nullptr;
+    }
     for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
                     (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
                     (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
@@ -816,7 +785,7 @@ struct SysGuard {
 
 extern "C" {
 
-const char* asyrk_last_error(void) { return g_err.c_str(); }
+const char* asyrk_last_error(void) { return err_buf().c_str(); }
 int asyrk_abi_version(void) { return ASYRK_ABI_VERSION; }
 
 asyrk_status asyrk_set_device(int32_t device) {
@@ -999,6 +968,279 @@ asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const
         for (int64_t t = 0; t < n_threads; ++t) speedup[t] = wall_seconds[t] > 0.0 ? w1 / wall_seconds[t] : 0.0;
         return ASYRK_OK;
     });
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Multi-right-hand-side AsyRK (BASELINE config 5): asyrk_mrhs_* (asyrk_cuda.h)
+// ===========================================================================
+struct asyrk_mrhs {
+    asyrk_system* sys = nullptr;  // fp32 records + plain CSC of A
+    int64_t k_total = 0, c0 = 0, c1 = 0, kl = 0;
+    float* X = nullptr;           // n x kl
+    float* B = nullptr;           // m x kl
+    float* R = nullptr;           // m x kl
+    double* Xstar = nullptr;      // n x kl (optional)
+    double* part = nullptr;
+    double* norms = nullptr;      // device {r_sq, g_sq, d_sq}
+    bool have_xstar = false;
+    int64_t threads = 0;
+    double gamma = 1.0;
+    uint64_t seed = 0;
+    long long chunks = 0, max_chunks = 0;
+    asyrk_solve_stats stats{};
+};
+
+namespace {
+
+MrhsArgs mrhs_args(asyrk_mrhs* h) {
+    asyrk_system* s = h->sys;
+    MrhsArgs a{};
+    a.L = s->layout();
+    a.X = h->X;
+    a.B = h->B;
+    a.R = h->R;
+    a.Xstar = h->have_xstar ? h->Xstar : nullptr;
+    a.col_ptr = s->col_ptr;
+    a.csc_row = s->csc_row;
+    a.csc_val = s->csc_val;
+    a.part = h->part;
+    a.norms = h->norms;
+    a.rec = s->recs;
+    a.rec_cap = s->rec_cap;
+    a.st = s->st;
+    a.host_flag = s->host_flag_dev;
+    a.W = h->threads;
+    a.gamma = h->gamma;
+    const uint64_t k = splitmix64(h->seed ^ 0x3C6EF372FE94F82Bull);
+    a.key0 = (uint32_t)k;
+    a.key1 = (uint32_t)(k >> 32);
+    a.KL = (int)h->kl;
+    return a;
+}
+
+void mrhs_free(asyrk_mrhs* h) {
+    if (!h) return;
+    if (h->sys) {
+        cudaStream_t st = h->sys->stream;
+        for (void* p : {(void*)h->X, (void*)h->B, (void*)h->R, (void*)h->Xstar, (void*)h->part, (void*)h->norms})
+            pool_free(p, st);
+        free_all(h->sys);
+        delete h->sys;
+    }
+    delete h;
+}
+
+asyrk_status mrhs_create_impl(const asyrk_csr_view* A, const float* B, int64_t k_total, int64_t c0, int64_t c1,
+                              void* stream, asyrk_mrhs** out) {
+    if (!B || k_total < 1 || c0 < 0 || c1 > k_total || c1 <= c0)
+        return fail(ASYRK_E_InvalidArgument, "mrhs: need 0 <= c0 < c1 <= k_total and B");
+    const int64_t kl = c1 - c0;
+    if (!mrhs_supported_kl(kl))
+        return fail(ASYRK_E_InvalidArgument, "mrhs: columns per GPU must be a power of two in [2, 64]");
+    auto h = std::unique_ptr<asyrk_mrhs, void (*)(asyrk_mrhs*)>(new asyrk_mrhs, mrhs_free);
+    asyrk_status st = create_impl(A, nullptr, P_F32, stream, &h->sys, true);
+    if (st) return st;
+    asyrk_system* s = h->sys;
+    AllocStream as(s->stream);
+    h->k_total = k_total;
+    h->c0 = c0;
+    h->c1 = c1;
+    h->kl = kl;
+    h->X = dalloc<float>((size_t)s->n * kl);
+    h->B = dalloc<float>((size_t)s->m * kl);
+    h->R = dalloc<float>((size_t)s->m * kl);
+    h->norms = dalloc<double>(4);
+    h->part = dalloc<double>((size_t)mrhs_row_blocks(s->m) + 2 * (size_t)mrhs_col_blocks(s->n) + 8);
+    // this shard's columns of B, contiguous (host gather, then staged upload)
+    std::vector<float> bl((size_t)s->m * kl);
+    for (int64_t i = 0; i < s->m; ++i)
+        std::memcpy(&bl[(size_t)(i * kl)], B + i * k_total + c0, (size_t)kl * sizeof(float));
+    Stager::get().upload(h->B, bl.data(), bl.size() * sizeof(float), s->stream);
+    CK(cudaStreamSynchronize(s->stream));
+    *out = h.release();
+    return ASYRK_OK;
+}
+
+// X0 / Xstar are full n x k_total host arrays (row-major); this shard takes its columns
+asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar) {
+    if (!cfg) return fail(ASYRK_E_InvalidArgument, "null config");
+    asyrk_system* s = h->sys;
+    if (!s->normalized && !cfg->allow_unnormalized)
+        return fail(ASYRK_E_NotNormalized, "solve_parallel requires normalized rows");
+    if (cfg->threads < 1) return fail(ASYRK_E_InvalidArgument, "threads must be >= 1");
+    if (!(cfg->gamma > 0.0)) return fail(ASYRK_E_InvalidGamma, "gamma must be positive");
+    if (cfg->epochs < 0 || cfg->snapshot_interval < 1)
+        return fail(ASYRK_E_InvalidArgument, "epochs must be >= 0 and snapshot_interval >= 1");
+    cudaStream_t st = s->stream;
+    AllocStream as(st);
+    h->threads = cfg->threads;
+    h->gamma = cfg->gamma;
+    h->seed = cfg->seed;
+    h->chunks = 0;
+    h->max_chunks = cfg->epochs > 0 ? (cfg->epochs + cfg->snapshot_interval - 1) / cfg->snapshot_interval : 0;
+    h->stats = asyrk_solve_stats{};
+    ensure_records(s, std::max<long long>(256, h->max_chunks + 2));
+    ensure_events(s, 0);
+    const int64_t kl = h->kl;
+    if (X0) {
+        std::vector<float> xl((size_t)s->n * kl);
+        for (int64_t j = 0; j < s->n; ++j)
+            std::memcpy(&xl[(size_t)(j * kl)], X0 + j * h->k_total + h->c0, (size_t)kl * sizeof(float));
+        CK(cudaMemcpyAsync(h->X, xl.data(), xl.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        CK(cudaMemsetAsync(h->X, 0, (size_t)s->n * kl * sizeof(float), st));
+    }
+    h->have_xstar = Xstar != nullptr;
+    if (Xstar) {
+        if (!h->Xstar) h->Xstar = dalloc<double>((size_t)s->n * kl);
+        std::vector<double> xs((size_t)s->n * kl);
+        for (int64_t j = 0; j < s->n; ++j)
+            std::memcpy(&xs[(size_t)(j * kl)], Xstar + j * h->k_total + h->c0, (size_t)kl * sizeof(double));
+        CK(cudaMemcpyAsync(h->Xstar, xs.data(), xs.size() * sizeof(double), cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    *s->host_flag = 0;
+    CK(cudaEventRecord(s->ev_begin, st));
+    launch_state_init(s->st, cfg->epochs, cfg->snapshot_interval, cfg->target_r_sq, st);
+    launch_mrhs_monitor(mrhs_args(h), st);  // initial residual -> norms (this shard)
+    h->stats.kernel_launches += 4;
+    h->stats.monitor_launches++;
+    CK(cudaGetLastError());
+    return ASYRK_OK;
+}
+
+asyrk_status mrhs_step_impl(asyrk_mrhs* h) {
+    cudaStream_t st = h->sys->stream;
+    const MrhsArgs a = mrhs_args(h);
+    launch_mrhs_worker(a, st);
+    launch_mrhs_monitor(a, st);
+    h->chunks++;
+    h->stats.worker_launches++;
+    h->stats.monitor_launches++;
+    h->stats.kernel_launches += 4;
+    CK(cudaGetLastError());
+    return ASYRK_OK;
+}
+
+asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out) {
+    asyrk_system* s = h->sys;
+    cudaStream_t st = s->stream;
+    CK(cudaEventRecord(s->ev_end, st));
+    CK(cudaStreamSynchronize(st));
+    DevState hs;
+    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+    h->stats.solve_ms = ms;
+    h->stats.projections = hs.updates;
+    h->stats.warps = (int32_t)std::min<int64_t>(h->threads, INT32_MAX);
+    if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
+    if (trace) {
+        const long long k = std::min<long long>(hs.nrec, s->rec_cap);
+        std::vector<DevRecord> recs((size_t)k);
+        if (k) CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
+        trace->count = hs.nrec;
+        const long long w = std::min<long long>(k, trace->cap);
+        for (long long i = 0; i < w; ++i) {
+            const DevRecord& r = recs[(size_t)i];
+            if (trace->epoch_index) trace->epoch_index[i] = r.epoch;
+            if (trace->r_sq) trace->r_sq[i] = r.r_sq;
+            if (trace->grad_sq) trace->grad_sq[i] = r.grad_sq;
+            if (trace->dist_sq) trace->dist_sq[i] = r.dist_sq;
+            if (trace->wall_seconds) trace->wall_seconds[i] = 1e-9 * (double)r.t_ns;
+            if (trace->updates_applied) trace->updates_applied[i] = r.updates;
+        }
+    }
+    if (X_out) CK(cudaMemcpy(X_out, h->X, (size_t)s->n * h->kl * sizeof(float), cudaMemcpyDeviceToHost));
+    return ASYRK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+asyrk_status asyrk_mrhs_create(const asyrk_csr_view* A, const float* B, int64_t k_total, int64_t c0, int64_t c1,
+                               void* stream, asyrk_mrhs** out) {
+    return guarded([&] { return mrhs_create_impl(A, B, k_total, c0, c1, stream, out); });
+}
+
+asyrk_status asyrk_mrhs_destroy(asyrk_mrhs* h) {
+    mrhs_free(h);
+    return ASYRK_OK;
+}
+
+asyrk_status asyrk_mrhs_begin(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar) {
+    if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    return guarded([&] { return mrhs_begin_impl(h, cfg, X0, Xstar); });
+}
+
+asyrk_status asyrk_mrhs_norms(asyrk_mrhs* h, double** dev_norms) {
+    if (!h || !dev_norms) return fail(ASYRK_E_InvalidArgument, "null argument");
+    *dev_norms = h->norms;
+    return ASYRK_OK;
+}
+
+asyrk_status asyrk_mrhs_commit(asyrk_mrhs* h, int32_t advance) {
+    if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    return guarded([&] {
+        launch_mrhs_commit(mrhs_args(h), advance, h->sys->stream);
+        h->stats.kernel_launches += 1;
+        CK(cudaGetLastError());
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_mrhs_step(asyrk_mrhs* h) {
+    if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    return guarded([&] { return mrhs_step_impl(h); });
+}
+
+asyrk_status asyrk_mrhs_stopped(asyrk_mrhs* h, int32_t* stopped) {
+    if (!h || !stopped) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        CK(cudaStreamSynchronize(h->sys->stream));
+        *stopped = *reinterpret_cast<volatile int*>(h->sys->host_flag) ? 1 : 0;
+        if (h->chunks >= h->max_chunks) *stopped = 1;
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_mrhs_finish(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out) {
+    if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    return guarded([&] { return mrhs_finish_impl(h, trace, X_out); });
+}
+
+// Single-process loop: begin, then chunks of (workers + monitor + commit)
+// with the same bounded lookahead as asyrk_system_solve.
+asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
+                              asyrk_trace_out* trace, float* X_out) {
+    if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    return guarded([&] {
+        asyrk_status st = mrhs_begin_impl(h, cfg, X0, Xstar);
+        if (st) return st;
+        asyrk_system* s = h->sys;
+        launch_mrhs_commit(mrhs_args(h), 0, s->stream);
+        for (long long k = 0; k < h->max_chunks; ++k) {
+            if (k >= kLookahead) {
+                CK(cudaEventSynchronize(s->ev_chunk[(size_t)(k % (kLookahead + 1))]));
+                if (*reinterpret_cast<volatile int*>(s->host_flag)) break;
+            }
+            st = mrhs_step_impl(h);
+            if (st) return st;
+            launch_mrhs_commit(mrhs_args(h), 1, s->stream);
+            CK(cudaEventRecord(s->ev_chunk[(size_t)(k % (kLookahead + 1))], s->stream));
+        }
+        return mrhs_finish_impl(h, trace, X_out);
+    });
+}
+
+asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out) {
+    if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
+    *out = h->stats;
+    return ASYRK_OK;
 }
 
 }  // extern "C"

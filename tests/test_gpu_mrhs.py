@@ -1,0 +1,109 @@
+"""GPU tests of the multi-right-hand-side path (BASELINE config 5 shape at
+reduced size): convergence of every column to the tolerance, the sharded
+protocol with the global stop test (two shards on one GPU, norms summed on
+the host between step and commit — the all-reduce a multi-GPU run does with
+NCCL), and the device records against an independent CPU evaluation."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+capi = pytest.importorskip("paper_1401_4780_b200.capi")
+from paper_1401_4780_b200.mrhs import CudaShardBackend, shard_columns, solve_sharded  # noqa: E402
+
+TOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def problem():
+    A, B, Xs = capi.generate_fixed_theta(50000, 25000, 20, seed=1005, k=64)
+    return A, B.astype(np.float32), Xs
+
+
+def _residual(A, X, B):
+    m = A.m
+    v = A.values.reshape(m, -1)
+    c = A.col_idx.reshape(m, -1)
+    AX = np.einsum("it,itk->ik", v, X[c].astype(np.float64))
+    return AX - B
+
+
+def test_single_gpu_all_columns_converge(problem):
+    A, B, Xs = problem
+    S = capi.MultiRHS(A, B, 0, 64)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    t = S.solve(threads=2048, epochs=400, target=TOL * TOL * bb, seed=3, X_star=Xs)
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    R = _residual(A, t["X"], B)
+    rel = np.sqrt((R * R).sum() / bb)
+    assert rel <= 2 * TOL  # independent fp64 evaluation of the fp32 iterate
+    assert abs((R * R).sum() - t["r_sq"][-1]) <= 0.05 * t["r_sq"][-1]
+    err = np.linalg.norm(t["X"] - Xs) / np.linalg.norm(Xs)
+    assert err <= 10 * TOL
+    assert np.sqrt(t["dist_sq"][-1]) / np.linalg.norm(Xs) <= 10 * TOL
+    # every column individually reaches the tolerance band
+    col_rel = np.sqrt((R * R).sum(axis=0) / (B.astype(np.float64) ** 2).sum(axis=0))
+    assert col_rel.max() <= 10 * TOL
+    S.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_protocol_global_stop(problem, world):
+    A, B, Xs = problem
+    bb = float((B.astype(np.float64) ** 2).sum())
+    shards = [CudaShardBackend(A, B, *shard_columns(64, world, r)) for r in range(world)]
+
+    # host-side "all-reduce" over the in-process shards (NCCL sums in place on each rank)
+    def make_all_reduce(pending=[]):
+        def all_reduce(t):
+            pending.append(t)
+            if len(pending) == world:
+                tot = sum(p.clone() for p in pending)
+                for p in pending:
+                    p.copy_(tot)
+                pending.clear()
+        return all_reduce
+
+    ar = make_all_reduce()
+    cfg = dict(threads=1024, epochs=400, target=TOL * TOL * bb, X_star=Xs)
+    for r, s in enumerate(shards):
+        s.begin(seed=10 + r, **cfg)
+    for s in shards:
+        ar(s.norms())
+    for s in shards:
+        s.commit(False)
+    for _ in range(400):
+        for s in shards:
+            s.step()
+        for s in shards:
+            ar(s.norms())
+        for s in shards:
+            s.commit(True)
+        stops = [s.stopped() for s in shards]
+        assert len(set(stops)) == 1  # identical global decision
+        if stops[0]:
+            break
+    res = [s.finish() for s in shards]
+    assert all(np.array_equal(res[0]["epoch_index"], r["epoch_index"]) for r in res)
+    assert all(np.array_equal(res[0]["r_sq"], r["r_sq"]) for r in res)
+    X = np.concatenate([r["X"] for r in res], axis=1)
+    R = _residual(A, X, B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+    assert np.linalg.norm(X - Xs) / np.linalg.norm(Xs) <= 10 * TOL
+    for s in shards:
+        s.close()
+
+
+def test_solve_sharded_single_rank(problem):
+    A, B, Xs = problem
+    bb = float((B.astype(np.float64) ** 2).sum())
+    be = CudaShardBackend(A, B, 0, 64)
+    t = solve_sharded(be, all_reduce=lambda x: None, threads=2048, epochs=400, target=TOL * TOL * bb, seed=9)
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    be.close()
+
+
+def test_bad_shard_width_rejected(problem):
+    A, B, _ = problem
+    with pytest.raises(capi.AsyrkError, match="InvalidArgument"):
+        capi.MultiRHS(A, B, 0, 48)
