@@ -47,9 +47,25 @@ struct DetArgs {
     double gamma;
     int full_row;
     int x_in_smem;
+    const int32_t* need;          // per (event, nonzero): earlier events of the chunk on that column
+    const long long* flat_off;    // per event: offset of its nonzeros in need (nullptr: q * uniform_len)
+    const int32_t* ev_col;        // per (event, nonzero): column, in event order (prepass)
+    double* ev_val;               // per (event, nonzero): value, in event order (prepass)
+    double* ev_b;                 // per event: b_i
+    double* ev_nrm;               // per event: row_norm_i
+    long long* dbg;               // optional per-event phase timestamps (diagnostics)
 };
 void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
+struct DetPrep {
+    int32_t *keys, *vals, *keys_s, *vals_s, *start;
+    double *ev_val, *ev_b, *ev_nrm;
+    void* temp;
+    size_t temp_bytes;
+};
+size_t det_prepare_temp_bytes(long long total);
+// fills a.need for the chunk (total = number of (event, nonzero) pairs)
+void launch_det_prepare(const DetArgs& a, const DetPrep& p, long long total, cudaStream_t s);
 
 // ---- K3: residual monitor r = Ax - b, g = A^T r, dist = ||x - x*||^2
 // Columns of A in SELL-32 order: the 32 columns of group g interleave their

@@ -93,6 +93,10 @@ struct asyrk_system {
     int32_t* pick_dev[kLookahead + 1] = {};
     int32_t* seq_host[kLookahead + 1] = {};
     int32_t* pick_host[kLookahead + 1] = {};
+    long long* flat_dev[kLookahead + 1] = {};   // ragged rows: event -> offset of its (event, nonzero) pairs
+    long long* flat_host[kLookahead + 1] = {};
+    int32_t* need = nullptr;                    // dataflow prepass output
+    DetPrep prep{};
     size_t seq_cap = 0;
 
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
@@ -149,10 +153,22 @@ void free_all(asyrk_system* s) {
     F(s->st);
     F(s->incr);
     F(s->scratch);
+    F(s->need);
+    F(s->prep.keys);
+    F(s->prep.vals);
+    F(s->prep.keys_s);
+    F(s->prep.vals_s);
+    F(s->prep.start);
+    F(s->prep.temp);
+    F(s->prep.ev_val);
+    F(s->prep.ev_b);
+    F(s->prep.ev_nrm);
     flag_release(s->host_flag);
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
         F(s->pick_dev[k]);
+        F(s->flat_dev[k]);
+        if (s->flat_host[k]) cudaFreeHost(s->flat_host[k]);
         if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
         if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
     }
@@ -191,13 +207,34 @@ void ensure_seq(asyrk_system* s, size_t count) {
     for (int k = 0; k <= kLookahead; ++k) {
         pool_free(s->seq_dev[k], s->stream);
         pool_free(s->pick_dev[k], s->stream);
+        pool_free(s->flat_dev[k], s->stream);
         if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
         if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
+        if (s->flat_host[k]) cudaFreeHost(s->flat_host[k]);
         s->seq_dev[k] = dalloc<int32_t>(count);
         s->pick_dev[k] = dalloc<int32_t>(count);
+        s->flat_dev[k] = dalloc<long long>(count + 1);
         CK(cudaHostAlloc((void**)&s->seq_host[k], count * 4, cudaHostAllocDefault));
         CK(cudaHostAlloc((void**)&s->pick_host[k], count * 4, cudaHostAllocDefault));
+        CK(cudaHostAlloc((void**)&s->flat_host[k], (count + 1) * 8, cudaHostAllocDefault));
     }
+    // dataflow prepass buffers: one (event, nonzero) pair per entry
+    const size_t pairs = count * (size_t)s->max_len;
+    for (void* p : {(void*)s->need, (void*)s->prep.keys, (void*)s->prep.vals, (void*)s->prep.keys_s,
+                    (void*)s->prep.vals_s, (void*)s->prep.start, s->prep.temp, (void*)s->prep.ev_val,
+                    (void*)s->prep.ev_b, (void*)s->prep.ev_nrm})
+        pool_free(p, s->stream);
+    s->need = dalloc<int32_t>(pairs);
+    s->prep.ev_val = dalloc<double>(pairs);
+    s->prep.ev_b = dalloc<double>(count);
+    s->prep.ev_nrm = dalloc<double>(count);
+    s->prep.keys = dalloc<int32_t>(pairs);
+    s->prep.vals = dalloc<int32_t>(pairs);
+    s->prep.keys_s = dalloc<int32_t>(pairs);
+    s->prep.vals_s = dalloc<int32_t>(pairs);
+    s->prep.start = dalloc<int32_t>((size_t)s->n);
+    s->prep.temp_bytes = det_prepare_temp_bytes((long long)pairs);
+    s->prep.temp = dalloc<unsigned char>(s->prep.temp_bytes);
     s->seq_cap = count;
 }
 
@@ -523,6 +560,11 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.gamma = sp.gamma;
         da.full_row = sp.full_row ? 1 : 0;
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
+        da.need = s->need;
+        da.ev_col = s->prep.keys;
+        da.ev_val = s->prep.ev_val;
+        da.ev_b = s->prep.ev_b;
+        da.ev_nrm = s->prep.ev_nrm;
         s->stats.warps = 1;
         s->stats.resident_warps = 1;
     } else {
@@ -582,8 +624,37 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             da.seq = s->seq_dev[slot];
             da.picks = s->pick_dev[slot];
             da.count = (long long)cnt;
+            long long pairs = (long long)cnt * (long long)s->uniform_len;
+            da.flat_off = nullptr;
+            if (!s->uniform) {  // ragged rows: offsets of each event's (event, nonzero) pairs
+                long long* fo = s->flat_host[slot];
+                fo[0] = 0;
+                for (size_t q = 0; q < cnt; ++q) fo[q + 1] = fo[q] + s->h_len[(size_t)s->seq_host[slot][q]];
+                pairs = fo[cnt];
+                CK(cudaMemcpyAsync(s->flat_dev[slot], fo, (cnt + 1) * 8, cudaMemcpyHostToDevice, st));
+                da.flat_off = s->flat_dev[slot];
+            }
             if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
+            if (da.x_in_smem) launch_det_prepare(da, s->prep, pairs, st);
+            static const char* dbg_path = getenv("ASYRK_DET_DEBUG");
+            long long* dbg = nullptr;
+            if (dbg_path && k == 0) {
+                CK(cudaMalloc(&dbg, (size_t)cnt * 4 * 8));
+                CK(cudaMemset(dbg, 0, (size_t)cnt * 4 * 8));
+            }
+            da.dbg = dbg;
             launch_det(da, 0, st);
+            if (dbg) {
+                std::vector<long long> h((size_t)cnt * 4);
+                CK(cudaStreamSynchronize(st));
+                CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+                if (FILE* f = fopen(dbg_path, "wb")) {
+                    fwrite(h.data(), 8, h.size(), f);
+                    fclose(f);
+                }
+                cudaFree(dbg);
+                da.dbg = nullptr;
+            }
         } else {
             if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
             launch_worker(wa, prec, E, st);
