@@ -92,10 +92,16 @@ struct MonitorArgs {
     int exact;                    // 1: reference summation order (bitwise)
     CscDev rows;                  // SELL-32 rows of A (pass 1)
     const double* b;              // m
+    int slot;                     // >= 0: record the epoch-boundary snapshot in this slot (overlapped solve)
+    int force;                    // 1: run even after stop (the final exact record); replaces a same-epoch record
     int advance;                  // 0: initial record, 1: after a chunk
     long long m_rows;
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
+// overlapped solves: copy x into snapshot slot xs (if the epoch ran) and
+// advance the coordinator state (epoch, updates, slot meta, next go)
+void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
+                     long long m, cudaStream_t s);
 
 // ---- K2b/K3b: multi-right-hand-side worker and monitor (mrhs.cu)
 struct MrhsArgs {

@@ -81,6 +81,12 @@ struct DevState {
     int stop;               // no further work
     int status;             // 0 or ASYRK_E_NonFinite
     long long increments;   // instrument: component increments applied
+    // overlapped async solves: the worker launch runs iff go (decided on the
+    // worker stream before it, so every block of a launch agrees); snapshots
+    // of x at epoch boundaries feed the monitor stream
+    int go;
+    int snap_valid[2];
+    long long snap_epoch[2], snap_updates[2];
 };
 
 struct DevRecord {

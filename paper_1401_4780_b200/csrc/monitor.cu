@@ -44,10 +44,52 @@ __device__ __forceinline__ double ldro(const X* p) {
     return (double)__ldg(p);
 }
 
+// One SELL-32 lane: sum_t v_t * y[idx_t] in storage order from 0.0 (a serial
+// row_dot, csr.cpp:65-70, or a multiply_transpose column, csr.cpp:80-92).
+// Software-pipelined: the index/value loads of block t+1 are in flight while
+// block t's gathers resolve, and the ragged tail is a predicated block, so a
+// lane's latency chain is ceil(len/U)+1 load rounds instead of one per entry.
+template <int U, class V, class Y>
+__device__ __forceinline__ double sell_dot(const int32_t* __restrict__ idx, const V* __restrict__ val, long long e,
+                                           int len, const Y* __restrict__ y) {
+    int ci[U];
+    double av[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const bool ok = u < len;
+        ci[u] = ok ? __ldg(idx + e + 32 * u) : 0;
+        av[u] = ok ? (double)__ldg(val + e + 32 * u) : 0.0;
+    }
+    double s = 0.0;
+    for (int t = 0; t < len; t += U) {
+        double yv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) yv[u] = (t + u < len) ? ldro(y + ci[u]) : 0.0;
+        const long long en = e + 32ll * (t + U);
+        int cn[U];
+        double an[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool ok = t + U + u < len;
+            cn[u] = ok ? __ldg(idx + en + 32 * u) : 0;
+            an[u] = ok ? (double)__ldg(val + en + 32 * u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (t + u < len) s = __dadd_rn(s, __dmul_rn(av[u], yv[u]));
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            ci[u] = cn[u];
+            av[u] = an[u];
+        }
+    }
+    return s;
+}
+
 // Pass 1 / SpMV rows over the SELL-32 row copy: lane l of group g owns row
 // 32g + l and adds v_k * x[c_k] in storage order starting from 0.0 — the
 // reference's serial row_dot (csr.cpp:65-70) — with every load of a warp
-// contiguous and 8 independent gathers in flight per lane.
+// contiguous (sell_dot).
 // out[i] = a_i^T x (- b_i when b); part: r^2 block partials or null.
 template <class V, class X>
 __global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m, const X* __restrict__ x,
@@ -61,24 +103,7 @@ __global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m
     if (i < m) {
         const int len = __ldg(R.col_len + i);
         const long long base = __ldg(R.grp_off + (i >> 5)) + lane;
-        const V* rv = static_cast<const V*>(R.val);
-        double s = 0.0;
-        int t = 0;
-        for (; t + 8 <= len; t += 8) {
-            const long long e = base + 32ll * t;
-            double xv[8], av[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                xv[u] = ldro(x + __ldg(R.row + e + 32 * u));
-                av[u] = (double)__ldg(rv + e + 32 * u);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) s = __dadd_rn(s, __dmul_rn(av[u], xv[u]));
-        }
-        for (; t < len; ++t) {
-            const long long e = base + 32ll * t;
-            s = __dadd_rn(s, __dmul_rn((double)__ldg(rv + e), ldro(x + __ldg(R.row + e))));
-        }
+        double s = sell_dot<8>(R.row, static_cast<const V*>(R.val), base, len, x);
         if (b) s = __dsub_rn(s, b[i]);
         out[i] = s;
         r2 = s * s;
@@ -110,24 +135,7 @@ __global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n
     if (j < n) {
         const int len = __ldg(C.col_len + j);
         const long long base = __ldg(C.grp_off + grp) + lane;
-        const V* cv = static_cast<const V*>(C.val);
-        double g = 0.0;
-        int t = 0;
-        for (; t + 8 <= len; t += 8) {  // 8 independent gathers in flight per lane
-            const long long e = base + 32ll * t;
-            double rv[8], av[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                rv[u] = __ldg(r + __ldg(C.row + e + 32 * u));
-                av[u] = (double)__ldg(cv + e + 32 * u);
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) g = __dadd_rn(g, __dmul_rn(av[u], rv[u]));
-        }
-        for (; t < len; ++t) {
-            const long long e = base + 32ll * t;
-            g = __dadd_rn(g, __dmul_rn((double)__ldg(cv + e), __ldg(r + __ldg(C.row + e))));
-        }
+        const double g = sell_dot<8>(C.row, static_cast<const V*>(C.val), base, len, r);
         if (out) out[j] = g;
         g2 = g * g;
         if (x_star) {
@@ -154,22 +162,41 @@ __global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n
     }
 }
 
+// Record + stop decision. Three modes:
+//  * in-stream (slot < 0, !force): advance the epoch by this chunk's span
+//    (advance = 1) or record the initial state (advance = 0);
+//  * overlapped (slot >= 0): record the epoch-boundary snapshot of that slot,
+//    taken on the worker stream while the workers went on (the reference's
+//    coordinator snapshot, parallel.cpp:388-408, but quiesced);
+//  * final (force = 1): the exact record after the workers stopped; like the
+//    reference (parallel.cpp:415-426) it replaces a snapshot record of the
+//    same epoch.
 __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, double d_sq) {
     DevState* st = a.st;
-    if (a.advance) {
-        const long long sp = chunk_span(st);
-        st->epoch += sp;
-        st->updates += sp * a.m_rows;
+    long long epoch, updates;
+    if (a.slot >= 0) {
+        if (!st->snap_valid[a.slot]) return;
+        epoch = st->snap_epoch[a.slot];
+        updates = st->snap_updates[a.slot];
+    } else {
+        if (a.advance) {
+            const long long sp = chunk_span(st);
+            st->epoch += sp;
+            st->updates += sp * a.m_rows;
+        }
+        epoch = st->epoch;
+        updates = st->updates;
     }
     if (!isfinite(r_sq) || !isfinite(g_sq)) {
         st->status = 8;  // ASYRK_E_NonFinite
         st->stop = 1;
     } else {
-        const long long k = st->nrec;
+        long long k = st->nrec;
+        if (a.force && k > 0 && k <= a.rec_cap && a.rec[k - 1].epoch >= epoch) --k;
         if (k < a.rec_cap) {
             DevRecord rc;
-            rc.epoch = st->epoch;
-            rc.updates = st->updates;
+            rc.epoch = epoch;
+            rc.updates = updates;
             rc.r_sq = r_sq;
             rc.grad_sq = g_sq;
             rc.dist_sq = a.x_star ? d_sq : -1.0;
@@ -177,8 +204,9 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
             a.rec[k] = rc;
         }
         st->nrec = k + 1;
-        if (r_sq <= st->target || st->epoch >= st->epochs_cap) st->stop = 1;
+        if (r_sq <= st->target || epoch >= st->epochs_cap) st->stop = 1;
     }
+    if (a.slot < 0) st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
     if (st->stop && a.host_flag) {
         *reinterpret_cast<volatile int*>(a.host_flag) = 1;
         __threadfence_system();
@@ -204,7 +232,7 @@ __device__ __forceinline__ double serial_sumsq(const double* v, const double* w,
 }
 
 __global__ void finalize_exact_kernel(MonitorArgs a) {
-    if (a.st->stop) return;
+    if (!a.force && a.st->stop) return;
     const int lane = threadIdx.x & 31;
     const double rs = serial_sumsq(a.r, nullptr, a.L.m, lane);
     const double gs = serial_sumsq(a.g, nullptr, a.L.n, lane);
@@ -215,7 +243,7 @@ __global__ void finalize_exact_kernel(MonitorArgs a) {
 
 // ---- finalize, fast: fixed-order sum of the block partials (one block)
 __global__ void __launch_bounds__(kMonThreads) finalize_fast_kernel(MonitorArgs a, int nb_rows, int nb_cols) {
-    if (a.st->stop) return;
+    if (!a.force && a.st->stop) return;
     __shared__ double red[3][kMonThreads];
     double s[3] = {0.0, 0.0, 0.0};
     for (int k = threadIdx.x; k < nb_rows; k += kMonThreads) s[0] += a.part[k];
@@ -242,10 +270,11 @@ static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
     const int nbr = monitor_row_blocks(a.L.m);
     const int nbc = monitor_col_blocks(a.L.n);
     const X* x = static_cast<const X*>(a.x);
-    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, a.st);
+    const DevState* gate = a.force ? nullptr : a.st;  // the final record runs after stop
+    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, gate);
     cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.exact ? a.g : nullptr,
                                                   a.exact ? nullptr : a.part + nbr,
-                                                  a.exact ? nullptr : a.part + nbr + nbc, x, a.x_star, a.st);
+                                                  a.exact ? nullptr : a.part + nbr + nbc, x, a.x_star, gate);
     if (a.exact)
         finalize_exact_kernel<<<1, 32, 0, s>>>(a);
     else

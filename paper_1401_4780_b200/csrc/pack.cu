@@ -126,6 +126,8 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->stop = 0;
     st->status = 0;
     st->increments = 0;
+    st->go = 0;  // set by the initial record's commit
+    st->snap_valid[0] = st->snap_valid[1] = 0;
     st->t0_ns = globaltimer_ns();
 }
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
@@ -252,6 +254,45 @@ __global__ void set_rhs_kernel(Layout L, const double* __restrict__ b) {
 void launch_set_rhs(const Layout& L, const double* b, cudaStream_t s) {
     const unsigned blocks = (unsigned)std::min<long long>((L.m + 255) / 256, 148 * 8);
     set_rhs_kernel<<<blocks, 256, 0, s>>>(L, b);
+}
+
+}  // namespace ak
+
+namespace ak {
+
+// ---- overlapped async solve: epoch-boundary snapshot of x for the monitor
+// stream, then the coordinator state advance (one thread). Both read `go`,
+// which only advance_kernel changes, so a whole epoch is either run and
+// counted or skipped.
+template <class X>
+__global__ void snapshot_kernel(const DevState* st, const X* __restrict__ x, X* __restrict__ xs, long long n) {
+    if (!st->go) return;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        xs[k] = __ldcg(x + k);
+}
+
+__global__ void advance_kernel(DevState* st, int slot, long long m) {
+    if (st->go) {
+        const long long sp = chunk_span(st);
+        st->epoch += sp;
+        st->updates += sp * m;
+        st->snap_epoch[slot] = st->epoch;
+        st->snap_updates[slot] = st->updates;
+        st->snap_valid[slot] = 1;
+    } else {
+        st->snap_valid[slot] = 0;
+    }
+    st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
+}
+
+void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
+                     long long m, cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
+    if (precision == P_F32)
+        snapshot_kernel<float><<<blocks, 256, 0, s>>>(st, static_cast<const float*>(x), static_cast<float*>(xs), n);
+    else
+        snapshot_kernel<double><<<blocks, 256, 0, s>>>(st, static_cast<const double*>(x), static_cast<double*>(xs), n);
+    advance_kernel<<<1, 1, 0, s>>>(stw, slot, m);
 }
 
 }  // namespace ak

@@ -102,6 +102,10 @@ struct asyrk_system {
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     std::vector<cudaEvent_t> ev_w;   // 2 per timed worker launch
     std::vector<cudaEvent_t> ev_chunk;
+    // overlapped async solves: monitor stream, x snapshots, slot events
+    cudaStream_t mstream = nullptr;
+    void* xs[2] = {nullptr, nullptr};
+    cudaEvent_t snap_ev[2] = {nullptr, nullptr}, mon_ev[2] = {nullptr, nullptr};
     asyrk_solve_stats stats{};
 
     Layout layout() const {
@@ -176,6 +180,15 @@ void free_all(asyrk_system* s) {
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     for (auto e : s->ev_w) cudaEventDestroy(e);
     for (auto e : s->ev_chunk) cudaEventDestroy(e);
+    for (int q = 0; q < 2; ++q) {
+        F(s->xs[q]);
+        if (s->snap_ev[q]) cudaEventDestroy(s->snap_ev[q]);
+        if (s->mon_ev[q]) cudaEventDestroy(s->mon_ev[q]);
+    }
+    if (s->mstream) {
+        cudaStreamSynchronize(s->mstream);
+        cudaStreamDestroy(s->mstream);
+    }
     if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
@@ -479,6 +492,8 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.m_rows = s->m;
     a.rows = s->rsell();
     a.b = s->b;
+    a.slot = -1;
+    a.force = 0;
     return a;
 }
 
@@ -591,6 +606,21 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     }
     CK(cudaGetLastError());
 
+    // async solves overlap the residual monitor with the next epoch's workers
+    static const bool no_overlap = getenv("ASYRK_NO_OVERLAP") != nullptr;
+    const bool overlap = !sp.det && !no_overlap;
+    if (overlap && !s->mstream) {
+        // highest priority: monitor blocks take SM slots ahead of queued worker blocks
+        int lo = 0, hi = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        static const bool low_prio = getenv("ASYRK_MON_LOWPRIO") != nullptr;
+        CK(cudaStreamCreateWithPriority(&s->mstream, cudaStreamNonBlocking, low_prio ? lo : hi));
+        for (int q = 0; q < 2; ++q) {
+            CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&s->mon_ev[q], cudaEventDisableTiming));
+            s->xs[q] = dalloc<unsigned char>((size_t)s->n * s->xbytes());
+        }
+    }
     long long timed = 0;
     long long k = 0;
     for (; k < max_chunks; ++k) {
@@ -665,10 +695,40 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         }
         launches += 1;
         s->stats.worker_launches++;
-        launch_monitor(monitor_args(s, sp.det, 1, sp.x_star != nullptr), prec, st);
-        launches += 3;
+        if (overlap) {
+            // epoch-boundary snapshot on the worker stream; the residual monitor
+            // of that snapshot runs on the monitor stream while the next epoch's
+            // workers already go (the reference's coordinator thread,
+            // parallel.cpp:388-408, without its torn reads)
+            const int slot2 = (int)(k & 1);
+            if (k >= 2) CK(cudaStreamWaitEvent(st, s->mon_ev[slot2], 0));  // slot free: monitor k-2 done
+            launch_snapshot(s->st, s->x, s->xs[slot2], s->n, prec, slot2, s->st, s->m, st);
+            CK(cudaEventRecord(s->snap_ev[slot2], st));
+            CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[slot2], 0));
+            MonitorArgs ma = monitor_args(s, false, 0, sp.x_star != nullptr);
+            ma.x = s->xs[slot2];
+            ma.slot = slot2;
+            launch_monitor(ma, prec, s->mstream);
+            CK(cudaEventRecord(s->mon_ev[slot2], s->mstream));
+            launches += 5;
+        } else {
+            launch_monitor(monitor_args(s, sp.det, 1, sp.x_star != nullptr), prec, st);
+            launches += 3;
+        }
         s->stats.monitor_launches++;
         CK(cudaEventRecord(s->ev_chunk[(size_t)(k % (kLookahead + 1))], st));
+        CK(cudaGetLastError());
+    }
+    if (overlap) {
+        // join the monitor stream, then the exact record of the final iterate
+        // (parallel.cpp:415-426: epoch = the epochs actually run)
+        CK(cudaEventRecord(s->snap_ev[0], s->mstream));
+        CK(cudaStreamWaitEvent(st, s->snap_ev[0], 0));
+        MonitorArgs fa = monitor_args(s, false, 0, sp.x_star != nullptr);
+        fa.force = 1;
+        launch_monitor(fa, prec, st);
+        launches += 3;
+        s->stats.monitor_launches++;
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(s->ev_end, st));

@@ -105,7 +105,7 @@ template <class V, class X, int E, int R, bool FULL_ROW>
 __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerArgs a) {
     using T = X;  // arithmetic type of the projection (x's precision)
     const DevState* st = a.st;
-    if (st->stop) return;
+    if (!st->go) return;  // decided on the worker stream before this launch
     const long long epoch = st->epoch;
     const long long span = chunk_span(st);
     if (span <= 0) return;
@@ -228,7 +228,7 @@ template <class V, class X, bool FULL_ROW>
 __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
     using T = X;
     const DevState* st = a.st;
-    if (st->stop) return;
+    if (!st->go) return;
     const long long epoch = st->epoch;
     const long long span = chunk_span(st);
     if (span <= 0) return;
