@@ -53,13 +53,15 @@ void ThreadPool::run(const std::function<void(int)>& f) {
 }
 
 static int stager_threads() {
+    if (const char* e = getenv("ASYRK_STAGER_THREADS")) return std::max(1, atoi(e));
     const unsigned hc = std::thread::hardware_concurrency();
-    return (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+    return (int)std::max(1u, std::min(12u, hc ? hc * 3 / 4 : 1u));  // fills are memory-bound; leave the rest
 }
 
 Stager::Stager() : pool_(stager_threads()) {
+    if (const char* e = getenv("ASYRK_STAGE_CHUNK_KB")) chunk_ = std::max<size_t>(64, strtoull(e, nullptr, 10)) << 10;
     for (int k = 0; k < kSlots; ++k) {
-        if (cudaHostAlloc((void**)&slot_[k], kChunk, cudaHostAllocDefault) != cudaSuccess)
+        if (cudaHostAlloc((void**)&slot_[k], chunk_, cudaHostAllocDefault) != cudaSuccess)
             throw std::runtime_error("pinned staging allocation failed");
         cudaEventCreateWithFlags(&ev_[k], cudaEventDisableTiming);
     }
@@ -75,7 +77,7 @@ Stager& Stager::get() {
 template <class F>
 void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* dst, F&& fill) {
     std::lock_guard<std::mutex> lk(mu_);
-    const size_t per_chunk = kChunk / out_elem;
+    const size_t per_chunk = chunk_ / out_elem;
     const size_t total = out_bytes / out_elem;
     for (size_t e0 = 0; e0 < total; e0 += per_chunk) {
         const size_t ne = std::min(per_chunk, total - e0);
@@ -98,16 +100,31 @@ void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* d
     }
 }
 
+static bool have_avx2() {
+    static const bool ok = stage_nt_supported() && !getenv("ASYRK_NO_NT_STAGING");
+    return ok;
+}
+
 void Stager::upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    const char* sp = static_cast<const char*>(src);
-    pipeline(bytes, 1, s, static_cast<char*>(dst),
-             [sp](unsigned char* out, size_t first, size_t n) { std::memcpy(out, sp + first, n); });
+    const unsigned char* sp = static_cast<const unsigned char*>(src);
+    const bool nt = have_avx2();
+    pipeline(bytes, 1, s, static_cast<char*>(dst), [sp, nt](unsigned char* out, size_t first, size_t n) {
+        if (nt)
+            copy_nt(out, sp + first, n);
+        else
+            std::memcpy(out, sp + first, n);
+    });
 }
 
 void Stager::upload_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s) {
-    pipeline(count * 4, 4, s, reinterpret_cast<char*>(dst), [src](unsigned char* out, size_t first, size_t n) {
+    const bool nt = have_avx2();
+    pipeline(count * 4, 4, s, reinterpret_cast<char*>(dst), [src, nt](unsigned char* out, size_t first, size_t n) {
         int32_t* o = reinterpret_cast<int32_t*>(out);
         const int64_t* in = src + first;
+        if (nt) {
+            narrow_nt(o, in, n);
+            return;
+        }
         for (size_t k = 0; k < n; ++k) o[k] = (int32_t)in[k];
     });
 }

@@ -41,6 +41,11 @@ class ThreadPool {
     bool stop_ = false;
 };
 
+// host/stage_copy.cpp: AVX2 streaming-store copies (call only if stage_nt_supported())
+bool stage_nt_supported();
+void copy_nt(unsigned char* out, const unsigned char* in, size_t n);
+void narrow_nt(int32_t* out, const int64_t* in, size_t n);
+
 class Stager {
   public:
     static Stager& get();
@@ -52,7 +57,7 @@ class Stager {
   private:
     Stager();
     static constexpr int kSlots = 4;
-    static constexpr size_t kChunk = 8u << 20;
+    size_t chunk_ = 8u << 20;  // bytes per pinned slot (ASYRK_STAGE_CHUNK_KB)
     template <class F>
     void pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* dst, F&& fill);
     std::mutex mu_;

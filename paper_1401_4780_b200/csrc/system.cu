@@ -14,6 +14,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "capi_common.h"
@@ -302,121 +303,194 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         s->own_stream = true;
     }
     AllocStream alloc_on(s->stream);
+    // ASYRK_PROFILE_CREATE=1: synchronized phase times on stderr (diagnostics)
+    static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
+    auto t_prev = std::chrono::steady_clock::now();
+    auto phase = [&](const char* what) {
+        if (!prof) return;
+        cudaStreamSynchronize(s->stream);
+        const auto t = std::chrono::steady_clock::now();
+        fprintf(stderr, "[create] %-14s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(t - t_prev).count());
+        t_prev = t;
+    };
     const int vbytes = precision == P_F64 ? 8 : 4;
-    // row lengths, layout
-    s->h_len.resize((size_t)A->m);
-    s->h_norm.assign(A->row_norm, A->row_norm + A->m);
-    uint32_t maxl = 0, minl = UINT32_MAX;
-    for (int64_t i = 0; i < A->m; ++i) {
-        const int64_t l = A->row_ptr[i + 1] - A->row_ptr[i];
-        if (l <= 0) {
-            free_all(s.get());
-            return fail(ASYRK_E_ZeroRow, "row " + std::to_string(i) + " has no nonzeros");
-        }
-        s->h_len[(size_t)i] = (int32_t)l;
-        maxl = std::max<uint32_t>(maxl, (uint32_t)l);
-        minl = std::min<uint32_t>(minl, (uint32_t)l);
-    }
-    s->max_len = maxl;
-    s->uniform = maxl == minl;
-    size_t rec_bytes;
-    std::vector<uint2> info;
-    if (s->uniform) {
-        s->uniform_len = maxl;
-        s->stride16 = rec_size16(maxl, vbytes);
-        rec_bytes = (size_t)A->m * s->stride16 * 16u;
-    } else {
-        info.resize((size_t)A->m);
-        uint64_t off = 0;
-        for (int64_t i = 0; i < A->m; ++i) {
-            info[(size_t)i] = make_uint2((uint32_t)off, (uint32_t)s->h_len[(size_t)i]);
-            off += rec_size16((uint32_t)s->h_len[(size_t)i], vbytes);
-            if (off >= (1ull << 32)) {
-                free_all(s.get());
-                return fail(ASYRK_E_TooLarge, "row records exceed 64 GiB");
-            }
-        }
-        rec_bytes = (size_t)off * 16u;
-    }
     cudaStream_t st = s->stream;
-    s->rec = dalloc<unsigned char>(rec_bytes);
-    s->rec_bytes = rec_bytes;
-    if (!s->uniform) {
-        s->row_info = dalloc<uint2>(info.size());
-        CK(cudaMemcpyAsync(s->row_info, info.data(), info.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
-    }
-    // raw upload (the reference's int64/fp64 arrays), then pack on the device
+    // Overlapped build: the host scan of row lengths runs on a thread, and the
+    // column sort (CSC / SELL-columns, needs only row_ptr + col_idx) runs on an
+    // aux stream while the values are still being staged (runtime.h Stager).
     long long* d_rp = dalloc<long long>((size_t)A->m + 1);
     int32_t* d_col = dalloc<int32_t>((size_t)A->nnz);
     double* d_val = dalloc<double>((size_t)A->nnz);
     double* d_b = dalloc<double>((size_t)A->m);
     s->row_norm = dalloc<double>((size_t)A->m);
-    // pinned, multithreaded staging; int64 columns cross PCIe as int32 (runtime.h)
-    Stager& up = Stager::get();
-    up.upload(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, st);
-    up.upload_narrow(d_col, A->col_idx, (size_t)A->nnz, st);
-    up.upload(d_val, A->values, (size_t)A->nnz * 8, st);
-    up.upload(s->row_norm, A->row_norm, (size_t)A->m * 8, st);
-    if (b) up.upload(d_b, b, (size_t)A->m * 8, st);
-    else CK(cudaMemsetAsync(d_b, 0, (size_t)A->m * 8, st));
-    launch_pack_records(d_rp, d_col, d_val, s->row_norm, d_b, A->m, s->uniform ? nullptr : s->row_info, s->stride16,
-                        s->uniform_len, precision, s->rec, st);
-    CK(cudaGetLastError());
-    // CSC (stable by column => rows ascending within each column)
     int32_t* keys = dalloc<int32_t>((size_t)A->nnz);
     int32_t* idx = dalloc<int32_t>((size_t)A->nnz);
     int32_t* keys_s = dalloc<int32_t>((size_t)A->nnz);
     int32_t* idx_s = dalloc<int32_t>((size_t)A->nnz);
     int32_t* row_id = dalloc<int32_t>((size_t)A->nnz);
-    launch_iota_cols(d_col, A->nnz, keys, idx, st);
-    launch_row_ids(d_rp, A->m, row_id, st);
-    int end_bit = 1;
-    while ((1ll << end_bit) < A->n) ++end_bit;
     const size_t tb = csc_sort_temp_bytes(A->nnz);
     unsigned char* temp = dalloc<unsigned char>(tb);
-    csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, st);
     long long* col_ptr = dalloc<long long>((size_t)A->n + 1);
     int32_t* csc_row = dalloc<int32_t>((size_t)A->nnz);
     double* csc_val = dalloc<double>((size_t)A->nnz);
-    launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, st);
-    launch_col_hist(keys_s, A->nnz, A->n, col_ptr, st);
-    // SELL-32 columns for the monitor's coalesced thread-per-column pass
     const long long groups = (A->n + 31) / 32;
     s->col_len = dalloc<int32_t>((size_t)A->n);
     s->grp_off = dalloc<long long>((size_t)groups + 1);
     long long* grp_size = dalloc<long long>((size_t)groups + 1);
-    CK(cudaMemsetAsync(grp_size, 0, ((size_t)groups + 1) * 8, st));
-    launch_sell_len(col_ptr, A->n, s->col_len, grp_size, st);
     const size_t stb = scan_temp_bytes(groups + 1);
     unsigned char* stemp = dalloc<unsigned char>(stb);
-    exclusive_scan(stemp, stb, grp_size, s->grp_off, groups + 1, st);
+    const long long rgroups = (A->m + 31) / 32;
+    s->row_len = dalloc<int32_t>((size_t)A->m);
+    s->rgrp_off = dalloc<long long>((size_t)rgroups + 1);
+    long long* rgrp_size = dalloc<long long>((size_t)rgroups + 1);
+    const size_t rstb = scan_temp_bytes(rgroups + 1);
+    unsigned char* rstemp = dalloc<unsigned char>(rstb);
+    s->b = dalloc<double>((size_t)A->m);
+
+    // host scan: row lengths, layout, row-SELL size (sell_len_kernel's 32 * max per group)
+    struct Scan {
+        int64_t zero_row = -1;
+        uint32_t maxl = 0, minl = UINT32_MAX;
+        bool too_large = false;
+        size_t rec_bytes = 0;
+        long long rsell_total = 0;
+        std::vector<uint2> info;
+    } sc;
+    s->h_len.resize((size_t)A->m);
+    std::thread scan_thr([&] {
+        s->h_norm.assign(A->row_norm, A->row_norm + A->m);
+        for (int64_t g = 0; g < rgroups && sc.zero_row < 0; ++g) {
+            uint32_t gmax = 0;
+            for (int64_t i = g * 32; i < std::min<int64_t>(A->m, g * 32 + 32); ++i) {
+                const int64_t l = A->row_ptr[i + 1] - A->row_ptr[i];
+                if (l <= 0) {
+                    sc.zero_row = i;
+                    break;
+                }
+                s->h_len[(size_t)i] = (int32_t)l;
+                gmax = std::max<uint32_t>(gmax, (uint32_t)l);
+                sc.minl = std::min<uint32_t>(sc.minl, (uint32_t)l);
+            }
+            sc.maxl = std::max(sc.maxl, gmax);
+            sc.rsell_total += 32ll * gmax;
+        }
+        if (sc.zero_row >= 0) return;
+        if (sc.maxl == sc.minl) {
+            sc.rec_bytes = (size_t)A->m * rec_size16(sc.maxl, vbytes) * 16u;
+            return;
+        }
+        sc.info.resize((size_t)A->m);
+        uint64_t off = 0;
+        for (int64_t i = 0; i < A->m; ++i) {
+            sc.info[(size_t)i] = make_uint2((uint32_t)off, (uint32_t)s->h_len[(size_t)i]);
+            off += rec_size16((uint32_t)s->h_len[(size_t)i], vbytes);
+            if (off >= (1ull << 32)) {
+                sc.too_large = true;
+                return;
+            }
+        }
+        sc.rec_bytes = (size_t)off * 16u;
+    });
+    struct Join {
+        std::thread& t;
+        ~Join() {
+            if (t.joinable()) t.join();
+        }
+    } join_scan{scan_thr};
+
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_cols = nullptr, ev_sorted = nullptr;
+    struct AuxGuard {
+        cudaStream_t& a;
+        cudaEvent_t &e1, &e2;
+        ~AuxGuard() {
+            if (a) {
+                cudaStreamSynchronize(a);
+                cudaStreamDestroy(a);
+            }
+            if (e1) cudaEventDestroy(e1);
+            if (e2) cudaEventDestroy(e2);
+        }
+    } aux_guard{aux, ev_cols, ev_sorted};
+    CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
+
+    // pinned, multithreaded staging; int64 columns cross PCIe as int32 (runtime.h)
+    Stager& up = Stager::get();
+    up.upload(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, st);
+    up.upload_narrow(d_col, A->col_idx, (size_t)A->nnz, st);
+    CK(cudaEventRecord(ev_cols, st));
+    // aux: CSC order (stable by column => rows ascending within each column),
+    // column histogram, SELL-32 column groups
+    CK(cudaStreamWaitEvent(aux, ev_cols, 0));
+    launch_iota_cols(d_col, A->nnz, keys, idx, aux);
+    launch_row_ids(d_rp, A->m, row_id, aux);
+    int end_bit = 1;
+    while ((1ll << end_bit) < A->n) ++end_bit;
+    csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, aux);
+    launch_col_hist(keys_s, A->nnz, A->n, col_ptr, aux);
+    CK(cudaMemsetAsync(grp_size, 0, ((size_t)groups + 1) * 8, aux));
+    launch_sell_len(col_ptr, A->n, s->col_len, grp_size, aux);
+    exclusive_scan(stemp, stb, grp_size, s->grp_off, groups + 1, aux);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ev_sorted, aux));
+    // st: the values, norms and b keep streaming meanwhile
+    up.upload(d_val, A->values, (size_t)A->nnz * 8, st);
+    up.upload(s->row_norm, A->row_norm, (size_t)A->m * 8, st);
+    if (b) up.upload(d_b, b, (size_t)A->m * 8, st);
+    else CK(cudaMemsetAsync(d_b, 0, (size_t)A->m * 8, st));
+    CK(cudaMemcpyAsync(s->b, d_b, (size_t)A->m * 8, cudaMemcpyDeviceToDevice, st));
+    phase("upload");
+
+    scan_thr.join();
+    if (sc.zero_row >= 0 || sc.too_large) cudaStreamSynchronize(aux);  // aux still reads buffers free_all releases
+    if (sc.zero_row >= 0) {
+        free_all(s.get());
+        return fail(ASYRK_E_ZeroRow, "row " + std::to_string(sc.zero_row) + " has no nonzeros");
+    }
+    if (sc.too_large) {
+        free_all(s.get());
+        return fail(ASYRK_E_TooLarge, "row records exceed 64 GiB");
+    }
+    s->max_len = sc.maxl;
+    s->uniform = sc.maxl == sc.minl;
+    if (s->uniform) {
+        s->uniform_len = sc.maxl;
+        s->stride16 = rec_size16(sc.maxl, vbytes);
+    }
+    s->rec = dalloc<unsigned char>(sc.rec_bytes);
+    s->rec_bytes = sc.rec_bytes;
+    if (!s->uniform) {
+        s->row_info = dalloc<uint2>(sc.info.size());
+        CK(cudaMemcpyAsync(s->row_info, sc.info.data(), sc.info.size() * sizeof(uint2), cudaMemcpyHostToDevice, st));
+    }
+    launch_pack_records(d_rp, d_col, d_val, s->row_norm, d_b, A->m, s->uniform ? nullptr : s->row_info, s->stride16,
+                        s->uniform_len, precision, s->rec, st);
+    CK(cudaGetLastError());
+    phase("pack");
+    // SELL-32 rows for the monitor's coalesced thread-per-row pass (r = Ax - b);
+    // keys still holds the CSR-order columns (the sort wrote keys_s)
+    s->rsell_col = dalloc<int32_t>((size_t)sc.rsell_total);
+    s->rsell_val = dalloc<unsigned char>((size_t)sc.rsell_total * vbytes);
+    CK(cudaMemsetAsync(s->rsell_col, 0, (size_t)std::max<long long>(sc.rsell_total, 1) * 4, st));
+    CK(cudaMemsetAsync(rgrp_size, 0, ((size_t)rgroups + 1) * 8, st));
+    launch_sell_len(d_rp, A->m, s->row_len, rgrp_size, st);
+    exclusive_scan(rstemp, rstb, rgrp_size, s->rgrp_off, rgroups + 1, st);
+    CK(cudaStreamWaitEvent(st, ev_sorted, 0));  // keys (iota_cols) and the column sort
+    launch_sell_scatter(d_rp, keys, d_val, s->row_len, s->rgrp_off, A->m, precision, s->rsell_col, s->rsell_val, st);
+    phase("sell rows");
+    // SELL-32 columns for the monitor's coalesced thread-per-column pass
+    launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, st);
     long long sell_total = 0;
-    CK(cudaMemcpyAsync(&sell_total, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
+    CK(cudaMemcpyAsync(&sell_total, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, aux));
+    CK(cudaStreamSynchronize(aux));
     s->sell_row = dalloc<int32_t>((size_t)sell_total);
     s->sell_val = dalloc<unsigned char>((size_t)sell_total * vbytes);
     CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, st));
     launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row, s->sell_val,
                         st);
-    // SELL-32 rows for the monitor's coalesced thread-per-row pass (r = Ax - b)
-    const long long rgroups = (A->m + 31) / 32;
-    s->row_len = dalloc<int32_t>((size_t)A->m);
-    s->rgrp_off = dalloc<long long>((size_t)rgroups + 1);
-    long long* rgrp_size = dalloc<long long>((size_t)rgroups + 1);
-    CK(cudaMemsetAsync(rgrp_size, 0, ((size_t)rgroups + 1) * 8, st));
-    launch_sell_len(d_rp, A->m, s->row_len, rgrp_size, st);
-    const size_t rstb = scan_temp_bytes(rgroups + 1);
-    unsigned char* rstemp = dalloc<unsigned char>(rstb);
-    exclusive_scan(rstemp, rstb, rgrp_size, s->rgrp_off, rgroups + 1, st);
-    long long rsell_total = 0;
-    CK(cudaMemcpyAsync(&rsell_total, s->rgrp_off + rgroups, 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    s->rsell_col = dalloc<int32_t>((size_t)rsell_total);
-    s->rsell_val = dalloc<unsigned char>((size_t)rsell_total * vbytes);
-    CK(cudaMemsetAsync(s->rsell_col, 0, (size_t)std::max<long long>(rsell_total, 1) * 4, st));
-    launch_sell_scatter(d_rp, keys, d_val, s->row_len, s->rgrp_off, A->m, precision, s->rsell_col, s->rsell_val, st);
-    s->b = dalloc<double>((size_t)A->m);
-    CK(cudaMemcpyAsync(s->b, d_b, (size_t)A->m * 8, cudaMemcpyDeviceToDevice, st));
+    phase("sell cols");
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     if (keep_csc) {  // plain CSC stays for the multi-RHS monitor (warp per column)
@@ -432,6 +506,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
                     (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
         pool_free(p, st);
 
+    phase("free temps");
     // solve buffers
     s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
     s->xd = dalloc<double>((size_t)A->n);
@@ -446,6 +521,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
+    phase("solve buffers");
     CK(cudaStreamSynchronize(st));
     *out = s.release();
     return ASYRK_OK;
