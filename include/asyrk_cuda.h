@@ -17,6 +17,8 @@
  *   asyrk_residuals          residuals               ref/include/asyrk/csr.hpp:89-90
  *   asyrk_power_iteration_lambda_max
  *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:131-132
+ *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:47-60 (exact_spectral
+ *                                                    = false; ref/src/stats.cpp:52-130)
  *   asyrk_system_*           (new) device-resident CSR + b handle: the
  *                            "device-CSR cache" the reference has no
  *                            equivalent of (SURVEY.md §8b "Ownership").
@@ -180,6 +182,27 @@ asyrk_status asyrk_residuals(const asyrk_csr_view* A, const double* x, const dou
 asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double tol, int64_t max_iters,
                                               double* lambda_max);
 
+/* compute_stats (stats.hpp:47-60, stats.cpp:52-130) with exact_spectral =
+ * false: every field of SystemStats except lambda_min / sigma_r (dense SVD,
+ * not on the device path). mu, nu, delta, alpha, frob_sq, l_max, l_res and
+ * theta are bit-identical to the reference; lambda_max is the device power
+ * iteration (tol, max_iters = StatsOptions::tol / max_power_iters).
+ * Errors: NotNormalized (A not flagged normalized), ZeroColumn (first empty
+ * column), PowerIterationDiverged. */
+typedef struct asyrk_stats_out {
+    int64_t m, n;
+    double delta;            /* nnz / (m n) */
+    int64_t mu, nu;          /* max row / column nonzero count */
+    double alpha;            /* max_{i,t} theta_i |a_it| ||column t|| */
+    double lambda_max;       /* power iteration on A^T A */
+    double frob_sq;          /* ||A||_F^2, column order */
+    double l_max;            /* max diagonal entry of A^T A */
+    double l_res;            /* max row norm of A^T A */
+    int64_t power_iterations;
+    int64_t* theta;          /* optional caller buffer of m per-row counts */
+} asyrk_stats_out;
+asyrk_status asyrk_compute_stats(const asyrk_csr_view* A, double tol, int64_t max_iters, asyrk_stats_out* out);
+
 /* sweep_threads (parallel.hpp:73-75): one solve per entry of thread_list
  * (must contain 1); out arrays have n_threads entries. */
 asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const double* x0,
@@ -211,6 +234,8 @@ asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x,
 asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t max_iters, double* lambda_max,
                                           int64_t* iterations);
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
+/* compute_stats on a resident fp64 system (see asyrk_compute_stats). */
+asyrk_status asyrk_system_compute_stats(asyrk_system* sys, double tol, int64_t max_iters, asyrk_stats_out* out);
 /* Largest number of worker warps that are co-resident for this system. */
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
 

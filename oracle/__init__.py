@@ -69,6 +69,11 @@ class OracleError(ValueError):
         super().__init__(f"{self.name}: {msg}" if msg else self.name)
 
 
+def _stats_dict(mu, nu, d, theta):
+    return dict(mu=mu, nu=nu, delta=d[0], alpha=d[1], lambda_max=d[2], frob_sq=d[3], l_max=d[4], l_res=d[5],
+                theta=theta)
+
+
 def _p(a, t):
     return a.ctypes.data_as(t) if a is not None else None
 
@@ -154,6 +159,7 @@ class _RefLib(_Lib):
         L.ref_multiply_transpose.argtypes = [C_.c_void_p, _f64p, _f64p]
         L.ref_power_iteration.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _f64p]
         L.ref_stats.argtypes = [C_.c_void_p, C_.c_double, _i64p, _i64p, _f64p, _f64p, _f64p]
+        L.ref_stats_full.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _i64p, _i64p, _f64p, _i64p]
         L.ref_corollary.argtypes = [C_.c_int64, C_.c_int64, C_.c_double, C_.c_double, C_.c_int64, _f64p, _f64p,
                                     _f64p, C_.POINTER(C_.c_int)]
         L.ref_stream_raw.argtypes = [C_.c_uint64, C_.c_uint64, C_.c_int64, _u64p]
@@ -259,6 +265,15 @@ class _RefLib(_Lib):
                                      C_.byref(fs)))
         return dict(mu=mu.value, nu=nu.value, alpha=al.value, lambda_max=lm.value, frob_sq=fs.value)
 
+    def stats_full(self, A, tol=1e-9, max_iters=200000):
+        """compute_stats(exact_spectral=false): every scalar field and theta."""
+        mu, nu = C_.c_int64(), C_.c_int64()
+        d = np.zeros(6)
+        th = np.zeros(A.m, np.int64)
+        self._check(self.L.ref_stats_full(A.handle, tol, max_iters, C_.byref(mu), C_.byref(nu), _p(d, _f64p),
+                                          _p(th, _i64p)))
+        return _stats_dict(mu.value, nu.value, d, th)
+
     def corollary(self, m, mu, alpha, lambda_max, tau):
         rho, psi, gam = C_.c_double(), C_.c_double(), C_.c_double()
         f = C_.c_int()
@@ -341,6 +356,7 @@ class _OracleLib(_Lib):
         L.oc_alias_sample_seq.argtypes = [_f64p, C_.c_int64, C_.c_uint64, C_.c_int64, _i64p]
         L.oc_alias_sample_seq.restype = C_.c_int
         L.oc_rk_step.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_int64, _f64p]
+        L.oc_compute_stats.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _i64p, _i64p, _f64p, _i64p, _i64p]
 
     @staticmethod
     def _check(st):
@@ -426,6 +442,15 @@ class _OracleLib(_Lib):
         lam, it = C_.c_double(), C_.c_int64()
         self._check(self.L.oc_power_iteration(A.handle, tol, max_iters, C_.byref(lam), C_.byref(it)))
         return (lam.value, it.value) if return_iters else lam.value
+
+    def stats_full(self, A, tol=1e-9, max_iters=200000):
+        """oc_compute_stats: the same fields as REF.stats_full."""
+        mu, nu, zc = C_.c_int64(), C_.c_int64(), C_.c_int64(-1)
+        d = np.zeros(6)
+        th = np.zeros(A.m, np.int64)
+        self._check(self.L.oc_compute_stats(A.handle, tol, max_iters, C_.byref(mu), C_.byref(nu), _p(d, _f64p),
+                                            _p(th, _i64p), C_.byref(zc)))
+        return _stats_dict(mu.value, nu.value, d, th)
 
     def corollary(self, m, mu, lambda_max, tau):
         rho, psi, gam = C_.c_double(), C_.c_double(), C_.c_double()

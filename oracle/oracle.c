@@ -138,6 +138,7 @@ enum {
     OC_IndexOutOfRange = 1,
     OC_DuplicateEntry = 2,
     OC_ZeroRow = 3,
+    OC_ZeroColumn = 4,
     OC_NotNormalized = 5,
     OC_DimensionMismatch = 6,
     OC_PowerIterationDiverged = 7,
@@ -668,4 +669,113 @@ void oc_corollary(int64_t m, int64_t mu, double lambda_max, int64_t tau, double*
     *rho = 1.0 + lhs;
     *psi = oc_psi((double)mu, lambda_max, tau, *rho, m);
     *gamma = *feasible ? 1.0 / *psi : 0.0;
+}
+
+/* ref/src/stats.cpp:52-130 (compute_stats, exact_spectral = false): delta,
+ * theta/mu (row counts), CSC (ref csr.cpp:162-185, rows ascending per
+ * column), nu, column norms, frob_sq / l_max in column order, alpha, and
+ * l_res = max_t ||A^T (A e_t)|| with the reference's accumulation order
+ * (rows of column t ascending, each row in CSR order) and its first-touch
+ * order for the sum of squares; lambda_max by power iteration.
+ * d[6] = {delta, alpha, lambda_max, frob_sq, l_max, l_res}. */
+int oc_compute_stats(const oc_csr* A, double tol, int64_t max_iters, int64_t* mu_out, int64_t* nu_out, double* d,
+                     int64_t* theta, int64_t* zero_col) {
+    if (!A->normalized) return OC_NotNormalized;
+    const int64_t m = A->m, n = A->n, nnz = A->nnz;
+    double delta = (double)nnz / ((double)m * (double)n);
+    int64_t mu = 0, nu = 0;
+    for (int64_t i = 0; i < m; ++i) {
+        const int64_t l = A->row_ptr[i + 1] - A->row_ptr[i];
+        if (theta) theta[i] = l;
+        if (l > mu) mu = l;
+    }
+    int64_t* cp = (int64_t*)calloc((size_t)n + 1, 8);
+    int64_t* cur = (int64_t*)malloc((size_t)n * 8);
+    int64_t* crow = (int64_t*)malloc((size_t)(nnz ? nnz : 1) * 8);
+    double* cval = (double*)malloc((size_t)(nnz ? nnz : 1) * 8);
+    double* cn = (double*)malloc((size_t)n * 8);
+    for (int64_t k = 0; k < nnz; ++k) ++cp[A->col[k] + 1];
+    for (int64_t j = 0; j < n; ++j) cp[j + 1] += cp[j];
+    for (int64_t j = 0; j < n; ++j) cur[j] = cp[j];
+    for (int64_t i = 0; i < m; ++i)
+        for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; ++k) {
+            const int64_t dst = cur[A->col[k]]++;
+            crow[dst] = i;
+            cval[dst] = A->val[k];
+        }
+    double frob = 0.0, l_max = 0.0, alpha = 0.0, l_res = 0.0;
+    int st = OC_OK;
+    for (int64_t t = 0; t < n && st == OC_OK; ++t) {
+        const int64_t cnt = cp[t + 1] - cp[t];
+        if (cnt == 0) {
+            if (zero_col) *zero_col = t;
+            st = OC_ZeroColumn;
+            break;
+        }
+        if (cnt > nu) nu = cnt;
+        double c = 0.0;
+        for (int64_t k = cp[t]; k < cp[t + 1]; ++k) c += cval[k] * cval[k];
+        cn[t] = sqrt(c);
+        frob += c;
+        if (l_max < c) l_max = c;
+    }
+    if (st == OC_OK) {
+        for (int64_t i = 0; i < m; ++i) {
+            const double th = (double)(A->row_ptr[i + 1] - A->row_ptr[i]);
+            for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; ++k) {
+                const double cand = th * fabs(A->val[k]) * cn[A->col[k]];
+                if (alpha < cand) alpha = cand;
+            }
+        }
+        double* acc = (double*)calloc((size_t)n, 8);
+        int64_t cap = 1024, cnt_t = 0;
+        int64_t* touched = (int64_t*)malloc((size_t)cap * 8);
+        for (int64_t t = 0; t < n; ++t) {
+            cnt_t = 0;
+            for (int64_t k = cp[t]; k < cp[t + 1]; ++k) {
+                const int64_t i = crow[k];
+                const double av = cval[k];
+                for (int64_t kk = A->row_ptr[i]; kk < A->row_ptr[i + 1]; ++kk) {
+                    const int64_t u = A->col[kk];
+                    if (acc[u] == 0.0) {
+                        if (cnt_t == cap) {
+                            cap *= 2;
+                            touched = (int64_t*)realloc(touched, (size_t)cap * 8);
+                        }
+                        touched[cnt_t++] = u;
+                    }
+                    acc[u] += av * A->val[kk];
+                }
+            }
+            double rs = 0.0;
+            for (int64_t q = 0; q < cnt_t; ++q) {
+                const double x = acc[touched[q]];
+                rs += x * x;
+                acc[touched[q]] = 0.0;
+            }
+            const double r = sqrt(rs);
+            if (l_res < r) l_res = r;
+        }
+        free(acc);
+        free(touched);
+    }
+    free(cp);
+    free(cur);
+    free(crow);
+    free(cval);
+    free(cn);
+    if (st != OC_OK) return st;
+    double lam = 0.0;
+    int64_t iters = 0;
+    st = oc_power_iteration(A, tol, max_iters, &lam, &iters);
+    if (st != OC_OK) return st;
+    *mu_out = mu;
+    *nu_out = nu;
+    d[0] = delta;
+    d[1] = alpha;
+    d[2] = lam;
+    d[3] = frob;
+    d[4] = l_max;
+    d[5] = l_res;
+    return OC_OK;
 }

@@ -246,6 +246,28 @@ int ref_stats(void* hp, double tol, int64_t* mu, int64_t* nu, double* alpha, dou
     });
 }
 
+// compute_stats with exact_spectral=false, every scalar field + theta.
+// d[6] = {delta, alpha, lambda_max, frob_sq, l_max, l_res}
+int ref_stats_full(void* hp, double tol, int64_t max_iters, int64_t* mu, int64_t* nu, double* d, int64_t* theta) {
+    return guarded([&] {
+        StatsOptions o;
+        o.exact_spectral = false;
+        o.tol = tol;
+        o.max_power_iters = max_iters;
+        SystemStats s = compute_stats(static_cast<Handle*>(hp)->A, o);
+        *mu = s.mu;
+        *nu = s.nu;
+        d[0] = s.delta;
+        d[1] = s.alpha;
+        d[2] = s.lambda_max;
+        d[3] = s.frob_sq;
+        d[4] = s.l_max;
+        d[5] = s.l_res;
+        if (theta)
+            for (std::size_t i = 0; i < s.theta.size(); ++i) theta[i] = s.theta[i];
+    });
+}
+
 int ref_corollary(int64_t m, int64_t mu, double alpha, double lambda_max, int64_t tau, double* rho,
                   double* psi, double* gamma, int* feasible) {
     return guarded([&] {

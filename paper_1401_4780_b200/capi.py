@@ -67,6 +67,20 @@ class SolveStats(C.Structure):
                 ("projections", C.c_int64), ("resident_warps", C.c_int32), ("warps", C.c_int32)]
 
 
+class StatsOut(C.Structure):
+    """asyrk_stats_out (include/asyrk_cuda.h; SystemStats, ref stats.hpp:18-37)."""
+
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("delta", C.c_double), ("mu", C.c_int64), ("nu", C.c_int64),
+                ("alpha", C.c_double), ("lambda_max", C.c_double), ("frob_sq", C.c_double), ("l_max", C.c_double),
+                ("l_res", C.c_double), ("power_iterations", C.c_int64), ("theta", C.POINTER(C.c_int64))]
+
+
+def _stats_result(o, theta):
+    d = {f: getattr(o, f) for f, _ in StatsOut._fields_ if f != "theta"}
+    d["theta"] = theta
+    return d
+
+
 class AsyrkError(ValueError):
     def __init__(self, status: int, msg: str):
         self.status = status
@@ -103,6 +117,8 @@ def lib():
         L.asyrk_system_power_iteration.argtypes = [sp, C.c_double, C.c_int64, _f64p, _i64p]
         L.asyrk_system_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_system_max_resident_warps.argtypes = [sp, C.c_int32, _i32p]
+        L.asyrk_system_compute_stats.argtypes = [sp, C.c_double, C.c_int64, C.POINTER(StatsOut)]
+        L.asyrk_compute_stats.argtypes = [C.POINTER(CsrView), C.c_double, C.c_int64, C.POINTER(StatsOut)]
         L.asyrk_solve_parallel.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig),
                                            C.POINTER(TraceOut), C.POINTER(InstrumentOut)]
         L.asyrk_rk_solve.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
@@ -140,7 +156,7 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats",
+    "asyrk_mrhs_last_stats", "asyrk_compute_stats", "asyrk_system_compute_stats",
 ]
 
 
@@ -319,6 +335,12 @@ class System:
             lib().asyrk_system_destroy(self.h)
             self.h = None
 
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
     def __del__(self):
         try:
             self.close()
@@ -377,6 +399,14 @@ class System:
         check(lib().asyrk_system_power_iteration(self.h, tol, max_iters, C.byref(lam), C.byref(it)))
         return lam.value, it.value
 
+    def compute_stats(self, tol=1e-9, max_iters=200000):
+        """compute_stats(exact_spectral=false) on the device (ref stats.cpp:52-130)."""
+        theta = np.zeros(self.m, np.int64)
+        o = StatsOut()
+        o.theta = theta.ctypes.data_as(C.POINTER(C.c_int64))
+        check(lib().asyrk_system_compute_stats(self.h, tol, max_iters, C.byref(o)))
+        return _stats_result(o, theta)
+
     def stats(self):
         s = SolveStats()
         check(lib().asyrk_system_last_stats(self.h, C.byref(s)))
@@ -407,6 +437,15 @@ def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, *
                                max_abs_error=rep.max_abs_error, tolerance=rep.tolerance,
                                consistent=bool(rep.consistent))
     return d
+
+
+def compute_stats(A: HostCsr, tol=1e-9, max_iters=200000):
+    """One-shot asyrk_compute_stats with host buffers (exact_spectral=false)."""
+    theta = np.zeros(A.m, np.int64)
+    o = StatsOut()
+    o.theta = theta.ctypes.data_as(C.POINTER(C.c_int64))
+    check(lib().asyrk_compute_stats(C.byref(A.view()), tol, max_iters, C.byref(o)))
+    return _stats_result(o, theta)
 
 
 def rk_solve_host(A: HostCsr, b, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):

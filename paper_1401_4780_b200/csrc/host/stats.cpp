@@ -1,5 +1,6 @@
-// power_iteration_lambda_max on the device (ref/src/stats.cpp:15-50) and the
-// step-size corollary (ref/src/stepsize.cpp:26-82), scalar host math.
+// compute_stats / power_iteration_lambda_max on the device (ref/src/stats.cpp:
+// 15-130), SystemStats JSON, and the step-size corollary (ref/src/stepsize.cpp:
+// 26-82), scalar host math.
 #include <algorithm>
 #include <cmath>
 #include <numbers>
@@ -7,6 +8,7 @@
 #include "asyrk/error.hpp"
 #include "asyrk/stepsize.hpp"
 #include "asyrk_cuda.h"
+#include "json.hpp"
 
 namespace asyrk {
 
@@ -15,6 +17,85 @@ double power_iteration_lambda_max(const CsrMatrix& A, double tol, index_t max_it
     int64_t iters = 0;
     throw_status(asyrk_system_power_iteration(A.device(0), tol, max_iters, &lam, &iters));
     return lam;
+}
+
+SystemStats compute_stats(const CsrMatrix& A, const StatsOptions& opts) {
+    if (!A.is_normalized())
+        fail(ErrorCode::NotNormalized, "stats are defined for row-normalized matrices; call normalize_rows first");
+    if (opts.exact_spectral)
+        fail(ErrorCode::TooLarge,
+             "exact_spectral needs a dense SVD (ref dense.cpp), which is not on the device path; "
+             "set StatsOptions::exact_spectral = false for the power-iteration lambda_max");
+    SystemStats s;
+    s.theta.resize(static_cast<std::size_t>(A.rows()));
+    asyrk_stats_out o{};
+    o.theta = s.theta.data();
+    throw_status(asyrk_system_compute_stats(A.device(0), opts.tol, opts.max_power_iters, &o));
+    s.m = o.m;
+    s.n = o.n;
+    s.delta = o.delta;
+    s.mu = o.mu;
+    s.nu = o.nu;
+    s.alpha = o.alpha;
+    s.lambda_max = o.lambda_max;
+    s.frob_sq = o.frob_sq;
+    s.l_max = o.l_max;
+    s.l_res = o.l_res;
+    return s;
+}
+
+// ref stats.cpp:132-178 (field names and presence rules of the JSON object)
+std::string SystemStats::to_json() const {
+    json::Object j;
+    j["m"] = json::Value(m);
+    j["n"] = json::Value(n);
+    j["delta"] = json::Value(delta);
+    json::Array th;
+    th.reserve(theta.size());
+    for (index_t t : theta) th.emplace_back(t);
+    j["theta"] = json::Value(std::move(th));
+    j["mu"] = json::Value(mu);
+    j["nu"] = json::Value(nu);
+    j["alpha"] = json::Value(alpha);
+    if (lambda_min) j["lambda_min"] = json::Value(*lambda_min);
+    j["lambda_max"] = json::Value(lambda_max);
+    j["frob_sq"] = json::Value(frob_sq);
+    j["l_max"] = json::Value(l_max);
+    j["l_res"] = json::Value(l_res);
+    if (sigma_r) j["sigma_r"] = json::Value(*sigma_r);
+    return json::dump(json::Value(std::move(j)));
+}
+
+SystemStats SystemStats::from_json(const std::string& text) {
+    json::Value v;
+    try {
+        v = json::parse(text);
+    } catch (const std::exception& e) {
+        fail(ErrorCode::IoError, std::string("bad stats JSON: ") + e.what());
+    }
+    SystemStats s;
+    try {
+        if (!v.is_object()) throw std::runtime_error("not an object");
+        const json::Object& o = v.object();
+        s.m = o.at("m").integer();
+        s.n = o.at("n").integer();
+        s.delta = o.at("delta").number();
+        for (const auto& t : o.at("theta").array()) s.theta.push_back(t.integer());
+        s.mu = o.at("mu").integer();
+        s.nu = o.at("nu").integer();
+        s.alpha = o.at("alpha").number();
+        if (o.count("lambda_min")) s.lambda_min = o.at("lambda_min").number();
+        s.lambda_max = o.at("lambda_max").number();
+        s.frob_sq = o.at("frob_sq").number();
+        s.l_max = o.at("l_max").number();
+        s.l_res = o.at("l_res").number();
+        if (o.count("sigma_r")) s.sigma_r = o.at("sigma_r").number();
+    } catch (const Error&) {
+        throw;
+    } catch (const std::exception& e) {
+        fail(ErrorCode::IoError, std::string("bad stats JSON: ") + e.what());
+    }
+    return s;
 }
 
 double psi(double mu, double lambda_max, index_t tau, double rho, index_t m) {

@@ -146,6 +146,22 @@ void launch_spmv_cols(const CscDev& C, int precision, long long n, const double*
 void launch_dot(const double* a, const double* b, long long n, double* scratch, double* out, cudaStream_t s);
 void launch_power_update(double* v, const double* w, const double* wn_dot, long long n, cudaStream_t s);
 
+// ---- K5: compute_stats (stats.cu)
+struct StatsDev {
+    long long zero_col;                 // first empty column (LLONG_MAX: none)
+    long long nu;                       // max column count
+    long long max_w;                    // max over columns of the sum of its rows' lengths
+    unsigned long long l_max_bits, alpha_bits, l_res_bits;  // non-negative doubles as bits
+    double frob_sq;
+};
+void launch_stats_cols(const CscDev& C, long long n, const int32_t* row_len, double* col_sq, double* col_norm,
+                       StatsDev* out, cudaStream_t s);
+// alpha, frob_sq, l_res; scratch: global hash tables when a table exceeds shared memory
+void launch_stats_rest(const CscDev& C, const CscDev& R, long long m, long long n, const double* col_sq,
+                       const double* col_norm, long long max_w, unsigned char* scratch, size_t scratch_bytes,
+                       StatsDev* out, cudaStream_t s);
+int stats_table_cap(long long max_w, long long n);
+
 // ---- K0: packing
 void launch_pack_records(const long long* row_ptr, const int32_t* col, const double* val,
                          const double* row_norm, const double* b, long long m, const uint2* row_info,

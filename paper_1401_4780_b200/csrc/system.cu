@@ -978,6 +978,69 @@ asyrk_status power_impl(asyrk_system* s, double tol, int64_t max_iters, double* 
                 "power iteration did not converge within " + std::to_string(max_iters) + " iterations");
 }
 
+// compute_stats (ref/src/stats.cpp:52-130, exact_spectral = false), stats.cu
+asyrk_status stats_impl(asyrk_system* s, double tol, int64_t max_iters, asyrk_stats_out* out) {
+    if (!out) return fail(ASYRK_E_InvalidArgument, "null stats output");
+    if (!s->normalized)
+        return fail(ASYRK_E_NotNormalized,
+                    "stats are defined for row-normalized matrices; call normalize_rows first");
+    if (s->precision != P_F64) return fail(ASYRK_E_InvalidArgument, "compute_stats needs an fp64 system");
+    cudaStream_t st = s->stream;
+    AllocStream as(st);
+    double* col_sq = dalloc<double>((size_t)s->n);
+    double* col_norm = dalloc<double>((size_t)s->n);
+    StatsDev* dres = dalloc<StatsDev>(1);
+    unsigned char* scratch = nullptr;
+    struct Free {
+        std::vector<void*> p;
+        cudaStream_t s;
+        ~Free() {
+            for (void* q : p) pool_free(q, s);
+        }
+    } fr{{col_sq, col_norm, dres}, st};
+    StatsDev h{};
+    h.zero_col = LLONG_MAX;
+    CK(cudaMemcpyAsync(dres, &h, sizeof h, cudaMemcpyHostToDevice, st));
+    launch_stats_cols(s->csc(), s->n, s->row_len, col_sq, col_norm, dres, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h, dres, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h.zero_col != LLONG_MAX)
+        return fail(ASYRK_E_ZeroColumn, "column " + std::to_string(h.zero_col) + " has no nonzeros");
+    const size_t tbytes = (size_t)stats_table_cap(h.max_w, s->n) * 16;
+    size_t scratch_bytes = 0;
+    if (tbytes > (200u << 10)) {  // tables past shared memory live in global scratch (8 warps per block)
+        scratch_bytes = std::max<size_t>(8 * tbytes, std::min<size_t>((size_t)1 << 30, 8 * tbytes * 148));
+        scratch = dalloc<unsigned char>(scratch_bytes);
+        fr.p.push_back(scratch);
+    }
+    launch_stats_rest(s->csc(), s->rsell(), s->m, s->n, col_sq, col_norm, h.max_w, scratch, scratch_bytes, dres, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&h, dres, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    asyrk_stats_out o = *out;
+    o.m = s->m;
+    o.n = s->n;
+    o.delta = (double)s->nnz / ((double)s->m * (double)s->n);
+    o.mu = s->max_len;
+    o.nu = h.nu;
+    auto bits = [](unsigned long long b) {
+        double d;
+        std::memcpy(&d, &b, 8);
+        return d;
+    };
+    o.alpha = bits(h.alpha_bits);
+    o.frob_sq = h.frob_sq;
+    o.l_max = bits(h.l_max_bits);
+    o.l_res = bits(h.l_res_bits);
+    if (o.theta)
+        for (int64_t i = 0; i < s->m; ++i) o.theta[i] = s->h_len[(size_t)i];
+    asyrk_status ps = power_impl(s, tol, max_iters, &o.lambda_max, &o.power_iterations);
+    if (ps) return ps;
+    *out = o;
+    return ASYRK_OK;
+}
+
 struct SysGuard {
     asyrk_system* s = nullptr;
     ~SysGuard() {
@@ -1036,6 +1099,20 @@ asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t
                                           int64_t* iterations) {
     if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
     return guarded([&] { return power_impl(sys, tol, max_iters, lambda_max, iterations); });
+}
+
+asyrk_status asyrk_system_compute_stats(asyrk_system* sys, double tol, int64_t max_iters, asyrk_stats_out* out) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return stats_impl(sys, tol, max_iters, out); });
+}
+
+asyrk_status asyrk_compute_stats(const asyrk_csr_view* A, double tol, int64_t max_iters, asyrk_stats_out* out) {
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, nullptr, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return stats_impl(g.s, tol, max_iters, out);
+    });
 }
 
 asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b) {

@@ -13,6 +13,7 @@ Contents (all produced by reference code paths):
   par/<name>/<v>_<s>/*  solve_parallel(threads=1) traces + instrument reports
   res/<name>/*     residuals at a fixed x
   pow/<name>       power_iteration_lambda_max(tol=1e-10)
+  stats/<name>/*   compute_stats(exact_spectral=false): STATS_FIELDS + theta (or error code)
   kat/*            known-answer vectors of the reference unit tests
 """
 import os
@@ -40,6 +41,13 @@ INSTANCES = {
     "delay0_20x12": (20, 12, 0.3, 7),              # test_delay_sim.cpp:28-52
     "accept9_2000x1500": (2000, 1500, 0.01, 90210),  # acceptance.cpp:400-418 (C9)
 }
+
+
+STATS_FIELDS = ["mu", "nu", "delta", "alpha", "lambda_max", "frob_sq", "l_max", "l_res"]
+
+
+def stats_vector(st):
+    return np.array([float(st[k]) for k in STATS_FIELDS])
 
 
 def main():
@@ -96,6 +104,12 @@ def main():
         out[f"res/{name}/r_in"] = np.random.default_rng(seed).standard_normal(n + m)[n:]
         out[f"res/{name}/ATr"] = REF.multiply_transpose(A, out[f"res/{name}/r_in"])
         out[f"pow/{name}"] = np.array([REF.power_iteration(A, 1e-10, 200000)])
+        try:  # compute_stats(exact_spectral=false), stats.cpp:52-130
+            st = REF.stats_full(A, 1e-9, 200000)
+            out[f"stats/{name}/vals"] = stats_vector(st)
+            out[f"stats/{name}/theta"] = st["theta"]
+        except Exception as ex:  # e.g. ZeroColumn on the tiny instances
+            out[f"stats/{name}/error"] = np.array([ex.code])
 
     # ---- known answers of the reference unit tests
     A, bn = REF.build(1, 2, [0, 0], [0, 1], [3.0, 4.0], True, np.array([10.0]))  # test_kaczmarz.cpp:21-30
@@ -105,6 +119,12 @@ def main():
     out["kat/asyrk_update/third_row"] = np.array([REF.asyrk_update(A3, np.zeros(3), 2, 1, 0.5, np.array([1.0, 0.0]))])
     out["kat/asyrk_update/singleton"] = np.array([REF.asyrk_update(A3, np.array([4.0, 0.0, 0.0]), 0, 0, 1.0,
                                                                    np.array([3.0, 0.0]))])
+    # compute_stats known answers (test_stats.cpp:8-44): identity, rows e1, e2, (sqrt(.5), sqrt(.5))
+    # (unit rows: normalize_rows leaves them bit-identical and sets the flag)
+    I3, _ = REF.build(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0], True, None)
+    out["kat/stats/identity3"] = stats_vector(REF.stats_full(I3, 1e-9, 200000))
+    A3n, _ = REF.build(3, 2, [0, 1, 2, 2], [0, 1, 0, 1], [1.0, 1.0, s, s], True, None)
+    out["kat/stats/three_row"] = stats_vector(REF.stats_full(A3n, 1e-9, 200000))
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e3:.0f} kB")

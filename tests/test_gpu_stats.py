@@ -1,0 +1,102 @@
+"""GPU parity of compute_stats (ref/src/stats.cpp:52-130, exact_spectral=false)
+through the C ABI: mu, nu, delta, theta, alpha, frob_sq, l_max and l_res are
+BIT-IDENTICAL to the reference (golden fixtures from oracle/_ref) and to the C
+restatement at larger sizes; lambda_max (power iteration, tol 1e-9) agrees
+within 1e-8 relative (the device dot products use a fixed tree order)."""
+import numpy as np
+import pytest
+
+import oracle
+from conftest import triplets
+
+pytestmark = pytest.mark.gpu
+
+capi = pytest.importorskip("paper_1401_4780_b200.capi")
+FIELDS = ["mu", "nu", "delta", "alpha", "lambda_max", "frob_sq", "l_max", "l_res"]
+EXACT = ["mu", "nu", "delta", "alpha", "frob_sq", "l_max", "l_res"]
+LAMBDA_RTOL = 1e-8
+
+
+def host_csr(inst):
+    return capi.HostCsr(inst["m"], inst["n"], inst["row_ptr"], inst["col_idx"], inst["values"], inst["row_norm"])
+
+
+def check_against(st, ref_vec, ref_theta=None, tag=""):
+    ref = dict(zip(FIELDS, ref_vec))
+    for k in EXACT:
+        assert float(st[k]) == ref[k], (tag, k, st[k], ref[k])
+    assert abs(st["lambda_max"] - ref["lambda_max"]) <= LAMBDA_RTOL * ref["lambda_max"], tag
+    if ref_theta is not None:
+        assert np.array_equal(st["theta"], ref_theta), tag
+
+
+def test_compute_stats_matches_reference_golden(golden, instances):
+    for nm, inst in instances.items():
+        key = f"stats/{nm}/"
+        if key + "error" in golden.files:
+            with pytest.raises(capi.AsyrkError):
+                capi.compute_stats(host_csr(inst))
+            continue
+        st = capi.compute_stats(host_csr(inst), 1e-9, 200000)
+        check_against(st, golden[key + "vals"], golden[key + "theta"], nm)
+        with capi.System(host_csr(inst), inst["b"]) as S:  # resident-handle entry point
+            check_against(S.compute_stats(1e-9, 200000), golden[key + "vals"], golden[key + "theta"], nm)
+
+
+def test_compute_stats_known_answers(golden):
+    # test_stats.cpp:8-44: the identity and rows e1, e2, (sqrt(.5), sqrt(.5))
+    I3 = capi.HostCsr(3, 3, [0, 1, 2, 3], [0, 1, 2], [1.0, 1.0, 1.0])
+    st = capi.compute_stats(I3)
+    check_against(st, golden["kat/stats/identity3"], np.array([1, 1, 1]))
+    s = np.sqrt(0.5)
+    A3 = capi.HostCsr(3, 2, [0, 1, 2, 4], [0, 1, 0, 1], [1.0, 1.0, s, s])
+    st = capi.compute_stats(A3)
+    check_against(st, golden["kat/stats/three_row"], np.array([1, 1, 2]))
+    assert abs(st["alpha"] - 1.7320508075688772) <= 1.8e-14 and abs(st["l_res"] - 1.5811388300841898) <= 1.6e-14
+
+
+def _oracle_of(A):
+    Ac = oracle.C.from_arrays(A.m, A.n, A.row_ptr, A.col_idx, A.values)
+    return oracle.C.stats_full(Ac, 1e-9, 200000)
+
+
+def _vec(d):
+    return np.array([float(d[k]) for k in FIELDS])
+
+
+@pytest.mark.parametrize("m,n,theta,seed", [(20000, 10000, 20, 5), (30000, 12000, 24, 6)])
+def test_compute_stats_matches_oracle_fixed_theta(m, n, theta, seed):
+    A, b, xs = capi.generate_fixed_theta(m, n, theta, seed)
+    ref = _oracle_of(A)
+    check_against(capi.compute_stats(A), _vec(ref), ref["theta"], (m, n))
+
+
+def test_compute_stats_ragged_rows_and_heavy_column():
+    # ragged rows (1..40 nonzeros) plus one column present in every row: the
+    # l_res table of that column exceeds shared memory (global-scratch path)
+    rng = np.random.default_rng(11)
+    m, n = 6000, 5000
+    rows, cols = [], []
+    for i in range(m):
+        k = int(rng.integers(1, 41))
+        c = np.unique(np.concatenate([[0], rng.choice(np.arange(1, n), size=k, replace=False)]))
+        rows.append(np.full(c.size, i))
+        cols.append(c)
+    rows, cols = np.concatenate(rows), np.concatenate(cols)
+    vals = rng.standard_normal(rows.size)
+    Ac, _ = oracle.C.build(m, n, rows, cols, vals, normalize=True)
+    e = oracle.C._export(Ac)
+    A = capi.HostCsr(m, n, e["row_ptr"], e["col_idx"], e["values"], e["row_norm"], normalized=True)
+    ref = oracle.C.stats_full(Ac, 1e-9, 200000)
+    st = capi.compute_stats(A)
+    check_against(st, _vec(ref), ref["theta"], "ragged")
+    assert st["nu"] == m
+
+
+def test_compute_stats_errors():
+    A = capi.HostCsr(2, 2, [0, 1, 2], [0, 1], [2.0, 1.0])  # rows not unit
+    with pytest.raises(capi.AsyrkError, match="NotNormalized"):
+        capi.compute_stats(A)
+    Z = capi.HostCsr(2, 3, [0, 1, 2], [0, 2], [1.0, 1.0])  # column 1 empty
+    with pytest.raises(capi.AsyrkError, match="ZeroColumn: column 1"):
+        capi.compute_stats(Z)

@@ -137,3 +137,49 @@ def test_restatement_matches_reference_random_seeds():
             t1 = R.rk_solve(A, b, np.zeros(30), 15, 0.0, seed, s, xs)
             t2 = C.rk_solve(Ac, b, np.zeros(30), 15, 0.0, seed, s, xs)
             assert np.array_equal(t1["final_x"], t2["final_x"]) and np.array_equal(t1["r_sq"], t2["r_sq"])
+
+
+STATS_FIELDS = ["mu", "nu", "delta", "alpha", "lambda_max", "frob_sq", "l_max", "l_res"]
+
+
+def _stats_vec(st):
+    return np.array([float(st[k]) for k in STATS_FIELDS])
+
+
+def test_compute_stats_bitwise(golden, instances):
+    # compute_stats(exact_spectral=false), stats.cpp:52-130, against the reference's own output
+    for nm, inst in instances.items():
+        A = _build(inst)
+        if f"stats/{nm}/error" in golden.files:
+            with pytest.raises(oracle.OracleError):
+                C.stats_full(A)
+            continue
+        st = C.stats_full(A, 1e-9, 200000)
+        assert np.array_equal(_stats_vec(st), golden[f"stats/{nm}/vals"]), nm
+        assert np.array_equal(st["theta"], golden[f"stats/{nm}/theta"]), nm
+
+
+def test_compute_stats_known_answers(golden):
+    # test_stats.cpp:8-44
+    I3, _ = C.build(3, 3, [0, 1, 2], [0, 1, 2], [1.0, 1.0, 1.0], True)
+    st = C.stats_full(I3)
+    assert np.array_equal(_stats_vec(st), golden["kat/stats/identity3"])
+    assert st["mu"] == 1 and st["nu"] == 1 and abs(st["delta"] - 1 / 3) < 1e-15 and list(st["theta"]) == [1, 1, 1]
+    assert st["alpha"] == 1.0 and st["frob_sq"] == 3.0 and st["l_max"] == 1.0 and st["l_res"] == 1.0
+    s = np.sqrt(0.5)
+    A3, _ = C.build(3, 2, [0, 1, 2, 2], [0, 1, 0, 1], [1.0, 1.0, s, s], True)
+    st = C.stats_full(A3)
+    assert np.array_equal(_stats_vec(st), golden["kat/stats/three_row"])
+    assert list(st["theta"]) == [1, 1, 2] and st["mu"] == 2 and st["nu"] == 2
+    assert abs(st["alpha"] - 1.7320508075688772) <= 1.8e-14
+    assert abs(st["l_max"] - 1.5) <= 1.5e-14 and abs(st["l_res"] - 1.5811388300841898) <= 1.6e-14
+    assert abs(st["lambda_max"] - 2.0) <= 2e-9  # power iteration at tol 1e-9 (the reference test uses the dense SVD)
+
+
+def test_compute_stats_errors():
+    A, _ = C.build(2, 2, [0, 1], [0, 1], [2.0, 1.0], False)
+    with pytest.raises(oracle.OracleError, match="NotNormalized"):
+        C.stats_full(A)
+    Z, _ = C.build(2, 3, [0, 1], [0, 2], [1.0, 1.0], True)  # column 1 empty
+    with pytest.raises(oracle.OracleError, match="ZeroColumn"):
+        C.stats_full(Z)
