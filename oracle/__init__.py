@@ -69,6 +69,50 @@ class OracleError(ValueError):
         super().__init__(f"{self.name}: {msg}" if msg else self.name)
 
 
+class _SimOut(C_.Structure):
+    _fields_ = [("ev_cap", C_.c_int64), ("ev_count", C_.c_int64), ("ev_j", C_.POINTER(C_.c_int64)),
+                ("ev_i", C_.POINTER(C_.c_int64)), ("ev_t", C_.POINTER(C_.c_int64)), ("ev_k", C_.POINTER(C_.c_int64)),
+                ("ev_step", C_.POINTER(C_.c_double)), ("hist_cap", C_.c_int64), ("hist_rows", C_.c_int64),
+                ("history", C_.POINTER(C_.c_double)), ("probe_cap", C_.c_int64), ("probe_count", C_.c_int64),
+                ("probe_iteration", C_.POINTER(C_.c_int64)), ("probe_r_sq", C_.POINTER(C_.c_double))]
+
+
+class _RefSimOut(C_.Structure):
+    """ref_sim_out (ref_shim.cpp): the trace, then the _SimOut fields."""
+
+    _fields_ = [("trace", _Trace)] + _SimOut._fields_
+
+    def __init__(self, t, o):
+        super().__init__()
+        self.trace = t
+        for f, _ in _SimOut._fields_:
+            setattr(self, f, getattr(o, f))
+
+
+DELAY_KINDS = {"fixed": 0, "uniform_random": 1, "max_staleness": 2}
+SIM_VARIANTS = {"single_component": 0, "full_row": 1}
+
+
+def _sim_buffers(n, iterations, tau, probe_every, max_events):
+    ev = {k: np.zeros(max(max_events, 1), np.int64) for k in ["j", "i", "t", "k"]}
+    ev["step"] = np.zeros(max(max_events, 1))
+    hist = np.zeros((tau + 1, n))
+    npr = iterations // probe_every + 1 if probe_every > 0 else 1
+    pit, prs = np.zeros(npr, np.int64), np.zeros(npr)
+    o = _SimOut(max_events, 0, _p(ev["j"], _i64p), _p(ev["i"], _i64p), _p(ev["t"], _i64p), _p(ev["k"], _i64p),
+                _p(ev["step"], _f64p), tau + 1, 0, _p(hist, _f64p), npr, 0, _p(pit, _i64p), _p(prs, _f64p))
+    return o, ev, hist, pit, prs
+
+
+def _sim_result(trace, o, ev, hist, pit, prs):
+    ne = min(o.ev_count, o.ev_cap)
+    trace["events"] = {k: v[:ne].copy() for k, v in ev.items()}
+    trace["history"] = hist[:o.hist_rows].copy()
+    trace["probe_iteration"] = pit[:o.probe_count].copy()
+    trace["probe_r_sq"] = prs[:o.probe_count].copy()
+    return trace
+
+
 def _stats_dict(mu, nu, d, theta):
     return dict(mu=mu, nu=nu, delta=d[0], alpha=d[1], lambda_max=d[2], frob_sq=d[3], l_max=d[4], l_res=d[5],
                 theta=theta)
@@ -160,6 +204,11 @@ class _RefLib(_Lib):
         L.ref_power_iteration.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _f64p]
         L.ref_stats.argtypes = [C_.c_void_p, C_.c_double, _i64p, _i64p, _f64p, _f64p, _f64p]
         L.ref_stats_full.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _i64p, _i64p, _f64p, _i64p]
+        L.ref_simulate.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
+                                   C_.c_uint64, C_.c_int, C_.c_int64, C_.c_int, C_.c_int64, C_.c_void_p]
+        L.ref_monte_carlo.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
+                                      C_.c_int64, C_.c_uint64, C_.c_int, _f64p, _f64p]
+        L.ref_rate_fit.argtypes = [_f64p, C_.c_int64, C_.c_double, _f64p, _f64p]
         L.ref_corollary.argtypes = [C_.c_int64, C_.c_int64, C_.c_double, C_.c_double, C_.c_int64, _f64p, _f64p,
                                     _f64p, C_.POINTER(C_.c_int)]
         L.ref_stream_raw.argtypes = [C_.c_uint64, C_.c_uint64, C_.c_int64, _u64p]
@@ -265,6 +314,32 @@ class _RefLib(_Lib):
                                      C_.byref(fs)))
         return dict(mu=mu.value, nu=nu.value, alpha=al.value, lambda_max=lm.value, frob_sq=fs.value)
 
+    def simulate(self, A, b, x0, gamma, tau, delay, iterations, seed, variant, probe_every=0, probe_r_sq=False,
+                 max_events=0):
+        """simulate (delay_sim.cpp:71-228): trace + events + history + probes."""
+        b, x0 = _f64(b), _f64(x0)
+        o, ev, hist, pit, prs = _sim_buffers(A.n, iterations, tau, probe_every, max_events)
+        t, bufs = self._trace(A.n, iterations // A.m + 3)
+        ro = _RefSimOut(t, o)
+        self._check(self.L.ref_simulate(A.handle, _p(b, _f64p), _p(x0, _f64p), gamma, tau, DELAY_KINDS[delay],
+                                        iterations, seed, SIM_VARIANTS[variant], probe_every, int(probe_r_sq),
+                                        max_events, C_.byref(ro)))
+        return _sim_result(self._trace_dict(ro.trace, bufs, False), ro, ev, hist, pit, prs)
+
+    def monte_carlo(self, A, b, x0, gamma, tau, delay, iterations, runs, base_seed, variant="single_component"):
+        b, x0 = _f64(b), _f64(x0)
+        mean, ratios = np.zeros(iterations + 1), np.zeros(iterations)
+        self._check(self.L.ref_monte_carlo(A.handle, _p(b, _f64p), _p(x0, _f64p), gamma, tau, DELAY_KINDS[delay],
+                                           iterations, runs, base_seed, SIM_VARIANTS[variant], _p(mean, _f64p),
+                                           _p(ratios, _f64p)))
+        return dict(mean_r_sq=mean, ratios=ratios)
+
+    def rate_fit(self, y, stride=1.0):
+        y = _f64(y)
+        sl, r2 = C_.c_double(), C_.c_double()
+        self._check(self.L.ref_rate_fit(_p(y, _f64p), len(y), stride, C_.byref(sl), C_.byref(r2)))
+        return dict(slope=sl.value, r2=r2.value)
+
     def stats_full(self, A, tol=1e-9, max_iters=200000):
         """compute_stats(exact_spectral=false): every scalar field and theta."""
         mu, nu = C_.c_int64(), C_.c_int64()
@@ -357,6 +432,12 @@ class _OracleLib(_Lib):
         L.oc_alias_sample_seq.restype = C_.c_int
         L.oc_rk_step.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_int64, _f64p]
         L.oc_compute_stats.argtypes = [C_.c_void_p, C_.c_double, C_.c_int64, _i64p, _i64p, _f64p, _i64p, _i64p]
+        L.oc_simulate.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
+                                  C_.c_uint64, C_.c_int, C_.c_int64, C_.c_int, C_.c_int64, C_.POINTER(_Trace),
+                                  C_.POINTER(_SimOut)]
+        L.oc_monte_carlo.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
+                                     C_.c_int64, C_.c_uint64, C_.c_int, _f64p, _f64p]
+        L.oc_rate_fit.argtypes = [_f64p, C_.c_int64, C_.c_double, _f64p, _f64p]
 
     @staticmethod
     def _check(st):
@@ -442,6 +523,30 @@ class _OracleLib(_Lib):
         lam, it = C_.c_double(), C_.c_int64()
         self._check(self.L.oc_power_iteration(A.handle, tol, max_iters, C_.byref(lam), C_.byref(it)))
         return (lam.value, it.value) if return_iters else lam.value
+
+    def simulate(self, A, b, x0, gamma, tau, delay, iterations, seed, variant, probe_every=0, probe_r_sq=False,
+                 max_events=0):
+        b, x0 = _f64(b), _f64(x0)
+        o, ev, hist, pit, prs = _sim_buffers(A.n, iterations, tau, probe_every, max_events)
+        t, bufs = self._trace(A.n, iterations // A.m + 3)
+        self._check(self.L.oc_simulate(A.handle, _p(b, _f64p), _p(x0, _f64p), gamma, tau, DELAY_KINDS[delay],
+                                       iterations, seed, SIM_VARIANTS[variant], probe_every, int(probe_r_sq),
+                                       max_events, C_.byref(t), C_.byref(o)))
+        return _sim_result(self._trace_dict(t, bufs, False), o, ev, hist, pit, prs)
+
+    def monte_carlo(self, A, b, x0, gamma, tau, delay, iterations, runs, base_seed, variant="single_component"):
+        b, x0 = _f64(b), _f64(x0)
+        mean, ratios = np.zeros(iterations + 1), np.zeros(iterations)
+        self._check(self.L.oc_monte_carlo(A.handle, _p(b, _f64p), _p(x0, _f64p), gamma, tau, DELAY_KINDS[delay],
+                                          iterations, runs, base_seed, SIM_VARIANTS[variant], _p(mean, _f64p),
+                                          _p(ratios, _f64p)))
+        return dict(mean_r_sq=mean, ratios=ratios)
+
+    def rate_fit(self, y, stride=1.0):
+        y = _f64(y)
+        sl, r2 = C_.c_double(), C_.c_double()
+        self._check(self.L.oc_rate_fit(_p(y, _f64p), len(y), stride, C_.byref(sl), C_.byref(r2)))
+        return dict(slope=sl.value, r2=r2.value)
 
     def stats_full(self, A, tol=1e-9, max_iters=200000):
         """oc_compute_stats: the same fields as REF.stats_full."""

@@ -144,6 +144,8 @@ enum {
     OC_PowerIterationDiverged = 7,
     OC_NonFinite = 8,
     OC_InvalidGamma = 16,
+    OC_NonPositiveData = 17,
+    OC_InsufficientData = 18,
     OC_InvalidArgument = 24,
 };
 
@@ -777,5 +779,239 @@ int oc_compute_stats(const oc_csr* A, double tol, int64_t max_iters, int64_t* mu
     d[3] = frob;
     d[4] = l_max;
     d[5] = l_res;
+    return OC_OK;
+}
+
+/* ------------------------------------------------------------- delay simulator */
+/* ref/src/delay_sim.cpp:71-228 (simulate), :230-270 (monte_carlo_ratios),
+ * :272-338 (rate_fit). Delay kinds: 0 fixed, 1 uniform_random, 2
+ * max_staleness (delay_sim.hpp:17); variant 0 single_component, 1 full_row.
+ * LiveResidual (delay_sim.cpp:27-60): r = Ax - b with a running r_sq, bumped
+ * column by column (CSC order, rows ascending) and recomputed at every epoch. */
+typedef struct {
+    int64_t ev_cap, ev_count;
+    int64_t *ev_j, *ev_i, *ev_t, *ev_k;
+    double* ev_step;
+    int64_t hist_cap, hist_rows;
+    double* history;
+    int64_t probe_cap, probe_count;
+    int64_t* probe_iteration;
+    double* probe_r_sq;
+} oc_sim_extra;
+
+typedef struct {
+    int64_t *cp, *row;
+    double* val;
+    double *r, r_sq;
+    const double* b;
+} oc_live;
+
+static void live_recompute(oc_live* L, const oc_csr* A, const double* x) {
+    oc_multiply(A, x, L->r);
+    L->r_sq = 0.0;
+    for (int64_t i = 0; i < A->m; ++i) {
+        L->r[i] -= L->b[i];
+        L->r_sq += L->r[i] * L->r[i];
+    }
+}
+
+static void live_bump(oc_live* L, int64_t t, double delta) {
+    for (int64_t k = L->cp[t]; k < L->cp[t + 1]; ++k) {
+        const int64_t i = L->row[k];
+        L->r_sq -= L->r[i] * L->r[i];
+        L->r[i] += L->val[k] * delta;
+        L->r_sq += L->r[i] * L->r[i];
+    }
+}
+
+static void live_init(oc_live* L, const oc_csr* A, const double* b, const double* x) {
+    const int64_t n = A->n, nnz = A->nnz;
+    L->cp = (int64_t*)calloc((size_t)n + 1, 8);
+    L->row = (int64_t*)malloc((size_t)(nnz ? nnz : 1) * 8);
+    L->val = (double*)malloc((size_t)(nnz ? nnz : 1) * 8);
+    L->r = (double*)malloc((size_t)A->m * 8);
+    L->b = b;
+    int64_t* cur = (int64_t*)malloc((size_t)n * 8);
+    for (int64_t k = 0; k < nnz; ++k) ++L->cp[A->col[k] + 1];
+    for (int64_t j = 0; j < n; ++j) L->cp[j + 1] += L->cp[j];
+    for (int64_t j = 0; j < n; ++j) cur[j] = L->cp[j];
+    for (int64_t i = 0; i < A->m; ++i)
+        for (int64_t k = A->row_ptr[i]; k < A->row_ptr[i + 1]; ++k) {
+            const int64_t d = cur[A->col[k]]++;
+            L->row[d] = i;
+            L->val[d] = A->val[k];
+        }
+    free(cur);
+    live_recompute(L, A, x);
+}
+
+static void live_free(oc_live* L) {
+    free(L->cp);
+    free(L->row);
+    free(L->val);
+    free(L->r);
+}
+
+int oc_simulate(const oc_csr* A, const double* b, const double* x0, double gamma, int64_t tau, int kind,
+                int64_t iterations, uint64_t seed, int variant, int64_t probe_every, int probe_r_sq,
+                int64_t max_events, oc_trace* tr, oc_sim_extra* ex) {
+    const int64_t m = A->m, n = A->n;
+    if (!A->normalized) return OC_NotNormalized;
+    if (gamma < 0.0) return OC_InvalidGamma;
+    if (iterations < 1 || tau < 0) return OC_InvalidArgument;
+    const int64_t ring_len = tau + 1;
+    oc_mt64 g;
+    oc_make_stream(&g, seed, 0);
+    double* x = (double*)malloc((size_t)n * 8);
+    double* ring = (double*)malloc((size_t)(ring_len * n) * 8);
+    memcpy(x, x0, (size_t)n * 8);
+    memcpy(ring, x, (size_t)n * 8);
+    const int probing = probe_every > 0 && probe_r_sq;
+    oc_live live;
+    int have_live = probing;
+    if (have_live) live_init(&live, A, b, x);
+    tr->count = 0;
+    ex->ev_count = 0;
+    ex->probe_count = 0;
+#define OC_PROBE(jj)                                                              \
+    do {                                                                          \
+        const int64_t q_ = ex->probe_count++;                                     \
+        if (q_ < ex->probe_cap) {                                                 \
+            ex->probe_iteration[q_] = (jj);                                       \
+            if (ex->probe_r_sq) ex->probe_r_sq[q_] = live.r_sq;                   \
+        }                                                                         \
+    } while (0)
+    const double t0 = now_s();
+    double rs;
+    int st = record(tr, A, x, b, NULL, 0, 0, t0, &rs);
+    if (st == OC_OK && probing) OC_PROBE(0);
+    for (int64_t j = 0; j < iterations && st == OC_OK; ++j) {
+        const int64_t i = (int64_t)oc_uniform_below(&g, (uint64_t)m);
+        int64_t k;
+        if (kind == 1) {
+            const int64_t d = (int64_t)oc_uniform_below(&g, (uint64_t)(tau + 1));
+            k = j - d > 0 ? j - d : 0;
+        } else {
+            k = j - tau > 0 ? j - tau : 0;
+        }
+        const double* xr = ring + (k % ring_len) * n;
+        const double res = stale_residual(A, xr, b, i);
+        int64_t ev_t;
+        double ev_step;
+        if (variant == 0) {
+            const int64_t theta = A->row_ptr[i + 1] - A->row_ptr[i];
+            const int64_t pick = (int64_t)oc_uniform_below(&g, (uint64_t)theta);
+            const int64_t slot = A->row_ptr[i] + pick;
+            const int64_t t = A->col[slot];
+            const double delta = -gamma * (double)theta * A->val[slot] * res;
+            x[t] += delta;
+            if (have_live) live_bump(&live, t, delta);
+            ev_t = t;
+            ev_step = delta;
+        } else {
+            const double c = row_coef(A, i, gamma, res);
+            apply_row(A, i, c, x);
+            if (have_live)
+                for (int64_t q = A->row_ptr[i]; q < A->row_ptr[i + 1]; ++q) live_bump(&live, A->col[q], -c * A->val[q]);
+            ev_t = -1;
+            ev_step = c;
+        }
+        memcpy(ring + ((j + 1) % ring_len) * n, x, (size_t)n * 8);
+        if (ex->ev_count < max_events) {
+            const int64_t e = ex->ev_count++;
+            if (e < ex->ev_cap) {
+                ex->ev_j[e] = j;
+                ex->ev_i[e] = i;
+                ex->ev_t[e] = ev_t;
+                ex->ev_k[e] = k;
+                ex->ev_step[e] = ev_step;
+            }
+        }
+        const int64_t done = j + 1;
+        if (done % m == 0) {
+            st = record(tr, A, x, b, NULL, done / m, done, t0, &rs);
+            if (st != OC_OK) break;
+            if (have_live) live_recompute(&live, A, x);
+        }
+        if (probing && done % probe_every == 0) OC_PROBE(done);
+    }
+    if (st == OC_OK && iterations % m != 0) st = record(tr, A, x, b, NULL, iterations / m + 1, iterations, t0, &rs);
+#undef OC_PROBE
+    if (st == OC_OK) {
+        const int64_t kept = ring_len < iterations + 1 ? ring_len : iterations + 1;
+        ex->hist_rows = kept;
+        int64_t row = 0;
+        for (int64_t idx = iterations - kept + 1; idx <= iterations; ++idx, ++row)
+            if (row < ex->hist_cap) memcpy(ex->history + row * n, ring + (idx % ring_len) * n, (size_t)n * 8);
+        if (tr->final_x) memcpy(tr->final_x, x, (size_t)n * 8);
+    }
+    if (have_live) live_free(&live);
+    free(x);
+    free(ring);
+    return st;
+}
+
+int oc_monte_carlo(const oc_csr* A, const double* b, const double* x0, double gamma, int64_t tau, int kind,
+                   int64_t iterations, int64_t runs, uint64_t base_seed, int variant, double* mean_r_sq,
+                   double* ratios) {
+    if (runs < 100) return OC_InsufficientData;
+    const int64_t K = iterations;
+    double* pr = (double*)malloc((size_t)(K + 1) * 8);
+    int64_t* pi = (int64_t*)malloc((size_t)(K + 1) * 8);
+    for (int64_t j = 0; j <= K; ++j) mean_r_sq[j] = 0.0;
+    int st = OC_OK;
+    for (int64_t r = 0; r < runs && st == OC_OK; ++r) {
+        oc_trace tr;
+        memset(&tr, 0, sizeof tr);
+        oc_sim_extra ex;
+        memset(&ex, 0, sizeof ex);
+        ex.probe_cap = K + 1;
+        ex.probe_iteration = pi;
+        ex.probe_r_sq = pr;
+        st = oc_simulate(A, b, x0, gamma, tau, kind, iterations, base_seed + (uint64_t)r, variant, 1, 1, 0, &tr, &ex);
+        if (st == OC_OK)
+            for (int64_t j = 0; j <= K; ++j) mean_r_sq[j] += pr[j];
+    }
+    free(pr);
+    free(pi);
+    if (st != OC_OK) return st;
+    const double inv = 1.0 / (double)runs;
+    for (int64_t j = 0; j <= K; ++j) mean_r_sq[j] *= inv;
+    for (int64_t j = 0; j < K; ++j) {
+        const double a = mean_r_sq[j], c = mean_r_sq[j + 1];
+        ratios[j] = a == 0.0 ? (c == 0.0 ? 1.0 : INFINITY) : c / a;
+    }
+    return OC_OK;
+}
+
+int oc_rate_fit(const double* y, int64_t n, double stride, double* slope, double* r2) {
+    if (n < 20) return OC_InsufficientData;
+    if (!(stride > 0.0)) return OC_InvalidArgument;
+    double* ly = (double*)malloc((size_t)n * 8);
+    for (int64_t k = 0; k < n; ++k) {
+        if (!(y[k] > 0.0)) {
+            free(ly);
+            return OC_NonPositiveData;
+        }
+        ly[k] = log(y[k]);
+    }
+    const double shift = ly[0];
+    for (int64_t k = 0; k < n; ++k) ly[k] -= shift;
+    double sx = 0.0, sy = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+        sx += (double)k;
+        sy += ly[k];
+    }
+    const double mx = sx / (double)n, my = sy / (double)n;
+    double sxx = 0.0, sxy = 0.0, syy = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+        const double dx = (double)k - mx, dy = ly[k] - my;
+        sxx += dx * dx;
+        sxy += dx * dy;
+        syy += dy * dy;
+    }
+    *slope = sxy / sxx / stride;
+    *r2 = syy == 0.0 ? 1.0 : 1.0 - (syy - sxy * sxy / sxx) / syy;
+    free(ly);
     return OC_OK;
 }

@@ -10,6 +10,7 @@
 //   corollary_params                           (ref/src/stepsize.cpp:59-82)
 //   gen_sparse_gaussian                        (ref/src/datagen.cpp:13-137)
 //   AliasTable, make_stream/uniform_below      (ref/src/kaczmarz.cpp:14-61, rng.hpp)
+//   simulate / monte_carlo_ratios / rate_fit   (ref/src/delay_sim.cpp:71-338)
 // Nothing here is shipped; the product never links this library.
 #include <cstdint>
 #include <cstring>
@@ -18,6 +19,7 @@
 
 #include "asyrk/csr.hpp"
 #include "asyrk/datagen.hpp"
+#include "asyrk/delay_sim.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk/kaczmarz.hpp"
 #include "asyrk/parallel.hpp"
@@ -335,6 +337,89 @@ int ref_asyrk_update(void* hp, const double* b, int64_t i, int64_t t, double gam
         const CsrMatrix& A = static_cast<Handle*>(hp)->A;
         *out = asyrk_update(A, {b, static_cast<std::size_t>(A.rows())}, i, t, gamma,
                             {x, static_cast<std::size_t>(A.cols())});
+    });
+}
+
+// ---- bounded-delay simulator (delay_sim.hpp:13-96)
+struct ref_sim_out {
+    ref_trace trace;
+    int64_t ev_cap, ev_count;
+    int64_t *ev_j, *ev_i, *ev_t, *ev_k;
+    double* ev_step;
+    int64_t hist_cap, hist_rows;  // rows of n
+    double* history;
+    int64_t probe_cap, probe_count;
+    int64_t* probe_iteration;
+    double* probe_r_sq;
+};
+
+static DelayModel delay_of(int kind, int64_t tau) {
+    if (kind == 1) return DelayModel::uniform_random(tau);
+    if (kind == 2) return DelayModel::max_staleness(tau);
+    return DelayModel::fixed(tau);
+}
+
+static StepParams params_of(double gamma, int64_t tau) {
+    StepParams p;
+    p.tau = tau;
+    p.gamma = gamma;
+    p.feasible = true;
+    return p;
+}
+
+// variant: 0 single_component, 1 full_row (UpdateVariant order, kaczmarz.hpp:20)
+int ref_simulate(void* hp, const double* b, const double* x0, double gamma, int64_t tau, int kind,
+                 int64_t iterations, uint64_t seed, int variant, int64_t probe_every, int probe_r_sq,
+                 int64_t max_events, ref_sim_out* out) {
+    return guarded([&] {
+        const CsrMatrix& A = static_cast<Handle*>(hp)->A;
+        SimOptions o;
+        o.probe_every = probe_every;
+        o.probe_r_sq = probe_r_sq != 0;
+        o.max_events = max_events;
+        SimRun r = simulate(A, std::span<const double>(b, (size_t)A.rows()),
+                            std::span<const double>(x0, (size_t)A.cols()), params_of(gamma, tau), delay_of(kind, tau),
+                            iterations, seed, variant ? SimVariant::full_row : SimVariant::single_component, o);
+        dump_trace(r.trace, &out->trace);
+        out->ev_count = (int64_t)r.events.size();
+        for (int64_t k = 0; k < std::min(out->ev_cap, out->ev_count); ++k) {
+            const auto& e = r.events[(size_t)k];
+            out->ev_j[k] = e.j;
+            out->ev_i[k] = e.i;
+            out->ev_t[k] = e.t;
+            out->ev_k[k] = e.k;
+            out->ev_step[k] = e.step;
+        }
+        out->hist_rows = (int64_t)r.history.size();
+        for (int64_t k = 0; k < std::min(out->hist_cap, out->hist_rows); ++k)
+            std::memcpy(out->history + k * A.cols(), r.history[(size_t)k].data(), (size_t)A.cols() * 8);
+        out->probe_count = (int64_t)r.probe_iteration.size();
+        for (int64_t k = 0; k < std::min(out->probe_cap, out->probe_count); ++k) {
+            out->probe_iteration[k] = r.probe_iteration[(size_t)k];
+            if (o.probe_r_sq) out->probe_r_sq[k] = r.probe_r_sq[(size_t)k];
+        }
+    });
+}
+
+int ref_monte_carlo(void* hp, const double* b, const double* x0, double gamma, int64_t tau, int kind,
+                    int64_t iterations, int64_t runs, uint64_t base_seed, int variant, double* mean_r_sq,
+                    double* ratios) {
+    return guarded([&] {
+        const CsrMatrix& A = static_cast<Handle*>(hp)->A;
+        MonteCarloRatios mc = monte_carlo_ratios(
+            A, std::span<const double>(b, (size_t)A.rows()), std::span<const double>(x0, (size_t)A.cols()),
+            params_of(gamma, tau), delay_of(kind, tau), iterations, runs, base_seed,
+            variant ? SimVariant::full_row : SimVariant::single_component);
+        std::memcpy(mean_r_sq, mc.mean_r_sq.data(), mc.mean_r_sq.size() * 8);
+        std::memcpy(ratios, mc.ratios.data(), mc.ratios.size() * 8);
+    });
+}
+
+int ref_rate_fit(const double* y, int64_t n, double stride, double* slope, double* r2) {
+    return guarded([&] {
+        RateFit f = rate_fit(std::span<const double>(y, (size_t)n), stride);
+        *slope = f.slope;
+        *r2 = f.r2;
     });
 }
 

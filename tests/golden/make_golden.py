@@ -14,6 +14,7 @@ Contents (all produced by reference code paths):
   res/<name>/*     residuals at a fixed x
   pow/<name>       power_iteration_lambda_max(tol=1e-10)
   stats/<name>/*   compute_stats(exact_spectral=false): STATS_FIELDS + theta (or error code)
+  sim_inst/, sim/, mc/, fit/  simulate / monte_carlo_ratios / rate_fit cases (delay_sim.cpp)
   kat/*            known-answer vectors of the reference unit tests
 """
 import os
@@ -48,6 +49,76 @@ STATS_FIELDS = ["mu", "nu", "delta", "alpha", "lambda_max", "frob_sq", "l_max", 
 
 def stats_vector(st):
     return np.array([float(st[k]) for k in STATS_FIELDS])
+
+
+# bounded-delay simulator cases of test_delay_sim.cpp (name: instance, x0 fill, kwargs)
+SIM_INSTANCES = {
+    "d20x12": (20, 12, 0.3, 7),     # test_delay_sim.cpp:28-52, 136-146
+    "d8x5": (8, 5, 0.5, 17),        # :69-124
+    "d6x4": (6, 4, 0.5, 19),        # :126-134
+    "d10x8": (10, 8, 0.4, 23),      # :148-170
+    "d10x6": (10, 6, 0.4, 29),      # :172-181
+    "d30x20": (30, 20, 0.25, 3),    # :213-234
+}
+SIM_CASES = [
+    ("serial_equiv", "d20x12", 0.0, dict(gamma=1.0, tau=0, delay="fixed", iterations=100, seed=42,
+                                          variant="full_row")),
+    ("fixed2_single", "d8x5", 0.0, dict(gamma=0.3, tau=2, delay="fixed", iterations=100, seed=5,
+                                         variant="single_component", max_events=256)),
+    ("maxst3_single", "d8x5", 0.0, dict(gamma=0.3, tau=3, delay="max_staleness", iterations=100, seed=5,
+                                         variant="single_component", max_events=256)),
+    ("unif3_single", "d8x5", 0.0, dict(gamma=0.3, tau=3, delay="uniform_random", iterations=200, seed=5,
+                                        variant="single_component", max_events=256)),
+    ("fixed1_full", "d8x5", 0.0, dict(gamma=0.5, tau=1, delay="fixed", iterations=60, seed=5, variant="full_row",
+                                       max_events=256)),
+    ("history", "d6x4", 0.0, dict(gamma=0.4, tau=2, delay="fixed", iterations=7, seed=11, variant="full_row")),
+    ("partial_epoch", "d20x12", 0.0, dict(gamma=1.0, tau=0, delay="fixed", iterations=25, seed=4,
+                                          variant="full_row")),
+    ("probes", "d10x8", 0.0, dict(gamma=0.5, tau=1, delay="uniform_random", iterations=50, seed=2,
+                                   variant="full_row", probe_every=10, probe_r_sq=True)),
+    ("probes_single", "d30x20", 0.0, dict(gamma=0.06, tau=4, delay="uniform_random", iterations=700, seed=9,
+                                           variant="single_component", probe_every=7, probe_r_sq=True,
+                                           max_events=1000)),
+]
+MC_CASES = [
+    ("frozen", "d10x6", 0.5, dict(gamma=0.0, tau=2, delay="uniform_random", iterations=5, runs=100, base_seed=77)),
+    ("stale8", "d30x20", 0.0, dict(gamma=0.06, tau=8, delay="max_staleness", iterations=1200, runs=200,
+                                    base_seed=11)),
+    ("unif5_full", "d20x12", 0.0, dict(gamma=0.7, tau=5, delay="uniform_random", iterations=300, runs=100,
+                                        base_seed=3, variant="full_row")),
+]
+
+
+def sim_golden(out):
+    """simulate / monte_carlo_ratios / rate_fit outputs of the reference (delay_sim.cpp)."""
+    insts = {}
+    for nm, (m, n, delta, seed) in SIM_INSTANCES.items():
+        A, b, xs = REF.gen_sparse_gaussian(m, n, delta, seed)
+        e = A.export()
+        insts[nm] = (A, b)
+        p = f"sim_inst/{nm}/"
+        out[p + "shape"] = np.array([m, n])
+        for k in ["row_ptr", "col_idx", "values", "row_norm"]:
+            out[p + k] = e[k]
+        out[p + "b"] = b
+    for case, nm, fill, kw in SIM_CASES:
+        A, b = insts[nm]
+        r = REF.simulate(A, b, np.full(A.n, fill), **kw)
+        q = f"sim/{case}/"
+        for k in ["epoch_index", "r_sq", "grad_sq", "updates_applied", "final_x", "history", "probe_iteration",
+                  "probe_r_sq"]:
+            out[q + k] = r[k]
+        for k, v in r["events"].items():
+            out[q + "ev_" + k] = v
+    for case, nm, fill, kw in MC_CASES:
+        A, b = insts[nm]
+        r = REF.monte_carlo(A, b, np.full(A.n, fill), **kw)
+        out[f"mc/{case}/mean_r_sq"] = r["mean_r_sq"]
+        out[f"mc/{case}/ratios"] = r["ratios"]
+    y = np.exp(-0.1 * np.arange(40)) * (1 + 0.01 * np.sin(np.arange(40)))
+    out["fit/y"] = y
+    f = REF.rate_fit(y, 3.0)
+    out["fit/vals"] = np.array([f["slope"], f["r2"]])
 
 
 def main():
@@ -125,6 +196,7 @@ def main():
     out["kat/stats/identity3"] = stats_vector(REF.stats_full(I3, 1e-9, 200000))
     A3n, _ = REF.build(3, 2, [0, 1, 2, 2], [0, 1, 0, 1], [1.0, 1.0, s, s], True, None)
     out["kat/stats/three_row"] = stats_vector(REF.stats_full(A3n, 1e-9, 200000))
+    sim_golden(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e3:.0f} kB")

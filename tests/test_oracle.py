@@ -183,3 +183,85 @@ def test_compute_stats_errors():
     Z, _ = C.build(2, 3, [0, 1], [0, 2], [1.0, 1.0], True)  # column 1 empty
     with pytest.raises(oracle.OracleError, match="ZeroColumn"):
         C.stats_full(Z)
+
+
+# ---------------------------------------------------------------- bounded-delay simulator (delay_sim.cpp)
+SIM_KEYS = ["epoch_index", "r_sq", "grad_sq", "updates_applied", "final_x", "history", "probe_iteration",
+            "probe_r_sq"]
+
+
+def sim_instance(golden, nm):
+    p = f"sim_inst/{nm}/"
+    m, n = (int(v) for v in golden[p + "shape"])
+    A = C.from_arrays(m, n, golden[p + "row_ptr"], golden[p + "col_idx"], golden[p + "values"])
+    return A, golden[p + "b"]
+
+
+def _sim_cases():
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "golden"))
+    import make_golden  # noqa: E402  (case table only; no reference access)
+
+    return make_golden.SIM_CASES, make_golden.MC_CASES
+
+
+def test_simulate_bitwise(golden):
+    sim_cases, _ = _sim_cases()
+    for case, nm, fill, kw in sim_cases:
+        A, b = sim_instance(golden, nm)
+        r = C.simulate(A, b, np.full(A.n, fill), **kw)
+        for k in SIM_KEYS:
+            assert np.array_equal(r[k], golden[f"sim/{case}/{k}"]), (case, k)
+        for k, v in r["events"].items():
+            assert np.array_equal(v, golden[f"sim/{case}/ev_{k}"]), (case, k)
+
+
+def test_simulate_reference_properties(golden):
+    # test_delay_sim.cpp:28-52: zero delay + full_row == rk_solve(uniform), bitwise
+    A, b = sim_instance(golden, "d20x12")
+    serial = C.rk_solve(A, b, np.zeros(12), 5, 0.0, 42, "uniform")
+    sim = C.simulate(A, b, np.zeros(12), 1.0, 0, "fixed", 100, 42, "full_row")
+    for k in ["epoch_index", "r_sq", "grad_sq", "updates_applied", "final_x"]:
+        assert np.array_equal(sim[k], serial[k]), k
+    # :126-134 history newest last; :136-146 trailing partial epoch
+    A6, b6 = sim_instance(golden, "d6x4")
+    h = C.simulate(A6, b6, np.zeros(4), 0.4, 2, "fixed", 7, 11, "full_row")
+    assert h["history"].shape == (3, 4) and np.array_equal(h["history"][-1], h["final_x"])
+    p = C.simulate(A, b, np.zeros(12), 1.0, 0, "fixed", 25, 4, "full_row")
+    assert list(p["epoch_index"]) == [0, 1, 2] and list(p["updates_applied"]) == [0, 20, 25]
+    # :54-67 gamma = 0 freezes the iterate
+    A10, b10 = sim_instance(golden, "d10x6")
+    f = C.simulate(A10, b10, np.ones(6), 0.0, 2, "uniform_random", 50, 3, "single_component", max_events=1000)
+    assert np.array_equal(f["final_x"], np.ones(6)) and len(f["events"]["j"]) == 50
+    assert np.all(f["events"]["step"] == 0.0)
+
+
+def test_monte_carlo_bitwise(golden):
+    _, mc_cases = _sim_cases()
+    for case, nm, fill, kw in mc_cases:
+        A, b = sim_instance(golden, nm)
+        r = C.monte_carlo(A, b, np.full(A.n, fill), **kw)
+        assert np.array_equal(r["mean_r_sq"], golden[f"mc/{case}/mean_r_sq"]), case
+        assert np.array_equal(r["ratios"], golden[f"mc/{case}/ratios"]), case
+    assert np.all(golden["mc/frozen/ratios"] == 1.0)  # test_delay_sim.cpp:172-181
+
+
+def test_rate_fit_and_errors(golden):
+    f = C.rate_fit(golden["fit/y"], 3.0)
+    assert np.array_equal(np.array([f["slope"], f["r2"]]), golden["fit/vals"])
+    g = C.rate_fit(0.8 ** np.arange(100))  # test_delay_sim.cpp:236-250
+    assert abs(g["slope"] - np.log(0.8)) <= 1e-12 * abs(np.log(0.8)) and abs(g["r2"] - 1.0) <= 1e-12
+    assert C.rate_fit(np.full(50, 3.25)) == {"slope": 0.0, "r2": 1.0}
+    with pytest.raises(oracle.OracleError, match="InsufficientData"):
+        C.rate_fit(np.ones(10))
+    z = np.ones(25)
+    z[7] = 0.0
+    with pytest.raises(oracle.OracleError, match="NonPositiveData"):
+        C.rate_fit(z)
+    A, b = sim_instance(golden, "d10x6")
+    with pytest.raises(oracle.OracleError, match="InsufficientData"):
+        C.monte_carlo(A, b, np.zeros(6), 0.1, 1, "fixed", 5, 50, 1)
+    with pytest.raises(oracle.OracleError, match="InvalidGamma"):
+        C.simulate(A, b, np.zeros(6), -0.1, 1, "fixed", 5, 1, "full_row")
+    with pytest.raises(oracle.OracleError, match="InvalidArgument"):
+        C.simulate(A, b, np.zeros(6), 0.1, 1, "fixed", 0, 1, "full_row")
