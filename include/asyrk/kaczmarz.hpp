@@ -20,6 +20,15 @@ inline constexpr index_t kAllComponents = -1;
 
 enum class UpdateVariant { single_component, full_row };
 
+/// What one update event touches (ref kaczmarz.hpp:22-29).
+struct UpdateEvent {
+    index_t j = 0;                // iteration index
+    index_t i = 0;                // selected row
+    index_t t = kAllComponents;   // selected component, kAllComponents for the row
+    index_t k = 0;                // iterate index the residual was read from
+    double step = 0.0;            // single component: the increment; row: the multiplier c
+};
+
 /// Walker alias sampler over a fixed nonnegative weight vector
 /// (ref kaczmarz.hpp:32-41); the construction order matches the reference so
 /// seeded draws are identical.

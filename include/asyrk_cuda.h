@@ -19,6 +19,9 @@
  *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:131-132
  *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:47-60 (exact_spectral
  *                                                    = false; ref/src/stats.cpp:52-130)
+ *   asyrk_simulate           simulate                ref/include/asyrk/delay_sim.hpp:61-71
+ *   asyrk_monte_carlo_ratios monte_carlo_ratios      ref/include/asyrk/delay_sim.hpp:81-88
+ *   asyrk_rate_fit           rate_fit                ref/include/asyrk/delay_sim.hpp:95
  *   asyrk_system_*           (new) device-resident CSR + b handle: the
  *                            "device-CSR cache" the reference has no
  *                            equivalent of (SURVEY.md §8b "Ownership").
@@ -203,6 +206,50 @@ typedef struct asyrk_stats_out {
 } asyrk_stats_out;
 asyrk_status asyrk_compute_stats(const asyrk_csr_view* A, double tol, int64_t max_iters, asyrk_stats_out* out);
 
+/* ---- bounded-delay simulator (delay_sim.hpp, delay_sim.cpp:71-338) -------- *
+ * Deterministic replay of the asynchronous recursion with a delay model
+ * (DelayModel, delay_sim.hpp:17-31), bit-identical to the reference: trace
+ * records, events, history, probes, final_x and Monte-Carlo means. The
+ * projector-based dist_sq (dense SVD) is not available: probe_dist_sq fails
+ * with InvalidArgument as the reference does without a SolutionProjector. */
+typedef struct {
+    double gamma;          /* StepParams::gamma, >= 0 (InvalidGamma) */
+    int64_t tau;           /* DelayModel::tau, >= 0 */
+    int32_t delay;         /* 0 fixed, 1 uniform_random, 2 max_staleness */
+    int32_t variant;       /* 0 single_component, 1 full_row (UpdateVariant) */
+    int64_t iterations;    /* >= 1 */
+    uint64_t seed;         /* simulate: seed; monte_carlo_ratios: base_seed */
+    int64_t probe_every;   /* SimOptions (simulate only) */
+    int32_t probe_r_sq;
+    int32_t probe_dist_sq; /* needs a SolutionProjector: InvalidArgument */
+    int64_t max_events;
+} asyrk_sim_config;
+
+/* SimRun (delay_sim.hpp:44-55). Caller buffers with capacities; counts are
+ * the reference's sizes (at most cap entries are written). history holds
+ * history_rows x n doubles (the last min(tau+1, iterations+1) iterates,
+ * oldest first). Events: t = -1 marks full_row (kAllComponents). */
+typedef struct {
+    asyrk_trace_out trace;
+    int64_t ev_cap, ev_count;
+    int64_t *ev_j, *ev_i, *ev_t, *ev_k;
+    double* ev_step;
+    int64_t history_cap, history_rows;
+    double* history;
+    int64_t probe_cap, probe_count;
+    int64_t* probe_iteration;
+    double* probe_r_sq;
+} asyrk_sim_out;
+
+asyrk_status asyrk_simulate(const asyrk_csr_view* A, const double* b, const double* x0, const asyrk_sim_config* cfg,
+                            asyrk_sim_out* out);
+/* mean_r_sq: iterations + 1 entries; ratios: iterations entries. runs >= 100
+ * (InsufficientData); run r uses seed base_seed + r. */
+asyrk_status asyrk_monte_carlo_ratios(const asyrk_csr_view* A, const double* b, const double* x0,
+                                      const asyrk_sim_config* cfg, int64_t runs, double* mean_r_sq, double* ratios);
+/* rate_fit (host arithmetic, delay_sim.cpp:272-338). */
+asyrk_status asyrk_rate_fit(const double* y, int64_t count, double stride, double* slope, double* r2);
+
 /* sweep_threads (parallel.hpp:73-75): one solve per entry of thread_list
  * (must contain 1); out arrays have n_threads entries. */
 asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const double* x0,
@@ -234,6 +281,11 @@ asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x,
 asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t max_iters, double* lambda_max,
                                           int64_t* iterations);
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
+/* simulate / monte_carlo_ratios on a resident fp64 system (b = the system's). */
+asyrk_status asyrk_system_simulate(asyrk_system* sys, const double* x0, const asyrk_sim_config* cfg,
+                                   asyrk_sim_out* out);
+asyrk_status asyrk_system_monte_carlo_ratios(asyrk_system* sys, const double* x0, const asyrk_sim_config* cfg,
+                                             int64_t runs, double* mean_r_sq, double* ratios);
 /* compute_stats on a resident fp64 system (see asyrk_compute_stats). */
 asyrk_status asyrk_system_compute_stats(asyrk_system* sys, double tol, int64_t max_iters, asyrk_stats_out* out);
 /* Largest number of worker warps that are co-resident for this system. */

@@ -81,6 +81,55 @@ def _stats_result(o, theta):
     return d
 
 
+class SimConfig(C.Structure):
+    """asyrk_sim_config (include/asyrk_cuda.h; DelayModel + StepParams.gamma + SimOptions)."""
+
+    _fields_ = [("gamma", C.c_double), ("tau", C.c_int64), ("delay", C.c_int32), ("variant", C.c_int32),
+                ("iterations", C.c_int64), ("seed", C.c_uint64), ("probe_every", C.c_int64),
+                ("probe_r_sq", C.c_int32), ("probe_dist_sq", C.c_int32), ("max_events", C.c_int64)]
+
+
+class SimOut(C.Structure):
+    _fields_ = [("trace", TraceOut), ("ev_cap", C.c_int64), ("ev_count", C.c_int64), ("ev_j", _i64p),
+                ("ev_i", _i64p), ("ev_t", _i64p), ("ev_k", _i64p), ("ev_step", _f64p), ("history_cap", C.c_int64),
+                ("history_rows", C.c_int64), ("history", _f64p), ("probe_cap", C.c_int64),
+                ("probe_count", C.c_int64), ("probe_iteration", _i64p), ("probe_r_sq", _f64p)]
+
+
+DELAY = {"fixed": 0, "uniform_random": 1, "max_staleness": 2}
+SIM_VARIANT = {"single_component": 0, "full_row": 1}
+
+
+def _sim_config(gamma, tau, delay, iterations, seed, variant, probe_every=0, probe_r_sq=False, probe_dist_sq=False,
+                max_events=0):
+    return SimConfig(gamma, tau, DELAY[delay], SIM_VARIANT[variant], iterations, seed, probe_every,
+                     int(probe_r_sq), int(probe_dist_sq), max_events)
+
+
+def _sim_call(fn, n, m, cfg: SimConfig):
+    """Run asyrk_(system_)simulate through fn(out) and collect SimRun-like dicts."""
+    K = max(cfg.iterations, 0)
+    tr = _Trace(n, K // max(m, 1) + 3)
+    ne = max(min(cfg.max_events, K), 1)
+    ev = {k: np.zeros(ne, np.int64) for k in ["j", "i", "t", "k"]}
+    ev["step"] = np.zeros(ne)
+    hist = np.zeros((max(cfg.tau, 0) + 1, n))
+    npr = K // cfg.probe_every + 1 if cfg.probe_every > 0 else 1
+    pit, prs = np.zeros(npr, np.int64), np.zeros(npr)
+    o = SimOut(tr.out, min(cfg.max_events, K), 0, _ptr(ev["j"], _i64p), _ptr(ev["i"], _i64p), _ptr(ev["t"], _i64p),
+               _ptr(ev["k"], _i64p), _ptr(ev["step"], _f64p), hist.shape[0], 0, _ptr(hist, _f64p), npr, 0,
+               _ptr(pit, _i64p), _ptr(prs, _f64p))
+    check(fn(o))
+    tr.out = o.trace
+    d = tr.result(False)
+    nev = min(o.ev_count, o.ev_cap)
+    d["events"] = {k: v[:nev].copy() for k, v in ev.items()}
+    d["history"] = hist[:o.history_rows].copy()
+    d["probe_iteration"] = pit[:o.probe_count].copy()
+    d["probe_r_sq"] = prs[:o.probe_count].copy()
+    return d
+
+
 class AsyrkError(ValueError):
     def __init__(self, status: int, msg: str):
         self.status = status
@@ -119,6 +168,12 @@ def lib():
         L.asyrk_system_max_resident_warps.argtypes = [sp, C.c_int32, _i32p]
         L.asyrk_system_compute_stats.argtypes = [sp, C.c_double, C.c_int64, C.POINTER(StatsOut)]
         L.asyrk_compute_stats.argtypes = [C.POINTER(CsrView), C.c_double, C.c_int64, C.POINTER(StatsOut)]
+        L.asyrk_simulate.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(SimConfig), C.POINTER(SimOut)]
+        L.asyrk_system_simulate.argtypes = [sp, _f64p, C.POINTER(SimConfig), C.POINTER(SimOut)]
+        L.asyrk_monte_carlo_ratios.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(SimConfig), C.c_int64,
+                                               _f64p, _f64p]
+        L.asyrk_system_monte_carlo_ratios.argtypes = [sp, _f64p, C.POINTER(SimConfig), C.c_int64, _f64p, _f64p]
+        L.asyrk_rate_fit.argtypes = [_f64p, C.c_int64, C.c_double, _f64p, _f64p]
         L.asyrk_solve_parallel.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig),
                                            C.POINTER(TraceOut), C.POINTER(InstrumentOut)]
         L.asyrk_rk_solve.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
@@ -156,7 +211,8 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_compute_stats", "asyrk_system_compute_stats",
+    "asyrk_mrhs_last_stats", "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
+    "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
 ]
 
 
@@ -399,6 +455,21 @@ class System:
         check(lib().asyrk_system_power_iteration(self.h, tol, max_iters, C.byref(lam), C.byref(it)))
         return lam.value, it.value
 
+    def simulate(self, x0, gamma, tau, delay, iterations, seed, variant, **opts):
+        """simulate (ref delay_sim.cpp:71-228) with the system's b."""
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        cfg = _sim_config(gamma, tau, delay, iterations, seed, variant, **opts)
+        return _sim_call(lambda o: lib().asyrk_system_simulate(self.h, _ptr(x0, _f64p), C.byref(cfg), C.byref(o)),
+                         self.n, self.m, cfg)
+
+    def monte_carlo_ratios(self, x0, gamma, tau, delay, iterations, runs, base_seed, variant="single_component"):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        cfg = _sim_config(gamma, tau, delay, iterations, base_seed, variant)
+        mean, ratios = np.zeros(iterations + 1), np.zeros(max(iterations, 1))
+        check(lib().asyrk_system_monte_carlo_ratios(self.h, _ptr(x0, _f64p), C.byref(cfg), runs, _ptr(mean, _f64p),
+                                                    _ptr(ratios, _f64p)))
+        return dict(mean_r_sq=mean, ratios=ratios[:iterations])
+
     def compute_stats(self, tol=1e-9, max_iters=200000):
         """compute_stats(exact_spectral=false) on the device (ref stats.cpp:52-130)."""
         theta = np.zeros(self.m, np.int64)
@@ -437,6 +508,34 @@ def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, *
                                max_abs_error=rep.max_abs_error, tolerance=rep.tolerance,
                                consistent=bool(rep.consistent))
     return d
+
+
+def simulate(A: HostCsr, b, x0, gamma, tau, delay, iterations, seed, variant, **opts):
+    """One-shot asyrk_simulate (ref delay_sim.cpp:71-228); opts = probe_every, probe_r_sq, max_events."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    cfg = _sim_config(gamma, tau, delay, iterations, seed, variant, **opts)
+    return _sim_call(lambda o: lib().asyrk_simulate(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0, _f64p), C.byref(cfg),
+                                                    C.byref(o)), A.n, A.m, cfg)
+
+
+def monte_carlo_ratios(A: HostCsr, b, x0, gamma, tau, delay, iterations, runs, base_seed,
+                       variant="single_component"):
+    """One-shot asyrk_monte_carlo_ratios (ref delay_sim.cpp:230-270)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    cfg = _sim_config(gamma, tau, delay, iterations, base_seed, variant)
+    mean, ratios = np.zeros(iterations + 1), np.zeros(max(iterations, 1))
+    check(lib().asyrk_monte_carlo_ratios(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0, _f64p), C.byref(cfg), runs,
+                                         _ptr(mean, _f64p), _ptr(ratios, _f64p)))
+    return dict(mean_r_sq=mean, ratios=ratios[:iterations])
+
+
+def rate_fit(y, stride=1.0):
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    sl, r2 = C.c_double(), C.c_double()
+    check(lib().asyrk_rate_fit(_ptr(y, _f64p), len(y), stride, C.byref(sl), C.byref(r2)))
+    return dict(slope=sl.value, r2=r2.value)
 
 
 def compute_stats(A: HostCsr, tol=1e-9, max_iters=200000):

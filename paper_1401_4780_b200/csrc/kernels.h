@@ -162,6 +162,44 @@ void launch_stats_rest(const CscDev& C, const CscDev& R, long long m, long long 
                        StatsDev* out, cudaStream_t s);
 int stats_table_cap(long long max_w, long long n);
 
+// ---- K6: batched bounded-delay simulator (delay.cu)
+struct SimEventDev {
+    long long j, i, t, k;
+    double step;
+};
+struct SimArgs {
+    CscDev R;                      // SELL-32 rows (fp64)
+    CscDev C;                      // SELL-32 columns (fp64, rows ascending)
+    const double* row_norm;        // m
+    const double* b;               // m
+    const double* x0;              // n
+    long long m, n;
+    double gamma;
+    long long tau;
+    int delay_kind;                // 0 fixed, 1 uniform_random, 2 max_staleness
+    int variant;                   // 0 single_component, 1 full_row
+    long long iterations;
+    unsigned long long seed0;      // run r uses seed0 + r
+    long long probe_every;
+    int probe_r_sq;
+    long long max_events;
+    long long runs;
+    double* work;                  // runs x work_stride doubles (sim_work_doubles)
+    long long work_stride;
+    double* probe;                 // runs x probe_stride, or nullptr
+    long long probe_stride;
+    DevRecord* rec;                // run 0's epoch records, or nullptr
+    long long rec_cap;
+    long long *nrec, *nev, *nprobe;  // run 0 counts, or nullptr
+    SimEventDev* ev;               // run 0's events, or nullptr
+    int* status;                   // per run: 0 or ASYRK_E_NonFinite
+    long long* fail_updates;       // per run
+};
+size_t sim_work_doubles(long long m, long long n, long long tau);
+void launch_sim(const SimArgs& a, bool cta_per_run, cudaStream_t s);
+void launch_sim_mean(const double* probe, long long probe_stride, long long runs, long long K, double* mean,
+                     double* ratios, cudaStream_t s);
+
 // ---- K0: packing
 void launch_pack_records(const long long* row_ptr, const int32_t* col, const double* val,
                          const double* row_norm, const double* b, long long m, const uint2* row_info,

@@ -1041,6 +1041,206 @@ asyrk_status stats_impl(asyrk_system* s, double tol, int64_t max_iters, asyrk_st
     return ASYRK_OK;
 }
 
+// ---- bounded-delay simulator (ref/src/delay_sim.cpp:71-270), delay.cu
+asyrk_status sim_validate(const asyrk_system* s, const asyrk_sim_config* c) {
+    if (!c) return fail(ASYRK_E_InvalidArgument, "null simulator config");
+    if (!s->normalized) return fail(ASYRK_E_NotNormalized, "simulate requires normalized rows");
+    if (s->precision != P_F64) return fail(ASYRK_E_InvalidArgument, "the simulator needs an fp64 system");
+    if (c->gamma < 0.0) return fail(ASYRK_E_InvalidGamma, "gamma must be >= 0");
+    if (c->iterations < 1) return fail(ASYRK_E_InvalidArgument, "need at least one iteration");
+    if (c->tau < 0) return fail(ASYRK_E_InvalidArgument, "tau must be >= 0");
+    if (c->probe_dist_sq) return fail(ASYRK_E_InvalidArgument, "probe_dist_sq needs a SolutionProjector");
+    if (c->delay < 0 || c->delay > 2) return fail(ASYRK_E_InvalidArgument, "unknown delay model");
+    if (c->variant < 0 || c->variant > 1) return fail(ASYRK_E_InvalidArgument, "unknown update variant");
+    return ASYRK_OK;
+}
+
+SimArgs sim_args(asyrk_system* s, const asyrk_sim_config* c) {
+    SimArgs a{};
+    a.R = s->rsell();
+    a.C = s->csc();
+    a.row_norm = s->row_norm;
+    a.b = s->b;
+    a.x0 = s->x0d;
+    a.m = s->m;
+    a.n = s->n;
+    a.gamma = c->gamma;
+    a.tau = c->tau;
+    a.delay_kind = c->delay;
+    a.variant = c->variant;
+    a.iterations = c->iterations;
+    a.seed0 = c->seed;
+    return a;
+}
+
+void sim_upload_x0(asyrk_system* s, const double* x0) {
+    if (x0)
+        CK(cudaMemcpyAsync(s->x0d, x0, (size_t)s->n * 8, cudaMemcpyHostToDevice, s->stream));
+    else
+        CK(cudaMemsetAsync(s->x0d, 0, (size_t)s->n * 8, s->stream));
+}
+
+asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config* c, asyrk_sim_out* out) {
+    if (asyrk_status v = sim_validate(s, c)) return v;
+    if (!out) return fail(ASYRK_E_InvalidArgument, "null simulator output");
+    cudaStream_t st = s->stream;
+    AllocStream as(st);
+    const long long m = s->m, n = s->n, K = c->iterations;
+    const bool probing = c->probe_every > 0 && c->probe_r_sq;
+    const long long nprobe_max = probing ? K / c->probe_every + 1 : 0;
+    const long long rec_cap = K / m + 2;
+    const long long ev_cap = std::min<long long>(c->max_events, K);
+    const size_t wd = sim_work_doubles(m, n, c->tau);
+    double* work = dalloc<double>(wd);
+    double* probe = dalloc<double>((size_t)std::max<long long>(nprobe_max, 1));
+    DevRecord* rec = dalloc<DevRecord>((size_t)rec_cap);
+    SimEventDev* ev = dalloc<SimEventDev>((size_t)std::max<long long>(ev_cap, 1));
+    long long* cnt = dalloc<long long>(4);  // nrec, nev, nprobe, fail_updates
+    int* status = dalloc<int>(1);
+    struct Free {
+        std::vector<void*> p;
+        cudaStream_t s;
+        ~Free() {
+            for (void* q : p) pool_free(q, s);
+        }
+    } fr{{work, probe, rec, ev, cnt, status}, st};
+    sim_upload_x0(s, x0);
+    CK(cudaMemsetAsync(cnt, 0, 4 * 8, st));
+    CK(cudaMemsetAsync(status, 0, 4, st));
+    SimArgs a = sim_args(s, c);
+    a.probe_every = c->probe_every;
+    a.probe_r_sq = c->probe_r_sq;
+    a.max_events = ev_cap;
+    a.runs = 1;
+    a.work = work;
+    a.work_stride = (long long)wd;
+    a.probe = probing ? probe : nullptr;
+    a.probe_stride = nprobe_max;
+    a.rec = rec;
+    a.rec_cap = rec_cap;
+    a.nrec = cnt;
+    a.nev = cnt + 1;
+    a.nprobe = cnt + 2;
+    a.ev = ev;
+    a.status = status;
+    a.fail_updates = cnt + 3;
+    launch_sim(a, true, st);
+    CK(cudaGetLastError());
+    long long hc[4];
+    int hst = 0;
+    CK(cudaMemcpyAsync(hc, cnt, sizeof hc, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hst, status, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hst) return fail(ASYRK_E_NonFinite, "iterate became non-finite at iteration " + std::to_string(hc[3]));
+    // trace records (one per epoch boundary + a trailing partial epoch)
+    std::vector<DevRecord> recs((size_t)std::min(hc[0], rec_cap));
+    if (!recs.empty()) CK(cudaMemcpy(recs.data(), rec, recs.size() * sizeof(DevRecord), cudaMemcpyDeviceToHost));
+    asyrk_trace_out& tr = out->trace;
+    tr.count = hc[0];
+    for (long long k = 0; k < std::min<long long>((long long)recs.size(), tr.cap); ++k) {
+        const DevRecord& r = recs[(size_t)k];
+        if (tr.epoch_index) tr.epoch_index[k] = r.epoch;
+        if (tr.r_sq) tr.r_sq[k] = r.r_sq;
+        if (tr.grad_sq) tr.grad_sq[k] = r.grad_sq;
+        if (tr.dist_sq) tr.dist_sq[k] = -1.0;
+        if (tr.wall_seconds) tr.wall_seconds[k] = 1e-9 * (double)r.t_ns;
+        if (tr.updates_applied) tr.updates_applied[k] = r.updates;
+    }
+    if (tr.final_x) CK(cudaMemcpy(tr.final_x, work, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    // events
+    out->ev_count = hc[1];
+    const long long ne = std::min<long long>(hc[1], out->ev_cap);
+    if (ne > 0) {
+        std::vector<SimEventDev> e((size_t)ne);
+        CK(cudaMemcpy(e.data(), ev, (size_t)ne * sizeof(SimEventDev), cudaMemcpyDeviceToHost));
+        for (long long k = 0; k < ne; ++k) {
+            if (out->ev_j) out->ev_j[k] = e[(size_t)k].j;
+            if (out->ev_i) out->ev_i[k] = e[(size_t)k].i;
+            if (out->ev_t) out->ev_t[k] = e[(size_t)k].t;
+            if (out->ev_k) out->ev_k[k] = e[(size_t)k].k;
+            if (out->ev_step) out->ev_step[k] = e[(size_t)k].step;
+        }
+    }
+    // history: the last min(tau+1, K+1) iterates, oldest first (delay_sim.cpp:223-227)
+    const long long ring_len = c->tau + 1;
+    const long long kept = std::min(ring_len, K + 1);
+    out->history_rows = kept;
+    if (out->history) {
+        const double* ring = c->tau == 0 ? work : work + n;
+        long long row = 0;
+        for (long long idx = K - kept + 1; idx <= K && row < out->history_cap; ++idx, ++row)
+            CK(cudaMemcpy(out->history + row * n, ring + (idx % ring_len) * n, (size_t)n * 8,
+                          cudaMemcpyDeviceToHost));
+    }
+    // probes at iterations 0, probe_every, 2 probe_every, ...
+    out->probe_count = probing ? hc[2] : 0;
+    const long long np = std::min<long long>(out->probe_count, out->probe_cap);
+    if (np > 0) {
+        if (out->probe_r_sq) CK(cudaMemcpy(out->probe_r_sq, probe, (size_t)np * 8, cudaMemcpyDeviceToHost));
+        if (out->probe_iteration)
+            for (long long k = 0; k < np; ++k) out->probe_iteration[k] = k * c->probe_every;
+    }
+    return ASYRK_OK;
+}
+
+asyrk_status mc_impl(asyrk_system* s, const double* x0, const asyrk_sim_config* c, int64_t runs, double* mean_r_sq,
+                     double* ratios) {
+    if (runs < 100) return fail(ASYRK_E_InsufficientData, "need >= 100 runs for stable ratio estimates");
+    asyrk_sim_config cc = *c;  // monte_carlo_ratios probes every iteration (delay_sim.cpp:239-241)
+    cc.probe_every = 1;
+    cc.probe_r_sq = 1;
+    cc.probe_dist_sq = 0;
+    cc.max_events = 0;
+    if (asyrk_status v = sim_validate(s, &cc)) return v;
+    if (!mean_r_sq || (!ratios && cc.iterations > 0)) return fail(ASYRK_E_InvalidArgument, "null output");
+    cudaStream_t st = s->stream;
+    AllocStream as(st);
+    const long long K = cc.iterations;
+    const size_t wd = sim_work_doubles(s->m, s->n, cc.tau);
+    if ((double)wd * (double)runs * 8.0 + (double)(K + 1) * (double)runs * 8.0 > 64e9)
+        return fail(ASYRK_E_TooLarge, "Monte-Carlo working set exceeds 64 GB");
+    double* work = dalloc<double>(wd * (size_t)runs);
+    double* probe = dalloc<double>((size_t)(K + 1) * (size_t)runs);
+    double* mean = dalloc<double>((size_t)K + 1);
+    double* rat = dalloc<double>((size_t)std::max<long long>(K, 1));
+    int* status = dalloc<int>((size_t)runs);
+    long long* failu = dalloc<long long>((size_t)runs);
+    struct Free {
+        std::vector<void*> p;
+        cudaStream_t s;
+        ~Free() {
+            for (void* q : p) pool_free(q, s);
+        }
+    } fr{{work, probe, mean, rat, status, failu}, st};
+    sim_upload_x0(s, x0);
+    CK(cudaMemsetAsync(status, 0, (size_t)runs * 4, st));
+    SimArgs a = sim_args(s, &cc);
+    a.probe_every = 1;
+    a.probe_r_sq = 1;
+    a.runs = runs;
+    a.work = work;
+    a.work_stride = (long long)wd;
+    a.probe = probe;
+    a.probe_stride = K + 1;
+    a.status = status;
+    a.fail_updates = failu;
+    launch_sim(a, false, st);
+    launch_sim_mean(probe, K + 1, runs, K, mean, rat, st);
+    CK(cudaGetLastError());
+    std::vector<int> hs((size_t)runs);
+    CK(cudaMemcpyAsync(hs.data(), status, (size_t)runs * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t r = 0; r < runs; ++r)
+        if (hs[(size_t)r]) {  // the reference throws from the first failing run
+            long long u = 0;
+            CK(cudaMemcpy(&u, failu + r, 8, cudaMemcpyDeviceToHost));
+            return fail(ASYRK_E_NonFinite, "iterate became non-finite at iteration " + std::to_string(u));
+        }
+    CK(cudaMemcpy(mean_r_sq, mean, (size_t)(K + 1) * 8, cudaMemcpyDeviceToHost));
+    if (K > 0) CK(cudaMemcpy(ratios, rat, (size_t)K * 8, cudaMemcpyDeviceToHost));
+    return ASYRK_OK;
+}
+
 struct SysGuard {
     asyrk_system* s = nullptr;
     ~SysGuard() {
@@ -1113,6 +1313,73 @@ asyrk_status asyrk_compute_stats(const asyrk_csr_view* A, double tol, int64_t ma
         if (s) return s;
         return stats_impl(g.s, tol, max_iters, out);
     });
+}
+
+asyrk_status asyrk_system_simulate(asyrk_system* sys, const double* x0, const asyrk_sim_config* cfg,
+                                   asyrk_sim_out* out) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return sim_impl(sys, x0, cfg, out); });
+}
+
+asyrk_status asyrk_system_monte_carlo_ratios(asyrk_system* sys, const double* x0, const asyrk_sim_config* cfg,
+                                             int64_t runs, double* mean_r_sq, double* ratios) {
+    if (!sys || !cfg) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] { return mc_impl(sys, x0, cfg, runs, mean_r_sq, ratios); });
+}
+
+asyrk_status asyrk_simulate(const asyrk_csr_view* A, const double* b, const double* x0, const asyrk_sim_config* cfg,
+                            asyrk_sim_out* out) {
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, b, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return sim_impl(g.s, x0, cfg, out);
+    });
+}
+
+asyrk_status asyrk_monte_carlo_ratios(const asyrk_csr_view* A, const double* b, const double* x0,
+                                      const asyrk_sim_config* cfg, int64_t runs, double* mean_r_sq, double* ratios) {
+    if (!cfg) return fail(ASYRK_E_InvalidArgument, "null simulator config");
+    if (runs < 100) return fail(ASYRK_E_InsufficientData, "need >= 100 runs for stable ratio estimates");
+    return guarded([&] {
+        SysGuard g;
+        asyrk_status s = create_impl(A, b, P_F64, nullptr, &g.s);
+        if (s) return s;
+        return mc_impl(g.s, x0, cfg, runs, mean_r_sq, ratios);
+    });
+}
+
+// rate_fit (ref/src/delay_sim.cpp:272-338): least-squares slope of log(y[k])
+// against k * stride, in the reference's summation order. Host arithmetic.
+asyrk_status asyrk_rate_fit(const double* y, int64_t count, double stride, double* slope, double* r2) {
+    if (!slope || !r2 || (count > 0 && !y)) return fail(ASYRK_E_InvalidArgument, "null argument");
+    if (count < 20) return fail(ASYRK_E_InsufficientData, "rate_fit needs >= 20 points");
+    if (!(stride > 0.0)) return fail(ASYRK_E_InvalidArgument, "stride must be positive");
+    std::vector<double> ly((size_t)count);
+    for (int64_t k = 0; k < count; ++k) {
+        if (!(y[k] > 0.0))
+            return fail(ASYRK_E_NonPositiveData,
+                        "rate_fit needs strictly positive values (index " + std::to_string(k) + ")");
+        ly[(size_t)k] = std::log(y[k]);
+    }
+    const double shift = ly[0];
+    for (double& v : ly) v -= shift;
+    double sx = 0.0, sy = 0.0;
+    for (int64_t k = 0; k < count; ++k) {
+        sx += static_cast<double>(k);
+        sy += ly[(size_t)k];
+    }
+    const double mx = sx / static_cast<double>(count), my = sy / static_cast<double>(count);
+    double sxx = 0.0, sxy = 0.0, syy = 0.0;
+    for (int64_t k = 0; k < count; ++k) {
+        const double dx = static_cast<double>(k) - mx, dy = ly[(size_t)k] - my;
+        sxx += dx * dx;
+        sxy += dx * dy;
+        syy += dy * dy;
+    }
+    *slope = sxy / sxx / stride;
+    *r2 = syy == 0.0 ? 1.0 : 1.0 - (syy - sxy * sxy / sxx) / syy;
+    return ASYRK_OK;
 }
 
 asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b) {
