@@ -3,17 +3,18 @@
 //
 // One warp replays one run (Monte-Carlo: `runs` warps side by side, run r
 // seeded base_seed + r as in delay_sim.cpp:249-251); a single `simulate` uses
-// a whole CTA for its run. Lane 0 executes the recursion serially — the row /
-// delay / component draws of the reference's own generator (std::mt19937_64
-// restated on the device, state in shared memory), the stale residual read
-// from the iterate ring, the update and the LiveResidual bumps with their
-// running r_sq — with the reference's floating-point order and explicitly
-// rounded intrinsics, so every trace record, probe, event, history row and
-// final_x is bit-identical to the reference. The other lanes copy the new
-// iterate into its ring slot (tau + 1 iterates, delay_sim.cpp:100-104) and
-// run the epoch-boundary residual passes (rows, then columns in make_csc
-// order) that feed the records and the LiveResidual recompute. A is read
-// from the system's SELL-32 row and column copies (fp64 systems).
+// a whole CTA for its run. The recursion is a serial chain; warp 0 of a run
+// replays it: lane 0 draws from the reference's own generator
+// (std::mt19937_64 restated on the device, state in shared memory), lanes
+// load the row / column entries and form products in parallel, and the
+// serial sums (stale residual, the LiveResidual running r_sq) are replayed in
+// the reference's order from shuffles, with explicitly rounded intrinsics —
+// so every trace record, probe, event, history row and final_x is
+// bit-identical to the reference. The run's iterate, ring of tau + 1
+// iterates (delay_sim.cpp:100-104) and LiveResidual r live in shared memory
+// when they fit. The epoch-boundary residual passes (rows, then columns in
+// make_csc order) use every thread of the run. A is read from the fp64 row
+// records and the plain CSC (serial walks) and the SELL-32 copies (passes).
 #include "kernels.h"
 
 namespace ak {
@@ -89,20 +90,49 @@ __device__ __forceinline__ double row_dot(const Rows& rw, long long i, const dou
     return s;
 }
 
-// LiveResidual::bump (delay_sim.cpp:35-44): column t in make_csc order (the
-// SELL-32 column copy, rows ascending); returns the running r_sq
-__device__ __forceinline__ double bump(const CscDev& C, int t, double delta, double* rl, double rsq) {
-    const long long c0 = __ldg(C.grp_off + (t >> 5)) + (t & 31);
-    const int cl = __ldg(C.col_len + t);
-    const double* cv = static_cast<const double*>(C.val);
-    for (int q = 0; q < cl; ++q) {
-        const long long e = c0 + 32ll * q;
-        const int r = __ldg(C.row + e);
-        rsq = __dsub_rn(rsq, __dmul_rn(rl[r], rl[r]));
-        rl[r] = __dadd_rn(rl[r], __dmul_rn(__ldg(cv + e), delta));
-        rsq = __dadd_rn(rsq, __dmul_rn(rl[r], rl[r]));
+// LiveResidual::bump (delay_sim.cpp:35-44) of column t over the plain CSC
+// (make_csc order, rows ascending), by the whole warp: lane u holds entry u
+// of a 32-entry chunk (the rows of a column are distinct, so the loads and
+// the r updates run in parallel) and every lane replays the serial r_sq
+// chain -old^2 +new^2 in entry order from shuffles. Returns the new r_sq
+// (warp-uniform).
+__device__ __forceinline__ double warp_bump(const SimArgs& a, int t, double delta, double* rl, double rsq, int lane) {
+    const long long q1 = __ldg(a.col_ptr + t + 1);
+    for (long long q0 = __ldg(a.col_ptr + t); q0 < q1; q0 += 32) {
+        const long long q = q0 + lane;
+        const bool act = q < q1;
+        double o2 = 0.0, n2 = 0.0;
+        if (act) {
+            const int r = __ldg(a.csc_row + q);
+            const double old = rl[r];
+            const double nv = __dadd_rn(old, __dmul_rn(__ldg(a.csc_val + q), delta));
+            rl[r] = nv;
+            o2 = __dmul_rn(old, old);
+            n2 = __dmul_rn(nv, nv);
+        }
+        const int lim = (int)min(32ll, q1 - q0);
+        for (int u = 0; u < lim; ++u) {
+            rsq = __dsub_rn(rsq, __shfl_sync(FULL, o2, u));
+            rsq = __dadd_rn(rsq, __shfl_sync(FULL, n2, u));
+        }
     }
+    __syncwarp();  // the next column may touch the same rows
     return rsq;
+}
+
+// a_i^T x - b_i (stale_residual, kaczmarz.hpp:48-60) from the contiguous fp64
+// row record, by the whole warp: products in parallel, the storage-order sum
+// replayed from shuffles. The record's b_i is a bit copy of b[i].
+__device__ __forceinline__ double warp_residual(const double* v, const int32_t* c, int len, const double* x, double bi,
+                                                int lane) {
+    double s = 0.0;
+    for (int c0 = 0; c0 < len; c0 += 32) {
+        const int u = c0 + lane;
+        const double p = u < len ? __dmul_rn(__ldg(v + u), x[__ldg(c + u)]) : 0.0;
+        const int lim = min(32, len - c0);
+        for (int q = 0; q < lim; ++q) s = __dadd_rn(s, __shfl_sync(FULL, p, q));
+    }
+    return __dsub_rn(s, bi);
 }
 
 template <bool CTA>
@@ -145,7 +175,7 @@ __device__ void run_residuals(const SimArgs& a, const Rows& rw, const double* x,
 
 template <bool CTA>
 __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
-    extern __shared__ unsigned long long sm_mt[];
+    extern __shared__ __align__(16) unsigned char sm_raw[];
     __shared__ int stop_flag[8];
     const int wib = threadIdx.x >> 5;
     const int tid = CTA ? (int)threadIdx.x : (int)(threadIdx.x & 31);
@@ -153,13 +183,17 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
     const long long run = CTA ? (long long)blockIdx.x : (long long)blockIdx.x * (blockDim.x >> 5) + wib;
     if (run >= a.runs) return;  // warp- (or block-) uniform
     const int slot = CTA ? 0 : wib;
-    DevMt g{sm_mt + (size_t)slot * kMtN, kMtN};
+    const int lane = threadIdx.x & 31;
     const long long m = a.m, n = a.n;
     const long long ring_len = a.tau + 1;
-    double* x = a.work + run * a.work_stride;
+    // per run: mt state, then (smem_state) the hot doubles x | ring | LiveResidual r
+    unsigned char* mine = sm_raw + (size_t)slot * (kMtN * 8 + (a.smem_state ? (size_t)a.hot * 8 : 0));
+    DevMt g{reinterpret_cast<unsigned long long*>(mine), kMtN};
+    double* gw = a.work + run * a.work_stride;  // global: [hot | rt m | gt n]
+    double* x = a.smem_state ? reinterpret_cast<double*>(mine + kMtN * 8) : gw;
     double* ring = a.tau == 0 ? x : x + n;  // tau = 0: the ring's only slot is always the current iterate
     double* rl = x + n + (a.tau == 0 ? 0 : ring_len * n);  // LiveResidual r
-    double* rt = rl + m;
+    double* rt = gw + a.hot;
     double* gt = rt + m;
     const Rows rw{a.R};
     const bool probing = a.probe_every > 0 && a.probe_r_sq;
@@ -204,7 +238,7 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
         }
         if (recompute) {  // LiveResidual::recompute == the rows pass above, summed the same way
             for (long long i = tid; i < m; i += nthr) rl[i] = rt[i];
-            if (tid == 0) live_rsq = r_sq;
+            if (tid < 32) live_rsq = __shfl_sync(FULL, r_sq, 0);
         }
         run_sync<CTA>();
     };
@@ -217,49 +251,50 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
     if (!stop_flag[slot] && probing) do_probe(0);
 
     for (long long j = 0; j < a.iterations && !stop_flag[slot]; ++j) {
-        if (tid == 0) {
-            const long long i = (long long)g.below((unsigned long long)m);
-            long long k;
-            if (a.delay_kind == 1) {
-                const long long d = (long long)g.below((unsigned long long)(a.tau + 1));
-                k = j - d > 0 ? j - d : 0;
-            } else {
-                k = j - a.tau > 0 ? j - a.tau : 0;
+        if (tid < 32) {  // warp 0 of the run replays iteration j; lane 0 owns the generator
+            long long i = 0, k = 0, pick = 0;
+            if (lane == 0) {  // draw order: row, delay (uniform_random), component (single)
+                i = (long long)g.below((unsigned long long)m);
+                if (a.delay_kind == 1) {
+                    const long long d = (long long)g.below((unsigned long long)(a.tau + 1));
+                    k = j - d > 0 ? j - d : 0;
+                } else {
+                    k = j - a.tau > 0 ? j - a.tau : 0;
+                }
+                if (a.variant == 0) pick = (long long)g.below((unsigned long long)row_ref(a.L, i).len);
             }
+            i = __shfl_sync(FULL, i, 0);
+            k = __shfl_sync(FULL, k, 0);
+            pick = __shfl_sync(FULL, pick, 0);
+            const RowRef rr = row_ref(a.L, i);
+            const double* rv = rec_vals<double>(rr);
+            const int32_t* rc = rec_cols<double>(rr);
+            const int theta = rr.len;
             const double* xr = ring + (a.tau == 0 ? 0 : (k % ring_len) * n);
-            const double res = __dsub_rn(row_dot(rw, i, xr), a.b[i]);  // stale_residual, kaczmarz.hpp:48-60
-            const long long b0 = rw.base(i);
-            const int theta = rw.len(i);
+            const double res = warp_residual(rv, rc, theta, xr, rec_b(rr), lane);  // stale_residual
             long long ev_t;
             double ev_step;
             if (a.variant == 0) {  // single_component
-                const long long pick = (long long)g.below((unsigned long long)theta);
-                const long long e = b0 + 32ll * pick;
-                const int t = rw.col(e);
-                const double delta = __dmul_rn(__dmul_rn(__dmul_rn(-a.gamma, (double)theta), rw.val(e)), res);
-                x[t] = __dadd_rn(x[t], delta);
-                if (probing) live_rsq = bump(a.C, t, delta, rl, live_rsq);
+                const int t = __ldg(rc + pick);
+                const double delta = __dmul_rn(__dmul_rn(__dmul_rn(-a.gamma, (double)theta), __ldg(rv + pick)), res);
+                if (lane == 0) x[t] = __dadd_rn(x[t], delta);
+                if (probing) live_rsq = warp_bump(a, t, delta, rl, live_rsq, lane);
                 ev_t = t;
                 ev_step = delta;
-            } else {  // full_row: row_coef + apply_row, kaczmarz.hpp:63-80
+            } else {  // full_row: row_coef + apply_row, kaczmarz.hpp:63-80 (distinct columns)
                 const double nrm = a.row_norm[i];
                 const double c = __ddiv_rn(__dmul_rn(a.gamma, res), __dmul_rn(nrm, nrm));
-                for (int u = 0; u < theta; ++u) {
-                    const long long e = b0 + 32ll * u;
-                    const int t = rw.col(e);
-                    x[t] = __dsub_rn(x[t], __dmul_rn(c, rw.val(e)));
+                for (int u = lane; u < theta; u += 32) {
+                    const int t = __ldg(rc + u);
+                    x[t] = __dsub_rn(x[t], __dmul_rn(c, __ldg(rv + u)));
                 }
-                if (probing) {
-                    for (int u = 0; u < theta; ++u) {
-                        const long long e = b0 + 32ll * u;
-                        const int t = rw.col(e);
-                        live_rsq = bump(a.C, t, __dmul_rn(-c, rw.val(e)), rl, live_rsq);
-                    }
-                }
+                if (probing)
+                    for (int u = 0; u < theta; ++u)
+                        live_rsq = warp_bump(a, __ldg(rc + u), __dmul_rn(-c, __ldg(rv + u)), rl, live_rsq, lane);
                 ev_t = -1;  // kAllComponents
                 ev_step = c;
             }
-            if (run == 0 && a.ev && nev < a.max_events) {
+            if (lane == 0 && run == 0 && a.ev && nev < a.max_events) {
                 a.ev[nev] = SimEventDev{j, i, ev_t, k, ev_step};
                 ++nev;
             }
@@ -276,6 +311,10 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
         if (probing && done % a.probe_every == 0) do_probe(done);
     }
     if (!stop_flag[slot] && a.iterations % m != 0) boundary(a.iterations / m + 1, a.iterations, false);
+    if (a.smem_state && run == 0) {  // final x and the ring back to global memory for the host
+        run_sync<CTA>();
+        for (long long q = tid; q < a.hot; q += nthr) gw[q] = x[q];
+    }
     if (tid == 0) {
         if (run == 0 && a.nrec) *a.nrec = nrec;
         if (run == 0 && a.nev) *a.nev = nev;
@@ -300,16 +339,34 @@ __global__ void sim_ratio_kernel(const double* mean, long long K, double* ratios
     ratios[j] = a == 0.0 ? (c == 0.0 ? 1.0 : __longlong_as_double(0x7ff0000000000000LL)) : __ddiv_rn(c, a);
 }
 
-size_t sim_work_doubles(long long m, long long n, long long tau) {
-    return (size_t)n * (tau == 0 ? 1 : (size_t)(tau + 2)) + 2 * (size_t)m + (size_t)n;
+static long long sim_hot_doubles(long long m, long long n, long long tau) {
+    return n * (tau == 0 ? 1 : tau + 2) + m;  // x | ring | LiveResidual r
 }
 
-void launch_sim(const SimArgs& a, bool cta_per_run, cudaStream_t s) {
+size_t sim_work_doubles(long long m, long long n, long long tau) {
+    return (size_t)sim_hot_doubles(m, n, tau) + (size_t)m + (size_t)n;  // + residual scratch rt, gt
+}
+
+// The recursion is a serial latency chain per run (the LiveResidual r_sq
+// chain, store -> load through r): its state lives in shared memory when it
+// fits (up to 4 runs per block in warp mode).
+void launch_sim(const SimArgs& a0, bool cta_per_run, cudaStream_t s) {
+    SimArgs a = a0;
+    a.hot = sim_hot_doubles(a.m, a.n, a.tau);
+    constexpr size_t kBudget = 200u << 10;
+    const size_t per_run = kMtN * 8 + (size_t)a.hot * 8;
     if (cta_per_run) {
-        sim_kernel<true><<<(unsigned)a.runs, 256, kMtN * 8, s>>>(a);
+        a.smem_state = per_run <= kBudget;
+        const size_t smem = a.smem_state ? per_run : kMtN * 8;
+        cudaFuncSetAttribute(sim_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sim_kernel<true><<<(unsigned)a.runs, 256, smem, s>>>(a);
     } else {
-        constexpr int wpb = 4;
-        sim_kernel<false><<<(unsigned)((a.runs + wpb - 1) / wpb), 32 * wpb, wpb * kMtN * 8, s>>>(a);
+        int wpb = 4;
+        while (wpb > 1 && per_run * wpb > kBudget) wpb >>= 1;
+        a.smem_state = per_run * wpb <= kBudget;
+        const size_t smem = (size_t)wpb * (a.smem_state ? per_run : kMtN * 8);
+        cudaFuncSetAttribute(sim_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        sim_kernel<false><<<(unsigned)((a.runs + wpb - 1) / wpb), 32 * wpb, smem, s>>>(a);
     }
 }
 

@@ -168,8 +168,12 @@ struct SimEventDev {
     double step;
 };
 struct SimArgs {
-    CscDev R;                      // SELL-32 rows (fp64)
-    CscDev C;                      // SELL-32 columns (fp64, rows ascending)
+    Layout L;                      // fp64 row records (lane 0's contiguous row walks)
+    CscDev R;                      // SELL-32 rows (fp64; the residual passes)
+    CscDev C;                      // SELL-32 columns (fp64, rows ascending; the residual passes)
+    const long long* col_ptr;      // plain CSC (rows ascending): lane 0's LiveResidual bumps
+    const int32_t* csc_row;
+    const double* csc_val;
     const double* row_norm;        // m
     const double* b;               // m
     const double* x0;              // n
@@ -194,6 +198,8 @@ struct SimArgs {
     SimEventDev* ev;               // run 0's events, or nullptr
     int* status;                   // per run: 0 or ASYRK_E_NonFinite
     long long* fail_updates;       // per run
+    long long hot;                 // set by launch_sim: doubles of x | ring | LiveResidual r
+    int smem_state;                // set by launch_sim: hot state in shared memory
 };
 size_t sim_work_doubles(long long m, long long n, long long tau);
 void launch_sim(const SimArgs& a, bool cta_per_run, cudaStream_t s);

@@ -62,7 +62,7 @@ struct asyrk_system {
     int32_t* rsell_col = nullptr;
     void* rsell_val = nullptr;
     double* b = nullptr;            // right-hand side (also in the record headers)
-    long long* col_ptr = nullptr;   // plain CSC (kept only for multi-RHS systems)
+    long long* col_ptr = nullptr;   // plain CSC (fp64 and multi-RHS systems)
     int32_t* csc_row = nullptr;
     double* csc_val = nullptr;
     AliasEntry* alias = nullptr;  // device alias table (async norm_proportional), built lazily
@@ -493,7 +493,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     phase("sell cols");
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
-    if (keep_csc) {  // plain CSC stays for the multi-RHS monitor (warp per column)
+    if (keep_csc || precision == P_F64) {  // plain CSC: multi-RHS monitor, simulator's serial column walks
         s->col_ptr = col_ptr;
         s->csc_row = csc_row;
         s->csc_val = csc_val;
@@ -1057,8 +1057,12 @@ asyrk_status sim_validate(const asyrk_system* s, const asyrk_sim_config* c) {
 
 SimArgs sim_args(asyrk_system* s, const asyrk_sim_config* c) {
     SimArgs a{};
+    a.L = s->layout();
     a.R = s->rsell();
     a.C = s->csc();
+    a.col_ptr = s->col_ptr;
+    a.csc_row = s->csc_row;
+    a.csc_val = s->csc_val;
     a.row_norm = s->row_norm;
     a.b = s->b;
     a.x0 = s->x0d;
