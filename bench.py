@@ -448,6 +448,80 @@ def run_gpu_cfg5(args):
     return 0
 
 
+MC = dict(m=1200, n=60, theta=5, seed=77, runs=1000, iterations=2000, tau=5, gamma=0.15, base_seed=99)
+MC_METRIC = "bounded-delay simulator iterations/sec (monte_carlo_ratios, acceptance C2 shape)"
+
+
+def run_mc(args):
+    """monte_carlo_ratios on acceptance criterion 2's shape
+    (acceptance.cpp:137-155: 1000 runs x 2000 iterations, uniform delays tau=5,
+    single component). b200 arm: device time of the resident-system call (CUDA
+    events) as `value`, the one-shot host call as `e2e`. Reference arm: the
+    reference's monte_carlo_ratios (oracle/_ref, single-threaded as upstream)
+    on a bounded sample of 100 runs per step."""
+    from paper_1401_4780_b200 import capi
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    A, b, _ = capi.generate_fixed_theta(MC["m"], MC["n"], MC["theta"], seed=MC["seed"])
+    x0 = np.zeros(MC["n"])
+    kw = dict(gamma=MC["gamma"], tau=MC["tau"], delay="uniform_random", iterations=MC["iterations"],
+              base_seed=MC["base_seed"])
+    cfg = {"workload": f"monte_carlo_ratios m={MC['m']} n={MC['n']} theta={MC['theta']} tau={MC['tau']} "
+                       f"uniform_random single_component, {MC['iterations']} iterations"}
+    line = {"metric": MC_METRIC, "unit": "iterations/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
+    if args.impl == "reference":
+        R = load_ref()
+        if R is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return 0
+        Ar, _ = R.build(A.m, A.n, np.repeat(np.arange(A.m), np.diff(A.row_ptr)), A.col_idx, A.values, True, None)
+        runs = 100
+        for _ in range(args.warmup):
+            R.monte_carlo(Ar, b, x0, runs=runs, **kw)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            R.monte_carlo(Ar, b, x0, runs=runs, **kw)
+        wall = time.perf_counter() - t0
+        v = runs * MC["iterations"] * args.steps / wall
+        line.update(value=v, ms_per_step=1e3 * wall / args.steps, impl="reference",
+                    config=dict(cfg, runs=runs, threads=1),
+                    cpu_baseline={"value": v, "unit": "iterations/s", "cores": 1, "kind": "reference",
+                                  "sample": f"{runs} runs x {MC['iterations']} iterations per step"},
+                    e2e={"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line))
+        return 0
+    import torch
+
+    runs = MC["runs"]
+    S = capi.System(A, b)
+    for _ in range(args.warmup):
+        S.monte_carlo_ratios(x0, runs=runs, **kw)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            ev[k][0].record()
+            S.monte_carlo_ratios(x0, runs=runs, **kw)
+            ev[k][1].record()
+        torch.cuda.synchronize()
+    dev_ms = sum(a.elapsed_time(c) for a, c in ev)
+    S.close()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        capi.monte_carlo_ratios(A, b, x0, runs=runs, **kw)
+    wall = time.perf_counter() - t0
+    it = runs * MC["iterations"] * args.steps
+    line.update(value=it / (dev_ms * 1e-3), ms_per_step=dev_ms / args.steps, config=dict(cfg, runs=runs),
+                e2e={"value": it / wall, "unit": "iterations/s",
+                     "h2d_bytes_per_step": int(8 * (A.m + 1) + 12 * A.nnz + 16 * A.m + 8 * A.n),
+                     "d2h_bytes_per_step": int(8 * (2 * MC["iterations"] + 1)), "ms_per_step": 1e3 * wall / args.steps},
+                gpu_launches=3 * args.steps, clocks=clk.summary())
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -455,9 +529,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = 3/4 of the resident warp slots)")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.workload == "mc":
+        return run_mc(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg5":
