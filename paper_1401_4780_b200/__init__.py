@@ -11,6 +11,11 @@ hot path:
 * ``solve_parallel(m, n, rows, cols, vals, b, threads=1, gamma=1.0,
   epochs=100, target=0.0, seed=0, variant="full-row")`` — ``threads``
   concurrent warp-workers (``threads == 1``: the deterministic worker).
+* ``system_stats(m, n, rows, cols, vals)``, ``step_params(..., tau)`` —
+  device compute_stats (power-iteration lambda_max; no dense-SVD fields).
+* ``simulate(m, n, rows, cols, vals, b, iterations, tau, gamma,
+  delay="uniform", variant="single", seed=0)`` — the bounded-delay replay on
+  the device, bit-identical to the reference's ``simulate``.
 
 Device extensions: ``solve_parallel_device`` (sampling / precision /
 snapshot interval / x_star), ``lambda_max``, ``residuals``,
@@ -40,10 +45,16 @@ solve_parallel_device = _asyrk.solve_parallel_device
 lambda_max = _asyrk.lambda_max
 residuals = _asyrk.residuals
 max_feasible_tau = _asyrk.max_feasible_tau
+system_stats = _asyrk.system_stats
+step_params = _asyrk.step_params
+simulate = _asyrk.simulate
 
 __all__ = [
     "solve_rk",
     "solve_parallel",
+    "system_stats",
+    "step_params",
+    "simulate",
     "solve_parallel_device",
     "lambda_max",
     "residuals",

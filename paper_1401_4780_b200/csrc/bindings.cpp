@@ -1,7 +1,10 @@
 // pybind11 module `_asyrk` with the reference's Python signatures
-// (ref/bindings/module.cpp:281-318, hot-path subset): dict in / dict out,
-// triplets -> CSR -> normalize_rows inside, errors as
-// ValueError("<ErrorCodeName>: message") (module.cpp:271-279).
+// (ref/bindings/module.cpp:281-318: solve_rk, solve_parallel, system_stats,
+// step_params, simulate): dict in / dict out, triplets -> CSR ->
+// normalize_rows inside, errors as ValueError("<ErrorCodeName>: message")
+// (module.cpp:271-279). Statistics use the device compute_stats with
+// power-iteration lambda_max (exact_spectral = false): lambda_min / sigma_r
+// and the rate fields that need them are absent from the dicts.
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
@@ -9,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "asyrk/delay_sim.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk/kaczmarz.hpp"
 #include "asyrk/parallel.hpp"
@@ -133,6 +137,96 @@ py::dict solve_parallel_core(index_t m, index_t n, const std::vector<index_t>& r
     return d;
 }
 
+SystemStats device_stats(const CsrMatrix& N) {
+    StatsOptions o;
+    o.exact_spectral = false;  // the dense SVD is not on the device path
+    return compute_stats(N, o);
+}
+
+// module.cpp:113-135
+py::dict system_stats_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                         const std::vector<double>& vals) {
+    CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
+    std::vector<double> dummy(static_cast<std::size_t>(m), 0.0);
+    auto [N, ignored] = normalize_rows(A, dummy);
+    SystemStats st;
+    {
+        py::gil_scoped_release nogil;
+        st = device_stats(N);
+    }
+    py::dict d;
+    d["m"] = st.m;
+    d["n"] = st.n;
+    d["delta"] = st.delta;
+    d["theta"] = st.theta;
+    d["mu"] = st.mu;
+    d["nu"] = st.nu;
+    d["alpha"] = st.alpha;
+    d["lambda_max"] = st.lambda_max;
+    if (st.lambda_min) d["lambda_min"] = *st.lambda_min;
+    if (st.sigma_r) d["sigma_r"] = *st.sigma_r;
+    d["frob_sq"] = st.frob_sq;
+    d["l_max"] = st.l_max;
+    d["l_res"] = st.l_res;
+    return d;
+}
+
+// module.cpp:137-157
+py::dict step_params_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                        const std::vector<double>& vals, index_t tau) {
+    CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
+    std::vector<double> dummy(static_cast<std::size_t>(m), 0.0);
+    auto [N, ignored] = normalize_rows(A, dummy);
+    SystemStats st;
+    {
+        py::gil_scoped_release nogil;
+        st = device_stats(N);
+    }
+    StepParams p = corollary_params(st, tau);
+    py::dict d;
+    d["tau"] = p.tau;
+    d["rho"] = p.rho;
+    d["psi"] = p.psi;
+    d["feasible"] = p.feasible;
+    d["gamma"] = p.gamma;
+    d["bounds"] = py::make_tuple(p.gamma_bounds.b1, p.gamma_bounds.b2, p.gamma_bounds.b3);
+    if (p.rate_iter) d["rate_iteration"] = *p.rate_iter;
+    if (p.rate_simplified) d["rate_simplified"] = *p.rate_simplified;
+    return d;
+}
+
+// module.cpp:213-238: step parameters from the statistics, gamma overridden,
+// then the device bounded-delay simulation
+py::dict simulate_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                     const std::vector<double>& vals, const std::vector<double>& b, index_t iterations, index_t tau,
+                     double gamma, const std::string& delay, const std::string& variant, std::uint64_t seed) {
+    CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
+    auto [A, bn] = normalize_rows(A0, b);
+    SimRun run;
+    StepParams p;
+    {
+        py::gil_scoped_release nogil;
+        p = corollary_params(device_stats(A), tau);
+        p.gamma = gamma;
+        DelayModel dm;
+        if (delay == "fixed")
+            dm = DelayModel::fixed(tau);
+        else if (delay == "uniform")
+            dm = DelayModel::uniform_random(tau);
+        else if (delay == "max")
+            dm = DelayModel::max_staleness(tau);
+        else
+            fail(ErrorCode::InvalidArgument, "delay: expected fixed|uniform|max");
+        std::vector<double> x0(static_cast<std::size_t>(n), 0.0);
+        run = simulate(A, bn, x0, p, dm, iterations, seed, parse_variant(variant), {});
+    }
+    py::dict d = to_dict(run.trace);
+    d["gamma"] = p.gamma;
+    d["rho"] = p.rho;
+    d["psi"] = p.psi;
+    return d;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_asyrk, mod) {
@@ -181,6 +275,17 @@ PYBIND11_MODULE(_asyrk, mod) {
         py::arg("snapshot_interval") = 1, py::arg("precision") = 0, py::arg("instrument") = false,
         py::arg("x_star") = py::none(),
         "solve_parallel with the device options: sampling slice|replacement|norm, precision 0/1/2.");
+    mod.def("system_stats", &system_stats_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"),
+            py::arg("vals"),
+            "Structural and spectral statistics (rows normalized first; device compute_stats, "
+            "power-iteration lambda_max).");
+    mod.def("step_params", &step_params_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"),
+            py::arg("vals"), py::arg("tau"), "Staleness-aware step size and rate bounds for delay bound tau.");
+    mod.def("simulate", &simulate_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"),
+            py::arg("b"), py::arg("iterations"), py::arg("tau"), py::arg("gamma"), py::arg("delay") = "uniform",
+            py::arg("variant") = "single", py::arg("seed") = 0,
+            "Deterministic bounded-delay simulation of the asynchronous update recursion (device replay, "
+            "bit-identical to the reference).");
     mod.def(
         "lambda_max",
         [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,

@@ -102,6 +102,10 @@ void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 // advance the coordinator state (epoch, updates, slot meta, next go)
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
                      long long m, cudaStream_t s);
+// end of an overlapped solve: x, epoch and updates back to the snapshot whose
+// record decided the stop (no-op when the stop came from the epoch cap in-stream)
+void launch_restore(DevState* st, void* x, const void* xs0, const void* xs1, long long n, int precision,
+                    cudaStream_t s);
 
 // ---- K2b/K3b: multi-right-hand-side worker and monitor (mrhs.cu)
 struct MrhsArgs {

@@ -87,6 +87,10 @@ struct DevState {
     int go;
     int snap_valid[2];
     long long snap_epoch[2], snap_updates[2];
+    // the snapshot whose record decided the stop (-1: none / in-stream): the
+    // solve returns that snapshot, not the epochs that ran past it
+    int stop_slot;
+    long long stop_epoch, stop_updates;
 };
 
 struct DevRecord {

@@ -204,7 +204,14 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
             a.rec[k] = rc;
         }
         st->nrec = k + 1;
-        if (r_sq <= st->target || epoch >= st->epochs_cap) st->stop = 1;
+        if (!st->stop && (r_sq <= st->target || epoch >= st->epochs_cap)) {
+            st->stop = 1;
+            if (a.slot >= 0) {
+                st->stop_slot = a.slot;
+                st->stop_epoch = epoch;
+                st->stop_updates = updates;
+            }
+        }
     }
     if (a.slot < 0) st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
     if (st->stop && a.host_flag) {

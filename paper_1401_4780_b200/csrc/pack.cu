@@ -128,6 +128,7 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->increments = 0;
     st->go = 0;  // set by the initial record's commit
     st->snap_valid[0] = st->snap_valid[1] = 0;
+    st->stop_slot = -1;
     st->t0_ns = globaltimer_ns();
 }
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
@@ -266,12 +267,16 @@ namespace ak {
 // counted or skipped.
 template <class X>
 __global__ void snapshot_kernel(const DevState* st, const X* __restrict__ x, X* __restrict__ xs, long long n) {
-    if (!st->go) return;
+    if (!st->go || st->stop) return;  // after a stop the deciding snapshot must survive
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
         xs[k] = __ldcg(x + k);
 }
 
 __global__ void advance_kernel(DevState* st, int slot, long long m) {
+    if (st->stop) {  // stopped: the slots are frozen, no further epochs
+        st->go = 0;
+        return;
+    }
     if (st->go) {
         const long long sp = chunk_span(st);
         st->epoch += sp;
@@ -283,6 +288,32 @@ __global__ void advance_kernel(DevState* st, int slot, long long m) {
         st->snap_valid[slot] = 0;
     }
     st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
+}
+
+// end of an overlapped solve: return the snapshot that decided the stop
+template <class X>
+__global__ void restore_kernel(DevState* st, X* __restrict__ x, const X* __restrict__ xs0, const X* __restrict__ xs1,
+                               long long n) {
+    const int slot = st->stop_slot;
+    if (slot < 0) return;
+    const X* src = slot == 0 ? xs0 : xs1;
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        x[k] = src[k];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        st->epoch = st->stop_epoch;
+        st->updates = st->stop_updates;
+    }
+}
+
+void launch_restore(DevState* st, void* x, const void* xs0, const void* xs1, long long n, int precision,
+                    cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
+    if (precision == P_F32)
+        restore_kernel<float><<<blocks, 256, 0, s>>>(st, static_cast<float*>(x), static_cast<const float*>(xs0),
+                                                     static_cast<const float*>(xs1), n);
+    else
+        restore_kernel<double><<<blocks, 256, 0, s>>>(st, static_cast<double*>(x), static_cast<const double*>(xs0),
+                                                      static_cast<const double*>(xs1), n);
 }
 
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,

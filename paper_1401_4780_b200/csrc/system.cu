@@ -684,7 +684,9 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
 
     // async solves overlap the residual monitor with the next epoch's workers
     static const bool no_overlap = getenv("ASYRK_NO_OVERLAP") != nullptr;
-    const bool overlap = !sp.det && !no_overlap;
+    // (instrumented runs keep the in-stream monitor: restoring the stopping
+    // snapshot would desynchronize x from the shadow increments)
+    const bool overlap = !sp.det && !no_overlap && !instr;
     if (overlap && !s->mstream) {
         // highest priority: monitor blocks take SM slots ahead of queued worker blocks
         int lo = 0, hi = 0;
@@ -800,6 +802,9 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         // (parallel.cpp:415-426: epoch = the epochs actually run)
         CK(cudaEventRecord(s->snap_ev[0], s->mstream));
         CK(cudaStreamWaitEvent(st, s->snap_ev[0], 0));
+        // the epochs that ran past the stopping snapshot are discarded: the
+        // solve returns the iterate whose residual met the target
+        launch_restore(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, st);
         MonitorArgs fa = monitor_args(s, false, 0, sp.x_star != nullptr);
         fa.force = 1;
         launch_monitor(fa, prec, st);

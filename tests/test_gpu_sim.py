@@ -118,3 +118,23 @@ def test_simulator_errors(golden):
     with pytest.raises(oracle.OracleError, match="NonFinite"):
         Ac = oracle.C.from_arrays(A.m, A.n, A.row_ptr, A.col_idx, A.values)
         oracle.C.simulate(Ac, b, x0, 1e300, 0, "fixed", 200, 1, "single_component")
+
+
+def test_pybind_simulate_matches_oracle(golden):
+    # module.cpp:213-238: normalize, step parameters from the statistics,
+    # gamma overridden, simulate; the trace is the reference's simulate trace
+    import paper_1401_4780_b200 as pkg
+
+    A, b = sim_csr(golden, "d30x20")
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    d = pkg.simulate(A.m, A.n, rows, A.col_idx, A.values, b, 500, 3, 0.05, delay="max", variant="single", seed=4)
+    Ac = oracle.C.from_arrays(A.m, A.n, A.row_ptr, A.col_idx, A.values)
+    ref = oracle.C.simulate(Ac, b, np.zeros(A.n), 0.05, 3, "max_staleness", 500, 4, "single_component")
+    for k in ["epoch_index", "r_sq", "grad_sq", "updates_applied", "final_x"]:
+        assert np.array_equal(np.asarray(d[k]), ref[k]), k
+    assert d["gamma"] == 0.05
+    st = oracle.C.stats_full(Ac)
+    cor = oracle.C.corollary(A.m, st["mu"], st["lambda_max"], 3)
+    assert abs(d["rho"] - cor["rho"]) <= 1e-9 * cor["rho"] and abs(d["psi"] - cor["psi"]) <= 1e-9 * cor["psi"]
+    with pytest.raises(ValueError, match="InvalidArgument"):
+        pkg.simulate(A.m, A.n, rows, A.col_idx, A.values, b, 10, 1, 0.1, delay="sometimes")

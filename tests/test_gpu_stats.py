@@ -100,3 +100,23 @@ def test_compute_stats_errors():
     Z = capi.HostCsr(2, 3, [0, 1, 2], [0, 2], [1.0, 1.0])  # column 1 empty
     with pytest.raises(capi.AsyrkError, match="ZeroColumn: column 1"):
         capi.compute_stats(Z)
+
+
+def test_pybind_system_stats_and_step_params(golden, instances):
+    # module.cpp:113-157 with the device statistics (power-iteration lambda_max)
+    import paper_1401_4780_b200 as pkg
+
+    nm = "stats_200x120"
+    inst = instances[nm]
+    rows = np.repeat(np.arange(inst["m"]), np.diff(inst["row_ptr"]))
+    d = pkg.system_stats(inst["m"], inst["n"], rows, inst["col_idx"], inst["values"])
+    ref = dict(zip(FIELDS, golden[f"stats/{nm}/vals"]))
+    for k in EXACT:
+        assert float(d[k]) == ref[k], k
+    assert list(d["theta"]) == list(golden[f"stats/{nm}/theta"])
+    assert "lambda_min" not in d and "sigma_r" not in d
+    p = pkg.step_params(inst["m"], inst["n"], rows, inst["col_idx"], inst["values"], 2)
+    Ac = oracle.C.from_arrays(inst["m"], inst["n"], inst["row_ptr"], inst["col_idx"], inst["values"])
+    cor = oracle.C.corollary(inst["m"], int(ref["mu"]), ref["lambda_max"], 2)
+    assert p["feasible"] == cor["feasible"] and abs(p["rho"] - cor["rho"]) <= 1e-9 * cor["rho"]
+    assert abs(p["gamma"] - cor["gamma"]) <= 1e-8 * abs(cor["gamma"]) and len(p["bounds"]) == 3

@@ -147,3 +147,17 @@ def test_corollary_tau_bound():
     lam = 6.076
     t = pkg.max_feasible_tau(200000, lam)
     assert 2 * np.e * lam * (t + 1) / 200000 <= 1 < 2 * np.e * lam * (t + 2) / 200000
+
+
+def test_pybind_stats_and_simulate_signatures_match_reference():
+    # ref/bindings/module.cpp:286-310
+    import paper_1401_4780_b200 as pkg
+
+    doc = pkg.simulate.__doc__
+    for arg in ["m", "n", "rows", "cols", "vals", "b", "iterations", "tau", "gamma"]:
+        assert f"{arg}:" in doc
+    for arg, default in [("delay", "'uniform'"), ("variant", "'single'"), ("seed", "0")]:
+        assert re.search(rf"\b{arg}: [^=]*= {re.escape(default)}[,)]", doc), arg
+    for fn, extra in [(pkg.system_stats, []), (pkg.step_params, ["tau"])]:
+        for arg in ["m", "n", "rows", "cols", "vals"] + extra:
+            assert f"{arg}:" in fn.__doc__
