@@ -209,6 +209,17 @@ class _RefLib(_Lib):
         L.ref_monte_carlo.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
                                       C_.c_int64, C_.c_uint64, C_.c_int, _f64p, _f64p]
         L.ref_rate_fit.argtypes = [_f64p, C_.c_int64, C_.c_double, _f64p, _f64p]
+        L.ref_csr_dims.argtypes = [C_.c_void_p, _i64p, _i64p]
+        L.ref_write_mtx.argtypes = [C_.c_void_p, C_.c_char_p]
+        L.ref_read_mtx.restype = C_.c_void_p
+        L.ref_read_mtx.argtypes = [C_.c_char_p, C_.POINTER(C_.c_int)]
+        L.ref_write_vector.argtypes = [C_.c_char_p, _f64p, C_.c_int64]
+        L.ref_read_vector.argtypes = [C_.c_char_p, _f64p, C_.c_int64, _i64p]
+        L.ref_write_instance.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_int64, C_.c_int64, C_.c_double, C_.c_uint64,
+                                         C_.c_int, C_.c_double, C_.c_char_p]
+        L.ref_read_instance.restype = C_.c_void_p
+        L.ref_read_instance.argtypes = [C_.c_char_p, _f64p, C_.c_int64, _f64p, C_.c_int64, C_.POINTER(C_.c_int), _f64p,
+                                        C_.POINTER(C_.c_int)]
         L.ref_corollary.argtypes = [C_.c_int64, C_.c_int64, C_.c_double, C_.c_double, C_.c_int64, _f64p, _f64p,
                                     _f64p, C_.POINTER(C_.c_int)]
         L.ref_stream_raw.argtypes = [C_.c_uint64, C_.c_uint64, C_.c_int64, _u64p]
@@ -333,6 +344,49 @@ class _RefLib(_Lib):
                                            iterations, runs, base_seed, SIM_VARIANTS[variant], _p(mean, _f64p),
                                            _p(ratios, _f64p)))
         return dict(mean_r_sq=mean, ratios=ratios)
+
+    def write_mtx(self, A, path):
+        self._check(self.L.ref_write_mtx(A.handle, path.encode()))
+
+    def read_mtx(self, path):
+        st = C_.c_int(0)
+        h = self.L.ref_read_mtx(path.encode(), C_.byref(st))
+        self._check(st.value)
+        return self._csr_from_handle(h)
+
+    def _csr_from_handle(self, h):
+        m, n = C_.c_int64(), C_.c_int64()
+        self.L.ref_csr_dims(h, C_.byref(m), C_.byref(n))
+        return Csr(self, h, m.value, n.value)
+
+    def write_vector(self, path, v):
+        v = _f64(v)
+        self._check(self.L.ref_write_vector(path.encode(), _p(v, _f64p), len(v)))
+
+    def read_vector(self, path, cap=1 << 22):
+        out = np.zeros(cap)
+        cnt = C_.c_int64()
+        self._check(self.L.ref_read_vector(path.encode(), _p(out, _f64p), cap, C_.byref(cnt)))
+        return out[:cnt.value].copy()
+
+    def write_instance(self, A, b, xs, spec, path):
+        b = _f64(b)
+        xs = _f64(xs) if xs is not None else None
+        self._check(self.L.ref_write_instance(A.handle, _p(b, _f64p), _p(xs, _f64p), spec["m"], spec["n"],
+                                              spec["delta"], spec["seed"], int(spec["consistent"]),
+                                              spec["noise_level"], path.encode()))
+
+    def read_instance(self, path, m_cap=1 << 20, n_cap=1 << 20):
+        b, xs, meta = np.zeros(m_cap), np.zeros(n_cap), np.zeros(6)
+        has, st = C_.c_int(0), C_.c_int(0)
+        h = self.L.ref_read_instance(path.encode(), _p(b, _f64p), m_cap, _p(xs, _f64p), n_cap, C_.byref(has),
+                                     _p(meta, _f64p), C_.byref(st))
+        self._check(st.value)
+        m, n = int(meta[0]), int(meta[1])
+        A = Csr(self, h, m, n)
+        return dict(A=A, b=b[:m].copy(), x_star=xs[:n].copy() if has.value else None,
+                    spec=dict(m=m, n=n, delta=meta[2], seed=int(meta[3]), consistent=bool(meta[4]),
+                              noise_level=meta[5]))
 
     def rate_fit(self, y, stride=1.0):
         y = _f64(y)

@@ -11,6 +11,7 @@
 //   gen_sparse_gaussian                        (ref/src/datagen.cpp:13-137)
 //   AliasTable, make_stream/uniform_below      (ref/src/kaczmarz.cpp:14-61, rng.hpp)
 //   simulate / monte_carlo_ratios / rate_fit   (ref/src/delay_sim.cpp:71-338)
+//   Matrix Market / vector / instance I/O      (ref/src/io.cpp:41-183)
 // Nothing here is shipped; the product never links this library.
 #include <cstdint>
 #include <cstring>
@@ -20,6 +21,7 @@
 #include "asyrk/csr.hpp"
 #include "asyrk/datagen.hpp"
 #include "asyrk/delay_sim.hpp"
+#include "asyrk/io.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk/kaczmarz.hpp"
 #include "asyrk/parallel.hpp"
@@ -115,6 +117,11 @@ void* ref_csr_build(int64_t m, int64_t n, int64_t nnz, const int64_t* rows, cons
 void ref_csr_free(void* h) { delete static_cast<Handle*>(h); }
 
 int64_t ref_csr_nnz(void* h) { return static_cast<Handle*>(h)->A.nnz(); }
+
+void ref_csr_dims(void* h, int64_t* m, int64_t* n) {
+    *m = static_cast<Handle*>(h)->A.rows();
+    *n = static_cast<Handle*>(h)->A.cols();
+}
 
 void ref_csr_export(void* hp, int64_t* row_ptr, int64_t* col_idx, double* vals, double* row_norm,
                     int* normalized) {
@@ -421,6 +428,63 @@ int ref_rate_fit(const double* y, int64_t n, double stride, double* slope, doubl
         *slope = f.slope;
         *r2 = f.r2;
     });
+}
+
+// ---- instance I/O (io.hpp:12-33)
+int ref_write_mtx(void* hp, const char* path) {
+    return guarded([&] { write_matrix_market(path, static_cast<Handle*>(hp)->A); });
+}
+
+void* ref_read_mtx(const char* path, int* status) {
+    Handle* h = nullptr;
+    *status = guarded([&] { h = new Handle{read_matrix_market(path)}; });
+    return h;
+}
+
+int ref_write_vector(const char* path, const double* v, int64_t n) {
+    return guarded([&] { write_vector(path, std::span<const double>(v, (size_t)n)); });
+}
+
+// count = the vector length; at most cap values copied
+int ref_read_vector(const char* path, double* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        std::vector<double> v = read_vector(path);
+        *count = (int64_t)v.size();
+        std::memcpy(out, v.data(), (size_t)std::min<int64_t>(cap, *count) * 8);
+    });
+}
+
+int ref_write_instance(void* hp, const double* b, const double* xs, int64_t m, int64_t n, double delta, uint64_t seed,
+                       int consistent, double noise_level, const char* dir) {
+    return guarded([&] {
+        Instance inst;
+        inst.A = static_cast<Handle*>(hp)->A;
+        inst.b.assign(b, b + inst.A.rows());
+        if (xs) inst.x_star = std::vector<double>(xs, xs + inst.A.cols());
+        inst.spec = GenSpec{m, n, delta, seed, consistent != 0, noise_level};
+        write_instance(dir, inst);
+    });
+}
+
+// b_out: m values, xs_out: n values (has_xs = 0 when absent); meta6 = {m, n, delta, seed, consistent, noise}
+void* ref_read_instance(const char* dir, double* b_out, int64_t b_cap, double* xs_out, int64_t xs_cap, int* has_xs,
+                        double* meta6, int* status) {
+    Handle* h = nullptr;
+    *status = guarded([&] {
+        Instance inst = read_instance(dir);
+        std::memcpy(b_out, inst.b.data(), (size_t)std::min<int64_t>(b_cap, (int64_t)inst.b.size()) * 8);
+        *has_xs = inst.x_star ? 1 : 0;
+        if (inst.x_star)
+            std::memcpy(xs_out, inst.x_star->data(), (size_t)std::min<int64_t>(xs_cap, (int64_t)inst.x_star->size()) * 8);
+        meta6[0] = (double)inst.spec.m;
+        meta6[1] = (double)inst.spec.n;
+        meta6[2] = inst.spec.delta;
+        meta6[3] = (double)inst.spec.seed;
+        meta6[4] = inst.spec.consistent ? 1.0 : 0.0;
+        meta6[5] = inst.spec.noise_level;
+        h = new Handle{std::move(inst.A)};
+    });
+    return h;
 }
 
 }  // extern "C"

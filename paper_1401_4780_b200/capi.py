@@ -130,6 +130,17 @@ def _sim_call(fn, n, m, cfg: SimConfig):
     return d
 
 
+class HostCsrInfo(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("nnz", C.c_int64), ("normalized", C.c_int32)]
+
+
+class InstanceMeta(C.Structure):
+    """asyrk_instance_meta (include/asyrk_io.h; ref GenSpec, datagen.hpp:11-18)."""
+
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("delta", C.c_double), ("seed", C.c_uint64),
+                ("consistent", C.c_int32), ("noise_level", C.c_double), ("has_x_star", C.c_int32)]
+
+
 class AsyrkError(ValueError):
     def __init__(self, status: int, msg: str):
         self.status = status
@@ -174,6 +185,19 @@ def lib():
                                                _f64p, _f64p]
         L.asyrk_system_monte_carlo_ratios.argtypes = [sp, _f64p, C.POINTER(SimConfig), C.c_int64, _f64p, _f64p]
         L.asyrk_rate_fit.argtypes = [_f64p, C.c_int64, C.c_double, _f64p, _f64p]
+        L.asyrk_read_matrix_market.argtypes = [C.c_char_p, C.POINTER(sp), C.POINTER(HostCsrInfo)]
+        L.asyrk_write_matrix_market.argtypes = [C.c_char_p, C.POINTER(CsrView)]
+        L.asyrk_read_csr_cache.argtypes = [C.c_char_p, C.POINTER(sp), C.POINTER(HostCsrInfo)]
+        L.asyrk_write_csr_cache.argtypes = [C.c_char_p, C.POINTER(CsrView)]
+        L.asyrk_host_csr_copy.argtypes = [sp, _i64p, _i64p, _f64p, _f64p]
+        L.asyrk_host_csr_free.argtypes = [sp]
+        L.asyrk_host_csr_get_info.argtypes = [sp, C.POINTER(HostCsrInfo)]
+        L.asyrk_read_vector.argtypes = [C.c_char_p, C.POINTER(_f64p), _i64p]
+        L.asyrk_write_vector.argtypes = [C.c_char_p, _f64p, C.c_int64]
+        L.asyrk_free.argtypes = [C.c_void_p]
+        L.asyrk_write_instance.argtypes = [C.c_char_p, C.POINTER(CsrView), _f64p, _f64p, C.POINTER(InstanceMeta)]
+        L.asyrk_read_instance.argtypes = [C.c_char_p, C.POINTER(sp), C.POINTER(_f64p), C.POINTER(_f64p),
+                                          C.POINTER(InstanceMeta)]
         L.asyrk_solve_parallel.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig),
                                            C.POINTER(TraceOut), C.POINTER(InstrumentOut)]
         L.asyrk_rk_solve.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
@@ -213,6 +237,9 @@ EXPORTED = [
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
     "asyrk_mrhs_last_stats", "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
+    "asyrk_read_matrix_market", "asyrk_write_matrix_market", "asyrk_read_csr_cache", "asyrk_write_csr_cache",
+    "asyrk_host_csr_copy", "asyrk_host_csr_free", "asyrk_host_csr_get_info", "asyrk_read_vector", "asyrk_write_vector", "asyrk_free",
+    "asyrk_write_instance", "asyrk_read_instance",
 ]
 
 
@@ -536,6 +563,83 @@ def rate_fit(y, stride=1.0):
     sl, r2 = C.c_double(), C.c_double()
     check(lib().asyrk_rate_fit(_ptr(y, _f64p), len(y), stride, C.byref(sl), C.byref(r2)))
     return dict(slope=sl.value, r2=r2.value)
+
+
+# ---- instance I/O (include/asyrk_io.h; ref io.hpp:12-33)
+def _take_host_csr(h, info):
+    m, n, nnz = info.m, info.n, info.nnz
+    rp, ci = np.zeros(m + 1, np.int64), np.zeros(nnz, np.int64)
+    v, rn = np.zeros(nnz), np.zeros(m)
+    try:
+        check(lib().asyrk_host_csr_copy(h, _ptr(rp, _i64p), _ptr(ci, _i64p), _ptr(v, _f64p), _ptr(rn, _f64p)))
+    finally:
+        lib().asyrk_host_csr_free(h)
+    return HostCsr(m, n, rp, ci, v, rn, normalized=bool(info.normalized))
+
+
+def read_matrix_market(path):
+    """read_matrix_market (ref io.cpp:60-96): Matrix Market coordinate file -> HostCsr."""
+    h, info = C.c_void_p(), HostCsrInfo()
+    check(lib().asyrk_read_matrix_market(os.fsencode(path), C.byref(h), C.byref(info)))
+    return _take_host_csr(h, info)
+
+
+def write_matrix_market(path, A: HostCsr):
+    check(lib().asyrk_write_matrix_market(os.fsencode(path), C.byref(A.view())))
+
+
+def read_csr_cache(path):
+    h, info = C.c_void_p(), HostCsrInfo()
+    check(lib().asyrk_read_csr_cache(os.fsencode(path), C.byref(h), C.byref(info)))
+    return _take_host_csr(h, info)
+
+
+def write_csr_cache(path, A: HostCsr):
+    check(lib().asyrk_write_csr_cache(os.fsencode(path), C.byref(A.view())))
+
+
+def _take_vec(p, count):
+    try:
+        return np.ctypeslib.as_array(p, shape=(count,)).copy() if count else np.zeros(0)
+    finally:
+        lib().asyrk_free(p)
+
+
+def read_vector(path):
+    p, cnt = _f64p(), C.c_int64()
+    check(lib().asyrk_read_vector(os.fsencode(path), C.byref(p), C.byref(cnt)))
+    return _take_vec(p, cnt.value)
+
+
+def write_vector(path, v):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    check(lib().asyrk_write_vector(os.fsencode(path), _ptr(v, _f64p), len(v)))
+
+
+def write_instance(path, A: HostCsr, b, x_star=None, spec=None):
+    """write_instance (ref io.cpp:125-150): A.mtx, b.txt, xstar.txt, meta.json."""
+    spec = dict(spec or {})
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    xs = np.ascontiguousarray(x_star, dtype=np.float64) if x_star is not None else None
+    meta = InstanceMeta(spec.get("m", A.m), spec.get("n", A.n), spec.get("delta", A.nnz / (A.m * A.n)),
+                        spec.get("seed", 0), int(spec.get("consistent", xs is not None)),
+                        spec.get("noise_level", 0.0), int(xs is not None))
+    check(lib().asyrk_write_instance(os.fsencode(path), C.byref(A.view()), _ptr(b, _f64p), _ptr(xs, _f64p),
+                                     C.byref(meta)))
+
+
+def read_instance(path):
+    """read_instance (ref io.cpp:152-183) -> dict(A, b, x_star, spec)."""
+    h, pb, px, meta = C.c_void_p(), _f64p(), _f64p(), InstanceMeta()
+    check(lib().asyrk_read_instance(os.fsencode(path), C.byref(h), C.byref(pb), C.byref(px), C.byref(meta)))
+    info = HostCsrInfo()
+    check(lib().asyrk_host_csr_get_info(h, C.byref(info)))
+    A = _take_host_csr(h, info)
+    b = _take_vec(pb, meta.m)
+    xs = _take_vec(px, meta.n) if meta.has_x_star else None
+    spec = dict(m=meta.m, n=meta.n, delta=meta.delta, seed=meta.seed, consistent=bool(meta.consistent),
+                noise_level=meta.noise_level)
+    return dict(A=A, b=b, x_star=xs, spec=spec)
 
 
 def compute_stats(A: HostCsr, tol=1e-9, max_iters=200000):

@@ -11,7 +11,8 @@ import pytest
 
 from conftest import ROOT
 
-HEADERS = [os.path.join(ROOT, "include", "asyrk_cuda.h"), os.path.join(ROOT, "include", "asyrk_datagen.h")]
+HEADERS = [os.path.join(ROOT, "include", "asyrk_cuda.h"), os.path.join(ROOT, "include", "asyrk_datagen.h"),
+           os.path.join(ROOT, "include", "asyrk_io.h")]
 
 
 def declared_functions():
