@@ -91,6 +91,8 @@ struct DevState {
     // solve returns that snapshot, not the epochs that ran past it
     int stop_slot;
     long long stop_epoch, stop_updates;
+    // last-block tickets of the fused snapshot+advance and columns+finalize kernels
+    unsigned snap_ticket, mon_ticket;
 };
 
 struct DevRecord {

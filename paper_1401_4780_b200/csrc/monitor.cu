@@ -122,11 +122,9 @@ __global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m
 // Pass 2 / SpMV columns over SELL-32: lane l of group g owns column 32g + l.
 // out: g (or null), part: {g^2, dist^2} block partials (or null).
 template <class V, class X>
-__global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n, const double* __restrict__ r,
-                                                          double* out, double* part_g, double* part_d,
-                                                          const X* __restrict__ x, const double* __restrict__ x_star,
-                                                          const DevState* st) {
-    if (st && st->stop) return;
+__device__ __forceinline__ void cols_block(const CscDev& C, long long n, const double* __restrict__ r, double* out,
+                                           double* part_g, double* part_d, const X* __restrict__ x,
+                                           const double* __restrict__ x_star) {
     __shared__ double red_g[kMonThreads / 32], red_d[kMonThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long j = (long long)blockIdx.x * kMonThreads + threadIdx.x;
@@ -160,6 +158,15 @@ __global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n
         part_g[blockIdx.x] = a;
         part_d[blockIdx.x] = b;
     }
+}
+
+template <class V, class X>
+__global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n, const double* __restrict__ r,
+                                                          double* out, double* part_g, double* part_d,
+                                                          const X* __restrict__ x, const double* __restrict__ x_star,
+                                                          const DevState* st) {
+    if (st && st->stop) return;
+    cols_block<V, X>(C, n, r, out, part_g, part_d, x, x_star);
 }
 
 // Record + stop decision. Three modes:
@@ -249,14 +256,14 @@ __global__ void finalize_exact_kernel(MonitorArgs a) {
 }
 
 // ---- finalize, fast: fixed-order sum of the block partials (one block)
-__global__ void __launch_bounds__(kMonThreads) finalize_fast_kernel(MonitorArgs a, int nb_rows, int nb_cols) {
+__device__ __forceinline__ void finalize_fast_block(const MonitorArgs& a, int nb_rows, int nb_cols) {
     if (!a.force && a.st->stop) return;
     __shared__ double red[3][kMonThreads];
     double s[3] = {0.0, 0.0, 0.0};
-    for (int k = threadIdx.x; k < nb_rows; k += kMonThreads) s[0] += a.part[k];
+    for (int k = threadIdx.x; k < nb_rows; k += kMonThreads) s[0] += __ldcg(a.part + k);
     for (int k = threadIdx.x; k < nb_cols; k += kMonThreads) {
-        s[1] += a.part[nb_rows + k];
-        s[2] += a.part[nb_rows + nb_cols + k];
+        s[1] += __ldcg(a.part + nb_rows + k);
+        s[2] += __ldcg(a.part + nb_rows + nb_cols + k);
     }
     for (int c = 0; c < 3; ++c) red[c][threadIdx.x] = s[c];
     __syncthreads();
@@ -266,6 +273,25 @@ __global__ void __launch_bounds__(kMonThreads) finalize_fast_kernel(MonitorArgs 
         __syncthreads();
     }
     if (threadIdx.x == 0) commit_record(a, red[0][0], red[1][0], red[2][0]);
+}
+
+// columns pass + finalize_fast in the last block to finish (async path):
+// blocks always take their ticket, so the counter resets even when a stop
+// makes them skip the work (the finalize then skips too)
+template <class V, class X>
+__global__ void __launch_bounds__(kMonThreads) cols_final_kernel(MonitorArgs a, int nb_rows, int nb_cols) {
+    const DevState* gate = a.force ? nullptr : a.st;
+    if (!(gate && gate->stop))
+        cols_block<V, X>(a.csc, a.L.n, a.r, nullptr, a.part + nb_rows, a.part + nb_rows + nb_cols,
+                         static_cast<const X*>(a.x), a.x_star);
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&a.st->mon_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    if (threadIdx.x == 0) a.st->mon_ticket = 0;
+    finalize_fast_block(a, nb_rows, nb_cols);
 }
 
 // ---- launch geometry
@@ -279,13 +305,12 @@ static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
     const X* x = static_cast<const X*>(a.x);
     const DevState* gate = a.force ? nullptr : a.st;  // the final record runs after stop
     rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, gate);
-    cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.exact ? a.g : nullptr,
-                                                  a.exact ? nullptr : a.part + nbr,
-                                                  a.exact ? nullptr : a.part + nbr + nbc, x, a.x_star, gate);
-    if (a.exact)
+    if (a.exact) {
+        cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.g, nullptr, nullptr, x, a.x_star, gate);
         finalize_exact_kernel<<<1, 32, 0, s>>>(a);
-    else
-        finalize_fast_kernel<<<1, kMonThreads, 0, s>>>(a, nbr, nbc);
+    } else {
+        cols_final_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr, nbc);
+    }
 }
 
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s) {

@@ -129,6 +129,7 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->go = 0;  // set by the initial record's commit
     st->snap_valid[0] = st->snap_valid[1] = 0;
     st->stop_slot = -1;
+    st->snap_ticket = st->mon_ticket = 0;
     st->t0_ns = globaltimer_ns();
 }
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
@@ -262,17 +263,26 @@ void launch_set_rhs(const Layout& L, const double* b, cudaStream_t s) {
 namespace ak {
 
 // ---- overlapped async solve: epoch-boundary snapshot of x for the monitor
-// stream, then the coordinator state advance (one thread). Both read `go`,
-// which only advance_kernel changes, so a whole epoch is either run and
-// counted or skipped.
+// stream, then (last block to finish) the coordinator state advance. Every
+// block reads `go` before taking its ticket and only the last block changes
+// it, so a whole epoch is either run and counted or skipped.
 template <class X>
-__global__ void snapshot_kernel(const DevState* st, const X* __restrict__ x, X* __restrict__ xs, long long n) {
-    if (!st->go || st->stop) return;  // after a stop the deciding snapshot must survive
-    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
-        xs[k] = __ldcg(x + k);
-}
-
-__global__ void advance_kernel(DevState* st, int slot, long long m) {
+__global__ void snapshot_kernel(DevState* st, const X* __restrict__ x, X* __restrict__ xs, long long n, int slot,
+                                long long m) {
+    __shared__ int copy;
+    __shared__ bool last;
+    if (threadIdx.x == 0) copy = st->go && !st->stop;  // after a stop the deciding snapshot must survive
+    __syncthreads();
+    if (copy)
+        for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+             k += (long long)gridDim.x * blockDim.x)
+            xs[k] = __ldcg(x + k);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->snap_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    st->snap_ticket = 0;
     if (st->stop) {  // stopped: the slots are frozen, no further epochs
         st->go = 0;
         return;
@@ -318,12 +328,14 @@ void launch_restore(DevState* st, void* x, const void* xs0, const void* xs1, lon
 
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
                      long long m, cudaStream_t s) {
+    (void)st;
     const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
     if (precision == P_F32)
-        snapshot_kernel<float><<<blocks, 256, 0, s>>>(st, static_cast<const float*>(x), static_cast<float*>(xs), n);
+        snapshot_kernel<float><<<blocks, 256, 0, s>>>(stw, static_cast<const float*>(x), static_cast<float*>(xs), n,
+                                                      slot, m);
     else
-        snapshot_kernel<double><<<blocks, 256, 0, s>>>(st, static_cast<const double*>(x), static_cast<double*>(xs), n);
-    advance_kernel<<<1, 1, 0, s>>>(stw, slot, m);
+        snapshot_kernel<double><<<blocks, 256, 0, s>>>(stw, static_cast<const double*>(x), static_cast<double*>(xs),
+                                                       n, slot, m);
 }
 
 }  // namespace ak

@@ -621,7 +621,8 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st);
     long long launches = 1;
     launch_monitor(monitor_args(s, sp.det, 0, sp.x_star != nullptr), prec, st);
-    launches += 3;
+    const int mon_kernels = sp.det ? 3 : 2;  // rows + columns (+ exact finalize); fast finalize is fused
+    launches += mon_kernels;
     s->stats.monitor_launches++;
 
     // worker setup
@@ -788,10 +789,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             ma.slot = slot2;
             launch_monitor(ma, prec, s->mstream);
             CK(cudaEventRecord(s->mon_ev[slot2], s->mstream));
-            launches += 5;
+            launches += 1 + mon_kernels;  // snapshot (+ fused advance) + monitor
         } else {
             launch_monitor(monitor_args(s, sp.det, 1, sp.x_star != nullptr), prec, st);
-            launches += 3;
+            launches += mon_kernels;
         }
         s->stats.monitor_launches++;
         CK(cudaEventRecord(s->ev_chunk[(size_t)(k % (kLookahead + 1))], st));
@@ -808,7 +809,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         MonitorArgs fa = monitor_args(s, false, 0, sp.x_star != nullptr);
         fa.force = 1;
         launch_monitor(fa, prec, st);
-        launches += 3;
+        launches += 1 + mon_kernels;  // restore + final record
         s->stats.monitor_launches++;
         CK(cudaGetLastError());
     }
