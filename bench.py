@@ -452,6 +452,161 @@ def run_gpu_cfg5(args):
     return 0
 
 
+# ---- the other BASELINE configs (BASELINE.json configs[0], [2], [3]) and the warp sweep
+OTHER = {
+    "cfg1": dict(m=20000, n=10000, theta=20, seed=1001, dist="normal", scale=0.0, tol=1e-8, epochs=20,
+                 desc="config1: m=20000 n=10000 theta=20 N(0,1) unit rows fp64, deterministic 1 worker, uniform "
+                      "seeded sequence, until ||r||/||b||<1e-8 or 20 epochs"),
+    "cfg3": dict(m=2000000, n=1000000, theta=50, seed=1003, dist="uniform", scale=0.0, tol=1e-5, epochs=400,
+                 desc="config3: m=2000000 n=1000000 theta=50 U(-1,1) unit rows, fp32 values + fp32 x/atomics, "
+                      "async to ||r||/||b||<1e-5"),
+    "cfg3x": dict(m=2000000, n=1000000, theta=50, seed=1003, dist="uniform", scale=0.0, tol=1e-5, epochs=400,
+                  desc="config3 (fp64-x variant): fp32 values, fp64 x/atomics, async to ||r||/||b||<1e-5"),
+    "cfg4": dict(m=400000, n=100000, theta=25, seed=1004, dist="normal", scale=1.0, tol=1e-6, epochs=1000,
+                 desc="config4: m=400000 n=100000 theta=25 N(0,1) rows scaled log-uniform [0.1,10] fp64, "
+                      "alias sampling P(i)=||a_i||^2/||A||_F^2, async to ||r||/||b||<1e-6"),
+}
+
+
+def run_other(args):
+    """Throughput and time-to-tolerance of BASELINE configs 1, 3 (+fp64-x), 4 on one GPU
+    (device time, CUDA events), with the reference's CPU path on a bounded sample
+    beside it (rank 0 only; replicas are not run for these)."""
+    import torch
+
+    from paper_1401_4780_b200 import capi
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    c = OTHER[args.workload]
+    A, b, xs = capi.generate_fixed_theta(c["m"], c["n"], c["theta"], seed=c["seed"], dist=c["dist"],
+                                         scale_decades=c["scale"])
+    bb = float(b @ b)
+    target = c["tol"] ** 2 * bb
+    prec = {"cfg3": capi.F32, "cfg3x": capi.F32X64}.get(args.workload, capi.F64)
+    S = capi.System(A, b, precision=prec)
+    det = args.workload == "cfg1"
+    W = 1 if det else (args.warps or (3 * S.max_resident_warps()) // 4)
+    if det:
+        run = lambda k: S.rk_solve(max_epochs=c["epochs"], target=target, seed=42 + k,  # noqa: E731
+                                   sampling=capi.RK_UNIFORM, x_star=xs)
+    else:
+        samp = capi.NORM_PROPORTIONAL if args.workload == "cfg4" else capi.WITH_REPLACEMENT
+        run = lambda k: S.solve(threads=W, gamma=1.0, epochs=c["epochs"], target=target, sampling=samp,  # noqa: E731
+                                seed=100 + k, snapshot_interval=1, x_star=xs, want_x=False, precision=prec)
+    for k in range(args.warmup):
+        run(k)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    proj, ttt, rels, errs, epochs = 0, [], [], [], []
+    with ClockSampler(0) as clk:
+        for k in range(args.steps):
+            ev[k][0].record()
+            t = run(1000 + k)
+            ev[k][1].record()
+            torch.cuda.synchronize()
+            ttt.append(ev[k][0].elapsed_time(ev[k][1]))
+            proj += int(t["updates_applied"][-1])
+            epochs.append(int(t["epoch_index"][-1]))
+            rels.append(float(np.sqrt(t["r_sq"][-1] / bb)))
+            errs.append(float(np.sqrt(t["dist_sq"][-1] / float(xs @ xs))))
+    dev_ms = sum(ttt)
+    line = {"metric": METRIC + f" ({args.workload})", "value": proj / (dev_ms * 1e-3), "unit": "proj/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": {"cfg3": "f32", "cfg3x": "f32 values, f64 x"}.get(args.workload, "f64"), "data": "synthetic",
+            "config": {"workload": c["desc"], "warps": W, "l2": "A resident (no flush between steps)"},
+            "time_to_tolerance_ms": statistics.median(ttt), "epochs": statistics.median(epochs),
+            "final_rel_residual": max(rels), "final_rel_error": max(errs), "tolerance": c["tol"],
+            "gpu_launches": S.stats()["kernel_launches"] * args.steps, "clocks": clk.summary()}
+    if det:
+        line["parity"] = "final_x bit-identical to the reference rk_solve" if ref_cfg1_parity(A, b, c, xs, S) \
+            else "MISMATCH against the reference rk_solve"
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = other_cpu_baseline(args.workload, c, A, b)
+    S.close()
+    print(json.dumps(line))
+    return 0
+
+
+def ref_cfg1_parity(A, b, c, xs, S):
+    from paper_1401_4780_b200 import capi
+
+    R = load_ref()
+    if R is None:
+        return False
+    Ah = ref_matrix(R, A)
+    t = R.rk_solve(Ah, b, np.zeros(A.n), c["epochs"], c["tol"] ** 2 * float(b @ b), 42, "uniform", xs)
+    mine = S.rk_solve(max_epochs=c["epochs"], target=c["tol"] ** 2 * float(b @ b), seed=42, sampling=capi.RK_UNIFORM,
+                      x_star=xs)
+    return bool(np.array_equal(t["final_x"], mine["final_x"]) and np.array_equal(t["r_sq"], mine["r_sq"]))
+
+
+def other_cpu_baseline(name, c, A, b):
+    """The reference's own CPU path on a bounded sample of the same workload."""
+    R = load_ref()
+    if R is None:
+        return None
+    Ah = ref_matrix(R, A)
+    cores = host_cores()
+    x0 = np.zeros(A.n)
+    if name == "cfg1":  # serial rk_solve, the full run (20 epochs)
+        t = R.rk_solve(Ah, b, x0, c["epochs"], c["tol"] ** 2 * float(b @ b), 42, "uniform")
+        p, w, cores, sample = int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), 1, "the full config-1 run"
+    elif name == "cfg4":  # raw rows: the reference's async solver needs unit rows; serial norm-proportional rk_solve
+        Ar, _ = R.build(A.m, A.n, np.repeat(np.arange(A.m), np.diff(A.row_ptr)), A.col_idx, A.values, False, None)
+        t = R.rk_solve(Ar, b, x0, 1, 0.0, 42, "norm")
+        p, w, cores, sample = int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), 1, \
+            "1 epoch of serial rk_solve(norm_proportional) on the raw rows"
+    else:  # cfg3: the reference runs fp64 only; 1 epoch of solve_parallel on all host threads
+        t = R.solve_parallel(Ah, b, x0, threads=cores, gamma=1.0, epochs=1, target=0.0, variant="full_row",
+                             sampling="with_replacement", seed=7, snapshot_interval=1, cap=4)
+        p, w, sample = int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), \
+            f"1 epoch of solve_parallel (fp64), {cores} threads"
+    return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference", "sample": sample}
+
+
+def run_sweep(args):
+    """Config 2 with the active-warp count swept (BASELINE configs[1]): time to
+    tolerance, epochs and throughput per warp count W beside the delay bound
+    tau_max = m / (2 e lambda_max) - 1 (stepsize.cpp:59-82); ~2 W rows are in
+    flight at once (2 per warp)."""
+    import torch
+
+    from paper_1401_4780_b200 import capi
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    A, b, xs = gen_system(CFG2["seed"])
+    bb = float(b @ b)
+    S = capi.System(A, b)
+    lam, _ = S.power_iteration(1e-6)
+    tau_max = CFG2["m"] / (2 * np.e * lam) - 1
+    res = S.max_resident_warps()
+    points = []
+    for W in [32, 148, 592, 1184, 2368, 2664, 3552]:
+        if W > res:
+            continue
+        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL * TOL * bb, sampling=capi.WITH_REPLACEMENT,
+                  snapshot_interval=1, x_star=xs, want_x=False)
+        S.solve(seed=1, **kw)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        t = S.solve(seed=2, **kw)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        points.append({"warps": W, "rows_in_flight": 2 * W, "time_to_tolerance_ms": ms,
+                       "epochs": int(t["epoch_index"][-1]), "proj_per_s": int(t["updates_applied"][-1]) / (ms * 1e-3),
+                       "rel_error": float(np.sqrt(t["dist_sq"][-1] / float(xs @ xs)))})
+    S.close()
+    print(json.dumps({"metric": METRIC + " (warp sweep)", "unit": "proj/s", "n_gpus": 1, "data": "synthetic",
+                      "dtype": "f64", "config": {"workload": workload_config(None)["workload"],
+                                                 "lambda_max": lam, "tau_max": tau_max,
+                                                 "resident_warps": res}, "points": points}))
+    return 0
+
+
 MC = dict(m=1200, n=60, theta=5, seed=77, runs=1000, iterations=2000, tau=5, gamma=0.15, base_seed=99)
 MC_METRIC = "bounded-delay simulator iterations/sec (monte_carlo_ratios, acceptance C2 shape)"
 
@@ -533,11 +688,16 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = 3/4 of the resident warp slots)")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc", "cfg1", "cfg3", "cfg3x", "cfg4",
+                                                           "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.workload == "mc":
         return run_mc(args)
+    if args.workload in OTHER:
+        return run_other(args)
+    if args.workload == "sweep":
+        return run_sweep(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg5":
