@@ -436,7 +436,22 @@ def run_gpu_cfg5(args):
         dist.all_reduce(t)
         col_proj = float(t.item())
     if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            R = load_ref()
+            if R is not None:  # the reference solves one RHS at a time: 1 epoch of column 0 on all host threads
+                Ah = ref_matrix(R, A)
+                cores = host_cores()
+                bn = B[:, 0].astype(np.float64)
+                t = R.solve_parallel(Ah, bn, np.zeros(A.n), threads=cores, gamma=1.0, epochs=1, target=0.0,
+                                     variant="full_row", sampling="with_replacement", seed=7, snapshot_interval=1,
+                                     cap=4)
+                cpu = {"value": int(t["updates_applied"][-1]) / float(t["wall_seconds"][-1]), "unit": "proj/s",
+                       "cores": cores, "kind": "reference",
+                       "sample": "1 epoch of solve_parallel (fp64) on RHS column 0; the reference solves the 64 "
+                                 "columns one after another"}
         print(json.dumps({
+            "cpu_baseline": cpu,
             "metric": METRIC + " (config 5: column projections/sec)", "value": col_proj / (dev_ms * 1e-3),
             "unit": "proj/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
