@@ -54,6 +54,8 @@ struct DetArgs {
     double* ev_b;                 // per event: b_i
     double* ev_nrm;               // per event: row_norm_i
     long long* dbg;               // optional per-event phase timestamps (diagnostics)
+    int poll_ns;                  // dataflow polling back-off (0: spin)
+    uint32_t max_len;             // longest row (picks the dataflow kernel's elements per lane)
 };
 void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);

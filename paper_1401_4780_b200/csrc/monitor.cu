@@ -228,31 +228,113 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
 }
 
 // ---- finalize, exact: serial sums in the reference's order (residuals
-// csr.cpp:147-158, dist oracle parallel.cpp:82-92). Lanes square 32 values at
-// a time; lane 0 accumulates them in index order.
-__device__ __forceinline__ double serial_sumsq(const double* v, const double* w, long long n, int lane) {
-    double s = 0.0;
-    for (long long c0 = 0; c0 < n; c0 += 32) {
-        const long long k = c0 + lane;
-        double q = 0.0;
-        if (k < n) {
-            const double d = w ? __dsub_rn(v[k], w[k]) : v[k];
-            q = __dmul_rn(d, d);
+// csr.cpp:147-158, dist oracle parallel.cpp:82-92). The three sums are
+// independent chains, one warp each; lane 0 of the warp streams its series
+// through a kFinStages-deep shared-memory ring filled by 1D bulk copies
+// (cp.async.bulk, completion on an mbarrier), so its loop runs at the
+// latency of the dependent adds instead of a memory round trip per element.
+constexpr int kFinChunk = 256;  // doubles per stage (2 KB)
+constexpr int kFinStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(phase)
+                     : "memory");
+}
+
+// serial sum_k (v_k - w_k)^2 (w may be null) by one thread, streamed through
+// bv / bw (kFinStages x kFinChunk doubles each)
+__device__ double streamed_sumsq(const double* v, const double* w, long long n, double* bv, double* bw,
+                                 uint64_t* bar) {
+    const long long chunks = (n + kFinChunk - 1) / kFinChunk;
+    auto issue = [&](long long c) {
+        const int st = (int)(c % kFinStages);
+        const long long e0 = c * kFinChunk;
+        const int cnt = (int)min((long long)kFinChunk, n - e0) & ~1;  // bulk copies move multiples of 16 B
+        const uint32_t bytes = (uint32_t)cnt * 8u * (w ? 2u : 1u);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + st)), "r"(bytes)
+                     : "memory");
+        if (cnt) {
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(bv + st * kFinChunk)),
+                "l"(v + e0), "r"((uint32_t)cnt * 8u), "r"(smem_u32(bar + st))
+                : "memory");
+            if (w)
+                asm volatile(
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                        smem_u32(bw + st * kFinChunk)),
+                    "l"(w + e0), "r"((uint32_t)cnt * 8u), "r"(smem_u32(bar + st))
+                    : "memory");
         }
-        const int lim = (int)min(32ll, n - c0);
-        for (int t = 0; t < lim; ++t) s = __dadd_rn(s, __shfl_sync(FULL, q, t));
+    };
+    for (long long c = 0; c < chunks && c < kFinStages; ++c) issue(c);
+    double s = 0.0;
+    for (long long c = 0; c < chunks; ++c) {
+        const int st = (int)(c % kFinStages);
+        mbar_wait(bar + st, (uint32_t)((c / kFinStages) & 1));
+        const long long e0 = c * kFinChunk;
+        const int cnt = (int)min((long long)kFinChunk, n - e0);
+        const int even = cnt & ~1;
+        const double* pv = bv + st * kFinChunk;
+        const double* pw = bw + st * kFinChunk;
+        int k = 0;
+        for (; k + 8 <= even; k += 8) {
+            double q[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const double d = w ? __dsub_rn(pv[k + u], pw[k + u]) : pv[k + u];
+                q[u] = __dmul_rn(d, d);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s = __dadd_rn(s, q[u]);
+        }
+        for (; k < even; ++k) {
+            const double d = w ? __dsub_rn(pv[k], pw[k]) : pv[k];
+            s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+        if (cnt & 1) {  // the odd last element straight from global memory
+            const double d = w ? __dsub_rn(__ldcg(v + e0 + cnt - 1), __ldcg(w + e0 + cnt - 1)) : __ldcg(v + e0 + cnt - 1);
+            s = __dadd_rn(s, __dmul_rn(d, d));
+        }
+        if (c + kFinStages < chunks) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+            issue(c + kFinStages);
+        }
     }
     return s;
 }
 
-__global__ void finalize_exact_kernel(MonitorArgs a) {
+__global__ void __launch_bounds__(96) finalize_exact_kernel(MonitorArgs a) {
     if (!a.force && a.st->stop) return;
-    const int lane = threadIdx.x & 31;
-    const double rs = serial_sumsq(a.r, nullptr, a.L.m, lane);
-    const double gs = serial_sumsq(a.g, nullptr, a.L.n, lane);
-    double ds = 0.0;
-    if (a.x_star) ds = serial_sumsq(static_cast<const double*>(a.x), a.x_star, a.L.n, lane);  // exact mode is fp64
-    if (lane == 0) commit_record(a, rs, gs, ds);
+    __shared__ __align__(128) double bufv[3][kFinStages * kFinChunk];
+    __shared__ __align__(128) double bufw[kFinStages * kFinChunk];
+    __shared__ __align__(8) uint64_t bar[3][kFinStages];
+    __shared__ double res[3];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        for (int k = 0; k < kFinStages; ++k) mbar_init(&bar[w][k]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        double r = 0.0;
+        if (w == 0)
+            r = streamed_sumsq(a.r, nullptr, a.L.m, bufv[0], nullptr, bar[0]);
+        else if (w == 1)
+            r = streamed_sumsq(a.g, nullptr, a.L.n, bufv[1], nullptr, bar[1]);
+        else if (a.x_star)  // exact mode is fp64
+            r = streamed_sumsq(static_cast<const double*>(a.x), a.x_star, a.L.n, bufv[2], bufw, bar[2]);
+        res[w] = r;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) commit_record(a, res[0], res[1], res[2]);
 }
 
 // ---- finalize, fast: fixed-order sum of the block partials (one block)
@@ -307,7 +389,7 @@ static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
     rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, gate);
     if (a.exact) {
         cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.g, nullptr, nullptr, x, a.x_star, gate);
-        finalize_exact_kernel<<<1, 32, 0, s>>>(a);
+        finalize_exact_kernel<<<1, 96, 0, s>>>(a);
     } else {
         cols_final_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a, nbr, nbc);
     }

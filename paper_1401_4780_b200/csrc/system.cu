@@ -652,6 +652,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.gamma = sp.gamma;
         da.full_row = sp.full_row ? 1 : 0;
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
+        // waiting warps back off between polls so they leave issue slots to the running events
+        static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
+        da.poll_ns = poll_ns;
+        da.max_len = s->max_len;
         da.need = s->need;
         da.ev_col = s->prep.keys;
         da.ev_val = s->prep.ev_val;
