@@ -33,10 +33,17 @@ if os.path.exists(rep):
     txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), rep],
                          capture_output=True, text=True).stdout
     open(os.path.join(dst, f"{tag}_ncu_full.txt"), "w").write(
-        "# ncu --set full --clock-control none --import-source on -k regex:worker_kernel|rows_kernel|cols_kernel\n" + txt)
+        "# ncu --set full --clock-control none --import-source on -k regex:worker_kernel|rows_kernel|cols_kernel|cols_final_kernel\n" + txt)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h = rows[0]
+    reqs = {}
+    for v in rows[2:]:  # L2 requests per launch of each captured kernel (first launch of each)
+        name = v[h.index("Kernel Name")]
+        key = "worker" if "worker_kernel" in name else "rows" if "rows_kernel" in name else \
+            "cols" if "cols" in name else None
+        if key and key not in reqs:
+            reqs[key] = float(v[h.index("lts__t_requests.sum")].replace(",", ""))
     for v in rows[2:]:
         if "worker_kernel" in v[h.index("Kernel Name")]:
             num = lambda k: float(v[h.index(k)].replace(",", ""))  # noqa: E731
@@ -48,7 +55,8 @@ if os.path.exists(rep):
                  "lts_t_requests": num("lts__t_requests.sum"),
                  "lts_tag_requests_pct_avg": num("lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed"),
                  "lts_tag_requests_pct_max": num("lts__t_tag_requests.max.pct_of_peak_sustained_elapsed"),
-                 "projections_per_launch": 200000}
+                 "projections_per_launch": 200000,
+                 "lts_requests_per_launch": reqs}
             json.dump(d, open(os.path.join(dst, "worker_ncu_summary.json"), "w"), indent=1)
             break
 print("saved", tag)
