@@ -1,11 +1,12 @@
 // x-side roofline microbenchmark (SURVEY.md §8d "R_x"): the x traffic of one
-// projection with no A stream — theta random L2-resident gathers of x, a warp
+// projection with no A stream — theta (<= 128) random L2-resident gathers of x, a warp
 // reduction, then theta random red.global.add — at a given warp count and x
 // footprint. Modes: 0 gather -> reduce -> red (the worker's dependent chain),
 // 1 gathers only, 2 reds only. Indices come from a counter hash, so no memory
 // other than x is touched. Used by bench.py to state the L2/atomic-bound
 // roofline beside the HBM one.
 #include "../../include/asyrk_cuda.h"
+#include "capi_common.h"
 #include "kernels.h"
 
 namespace ak {
@@ -26,16 +27,27 @@ __global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta,
     const int lane = threadIdx.x & 31;
     X acc_all = X(0);
     for (long long q = 0; q < per_warp; ++q) {
-        const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)lane * 0xC2B2AE35u);
-        const uint32_t col = (uint32_t)(((uint64_t)h * n) >> 32);
-        const bool on = lane < theta;
+        // theta <= 128: lane l owns entries l, l + 32, l + 64, l + 96 (the worker's E slots)
+        uint32_t col[4];
+        bool on[4];
         X s = X(0);
-        if (mode != 2 && on) s = __ldcg(x + col);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int k = lane + 32 * e;
+            on[e] = k < theta;
+            const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)k * 0xC2B2AE35u);
+            col[e] = (uint32_t)(((uint64_t)h * n) >> 32);
+            if (mode != 2 && on[e]) s += __ldcg(x + col[e]);
+        }
         if (mode == 0) {
             s = warp_sum(s);
-            if (on) atomicAdd(x + col, X(1e-30) * s);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (on[e]) atomicAdd(x + col[e], X(1e-30) * s);
         } else if (mode == 2) {
-            if (on) atomicAdd(x + col, X(1e-30));
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (on[e]) atomicAdd(x + col[e], X(1e-30));
         } else {
             acc_all += s;
         }
@@ -49,7 +61,8 @@ extern "C" asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t
                                                int64_t proj_per_warp, int32_t mode, double* proj_per_s,
                                                double* kernel_ms) {
     using namespace ak;
-    if (n < 1 || theta < 1 || theta > 32 || warps < 1 || proj_per_warp < 1) return ASYRK_E_InvalidArgument;
+    if (n < 1 || theta < 1 || theta > 128 || warps < 1 || proj_per_warp < 1)
+        return fail(ASYRK_E_InvalidArgument, "microbench_xside: need n >= 1, 1 <= theta <= 128, warps >= 1");
     void* x = nullptr;
     unsigned long long* sink = nullptr;
     const size_t xb = (size_t)n * (precision == P_F32 ? 4 : 8);
