@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -127,6 +128,65 @@ struct asyrk_system {
 
 namespace {
 
+// Streams and events of library-owned systems are recycled: the one-shot
+// entry points build and drop a system per call, and creating / destroying
+// three streams and a dozen events costs ~0.3 ms a call.
+struct StreamKit {
+    int dev = 0;
+    cudaStream_t stream = nullptr, mstream = nullptr;
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    std::vector<cudaEvent_t> ev_w, ev_chunk;
+    cudaEvent_t snap_ev[2] = {nullptr, nullptr}, mon_ev[2] = {nullptr, nullptr};
+};
+std::mutex g_kit_mu;
+std::vector<StreamKit> g_kits;
+constexpr size_t kMaxKits = 8;
+
+bool kit_take(asyrk_system* s) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_kit_mu);
+    for (size_t i = 0; i < g_kits.size(); ++i)
+        if (g_kits[i].dev == dev) {
+            StreamKit k = std::move(g_kits[i]);
+            g_kits.erase(g_kits.begin() + (long)i);
+            s->stream = k.stream;
+            s->mstream = k.mstream;
+            s->ev_begin = k.ev_begin;
+            s->ev_end = k.ev_end;
+            s->ev_w = std::move(k.ev_w);
+            s->ev_chunk = std::move(k.ev_chunk);
+            for (int q = 0; q < 2; ++q) {
+                s->snap_ev[q] = k.snap_ev[q];
+                s->mon_ev[q] = k.mon_ev[q];
+            }
+            return true;
+        }
+    return false;
+}
+
+// after the streams are idle: park them for the next library-owned system
+bool kit_put(asyrk_system* s) {
+    int dev = 0;
+    if (!s->own_stream || !s->stream || cudaGetDevice(&dev) != cudaSuccess) return false;
+    std::lock_guard<std::mutex> lk(g_kit_mu);
+    if (g_kits.size() >= kMaxKits) return false;
+    StreamKit k;
+    k.dev = dev;
+    k.stream = s->stream;
+    k.mstream = s->mstream;
+    k.ev_begin = s->ev_begin;
+    k.ev_end = s->ev_end;
+    k.ev_w = std::move(s->ev_w);
+    k.ev_chunk = std::move(s->ev_chunk);
+    for (int q = 0; q < 2; ++q) {
+        k.snap_ev[q] = s->snap_ev[q];
+        k.mon_ev[q] = s->mon_ev[q];
+    }
+    g_kits.push_back(std::move(k));
+    return true;
+}
+
 void free_all(asyrk_system* s) {
     cudaStream_t fs = s->stream;
     auto F = [fs](void* p) { pool_free(p, fs); };
@@ -177,20 +237,19 @@ void free_all(asyrk_system* s) {
         if (s->seq_host[k]) cudaFreeHost(s->seq_host[k]);
         if (s->pick_host[k]) cudaFreeHost(s->pick_host[k]);
     }
+    for (int q = 0; q < 2; ++q) F(s->xs[q]);
+    if (s->mstream) cudaStreamSynchronize(s->mstream);
+    if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
+    if (kit_put(s)) return;
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
     for (auto e : s->ev_w) cudaEventDestroy(e);
     for (auto e : s->ev_chunk) cudaEventDestroy(e);
     for (int q = 0; q < 2; ++q) {
-        F(s->xs[q]);
         if (s->snap_ev[q]) cudaEventDestroy(s->snap_ev[q]);
         if (s->mon_ev[q]) cudaEventDestroy(s->mon_ev[q]);
     }
-    if (s->mstream) {
-        cudaStreamSynchronize(s->mstream);
-        cudaStreamDestroy(s->mstream);
-    }
-    if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
+    if (s->mstream) cudaStreamDestroy(s->mstream);
     if (s->own_stream && s->stream) cudaStreamDestroy(s->stream);
 }
 
@@ -299,7 +358,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     if (stream) {
         s->stream = static_cast<cudaStream_t>(stream);
     } else {
-        CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+        if (!kit_take(s.get())) CK(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
         s->own_stream = true;
     }
     AllocStream alloc_on(s->stream);
@@ -701,9 +760,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         for (int q = 0; q < 2; ++q) {
             CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&s->mon_ev[q], cudaEventDisableTiming));
-            s->xs[q] = dalloc<unsigned char>((size_t)s->n * s->xbytes());
         }
     }
+    if (overlap && !s->xs[0])  // (a recycled stream kit brings the stream and events, not the buffers)
+        for (int q = 0; q < 2; ++q) s->xs[q] = dalloc<unsigned char>((size_t)s->n * s->xbytes());
     long long timed = 0;
     long long k = 0;
     for (; k < max_chunks; ++k) {
@@ -1451,11 +1511,26 @@ asyrk_status asyrk_solve_parallel(const asyrk_csr_view* A, const double* b, cons
                                   asyrk_instrument_out* instrument) {
     if (!cfg) return fail(ASYRK_E_InvalidArgument, "null config");
     return guarded([&] {
-        SysGuard g;
-        const int prec = cfg->threads == 1 ? P_F64 : cfg->precision;
-        asyrk_status s = create_impl(A, b, prec, nullptr, &g.s);
-        if (s) return s;
-        return system_solve_impl(g.s, x0, cfg, trace, instrument);
+        static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
+        asyrk_status s;
+        {
+            SysGuard g;
+            const int prec = cfg->threads == 1 ? P_F64 : cfg->precision;
+            s = create_impl(A, b, prec, nullptr, &g.s);
+            if (s) return s;
+            const auto t1 = std::chrono::steady_clock::now();
+            s = system_solve_impl(g.s, x0, cfg, trace, instrument);
+            if (prof)
+                fprintf(stderr, "[one-shot] create %.3f ms solve %.3f ms (device %.3f ms)\n",
+                        std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count(),
+                        g.s->stats.solve_ms);
+        }
+        if (prof)
+            fprintf(stderr, "[one-shot] total %.3f ms\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        return s;
     });
 }
 
