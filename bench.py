@@ -229,9 +229,9 @@ def run_gpu(args):
     target = TOL * TOL * bb
     stream = torch.cuda.Stream()
     S = capi.System(A, b, stream=stream.cuda_stream)
-    # 3/4 of the resident warp slots: the residual monitor of epoch k runs on its
-    # own stream beside the epoch-(k+1) workers and needs SM room
-    W = args.warps or (3 * S.max_resident_warps()) // 4
+    # all resident warp slots: the residual monitor runs on its own stream and takes
+    # the latest epoch boundary it can, so the workers never wait for it
+    W = args.warps or S.max_resident_warps()
     lam, lam_iters = S.power_iteration(1e-6)  # stats.cpp:15-50 on the device; tau bound beside the warp count
     flush =torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     solve_kw = dict(threads=W, gamma=1.0, epochs=2000, target=target, sampling=capi.WITH_REPLACEMENT,
@@ -720,7 +720,7 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = 3/4 of the resident warp slots)")
+    ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = all resident warp slots)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc", "cfg1", "cfg3", "cfg3x", "cfg4",
                                                            "sweep"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -94,7 +94,9 @@ struct MonitorArgs {
     int exact;                    // 1: reference summation order (bitwise)
     CscDev rows;                  // SELL-32 rows of A (pass 1)
     const double* b;              // m
-    int slot;                     // >= 0: record the epoch-boundary snapshot in this slot (overlapped solve)
+    int slot;                     // >= 0: record the epoch-boundary snapshot in this slot (overlapped solve);
+                                  // kDynSlot: the slot the monitor stream claimed (st->mon_slot), x / x_alt
+    const void* x_alt;            // kDynSlot: the snapshot buffer of slot 1 (x is slot 0's)
     int force;                    // 1: run even after stop (the final exact record); replaces a same-epoch record
     int advance;                  // 0: initial record, 1: after a chunk
     long long m_rows;
@@ -104,6 +106,12 @@ void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 // advance the coordinator state (epoch, updates, slot meta, next go)
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
                      long long m, cudaStream_t s);
+// decoupled variant: a free slot or none (no record for that boundary); then the
+// monitor stream claims the oldest filled slot (MonitorArgs::slot = kDynSlot)
+void launch_snapshot_dyn(DevState* st, const void* x, void* xs0, void* xs1, long long n, int precision, long long m,
+                         cudaStream_t s);
+void launch_claim(DevState* st, cudaStream_t s);
+constexpr int kDynSlot = 2;
 // end of an overlapped solve: x, epoch and updates back to the snapshot whose
 // record decided the stop (no-op when the stop came from the epoch cap in-stream)
 void launch_restore(DevState* st, void* x, const void* xs0, const void* xs1, long long n, int precision,

@@ -93,6 +93,12 @@ struct DevState {
     long long stop_epoch, stop_updates;
     // last-block tickets of the fused snapshot+advance and columns+finalize kernels
     unsigned snap_ticket, mon_ticket;
+    // decoupled snapshots (the reference coordinator's "latest boundary"): slot
+    // states 0 free, 1 filling, 2 filled, 3 being monitored; the snapshot kernel's
+    // first block picks a free slot (or none), the monitor claims the oldest filled
+    int slot_state[2];
+    unsigned snap_arrive, snap_seq, snap_decided;
+    int snap_target, mon_slot;
 };
 
 struct DevRecord {

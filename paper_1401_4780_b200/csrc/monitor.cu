@@ -94,8 +94,14 @@ __device__ __forceinline__ double sell_dot(const int32_t* __restrict__ idx, cons
 template <class V, class X>
 __global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m, const X* __restrict__ x,
                                                           const double* __restrict__ b, double* out, double* part,
-                                                          const DevState* st) {
+                                                          const DevState* st, const X* __restrict__ x_alt = nullptr,
+                                                          const int* sel = nullptr) {
     if (st && st->stop) return;
+    if (sel) {  // decoupled snapshots: the slot the monitor stream claimed, or none
+        const int q = *sel;
+        if (q < 0) return;
+        if (q == 1) x = x_alt;
+    }
     __shared__ double red[kMonThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const long long i = (long long)blockIdx.x * kMonThreads + threadIdx.x;
@@ -181,10 +187,12 @@ __global__ void __launch_bounds__(kMonThreads) cols_kernel(CscDev C, long long n
 __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, double d_sq) {
     DevState* st = a.st;
     long long epoch, updates;
-    if (a.slot >= 0) {
-        if (!st->snap_valid[a.slot]) return;
-        epoch = st->snap_epoch[a.slot];
-        updates = st->snap_updates[a.slot];
+    const int slot = a.slot == kDynSlot ? st->mon_slot : a.slot;
+    if (a.slot == kDynSlot && slot < 0) return;  // nothing claimed: no record
+    if (slot >= 0) {
+        if (!st->snap_valid[slot]) return;
+        epoch = st->snap_epoch[slot];
+        updates = st->snap_updates[slot];
     } else {
         if (a.advance) {
             const long long sp = chunk_span(st);
@@ -213,12 +221,17 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
         st->nrec = k + 1;
         if (!st->stop && (r_sq <= st->target || epoch >= st->epochs_cap)) {
             st->stop = 1;
-            if (a.slot >= 0) {
-                st->stop_slot = a.slot;
+            if (slot >= 0) {
+                st->stop_slot = slot;
                 st->stop_epoch = epoch;
                 st->stop_updates = updates;
             }
         }
+    }
+    // a decoupled slot goes back to the snapshot kernel unless it decided the stop
+    if (a.slot == kDynSlot && !(st->stop && st->stop_slot == slot)) {
+        __threadfence();
+        atomicExch(&st->slot_state[slot], 0);
     }
     if (a.slot < 0) st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
     if (st->stop && a.host_flag) {
@@ -363,9 +376,10 @@ __device__ __forceinline__ void finalize_fast_block(const MonitorArgs& a, int nb
 template <class V, class X>
 __global__ void __launch_bounds__(kMonThreads) cols_final_kernel(MonitorArgs a, int nb_rows, int nb_cols) {
     const DevState* gate = a.force ? nullptr : a.st;
-    if (!(gate && gate->stop))
+    const int q = a.slot == kDynSlot ? a.st->mon_slot : 0;
+    if (!(gate && gate->stop) && q >= 0)
         cols_block<V, X>(a.csc, a.L.n, a.r, nullptr, a.part + nb_rows, a.part + nb_rows + nb_cols,
-                         static_cast<const X*>(a.x), a.x_star);
+                         static_cast<const X*>(q == 1 ? a.x_alt : a.x), a.x_star);
     __shared__ bool last;
     __threadfence();
     __syncthreads();
@@ -386,7 +400,10 @@ static void monitor_impl(const MonitorArgs& a, cudaStream_t s) {
     const int nbc = monitor_col_blocks(a.L.n);
     const X* x = static_cast<const X*>(a.x);
     const DevState* gate = a.force ? nullptr : a.st;  // the final record runs after stop
-    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, gate);
+    const bool dyn = a.slot == kDynSlot;
+    rows_kernel<V, X><<<nbr, kMonThreads, 0, s>>>(a.rows, a.L.m, x, a.b, a.r, a.exact ? nullptr : a.part, gate,
+                                                  dyn ? static_cast<const X*>(a.x_alt) : nullptr,
+                                                  dyn ? &a.st->mon_slot : nullptr);
     if (a.exact) {
         cols_kernel<V, X><<<nbc, kMonThreads, 0, s>>>(a.csc, a.L.n, a.r, a.g, nullptr, nullptr, x, a.x_star, gate);
         finalize_exact_kernel<<<1, 96, 0, s>>>(a);

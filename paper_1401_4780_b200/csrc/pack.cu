@@ -130,6 +130,9 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->snap_valid[0] = st->snap_valid[1] = 0;
     st->stop_slot = -1;
     st->snap_ticket = st->mon_ticket = 0;
+    st->slot_state[0] = st->slot_state[1] = 0;
+    st->snap_arrive = st->snap_seq = st->snap_decided = 0;
+    st->snap_target = st->mon_slot = -1;
     st->t0_ns = globaltimer_ns();
 }
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
@@ -299,6 +302,90 @@ __global__ void snapshot_kernel(DevState* st, const X* __restrict__ x, X* __rest
     }
     st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
 }
+
+// Decoupled snapshot (no back-pressure from the monitor): the first block to
+// arrive takes a free slot if there is one and publishes the choice; the
+// epoch is counted either way, and a skipped boundary gets no record — the
+// reference's coordinator likewise reports only the latest boundary it
+// catches (parallel.cpp:388-399).
+template <class X>
+__global__ void snapshot_dyn_kernel(DevState* st, const X* __restrict__ x, X* __restrict__ xs0, X* __restrict__ xs1,
+                                    long long n, long long m) {
+    __shared__ int target;
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        const unsigned seq = *reinterpret_cast<volatile unsigned*>(&st->snap_seq);
+        if (atomicAdd(&st->snap_arrive, 1u) == 0) {
+            int t = -1;
+            if (st->go && !st->stop)
+                for (int q = 0; q < 2 && t < 0; ++q)
+                    if (atomicCAS(&st->slot_state[q], 0, 1) == 0) t = q;
+            st->snap_target = t;
+            __threadfence();
+            atomicExch(&st->snap_decided, seq + 1u);
+        } else {
+            while (*reinterpret_cast<volatile unsigned*>(&st->snap_decided) != seq + 1u) __nanosleep(64);
+            __threadfence();
+        }
+        target = *reinterpret_cast<volatile int*>(&st->snap_target);
+    }
+    __syncthreads();
+    if (target >= 0) {
+        X* xs = target == 0 ? xs0 : xs1;
+        for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+             k += (long long)gridDim.x * blockDim.x)
+            xs[k] = __ldcg(x + k);
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->snap_ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    st->snap_ticket = 0;
+    st->snap_arrive = 0;
+    st->snap_seq += 1u;
+    if (st->go && !st->stop) {
+        const long long sp = chunk_span(st);
+        st->epoch += sp;
+        st->updates += sp * m;
+        if (target >= 0) {
+            st->snap_epoch[target] = st->epoch;
+            st->snap_updates[target] = st->updates;
+            st->snap_valid[target] = 1;
+            __threadfence();
+            atomicExch(&st->slot_state[target], 2);
+        }
+    } else if (target >= 0) {
+        atomicExch(&st->slot_state[target], 0);
+    }
+    st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
+}
+
+// monitor stream: claim the oldest filled snapshot (or none) for the passes that follow
+__global__ void claim_kernel(DevState* st) {
+    int best = -1;
+    long long be = 0;
+    for (int q = 0; q < 2; ++q)
+        if (atomicAdd(&st->slot_state[q], 0) == 2 && (best < 0 || st->snap_epoch[q] < be)) {
+            best = q;
+            be = st->snap_epoch[q];
+        }
+    if (best >= 0) atomicExch(&st->slot_state[best], 3);
+    st->mon_slot = st->stop ? -1 : best;
+}
+
+void launch_snapshot_dyn(DevState* st, const void* x, void* xs0, void* xs1, long long n, int precision, long long m,
+                         cudaStream_t s) {
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
+    if (precision == P_F32)
+        snapshot_dyn_kernel<float><<<blocks, 256, 0, s>>>(st, static_cast<const float*>(x), static_cast<float*>(xs0),
+                                                          static_cast<float*>(xs1), n, m);
+    else
+        snapshot_dyn_kernel<double><<<blocks, 256, 0, s>>>(st, static_cast<const double*>(x),
+                                                           static_cast<double*>(xs0), static_cast<double*>(xs1), n, m);
+}
+
+void launch_claim(DevState* st, cudaStream_t s) { claim_kernel<<<1, 1, 0, s>>>(st); }
 
 // end of an overlapped solve: return the snapshot that decided the stop
 template <class X>

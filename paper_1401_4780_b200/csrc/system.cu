@@ -628,6 +628,7 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.rows = s->rsell();
     a.b = s->b;
     a.slot = -1;
+    a.x_alt = nullptr;
     a.force = 0;
     return a;
 }
@@ -645,6 +646,49 @@ struct SolveSpec {
     int precision;
     bool det;               // deterministic sequence path
     int det_mode;           // SeqGen mode
+};
+
+// ASYRK_TIMELINE=path (diagnostics): timing events around the first chunks'
+// worker / snapshot / monitor launches on both streams, written as CSV
+// (kind, chunk, start_us, end_us relative to the solve's first event).
+struct Timeline {
+    struct Mark {
+        const char* kind;
+        long long k;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> marks;
+    bool on = false;
+    static constexpr long long kChunks = 24;
+    Mark* begin(const char* kind, long long k, cudaStream_t st) {
+        if (!on || k >= kChunks) return nullptr;
+        Mark m{kind, k, nullptr, nullptr};
+        cudaEventCreate(&m.a);
+        cudaEventCreate(&m.b);
+        cudaEventRecord(m.a, st);
+        marks.push_back(m);
+        return &marks.back();
+    }
+    void end(Mark* m, cudaStream_t st) {
+        if (m) cudaEventRecord(m->b, st);
+    }
+    void dump(const char* path, cudaEvent_t base) {
+        if (!on) return;
+        if (FILE* f = fopen(path, "w")) {
+            fprintf(f, "kind,chunk,start_us,end_us\n");
+            for (auto& m : marks) {
+                float a = 0.f, b = 0.f;
+                cudaEventElapsedTime(&a, base, m.a);
+                cudaEventElapsedTime(&b, base, m.b);
+                fprintf(f, "%s,%lld,%.2f,%.2f\n", m.kind, m.k, 1e3 * a, 1e3 * b);
+            }
+            fclose(f);
+        }
+        for (auto& m : marks) {
+            cudaEventDestroy(m.a);
+            cudaEventDestroy(m.b);
+        }
+    }
 };
 
 asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
@@ -764,6 +808,14 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     }
     if (overlap && !s->xs[0])  // (a recycled stream kit brings the stream and events, not the buffers)
         for (int q = 0; q < 2; ++q) s->xs[q] = dalloc<unsigned char>((size_t)s->n * s->xbytes());
+    // ASYRK_EXACT_RECORDS=1: a record at every boundary (the workers wait for the
+    // monitor); default: the monitor takes the latest boundary it can, like the
+    // reference's coordinator, and the workers never wait for it
+    static const bool exact_records = getenv("ASYRK_EXACT_RECORDS") != nullptr;
+    static const char* tl_path = getenv("ASYRK_TIMELINE");
+    Timeline tl;
+    tl.marks.reserve(4 * Timeline::kChunks);
+    tl.on = tl_path != nullptr;
     long long timed = 0;
     long long k = 0;
     for (; k < max_chunks; ++k) {
@@ -830,7 +882,9 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             }
         } else {
             if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
+            Timeline::Mark* tm = tl.begin("worker", k, st);
             launch_worker(wa, prec, E, st);
+            tl.end(tm, st);
         }
         if (time_it) {
             CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed + 1)], st));
@@ -844,16 +898,31 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             // workers already go (the reference's coordinator thread,
             // parallel.cpp:388-408, without its torn reads)
             const int slot2 = (int)(k & 1);
-            if (k >= 2) CK(cudaStreamWaitEvent(st, s->mon_ev[slot2], 0));  // slot free: monitor k-2 done
-            launch_snapshot(s->st, s->x, s->xs[slot2], s->n, prec, slot2, s->st, s->m, st);
+            Timeline::Mark* ts = tl.begin("snapshot", k, st);
+            if (exact_records) {  // every boundary recorded: slot reuse waits for monitor k-2
+                if (k >= 2) CK(cudaStreamWaitEvent(st, s->mon_ev[slot2], 0));
+                launch_snapshot(s->st, s->x, s->xs[slot2], s->n, prec, slot2, s->st, s->m, st);
+            } else {  // latest boundary the monitor can take (parallel.cpp:388-399)
+                launch_snapshot_dyn(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, s->m, st);
+            }
+            tl.end(ts, st);
             CK(cudaEventRecord(s->snap_ev[slot2], st));
             CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[slot2], 0));
             MonitorArgs ma = monitor_args(s, false, 0, sp.x_star != nullptr);
-            ma.x = s->xs[slot2];
-            ma.slot = slot2;
+            if (exact_records) {
+                ma.x = s->xs[slot2];
+                ma.slot = slot2;
+            } else {
+                launch_claim(s->st, s->mstream);
+                ma.x = s->xs[0];
+                ma.x_alt = s->xs[1];
+                ma.slot = kDynSlot;
+            }
+            Timeline::Mark* tmo = tl.begin("monitor", k, s->mstream);
             launch_monitor(ma, prec, s->mstream);
+            tl.end(tmo, s->mstream);
             CK(cudaEventRecord(s->mon_ev[slot2], s->mstream));
-            launches += 1 + mon_kernels;  // snapshot (+ fused advance) + monitor
+            launches += 1 + mon_kernels + (exact_records ? 0 : 1);  // snapshot (+ claim) + monitor
         } else {
             launch_monitor(monitor_args(s, sp.det, 1, sp.x_star != nullptr), prec, st);
             launches += mon_kernels;
@@ -880,6 +949,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     CK(cudaEventRecord(s->ev_end, st));
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
+    tl.dump(tl_path, s->ev_begin);
 
     DevState hs;
     CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
