@@ -519,7 +519,7 @@ def run_other(args):
     prec = {"cfg3": capi.F32, "cfg3x": capi.F32X64}.get(args.workload, capi.F64)
     S = capi.System(A, b, precision=prec)
     det = args.workload == "cfg1"
-    W = 1 if det else (args.warps or (3 * S.max_resident_warps()) // 4)
+    W = 1 if det else (args.warps or S.max_resident_warps())
     if det:
         run = lambda k: S.rk_solve(max_epochs=c["epochs"], target=target, seed=42 + k,  # noqa: E731
                                    sampling=capi.RK_UNIFORM, x_star=xs)
