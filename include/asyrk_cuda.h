@@ -117,6 +117,9 @@ typedef struct {
     /* --- device extensions (zero = reference behaviour) --- */
     int32_t precision;         /* ASYRK_F64 ... */
     int32_t allow_unnormalized; /* 1: async/norm_proportional on raw rows (config 4) */
+    int32_t record_every_boundary; /* async: 1 = a record at every snapshot boundary (the workers
+                                      wait for the residual monitor); 0 = the monitor records the
+                                      latest boundary it can, like the reference coordinator */
 } asyrk_run_config;
 
 /* RkConfig (kaczmarz.hpp:95-103) */

@@ -42,7 +42,7 @@ class RunConfig(C.Structure):
     _fields_ = [("threads", C.c_int64), ("gamma", C.c_double), ("epochs", C.c_int64), ("target_r_sq", C.c_double),
                 ("variant", C.c_int32), ("sampling", C.c_int32), ("seed", C.c_uint64),
                 ("snapshot_interval", C.c_int64), ("x_star", _f64p), ("precision", C.c_int32),
-                ("allow_unnormalized", C.c_int32)]
+                ("allow_unnormalized", C.c_int32), ("record_every_boundary", C.c_int32)]
 
 
 class RkConfig(C.Structure):
@@ -395,9 +395,9 @@ class _Trace:
 
 
 def _run_config(threads=1, gamma=1.0, epochs=100, target=0.0, variant=FULL_ROW, sampling=SLICE_SHUFFLE, seed=0,
-                snapshot_interval=1, x_star=None, precision=F64, allow_unnormalized=0):
+                snapshot_interval=1, x_star=None, precision=F64, allow_unnormalized=0, record_every_boundary=0):
     return RunConfig(threads, gamma, epochs, target, variant, sampling, seed, snapshot_interval,
-                     _ptr(x_star, _f64p), precision, allow_unnormalized)
+                     _ptr(x_star, _f64p), precision, allow_unnormalized, int(record_every_boundary))
 
 
 class System:

@@ -646,6 +646,7 @@ struct SolveSpec {
     int precision;
     bool det;               // deterministic sequence path
     int det_mode;           // SeqGen mode
+    bool every_boundary;    // async: record every boundary (run config record_every_boundary)
 };
 
 // ASYRK_TIMELINE=path (diagnostics): timing events around the first chunks'
@@ -808,10 +809,11 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     }
     if (overlap && !s->xs[0])  // (a recycled stream kit brings the stream and events, not the buffers)
         for (int q = 0; q < 2; ++q) s->xs[q] = dalloc<unsigned char>((size_t)s->n * s->xbytes());
-    // ASYRK_EXACT_RECORDS=1: a record at every boundary (the workers wait for the
-    // monitor); default: the monitor takes the latest boundary it can, like the
-    // reference's coordinator, and the workers never wait for it
-    static const bool exact_records = getenv("ASYRK_EXACT_RECORDS") != nullptr;
+    // record_every_boundary (or ASYRK_EXACT_RECORDS=1): a record at every boundary
+    // (the workers wait for the monitor); default: the monitor takes the latest
+    // boundary it can, like the reference's coordinator, and the workers never wait
+    static const bool exact_env = getenv("ASYRK_EXACT_RECORDS") != nullptr;
+    const bool exact_records = exact_env || sp.every_boundary;
     static const char* tl_path = getenv("ASYRK_TIMELINE");
     Timeline tl;
     tl.marks.reserve(4 * Timeline::kChunks);
@@ -1023,6 +1025,7 @@ asyrk_status system_solve_impl(asyrk_system* s, const double* x0, const asyrk_ru
     sp.precision = c->precision;
     sp.det = c->threads == 1;
     sp.det_mode = c->sampling == ASYRK_SLICE_SHUFFLE ? 2 : (c->sampling == ASYRK_NORM_PROPORTIONAL ? 1 : 0);
+    sp.every_boundary = c->record_every_boundary != 0;
     return run_solve(s, x0, sp, trace, instr);
 }
 

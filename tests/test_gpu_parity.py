@@ -265,3 +265,23 @@ def test_one_shot_host_entry_points(instances):
     t = capi.solve_parallel_host(A, inst["b"], threads=16, epochs=300, target=1e-20, seed=4,
                                  sampling=capi.WITH_REPLACEMENT)
     assert t["r_sq"][-1] <= 1e-20
+
+
+def test_record_modes_of_the_overlapped_monitor():
+    # default: the monitor records the latest boundary it can (the reference's
+    # coordinator, parallel.cpp:388-399) — records are a strictly increasing
+    # subset of the boundaries plus the final one; record_every_boundary: all
+    A, b, xs = capi.generate_fixed_theta(200000, 100000, 30, seed=1002)
+    S = capi.System(A, b)
+    bb = float(b @ b)
+    kw = dict(threads=S.max_resident_warps(), epochs=400, target=1e-12 * bb, sampling=capi.WITH_REPLACEMENT,
+              x_star=xs, want_x=False)
+    t = S.solve(seed=3, **kw)
+    ep = np.asarray(t["epoch_index"])
+    assert ep[0] == 0 and np.all(np.diff(ep) > 0) and t["r_sq"][-1] <= 1e-12 * bb
+    u = S.solve(seed=3, record_every_boundary=1, **kw)
+    eu = np.asarray(u["epoch_index"])
+    assert np.array_equal(eu, np.arange(len(eu))) and u["r_sq"][-1] <= 1e-12 * bb
+    for r in (t, u):
+        assert np.sqrt(r["dist_sq"][-1] / float(xs @ xs)) <= 1e-5
+    S.close()
