@@ -714,6 +714,58 @@ def run_mc(args):
     return 0
 
 
+def run_cfg5_shards(args):
+    """Config 5 per-rank work at G = 1, 2, 4, 8 on ONE GPU: the shard a rank of a
+    G-GPU job owns (k/G RHS columns) solved alone with its own stop test. A
+    projection of strong scaling, NOT a multi-GPU measurement: the G-GPU job
+    adds one all-reduce of 3 doubles per epoch (NCCL, not timed here) and its
+    stop is global."""
+    import torch
+
+    from paper_1401_4780_b200 import capi
+    from paper_1401_4780_b200.mrhs import CudaShardBackend, shard_columns, solve_sharded
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    A, B, Xs = capi.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"], k=CFG5["k"])
+    B = B.astype(np.float32)
+    W = args.warps or 4096
+    points = []
+    for G in [1, 2, 4, 8]:
+        c0, c1 = shard_columns(CFG5["k"], G, 0)
+        bb = float((B[:, c0:c1].astype(np.float64) ** 2).sum())
+        be = CudaShardBackend(A, B, c0, c1)
+        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1)
+        solve_sharded(be, seed=1, **kw)
+        times, epochs, rows = [], [], 0
+        for k in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            t = solve_sharded(be, seed=100 + k, **kw)
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            epochs.append(int(t["epoch_index"][-1]))
+            rows += int(t["updates_applied"][-1])
+        be.close()
+        ms = statistics.median(times)
+        points.append({"gpus": G, "columns_per_gpu": c1 - c0, "shard_time_to_tolerance_ms": ms,
+                       "epochs": statistics.median(epochs),
+                       "shard_column_proj_per_s": rows * (c1 - c0) / (sum(times) * 1e-3)})
+    t1 = points[0]["shard_time_to_tolerance_ms"]
+    for p in points:
+        p["projected_speedup_vs_1"] = t1 / p["shard_time_to_tolerance_ms"]
+    print(json.dumps({"metric": METRIC + " (config 5 per-rank shard, projection)", "unit": "ms", "n_gpus": 1,
+                      "data": "synthetic", "dtype": "f32", "steps": args.steps,
+                      "config": {"workload": "config5: m=500000 n=250000 theta=20 k=64 fp32; each point = the "
+                                             "k/G-column shard of one rank of a G-GPU job, solved alone on one "
+                                             "GPU with a shard-local stop at 1e-5 (the real job all-reduces 3 "
+                                             "doubles per epoch and stops globally)", "warps": W},
+                      "points": points}))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -722,7 +774,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = all resident warp slots)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc", "cfg1", "cfg3", "cfg3x", "cfg4",
-                                                           "sweep"])
+                                                           "sweep", "cfg5shards"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.workload == "mc":
@@ -731,6 +783,8 @@ def main():
         return run_other(args)
     if args.workload == "sweep":
         return run_sweep(args)
+    if args.workload == "cfg5shards":
+        return run_cfg5_shards(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg5":
