@@ -333,6 +333,22 @@ def check(status: int):
         raise AsyrkError(status, lib().asyrk_last_error().decode())
 
 
+def serial_row_sumsq(row_ptr, values):
+    """sum_k v_k^2 per row in storage order from 0.0 — the reference's cached
+    row norms are sqrt of exactly this (csr.cpp:53-61); np.add.reduceat sums in
+    a different order and can differ by an ulp, which changes every projection
+    coefficient gamma*res/(nrm*nrm). Vectorized across rows, serial within."""
+    lens = np.diff(row_ptr)
+    acc = np.zeros(len(lens))
+    sq = values * values
+    start = row_ptr[:-1]
+    live = np.arange(len(lens))
+    for k in range(int(lens.max()) if len(lens) else 0):
+        live = live[lens[live] > k]
+        acc[live] += sq[start[live] + k]
+    return acc
+
+
 class HostCsr:
     """Host CSR arrays in the reference's layout (int64 indices, fp64 values)."""
 
@@ -342,8 +358,7 @@ class HostCsr:
         self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
         self.values = np.ascontiguousarray(values, dtype=np.float64)
         if row_norm is None:
-            seg = np.add.reduceat(self.values * self.values, self.row_ptr[:-1]) if self.m else np.zeros(0)
-            row_norm = np.sqrt(seg)
+            row_norm = np.sqrt(serial_row_sumsq(self.row_ptr, self.values))
         self.row_norm = np.ascontiguousarray(row_norm, dtype=np.float64)
         if normalized is None:
             normalized = bool(np.all(np.abs(self.row_norm - 1.0) <= 1e-12))

@@ -162,3 +162,24 @@ def test_pybind_stats_and_simulate_signatures_match_reference():
     for fn, extra in [(pkg.system_stats, []), (pkg.step_params, ["tau"])]:
         for arg in ["m", "n", "rows", "cols", "vals"] + extra:
             assert f"{arg}:" in fn.__doc__
+
+
+def test_host_csr_row_norms_are_serial_sums():
+    # csr.cpp:53-61: the cached norm is sqrt of a storage-order serial sum; a
+    # pairwise sum differs in the last ulp for many rows and would change every
+    # projection coefficient of the deterministic path
+    import math
+
+    from paper_1401_4780_b200 import capi
+    rng = np.random.default_rng(4)
+    lens = rng.integers(1, 200, size=300)
+    rp = np.concatenate([[0], np.cumsum(lens)])
+    v = rng.standard_normal(rp[-1])
+    A = capi.HostCsr(300, 250, rp, np.zeros(rp[-1], np.int64), v)
+    want = []
+    for i in range(300):
+        s = 0.0
+        for k in range(rp[i], rp[i + 1]):
+            s += v[k] * v[k]
+        want.append(math.sqrt(s))
+    assert np.array_equal(A.row_norm, np.array(want))
