@@ -14,7 +14,7 @@
 
 namespace asyrk {
 
-class SolutionProjector;  // dense oracle of the reference (not on the device path)
+class SolutionProjector;  // dense oracle (asyrk/dense.hpp); its distance runs on the device as x_star = A^+ b
 
 inline constexpr index_t kAllComponents = -1;
 

@@ -192,7 +192,10 @@ asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double to
  * false: every field of SystemStats except lambda_min / sigma_r (dense SVD,
  * not on the device path). mu, nu, delta, alpha, frob_sq, l_max, l_res and
  * theta are bit-identical to the reference; lambda_max is the device power
- * iteration (tol, max_iters = StatsOptions::tol / max_power_iters).
+ * iteration (tol, max_iters = StatsOptions::tol / max_power_iters);
+ * max_iters < 0 skips it (lambda_max = 0), for exact_spectral callers that
+ * take lambda_max / lambda_min / sigma_r from asyrk_dense_spectrum
+ * (include/asyrk_dense.h).
  * Errors: NotNormalized (A not flagged normalized), ZeroColumn (first empty
  * column), PowerIterationDiverged. */
 typedef struct asyrk_stats_out {

@@ -229,6 +229,15 @@ class _RefLib(_Lib):
         L.ref_alias_sample_seq.argtypes = [_f64p, C_.c_int64, C_.c_uint64, C_.c_int64, _i64p]
         L.ref_rk_step.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_int64, _f64p]
         L.ref_asyrk_update.argtypes = [C_.c_void_p, _f64p, C_.c_int64, C_.c_int64, C_.c_double, _f64p, _f64p]
+        L.ref_gen_instance.restype = C_.c_void_p
+        L.ref_gen_instance.argtypes = [C_.c_int64, C_.c_int64, C_.c_double, C_.c_uint64, C_.c_int, C_.c_double,
+                                       _f64p, _f64p, C_.POINTER(C_.c_int), C_.POINTER(C_.c_int)]
+        L.ref_optimal_params.argtypes = [C_.c_double, _f64p, _f64p]
+        L.ref_critical_ratio.argtypes = [C_.c_double, C_.c_double, C_.c_int64, C_.c_double, C_.c_double, _f64p]
+        L.ref_augment.restype = C_.c_void_p
+        L.ref_augment.argtypes = [C_.c_void_p, _f64p, C_.c_double, C_.c_double, _f64p, _f64p, C_.POINTER(C_.c_int)]
+        L.ref_lsq_solve.argtypes = [C_.c_void_p, _f64p, C_.c_double, C_.c_double, C_.c_double, C_.c_int64,
+                                    C_.c_double, C_.c_uint64, C_.c_int, _f64p, _f64p, _f64p, C_.POINTER(_Trace)]
 
     def _check(self, st):
         if st:
@@ -251,6 +260,44 @@ class _RefLib(_Lib):
         h = self.L.ref_gen_sparse_gaussian(m, n, delta, seed, _p(b, _f64p), _p(xs, _f64p), C_.byref(st))
         self._check(st.value)
         return Csr(self, h, m, n), b, xs
+
+    def gen_instance(self, m, n, delta, seed, consistent=True, noise_level=0.0):
+        """gen_sparse_gaussian with the full GenSpec (datagen.cpp:13-137)."""
+        b, xs = np.zeros(m), np.zeros(n)
+        st, has = C_.c_int(0), C_.c_int(0)
+        h = self.L.ref_gen_instance(m, n, delta, seed, int(consistent), noise_level, _p(b, _f64p), _p(xs, _f64p),
+                                    C_.byref(has), C_.byref(st))
+        self._check(st.value)
+        return Csr(self, h, m, n), b, (xs if has.value else None)
+
+    # -- least squares (lsq.cpp:12-170)
+    def optimal_params(self, sigma_r):
+        phi, zeta = C_.c_double(), C_.c_double()
+        self._check(self.L.ref_optimal_params(sigma_r, C_.byref(phi), C_.byref(zeta)))
+        return phi.value, zeta.value
+
+    def critical_ratio(self, sigma_r, frob_sq, m, zeta, phi):
+        r = C_.c_double()
+        self._check(self.L.ref_critical_ratio(sigma_r, frob_sq, m, zeta, phi, C_.byref(r)))
+        return r.value
+
+    def augment(self, A, b, zeta, phi):
+        N = A.m + A.n
+        bt, rs = np.zeros(N), np.zeros(N)
+        st = C_.c_int(0)
+        h = self.L.ref_augment(A.handle, _p(_f64(b), _f64p), zeta, phi, _p(bt, _f64p), _p(rs, _f64p), C_.byref(st))
+        self._check(st.value)
+        return dict(a_tilde=Csr(self, h, N, N), b_tilde=bt, row_scales=rs)
+
+    def lsq_solve(self, A, b, sigma_r, zeta=0.0, phi=0.0, max_epochs=5000, target=0.0, seed=0, sampling="uniform",
+                  cap=100000):
+        s = {"uniform": 0, "norm": 1, "norm_proportional": 1, "shuffle": 2}[sampling]
+        x_ls, y, scal = np.zeros(A.n), np.zeros(A.m), np.zeros(4)
+        t, bufs = self._trace(A.n + A.m, min(cap, max_epochs + 2))
+        self._check(self.L.ref_lsq_solve(A.handle, _p(_f64(b), _f64p), zeta, phi, sigma_r, max_epochs, target, seed,
+                                         s, _p(x_ls, _f64p), _p(y, _f64p), _p(scal, _f64p), C_.byref(t)))
+        return dict(x_ls=x_ls, y=y, grad_norm=scal[0], zeta=scal[1], phi=scal[2], sigma_r=scal[3],
+                    trace=self._trace_dict(t, bufs, False))
 
     def _export(self, A):
         nnz = self.L.ref_csr_nnz(A.handle)

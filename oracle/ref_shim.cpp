@@ -12,6 +12,7 @@
 //   AliasTable, make_stream/uniform_below      (ref/src/kaczmarz.cpp:14-61, rng.hpp)
 //   simulate / monte_carlo_ratios / rate_fit   (ref/src/delay_sim.cpp:71-338)
 //   Matrix Market / vector / instance I/O      (ref/src/io.cpp:41-183)
+//   augment / lsq_solve / optimal_params       (ref/src/lsq.cpp:12-170)
 // Nothing here is shipped; the product never links this library.
 #include <cstdint>
 #include <cstring>
@@ -24,6 +25,7 @@
 #include "asyrk/io.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk/kaczmarz.hpp"
+#include "asyrk/lsq.hpp"
 #include "asyrk/parallel.hpp"
 #include "asyrk/rng.hpp"
 #include "asyrk/stats.hpp"
@@ -485,6 +487,78 @@ void* ref_read_instance(const char* dir, double* b_out, int64_t b_cap, double* x
         h = new Handle{std::move(inst.A)};
     });
     return h;
+}
+
+}  // extern "C"
+
+// ---- least squares (ref/src/lsq.cpp:12-170) and general instances
+extern "C" {
+
+// gen_sparse_gaussian with the full GenSpec (datagen.hpp:11-18): consistent
+// or noisy b; x* written only when present (*has_xs).
+void* ref_gen_instance(int64_t m, int64_t n, double delta, uint64_t seed, int consistent, double noise,
+                       double* b_out, double* xstar_out, int* has_xs, int* status) {
+    Handle* h = nullptr;
+    *status = guarded([&] {
+        Instance inst = gen_sparse_gaussian({m, n, delta, seed, consistent != 0, noise});
+        std::memcpy(b_out, inst.b.data(), inst.b.size() * 8);
+        *has_xs = inst.x_star ? 1 : 0;
+        if (inst.x_star && xstar_out) std::memcpy(xstar_out, inst.x_star->data(), inst.x_star->size() * 8);
+        h = new Handle{std::move(inst.A)};
+    });
+    return h;
+}
+
+int ref_optimal_params(double sigma_r, double* phi, double* zeta) {
+    return guarded([&] {
+        auto p = optimal_params(sigma_r);
+        *phi = p.first;
+        *zeta = p.second;
+    });
+}
+
+int ref_critical_ratio(double sigma_r, double frob_sq, int64_t m, double zeta, double phi, double* out) {
+    return guarded([&] { *out = critical_ratio(sigma_r, frob_sq, m, zeta, phi); });
+}
+
+// augment: returns a_tilde as a handle; b_tilde / row_scales (n+m entries)
+void* ref_augment(void* hp, const double* b, double zeta, double phi, double* b_tilde, double* row_scales,
+                  int* status) {
+    Handle* h = nullptr;
+    *status = guarded([&] {
+        const CsrMatrix& A = static_cast<Handle*>(hp)->A;
+        AugmentedSystem aug = augment(A, std::span<const double>(b, (size_t)A.rows()), zeta, phi);
+        std::memcpy(b_tilde, aug.b_tilde.data(), aug.b_tilde.size() * 8);
+        std::memcpy(row_scales, aug.row_scales.data(), aug.row_scales.size() * 8);
+        h = new Handle{std::move(aug.a_tilde)};
+    });
+    return h;
+}
+
+// lsq_solve with a supplied sigma_r (> 0; <= 0 leaves it unset, which needs
+// the dense SVD the stub refuses). scal <- {grad_norm, zeta, phi, sigma_r}.
+int ref_lsq_solve(void* hp, const double* b, double zeta, double phi, double sigma_r, int64_t max_epochs,
+                  double target, uint64_t seed, int sampling, double* x_ls, double* y, double* scal, ref_trace* tr) {
+    return guarded([&] {
+        const CsrMatrix& A = static_cast<Handle*>(hp)->A;
+        LsqConfig cfg;
+        cfg.zeta = zeta;
+        cfg.phi = phi;
+        if (sigma_r > 0.0) cfg.sigma_r = sigma_r;
+        cfg.max_epochs = max_epochs;
+        cfg.target_r_sq = target;
+        cfg.seed = seed;
+        cfg.sampling = sampling == 1 ? Sampling::norm_proportional : sampling == 2 ? Sampling::shuffle
+                                                                                   : Sampling::uniform;
+        LsqResult r = lsq_solve(A, std::span<const double>(b, (size_t)A.rows()), cfg);
+        std::memcpy(x_ls, r.x_ls.data(), r.x_ls.size() * 8);
+        if (y) std::memcpy(y, r.y.data(), r.y.size() * 8);
+        scal[0] = r.grad_norm;
+        scal[1] = r.zeta;
+        scal[2] = r.phi;
+        scal[3] = r.sigma_r;
+        if (tr) dump_trace(r.trace, tr);
+    });
 }
 
 }  // extern "C"

@@ -12,14 +12,18 @@ hot path:
   epochs=100, target=0.0, seed=0, variant="full-row")`` — ``threads``
   concurrent warp-workers (``threads == 1``: the deterministic worker).
 * ``system_stats(m, n, rows, cols, vals)``, ``step_params(..., tau)`` —
-  device compute_stats (power-iteration lambda_max; no dense-SVD fields).
+  device compute_stats with the dense spectrum (lambda_max, lambda_min,
+  sigma_r) from the device one-sided Jacobi SVD.
+* ``lsq(m, n, rows, cols, vals, b, epochs=5000, target=0.0, seed=0)`` —
+  least squares through the augmented system, solved on the device.
 * ``simulate(m, n, rows, cols, vals, b, iterations, tau, gamma,
   delay="uniform", variant="single", seed=0)`` — the bounded-delay replay on
   the device, bit-identical to the reference's ``simulate``.
 
 Device extensions: ``solve_parallel_device`` (sampling / precision /
 snapshot interval / x_star), ``lambda_max``, ``residuals``,
-``max_feasible_tau``; and :mod:`paper_1401_4780_b200.capi` for the C ABI
+``max_feasible_tau``, ``dense_spectrum``, ``lsq(..., sigma_r=, threads=,
+gamma=)``; and :mod:`paper_1401_4780_b200.capi` for the C ABI
 (device-resident systems, timing). Errors surface as
 ``ValueError("<ErrorCodeName>: message")`` like the reference.
 
@@ -48,6 +52,8 @@ max_feasible_tau = _asyrk.max_feasible_tau
 system_stats = _asyrk.system_stats
 step_params = _asyrk.step_params
 simulate = _asyrk.simulate
+lsq = _asyrk.lsq
+dense_spectrum = _asyrk.dense_spectrum
 
 __all__ = [
     "solve_rk",
@@ -55,7 +61,9 @@ __all__ = [
     "system_stats",
     "step_params",
     "simulate",
+    "lsq",
     "solve_parallel_device",
+    "dense_spectrum",
     "lambda_max",
     "residuals",
     "max_feasible_tau",

@@ -141,6 +141,28 @@ class InstanceMeta(C.Structure):
                 ("consistent", C.c_int32), ("noise_level", C.c_double), ("has_x_star", C.c_int32)]
 
 
+class Spectrum(C.Structure):
+    """asyrk_spectrum (include/asyrk_dense.h; Spectrum, ref dense.hpp:15-20)."""
+
+    _fields_ = [("lambda_max", C.c_double), ("lambda_min", C.c_double), ("sigma_r", C.c_double),
+                ("rank", C.c_int32)]
+
+
+class LsqConfig(C.Structure):
+    """asyrk_lsq_config (include/asyrk_dense.h; LsqConfig, ref lsq.hpp:40-50 + device solver choice)."""
+
+    _fields_ = [("zeta", C.c_double), ("phi", C.c_double), ("has_sigma_r", C.c_int32), ("sigma_r", C.c_double),
+                ("max_epochs", C.c_int64), ("target_r_sq", C.c_double), ("seed", C.c_uint64),
+                ("sampling", C.c_int32), ("threads", C.c_int64), ("gamma", C.c_double)]
+
+
+class LsqOut(C.Structure):
+    """asyrk_lsq_out (include/asyrk_dense.h; LsqResult, ref lsq.hpp:52-60)."""
+
+    _fields_ = [("x_ls", _f64p), ("y", _f64p), ("grad_norm", C.c_double), ("zeta", C.c_double),
+                ("phi", C.c_double), ("sigma_r", C.c_double), ("trace", TraceOut)]
+
+
 class AsyrkError(ValueError):
     def __init__(self, status: int, msg: str):
         self.status = status
@@ -198,6 +220,15 @@ def lib():
         L.asyrk_write_instance.argtypes = [C.c_char_p, C.POINTER(CsrView), _f64p, _f64p, C.POINTER(InstanceMeta)]
         L.asyrk_read_instance.argtypes = [C.c_char_p, C.POINTER(sp), C.POINTER(_f64p), C.POINTER(_f64p),
                                           C.POINTER(InstanceMeta)]
+        L.asyrk_dense_svd.argtypes = [C.POINTER(CsrView), C.c_int64, _f64p, _f64p, _f64p, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_int32)]
+        L.asyrk_dense_spectrum.argtypes = [C.POINTER(CsrView), C.POINTER(Spectrum)]
+        L.asyrk_dense_lstsq.argtypes = [C.POINTER(CsrView), _f64p, _f64p]
+        L.asyrk_lsq_optimal_params.argtypes = [C.c_double, _f64p, _f64p]
+        L.asyrk_lsq_critical_ratio.argtypes = [C.c_double, C.c_double, C.c_int64, C.c_double, C.c_double, _f64p]
+        L.asyrk_lsq_augment.argtypes = [C.POINTER(CsrView), _f64p, C.c_double, C.c_double, C.POINTER(sp), _f64p,
+                                        _f64p]
+        L.asyrk_lsq_solve.argtypes = [C.POINTER(CsrView), _f64p, C.POINTER(LsqConfig), C.POINTER(LsqOut)]
         L.asyrk_solve_parallel.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RunConfig),
                                            C.POINTER(TraceOut), C.POINTER(InstrumentOut)]
         L.asyrk_rk_solve.argtypes = [C.POINTER(CsrView), _f64p, _f64p, C.POINTER(RkConfig), C.POINTER(TraceOut)]
@@ -239,7 +270,8 @@ EXPORTED = [
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
     "asyrk_read_matrix_market", "asyrk_write_matrix_market", "asyrk_read_csr_cache", "asyrk_write_csr_cache",
     "asyrk_host_csr_copy", "asyrk_host_csr_free", "asyrk_host_csr_get_info", "asyrk_read_vector", "asyrk_write_vector", "asyrk_free",
-    "asyrk_write_instance", "asyrk_read_instance",
+    "asyrk_write_instance", "asyrk_read_instance", "asyrk_dense_svd", "asyrk_dense_spectrum", "asyrk_dense_lstsq",
+    "asyrk_lsq_optimal_params", "asyrk_lsq_critical_ratio", "asyrk_lsq_augment", "asyrk_lsq_solve",
 ]
 
 
@@ -578,6 +610,90 @@ def rate_fit(y, stride=1.0):
     sl, r2 = C.c_double(), C.c_double()
     check(lib().asyrk_rate_fit(_ptr(y, _f64p), len(y), stride, C.byref(sl), C.byref(r2)))
     return dict(slope=sl.value, r2=r2.value)
+
+
+# ---- dense spectrum and least squares (include/asyrk_dense.h; ref dense.hpp, lsq.hpp)
+DENSE_CAP_DEFAULT = 4000000     # SolutionProjector::kDefaultDenseCap
+DENSE_DEVICE_CAP = 67108864
+
+
+def dense_svd(A: "HostCsr", vectors=False, max_cells=0):
+    """Thin SVD of A on the device (one-sided Jacobi; replaces ref dense.cpp:27-50).
+    Returns dict(sigma (descending), rank, sweeps[, U (m x k), V (n x k)])."""
+    k = min(A.m, A.n)
+    sigma = np.zeros(k)
+    U = np.zeros((k, A.m)) if vectors else None   # column-major m x k == row-major k x m
+    V = np.zeros((k, A.n)) if vectors else None
+    rank, sweeps = C.c_int32(), C.c_int32()
+    check(lib().asyrk_dense_svd(C.byref(A.view()), max_cells, _ptr(sigma, _f64p), _ptr(U, _f64p), _ptr(V, _f64p),
+                                C.byref(rank), C.byref(sweeps)))
+    d = dict(sigma=sigma, rank=rank.value, sweeps=sweeps.value)
+    if vectors:
+        d["U"], d["V"] = U.T.copy(), V.T.copy()
+    return d
+
+
+def dense_spectrum(A: "HostCsr"):
+    """dense_spectrum (ref dense.cpp:62-64): lambda_max, lambda_min, sigma_r, rank."""
+    o = Spectrum()
+    check(lib().asyrk_dense_spectrum(C.byref(A.view()), C.byref(o)))
+    return {f: getattr(o, f) for f, _ in Spectrum._fields_}
+
+
+def dense_lstsq(A: "HostCsr", b):
+    """dense_min_norm_lstsq (ref dense.cpp:110-117): A^+ b from the device SVD."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    x = np.zeros(A.n)
+    check(lib().asyrk_dense_lstsq(C.byref(A.view()), _ptr(b, _f64p), _ptr(x, _f64p)))
+    return x
+
+
+def lsq_optimal_params(sigma_r):
+    """optimal_params (ref lsq.cpp:12-18) -> (phi, zeta)."""
+    phi, zeta = C.c_double(), C.c_double()
+    check(lib().asyrk_lsq_optimal_params(sigma_r, C.byref(phi), C.byref(zeta)))
+    return phi.value, zeta.value
+
+
+def lsq_critical_ratio(sigma_r, frob_sq, m, zeta, phi):
+    """critical_ratio (ref lsq.cpp:20-34)."""
+    r = C.c_double()
+    check(lib().asyrk_lsq_critical_ratio(sigma_r, frob_sq, m, zeta, phi, C.byref(r)))
+    return r.value
+
+
+def lsq_augment(A: "HostCsr", b, zeta, phi):
+    """augment (ref lsq.cpp:36-101) -> dict(a_tilde HostCsr, b_tilde, row_scales, zeta, phi)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if len(b) != A.m:  # (the C ABI takes m entries by pointer)
+        raise AsyrkError(6, "augment: b size mismatch")
+    N = A.m + A.n
+    bt, rs = np.zeros(N), np.zeros(N)
+    h = C.c_void_p()
+    check(lib().asyrk_lsq_augment(C.byref(A.view()), _ptr(b, _f64p), zeta, phi, C.byref(h), _ptr(bt, _f64p),
+                                  _ptr(rs, _f64p)))
+    info = HostCsrInfo()
+    check(lib().asyrk_host_csr_get_info(h, C.byref(info)))
+    return dict(a_tilde=_take_host_csr(h, info), b_tilde=bt, row_scales=rs, zeta=zeta, phi=phi)
+
+
+def lsq_solve(A: "HostCsr", b, zeta=0.0, phi=0.0, sigma_r=None, max_epochs=5000, target=0.0, seed=0,
+              sampling=RK_UNIFORM, threads=1, gamma=1.0, cap=None):
+    """lsq_solve (ref lsq.cpp:103-170): min ||Ax - b|| through the augmented
+    system, solved by the device rk_solve (threads <= 1) or the async warp
+    workers (threads > 1). Returns dict(x_ls, y, grad_norm, zeta, phi, sigma_r, trace)."""
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if len(b) != A.m:
+        raise AsyrkError(6, "lsq_solve: b size mismatch")
+    c = LsqConfig(zeta, phi, 1 if sigma_r is not None else 0, sigma_r or 0.0, max_epochs, target, seed, sampling,
+                  threads, gamma)
+    x_ls, y = np.zeros(A.n), np.zeros(A.m)
+    tr = _Trace(A.n + A.m, cap or (max_epochs + 2))
+    o = LsqOut(_ptr(x_ls, _f64p), _ptr(y, _f64p), 0.0, 0.0, 0.0, 0.0, tr.out)
+    check(lib().asyrk_lsq_solve(C.byref(A.view()), _ptr(b, _f64p), C.byref(c), C.byref(o)))
+    tr.out.count = o.trace.count
+    return dict(x_ls=x_ls, y=y, grad_norm=o.grad_norm, zeta=o.zeta, phi=o.phi, sigma_r=o.sigma_r,
+                trace=tr.result(False))
 
 
 # ---- instance I/O (include/asyrk_io.h; ref io.hpp:12-33)

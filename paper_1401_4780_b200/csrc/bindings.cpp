@@ -2,9 +2,9 @@
 // (ref/bindings/module.cpp:281-318: solve_rk, solve_parallel, system_stats,
 // step_params, simulate): dict in / dict out, triplets -> CSR ->
 // normalize_rows inside, errors as ValueError("<ErrorCodeName>: message")
-// (module.cpp:271-279). Statistics use the device compute_stats with
-// power-iteration lambda_max (exact_spectral = false): lambda_min / sigma_r
-// and the rate fields that need them are absent from the dicts.
+// (module.cpp:271-279). Statistics use the device compute_stats with the
+// dense spectrum from the device Jacobi SVD (exact_spectral, the reference
+// default) up to ASYRK_DENSE_DEVICE_CAP cells, power iteration beyond.
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
@@ -13,6 +13,9 @@
 #include <vector>
 
 #include "asyrk/delay_sim.hpp"
+#include "asyrk/dense.hpp"
+#include "asyrk/lsq.hpp"
+#include "asyrk_dense.h"
 #include "asyrk/error.hpp"
 #include "asyrk/kaczmarz.hpp"
 #include "asyrk/parallel.hpp"
@@ -137,9 +140,13 @@ py::dict solve_parallel_core(index_t m, index_t n, const std::vector<index_t>& r
     return d;
 }
 
+// compute_stats(N) with the reference default exact_spectral = true: the
+// dense spectrum is the device Jacobi SVD (csrc/dense.cu). Past the device
+// SVD cap the power-iteration lambda_max stands in (lambda_min / sigma_r
+// then absent), where the reference would attempt a dense SVD it cannot hold.
 SystemStats device_stats(const CsrMatrix& N) {
     StatsOptions o;
-    o.exact_spectral = false;  // the dense SVD is not on the device path
+    o.exact_spectral = static_cast<double>(N.rows()) * static_cast<double>(N.cols()) <= ASYRK_DENSE_DEVICE_CAP;
     return compute_stats(N, o);
 }
 
@@ -227,6 +234,35 @@ py::dict simulate_py(index_t m, index_t n, const std::vector<index_t>& rows, con
     return d;
 }
 
+// module.cpp:227-246: triplets -> normalize_rows(A0, b) -> lsq_solve with the
+// derived (phi, zeta); the augmented solve runs on the device
+py::dict lsq_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+                const std::vector<double>& vals, const std::vector<double>& b, index_t epochs, double target,
+                std::uint64_t seed, std::optional<double> sigma_r, index_t threads, double gamma) {
+    CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
+    auto [A, bn] = normalize_rows(A0, b);
+    LsqConfig cfg;
+    cfg.max_epochs = epochs;
+    cfg.target_r_sq = target;
+    cfg.seed = seed;
+    cfg.sigma_r = sigma_r;
+    cfg.threads = threads;
+    cfg.gamma = gamma;
+    LsqResult res;
+    {
+        py::gil_scoped_release nogil;
+        res = lsq_solve(A, bn, cfg);
+    }
+    py::dict d;
+    d["x_ls"] = res.x_ls;
+    d["grad_norm"] = res.grad_norm;
+    d["zeta"] = res.zeta;
+    d["phi"] = res.phi;
+    d["sigma_r"] = res.sigma_r;
+    d["trace"] = to_dict(res.trace);
+    return d;
+}
+
 }  // namespace
 
 PYBIND11_MODULE(_asyrk, mod) {
@@ -278,7 +314,7 @@ PYBIND11_MODULE(_asyrk, mod) {
     mod.def("system_stats", &system_stats_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"),
             py::arg("vals"),
             "Structural and spectral statistics (rows normalized first; device compute_stats, "
-            "power-iteration lambda_max).");
+            "dense spectrum from the device Jacobi SVD).");
     mod.def("step_params", &step_params_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"),
             py::arg("vals"), py::arg("tau"), "Staleness-aware step size and rate bounds for delay bound tau.");
     mod.def("simulate", &simulate_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"),
@@ -286,6 +322,26 @@ PYBIND11_MODULE(_asyrk, mod) {
             py::arg("variant") = "single", py::arg("seed") = 0,
             "Deterministic bounded-delay simulation of the asynchronous update recursion (device replay, "
             "bit-identical to the reference).");
+    mod.def("lsq", &lsq_py, py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"),
+            py::arg("b"), py::arg("epochs") = 5000, py::arg("target") = 0.0, py::arg("seed") = 0,
+            py::arg("sigma_r") = py::none(), py::arg("threads") = 1, py::arg("gamma") = 1.0,
+            "Least squares through the square augmented encoding with the optimal coupling parameters "
+            "(device rk_solve; threads > 1: async warp workers; sigma_r skips the dense SVD).");
+    mod.def(
+        "dense_spectrum",
+        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
+           const std::vector<double>& vals) {
+            CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
+            Spectrum sp;
+            {
+                py::gil_scoped_release nogil;
+                sp = dense_spectrum(A);
+            }
+            return py::dict(py::arg("lambda_max") = sp.lambda_max, py::arg("lambda_min") = sp.lambda_min,
+                            py::arg("sigma_r") = sp.sigma_r, py::arg("rank") = sp.rank);
+        },
+        py::arg("m"), py::arg("n"), py::arg("rows"), py::arg("cols"), py::arg("vals"),
+        "Dense spectrum of the raw matrix (device one-sided Jacobi SVD; ref dense_spectrum).");
     mod.def(
         "lambda_max",
         [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,

@@ -4,8 +4,14 @@
 
 #include <vector>
 
+#include "asyrk/csr.hpp"
 #include "asyrk/trace.hpp"
 #include "asyrk_cuda.h"
+
+// opaque host CSR handle of the C ABI (include/asyrk_io.h)
+struct asyrk_host_csr {
+    asyrk::CsrMatrix A;
+};
 
 namespace asyrk {
 

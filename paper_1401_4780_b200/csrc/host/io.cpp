@@ -26,6 +26,7 @@
 #include "../capi_common.h"
 #include "asyrk/error.hpp"
 #include "asyrk_io.h"
+#include "common.hpp"
 #include "json.hpp"
 
 namespace asyrk {
@@ -567,10 +568,6 @@ CsrMatrix read_csr_cache(const std::string& path) {
 }  // namespace asyrk
 
 // ---- C ABI (include/asyrk_io.h) ------------------------------------------
-struct asyrk_host_csr {
-    asyrk::CsrMatrix A;
-};
-
 namespace {
 
 template <class F>

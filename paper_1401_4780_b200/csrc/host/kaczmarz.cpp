@@ -2,6 +2,7 @@
 // (kaczmarz.cpp:14-61): the solve runs on the device's deterministic worker.
 #include "asyrk/kaczmarz.hpp"
 
+#include "asyrk/dense.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk_cuda.h"
 #include "common.hpp"
@@ -64,8 +65,8 @@ Trace rk_solve(const CsrMatrix& A, std::span<const double> b, std::span<const do
         fail(ErrorCode::NotNormalized,
              "uniform row sampling is only unbiased on normalized rows; use norm_proportional or normalize first");
     if (cfg.max_epochs < 0) fail(ErrorCode::InvalidArgument, "max_epochs must be >= 0");
-    if (cfg.projector && !cfg.x_star)
-        fail(ErrorCode::TooLarge, "the dense SolutionProjector oracle is not available on the device path");
+    const std::vector<double>* xs =
+        cfg.x_star ? cfg.x_star : (cfg.projector ? &projector_point(*cfg.projector, n) : nullptr);
 
     json::Object c;
     c["solver"] = "rk";
@@ -75,7 +76,7 @@ Trace rk_solve(const CsrMatrix& A, std::span<const double> b, std::span<const do
     c["target_r_sq"] = cfg.target_r_sq;
     c["seed"] = cfg.seed;
     c["sampling"] = sampling_label(cfg.sampling);
-    c["dist_oracle"] = cfg.x_star ? "x_star" : "none";
+    c["dist_oracle"] = cfg.x_star ? "x_star" : (cfg.projector ? "projector" : "none");
     c["device"] = "sm_100a";
 
     asyrk_system* sys = A.device(0);
@@ -87,10 +88,10 @@ Trace rk_solve(const CsrMatrix& A, std::span<const double> b, std::span<const do
     rc.sampling = cfg.sampling == Sampling::uniform ? ASYRK_RK_UNIFORM
                   : cfg.sampling == Sampling::norm_proportional ? ASYRK_RK_NORM_PROPORTIONAL
                                                                  : ASYRK_RK_SHUFFLE;
-    rc.x_star = cfg.x_star ? cfg.x_star->data() : nullptr;
+    rc.x_star = xs ? xs->data() : nullptr;
     TraceBuffers tb(n, cfg.max_epochs + 1);
     throw_status(asyrk_system_rk_solve(sys, x0.data(), &rc, &tb.out));
-    Trace t = tb.to_trace(cfg.x_star != nullptr);
+    Trace t = tb.to_trace(xs != nullptr);
     t.config_echo = json::dump(json::Value(std::move(c)));
     return t;
 }

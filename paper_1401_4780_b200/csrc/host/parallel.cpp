@@ -5,6 +5,7 @@
 
 #include <algorithm>
 
+#include "asyrk/dense.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk_cuda.h"
 #include "common.hpp"
@@ -30,7 +31,7 @@ std::string run_config_json(const RunConfig& cfg, index_t m, index_t n, const De
     c["seed"] = cfg.seed;
     c["snapshot_interval"] = cfg.snapshot_interval;
     c["epoch_updates"] = m;
-    c["dist_oracle"] = cfg.x_star ? "x_star" : "none";
+    c["dist_oracle"] = cfg.x_star ? "x_star" : (cfg.projector ? "projector" : "none");
     c["device"] = "sm_100a";
     c["worker"] = cfg.threads == 1 ? "deterministic" : "warp";
     c["precision"] = dev.precision == 0 ? "fp64" : dev.precision == 1 ? "fp32" : "fp32_values_fp64_x";
@@ -67,17 +68,18 @@ Trace solve_parallel(const CsrMatrix& A, std::span<const double> b, std::span<co
                      const RunConfig& cfg, InstrumentReport* instrument, const DeviceOptions& dev) {
     if (static_cast<index_t>(b.size()) != A.rows() || static_cast<index_t>(x0.size()) != A.cols())
         fail(ErrorCode::DimensionMismatch, "solve_parallel: b or x0 size mismatch");
-    if (cfg.projector && !cfg.x_star)
-        fail(ErrorCode::TooLarge, "the dense SolutionProjector oracle is not available on the device path");
+    // a projector's distance is ||x - A^+ b||^2 on the device (full column rank)
+    RunConfig dc = cfg;
+    if (!dc.x_star && dc.projector) dc.x_star = &projector_point(*cfg.projector, A.cols());
     const int prec = cfg.threads == 1 ? 0 : dev.precision;
     asyrk_system* sys = A.device(prec);
     throw_status(asyrk_system_set_rhs(sys, b.data()));
-    const asyrk_run_config c = to_c(cfg, dev);
+    const asyrk_run_config c = to_c(dc, dev);
     const index_t interval = std::max<index_t>(cfg.snapshot_interval, 1);
     TraceBuffers tb(A.cols(), std::max<index_t>(cfg.epochs, 0) / interval + 2);
     asyrk_instrument_out rep{};
     throw_status(asyrk_system_solve(sys, x0.data(), &c, &tb.out, instrument ? &rep : nullptr));
-    Trace t = tb.to_trace(cfg.x_star != nullptr);
+    Trace t = tb.to_trace(dc.x_star != nullptr);
     t.config_echo = run_config_json(cfg, A.rows(), A.cols(), dev);
     if (instrument) {
         instrument->row_updates = rep.row_updates;

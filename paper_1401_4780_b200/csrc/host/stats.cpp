@@ -5,6 +5,7 @@
 #include <cmath>
 #include <numbers>
 
+#include "asyrk/dense.hpp"
 #include "asyrk/error.hpp"
 #include "asyrk/stepsize.hpp"
 #include "asyrk_cuda.h"
@@ -22,25 +23,28 @@ double power_iteration_lambda_max(const CsrMatrix& A, double tol, index_t max_it
 SystemStats compute_stats(const CsrMatrix& A, const StatsOptions& opts) {
     if (!A.is_normalized())
         fail(ErrorCode::NotNormalized, "stats are defined for row-normalized matrices; call normalize_rows first");
-    if (opts.exact_spectral)
-        fail(ErrorCode::TooLarge,
-             "exact_spectral needs a dense SVD (ref dense.cpp), which is not on the device path; "
-             "set StatsOptions::exact_spectral = false for the power-iteration lambda_max");
     SystemStats s;
     s.theta.resize(static_cast<std::size_t>(A.rows()));
     asyrk_stats_out o{};
     o.theta = s.theta.data();
-    throw_status(asyrk_system_compute_stats(A.device(0), opts.tol, opts.max_power_iters, &o));
+    throw_status(asyrk_system_compute_stats(A.device(0), opts.tol, opts.exact_spectral ? -1 : opts.max_power_iters, &o));
     s.m = o.m;
     s.n = o.n;
     s.delta = o.delta;
     s.mu = o.mu;
     s.nu = o.nu;
     s.alpha = o.alpha;
-    s.lambda_max = o.lambda_max;
     s.frob_sq = o.frob_sq;
     s.l_max = o.l_max;
     s.l_res = o.l_res;
+    if (opts.exact_spectral) {  // stats.cpp:136-140, dense spectrum from the device Jacobi SVD
+        const Spectrum sp = dense_spectrum(A);
+        s.lambda_max = sp.lambda_max;
+        s.lambda_min = sp.lambda_min;
+        s.sigma_r = sp.sigma_r;
+    } else {
+        s.lambda_max = o.lambda_max;
+    }
     return s;
 }
 
@@ -139,12 +143,35 @@ StepParams corollary_params(const SystemStats& s, index_t tau) {
         p.gamma_bounds = gamma_bounds(s, tau, p.rho);
         p.gamma = 1.0 / p.psi;
         if (s.lambda_min) {
-            if (!(p.gamma < 2.0 / p.psi)) fail(ErrorCode::StepTooLarge, "gamma must stay below 2/psi");
-            p.rate_iter = 1.0 - *s.lambda_min * p.gamma * (2.0 - p.gamma * p.psi) / m;
+            p.rate_iter = rate_iteration(s, p.gamma, p.psi).per_iteration;
             p.rate_simplified = 1.0 - *s.lambda_min / (m * (static_cast<double>(s.mu) + 1.0));
         }
     }
     return p;
+}
+
+RateIteration rate_iteration(const SystemStats& s, double gamma, double psi_value) {
+    if (!(gamma > 0.0)) fail(ErrorCode::InvalidGamma, "gamma must be positive");
+    if (!(gamma < 2.0 / psi_value)) fail(ErrorCode::StepTooLarge, "gamma must stay below 2/psi for guaranteed progress");
+    if (!s.lambda_min) fail(ErrorCode::MissingStats, "lambda_min required for rate");
+    const double m = static_cast<double>(s.m);
+    RateIteration r;
+    r.per_iteration = 1.0 - *s.lambda_min * gamma * (2.0 - gamma * psi_value) / m;
+    r.per_epoch = std::pow(r.per_iteration, m);
+    return r;
+}
+
+ProbBound iteration_bound(const SystemStats& s, double x0_dist_sq, double epsilon, double eta) {
+    if (!s.lambda_min || !(*s.lambda_min > 0.0)) fail(ErrorCode::ZeroLambdaMin, "the bound requires lambda_min > 0");
+    if (!(epsilon > 0.0) || !(x0_dist_sq > 0.0)) fail(ErrorCode::InvalidArgument, "epsilon and x0_dist_sq must be > 0");
+    if (!(eta > 0.0 && eta < 1.0)) fail(ErrorCode::InvalidArgument, "eta must lie in (0,1)");
+    const double m = static_cast<double>(s.m), mu = static_cast<double>(s.mu);
+    const double j = m * (mu + 1.0) / *s.lambda_min * std::abs(std::log(x0_dist_sq / (eta * epsilon)));
+    ProbBound b;
+    b.epsilon = epsilon;
+    b.eta = eta;
+    b.j_min = static_cast<index_t>(std::ceil(j));
+    return b;
 }
 
 index_t max_feasible_tau(index_t m, double lambda_max) {

@@ -1178,8 +1178,12 @@ asyrk_status stats_impl(asyrk_system* s, double tol, int64_t max_iters, asyrk_st
     o.l_res = bits(h.l_res_bits);
     if (o.theta)
         for (int64_t i = 0; i < s->m; ++i) o.theta[i] = s->h_len[(size_t)i];
-    asyrk_status ps = power_impl(s, tol, max_iters, &o.lambda_max, &o.power_iterations);
-    if (ps) return ps;
+    o.lambda_max = 0.0;
+    o.power_iterations = 0;
+    if (max_iters >= 0) {  // (< 0: the caller takes lambda_max from the dense spectrum)
+        asyrk_status ps = power_impl(s, tol, max_iters, &o.lambda_max, &o.power_iterations);
+        if (ps) return ps;
+    }
     *out = o;
     return ASYRK_OK;
 }

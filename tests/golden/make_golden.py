@@ -121,6 +121,51 @@ def sim_golden(out):
     out["fit/vals"] = np.array([f["slope"], f["r2"]])
 
 
+# least-squares cases of test_lsq.cpp:128-213 and acceptance.cpp:316-340 (C7):
+# name: (m, n, delta, seed, noise, lsq kwargs). The reference's inconsistent
+# generator needs the Eigen SVD (absent), so b = consistent b + noise *
+# N(0,1) from numpy's generator seeded with the instance seed; sigma_r (which
+# the reference would take from its dense SVD) is LAPACK's via numpy and is
+# passed to both implementations.
+LSQ_CASES = {
+    "l60x30": (60, 30, 0.25, 101, 0.4, dict(max_epochs=60000, target=1e-18, seed=3)),
+    "l60x30_shuffle": (60, 30, 0.25, 101, 0.4, dict(max_epochs=300, target=0.0, seed=4, sampling="shuffle")),
+    "l40x16_consistent": (40, 16, 0.3, 107, 0.0, dict(max_epochs=40000, target=1e-20)),
+    "l30x12_explicit": (30, 12, 0.3, 109, 0.3, dict(zeta=0.37, phi=1.5, max_epochs=10)),
+    "l200x100_c7": (200, 100, 0.1, 61, 0.5, dict(max_epochs=200000, target=1e-16, seed=17)),
+}
+
+
+def dense_of(e, m, n):
+    D = np.zeros((m, n))
+    for i in range(m):
+        for k in range(e["row_ptr"][i], e["row_ptr"][i + 1]):
+            D[i, e["col_idx"][k]] = e["values"][k]
+    return D
+
+
+def lsq_golden(out):
+    for nm, (m, n, delta, seed, noise, kw) in LSQ_CASES.items():
+        A, b, xs = REF.gen_sparse_gaussian(m, n, delta, seed)
+        if noise:
+            b = b + noise * np.random.default_rng(seed).standard_normal(m)
+        e = A.export()
+        s = np.linalg.svd(dense_of(e, m, n), compute_uv=False)
+        sigma_r = float(s[s > 1e-10 * s[0]][-1])
+        p = f"lsq/{nm}/"
+        out[p + "shape"] = np.array([m, n])
+        for k in ["row_ptr", "col_idx", "values", "row_norm"]:
+            out[p + k] = e[k]
+        out[p + "b"] = b
+        out[p + "sigma_r"] = np.array([sigma_r])
+        r = REF.lsq_solve(A, b, sigma_r, **kw)
+        for k in ["x_ls", "y"]:
+            out[p + k] = r[k]
+        out[p + "scal"] = np.array([r["grad_norm"], r["zeta"], r["phi"], r["sigma_r"]])
+        out[p + "r_sq"] = r["trace"]["r_sq"]
+        out[p + "epoch_index"] = r["trace"]["epoch_index"]
+
+
 def main():
     out = {}
     # ---- RNG known answers
@@ -197,6 +242,7 @@ def main():
     A3n, _ = REF.build(3, 2, [0, 1, 2, 2], [0, 1, 0, 1], [1.0, 1.0, s, s], True, None)
     out["kat/stats/three_row"] = stats_vector(REF.stats_full(A3n, 1e-9, 200000))
     sim_golden(out)
+    lsq_golden(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e3:.0f} kB")

@@ -134,7 +134,13 @@ def test_pybind_simulate_matches_oracle(golden):
         assert np.array_equal(np.asarray(d[k]), ref[k]), k
     assert d["gamma"] == 0.05
     st = oracle.C.stats_full(Ac)
-    cor = oracle.C.corollary(A.m, st["mu"], st["lambda_max"], 3)
-    assert abs(d["rho"] - cor["rho"]) <= 1e-9 * cor["rho"] and abs(d["psi"] - cor["psi"]) <= 1e-9 * cor["psi"]
+    # compute_stats' default exact_spectral: lambda_max = sigma_max^2 of the dense SVD
+    D = np.zeros((A.m, A.n))
+    for i in range(A.m):
+        D[i, A.col_idx[A.row_ptr[i]:A.row_ptr[i + 1]]] = A.values[A.row_ptr[i]:A.row_ptr[i + 1]]
+    lam = np.linalg.svd(D, compute_uv=False)[0] ** 2
+    assert abs(lam - st["lambda_max"]) <= 1e-7 * lam  # (power iteration, tol 1e-9 on the quotient)
+    cor = oracle.C.corollary(A.m, st["mu"], lam, 3)
+    assert abs(d["rho"] - cor["rho"]) <= 1e-12 * cor["rho"] and abs(d["psi"] - cor["psi"]) <= 1e-12 * cor["psi"]
     with pytest.raises(ValueError, match="InvalidArgument"):
         pkg.simulate(A.m, A.n, rows, A.col_idx, A.values, b, 10, 1, 0.1, delay="sometimes")

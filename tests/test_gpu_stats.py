@@ -103,7 +103,8 @@ def test_compute_stats_errors():
 
 
 def test_pybind_system_stats_and_step_params(golden, instances):
-    # module.cpp:113-157 with the device statistics (power-iteration lambda_max)
+    # module.cpp:113-157 with the device statistics; compute_stats' default
+    # exact_spectral: lambda_max / lambda_min / sigma_r from the device SVD
     import paper_1401_4780_b200 as pkg
 
     nm = "stats_200x120"
@@ -114,9 +115,18 @@ def test_pybind_system_stats_and_step_params(golden, instances):
     for k in EXACT:
         assert float(d[k]) == ref[k], k
     assert list(d["theta"]) == list(golden[f"stats/{nm}/theta"])
-    assert "lambda_min" not in d and "sigma_r" not in d
+    D = np.zeros((inst["m"], inst["n"]))
+    for i in range(inst["m"]):
+        lo, hi = inst["row_ptr"][i], inst["row_ptr"][i + 1]
+        D[i, inst["col_idx"][lo:hi]] = inst["values"][lo:hi]
+    sv = np.linalg.svd(D, compute_uv=False)
+    sr = sv[sv > 1e-10 * sv[0]][-1]
+    assert abs(d["lambda_max"] - sv[0] ** 2) <= 1e-12 * sv[0] ** 2
+    assert abs(d["lambda_max"] - ref["lambda_max"]) <= 1e-8 * ref["lambda_max"]  # vs the power iteration
+    assert abs(d["sigma_r"] - sr) <= 1e-12 * sv[0] and abs(d["lambda_min"] - d["sigma_r"] ** 2) == 0.0
     p = pkg.step_params(inst["m"], inst["n"], rows, inst["col_idx"], inst["values"], 2)
     Ac = oracle.C.from_arrays(inst["m"], inst["n"], inst["row_ptr"], inst["col_idx"], inst["values"])
-    cor = oracle.C.corollary(inst["m"], int(ref["mu"]), ref["lambda_max"], 2)
-    assert p["feasible"] == cor["feasible"] and abs(p["rho"] - cor["rho"]) <= 1e-9 * cor["rho"]
-    assert abs(p["gamma"] - cor["gamma"]) <= 1e-8 * abs(cor["gamma"]) and len(p["bounds"]) == 3
+    cor = oracle.C.corollary(inst["m"], int(ref["mu"]), sv[0] ** 2, 2)  # exact lambda_max, as the reference's SVD
+    assert p["feasible"] == cor["feasible"] and abs(p["rho"] - cor["rho"]) <= 1e-12 * cor["rho"]
+    assert abs(p["gamma"] - cor["gamma"]) <= 1e-11 * abs(cor["gamma"]) and len(p["bounds"]) == 3
+    assert "rate_iteration" in p or not p["feasible"]  # lambda_min is known now

@@ -12,7 +12,7 @@ import pytest
 from conftest import ROOT
 
 HEADERS = [os.path.join(ROOT, "include", "asyrk_cuda.h"), os.path.join(ROOT, "include", "asyrk_datagen.h"),
-           os.path.join(ROOT, "include", "asyrk_io.h")]
+           os.path.join(ROOT, "include", "asyrk_io.h"), os.path.join(ROOT, "include", "asyrk_dense.h")]
 
 
 def declared_functions():
@@ -162,6 +162,11 @@ def test_pybind_stats_and_simulate_signatures_match_reference():
     for fn, extra in [(pkg.system_stats, []), (pkg.step_params, ["tau"])]:
         for arg in ["m", "n", "rows", "cols", "vals"] + extra:
             assert f"{arg}:" in fn.__doc__
+    # module.cpp:311-316
+    for arg in ["m", "n", "rows", "cols", "vals", "b"]:
+        assert f"{arg}:" in pkg.lsq.__doc__
+    for arg, default in [("epochs", "5000"), ("target", "0.0"), ("seed", "0")]:
+        assert re.search(rf"\b{arg}: [^=]*= {re.escape(default)}[,)]", pkg.lsq.__doc__), arg
 
 
 def test_host_csr_row_norms_are_serial_sums():
