@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libasyrk_b200.so")
+# (ASYRK_LIB: an alternative build of the same library, for A/B experiments)
+LIB_PATH = os.environ.get("ASYRK_LIB") or os.path.join(_HERE, "libasyrk_b200.so")
 
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)

@@ -52,7 +52,8 @@ struct DetArgs {
     const int32_t* ev_col;        // per (event, nonzero): column, in event order (prepass)
     double* ev_val;               // per (event, nonzero): value, in event order (prepass)
     double* ev_b;                 // per event: b_i
-    double* ev_nrm;               // per event: row_norm_i
+    double* ev_nn;                // per event: row_norm_i^2 (rounded, as the reference forms it)
+    double* ev_rcp;               // per event: RN(1 / ev_nn), the division's reciprocal
     long long* dbg;               // optional per-event phase timestamps (diagnostics)
     int poll_ns;                  // dataflow polling back-off (0: spin)
     uint32_t max_len;             // longest row (picks the dataflow kernel's elements per lane)
@@ -61,7 +62,7 @@ void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
 struct DetPrep {
     int32_t *keys, *vals, *keys_s, *vals_s, *start;
-    double *ev_val, *ev_b, *ev_nrm;
+    double *ev_val, *ev_b, *ev_nn, *ev_rcp;
     void* temp;
     size_t temp_bytes;
 };

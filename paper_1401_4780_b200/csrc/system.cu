@@ -227,7 +227,8 @@ void free_all(asyrk_system* s) {
     F(s->prep.temp);
     F(s->prep.ev_val);
     F(s->prep.ev_b);
-    F(s->prep.ev_nrm);
+    F(s->prep.ev_nn);
+    F(s->prep.ev_rcp);
     flag_release(s->host_flag);
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
@@ -295,12 +296,13 @@ void ensure_seq(asyrk_system* s, size_t count) {
     const size_t pairs = count * (size_t)s->max_len;
     for (void* p : {(void*)s->need, (void*)s->prep.keys, (void*)s->prep.vals, (void*)s->prep.keys_s,
                     (void*)s->prep.vals_s, (void*)s->prep.start, s->prep.temp, (void*)s->prep.ev_val,
-                    (void*)s->prep.ev_b, (void*)s->prep.ev_nrm})
+                    (void*)s->prep.ev_b, (void*)s->prep.ev_nn, (void*)s->prep.ev_rcp})
         pool_free(p, s->stream);
     s->need = dalloc<int32_t>(pairs);
     s->prep.ev_val = dalloc<double>(pairs);
     s->prep.ev_b = dalloc<double>(count);
-    s->prep.ev_nrm = dalloc<double>(count);
+    s->prep.ev_nn = dalloc<double>(count);
+    s->prep.ev_rcp = dalloc<double>(count);
     s->prep.keys = dalloc<int32_t>(pairs);
     s->prep.vals = dalloc<int32_t>(pairs);
     s->prep.keys_s = dalloc<int32_t>(pairs);
@@ -764,7 +766,8 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.ev_col = s->prep.keys;
         da.ev_val = s->prep.ev_val;
         da.ev_b = s->prep.ev_b;
-        da.ev_nrm = s->prep.ev_nrm;
+        da.ev_nn = s->prep.ev_nn;
+        da.ev_rcp = s->prep.ev_rcp;
         s->stats.warps = 1;
         s->stats.resident_warps = 1;
     } else {
