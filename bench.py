@@ -714,6 +714,103 @@ def run_mc(args):
     return 0
 
 
+LSQ = dict(m=4000, n=1000, theta=10, seed=7, noise=0.5, target_rel=1e-20, threads=256, gamma=1.0, epochs=20000)
+LSQ_METRIC = "least-squares solves/sec (lsq_solve through the augmented system to the augmented-residual target)"
+
+
+def run_lsq(args):
+    """lsq_solve (lsq.cpp:103-170) on a noisy fixed-theta
+    system. sigma_r (which the reference takes from its Eigen SVD, absent
+    here) comes from the device dense SVD once and is passed to both arms.
+    b200 arm: the host-buffer call (augment + upload + the augmented solve by
+    LSQ['threads'] async warp workers + grad) — a host-to-host call, so value
+    and e2e coincide; the deterministic (bit-identical) variant and the SVD
+    time are reported in config. Reference arm: the reference lsq_solve
+    (oracle/_ref, single core, rk_solve inside)."""
+    from paper_1401_4780_b200 import capi
+
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    A, b, _ = capi.generate_fixed_theta(LSQ["m"], LSQ["n"], LSQ["theta"], seed=LSQ["seed"])
+    b = b + LSQ["noise"] * np.random.default_rng(LSQ["seed"]).standard_normal(LSQ["m"])
+    cfg = {"workload": f"lsq_solve m={LSQ['m']} n={LSQ['n']} theta={LSQ['theta']} N(0,1) unit rows, b = A x* + "
+                       f"{LSQ['noise']} N(0,1); augmented {LSQ['m'] + LSQ['n']}^2 system to r_sq <= "
+                       f"{LSQ['target_rel']} ||b_tilde||^2-scale target"}
+    line = {"metric": LSQ_METRIC, "unit": "solves/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic"}
+    capi.dense_svd(A)  # (the first device call of the process also pays the CUDA context)
+    t0 = time.perf_counter()
+    sv = capi.dense_svd(A)
+    svd_ms = 1e3 * (time.perf_counter() - t0)
+    sr = float(sv["sigma"][sv["rank"] - 1])
+    target = LSQ["target_rel"] * float(b @ b)
+    kw = dict(sigma_r=sr, max_epochs=LSQ["epochs"], target=target, seed=1)
+    if args.impl == "reference":
+        R = load_ref()
+        if R is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+            return 0
+        Ar, _ = R.build(A.m, A.n, np.repeat(np.arange(A.m), np.diff(A.row_ptr)), A.col_idx, A.values, True, None)
+        for _ in range(args.warmup):
+            r = R.lsq_solve(Ar, b, sr, max_epochs=LSQ["epochs"], target=target, seed=1)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            r = R.lsq_solve(Ar, b, sr, max_epochs=LSQ["epochs"], target=target, seed=1)
+        wall = time.perf_counter() - t0
+        v = args.steps / wall
+        line.update(value=v, ms_per_step=1e3 * wall / args.steps, impl="reference",
+                    config=dict(cfg, solver="rk_solve (1 core)", grad_norm=r["grad_norm"],
+                                epochs=int(r["trace"]["epoch_index"][-1])),
+                    cpu_baseline={"value": v, "unit": "solves/s", "cores": 1, "kind": "reference",
+                                  "sample": "one full lsq_solve per step"},
+                    e2e={"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+        print(json.dumps(line))
+        return 0
+
+    def timed(threads, gamma, steps, warmup):
+        for _ in range(warmup):
+            capi.lsq_solve(A, b, threads=threads, gamma=gamma, **kw)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            r = capi.lsq_solve(A, b, threads=threads, gamma=gamma, **kw)
+        return 1e3 * (time.perf_counter() - t0) / steps, r
+
+    with ClockSampler(0) as clk:
+        ms, r = timed(LSQ["threads"], LSQ["gamma"], args.steps, args.warmup)
+    det_ms, rd = timed(1, 1.0, max(1, args.steps // 5), 1)
+    # kernel launches of one augmented solve (the resident-system twin of the call)
+    phi, zeta = capi.lsq_optimal_params(sr)
+    aug = capi.lsq_augment(A, b, zeta, phi)
+    with capi.System(aug["a_tilde"], aug["b_tilde"]) as S:
+        S.solve(threads=LSQ["threads"], gamma=LSQ["gamma"], epochs=LSQ["epochs"], target=target, seed=1,
+                sampling=capi.WITH_REPLACEMENT)
+        launches = int(S.stats()["kernel_launches"])
+    cpu = None
+    if not args.no_cpu_baseline:
+        R = load_ref()
+        if R is not None:
+            Ar, _ = R.build(A.m, A.n, np.repeat(np.arange(A.m), np.diff(A.row_ptr)), A.col_idx, A.values, True, None)
+            t0 = time.perf_counter()
+            rr = R.lsq_solve(Ar, b, sr, max_epochs=LSQ["epochs"], target=target, seed=1)
+            w = time.perf_counter() - t0
+            cpu = {"value": 1.0 / w, "unit": "solves/s", "cores": 1, "kind": "reference",
+                   "sample": f"one reference lsq_solve ({1e3 * w:.1f} ms, grad_norm {rr['grad_norm']:.3g})"}
+    v = 1e3 / ms
+    nbytes_in = int(8 * (A.m + 1) + 16 * A.nnz + 8 * A.m)
+    line.update(value=v, ms_per_step=ms,
+                config=dict(cfg, threads=LSQ["threads"], gamma=LSQ["gamma"], grad_norm=r["grad_norm"],
+                            epochs=int(r["trace"]["epoch_index"][-1]), sigma_r=sr, dense_svd_ms=round(svd_ms, 2),
+                            deterministic_ms=round(det_ms, 3), deterministic_grad_norm=rd["grad_norm"],
+                            timing="wall clock of the host-buffer call (host-to-host API)"),
+                e2e={"value": v, "unit": "solves/s", "h2d_bytes_per_step": nbytes_in,
+                     "d2h_bytes_per_step": int(8 * (A.m + A.n)), "ms_per_step": ms},
+                gpu_launches=launches, clocks=clk.summary())
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line))
+    return 0
+
+
 def run_cfg5_shards(args):
     """Config 5 per-rank work at G = 1, 2, 4, 8 on ONE GPU: the shard a rank of a
     G-GPU job owns (k/G RHS columns) solved alone with its own stop test. A
@@ -774,7 +871,7 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--warps", type=int, default=0, help="worker warps (0 = all resident warp slots)")
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc", "cfg1", "cfg3", "cfg3x", "cfg4",
-                                                           "sweep", "cfg5shards"])
+                                                           "sweep", "cfg5shards", "lsq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.workload == "mc":
@@ -785,6 +882,8 @@ def main():
         return run_sweep(args)
     if args.workload == "cfg5shards":
         return run_cfg5_shards(args)
+    if args.workload == "lsq":
+        return run_lsq(args)
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg5":
