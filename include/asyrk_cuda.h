@@ -215,9 +215,12 @@ asyrk_status asyrk_compute_stats(const asyrk_csr_view* A, double tol, int64_t ma
 /* ---- bounded-delay simulator (delay_sim.hpp, delay_sim.cpp:71-338) -------- *
  * Deterministic replay of the asynchronous recursion with a delay model
  * (DelayModel, delay_sim.hpp:17-31), bit-identical to the reference: trace
- * records, events, history, probes, final_x and Monte-Carlo means. The
- * projector-based dist_sq (dense SVD) is not available: probe_dist_sq fails
- * with InvalidArgument as the reference does without a SolutionProjector. */
+ * records, events, history, probes, final_x and Monte-Carlo means.
+ * Distances (SimOptions::projector): dist_point = the projector's solution
+ * point A^+ b (n entries; SolutionProjector::solution_point, full column
+ * rank) adds ||x - dist_point||^2 to every record and enables probe_dist_sq;
+ * without it probe_dist_sq fails with InvalidArgument, as the reference does
+ * without a SolutionProjector. */
 typedef struct {
     double gamma;          /* StepParams::gamma, >= 0 (InvalidGamma) */
     int64_t tau;           /* DelayModel::tau, >= 0 */
@@ -227,8 +230,9 @@ typedef struct {
     uint64_t seed;         /* simulate: seed; monte_carlo_ratios: base_seed */
     int64_t probe_every;   /* SimOptions (simulate only) */
     int32_t probe_r_sq;
-    int32_t probe_dist_sq; /* needs a SolutionProjector: InvalidArgument */
+    int32_t probe_dist_sq; /* needs dist_point: InvalidArgument */
     int64_t max_events;
+    const double* dist_point;  /* NULL, or the projector's A^+ b (n) */
 } asyrk_sim_config;
 
 /* SimRun (delay_sim.hpp:44-55). Caller buffers with capacities; counts are
@@ -245,6 +249,7 @@ typedef struct {
     int64_t probe_cap, probe_count;
     int64_t* probe_iteration;
     double* probe_r_sq;
+    double* probe_dist_sq;     /* probe_cap entries when probe_dist_sq (may be NULL otherwise) */
 } asyrk_sim_out;
 
 asyrk_status asyrk_simulate(const asyrk_csr_view* A, const double* b, const double* x0, const asyrk_sim_config* cfg,

@@ -87,14 +87,16 @@ class SimConfig(C.Structure):
 
     _fields_ = [("gamma", C.c_double), ("tau", C.c_int64), ("delay", C.c_int32), ("variant", C.c_int32),
                 ("iterations", C.c_int64), ("seed", C.c_uint64), ("probe_every", C.c_int64),
-                ("probe_r_sq", C.c_int32), ("probe_dist_sq", C.c_int32), ("max_events", C.c_int64)]
+                ("probe_r_sq", C.c_int32), ("probe_dist_sq", C.c_int32), ("max_events", C.c_int64),
+                ("dist_point", _f64p)]
 
 
 class SimOut(C.Structure):
     _fields_ = [("trace", TraceOut), ("ev_cap", C.c_int64), ("ev_count", C.c_int64), ("ev_j", _i64p),
                 ("ev_i", _i64p), ("ev_t", _i64p), ("ev_k", _i64p), ("ev_step", _f64p), ("history_cap", C.c_int64),
                 ("history_rows", C.c_int64), ("history", _f64p), ("probe_cap", C.c_int64),
-                ("probe_count", C.c_int64), ("probe_iteration", _i64p), ("probe_r_sq", _f64p)]
+                ("probe_count", C.c_int64), ("probe_iteration", _i64p), ("probe_r_sq", _f64p),
+                ("probe_dist_sq", _f64p)]
 
 
 DELAY = {"fixed": 0, "uniform_random": 1, "max_staleness": 2}
@@ -102,9 +104,14 @@ SIM_VARIANT = {"single_component": 0, "full_row": 1}
 
 
 def _sim_config(gamma, tau, delay, iterations, seed, variant, probe_every=0, probe_r_sq=False, probe_dist_sq=False,
-                max_events=0):
-    return SimConfig(gamma, tau, DELAY[delay], SIM_VARIANT[variant], iterations, seed, probe_every,
-                     int(probe_r_sq), int(probe_dist_sq), max_events)
+                max_events=0, dist_point=None):
+    """dist_point: the SolutionProjector's solution point A^+ b (e.g. dense_lstsq(A, b)), which
+    adds dist_sq to the records and enables probe_dist_sq."""
+    dp = np.ascontiguousarray(dist_point, dtype=np.float64) if dist_point is not None else None
+    c = SimConfig(gamma, tau, DELAY[delay], SIM_VARIANT[variant], iterations, seed, probe_every,
+                  int(probe_r_sq), int(probe_dist_sq), max_events, _ptr(dp, _f64p))
+    c._keep = dp  # the pointer's owner lives as long as the config
+    return c
 
 
 def _sim_call(fn, n, m, cfg: SimConfig):
@@ -116,18 +123,20 @@ def _sim_call(fn, n, m, cfg: SimConfig):
     ev["step"] = np.zeros(ne)
     hist = np.zeros((max(cfg.tau, 0) + 1, n))
     npr = K // cfg.probe_every + 1 if cfg.probe_every > 0 else 1
-    pit, prs = np.zeros(npr, np.int64), np.zeros(npr)
+    pit, prs, pds = np.zeros(npr, np.int64), np.zeros(npr), np.zeros(npr)
     o = SimOut(tr.out, min(cfg.max_events, K), 0, _ptr(ev["j"], _i64p), _ptr(ev["i"], _i64p), _ptr(ev["t"], _i64p),
                _ptr(ev["k"], _i64p), _ptr(ev["step"], _f64p), hist.shape[0], 0, _ptr(hist, _f64p), npr, 0,
-               _ptr(pit, _i64p), _ptr(prs, _f64p))
+               _ptr(pit, _i64p), _ptr(prs, _f64p), _ptr(pds, _f64p))
     check(fn(o))
     tr.out = o.trace
-    d = tr.result(False)
+    d = tr.result(bool(cfg.dist_point))
     nev = min(o.ev_count, o.ev_cap)
     d["events"] = {k: v[:nev].copy() for k, v in ev.items()}
     d["history"] = hist[:o.history_rows].copy()
     d["probe_iteration"] = pit[:o.probe_count].copy()
-    d["probe_r_sq"] = prs[:o.probe_count].copy()
+    d["probe_r_sq"] = prs[:o.probe_count].copy() if cfg.probe_r_sq else np.zeros(0)
+    if cfg.probe_dist_sq:
+        d["probe_dist_sq"] = pds[:o.probe_count].copy()
     return d
 
 
@@ -586,7 +595,8 @@ def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, *
 
 
 def simulate(A: HostCsr, b, x0, gamma, tau, delay, iterations, seed, variant, **opts):
-    """One-shot asyrk_simulate (ref delay_sim.cpp:71-228); opts = probe_every, probe_r_sq, max_events."""
+    """One-shot asyrk_simulate (ref delay_sim.cpp:71-228); opts = probe_every, probe_r_sq, max_events,
+    probe_dist_sq + dist_point (the projector's A^+ b)."""
     b = np.ascontiguousarray(b, dtype=np.float64)
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
     cfg = _sim_config(gamma, tau, delay, iterations, seed, variant, **opts)

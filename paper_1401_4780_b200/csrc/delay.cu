@@ -143,6 +143,29 @@ __device__ __forceinline__ void run_sync() {
         __syncwarp();
 }
 
+// ||x - xd||^2 by the run's threads (strided partial sums, fixed-order tree):
+// the SolutionProjector distance for a full-column-rank A (dense.hpp), equal
+// to the reference's SVD-based dist_sq up to rounding; returned to every thread
+template <bool CTA>
+__device__ double run_dist(const double* x, const double* xd, long long n, int tid, int nthr) {
+    double s = 0.0;
+    for (long long q = tid; q < n; q += nthr) {
+        const double d = x[q] - xd[q];
+        s = fma(d, d, s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if (!CTA) return s;
+    __shared__ double red[8];
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < (nthr >> 5); ++w) t += red[w];
+    __syncthreads();
+    return t;
+}
+
 // residuals (csr.cpp:140-160) of x by every thread of the run: rt = Ax - b,
 // gt = A^T rt; returns {r_sq, grad_sq} on thread 0 (serial sums)
 template <bool CTA>
@@ -196,9 +219,11 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
     double* rt = gw + a.hot;
     double* gt = rt + m;
     const Rows rw{a.R};
-    const bool probing = a.probe_every > 0 && a.probe_r_sq;
+    const bool probing = a.probe_every > 0 && a.probe_r_sq;  // LiveResidual maintained
+    const bool probe_any = a.probe_every > 0 && (a.probe_r_sq || a.probe_d != nullptr);
     const bool rec_out = run == 0 && a.rec != nullptr;
     double* probe = a.probe ? a.probe + run * a.probe_stride : nullptr;
+    double* probe_d = a.probe_d ? a.probe_d + run * a.probe_stride : nullptr;
     const unsigned long long t0 = globaltimer_ns();
 
     for (long long q = tid; q < n; q += nthr) {
@@ -217,6 +242,7 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
     auto boundary = [&](long long epoch, long long updates, bool recompute) {
         double r_sq = 0.0, g_sq = 0.0;
         run_residuals<CTA>(a, rw, x, rt, gt, tid, nthr, r_sq, g_sq);
+        const double dist = (rec_out && a.xdist) ? run_dist<CTA>(x, a.xdist, n, tid, nthr) : -1.0;
         if (tid == 0) {
             if (!isfinite(r_sq) || !isfinite(g_sq)) {
                 a.status[run] = 8;  // ASYRK_E_NonFinite
@@ -229,7 +255,7 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
                     rc.updates = updates;
                     rc.r_sq = r_sq;
                     rc.grad_sq = g_sq;
-                    rc.dist_sq = -1.0;
+                    rc.dist_sq = dist;
                     rc.t_ns = globaltimer_ns() - t0;
                     a.rec[nrec] = rc;
                 }
@@ -244,11 +270,15 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
     };
     auto do_probe = [&](long long jj) {
         if (tid == 0 && probe) probe[nprobe] = live_rsq;
+        if (probe_d) {
+            const double d = run_dist<CTA>(x, a.xdist, n, tid, nthr);
+            if (tid == 0) probe_d[nprobe] = d;
+        }
         ++nprobe;
     };
 
     boundary(0, 0, probing);  // LiveResidual ctor recompute(A, x0) + record(0, 0)
-    if (!stop_flag[slot] && probing) do_probe(0);
+    if (!stop_flag[slot] && probe_any) do_probe(0);
 
     for (long long j = 0; j < a.iterations && !stop_flag[slot]; ++j) {
         if (tid < 32) {  // warp 0 of the run replays iteration j; lane 0 owns the generator
@@ -308,7 +338,7 @@ __global__ void __launch_bounds__(256) sim_kernel(SimArgs a) {
         const long long done = j + 1;
         if (done % m == 0) boundary(done / m, done, probing);
         if (stop_flag[slot]) break;
-        if (probing && done % a.probe_every == 0) do_probe(done);
+        if (probe_any && done % a.probe_every == 0) do_probe(done);
     }
     if (!stop_flag[slot] && a.iterations % m != 0) boundary(a.iterations / m + 1, a.iterations, false);
     if (a.smem_state && run == 0) {  // final x and the ring back to global memory for the host

@@ -1,6 +1,7 @@
 // simulate / monte_carlo_ratios / rate_fit (ref/src/delay_sim.cpp:71-338)
 // over the C ABI: the recursion runs on the device (csrc/delay.cu).
 #include "asyrk/delay_sim.hpp"
+#include "asyrk/dense.hpp"
 
 #include "asyrk/error.hpp"
 #include "asyrk_cuda.h"
@@ -44,9 +45,9 @@ SimRun simulate(const CsrMatrix& A, std::span<const double> b, std::span<const d
                 const DelayModel& delay, index_t iterations, std::uint64_t seed, SimVariant variant,
                 const SimOptions& opts) {
     check_dims(A, b, x0);
-    if (opts.projector)
-        fail(ErrorCode::TooLarge, "SolutionProjector distances need the dense SVD, not on the device path");
     asyrk_sim_config c = sim_config(params, delay, iterations, seed, variant);
+    // the projector's distance runs on the device as ||x - A^+ b||^2 (full column rank)
+    if (opts.projector) c.dist_point = projector_point(*opts.projector, A.cols()).data();
     c.probe_every = opts.probe_every;
     c.probe_r_sq = opts.probe_r_sq ? 1 : 0;
     c.probe_dist_sq = opts.probe_dist_sq ? 1 : 0;
@@ -55,16 +56,17 @@ SimRun simulate(const CsrMatrix& A, std::span<const double> b, std::span<const d
     const index_t rec_cap = iterations > 0 ? iterations / m + 2 : 1;
     const index_t ev_cap = std::max<index_t>(0, std::min<index_t>(opts.max_events, std::max<index_t>(iterations, 0)));
     const index_t hist_cap = delay.tau >= 0 ? std::min<index_t>(delay.tau + 1, std::max<index_t>(iterations, 0) + 1) : 0;
-    const bool probing = opts.probe_every > 0 && opts.probe_r_sq;
+    const bool probing = opts.probe_every > 0 && (opts.probe_r_sq || opts.probe_dist_sq);
     const index_t probe_cap = probing && iterations > 0 ? iterations / opts.probe_every + 1 : 0;
 
     std::vector<int64_t> ep(rec_cap), upd(rec_cap), ej(ev_cap), ei(ev_cap), et(ev_cap), ek(ev_cap), pit(probe_cap);
-    std::vector<double> rs(rec_cap), gs(rec_cap), wall(rec_cap), es(ev_cap), hist(hist_cap * n), prs(probe_cap);
+    std::vector<double> rs(rec_cap), gs(rec_cap), ds(rec_cap), wall(rec_cap), es(ev_cap), hist(hist_cap * n),
+        prs(probe_cap), pds(probe_cap);
     SimRun run;
     run.params = params;
     run.trace.final_x.resize(static_cast<std::size_t>(n));
     asyrk_sim_out o{};
-    o.trace = asyrk_trace_out{rec_cap, 0, ep.data(), rs.data(), gs.data(), nullptr, wall.data(), upd.data(),
+    o.trace = asyrk_trace_out{rec_cap, 0, ep.data(), rs.data(), gs.data(), ds.data(), wall.data(), upd.data(),
                               run.trace.final_x.data()};
     o.ev_cap = ev_cap;
     o.ev_j = ej.data();
@@ -77,6 +79,7 @@ SimRun simulate(const CsrMatrix& A, std::span<const double> b, std::span<const d
     o.probe_cap = probe_cap;
     o.probe_iteration = pit.data();
     o.probe_r_sq = prs.data();
+    o.probe_dist_sq = pds.data();
     asyrk_system* sys = A.device(0);  // cached fp64 device matrix, b replaced in place
     throw_status(asyrk_system_set_rhs(sys, b.data()));
     throw_status(asyrk_system_simulate(sys, x0.data(), &c, &o));
@@ -98,6 +101,7 @@ SimRun simulate(const CsrMatrix& A, std::span<const double> b, std::span<const d
         e.epoch_index = ep[r];
         e.r_sq = rs[r];
         e.grad_sq = gs[r];
+        if (opts.projector) e.dist_sq = ds[r];
         e.wall_seconds = wall[r];
         e.updates_applied = upd[r];
         run.trace.epochs.push_back(e);
@@ -108,7 +112,8 @@ SimRun simulate(const CsrMatrix& A, std::span<const double> b, std::span<const d
         run.history.emplace_back(hist.begin() + h * n, hist.begin() + (h + 1) * n);
     for (index_t p = 0; p < std::min<index_t>(o.probe_count, probe_cap); ++p) {
         run.probe_iteration.push_back(pit[p]);
-        run.probe_r_sq.push_back(prs[p]);
+        if (opts.probe_r_sq) run.probe_r_sq.push_back(prs[p]);
+        if (opts.probe_dist_sq) run.probe_dist_sq.push_back(pds[p]);
     }
     return run;
 }

@@ -201,6 +201,8 @@ struct SimArgs {
     unsigned long long seed0;      // run r uses seed0 + r
     long long probe_every;
     int probe_r_sq;
+    const double* xdist;           // n: the projector's solution point (dist_sq records / probes), or nullptr
+    double* probe_d;               // runs x probe_stride dist probes, or nullptr
     long long max_events;
     long long runs;
     double* work;                  // runs x work_stride doubles (sim_work_doubles)

@@ -1199,7 +1199,8 @@ asyrk_status sim_validate(const asyrk_system* s, const asyrk_sim_config* c) {
     if (c->gamma < 0.0) return fail(ASYRK_E_InvalidGamma, "gamma must be >= 0");
     if (c->iterations < 1) return fail(ASYRK_E_InvalidArgument, "need at least one iteration");
     if (c->tau < 0) return fail(ASYRK_E_InvalidArgument, "tau must be >= 0");
-    if (c->probe_dist_sq) return fail(ASYRK_E_InvalidArgument, "probe_dist_sq needs a SolutionProjector");
+    if (c->probe_dist_sq && !c->dist_point)
+        return fail(ASYRK_E_InvalidArgument, "probe_dist_sq needs a SolutionProjector");
     if (c->delay < 0 || c->delay > 2) return fail(ASYRK_E_InvalidArgument, "unknown delay model");
     if (c->variant < 0 || c->variant > 1) return fail(ASYRK_E_InvalidArgument, "unknown update variant");
     return ASYRK_OK;
@@ -1240,13 +1241,15 @@ asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config*
     cudaStream_t st = s->stream;
     AllocStream as(st);
     const long long m = s->m, n = s->n, K = c->iterations;
-    const bool probing = c->probe_every > 0 && c->probe_r_sq;
+    const bool probing = c->probe_every > 0 && (c->probe_r_sq || c->probe_dist_sq);
     const long long nprobe_max = probing ? K / c->probe_every + 1 : 0;
     const long long rec_cap = K / m + 2;
     const long long ev_cap = std::min<long long>(c->max_events, K);
     const size_t wd = sim_work_doubles(m, n, c->tau);
     double* work = dalloc<double>(wd);
     double* probe = dalloc<double>((size_t)std::max<long long>(nprobe_max, 1));
+    double* probe_d = dalloc<double>((size_t)std::max<long long>(nprobe_max, 1));
+    double* xdist = c->dist_point ? dalloc<double>((size_t)n) : nullptr;
     DevRecord* rec = dalloc<DevRecord>((size_t)rec_cap);
     SimEventDev* ev = dalloc<SimEventDev>((size_t)std::max<long long>(ev_cap, 1));
     long long* cnt = dalloc<long long>(4);  // nrec, nev, nprobe, fail_updates
@@ -1257,18 +1260,21 @@ asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config*
         ~Free() {
             for (void* q : p) pool_free(q, s);
         }
-    } fr{{work, probe, rec, ev, cnt, status}, st};
+    } fr{{work, probe, probe_d, xdist, rec, ev, cnt, status}, st};
     sim_upload_x0(s, x0);
+    if (xdist) CK(cudaMemcpyAsync(xdist, c->dist_point, (size_t)n * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(cnt, 0, 4 * 8, st));
     CK(cudaMemsetAsync(status, 0, 4, st));
     SimArgs a = sim_args(s, c);
     a.probe_every = c->probe_every;
     a.probe_r_sq = c->probe_r_sq;
+    a.xdist = xdist;
+    a.probe_d = c->probe_dist_sq ? probe_d : nullptr;
     a.max_events = ev_cap;
     a.runs = 1;
     a.work = work;
     a.work_stride = (long long)wd;
-    a.probe = probing ? probe : nullptr;
+    a.probe = (probing && c->probe_r_sq) ? probe : nullptr;
     a.probe_stride = nprobe_max;
     a.rec = rec;
     a.rec_cap = rec_cap;
@@ -1296,7 +1302,7 @@ asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config*
         if (tr.epoch_index) tr.epoch_index[k] = r.epoch;
         if (tr.r_sq) tr.r_sq[k] = r.r_sq;
         if (tr.grad_sq) tr.grad_sq[k] = r.grad_sq;
-        if (tr.dist_sq) tr.dist_sq[k] = -1.0;
+        if (tr.dist_sq) tr.dist_sq[k] = r.dist_sq;
         if (tr.wall_seconds) tr.wall_seconds[k] = 1e-9 * (double)r.t_ns;
         if (tr.updates_applied) tr.updates_applied[k] = r.updates;
     }
@@ -1330,7 +1336,10 @@ asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config*
     out->probe_count = probing ? hc[2] : 0;
     const long long np = std::min<long long>(out->probe_count, out->probe_cap);
     if (np > 0) {
-        if (out->probe_r_sq) CK(cudaMemcpy(out->probe_r_sq, probe, (size_t)np * 8, cudaMemcpyDeviceToHost));
+        if (out->probe_r_sq && c->probe_r_sq)
+            CK(cudaMemcpy(out->probe_r_sq, probe, (size_t)np * 8, cudaMemcpyDeviceToHost));
+        if (out->probe_dist_sq && c->probe_dist_sq)
+            CK(cudaMemcpy(out->probe_dist_sq, probe_d, (size_t)np * 8, cudaMemcpyDeviceToHost));
         if (out->probe_iteration)
             for (long long k = 0; k < np; ++k) out->probe_iteration[k] = k * c->probe_every;
     }

@@ -166,6 +166,43 @@ def lsq_golden(out):
         out[p + "epoch_index"] = r["trace"]["epoch_index"]
 
 
+# instances of the reference's acceptance criteria (acceptance.cpp:66-103):
+# name: (m, n, delta, seed or None, tau, lambda_min floor). seed None = the
+# find_feasible scan over seeds 1..400 (ZeroColumn draws skipped; lambda_min
+# from the dense spectrum — LAPACK via numpy, the reference's Eigen being
+# absent — must reach the floor and the corollary be feasible at tau).
+ACCEPT = {
+    "c1": (500, 200, 0.10, 20240501, 0, 0.0),   # criterion 1
+    "c23": (1200, 60, 0.08, None, 5, 0.02),     # criteria 2 and 3 (shared instance)
+    "c6": (100, 50, 0.08, None, 2, 0.04),       # criterion 6
+}
+
+
+def accept_golden(out):
+    for nm, (m, n, delta, seed, tau, floor) in ACCEPT.items():
+        for sd in ([seed] if seed is not None else range(1, 401)):
+            A, b, xs = REF.gen_sparse_gaussian(m, n, delta, sd)
+            try:
+                st = REF.stats_full(A)
+            except Exception:  # ZeroColumn: skipped as find_feasible does
+                continue
+            e = A.export()
+            s = np.linalg.svd(dense_of(e, m, n), compute_uv=False)
+            lmin = float(s[s > 1e-10 * s[0]][-1]) ** 2
+            if seed is None:
+                if lmin < floor or not REF.corollary(m, st["mu"], st["alpha"], float(s[0]) ** 2, tau)["feasible"]:
+                    continue
+            p = f"acc/{nm}/"
+            out[p + "shape"] = np.array([m, n, sd])
+            for k in ["row_ptr", "col_idx", "values", "row_norm"]:
+                out[p + k] = e[k]
+            out[p + "b"] = b
+            out[p + "x_star"] = xs
+            break
+        else:
+            raise RuntimeError(f"no feasible instance for {nm}")
+
+
 def main():
     out = {}
     # ---- RNG known answers
@@ -243,6 +280,7 @@ def main():
     out["kat/stats/three_row"] = stats_vector(REF.stats_full(A3n, 1e-9, 200000))
     sim_golden(out)
     lsq_golden(out)
+    accept_golden(out)
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.npz")
     np.savez_compressed(path, **out)
     print(f"wrote {path}: {len(out)} arrays, {os.path.getsize(path) / 1e3:.0f} kB")

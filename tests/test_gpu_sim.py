@@ -144,3 +144,26 @@ def test_pybind_simulate_matches_oracle(golden):
     assert abs(d["rho"] - cor["rho"]) <= 1e-12 * cor["rho"] and abs(d["psi"] - cor["psi"]) <= 1e-12 * cor["psi"]
     with pytest.raises(ValueError, match="InvalidArgument"):
         pkg.simulate(A.m, A.n, rows, A.col_idx, A.values, b, 10, 1, 0.1, delay="sometimes")
+
+
+def test_simulator_projector_distances(golden):
+    # SimOptions::projector (delay_sim.cpp:94-123, 154): with the projector's
+    # solution point every record carries dist_sq and probe_dist_sq follows
+    # ||x - A^+ b||^2 at the probe iterations; the r_sq probes and the trace
+    # stay bit-identical to the run without distances
+    A, b = sim_csr(golden, "d30x20")
+    xp = capi.dense_lstsq(A, b)
+    x0 = np.full(A.n, 0.25)
+    kw = dict(probe_every=7, probe_r_sq=True)
+    plain = capi.simulate(A, b, x0, 0.05, 3, "uniform_random", 400, 11, "single_component", **kw)
+    d = capi.simulate(A, b, x0, 0.05, 3, "uniform_random", 400, 11, "single_component", probe_dist_sq=True,
+                      dist_point=xp, **kw)
+    for k in ["epoch_index", "r_sq", "grad_sq", "final_x", "probe_r_sq", "probe_iteration"]:
+        assert np.array_equal(d[k], plain[k]), k
+    assert len(d["dist_sq"]) == len(d["r_sq"]) and len(d["probe_dist_sq"]) == len(d["probe_iteration"])
+    f = d["final_x"] - xp
+    assert abs(d["dist_sq"][-1] - f @ f) <= 1e-12 * (f @ f)
+    assert abs(d["probe_dist_sq"][0] - (x0 - xp) @ (x0 - xp)) <= 1e-12 * ((x0 - xp) @ (x0 - xp))
+    with pytest.raises(capi.AsyrkError, match="InvalidArgument"):
+        capi.simulate(A, b, x0, 0.05, 3, "uniform_random", 40, 11, "single_component", probe_every=7,
+                      probe_dist_sq=True)
