@@ -4,7 +4,9 @@
 Workload (N=1, BASELINE.json configs[1]): m=200000, n=100000, 30 nonzeros per
 row at distinct uniform columns, N(0,1) values, rows normalized, fp64;
 x* ~ N(0,1), b = A x*, x0 = 0; asynchronous lock-free warp-workers with
-Philox with-replacement row sampling, gamma = 1, a residual snapshot every
+slice-shuffle row sampling (each worker reshuffles its slice of the rows every
+epoch — the reference's default ParSampling, parallel.hpp:14-31, and the only
+one its Python solve_parallel uses), gamma = 1, a residual snapshot every
 epoch (snapshot_interval = 1, the reference default), stop at
 ||Ax-b|| / ||b|| < 1e-6. One "step" = one full solve to tolerance.
 
@@ -45,7 +47,7 @@ L2_FLUSH_BYTES = 256 << 20
 def workload_config(W, extra=None):
     c = {
         "workload": "config2: m=200000 n=100000 theta=30 N(0,1) unit rows fp64, x0=0, async to ||r||/||b||<1e-6",
-        "sampling": "with_replacement (Philox per warp)",
+        "sampling": "slice_shuffle (per-warp row slices reshuffled every epoch; the reference default)",
         "gamma": 1.0,
         "snapshot_interval": 1,
         "warps": W,
@@ -139,10 +141,10 @@ def gen_system(seed):
 
 
 # --------------------------------------------------------------------------- reference arm
-def ref_solve_once(R, Ah, b, threads, target, epochs=10000):
+def ref_solve_once(R, Ah, b, threads, target, epochs=10000, sampling="slice_shuffle"):
     x0 = np.zeros(Ah.n)
     t = R.solve_parallel(Ah, b, x0, threads=threads, gamma=1.0, epochs=epochs, target=target,
-                         variant="full_row", sampling="with_replacement", seed=7, snapshot_interval=1, cap=epochs + 2)
+                         variant="full_row", sampling=sampling, seed=7, snapshot_interval=1, cap=epochs + 2)
     return int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), t
 
 
@@ -193,12 +195,21 @@ def run_reference(args):
     value = proj / wall
     cpu = {"value": value, "unit": "proj/s", "cores": cores, "kind": "reference",
            "sample": f"{args.steps} full config-2 solves to 1e-6 (reference solve_parallel, {cores} threads, "
-                     "with_replacement, gamma=1, snapshot_interval=1)"}
+                     "slice_shuffle, gamma=1, snapshot_interval=1)"}
+    # the rest of SURVEY §8(d)'s CPU protocol, reported beside the line: T = 1
+    # (a bounded 5-epoch sample) and with_replacement sampling at T = nproc
+    p1, w1, _ = ref_solve_once(R, Ah, b, 1, 0.0, epochs=5)
+    ps, ws, ts = ref_solve_once(R, Ah, b, cores, target, sampling="with_replacement")
+    protocol = {"T1_slice_shuffle_proj_s": p1 / w1, "T1_sample": "5 epochs",
+                f"T{cores}_with_replacement_proj_s": ps / ws,
+                f"T{cores}_with_replacement_time_to_tolerance_ms": 1e3 * ws,
+                f"T{cores}_with_replacement_epochs": int(ts["epoch_index"][-1])}
     line = {
         "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "impl": "reference", "config": workload_config(cores, {"threads": cores, "warps": None}),
+        "impl": "reference",
+        "config": workload_config(cores, {"threads": cores, "warps": None, "cpu_protocol": protocol}),
         "time_to_tolerance_ms": 1e3 * statistics.median(ttt), "epochs": int(t["epoch_index"][-1]),
         "cpu_baseline": cpu, "e2e": {"value": value, "unit": "proj/s", "h2d_bytes_per_step": 0,
                                      "d2h_bytes_per_step": 0},
@@ -234,7 +245,7 @@ def run_gpu(args):
     W = args.warps or S.max_resident_warps()
     lam, lam_iters = S.power_iteration(1e-6)  # stats.cpp:15-50 on the device; tau bound beside the warp count
     flush =torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    solve_kw = dict(threads=W, gamma=1.0, epochs=2000, target=target, sampling=capi.WITH_REPLACEMENT,
+    solve_kw = dict(threads=W, gamma=1.0, epochs=2000, target=target, sampling=capi.SLICE_SHUFFLE,
                     snapshot_interval=1, want_x=False)
 
     for w in range(args.warmup):
@@ -288,7 +299,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = capi.solve_parallel_host(A, b, threads=W, gamma=1.0, epochs=2000, target=target,
-                                     sampling=capi.WITH_REPLACEMENT, seed=2000 + k)
+                                     sampling=capi.SLICE_SHUFFLE, seed=2000 + k)
         dt = time.perf_counter() - t0
         if k >= 0:
             e2e_wall += dt
@@ -386,7 +397,7 @@ def cpu_baseline(A, b):
     p, w, t = ref_solve_once(R, Ah, b, cores, target)
     return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference",
             "sample": f"1 full config-2 solve to 1e-6 ({int(t['epoch_index'][-1])} epochs, {w:.2f} s) with the "
-                      f"reference solve_parallel, {cores} threads, with_replacement",
+                      f"reference solve_parallel, {cores} threads, slice_shuffle",
             "time_to_tolerance_ms": 1e3 * w}
 
 
@@ -524,7 +535,7 @@ def run_other(args):
         run = lambda k: S.rk_solve(max_epochs=c["epochs"], target=target, seed=42 + k,  # noqa: E731
                                    sampling=capi.RK_UNIFORM, x_star=xs)
     else:
-        samp = capi.NORM_PROPORTIONAL if args.workload == "cfg4" else capi.WITH_REPLACEMENT
+        samp = capi.NORM_PROPORTIONAL if args.workload == "cfg4" else capi.SLICE_SHUFFLE
         run = lambda k: S.solve(threads=W, gamma=1.0, epochs=c["epochs"], target=target, sampling=samp,  # noqa: E731
                                 seed=100 + k, snapshot_interval=1, x_star=xs, want_x=False, precision=prec)
     for k in range(args.warmup):
@@ -593,7 +604,7 @@ def other_cpu_baseline(name, c, A, b):
             "1 epoch of serial rk_solve(norm_proportional) on the raw rows"
     else:  # cfg3: the reference runs fp64 only; 1 epoch of solve_parallel on all host threads
         t = R.solve_parallel(Ah, b, x0, threads=cores, gamma=1.0, epochs=1, target=0.0, variant="full_row",
-                             sampling="with_replacement", seed=7, snapshot_interval=1, cap=4)
+                             sampling="slice_shuffle", seed=7, snapshot_interval=1, cap=4)
         p, w, sample = int(t["updates_applied"][-1]), float(t["wall_seconds"][-1]), \
             f"1 epoch of solve_parallel (fp64), {cores} threads"
     return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference", "sample": sample}
@@ -620,7 +631,7 @@ def run_sweep(args):
     for W in [32, 148, 592, 1184, 2368, 2664, 3552]:
         if W > res:
             continue
-        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL * TOL * bb, sampling=capi.WITH_REPLACEMENT,
+        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL * TOL * bb, sampling=capi.SLICE_SHUFFLE,
                   snapshot_interval=1, x_star=xs, want_x=False)
         S.solve(seed=1, **kw)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
