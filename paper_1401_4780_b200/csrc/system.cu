@@ -97,8 +97,12 @@ struct asyrk_system {
     int32_t* pick_host[kLookahead + 1] = {};
     long long* flat_dev[kLookahead + 1] = {};   // ragged rows: event -> offset of its (event, nonzero) pairs
     long long* flat_host[kLookahead + 1] = {};
-    int32_t* need = nullptr;                    // dataflow prepass output
-    DetPrep prep{};
+    // dataflow prepass outputs, double-buffered: chunk k+1's prepass runs on
+    // pstream while chunk k's dataflow kernel runs
+    int32_t* need[2] = {nullptr, nullptr};
+    DetPrep prep[2] = {};
+    cudaStream_t pstream = nullptr;
+    cudaEvent_t ev_prep[2] = {nullptr, nullptr}, ev_det[2] = {nullptr, nullptr};
     size_t seq_cap = 0;
 
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
@@ -187,6 +191,19 @@ bool kit_put(asyrk_system* s) {
     return true;
 }
 
+void destroy_det_streams(asyrk_system* s) {
+    if (s->pstream) {
+        cudaStreamSynchronize(s->pstream);
+        cudaStreamDestroy(s->pstream);
+        s->pstream = nullptr;
+    }
+    for (int h = 0; h < 2; ++h) {
+        if (s->ev_prep[h]) cudaEventDestroy(s->ev_prep[h]);
+        if (s->ev_det[h]) cudaEventDestroy(s->ev_det[h]);
+        s->ev_prep[h] = s->ev_det[h] = nullptr;
+    }
+}
+
 void free_all(asyrk_system* s) {
     cudaStream_t fs = s->stream;
     auto F = [fs](void* p) { pool_free(p, fs); };
@@ -218,17 +235,19 @@ void free_all(asyrk_system* s) {
     F(s->st);
     F(s->incr);
     F(s->scratch);
-    F(s->need);
-    F(s->prep.keys);
-    F(s->prep.vals);
-    F(s->prep.keys_s);
-    F(s->prep.vals_s);
-    F(s->prep.start);
-    F(s->prep.temp);
-    F(s->prep.ev_val);
-    F(s->prep.ev_b);
-    F(s->prep.ev_nn);
-    F(s->prep.ev_rcp);
+    for (int h = 0; h < 2; ++h) {
+        F(s->need[h]);
+        F(s->prep[h].keys);
+        F(s->prep[h].vals);
+        F(s->prep[h].keys_s);
+        F(s->prep[h].vals_s);
+        F(s->prep[h].start);
+        F(s->prep[h].temp);
+        F(s->prep[h].ev_val);
+        F(s->prep[h].ev_b);
+        F(s->prep[h].ev_nn);
+        F(s->prep[h].ev_rcp);
+    }
     flag_release(s->host_flag);
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
@@ -241,6 +260,7 @@ void free_all(asyrk_system* s) {
     for (int q = 0; q < 2; ++q) F(s->xs[q]);
     if (s->mstream) cudaStreamSynchronize(s->mstream);
     if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
+    destroy_det_streams(s);
     if (kit_put(s)) return;
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
     if (s->ev_end) cudaEventDestroy(s->ev_end);
@@ -294,22 +314,24 @@ void ensure_seq(asyrk_system* s, size_t count) {
     }
     // dataflow prepass buffers: one (event, nonzero) pair per entry
     const size_t pairs = count * (size_t)s->max_len;
-    for (void* p : {(void*)s->need, (void*)s->prep.keys, (void*)s->prep.vals, (void*)s->prep.keys_s,
-                    (void*)s->prep.vals_s, (void*)s->prep.start, s->prep.temp, (void*)s->prep.ev_val,
-                    (void*)s->prep.ev_b, (void*)s->prep.ev_nn, (void*)s->prep.ev_rcp})
-        pool_free(p, s->stream);
-    s->need = dalloc<int32_t>(pairs);
-    s->prep.ev_val = dalloc<double>(pairs);
-    s->prep.ev_b = dalloc<double>(count);
-    s->prep.ev_nn = dalloc<double>(count);
-    s->prep.ev_rcp = dalloc<double>(count);
-    s->prep.keys = dalloc<int32_t>(pairs);
-    s->prep.vals = dalloc<int32_t>(pairs);
-    s->prep.keys_s = dalloc<int32_t>(pairs);
-    s->prep.vals_s = dalloc<int32_t>(pairs);
-    s->prep.start = dalloc<int32_t>((size_t)s->n);
-    s->prep.temp_bytes = det_prepare_temp_bytes((long long)pairs);
-    s->prep.temp = dalloc<unsigned char>(s->prep.temp_bytes);
+    for (int h = 0; h < 2; ++h) {
+        DetPrep& P = s->prep[h];
+        for (void* p : {(void*)s->need[h], (void*)P.keys, (void*)P.vals, (void*)P.keys_s, (void*)P.vals_s,
+                        (void*)P.start, P.temp, (void*)P.ev_val, (void*)P.ev_b, (void*)P.ev_nn, (void*)P.ev_rcp})
+            pool_free(p, s->stream);
+        s->need[h] = dalloc<int32_t>(pairs);
+        P.ev_val = dalloc<double>(pairs);
+        P.ev_b = dalloc<double>(count);
+        P.ev_nn = dalloc<double>(count);
+        P.ev_rcp = dalloc<double>(count);
+        P.keys = dalloc<int32_t>(pairs);
+        P.vals = dalloc<int32_t>(pairs);
+        P.keys_s = dalloc<int32_t>(pairs);
+        P.vals_s = dalloc<int32_t>(pairs);
+        P.start = dalloc<int32_t>((size_t)s->n);
+        P.temp_bytes = det_prepare_temp_bytes((long long)pairs);
+        P.temp = dalloc<unsigned char>(P.temp_bytes);
+    }
     s->seq_cap = count;
 }
 
@@ -762,12 +784,16 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
         da.poll_ns = poll_ns;
         da.max_len = s->max_len;
-        da.need = s->need;
-        da.ev_col = s->prep.keys;
-        da.ev_val = s->prep.ev_val;
-        da.ev_b = s->prep.ev_b;
-        da.ev_nn = s->prep.ev_nn;
-        da.ev_rcp = s->prep.ev_rcp;
+        if (!s->pstream) {
+            CK(cudaStreamCreateWithFlags(&s->pstream, cudaStreamNonBlocking));
+            for (int h = 0; h < 2; ++h) {
+                CK(cudaEventCreateWithFlags(&s->ev_prep[h], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&s->ev_det[h], cudaEventDisableTiming));
+            }
+        }
+        // the pstream work of this solve follows everything queued on st before it
+        CK(cudaEventRecord(s->ev_det[0], st));
+        CK(cudaStreamWaitEvent(s->pstream, s->ev_det[0], 0));
         s->stats.warps = 1;
         s->stats.resident_warps = 1;
     } else {
@@ -798,7 +824,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     static const bool no_overlap = getenv("ASYRK_NO_OVERLAP") != nullptr;
     // (instrumented runs keep the in-stream monitor: restoring the stopping
     // snapshot would desynchronize x from the shadow increments)
-    const bool overlap = !sp.det && !no_overlap && !instr;
+    // The deterministic path overlaps too: its exact monitor (serial sums,
+    // ~150 us per record at config 1) reads a boundary snapshot on the monitor
+    // stream while the next chunk runs; a chunk that ran past the stopping
+    // boundary is undone by restoring that snapshot, so records and the
+    // returned iterate are the in-order ones (bit-identical either way).
+    static const bool no_det_overlap = getenv("ASYRK_NO_DET_OVERLAP") != nullptr;
+    const bool overlap = !no_overlap && !instr && (!sp.det || !no_det_overlap);
     if (overlap && !s->mstream) {
         // highest priority: monitor blocks take SM slots ahead of queued worker blocks
         int lo = 0, hi = 0;
@@ -816,7 +848,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     // (the workers wait for the monitor); default: the monitor takes the latest
     // boundary it can, like the reference's coordinator, and the workers never wait
     static const bool exact_env = getenv("ASYRK_EXACT_RECORDS") != nullptr;
-    const bool exact_records = exact_env || sp.every_boundary;
+    const bool exact_records = exact_env || sp.every_boundary || sp.det;  // deterministic: every boundary
     static const char* tl_path = getenv("ASYRK_TIMELINE");
     Timeline tl;
     tl.marks.reserve(4 * Timeline::kChunks);
@@ -848,12 +880,23 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             }
             chunk_incr.push_back(inc);
             const size_t cnt = (size_t)(span * s->m);
-            CK(cudaMemcpyAsync(s->seq_dev[slot], s->seq_host[slot], cnt * 4, cudaMemcpyHostToDevice, st));
+            // uploads and the dataflow prepass go on pstream, one chunk ahead of
+            // the dataflow kernel on st; prepass set h was last read by chunk k-2
+            const int h = (int)(k & 1);
+            cudaStream_t ps = s->pstream;
+            if (k >= 2) CK(cudaStreamWaitEvent(ps, s->ev_det[h], 0));
+            CK(cudaMemcpyAsync(s->seq_dev[slot], s->seq_host[slot], cnt * 4, cudaMemcpyHostToDevice, ps));
             if (!sp.full_row)
-                CK(cudaMemcpyAsync(s->pick_dev[slot], s->pick_host[slot], cnt * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(s->pick_dev[slot], s->pick_host[slot], cnt * 4, cudaMemcpyHostToDevice, ps));
             da.seq = s->seq_dev[slot];
             da.picks = s->pick_dev[slot];
             da.count = (long long)cnt;
+            da.need = s->need[h];
+            da.ev_col = s->prep[h].keys;
+            da.ev_val = s->prep[h].ev_val;
+            da.ev_b = s->prep[h].ev_b;
+            da.ev_nn = s->prep[h].ev_nn;
+            da.ev_rcp = s->prep[h].ev_rcp;
             long long pairs = (long long)cnt * (long long)s->uniform_len;
             da.flat_off = nullptr;
             if (!s->uniform) {  // ragged rows: offsets of each event's (event, nonzero) pairs
@@ -861,11 +904,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
                 fo[0] = 0;
                 for (size_t q = 0; q < cnt; ++q) fo[q + 1] = fo[q] + s->h_len[(size_t)s->seq_host[slot][q]];
                 pairs = fo[cnt];
-                CK(cudaMemcpyAsync(s->flat_dev[slot], fo, (cnt + 1) * 8, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(s->flat_dev[slot], fo, (cnt + 1) * 8, cudaMemcpyHostToDevice, ps));
                 da.flat_off = s->flat_dev[slot];
             }
+            if (da.x_in_smem) launch_det_prepare(da, s->prep[h], pairs, ps);
+            CK(cudaEventRecord(s->ev_prep[h], ps));
+            CK(cudaStreamWaitEvent(st, s->ev_prep[h], 0));
             if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
-            if (da.x_in_smem) launch_det_prepare(da, s->prep, pairs, st);
             static const char* dbg_path = getenv("ASYRK_DET_DEBUG");
             long long* dbg = nullptr;
             if (dbg_path && k == 0) {
@@ -874,12 +919,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             }
             da.dbg = dbg;
             launch_det(da, 0, st);
+            CK(cudaEventRecord(s->ev_det[h], st));
             if (dbg) {
-                std::vector<long long> h((size_t)cnt * 4);
+                std::vector<long long> hd((size_t)cnt * 4);
                 CK(cudaStreamSynchronize(st));
-                CK(cudaMemcpy(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(hd.data(), dbg, hd.size() * 8, cudaMemcpyDeviceToHost));
                 if (FILE* f = fopen(dbg_path, "wb")) {
-                    fwrite(h.data(), 8, h.size(), f);
+                    fwrite(hd.data(), 8, hd.size(), f);
                     fclose(f);
                 }
                 cudaFree(dbg);
@@ -913,7 +959,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             tl.end(ts, st);
             CK(cudaEventRecord(s->snap_ev[slot2], st));
             CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[slot2], 0));
-            MonitorArgs ma = monitor_args(s, false, 0, sp.x_star != nullptr);
+            MonitorArgs ma = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
             if (exact_records) {
                 ma.x = s->xs[slot2];
                 ma.slot = slot2;
@@ -944,7 +990,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         // the epochs that ran past the stopping snapshot are discarded: the
         // solve returns the iterate whose residual met the target
         launch_restore(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, st);
-        MonitorArgs fa = monitor_args(s, false, 0, sp.x_star != nullptr);
+        MonitorArgs fa = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
         fa.force = 1;
         launch_monitor(fa, prec, st);
         launches += 1 + mon_kernels;  // restore + final record
