@@ -1,4 +1,5 @@
 // Host runtime of the C ABI (runtime.h).
+#include <chrono>
 #include "runtime.h"
 
 #include <algorithm>
@@ -79,11 +80,17 @@ void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* d
     std::lock_guard<std::mutex> lk(mu_);
     const size_t per_chunk = chunk_ / out_elem;
     const size_t total = out_bytes / out_elem;
+    static const bool prof = getenv("ASYRK_STAGE_PROFILE") != nullptr;  // diagnostics: fill vs wait
+    double t_wait = 0.0, t_fill = 0.0;
+    const auto t_start = std::chrono::steady_clock::now();
     for (size_t e0 = 0; e0 < total; e0 += per_chunk) {
         const size_t ne = std::min(per_chunk, total - e0);
         const int k = next_;
         next_ = (next_ + 1) % kSlots;
+        const auto t0 = std::chrono::steady_clock::now();
         cudaEventSynchronize(ev_[k]);  // slot's previous DMA done
+        const auto t1 = std::chrono::steady_clock::now();
+        t_wait += std::chrono::duration<double, std::milli>(t1 - t0).count();
         unsigned char* slot = slot_[k];
         const int nt = pool_.size();
         std::function<void(int)> task = [&](int t) {
@@ -94,10 +101,15 @@ void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* d
             pool_.run(task);
         else
             fill(slot, e0, ne);
+        t_fill += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count();
         if (cudaMemcpyAsync(dst + e0 * out_elem, slot, ne * out_elem, cudaMemcpyHostToDevice, s) != cudaSuccess)
             throw std::runtime_error("staged upload failed");
         cudaEventRecord(ev_[k], s);
     }
+    if (prof)
+        fprintf(stderr, "[stage] %9zu B: issue %.3f ms (fill %.3f, slot waits %.3f)\n", out_bytes,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(), t_fill,
+                t_wait);
 }
 
 static bool have_avx2() {

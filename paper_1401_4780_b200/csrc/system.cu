@@ -499,6 +499,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     CK(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
 
+    phase("alloc+aux");
     // pinned, multithreaded staging; int64 columns cross PCIe as int32 (runtime.h)
     Stager& up = Stager::get();
     up.upload(d_rp, A->row_ptr, ((size_t)A->m + 1) * 8, st);
@@ -524,6 +525,10 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     if (b) up.upload(d_b, b, (size_t)A->m * 8, st);
     else CK(cudaMemsetAsync(d_b, 0, (size_t)A->m * 8, st));
     CK(cudaMemcpyAsync(s->b, d_b, (size_t)A->m * 8, cudaMemcpyDeviceToDevice, st));
+    if (prof) {
+        fprintf(stderr, "[create] upload issued   %8.3f ms\n",
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_prev).count());
+    }
     phase("upload");
 
     scan_thr.join();
