@@ -17,8 +17,9 @@
  *   asyrk_residuals          residuals               ref/include/asyrk/csr.hpp:89-90
  *   asyrk_power_iteration_lambda_max
  *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:131-132
- *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:47-60 (exact_spectral
- *                                                    = false; ref/src/stats.cpp:52-130)
+ *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:47-60 (the
+ *                                                    structural fields; ref/src/stats.cpp:52-130;
+ *                                                    the dense spectrum: include/asyrk_dense.h)
  *   asyrk_simulate           simulate                ref/include/asyrk/delay_sim.hpp:61-71
  *   asyrk_monte_carlo_ratios monte_carlo_ratios      ref/include/asyrk/delay_sim.hpp:81-88
  *   asyrk_rate_fit           rate_fit                ref/include/asyrk/delay_sim.hpp:95
@@ -189,8 +190,8 @@ asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double to
                                               double* lambda_max);
 
 /* compute_stats (stats.hpp:47-60, stats.cpp:52-130) with exact_spectral =
- * false: every field of SystemStats except lambda_min / sigma_r (dense SVD,
- * not on the device path). mu, nu, delta, alpha, frob_sq, l_max, l_res and
+ * false: every field of SystemStats except lambda_min / sigma_r (those come
+ * from asyrk_dense_spectrum). mu, nu, delta, alpha, frob_sq, l_max, l_res and
  * theta are bit-identical to the reference; lambda_max is the device power
  * iteration (tol, max_iters = StatsOptions::tol / max_power_iters);
  * max_iters < 0 skips it (lambda_max = 0), for exact_spectral callers that
