@@ -285,3 +285,49 @@ def test_record_modes_of_the_overlapped_monitor():
     for r in (t, u):
         assert np.sqrt(r["dist_sq"][-1] / float(xs @ xs)) <= 1e-5
     S.close()
+
+
+def test_cpp_drop_in_caller_runs(tmp_path):
+    # the C++ drop-in API end to end (tests/cpp/drop_in_caller.cpp): rk_solve and
+    # solve_single bit-identical to the C restatement, async converged with a
+    # consistent audit, exact stats, projector distance, lsq, error codes
+    import subprocess
+
+    from test_host import _build_drop_in_caller
+    out = subprocess.run([_build_drop_in_caller(tmp_path)], check=True, capture_output=True, text=True).stdout
+    res = {ln.split()[0]: ln.split()[1:] for ln in out.splitlines() if ln.strip()}
+    # rebuild the same system as the caller (triplet order, normalize_rows) for the oracle
+    m, n = 60, 24
+    xs = np.sin(0.7 * np.arange(n) + 0.3)
+    trip = {}
+    for i in range(m):
+        for q in range(6):
+            j = (i * 7 + q * 5 + (i * q) % 3) % n
+            if (i, j) not in trip:
+                trip[(i, j)] = np.cos(1.3 * i + 0.9 * q) + 0.1 * (q + 1)
+    keys = sorted(trip)
+    rows = np.array([k[0] for k in keys])
+    cols = np.array([k[1] for k in keys])
+    vals = np.array([trip[k] for k in keys])
+    rp = np.concatenate([[0], np.cumsum(np.bincount(rows, minlength=m))])
+    b0 = np.zeros(m)
+    for i in range(m):  # CsrMatrix::row_dot order
+        s = 0.0
+        for k in range(rp[i], rp[i + 1]):
+            s += vals[k] * xs[cols[k]]
+        b0[i] = s
+    norms = np.sqrt(capi.serial_row_sumsq(rp, vals))
+    vn = vals / np.repeat(norms, np.diff(rp))
+    bn = b0 / norms
+    Ao = oracle.C.from_arrays(m, n, rp, cols, vn)
+    want = oracle.C.rk_solve(Ao, bn, np.zeros(n), 30, 0.0, 5, "uniform", xs)
+    got = np.array([float(v) for v in res["rk_final_x"]])
+    assert np.array_equal(got, want["final_x"])
+    want1 = oracle.C.solve_parallel(Ao, bn, np.zeros(n), 1, 1.0, 12, 0.0, "full_row", "slice_shuffle", 9, 1)
+    assert np.array_equal(np.array([float(v) for v in res["single_final_x"]]), want1["final_x"])
+    assert float(res["async_r_sq"][0]) <= 1e-24 and res["async_r_sq"][2] == "1"
+    assert float(res["stats"][4]) > 0.0  # lambda_min from the exact spectrum
+    rec, d, pd = (float(v) for v in res["projector"])
+    assert abs(rec - d) <= 1e-9 * max(d, 1e-30) and abs(pd - d) <= 1e-9 * max(d, 1e-30)
+    assert float(res["lsq"][0]) <= 1e-6 and float(res["lsq"][1]) <= 1e-6
+    assert res["error"] == ["InvalidArgument"]

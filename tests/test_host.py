@@ -188,3 +188,19 @@ def test_host_csr_row_norms_are_serial_sums():
             s += v[k] * v[k]
         want.append(math.sqrt(s))
     assert np.array_equal(A.row_norm, np.array(want))
+
+
+def _build_drop_in_caller(tmp_path):
+    import subprocess
+    exe = str(tmp_path / "drop_in_caller")
+    lib = os.path.join(ROOT, "paper_1401_4780_b200")
+    subprocess.run(["g++", "-std=gnu++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "drop_in_caller.cpp"), "-o", exe, "-L", lib, "-lasyrk_b200",
+                    f"-Wl,-rpath,{lib}"], check=True, capture_output=True)
+    return exe
+
+
+def test_cpp_drop_in_caller_compiles_against_the_headers(tmp_path):
+    # a reference-style C++ caller (tests/cpp/drop_in_caller.cpp) builds against
+    # include/asyrk/*.hpp and links libasyrk_b200.so (run on the GPU in test_gpu_parity.py)
+    assert os.path.exists(_build_drop_in_caller(tmp_path))
