@@ -89,6 +89,7 @@ struct asyrk_system {
     double* scratch = nullptr;
     int* host_flag = nullptr;      // pinned mapped
     int* host_flag_dev = nullptr;
+    void* host_scalar = nullptr;   // pinned scratch for small device -> host reads
 
     // det staging ring
     int32_t* seq_dev[kLookahead + 1] = {};
@@ -249,6 +250,8 @@ void free_all(asyrk_system* s) {
         F(s->prep[h].ev_rcp);
     }
     flag_release(s->host_flag);
+    if (s->host_scalar) cudaFreeHost(s->host_scalar);
+    s->host_scalar = nullptr;
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
         F(s->pick_dev[k]);
@@ -606,6 +609,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     s->incr = dalloc<unsigned long long>(1);
     s->scratch = dalloc<double>(4096);
     s->host_flag = flag_acquire(&s->host_flag_dev);
+    CK(cudaHostAlloc(&s->host_scalar, 64, cudaHostAllocDefault));
     if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
@@ -995,11 +999,23 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         // the epochs that ran past the stopping snapshot are discarded: the
         // solve returns the iterate whose residual met the target
         launch_restore(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, st);
-        MonitorArgs fa = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
-        fa.force = 1;
-        launch_monitor(fa, prec, st);
-        launches += 1 + mon_kernels;  // restore + final record
-        s->stats.monitor_launches++;
+        launches += 1;
+        // the final record of the returned iterate: when the run stopped at a
+        // monitored snapshot, x was just restored from it and its record
+        // (same bits, same monitor) is already the last one; otherwise (the
+        // last boundaries went unmonitored, or NonFinite) record it now
+        int stop_slot = -1;
+        CK(cudaMemcpyAsync(s->host_scalar, &s->st->stop_slot, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::memcpy(&stop_slot, s->host_scalar, sizeof(int));
+        static const bool always_final = getenv("ASYRK_ALWAYS_FINAL_RECORD") != nullptr;
+        if (stop_slot < 0 || always_final) {
+            MonitorArgs fa = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
+            fa.force = 1;
+            launch_monitor(fa, prec, st);
+            launches += mon_kernels;
+            s->stats.monitor_launches++;
+        }
         CK(cudaGetLastError());
     }
     CK(cudaEventRecord(s->ev_end, st));
