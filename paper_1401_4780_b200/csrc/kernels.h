@@ -104,13 +104,14 @@ struct MonitorArgs {
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 // overlapped solves: copy x into snapshot slot xs (if the epoch ran) and
-// advance the coordinator state (epoch, updates, slot meta, next go)
+// advance the coordinator state (epoch, updates, slot meta, next go);
+// advance = 0 takes boundary 0 (x0, before the first workers; sets go)
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
-                     long long m, cudaStream_t s);
+                     long long m, cudaStream_t s, int advance = 1);
 // decoupled variant: a free slot or none (no record for that boundary); then the
 // monitor stream claims the oldest filled slot (MonitorArgs::slot = kDynSlot)
 void launch_snapshot_dyn(DevState* st, const void* x, void* xs0, void* xs1, long long n, int precision, long long m,
-                         cudaStream_t s);
+                         cudaStream_t s, int advance = 1);
 void launch_claim(DevState* st, cudaStream_t s);
 constexpr int kDynSlot = 2;
 // end of an overlapped solve: x, epoch and updates back to the snapshot whose

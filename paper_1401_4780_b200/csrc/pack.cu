@@ -271,10 +271,11 @@ namespace ak {
 // it, so a whole epoch is either run and counted or skipped.
 template <class X>
 __global__ void snapshot_kernel(DevState* st, const X* __restrict__ x, X* __restrict__ xs, long long n, int slot,
-                                long long m) {
+                                long long m, int advance) {
     __shared__ int copy;
     __shared__ bool last;
-    if (threadIdx.x == 0) copy = st->go && !st->stop;  // after a stop the deciding snapshot must survive
+    // advance = 0: boundary 0 (x0), before any worker ran (go is not set yet)
+    if (threadIdx.x == 0) copy = (advance ? st->go : 1) && !st->stop;  // after a stop the deciding snapshot must survive
     __syncthreads();
     if (copy)
         for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
@@ -290,10 +291,12 @@ __global__ void snapshot_kernel(DevState* st, const X* __restrict__ x, X* __rest
         st->go = 0;
         return;
     }
-    if (st->go) {
-        const long long sp = chunk_span(st);
-        st->epoch += sp;
-        st->updates += sp * m;
+    if (advance ? st->go : 1) {
+        if (advance) {
+            const long long sp = chunk_span(st);
+            st->epoch += sp;
+            st->updates += sp * m;
+        }
         st->snap_epoch[slot] = st->epoch;
         st->snap_updates[slot] = st->updates;
         st->snap_valid[slot] = 1;
@@ -310,14 +313,14 @@ __global__ void snapshot_kernel(DevState* st, const X* __restrict__ x, X* __rest
 // catches (parallel.cpp:388-399).
 template <class X>
 __global__ void snapshot_dyn_kernel(DevState* st, const X* __restrict__ x, X* __restrict__ xs0, X* __restrict__ xs1,
-                                    long long n, long long m) {
+                                    long long n, long long m, int advance) {
     __shared__ int target;
     __shared__ bool last;
     if (threadIdx.x == 0) {
         const unsigned seq = *reinterpret_cast<volatile unsigned*>(&st->snap_seq);
         if (atomicAdd(&st->snap_arrive, 1u) == 0) {
             int t = -1;
-            if (st->go && !st->stop)
+            if ((advance ? st->go : 1) && !st->stop)
                 for (int q = 0; q < 2 && t < 0; ++q)
                     if (atomicCAS(&st->slot_state[q], 0, 1) == 0) t = q;
             st->snap_target = t;
@@ -344,10 +347,12 @@ __global__ void snapshot_dyn_kernel(DevState* st, const X* __restrict__ x, X* __
     st->snap_ticket = 0;
     st->snap_arrive = 0;
     st->snap_seq += 1u;
-    if (st->go && !st->stop) {
-        const long long sp = chunk_span(st);
-        st->epoch += sp;
-        st->updates += sp * m;
+    if ((advance ? st->go : 1) && !st->stop) {
+        if (advance) {
+            const long long sp = chunk_span(st);
+            st->epoch += sp;
+            st->updates += sp * m;
+        }
         if (target >= 0) {
             st->snap_epoch[target] = st->epoch;
             st->snap_updates[target] = st->updates;
@@ -375,14 +380,15 @@ __global__ void claim_kernel(DevState* st) {
 }
 
 void launch_snapshot_dyn(DevState* st, const void* x, void* xs0, void* xs1, long long n, int precision, long long m,
-                         cudaStream_t s) {
+                         cudaStream_t s, int advance) {
     const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
     if (precision == P_F32)
         snapshot_dyn_kernel<float><<<blocks, 256, 0, s>>>(st, static_cast<const float*>(x), static_cast<float*>(xs0),
-                                                          static_cast<float*>(xs1), n, m);
+                                                          static_cast<float*>(xs1), n, m, advance);
     else
         snapshot_dyn_kernel<double><<<blocks, 256, 0, s>>>(st, static_cast<const double*>(x),
-                                                           static_cast<double*>(xs0), static_cast<double*>(xs1), n, m);
+                                                           static_cast<double*>(xs0), static_cast<double*>(xs1), n, m,
+                                                           advance);
 }
 
 void launch_claim(DevState* st, cudaStream_t s) { claim_kernel<<<1, 1, 0, s>>>(st); }
@@ -414,15 +420,15 @@ void launch_restore(DevState* st, void* x, const void* xs0, const void* xs1, lon
 }
 
 void launch_snapshot(const DevState* st, const void* x, void* xs, long long n, int precision, int slot, DevState* stw,
-                     long long m, cudaStream_t s) {
+                     long long m, cudaStream_t s, int advance) {
     (void)st;
     const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 4);
     if (precision == P_F32)
         snapshot_kernel<float><<<blocks, 256, 0, s>>>(stw, static_cast<const float*>(x), static_cast<float*>(xs), n,
-                                                      slot, m);
+                                                      slot, m, advance);
     else
         snapshot_kernel<double><<<blocks, 256, 0, s>>>(stw, static_cast<const double*>(x), static_cast<double*>(xs),
-                                                       n, slot, m);
+                                                       n, slot, m, advance);
 }
 
 }  // namespace ak

@@ -757,10 +757,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     CK(cudaEventRecord(s->ev_begin, st));
     launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st);
     long long launches = 1;
-    launch_monitor(monitor_args(s, sp.det, 0, sp.x_star != nullptr), prec, st);
     const int mon_kernels = sp.det ? 3 : 2;  // rows + columns (+ exact finalize); fast finalize is fused
-    launches += mon_kernels;
-    s->stats.monitor_launches++;
 
     // worker setup
     WorkerArgs wa{};
@@ -858,6 +855,34 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     // boundary it can, like the reference's coordinator, and the workers never wait
     static const bool exact_env = getenv("ASYRK_EXACT_RECORDS") != nullptr;
     const bool exact_records = exact_env || sp.every_boundary || sp.det;  // deterministic: every boundary
+    // boundary 0 (x0): the overlapped modes take it through the same snapshot ->
+    // monitor-stream path as every later boundary, so the first workers start
+    // at once; a stop decided there is undone like any other (restore)
+    if (overlap) {
+        MonitorArgs ma = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
+        if (exact_records) {
+            launch_snapshot(s->st, s->x, s->xs[1], s->n, prec, 1, s->st, s->m, st, 0);
+            ma.x = s->xs[1];
+            ma.slot = 1;
+        } else {
+            launch_snapshot_dyn(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, s->m, st, 0);
+        }
+        CK(cudaEventRecord(s->snap_ev[1], st));
+        CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[1], 0));
+        if (!exact_records) {
+            launch_claim(s->st, s->mstream);
+            ma.x = s->xs[0];
+            ma.x_alt = s->xs[1];
+            ma.slot = kDynSlot;
+        }
+        launch_monitor(ma, prec, s->mstream);
+        CK(cudaEventRecord(s->mon_ev[1], s->mstream));
+        launches += 1 + mon_kernels + (exact_records ? 0 : 1);
+    } else {
+        launch_monitor(monitor_args(s, sp.det, 0, sp.x_star != nullptr), prec, st);
+        launches += mon_kernels;
+    }
+    s->stats.monitor_launches++;
     static const char* tl_path = getenv("ASYRK_TIMELINE");
     Timeline tl;
     tl.marks.reserve(4 * Timeline::kChunks);
@@ -960,7 +985,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             const int slot2 = (int)(k & 1);
             Timeline::Mark* ts = tl.begin("snapshot", k, st);
             if (exact_records) {  // every boundary recorded: slot reuse waits for monitor k-2
-                if (k >= 2) CK(cudaStreamWaitEvent(st, s->mon_ev[slot2], 0));
+                if (k >= 1) CK(cudaStreamWaitEvent(st, s->mon_ev[slot2], 0));  // (k = 1: boundary 0's monitor)
                 launch_snapshot(s->st, s->x, s->xs[slot2], s->n, prec, slot2, s->st, s->m, st);
             } else {  // latest boundary the monitor can take (parallel.cpp:388-399)
                 launch_snapshot_dyn(s->st, s->x, s->xs[0], s->xs[1], s->n, prec, s->m, st);
