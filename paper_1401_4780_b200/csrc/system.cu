@@ -90,6 +90,10 @@ struct asyrk_system {
     int* host_flag = nullptr;      // pinned mapped
     int* host_flag_dev = nullptr;
     void* host_scalar = nullptr;   // pinned scratch for small device -> host reads
+    // the monitor's structures (row / column SELL, plain CSC) finish on bstream
+    // after create returns; every consumer's stream waits on ev_mon_ready
+    cudaStream_t bstream = nullptr;
+    cudaEvent_t ev_mon_ready = nullptr;
 
     // det staging ring
     int32_t* seq_dev[kLookahead + 1] = {};
@@ -206,6 +210,15 @@ void destroy_det_streams(asyrk_system* s) {
 }
 
 void free_all(asyrk_system* s) {
+    if (s->bstream) {
+        cudaStreamSynchronize(s->bstream);
+        cudaStreamDestroy(s->bstream);
+        s->bstream = nullptr;
+    }
+    if (s->ev_mon_ready) {
+        cudaEventDestroy(s->ev_mon_ready);
+        s->ev_mon_ready = nullptr;
+    }
     cudaStream_t fs = s->stream;
     auto F = [fs](void* p) { pool_free(p, fs); };
     F(s->rec);
@@ -389,6 +402,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         s->own_stream = true;
     }
     AllocStream alloc_on(s->stream);
+    CK(cudaHostAlloc(&s->host_scalar, 64, cudaHostAllocDefault));
     // ASYRK_PROFILE_CREATE=1: synchronized phase times on stderr (diagnostics)
     static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
     auto t_prev = std::chrono::steady_clock::now();
@@ -404,6 +418,15 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     // Overlapped build: the host scan of row lengths runs on a thread, and the
     // column sort (CSC / SELL-columns, needs only row_ptr + col_idx) runs on an
     // aux stream while the values are still being staged (runtime.h Stager).
+    s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
+    s->xd = dalloc<double>((size_t)A->n);
+    s->x0d = dalloc<double>((size_t)A->n);
+    s->r = dalloc<double>((size_t)A->m);
+    s->g = dalloc<double>((size_t)A->n);
+    s->part = dalloc<double>((size_t)monitor_row_blocks(A->m) + 2 * (size_t)monitor_col_blocks(A->n) + 8);
+    s->st = dalloc<DevState>(1);
+    s->incr = dalloc<unsigned long long>(1);
+    s->scratch = dalloc<double>(4096);
     long long* d_rp = dalloc<long long>((size_t)A->m + 1);
     int32_t* d_col = dalloc<int32_t>((size_t)A->nnz);
     double* d_val = dalloc<double>((size_t)A->nnz);
@@ -520,6 +543,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     CK(cudaMemsetAsync(grp_size, 0, ((size_t)groups + 1) * 8, aux));
     launch_sell_len(col_ptr, A->n, s->col_len, grp_size, aux);
     exclusive_scan(stemp, stb, grp_size, s->grp_off, groups + 1, aux);
+    CK(cudaMemcpyAsync(s->host_scalar, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, aux));  // column-SELL size
     CK(cudaGetLastError());
     CK(cudaEventRecord(ev_sorted, aux));
     // st: the values, norms and b keep streaming meanwhile
@@ -560,56 +584,57 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
                         s->uniform_len, precision, s->rec, st);
     CK(cudaGetLastError());
     phase("pack");
-    // SELL-32 rows for the monitor's coalesced thread-per-row pass (r = Ax - b);
-    // keys still holds the CSR-order columns (the sort wrote keys_s)
+    // The monitor's structures are built on the aux (build) stream after the
+    // uploads; create returns without waiting for them — the workers need only
+    // the packed records, and every monitor consumer waits on ev_mon_ready.
+    CK(cudaEventSynchronize(ev_sorted));  // the column sort ran during the value upload
+    long long sell_total = 0;
+    std::memcpy(&sell_total, s->host_scalar, 8);
+    // outputs allocated on the solve stream as before (their placement is what
+    // the resident solves measured), then handed to the build stream
     s->rsell_col = dalloc<int32_t>((size_t)sc.rsell_total);
     s->rsell_val = dalloc<unsigned char>((size_t)sc.rsell_total * vbytes);
-    CK(cudaMemsetAsync(s->rsell_col, 0, (size_t)std::max<long long>(sc.rsell_total, 1) * 4, st));
-    CK(cudaMemsetAsync(rgrp_size, 0, ((size_t)rgroups + 1) * 8, st));
-    launch_sell_len(d_rp, A->m, s->row_len, rgrp_size, st);
-    exclusive_scan(rstemp, rstb, rgrp_size, s->rgrp_off, rgroups + 1, st);
-    CK(cudaStreamWaitEvent(st, ev_sorted, 0));  // keys (iota_cols) and the column sort
-    launch_sell_scatter(d_rp, keys, d_val, s->row_len, s->rgrp_off, A->m, precision, s->rsell_col, s->rsell_val, st);
-    phase("sell rows");
-    // SELL-32 columns for the monitor's coalesced thread-per-column pass
-    launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, st);
-    long long sell_total = 0;
-    CK(cudaMemcpyAsync(&sell_total, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, aux));
-    CK(cudaStreamSynchronize(aux));
     s->sell_row = dalloc<int32_t>((size_t)sell_total);
     s->sell_val = dalloc<unsigned char>((size_t)sell_total * vbytes);
-    CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, st));
-    launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row, s->sell_val,
-                        st);
-    phase("sell cols");
-    CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(st));
-    if (keep_csc || precision == P_F64) {  // plain CSC: multi-RHS monitor, simulator's serial column walks
-        s->col_ptr = col_ptr;
-        s->csc_row = csc_row;
-        s->csc_val = csc_val;
-        col_ptr = nullptr;
-        csc_row = nullptr;
-        csc_val = nullptr;
+    CK(cudaEventRecord(ev_cols, st));  // values, norms, b uploaded and packed; outputs allocated
+    CK(cudaStreamWaitEvent(aux, ev_cols, 0));
+    {
+        // SELL-32 rows for the monitor's coalesced thread-per-row pass (r = Ax - b);
+        // keys still holds the CSR-order columns (the sort wrote keys_s)
+        CK(cudaMemsetAsync(s->rsell_col, 0, (size_t)std::max<long long>(sc.rsell_total, 1) * 4, aux));
+        CK(cudaMemsetAsync(rgrp_size, 0, ((size_t)rgroups + 1) * 8, aux));
+        launch_sell_len(d_rp, A->m, s->row_len, rgrp_size, aux);
+        exclusive_scan(rstemp, rstb, rgrp_size, s->rgrp_off, rgroups + 1, aux);
+        launch_sell_scatter(d_rp, keys, d_val, s->row_len, s->rgrp_off, A->m, precision, s->rsell_col, s->rsell_val,
+                            aux);
+        phase("sell rows");
+        // SELL-32 columns for the monitor's coalesced thread-per-column pass
+        launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, aux);
+        CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, aux));
+        launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row,
+                            s->sell_val, aux);
+        phase("sell cols");
+        CK(cudaGetLastError());
+        if (keep_csc || precision == P_F64) {  // plain CSC: multi-RHS monitor, simulator's serial column walks
+            s->col_ptr = col_ptr;
+            s->csc_row = csc_row;
+            s->csc_val = csc_val;
+            col_ptr = nullptr;
+            csc_row = nullptr;
+            csc_val = nullptr;
+        }
+        for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
+                        (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
+                        (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
+            pool_free(p, aux);
+        CK(cudaEventCreateWithFlags(&s->ev_mon_ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(s->ev_mon_ready, aux));
     }
-    for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
-                    (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
-                    (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
-        pool_free(p, st);
-
+    s->bstream = aux;  // the build stream now belongs to the system
+    aux = nullptr;
     phase("free temps");
     // solve buffers
-    s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
-    s->xd = dalloc<double>((size_t)A->n);
-    s->x0d = dalloc<double>((size_t)A->n);
-    s->r = dalloc<double>((size_t)A->m);
-    s->g = dalloc<double>((size_t)A->n);
-    s->part = dalloc<double>((size_t)monitor_row_blocks(A->m) + 2 * (size_t)monitor_col_blocks(A->n) + 8);
-    s->st = dalloc<DevState>(1);
-    s->incr = dalloc<unsigned long long>(1);
-    s->scratch = dalloc<double>(4096);
     s->host_flag = flag_acquire(&s->host_flag_dev);
-    CK(cudaHostAlloc(&s->host_scalar, 64, cudaHostAllocDefault));
     if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
@@ -640,6 +665,17 @@ void write_trace(asyrk_system* s, const DevState& hs, asyrk_trace_out* trace, in
         CK(cudaMemcpyAsync(trace->final_x, s->xd, (size_t)s->n * 8, cudaMemcpyDeviceToHost, s->stream));
         CK(cudaStreamSynchronize(s->stream));
     }
+}
+
+// order `stream` after the monitor structures of create (bstream)
+void mon_wait(asyrk_system* s, cudaStream_t stream) {
+    if (!s->ev_mon_ready) return;
+    if (cudaEventQuery(s->ev_mon_ready) == cudaSuccess) {  // built: no cross-stream edge from now on
+        cudaEventDestroy(s->ev_mon_ready);
+        s->ev_mon_ready = nullptr;
+        return;
+    }
+    CK(cudaStreamWaitEvent(stream, s->ev_mon_ready, 0));
 }
 
 MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xstar) {
@@ -857,7 +893,9 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     const bool exact_records = exact_env || sp.every_boundary || sp.det;  // deterministic: every boundary
     // boundary 0 (x0): the overlapped modes take it through the same snapshot ->
     // monitor-stream path as every later boundary, so the first workers start
-    // at once; a stop decided there is undone like any other (restore)
+    // at once; a stop decided there is undone like any other (restore). Only
+    // the monitor's stream waits for create's build stream.
+    mon_wait(s, overlap ? s->mstream : st);
     if (overlap) {
         MonitorArgs ma = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
         if (exact_records) {
@@ -1148,6 +1186,7 @@ asyrk_status system_rk_impl(asyrk_system* s, const double* x0, const asyrk_rk_co
 
 asyrk_status residuals_impl(asyrk_system* s, const double* x, double* r_sq, double* grad_sq) {
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     CK(cudaMemcpyAsync(s->x0d, x, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
     launch_x_init(s->x0d, s->x, s->n, s->precision, st);
     launch_state_init(s->st, 0, 1, -1.0, st);
@@ -1173,6 +1212,7 @@ asyrk_status residuals_impl(asyrk_system* s, const double* x, double* r_sq, doub
 // power_iteration_lambda_max, ref/src/stats.cpp:15-50
 asyrk_status power_impl(asyrk_system* s, double tol, int64_t max_iters, double* lambda, int64_t* iters) {
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     const int64_t n = s->n;
     RefStream gen(0x5ca1ab1eULL, 0);
     std::vector<double> v((size_t)n);
@@ -1224,6 +1264,7 @@ asyrk_status stats_impl(asyrk_system* s, double tol, int64_t max_iters, asyrk_st
                     "stats are defined for row-normalized matrices; call normalize_rows first");
     if (s->precision != P_F64) return fail(ASYRK_E_InvalidArgument, "compute_stats needs an fp64 system");
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     AllocStream as(st);
     double* col_sq = dalloc<double>((size_t)s->n);
     double* col_norm = dalloc<double>((size_t)s->n);
@@ -1331,6 +1372,7 @@ asyrk_status sim_impl(asyrk_system* s, const double* x0, const asyrk_sim_config*
     if (asyrk_status v = sim_validate(s, c)) return v;
     if (!out) return fail(ASYRK_E_InvalidArgument, "null simulator output");
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     AllocStream as(st);
     const long long m = s->m, n = s->n, K = c->iterations;
     const bool probing = c->probe_every > 0 && (c->probe_r_sq || c->probe_dist_sq);
@@ -1449,6 +1491,7 @@ asyrk_status mc_impl(asyrk_system* s, const double* x0, const asyrk_sim_config* 
     if (asyrk_status v = sim_validate(s, &cc)) return v;
     if (!mean_r_sq || (!ratios && cc.iterations > 0)) return fail(ASYRK_E_InvalidArgument, "null output");
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     AllocStream as(st);
     const long long K = cc.iterations;
     const size_t wd = sim_work_doubles(s->m, s->n, cc.tau);
@@ -1652,6 +1695,7 @@ asyrk_status asyrk_system_set_rhs(asyrk_system* sys, const double* b) {
 asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y) {
     if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
+        mon_wait(sys, sys->stream);
         CK(cudaMemcpyAsync(sys->xd, x, (size_t)sys->n * 8, cudaMemcpyHostToDevice, sys->stream));
         launch_spmv_rows(sys->rsell(), sys->precision, sys->m, sys->xd, sys->r, sys->stream);
         CK(cudaMemcpyAsync(y, sys->r, (size_t)sys->m * 8, cudaMemcpyDeviceToHost, sys->stream));
@@ -1664,6 +1708,7 @@ asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y
 asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x, double* y) {
     if (!sys || !x || !y) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
+        mon_wait(sys, sys->stream);
         CK(cudaMemcpyAsync(sys->r, x, (size_t)sys->m * 8, cudaMemcpyHostToDevice, sys->stream));
         launch_spmv_cols(sys->csc(), sys->precision, sys->n, sys->r, sys->g, sys->stream);
         CK(cudaMemcpyAsync(y, sys->g, (size_t)sys->n * 8, cudaMemcpyDeviceToHost, sys->stream));
@@ -1895,6 +1940,7 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     if (cfg->epochs < 0 || cfg->snapshot_interval < 1)
         return fail(ASYRK_E_InvalidArgument, "epochs must be >= 0 and snapshot_interval >= 1");
     cudaStream_t st = s->stream;
+    mon_wait(s, st);
     AllocStream as(st);
     h->threads = cfg->threads;
     h->gamma = cfg->gamma;
