@@ -75,6 +75,7 @@ struct asyrk_system {
 
     // solve state
     void* x = nullptr;        // X[n]
+    void* x_base = nullptr;   // allocation holding x (x may be offset inside it, ASYRK_X_ALIGN)
     double* xd = nullptr;     // fp64 staging (x0, export, det x)
     void* shadow = nullptr;
     double* x0d = nullptr;
@@ -237,7 +238,7 @@ void free_all(asyrk_system* s) {
     F(s->csc_row);
     F(s->csc_val);
     F(s->alias);
-    F(s->x);
+    F(s->x_base ? s->x_base : s->x);
     F(s->xd);
     F(s->shadow);
     F(s->x0d);
@@ -418,7 +419,21 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     // Overlapped build: the host scan of row lengths runs on a thread, and the
     // column sort (CSC / SELL-columns, needs only row_ptr + col_idx) runs on an
     // aux stream while the values are still being staged (runtime.h Stager).
-    s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
+    {
+        // x starts on a 2 MB page boundary: the workers' random gathers and reds
+        // cover x uniformly, and an x straddling a page boundary measured 2-3%
+        // slower at config 2 (ASYRK_X_ALIGN / ASYRK_X_OFFSET: placement experiments)
+        static const long long xa = getenv("ASYRK_X_ALIGN") ? atoll(getenv("ASYRK_X_ALIGN")) : (2ll << 20);
+        static const long long xo = getenv("ASYRK_X_OFFSET") ? atoll(getenv("ASYRK_X_OFFSET")) : 0;
+        if (xa > 0) {
+            unsigned char* base = dalloc<unsigned char>((size_t)A->n * s->xbytes() + (size_t)xa + (size_t)xo);
+            const uintptr_t u = ((uintptr_t)base + (uintptr_t)xa - 1) / (uintptr_t)xa * (uintptr_t)xa + (uintptr_t)xo;
+            s->x_base = base;
+            s->x = reinterpret_cast<void*>(u);
+        } else {
+            s->x = dalloc<unsigned char>((size_t)A->n * s->xbytes());
+        }
+    }
     s->xd = dalloc<double>((size_t)A->n);
     s->x0d = dalloc<double>((size_t)A->n);
     s->r = dalloc<double>((size_t)A->m);
