@@ -124,3 +124,20 @@ def test_lsq_golden_vectors_pin_the_reference(golden):
         assert abs(g - golden[p + "scal"][0]) <= 1e-9 + 1e-6 * g, nm
         if nm != "l30x12_explicit":  # (10 epochs: not converged by design)
             assert np.linalg.norm(x - np.linalg.lstsq(D, golden[p + "b"], rcond=None)[0]) <= 1e-6, nm
+
+
+def test_dense_and_lsq_argument_errors_without_a_gpu():
+    # checks that precede any device work (include/asyrk_dense.h): the dense SVD's
+    # size cap, lsq_solve's sigma rules (lsq.cpp:110-129) and its input checks
+    A, b, _ = capi.generate_fixed_theta(3000, 1500, 4, seed=2)  # 4.5e6 cells > SolutionProjector cap
+    with pytest.raises(capi.AsyrkError, match="TooLarge"):
+        capi.dense_svd(A, max_cells=1000)
+    with pytest.raises(capi.AsyrkError, match="SigmaUnavailable"):
+        capi.lsq_solve(A, b, max_epochs=1)
+    with pytest.raises(capi.AsyrkError, match="NonPositiveSigma"):
+        capi.lsq_solve(A, b, sigma_r=0.0, max_epochs=1)
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.lsq_solve(A, b[:-1], sigma_r=0.5, max_epochs=1)
+    raw = capi.HostCsr(2, 2, [0, 1, 2], [0, 1], [2.0, 1.0])
+    with pytest.raises(capi.AsyrkError, match="NotNormalized"):
+        capi.lsq_solve(raw, np.ones(2), sigma_r=0.5, max_epochs=1)
