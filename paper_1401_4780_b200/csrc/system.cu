@@ -1882,6 +1882,11 @@ struct asyrk_mrhs {
     uint64_t seed = 0;
     long long chunks = 0, max_chunks = 0;
     asyrk_solve_stats stats{};
+    // stop checks one commit behind: commit k records commit_ev[k & 1] on the
+    // solve stream; a chunk queued after a stopping commit sees the device
+    // stop flag and returns at once (same stream), so nothing needs undoing
+    cudaEvent_t commit_ev[2] = {nullptr, nullptr};
+    long long commits = 0;
 };
 
 namespace {
@@ -1914,6 +1919,8 @@ MrhsArgs mrhs_args(asyrk_mrhs* h) {
 
 void mrhs_free(asyrk_mrhs* h) {
     if (!h) return;
+    for (cudaEvent_t e : h->commit_ev)
+        if (e) cudaEventDestroy(e);
     if (h->sys) {
         cudaStream_t st = h->sys->stream;
         for (void* p : {(void*)h->X, (void*)h->B, (void*)h->R, (void*)h->Xstar, (void*)h->part, (void*)h->norms})
@@ -1972,6 +1979,9 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     h->gamma = cfg->gamma;
     h->seed = cfg->seed;
     h->chunks = 0;
+    h->commits = 0;
+    for (cudaEvent_t& e : h->commit_ev)
+        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     h->max_chunks = cfg->epochs > 0 ? (cfg->epochs + cfg->snapshot_interval - 1) / cfg->snapshot_interval : 0;
     h->stats = asyrk_solve_stats{};
     ensure_records(s, std::max<long long>(256, h->max_chunks + 2));
@@ -2080,6 +2090,8 @@ asyrk_status asyrk_mrhs_commit(asyrk_mrhs* h, int32_t advance) {
     if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
     return guarded([&] {
         launch_mrhs_commit(mrhs_args(h), advance, h->sys->stream);
+        CK(cudaEventRecord(h->commit_ev[h->commits & 1], h->sys->stream));
+        h->commits++;
         h->stats.kernel_launches += 1;
         CK(cudaGetLastError());
         return ASYRK_OK;
@@ -2094,7 +2106,11 @@ asyrk_status asyrk_mrhs_step(asyrk_mrhs* h) {
 asyrk_status asyrk_mrhs_stopped(asyrk_mrhs* h, int32_t* stopped) {
     if (!h || !stopped) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
-        CK(cudaStreamSynchronize(h->sys->stream));
+        // the previous commit's decision (the latest one right after begin)
+        if (h->commits >= 2)
+            CK(cudaEventSynchronize(h->commit_ev[(h->commits - 2) & 1]));
+        else
+            CK(cudaStreamSynchronize(h->sys->stream));
         *stopped = *reinterpret_cast<volatile int*>(h->sys->host_flag) ? 1 : 0;
         if (h->chunks >= h->max_chunks) *stopped = 1;
         return ASYRK_OK;
