@@ -315,7 +315,10 @@ asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t pr
  *   loop { step -> [all-reduce(norms, sum)] -> commit(1) -> stopped? } -> finish
  * norms is a device double[3] = this shard's {||R||_F^2, ||A^T R||_F^2,
  * ||X - X*||_F^2}; after the all-reduce every rank takes the same global stop
- * decision (r_sq <= target_r_sq) on the device. */
+ * decision (r_sq <= target_r_sq) on the device. stopped() reports the
+ * decision of the previous commit (of the only one right after begin), so
+ * the host stays one chunk ahead; a chunk queued after the stopping commit
+ * sees the device stop flag and returns without touching X. */
 typedef struct asyrk_mrhs asyrk_mrhs;
 asyrk_status asyrk_mrhs_create(const asyrk_csr_view* A, const float* B, int64_t k_total, int64_t c0, int64_t c1,
                                void* stream, asyrk_mrhs** out);
