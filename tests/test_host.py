@@ -204,3 +204,22 @@ def test_cpp_drop_in_caller_compiles_against_the_headers(tmp_path):
     # a reference-style C++ caller (tests/cpp/drop_in_caller.cpp) builds against
     # include/asyrk/*.hpp and links libasyrk_b200.so (run on the GPU in test_gpu_parity.py)
     assert os.path.exists(_build_drop_in_caller(tmp_path))
+
+
+def test_bench_reference_arm_json_contract():
+    # bench.py --impl reference runs the reference's own CPU path (oracle/_ref)
+    # and prints one JSON line with the contract's keys (a CPU-only workload here)
+    import json
+    import subprocess
+    import sys
+    ref = os.path.join(ROOT, "oracle", "_ref", "libasyrk_ref.so")
+    if not os.path.exists(ref):
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", "mc",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, check=True)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ["metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"]:
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "reference"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
