@@ -47,6 +47,21 @@ def test_single_gpu_all_columns_converge(problem):
     S.close()
 
 
+def test_config5_full_size_all_columns():
+    # BASELINE config 5 at full size on one GPU: 500k x 250k, theta 20, k = 64
+    # fp32 right-hand sides -> global ||R||_F / ||B||_F < 1e-5, error within 10x
+    A, B, Xs = capi.generate_fixed_theta(500000, 250000, 20, seed=1005, k=64)
+    B = B.astype(np.float32)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    S = capi.MultiRHS(A, B, 0, 64)
+    t = S.solve(threads=4096, epochs=400, target=TOL * TOL * bb, seed=3, X_star=Xs)
+    S.close()
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    assert np.sqrt(t["dist_sq"][-1]) / np.linalg.norm(Xs) <= 10 * TOL
+    R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL  # independent fp64 evaluation
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_sharded_protocol_global_stop(problem, world):
     A, B, Xs = problem

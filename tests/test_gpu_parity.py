@@ -228,6 +228,19 @@ def test_config2_async_reaches_tolerance():
     S.close()
 
 
+def test_config3_full_size_fp32():
+    # BASELINE config 3 at full size: 2M x 1M, theta 50, U(-1,1) values, fp32 x
+    # and atomics, all resident warps -> rel residual 1e-5, error within 10x
+    A, b, xs = capi.generate_fixed_theta(2000000, 1000000, 50, seed=1003, dist="uniform")
+    bb = float(b @ b)
+    with capi.System(A, b, precision=capi.F32) as S:
+        t = S.solve(threads=S.max_resident_warps(capi.F32), epochs=300, target=1e-10 * bb,
+                    sampling=capi.SLICE_SHUFFLE, seed=1, precision=capi.F32, x_star=xs, want_x=False)
+    rel = _rel(t, b)
+    err = float(np.sqrt(t["dist_sq"][-1] / float(xs @ xs)))
+    assert rel <= 1e-5 and err <= 1e-4, (rel, err)
+
+
 def test_config3_fp32_and_fp64x():
     # BASELINE config 3 shape at 1/10 scale: U(-1,1) values, fp32 x / fp32 atomics, and fp64-x variant
     A, b, xs = capi.generate_fixed_theta(200000, 100000, 50, seed=1003, dist="uniform")
@@ -242,9 +255,11 @@ def test_config3_fp32_and_fp64x():
         S.close()
 
 
-def test_config4_alias_sampling_raw_rows():
-    # BASELINE config 4 shape at 1/4 scale: rows scaled log-uniform in [0.1, 10], P(i) ~ ||a_i||^2
-    A, b, xs = capi.generate_fixed_theta(100000, 25000, 25, seed=1004, scale_decades=1.0)
+@pytest.mark.parametrize("m,n", [(100000, 25000), (400000, 100000)])
+def test_config4_alias_sampling_raw_rows(m, n):
+    # BASELINE config 4 (full size, and at 1/4 scale): rows scaled log-uniform in
+    # [0.1, 10], P(i) ~ ||a_i||^2
+    A, b, xs = capi.generate_fixed_theta(m, n, 25, seed=1004, scale_decades=1.0)
     assert not A.normalized
     S = capi.System(A, b)
     bb = float(b @ b)
