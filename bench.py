@@ -244,7 +244,7 @@ def run_gpu(args):
     # the latest epoch boundary it can, so the workers never wait for it
     W = args.warps or S.max_resident_warps()
     lam, lam_iters = S.power_iteration(1e-6)  # stats.cpp:15-50 on the device; tau bound beside the warp count
-    flush =torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     solve_kw = dict(threads=W, gamma=1.0, epochs=2000, target=target, sampling=capi.SLICE_SHUFFLE,
                     snapshot_interval=1, want_x=False)
 
