@@ -41,22 +41,33 @@ METRIC = "Kaczmarz row projections/sec; time to ||Ax-b||/||b||<1e-6 vs CPU AsyRK
 CFG2 = dict(m=200000, n=100000, theta=30, seed=1002)
 TOL = 1e-6
 BYTES_PER_PROJ_F64 = 864  # S_A 384 + x gather 240 + atomic payload 240
+S_A_F64 = 384             # A stream per projection: 16 B header + 30 x (8 B value + 4 B column), record-padded
+X_BYTES_F64 = 480         # x side per projection: 30 gathered + 30 reduced doubles (L2-resident x)
 L2_FLUSH_BYTES = 256 << 20
 
 
-def workload_config(W, extra=None):
-    c = {
+def workload_config():
+    """The workload both arms run (identical dict on both lines; run-specific
+    parameters such as warp / thread counts go to the sibling key "run")."""
+    return {
         "workload": "config2: m=200000 n=100000 theta=30 N(0,1) unit rows fp64, x0=0, async to ||r||/||b||<1e-6",
-        "sampling": "slice_shuffle (per-warp row slices reshuffled every epoch; the reference default)",
+        "sampling": "slice_shuffle (per-worker row slices reshuffled every epoch; the reference default)",
         "gamma": 1.0,
         "snapshot_interval": 1,
-        "warps": W,
-        "l2": "flushed before every step (256 MiB write); A (75 MB records) re-read from HBM each step",
+        "instance_seed": CFG2["seed"],
         "x0": "zeros",
+        "l2": "GPU arm: 256 MiB L2 flush before every step (A, 75 MB of records, re-read from HBM each step)",
     }
-    if extra:
-        c.update(extra)
-    return c
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 class ClockSampler:
@@ -124,12 +135,12 @@ def measured_peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """dram read+write bytes per worker launch from the committed ncu capture, or None."""
+def ncu_summary():
+    """Per-launch ncu counters of the worker (K2) from the committed capture
+    (profiles/worker_ncu_summary.json, made by scripts/ncu_summary.py), or None."""
     p = os.path.join(ROOT, "profiles", "worker_ncu_summary.json")
     try:
-        d = json.load(open(p))
-        return d.get("dram_bytes_per_launch")
+        return json.load(open(p))
     except Exception:
         return None
 
@@ -138,6 +149,15 @@ def gen_system(seed):
     from paper_1401_4780_b200 import capi
 
     return capi.generate_fixed_theta(CFG2["m"], CFG2["n"], CFG2["theta"], seed=seed)
+
+
+def gen_system_ref(seed, **kw):
+    """The same instance for the reference arm, built by the C restatement of the
+    generator (oracle/workload.c, pinned bit for bit to the product generator by
+    tests/test_oracle.py) so the product library never maps into that process."""
+    import oracle
+
+    return oracle.C.generate_fixed_theta(CFG2["m"], CFG2["n"], CFG2["theta"], seed=seed, **kw)
 
 
 # --------------------------------------------------------------------------- reference arm
@@ -180,7 +200,7 @@ def run_reference(args):
     if R is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built and reference sources absent"}))
         return 0
-    A, b, xs = gen_system(CFG2["seed"])
+    A, b, xs = gen_system_ref(CFG2["seed"])
     Ah = ref_matrix(R, A)
     target = TOL * TOL * float(b @ b)
     cores = host_cores()
@@ -193,7 +213,7 @@ def run_reference(args):
         wall += w
         ttt.append(w)
     value = proj / wall
-    cpu = {"value": value, "unit": "proj/s", "cores": cores, "kind": "reference",
+    cpu = {"value": value, "unit": "proj/s", "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
            "sample": f"{args.steps} full config-2 solves to 1e-6 (reference solve_parallel, {cores} threads, "
                      "slice_shuffle, gamma=1, snapshot_interval=1)"}
     # the rest of SURVEY §8(d)'s CPU protocol, reported beside the line: T = 1
@@ -209,7 +229,9 @@ def run_reference(args):
         "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
-        "config": workload_config(cores, {"threads": cores, "warps": None, "cpu_protocol": protocol}),
+        "config": workload_config(),
+        "run": {"threads": cores, "cpu_model": cpu_model(), "cpu_protocol": protocol,
+                "instance": "oracle/workload.c (C restatement of the product generator, bitwise-pinned)"},
         "time_to_tolerance_ms": 1e3 * statistics.median(ttt), "epochs": int(t["epoch_index"][-1]),
         "cpu_baseline": cpu, "e2e": {"value": value, "unit": "proj/s", "h2d_bytes_per_step": 0,
                                      "d2h_bytes_per_step": 0},
@@ -233,6 +255,8 @@ def run_gpu(args):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     A, b, xs = gen_system(CFG2["seed"] + rank)
@@ -240,8 +264,7 @@ def run_gpu(args):
     target = TOL * TOL * bb
     stream = torch.cuda.Stream()
     S = capi.System(A, b, stream=stream.cuda_stream)
-    # all resident warp slots: the residual monitor runs on its own stream and takes
-    # the latest epoch boundary it can, so the workers never wait for it
+    # all resident warp slots
     W = args.warps or S.max_resident_warps()
     lam, lam_iters = S.power_iteration(1e-6)  # stats.cpp:15-50 on the device; tau bound beside the warp count
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
@@ -256,6 +279,7 @@ def run_gpu(args):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     stats = []
     epochs = []
+    records = []
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -268,6 +292,7 @@ def run_gpu(args):
             ev[k][1].record(stream)
             stats.append(S.stats())
             epochs.append(int(r["epoch_index"][-1]))
+            records.append(len(r["epoch_index"]))
             rel = float(np.sqrt(r["r_sq"][-1] / bb))
             if not rel < TOL:
                 raise RuntimeError(f"step {k} stopped at relative residual {rel} (epochs {epochs[-1]})")
@@ -290,8 +315,24 @@ def run_gpu(args):
         dev_ms_max, proj_all = dev_ms, float(proj)
     value = proj_all / (dev_ms_max * 1e-3)
 
+    # ---- instrumented drop-in call (the reference's Python solve_parallel always
+    # passes &rep, module.cpp:190-191): the same solve with the increment audit on
+    instr_ms = []
+    for k in range(-1, min(args.steps, 10)):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ri = S.solve(seed=3000 + k, instrument=True, **solve_kw)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if k >= 0:
+            instr_ms.append(e0.elapsed_time(e1))
+        if not ri["instrument"]["consistent"]:
+            raise RuntimeError("instrumented solve failed the increment audit")
+
     # ---- e2e: one-shot C-ABI call with host buffers (one untimed warm-up call)
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = args.steps
     e2e_wall = 0.0
     e2e_proj = 0
     e2e_calls = []
@@ -316,36 +357,38 @@ def run_gpu(args):
     h2d = 8 * (A.m + 1) + 12 * A.nnz + 8 * A.m + 8 * A.m
     d2h = 8 * A.n + 48 * (max(epochs) + 2)  # final_x + trace records
 
+    # ---- config 5 (the sharded configuration) at this N: k = 64 RHS split over the ranks
+    c5 = None
+    if not args.no_cfg5:
+        c5 = cfg5_sharded(max(2, min(args.steps, 5)), 1, dist, rank, world, local, stream)
+
     out = None
     if rank == 0:
-        peak, peak_kind = measured_peak_hbm()
         avg_launch_ms = w_ms / max(w_launch, 1)
-        proj_per_launch = CFG2["m"]
-        achieved = BYTES_PER_PROJ_F64 * proj_per_launch / (avg_launch_ms * 1e-3) / 1e9
-        traffic = ncu_traffic()
+        worker_rate = proj / (w_ms * 1e-3)  # credited projections / worker time: discarded epochs count as time
         out = {
             "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(W, {"resident_warps": stats[0]["resident_warps"],
-                                          "lambda_max": lam, "tau_max": CFG2["m"] / (2 * np.e * lam) - 1,
-                                          "parallelism": f"replicas x{world}"}),
+            "config": workload_config(),
+            "run": {"warps": W, "resident_warps": stats[0]["resident_warps"], "lambda_max": lam,
+                    "tau_max": CFG2["m"] / (2 * np.e * lam) - 1, "rows_in_flight": 2 * W,
+                    "parallelism": f"replicas x{world} (config 2 is one system: x is not sharded)"},
             "time_to_tolerance_ms": statistics.median(step_ms), "epochs": statistics.median(epochs),
+            "records_per_solve": statistics.median(records),
+            "worker_launches_per_solve": w_launch / args.steps,
             "e2e": {"value": e2e_proj / e2e_wall, "unit": "proj/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_wall / e2e_steps, "calls_ms": e2e_calls},
+            "instrumented": {"ms_per_solve": statistics.median(instr_ms),
+                             "ratio_vs_uninstrumented": statistics.median(instr_ms) / statistics.median(step_ms),
+                             "call": "System.solve(..., instrument=True): the increment audit of "
+                                     "solve_parallel's InstrumentReport (parallel.cpp:94-106)"},
             "gpu_launches": launches,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "asyrk worker (K2)", "bytes_per_proj": BYTES_PER_PROJ_F64,
-                         "avg_launch_ms": avg_launch_ms, "peak_source": peak_kind,
-                         "worker_share_of_step": w_ms / dev_ms},
-            "worker_proj_per_s": proj / (w_ms * 1e-3),
-            # R_proj = min(BW_HBM / S_A, R_x); R_x = the x-side traffic alone
-            # (30 random L2 gathers -> warp reduce -> 30 random red.add.f64 per projection),
-            # measured here at the same warp count and x footprint
-            "x_roofline": x_roofline(W, proj / (w_ms * 1e-3), statistics.median(epochs), dev_ms_max / args.steps),
+            "roofline": roofline(W, worker_rate, avg_launch_ms, value),
             "clocks": clk.summary(),
         }
+        if c5 is not None:
+            out["cfg5_sharded"] = c5
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(A, b)
     if dist:
@@ -357,33 +400,43 @@ def run_gpu(args):
     return 0
 
 
-def x_roofline(W, worker_rate, epochs, step_ms):
+def roofline(W, worker_rate, avg_launch_ms, step_rate):
+    """The binding ceiling of K2: R_proj = min(BW_HBM / S_A, R_x),
+    R_x = the x-side traffic of a projection alone (30 random L2 gathers ->
+    warp reduce -> 30 random red.add.f64), measured live at the worker's warp
+    count and x footprint, with 1 and 2 rows in flight per warp. Expressed in
+    GB/s of x-side L2 traffic (480 B per projection) so the unit matches the
+    contract; the proj/s figures sit beside it."""
     from paper_1401_4780_b200 import capi
 
-    rx = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 0) for _ in range(3))
-    peak, _ = measured_peak_hbm()
-    r_hbm = peak * 1e9 / 384.0  # A stream: 16 B header + 30 x (8 B value + 4 B column), record-padded
+    rx1 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 0) for _ in range(3))
+    rx2 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 16) for _ in range(3))
+    rx = max(rx1, rx2)
+    peak_hbm, hbm_kind = measured_peak_hbm()
+    r_hbm = peak_hbm * 1e9 / S_A_F64
     r_proj = min(r_hbm, rx)
-    out = {"R_x_proj_per_s": rx, "R_hbm_proj_per_s": r_hbm, "R_proj": r_proj,
-           "achieved_proj_per_s": worker_rate, "frac": worker_rate / r_proj,
-           "mode": "dependent gather->reduce->red.add.f64, theta=30, n=100000",
-           "note": "the worker shares the L2 request budget with the overlapped residual monitor; "
-                   "see l2_request_roofline for the whole step"}
-    # whole step against the same ceiling: L2 requests per epoch of the worker and the two
-    # monitor passes (ncu, profiles/worker_ncu_summary.json) per second of step time, vs the
-    # request rate the x-side microbenchmark sustains (R_x x the worker's requests/projection)
-    try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "worker_ncu_summary.json")))
-        req = d["lts_requests_per_launch"]
-        per_proj = req["worker"] / d["projections_per_launch"]
-        per_epoch = req["worker"] + req.get("rows", 0) + req.get("cols", 0)
-        achieved = per_epoch * epochs / (step_ms * 1e-3)
-        ceiling = rx * per_proj
-        out["l2_request_roofline"] = {"requests_per_epoch": per_epoch, "worker_requests_per_proj": per_proj,
-                                      "achieved_requests_per_s": achieved, "ceiling_requests_per_s": ceiling,
-                                      "frac": achieved / ceiling, "source": "ncu lts__t_requests.sum (r01 capture)"}
-    except Exception:
-        pass
+    ncu = ncu_summary()
+    dram = ncu.get("dram_bytes_per_launch") if ncu else None
+    out = {"bound": "l2_atomic", "unit": "GB/s",
+           "achieved": worker_rate * X_BYTES_F64 / 1e9, "peak": r_proj * X_BYTES_F64 / 1e9,
+           "frac": worker_rate / r_proj, "traffic": dram,
+           "kernel": "K2 worker_kernel (csrc/worker.cu)",
+           "achieved_proj_per_s": worker_rate, "peak_proj_per_s": r_proj,
+           "R_x_proj_per_s": {"rows_in_flight_1": rx1, "rows_in_flight_2": rx2},
+           "R_hbm_proj_per_s": r_hbm,
+           "step_frac": step_rate / r_proj,
+           "peak_source": "x-side microbenchmark (asyrk_microbench_xside) measured live in this run, the faster of "
+                          "1 and 2 rows in flight per warp; ncu counters of it in profiles/",
+           "achieved_source": "credited projections / CUDA-event time of the worker launches (K2) in the timed steps",
+           "avg_worker_launch_ms": avg_launch_ms,
+           "x_bytes_per_proj": X_BYTES_F64, "alg_bytes_per_proj": BYTES_PER_PROJ_F64}
+    # the A stream against HBM: algorithmic 384 B/projection vs ncu DRAM bytes
+    alg_launch = S_A_F64 * CFG2["m"]
+    out["hbm"] = {"achieved": alg_launch / (avg_launch_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s",
+                  "frac": alg_launch / (avg_launch_ms * 1e-3) / 1e9 / peak_hbm, "peak_source": hbm_kind,
+                  "alg_bytes_per_launch": alg_launch, "dram_bytes_per_launch": dram,
+                  "traffic_over_alg": (dram / alg_launch) if dram else None,
+                  "source": ncu.get("source") if ncu else None}
     return out
 
 
@@ -395,7 +448,7 @@ def cpu_baseline(A, b):
     cores = host_cores()
     target = TOL * TOL * float(b @ b)
     p, w, t = ref_solve_once(R, Ah, b, cores, target)
-    return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference",
+    return {"value": p / w, "unit": "proj/s", "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
             "sample": f"1 full config-2 solve to 1e-6 ({int(t['epoch_index'][-1])} epochs, {w:.2f} s) with the "
                       f"reference solve_parallel, {cores} threads, slice_shuffle",
             "time_to_tolerance_ms": 1e3 * w}
@@ -405,13 +458,91 @@ CFG5 = dict(m=500000, n=250000, theta=20, k=64, seed=1005)
 TOL5 = 1e-5
 
 
-def run_gpu_cfg5(args):
-    """BASELINE config 5: k=64 right-hand sides sharded by column over the ranks,
-    NCCL all-reduce of the shard residual norms as the global stop test."""
+def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
+    """BASELINE config 5 at this job's N: k=64 right-hand sides split into N
+    contiguous column shards, one per rank (A replicated), each rank's
+    lock-free warp-workers on its shard, and one NCCL all-reduce of the shard
+    residual norms per snapshot as the global stop test (paper_1401_4780_b200/
+    mrhs.py). Returns the summary on rank 0 (None elsewhere)."""
     import torch
 
     from paper_1401_4780_b200 import capi
     from paper_1401_4780_b200.mrhs import CudaShardBackend, shard_columns, solve_sharded
+
+    A, B, Xs = capi.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"], k=CFG5["k"])
+    B = B.astype(np.float32)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    c0, c1 = shard_columns(CFG5["k"], world, rank)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    with torch.cuda.stream(stream):
+        be = CudaShardBackend(A, B, c0, c1, stream=stream.cuda_stream)
+        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1)
+        for w in range(warmup):
+            flush.zero_()
+            solve_sharded(be, seed=100 + w, **kw)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        rows, epochs, records = 0, [], []
+        with ClockSampler(local) as clk:
+            for k in range(steps):
+                flush.zero_()
+                ev[k][0].record(stream)
+                t = solve_sharded(be, seed=1000 + k, **kw)
+                ev[k][1].record(stream)
+                rows += int(t["updates_applied"][-1])
+                epochs.append(int(t["epoch_index"][-1]))
+                records.append(len(t["epoch_index"]))
+                rel = float(np.sqrt(t["r_sq"][-1] / bb))
+                if not rel < TOL5:
+                    raise RuntimeError(f"config 5 step {k} stopped at relative residual {rel}")
+            torch.cuda.synchronize()
+        stats = be.impl.stats()
+        # the stop test's collective alone: all-reduce of the 3 shard norms, device time
+        ar_us = 0.0
+        if dist:
+            nt = be.norms()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            for _ in range(10):
+                dist.all_reduce(nt)
+            e0.record(stream)
+            for _ in range(200):
+                dist.all_reduce(nt)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ar_us = 1e3 * e0.elapsed_time(e1) / 200
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(c) for a, c in ev]
+    dev_ms = sum(step_ms)
+    col_proj = rows * (c1 - c0)  # one row event projects every owned RHS column
+    if dist:
+        t = torch.tensor([dev_ms, ar_us], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, ar_us = float(t[0].item()), float(t[1].item())
+        t = torch.tensor([float(col_proj)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        col_proj = float(t.item())
+    be.close()
+    if rank != 0:
+        return None
+    return {"metric": "config 5 column projections/sec (row projections x owned RHS columns, all ranks)",
+            "value": col_proj / (dev_ms * 1e-3), "unit": "proj/s", "n_gpus": world, "steps": steps,
+            "ms_per_step": dev_ms / steps, "time_to_tolerance_ms": statistics.median(step_ms),
+            "epochs": statistics.median(epochs), "records_per_solve": statistics.median(records),
+            "allreduce_us_per_epoch": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
+            "worker_launches": stats["worker_launches"], "kernel_launches": stats["kernel_launches"],
+            "workload": "config5: m=500000 n=250000 theta=20 k=64 fp32, RHS columns sharded over the ranks, "
+                        "all-reduced stop at ||R||_F/||B||_F<1e-5",
+            "warps": W, "clocks": clk.summary()}
+
+
+def run_gpu_cfg5(args):
+    """BASELINE config 5 as its own line (bench.py --workload cfg5)."""
+    import torch
+
+    from paper_1401_4780_b200 import capi
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -422,75 +553,39 @@ def run_gpu_cfg5(args):
     if world > 1:
         import torch.distributed as dist
 
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    A, B, Xs = capi.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"], k=CFG5["k"])
-    B = B.astype(np.float32)
-    bb = float((B.astype(np.float64) ** 2).sum())
-    c0, c1 = shard_columns(CFG5["k"], world, rank)
     stream = torch.cuda.Stream()
-    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    W = args.warps or 4096
-    with torch.cuda.stream(stream):
-        be = CudaShardBackend(A, B, c0, c1, stream=stream.cuda_stream)
-        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1)
-        for w in range(args.warmup):
-            flush.zero_()
-            solve_sharded(be, seed=100 + w, **kw)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        rows, epochs = 0, []
-        with ClockSampler(local) as clk:
-            for k in range(args.steps):
-                flush.zero_()
-                ev[k][0].record(stream)
-                t = solve_sharded(be, seed=1000 + k, **kw)
-                ev[k][1].record(stream)
-                rows += int(t["updates_applied"][-1])
-                epochs.append(int(t["epoch_index"][-1]))
-                rel = float(np.sqrt(t["r_sq"][-1] / bb))
-                if not rel < TOL5:
-                    raise RuntimeError(f"step {k} stopped at relative residual {rel}")
-            torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    dev_ms = sum(a.elapsed_time(c) for a, c in ev)
-    col_proj = rows * (c1 - c0)  # one row event projects every owned RHS column
-    if dist:
-        t = torch.tensor([dev_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dev_ms = float(t.item())
-        t = torch.tensor([float(col_proj)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        col_proj = float(t.item())
+    c5 = cfg5_sharded(args.steps, args.warmup, dist, rank, world, local, stream, W=args.warps or 4096)
     if rank == 0:
-        cpu = None
+        line = {"metric": METRIC + " (config 5: column projections/sec)", "value": c5["value"], "unit": "proj/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": c5["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": {"workload": c5["workload"]},
+                "run": {"warps": c5["warps"], "columns_per_gpu": c5["columns_per_gpu"],
+                        "parallelism": f"rhs-shard x{world}"},
+                "time_to_tolerance_ms": c5["time_to_tolerance_ms"], "epochs": c5["epochs"],
+                "allreduce_us_per_epoch": c5["allreduce_us_per_epoch"], "clocks": c5["clocks"]}
         if world == 1 and not args.no_cpu_baseline:
+            import oracle  # noqa: F401  (the reference's CPU path on a bounded sample)
+
             R = load_ref()
             if R is not None:  # the reference solves one RHS at a time: 1 epoch of column 0 on all host threads
+                A, B, _ = oracle.C.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"],
+                                                        k=CFG5["k"])
                 Ah = ref_matrix(R, A)
                 cores = host_cores()
-                bn = B[:, 0].astype(np.float64)
+                bn = B[:, 0].astype(np.float32).astype(np.float64)
                 t = R.solve_parallel(Ah, bn, np.zeros(A.n), threads=cores, gamma=1.0, epochs=1, target=0.0,
                                      variant="full_row", sampling="with_replacement", seed=7, snapshot_interval=1,
                                      cap=4)
-                cpu = {"value": int(t["updates_applied"][-1]) / float(t["wall_seconds"][-1]), "unit": "proj/s",
-                       "cores": cores, "kind": "reference",
-                       "sample": "1 epoch of solve_parallel (fp64) on RHS column 0; the reference solves the 64 "
-                                 "columns one after another"}
-        print(json.dumps({
-            "cpu_baseline": cpu,
-            "metric": METRIC + " (config 5: column projections/sec)", "value": col_proj / (dev_ms * 1e-3),
-            "unit": "proj/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config5: m=500000 n=250000 theta=20 k=64 fp32, RHS columns sharded, "
-                                   "NCCL all-reduce stop at ||R||_F/||B||_F<1e-5",
-                       "warps": W, "columns_per_gpu": c1 - c0, "parallelism": f"rhs-shard x{world}"},
-            "time_to_tolerance_ms": dev_ms / args.steps, "epochs": statistics.median(epochs),
-            "clocks": clk.summary()}))
-    be.close()
+                line["cpu_baseline"] = {
+                    "value": int(t["updates_applied"][-1]) / float(t["wall_seconds"][-1]), "unit": "proj/s",
+                    "cores": cores, "kind": "reference", "cpu_model": cpu_model(),
+                    "sample": "1 epoch of solve_parallel (fp64) on RHS column 0; the reference solves the 64 "
+                              "columns one after another"}
+        print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
     return 0
@@ -645,7 +740,7 @@ def run_sweep(args):
                        "rel_error": float(np.sqrt(t["dist_sq"][-1] / float(xs @ xs)))})
     S.close()
     print(json.dumps({"metric": METRIC + " (warp sweep)", "unit": "proj/s", "n_gpus": 1, "data": "synthetic",
-                      "dtype": "f64", "config": {"workload": workload_config(None)["workload"],
+                      "dtype": "f64", "config": {"workload": workload_config()["workload"],
                                                  "lambda_max": lam, "tau_max": tau_max,
                                                  "resident_warps": res}, "points": points}))
     return 0
@@ -884,6 +979,7 @@ def main():
     ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5", "mc", "cfg1", "cfg3", "cfg3x", "cfg4",
                                                            "sweep", "cfg5shards", "lsq"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the config-5 (RHS-sharded) sub-line of the cfg2 run")
     args = ap.parse_args()
     if args.workload == "mc":
         return run_mc(args)

@@ -339,7 +339,8 @@ asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out);
 /* ---- measurement ------------------------------------------------------- */
 /* x-side roofline R_x: theta random gathers of an n-element
  * x, a warp reduction, theta random red.global.add per "projection", no A
- * stream. mode 0 dependent gather->red, 1 gathers only, 2 reds only. */
+ * stream. mode 0 dependent gather->red, 1 gathers only, 2 reds only; mode + 16
+ * keeps 2 rows in flight per warp (the K2 worker's shape). */
 asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t precision, int32_t warps,
                                     int64_t proj_per_warp, int32_t mode, double* proj_per_s, double* kernel_ms);
 

@@ -147,6 +147,23 @@ class Csr:
             pass
 
 
+@dataclass
+class Instance:
+    """Host CSR arrays of a generated instance (the fields of capi.HostCsr)."""
+
+    m: int
+    n: int
+    row_ptr: np.ndarray
+    col_idx: np.ndarray
+    values: np.ndarray
+    row_norm: np.ndarray
+    normalized: bool
+
+    @property
+    def nnz(self):
+        return int(self.row_ptr[-1])
+
+
 class _Lib:
     kind = "?"
 
@@ -539,11 +556,35 @@ class _OracleLib(_Lib):
         L.oc_monte_carlo.argtypes = [C_.c_void_p, _f64p, _f64p, C_.c_double, C_.c_int64, C_.c_int, C_.c_int64,
                                      C_.c_int64, C_.c_uint64, C_.c_int, _f64p, _f64p]
         L.oc_rate_fit.argtypes = [_f64p, C_.c_int64, C_.c_double, _f64p, _f64p]
+        L.oc_generate_fixed_theta.argtypes = [C_.c_int64, C_.c_int64, C_.c_int64, C_.c_uint64, C_.c_int32,
+                                              C_.c_double, C_.c_int64, C_.c_int32, _i64p, _i64p, _f64p, _f64p,
+                                              _f64p, _f64p, C_.POINTER(C_.c_int32)]
+        L.oc_generate_fixed_theta.restype = C_.c_int
 
     @staticmethod
     def _check(st):
         if st:
             raise OracleError(st)
+
+    def generate_fixed_theta(self, m, n, theta, seed, dist="normal", scale_decades=0.0, k=1, threads=0):
+        """The benchmark instance generator restated in C (oracle/workload.c), so the
+        reference arm builds its instance without the product library. Returns
+        (Instance, b, x_star) with the arrays of capi.generate_fixed_theta."""
+        nnz = m * theta
+        rp = np.zeros(m + 1, np.int64)
+        ci = np.zeros(nnz, np.int64)
+        v = np.zeros(nnz)
+        rn = np.zeros(m)
+        b = np.zeros(m * k)
+        xs = np.zeros(n * k)
+        norm = C_.c_int32(0)
+        self._check(self.L.oc_generate_fixed_theta(m, n, theta, seed, 1 if dist == "uniform" else 0, scale_decades,
+                                                   k, threads, _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p),
+                                                   _p(rn, _f64p), _p(b, _f64p), _p(xs, _f64p), C_.byref(norm)))
+        A = Instance(m, n, rp, ci, v, rn, bool(norm.value))
+        if k > 1:
+            return A, b.reshape(m, k), xs.reshape(n, k)
+        return A, b, xs
 
     def build(self, m, n, rows, cols, vals, normalize=True, b=None):
         rows, cols, vals = _i64(rows), _i64(cols), _f64(vals)

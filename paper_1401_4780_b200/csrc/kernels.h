@@ -8,6 +8,11 @@
 
 namespace ak {
 
+// SM count of the calling thread's current device, cached per device ordinal
+// (runtime.cu); a process may drive several GPUs.
+int current_sm_count();
+
+
 enum Precision { P_F64 = 0, P_F32 = 1, P_F32X64 = 2 };
 enum Sampling { S_UNIFORM = 0, S_SLICE = 1, S_ALIAS = 2 };
 

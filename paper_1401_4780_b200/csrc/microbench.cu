@@ -2,7 +2,7 @@
 // projection with no A stream — theta (<= 128) random L2-resident gathers of x, a warp
 // reduction, then theta random red.global.add — at a given warp count and x
 // footprint. Modes: 0 gather -> reduce -> red (the worker's dependent chain),
-// 1 gathers only, 2 reds only. Indices come from a counter hash, so no memory
+// 1 gathers only, 2 reds only; mode + 16 keeps 2 rows in flight per warp. Indices come from a counter hash, so no memory
 // other than x is touched. Used by bench.py to state the L2/atomic-bound
 // roofline beside the HBM one.
 #include "../../include/asyrk_cuda.h"
@@ -20,39 +20,63 @@ __device__ __forceinline__ uint32_t hash32(uint32_t a) {
     return a;
 }
 
-template <class X>
+// R rows in flight per warp, like the worker (K2 keeps 2): the R rows'
+// gathers issue back to back, their reductions interleave, then their reds.
+template <class X, int R>
 __global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta, long long per_warp, int mode,
                                                     unsigned long long* sink) {
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     X acc_all = X(0);
-    for (long long q = 0; q < per_warp; ++q) {
+    for (long long q0 = 0; q0 < per_warp; q0 += R) {
         // theta <= 128: lane l owns entries l, l + 32, l + 64, l + 96 (the worker's E slots)
-        uint32_t col[4];
+        uint32_t col[R][4];
         bool on[4];
-        X s = X(0);
+        X s[R];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int k = lane + 32 * e;
-            on[e] = k < theta;
-            const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)k * 0xC2B2AE35u);
-            col[e] = (uint32_t)(((uint64_t)h * n) >> 32);
-            if (mode != 2 && on[e]) s += __ldcg(x + col[e]);
+        for (int r = 0; r < R; ++r) {
+            s[r] = X(0);
+            const uint32_t q = (uint32_t)(q0 + r);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = lane + 32 * e;
+                on[e] = k < theta;
+                const uint32_t h = hash32(warp * 0x9E3779B9u + q * 0x85EBCA6Bu + (uint32_t)k * 0xC2B2AE35u);
+                col[r][e] = (uint32_t)(((uint64_t)h * n) >> 32);
+                if (mode != 2 && on[e]) s[r] += __ldcg(x + col[r][e]);
+            }
         }
         if (mode == 0) {
-            s = warp_sum(s);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (on[e]) atomicAdd(x + col[e], X(1e-30) * s);
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int r = 0; r < R; ++r) s[r] += __shfl_xor_sync(FULL, s[r], o);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (on[e]) atomicAdd(x + col[r][e], X(1e-30) * s[r]);
         } else if (mode == 2) {
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-                if (on[e]) atomicAdd(x + col[e], X(1e-30));
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (on[e]) atomicAdd(x + col[r][e], X(1e-30));
         } else {
-            acc_all += s;
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc_all += s[r];
         }
     }
     if (mode == 1 && acc_all == X(12345.678)) atomicAdd(sink, 1ull);  // keep the gathers alive
+}
+
+template <class X>
+static void xside_launch(int rows, int blocks, int threads, void* x, int64_t n, int theta, int64_t per_warp, int mode,
+                         unsigned long long* sink) {
+    if (rows == 2)
+        xside_kernel<X, 2><<<blocks, threads>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
+    else
+        xside_kernel<X, 1><<<blocks, threads>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
 }
 
 }  // namespace ak
@@ -61,6 +85,10 @@ extern "C" asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t
                                                int64_t proj_per_warp, int32_t mode, double* proj_per_s,
                                                double* kernel_ms) {
     using namespace ak;
+    // mode + 16: the same traffic with 2 rows in flight per warp (the worker's shape)
+    const int rows = mode >= 16 ? 2 : 1;
+    mode &= 15;
+    if (rows == 2) proj_per_warp += proj_per_warp & 1;
     if (n < 1 || theta < 1 || theta > 128 || warps < 1 || proj_per_warp < 1)
         return fail(ASYRK_E_InvalidArgument, "microbench_xside: need n >= 1, 1 <= theta <= 128, warps >= 1");
     void* x = nullptr;
@@ -78,9 +106,9 @@ extern "C" asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t
     for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
         cudaEventRecord(e0);
         if (precision == P_F32)
-            xside_kernel<float><<<blocks, threads>>>((float*)x, (uint32_t)n, theta, proj_per_warp, mode, sink);
+            xside_launch<float>(rows, blocks, threads, x, n, theta, proj_per_warp, mode, sink);
         else
-            xside_kernel<double><<<blocks, threads>>>((double*)x, (uint32_t)n, theta, proj_per_warp, mode, sink);
+            xside_launch<double>(rows, blocks, threads, x, n, theta, proj_per_warp, mode, sink);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);

@@ -28,15 +28,7 @@ namespace ak {
 
 constexpr int kMonThreads = 256;
 
-static int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+static int sm_count() { return current_sm_count(); }
 
 
 template <class X>

@@ -248,15 +248,7 @@ __global__ void mrhs_commit_kernel(MrhsArgs a, int advance) {
     }
 }
 
-static int mr_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+static int mr_sms() { return current_sm_count(); }
 
 int mrhs_row_blocks(long long m) {
     const long long want = (m + 7) / 8;

@@ -3,6 +3,7 @@
 #include "runtime.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -153,17 +154,33 @@ static bool no_pool() {
     return d == 1;
 }
 
-cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
-    static int configured = -1;
+constexpr int kMaxDevices = 64;
+
+int current_sm_count() {
+    static std::atomic<int> cache[kMaxDevices];
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured != dev) {
+    int v = (dev >= 0 && dev < kMaxDevices) ? cache[dev].load(std::memory_order_relaxed) : 0;
+    if (!v) {
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        if (v <= 0) v = 1;
+        if (dev >= 0 && dev < kMaxDevices) cache[dev].store(v, std::memory_order_relaxed);
+    }
+    return v;
+}
+
+cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
+    static std::atomic<uint64_t> configured{0};  // one bit per device ordinal
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = (dev >= 0 && dev < kMaxDevices) ? (1ull << dev) : 0;
+    if (!bit || !(configured.load(std::memory_order_relaxed) & bit)) {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        configured = dev;
+        configured.fetch_or(bit, std::memory_order_relaxed);
     }
     const cudaError_t e = no_pool() ? cudaMalloc(p, bytes ? bytes : 1) : cudaMallocAsync(p, bytes ? bytes : 1, s);
     if (getenv("ASYRK_DEBUG_POOL")) fprintf(stderr, "[pool] alloc %p %zu\n", *p, bytes);

@@ -325,15 +325,7 @@ static const void* kernel_for(int precision, int E, int full_row) {
     }
 }
 
-static int num_sms() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
+static int num_sms() { return current_sm_count(); }
 
 // Spread W warps over all SMs: up to 8 warps per block, as few warps per
 // block as it takes to give every SM work when W is small.

@@ -14,9 +14,8 @@ GOLDEN = os.path.join(ROOT, "tests", "golden", "golden.npz")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
-    # the C restatement is test infrastructure; build it if this checkout has not
-    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
-        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "liboracle.so"], check=True)
+    # the C restatement is test infrastructure; (re)build it when its sources changed
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "liboracle.so"], check=True)
 
 
 @pytest.fixture(scope="session")

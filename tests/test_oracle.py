@@ -265,3 +265,25 @@ def test_rate_fit_and_errors(golden):
         C.simulate(A, b, np.zeros(6), -0.1, 1, "fixed", 5, 1, "full_row")
     with pytest.raises(oracle.OracleError, match="InvalidArgument"):
         C.simulate(A, b, np.zeros(6), 0.1, 1, "fixed", 0, 1, "full_row")
+
+
+@pytest.mark.parametrize("args,kw", [
+    ((2000, 1000, 12, 7), {}),
+    ((3000, 1000, 25, 1004), dict(scale_decades=1.0)),   # config 4's raw rows
+    ((4000, 2000, 50, 1003), dict(dist="uniform")),      # config 3's U(-1,1) values
+    ((5000, 2500, 20, 1005), dict(k=4)),                 # config 5's multi-RHS B = A X*
+    ((200000, 100000, 30, 1002), {}),                    # config 2 at full size (the bench instance)
+])
+def test_workload_generator_bitwise(args, kw):
+    """The reference arm of bench.py builds its instance with the C restatement
+    of the generator (oracle/workload.c) so the product library never maps into
+    the reference process; it must produce the product generator's arrays bit
+    for bit (include/asyrk_datagen.h)."""
+    from paper_1401_4780_b200 import capi
+
+    a = C.generate_fixed_theta(*args, **kw)
+    b = capi.generate_fixed_theta(*args, **kw)
+    for f in ("row_ptr", "col_idx", "values", "row_norm"):
+        assert np.array_equal(getattr(a[0], f), getattr(b[0], f)), f
+    assert a[0].normalized == b[0].normalized
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
