@@ -409,8 +409,8 @@ def roofline(W, worker_rate, avg_launch_ms, step_rate):
     contract; the proj/s figures sit beside it."""
     from paper_1401_4780_b200 import capi
 
-    rx1 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 0) for _ in range(3))
-    rx2 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 256, 16) for _ in range(3))
+    rx1 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 1024, 0) for _ in range(3))
+    rx2 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 1024, 16) for _ in range(3))
     rx = max(rx1, rx2)
     peak_hbm, hbm_kind = measured_peak_hbm()
     r_hbm = peak_hbm * 1e9 / S_A_F64
@@ -462,57 +462,71 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
     """BASELINE config 5 at this job's N: k=64 right-hand sides split into N
     contiguous column shards, one per rank (A replicated), each rank's
     lock-free warp-workers on its shard, and one NCCL all-reduce of the shard
-    residual norms per snapshot as the global stop test (paper_1401_4780_b200/
-    mrhs.py). Returns the summary on rank 0 (None elsewhere)."""
+    residual norms per evaluated boundary as the global stop test. The loop is
+    the library's native driver (asyrk_mrhs_solve_nccl): the NCCL communicator
+    is built by the library from a unique id broadcast over torch.distributed
+    (a 1-rank communicator at N = 1). Returns the summary on rank 0."""
     import torch
 
     from paper_1401_4780_b200 import capi
-    from paper_1401_4780_b200.mrhs import CudaShardBackend, shard_columns, solve_sharded
+    from paper_1401_4780_b200.mrhs import shard_columns
 
     A, B, Xs = capi.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"], k=CFG5["k"])
     B = B.astype(np.float32)
     bb = float((B.astype(np.float64) ** 2).sum())
     c0, c1 = shard_columns(CFG5["k"], world, rank)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    with torch.cuda.stream(stream):
-        be = CudaShardBackend(A, B, c0, c1, stream=stream.cuda_stream)
-        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1)
-        for w in range(warmup):
-            flush.zero_()
-            solve_sharded(be, seed=100 + w, **kw)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        rows, epochs, records = 0, [], []
-        with ClockSampler(local) as clk:
-            for k in range(steps):
-                flush.zero_()
-                ev[k][0].record(stream)
-                t = solve_sharded(be, seed=1000 + k, **kw)
-                ev[k][1].record(stream)
-                rows += int(t["updates_applied"][-1])
-                epochs.append(int(t["epoch_index"][-1]))
-                records.append(len(t["epoch_index"]))
-                rel = float(np.sqrt(t["r_sq"][-1] / bb))
-                if not rel < TOL5:
-                    raise RuntimeError(f"config 5 step {k} stopped at relative residual {rel}")
-            torch.cuda.synchronize()
-        stats = be.impl.stats()
-        # the stop test's collective alone: all-reduce of the 3 shard norms, device time
-        ar_us = 0.0
-        if dist:
-            nt = be.norms()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            for _ in range(10):
-                dist.all_reduce(nt)
-            e0.record(stream)
-            for _ in range(200):
-                dist.all_reduce(nt)
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ar_us = 1e3 * e0.elapsed_time(e1) / 200
     if dist:
+        uid = capi.nccl_unique_id() if rank == 0 else bytes(capi.NCCL_UNIQUE_ID_BYTES)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, src=0)
+        uid = bytes(t.cpu().tolist())
+    else:
+        uid = capi.nccl_unique_id()
+    comm = capi.NcclComm(world, uid, rank)
+    sh = capi.MultiRHS(A, B, c0, c1, stream=stream.cuda_stream)
+    kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1,
+              sampling=capi.SLICE_SHUFFLE)
+    for w in range(warmup):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        sh.solve_nccl(comm, seed=100 + w, **kw)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    rows, epochs, records, wms, wl = 0, [], [], 0.0, 0
+    with ClockSampler(local) as clk:
+        for k in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev[k][0].record(stream)
+            t = sh.solve_nccl(comm, seed=1000 + k, **kw)
+            ev[k][1].record(stream)
+            st = sh.stats()
+            wms += st["worker_ms"]
+            wl += st["worker_launches"]
+            rows += int(t["updates_applied"][-1])
+            epochs.append(int(t["epoch_index"][-1]))
+            records.append(len(t["epoch_index"]))
+            rel = float(np.sqrt(t["r_sq"][-1] / bb))
+            if not rel < TOL5:
+                raise RuntimeError(f"config 5 step {k} stopped at relative residual {rel}")
+        torch.cuda.synchronize()
+    # the stop test's collective alone: an all-reduce of 3 doubles over the job's
+    # NCCL fabric (torch's communicator), device time per call
+    ar_us = 0.0
+    if dist:
+        nt = torch.zeros(3, dtype=torch.float64, device="cuda")
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(10):
+            dist.all_reduce(nt)
+        e0.record()
+        for _ in range(200):
+            dist.all_reduce(nt)
+        e1.record()
+        torch.cuda.synchronize()
+        ar_us = 1e3 * e0.elapsed_time(e1) / 200
         dist.barrier()
     step_ms = [a.elapsed_time(c) for a, c in ev]
     dev_ms = sum(step_ms)
@@ -524,15 +538,18 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
         t = torch.tensor([float(col_proj)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
         col_proj = float(t.item())
-    be.close()
+    sh.close()
+    comm.close()
     if rank != 0:
         return None
     return {"metric": "config 5 column projections/sec (row projections x owned RHS columns, all ranks)",
             "value": col_proj / (dev_ms * 1e-3), "unit": "proj/s", "n_gpus": world, "steps": steps,
             "ms_per_step": dev_ms / steps, "time_to_tolerance_ms": statistics.median(step_ms),
             "epochs": statistics.median(epochs), "records_per_solve": statistics.median(records),
-            "allreduce_us_per_epoch": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
-            "worker_launches": stats["worker_launches"], "kernel_launches": stats["kernel_launches"],
+            "worker_ms_per_solve": wms / steps, "worker_launches_per_solve": wl / steps,
+            "allreduce_us_per_call": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
+            "driver": "asyrk_mrhs_solve_nccl (native loop, NCCL all-reduce of the shard norms per evaluated boundary)",
+            "sampling": "slice_shuffle",
             "workload": "config5: m=500000 n=250000 theta=20 k=64 fp32, RHS columns sharded over the ranks, "
                         "all-reduced stop at ||R||_F/||B||_F<1e-5",
             "warps": W, "clocks": clk.summary()}
@@ -566,7 +583,8 @@ def run_gpu_cfg5(args):
                 "run": {"warps": c5["warps"], "columns_per_gpu": c5["columns_per_gpu"],
                         "parallelism": f"rhs-shard x{world}"},
                 "time_to_tolerance_ms": c5["time_to_tolerance_ms"], "epochs": c5["epochs"],
-                "allreduce_us_per_epoch": c5["allreduce_us_per_epoch"], "clocks": c5["clocks"]}
+                "records_per_solve": c5["records_per_solve"], "allreduce_us_per_call": c5["allreduce_us_per_call"],
+                "driver": c5["driver"], "clocks": c5["clocks"]}
         if world == 1 and not args.no_cpu_baseline:
             import oracle  # noqa: F401  (the reference's CPU path on a bounded sample)
 

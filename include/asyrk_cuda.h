@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define ASYRK_ABI_VERSION 1
+#define ASYRK_ABI_VERSION 2
 
 /* ErrorCode ordinal + 1 (ref/include/asyrk/error.hpp:8-33). */
 typedef enum {
@@ -307,18 +307,28 @@ asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t pr
  * k right-hand sides share A and the row sequence: one row projection
  * updates every RHS column (X n x k row-major fp32, B m x k). A GPU owns the
  * column shard [c0, c1) (a power of two, 2..64 columns). The reference is
- * single-RHS: its oracle is k independent solves.
+ * single-RHS (its solve_parallel, ref/include/asyrk/parallel.hpp:52-54, per
+ * column is the oracle: SURVEY.md §8c). Sampling: with_replacement or
+ * slice_shuffle (RunConfig::sampling).
+ *
+ * Residual evaluations follow the host-driven monitor schedule:
+ * every boundary while the target is 0 or record_every_boundary is set, else
+ * the boundaries a decay fit of the last records picks, always the last one.
  *
  * Multi-GPU protocol (one process per GPU; the collective is the caller's,
  * e.g. NCCL all-reduce on the system's stream):
- *   begin -> [all-reduce(norms, sum)] -> commit(0) ->
- *   loop { step -> [all-reduce(norms, sum)] -> commit(1) -> stopped? } -> finish
+ *   begin -> [all-reduce(norms, sum)] -> commit ->
+ *   loop { stopped? -> step -> if due: [all-reduce(norms, sum)] -> commit }
+ *   -> finish
  * norms is a device double[3] = this shard's {||R||_F^2, ||A^T R||_F^2,
- * ||X - X*||_F^2}; after the all-reduce every rank takes the same global stop
- * decision (r_sq <= target_r_sq) on the device. stopped() reports the
- * decision of the previous commit (of the only one right after begin), so
- * the host stays one chunk ahead; a chunk queued after the stopping commit
- * sees the device stop flag and returns without touching X. */
+ * ||X - X*||_F^2}, valid when due() reports 1 (the step ended at an
+ * evaluated boundary); after the all-reduce every rank takes the same global
+ * stop decision (r_sq <= target_r_sq) on the device. stopped() waits for the
+ * latest commit that recorded and returns its decision (or 1 at the epoch
+ * cap), so all ranks leave the loop after the same step. Native drivers of
+ * the same loop: asyrk_mrhs_solve (one shard, no collective),
+ * asyrk_mrhs_solve_nccl (one shard per process, an NCCL communicator) and
+ * asyrk_mrhs_solve_devices (one process, several GPUs, ncclCommInitAll). */
 typedef struct asyrk_mrhs asyrk_mrhs;
 asyrk_status asyrk_mrhs_create(const asyrk_csr_view* A, const float* B, int64_t k_total, int64_t c0, int64_t c1,
                                void* stream, asyrk_mrhs** out);
@@ -326,6 +336,9 @@ asyrk_status asyrk_mrhs_destroy(asyrk_mrhs* h);
 /* X0 (n x k_total fp32) and Xstar (n x k_total fp64) may be NULL. */
 asyrk_status asyrk_mrhs_begin(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar);
 asyrk_status asyrk_mrhs_norms(asyrk_mrhs* h, double** dev_norms);
+/* 1 when the last begin/step ended at an evaluated boundary: all-reduce norms, then commit */
+asyrk_status asyrk_mrhs_due(asyrk_mrhs* h, int32_t* due);
+/* records the evaluated boundary the last begin/step reached (no-op otherwise; advance is ignored) */
 asyrk_status asyrk_mrhs_commit(asyrk_mrhs* h, int32_t advance);
 asyrk_status asyrk_mrhs_step(asyrk_mrhs* h);
 asyrk_status asyrk_mrhs_stopped(asyrk_mrhs* h, int32_t* stopped);
@@ -335,6 +348,32 @@ asyrk_status asyrk_mrhs_finish(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_o
 asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
                               asyrk_trace_out* trace, float* X_out);
 asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out);
+
+/* ---- multi-GPU: NCCL (SURVEY.md §8b "mrhs_shard_solve(..., ncclComm_t)") ----
+ * libnccl.so.2 is resolved at run time (the copy already loaded in the
+ * process if any, e.g. PyTorch's, else the system library), so the library
+ * has no link-time NCCL dependency; these return ThreadSpawnFailure with the
+ * reason when NCCL cannot be loaded. Communicators are ncclComm_t passed as
+ * void*. The unique id is the opaque 128-byte ncclUniqueId: rank 0 creates it
+ * and the launcher broadcasts it (e.g. torch.distributed / MPI). */
+#define ASYRK_NCCL_UNIQUE_ID_BYTES 128
+asyrk_status asyrk_nccl_available(int32_t* version);
+asyrk_status asyrk_nccl_get_unique_id(char* id /* [ASYRK_NCCL_UNIQUE_ID_BYTES] */);
+/* on the calling thread's current device */
+asyrk_status asyrk_nccl_comm_init_rank(void** comm, int32_t nranks, const char* id, int32_t rank);
+asyrk_status asyrk_nccl_comm_destroy(void* comm);
+/* One rank's shard of a sharded solve: the whole loop in C++, one
+ * ncclAllReduce(sum) of the 3 shard norms per evaluated boundary on the
+ * shard's stream. Every rank of comm calls it with the same cfg. */
+asyrk_status asyrk_mrhs_solve_nccl(asyrk_mrhs* h, const asyrk_run_config* cfg, void* comm, const float* X0,
+                                   const double* Xstar, asyrk_trace_out* trace, float* X_out);
+/* One process, ndev GPUs: k_total columns split evenly over devices[], one
+ * shard per device, ncclCommInitAll, the same loop with grouped all-reduces.
+ * trace: the (global, identical) records; X_out: n x k_total fp32; stats:
+ * device 0's solve stats (may be NULL). */
+asyrk_status asyrk_mrhs_solve_devices(const asyrk_csr_view* A, const float* B, int64_t k_total, const int32_t* devices,
+                                      int32_t ndev, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
+                                      asyrk_trace_out* trace, float* X_out, asyrk_solve_stats* stats);
 
 /* ---- measurement ------------------------------------------------------- */
 /* x-side roofline R_x: theta random gathers of an n-element

@@ -258,6 +258,16 @@ def lib():
         L.asyrk_mrhs_finish.argtypes = [sp, C.POINTER(TraceOut), _f32p]
         L.asyrk_mrhs_solve.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p]
         L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
+        L.asyrk_mrhs_due.argtypes = [sp, _i32p]
+        L.asyrk_nccl_available.argtypes = [_i32p]
+        L.asyrk_nccl_get_unique_id.argtypes = [C.c_char_p]
+        L.asyrk_nccl_comm_init_rank.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_char_p, C.c_int32]
+        L.asyrk_nccl_comm_destroy.argtypes = [C.c_void_p]
+        L.asyrk_mrhs_solve_nccl.argtypes = [sp, C.POINTER(RunConfig), C.c_void_p, _f32p, _f64p, C.POINTER(TraceOut),
+                                            _f32p]
+        L.asyrk_mrhs_solve_devices.argtypes = [C.POINTER(CsrView), _f32p, C.c_int64, _i32p, C.c_int32,
+                                               C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p,
+                                               C.POINTER(SolveStats)]
         L.asyrk_microbench_xside.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int32,
                                              _f64p, _f64p]
         L.asyrk_generate_fixed_theta.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int32, C.c_double,
@@ -276,7 +286,9 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
+    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
+    "asyrk_nccl_comm_init_rank", "asyrk_nccl_comm_destroy", "asyrk_mrhs_solve_nccl", "asyrk_mrhs_solve_devices",
+    "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
     "asyrk_read_matrix_market", "asyrk_write_matrix_market", "asyrk_read_csr_cache", "asyrk_write_csr_cache",
     "asyrk_host_csr_copy", "asyrk_host_csr_free", "asyrk_host_csr_get_info", "asyrk_read_vector", "asyrk_write_vector", "asyrk_free",
@@ -329,6 +341,12 @@ class MultiRHS:
     def step(self):
         check(lib().asyrk_mrhs_step(self.h))
 
+    def due(self):
+        """True when the last begin/step ended at an evaluated boundary (all-reduce the norms, then commit)."""
+        d = C.c_int32()
+        check(lib().asyrk_mrhs_due(self.h, C.byref(d)))
+        return bool(d.value)
+
     def stopped(self):
         s = C.c_int32()
         check(lib().asyrk_mrhs_stopped(self.h, C.byref(s)))
@@ -356,10 +374,89 @@ class MultiRHS:
         d["X"] = X
         return d
 
+    def solve_nccl(self, comm, X0=None, X_star=None, **cfg):
+        """This rank's shard of a sharded solve, the loop in C++ with one ncclAllReduce of the
+        shard norms per evaluated boundary (asyrk_mrhs_solve_nccl); comm from NcclComm."""
+        c = _run_config(**cfg)
+        cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
+        tr = _Trace(0, cap, want_x=False)
+        X = np.zeros((self.n, self.c1 - self.c0), np.float32)
+        x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
+        xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        check(lib().asyrk_mrhs_solve_nccl(self.h, C.byref(c), C.c_void_p(comm.handle),
+                                          x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None else None,
+                                          _ptr(xs, _f64p), C.byref(tr.out), X.ctypes.data_as(C.POINTER(C.c_float))))
+        d = tr.result(xs is not None)
+        d["X"] = X
+        return d
+
     def stats(self):
         s = SolveStats()
         check(lib().asyrk_mrhs_last_stats(self.h, C.byref(s)))
         return {f: getattr(s, f) for f, _ in SolveStats._fields_}
+
+
+NCCL_UNIQUE_ID_BYTES = 128
+
+
+def nccl_version():
+    """NCCL version code of the libnccl.so.2 the library resolves at run time (raises if none)."""
+    v = C.c_int32()
+    check(lib().asyrk_nccl_available(C.byref(v)))
+    return v.value
+
+
+def nccl_unique_id():
+    buf = C.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    check(lib().asyrk_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class NcclComm:
+    """An NCCL communicator created by the library (asyrk_nccl_comm_init_rank) on the current device."""
+
+    def __init__(self, nranks, unique_id, rank):
+        if len(unique_id) != NCCL_UNIQUE_ID_BYTES:
+            raise ValueError("InvalidArgument: the NCCL unique id is 128 bytes")
+        h = C.c_void_p()
+        check(lib().asyrk_nccl_comm_init_rank(C.byref(h), nranks, unique_id, rank))
+        self.handle = h.value
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().asyrk_nccl_comm_destroy(C.c_void_p(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def mrhs_solve_devices(A, B, devices, X0=None, X_star=None, **cfg):
+    """One process, several GPUs (asyrk_mrhs_solve_devices): the k columns of B split evenly
+    over `devices`, ncclCommInitAll, grouped all-reduces of the shard norms. Returns the
+    global trace, X (n x k fp32) and device 0's solve stats."""
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    k = B.shape[1]
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    c = _run_config(**cfg)
+    cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
+    tr = _Trace(0, cap, want_x=False)
+    X = np.zeros((A.n, k), np.float32)
+    x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
+    xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+    st = SolveStats()
+    check(lib().asyrk_mrhs_solve_devices(C.byref(A.view()), B.ctypes.data_as(C.POINTER(C.c_float)), k,
+                                         devs.ctypes.data_as(_i32p), len(devs), C.byref(c),
+                                         x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None else None,
+                                         _ptr(xs, _f64p), C.byref(tr.out), X.ctypes.data_as(C.POINTER(C.c_float)),
+                                         C.byref(st)))
+    d = tr.result(xs is not None)
+    d["X"] = X
+    d["stats"] = {f: getattr(st, f) for f, _ in SolveStats._fields_}
+    return d
 
 
 def microbench_xside(n, theta, precision=F64, warps=4736, proj_per_warp=256, mode=0):

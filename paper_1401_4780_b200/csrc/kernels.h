@@ -34,6 +34,8 @@ struct WorkerArgs {
     uint32_t key0, key1;          // seed
     int sampling;
     int full_row;
+    long long epoch0, span0;      // span0 > 0: this launch runs epochs [epoch0, epoch0 + span0) (host-scheduled
+                                  // solves); span0 = 0: the epoch / span come from st (chunk_span)
 };
 int worker_elems_per_lane(uint32_t max_len);  // 1, 2, 4 or 0 (looped)
 void launch_worker(const WorkerArgs& a, int precision, int E, cudaStream_t s);
@@ -106,6 +108,9 @@ struct MonitorArgs {
     int force;                    // 1: run even after stop (the final exact record); replaces a same-epoch record
     int advance;                  // 0: initial record, 1: after a chunk
     long long m_rows;
+    long long set_epoch;          // >= 0: the boundary this record is taken at (host-scheduled solves:
+                                  // st->epoch = set_epoch, st->updates = set_epoch * m_rows); -1: unused
+    HostMirror* mirror;           // or nullptr: the record's decision inputs for the host
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
 // overlapped solves: copy x into snapshot slot xs (if the epoch ran) and
@@ -144,13 +149,18 @@ struct MrhsArgs {
     double gamma;
     uint32_t key0, key1;
     int KL;
+    int sampling;                 // S_UNIFORM (with replacement) or S_SLICE
+    long long epoch0, span0;      // this worker launch runs epochs [epoch0, epoch0 + span0)
+    HostMirror* mirror;           // latest record for the host-driven schedule
+    uint32_t max_len;             // longest row (> 32: the looped worker)
 };
 bool mrhs_supported_kl(long long kl);
 int mrhs_row_blocks(long long m);
 int mrhs_col_blocks(long long n);
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s);
 void launch_mrhs_monitor(const MrhsArgs& a, cudaStream_t s);
-void launch_mrhs_commit(const MrhsArgs& a, int advance, cudaStream_t s);
+// record at boundary set_epoch (-1: the initial state) + stop decision
+void launch_mrhs_commit(const MrhsArgs& a, long long set_epoch, cudaStream_t s);
 
 // ---- K4: power iteration building blocks (stats.cpp:15-50)
 void launch_spmv_rows(const CscDev& R, int precision, long long m, const double* v, double* out, cudaStream_t s);

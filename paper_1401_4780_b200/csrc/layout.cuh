@@ -101,6 +101,19 @@ struct DevState {
     int snap_target, mon_slot;
 };
 
+// Pinned, device-mapped copy of the latest record's decision inputs, written
+// by the record kernel (__threadfence_system): the host-driven monitor
+// schedule reads it after the record's event without a copy.
+struct HostMirror {
+    long long epoch;        // epoch of the latest record
+    long long nrec;         // records written so far
+    double r_sq;            // its r_sq (the all-reduced one for multi-RHS shards)
+    int stop;               // stop decided (target, epoch cap or NonFinite)
+    int status;             // 0 or ASYRK_E_NonFinite
+    long long seq;          // commits seen (multi-RHS: index of the latest commit + 1)
+    long long pad[2];
+};
+
 struct DevRecord {
     long long epoch;
     long long updates;

@@ -186,7 +186,10 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
         epoch = st->snap_epoch[slot];
         updates = st->snap_updates[slot];
     } else {
-        if (a.advance) {
+        if (a.set_epoch >= 0) {
+            st->epoch = a.set_epoch;
+            st->updates = a.set_epoch * a.m_rows;
+        } else if (a.advance) {
             const long long sp = chunk_span(st);
             st->epoch += sp;
             st->updates += sp * a.m_rows;
@@ -226,10 +229,17 @@ __device__ void commit_record(const MonitorArgs& a, double r_sq, double g_sq, do
         atomicExch(&st->slot_state[slot], 0);
     }
     if (a.slot < 0) st->go = (!st->stop && st->epoch < st->epochs_cap) ? 1 : 0;
-    if (st->stop && a.host_flag) {
-        *reinterpret_cast<volatile int*>(a.host_flag) = 1;
-        __threadfence_system();
+    if (a.mirror) {
+        volatile HostMirror* hm = a.mirror;
+        hm->epoch = epoch;
+        hm->nrec = st->nrec;
+        hm->r_sq = r_sq;
+        hm->status = st->status;
+        hm->stop = st->stop;
+        hm->seq = hm->seq + 1;
     }
+    if (st->stop && a.host_flag) *reinterpret_cast<volatile int*>(a.host_flag) = 1;
+    if (a.mirror || (st->stop && a.host_flag)) __threadfence_system();
 }
 
 // ---- finalize, exact: serial sums in the reference's order (residuals

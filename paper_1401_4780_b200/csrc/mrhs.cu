@@ -23,38 +23,242 @@ namespace ak {
 
 constexpr int kMrThreads = 256;
 
+// Lane geometry of a KL-column row of X: VW consecutive floats per lane
+// (float4 for KL >= 4, one red.global.add.v4.f32 per lane per nonzero), GL
+// lanes cover one nonzero's KL columns, S nonzeros are processed side by side.
 template <int KL>
 struct MrGeom {
-    static constexpr int GL = KL / 2;      // lanes per nonzero slot (float2 each)
-    static constexpr int S = 32 / GL;      // nonzeros processed side by side
+    static constexpr int VW = KL >= 4 ? 4 : 2;
+    static constexpr int GL = KL / VW;
+    static constexpr int S = 32 / GL;
     static_assert(KL >= 2 && KL <= 64 && (KL & (KL - 1)) == 0, "KL must be a power of two in [2, 64]");
 };
 
-__device__ __forceinline__ float2 ld_x2(const float* p) { return __ldcg(reinterpret_cast<const float2*>(p)); }
+template <int VW>
+struct MrVec {
+    float v[VW];
+};
 
+template <int VW>
+__device__ __forceinline__ MrVec<VW> ld_xv(const float* p) {  // L1-bypassing: X takes other SMs' reds
+    MrVec<VW> r;
+    if constexpr (VW == 4) {
+        const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+        r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+    } else {
+        const float2 t = __ldcg(reinterpret_cast<const float2*>(p));
+        r.v[0] = t.x, r.v[1] = t.y;
+    }
+    return r;
+}
+
+template <int VW>
+__device__ __forceinline__ MrVec<VW> ld_bv(const float* p) {  // B is immutable
+    MrVec<VW> r;
+    if constexpr (VW == 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+    } else {
+        const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        r.v[0] = t.x, r.v[1] = t.y;
+    }
+    return r;
+}
+
+template <int VW>
+__device__ __forceinline__ void red_xv(float* p, const MrVec<VW>& d) {
+    if constexpr (VW == 4)
+        asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(d.v[0]), "f"(d.v[1]),
+                     "f"(d.v[2]), "f"(d.v[3])
+                     : "memory");
+    else
+        asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(d.v[0]), "f"(d.v[1])
+                     : "memory");
+}
+
+// Row draw of position j of this warp's launch: with-replacement Philox, or
+// slice_shuffle — warp w owns rows [w m / W, (w+1) m / W) and walks a keyed
+// Feistel permutation of them per pass (ref parallel.cpp:355-363).
+__device__ __forceinline__ long long mr_draw(const MrhsArgs& a, long long warp, long long epoch, long long j,
+                                             long long slice_lo, long long slice_len) {
+    const long long m = a.L.m;
+    if (a.sampling == S_SLICE) {
+        const long long s = j / slice_len;
+        const uint32_t jj = (uint32_t)(j - s * slice_len);
+        const uint32_t pass = (uint32_t)(epoch + s);
+        const uint32_t k0 = a.key0 ^ (uint32_t)(warp * 0x85EBCA6Bull) ^ 0x68E31DA4u;
+        const uint32_t k1 = a.key1 ^ (pass * 0xC2B2AE35u) ^ 0xB5297A4Du;
+        return slice_lo + permute_index(jj, (uint32_t)slice_len, feistel_half_bits((uint32_t)slice_len), k0, k1);
+    }
+    const U4 rr = philox4x32(U4{(uint32_t)j, (uint32_t)(j >> 32), (uint32_t)warp, (uint32_t)epoch}, a.key0, a.key1);
+    return (long long)bounded64(((uint64_t)rr.x << 32) | rr.y, (uint64_t)m);
+}
+
+// The row data one projection needs, held across the warp: lane k < len keeps
+// (value, column) of nonzero k (rows of at most 32 nonzeros), every lane the
+// B row slice of its columns and 1/||a_i||^2.
+template <int VW>
+struct MrRow {
+    float v;
+    int c;
+    MrVec<VW> b;
+    float inv;
+    int len;
+};
+
+template <int KL>
+__device__ __forceinline__ void mr_load(const MrhsArgs& a, long long i, int lane, MrRow<MrGeom<KL>::VW>& r) {
+    using G = MrGeom<KL>;
+    const RowRef rf = row_ref(a.L, i);
+    r.len = rf.len;
+    r.v = lane < rf.len ? __ldg(rec_vals<float>(rf) + lane) : 0.f;
+    r.c = lane < rf.len ? __ldg(rec_cols<float>(rf) + lane) : 0;
+    r.b = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * (lane % G::GL));
+    r.inv = (float)rec_inv(rf);
+}
+
+// K2b: one warp = one lock-free worker projecting R = 2 rows at a time for
+// all KL columns (the next 2 rows' records and B slices are prefetched while
+// the current ones gather / reduce / scatter; K2's structure).
 template <int KL>
 __global__ void __launch_bounds__(256) mrhs_worker_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
+    constexpr int R = 2;
     const DevState* st = a.st;
-    if (st->stop) return;
-    const long long epoch = st->epoch;
-    const long long span = chunk_span(st);
+    if (!st->go) return;
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
     if (span <= 0) return;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (warp >= a.W) return;
     const int lane = threadIdx.x & 31;
     const int slot = lane / G::GL, cl = lane % G::GL;
     const long long m = a.L.m;
-    const long long total = span * m;
-    const long long count = total / a.W + (warp < total % a.W ? 1 : 0);
+    long long count, slice_lo = 0, slice_len = 1;
+    if (a.sampling == S_SLICE) {
+        slice_lo = warp * m / a.W;
+        slice_len = (warp + 1) * m / a.W - slice_lo;
+        count = span * slice_len;
+    } else {
+        const long long total = span * m;
+        count = total / a.W + (warp < total % a.W ? 1 : 0);
+    }
+    if (count <= 0) return;
     float* __restrict__ X = a.X;
+    const float gamma = (float)a.gamma;
 
+    const long long nb = (count + 31) >> 5;
+    long long D0 = mr_draw(a, warp, epoch, lane, slice_lo, slice_len);
+    long long D1 = nb > 1 ? mr_draw(a, warp, epoch, 32 + lane, slice_lo, slice_len) : D0;
+
+    MrRow<G::VW> cur[R];
+    bool ok_cur[R];
+    {
+        const int nq0 = (int)min(32ll, count);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            ok_cur[r] = r < nq0;
+            const long long row = __shfl_sync(FULL, D0, r);
+            if (ok_cur[r]) mr_load<KL>(a, row, lane, cur[r]);
+        }
+    }
+    for (long long bi = 0; bi < nb; ++bi) {
+        const int nq = (int)min(32ll, count - bi * 32);
+        const int nq_next = bi + 1 < nb ? (int)min(32ll, count - (bi + 1) * 32) : 0;
+        for (int q0 = 0; q0 < nq; q0 += R) {
+            // ---- prefetch the next R rows (independent of X)
+            MrRow<G::VW> nxt[R];
+            bool ok_nxt[R];
+            const bool in_batch = q0 + R < nq;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int qn = in_batch ? q0 + R + r : r;
+                ok_nxt[r] = in_batch ? (q0 + R + r < nq) : (r < nq_next);
+                const long long nrow = __shfl_sync(FULL, in_batch ? D0 : D1, qn & 31);
+                if (ok_nxt[r]) mr_load<KL>(a, nrow, lane, nxt[r]);
+            }
+            // ---- stale residuals: the R rows' X gathers issue back to back
+            float acc[R][G::VW];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) acc[r][u] = 0.f;
+                const int len = ok_cur[r] ? cur[r].len : 0;
+                for (int t0 = 0; t0 < len; t0 += G::S) {
+                    const int t = t0 + slot;
+                    const float v = __shfl_sync(FULL, cur[r].v, t & 31);
+                    const int c = __shfl_sync(FULL, cur[r].c, t & 31);
+                    if (t < len) {
+                        const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)c * KL + G::VW * cl);
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) acc[r][u] = fmaf(v, xv.v[u], acc[r][u]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = G::GL; o < 32; o <<= 1)
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int u = 0; u < G::VW; ++u) acc[r][u] += __shfl_xor_sync(FULL, acc[r][u], o);
+            // ---- X[t, :] -= gamma (a_i^T X - B_i) / ||a_i||^2 * a_it
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (!ok_cur[r]) continue;
+                float cf[G::VW];
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[r][u] - cur[r].b.v[u]) * cur[r].inv;
+                const int len = cur[r].len;
+                for (int t0 = 0; t0 < len; t0 += G::S) {
+                    const int t = t0 + slot;
+                    const float v = __shfl_sync(FULL, cur[r].v, t & 31);
+                    const int c = __shfl_sync(FULL, cur[r].c, t & 31);
+                    if (t < len) {
+                        MrVec<G::VW> d;
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                        red_xv<G::VW>(X + (size_t)c * KL + G::VW * cl, d);
+                    }
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                cur[r] = nxt[r];
+                ok_cur[r] = ok_nxt[r];
+            }
+        }
+        D0 = D1;
+        if (bi + 2 < nb) D1 = mr_draw(a, warp, epoch, (bi + 2) * 32 + lane, slice_lo, slice_len);
+    }
+}
+
+// Rows longer than 32 nonzeros: one row at a time, record read in the loop.
+template <int KL>
+__global__ void __launch_bounds__(256) mrhs_worker_long_kernel(MrhsArgs a) {
+    using G = MrGeom<KL>;
+    const DevState* st = a.st;
+    if (!st->go) return;
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
+    if (span <= 0) return;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp >= a.W) return;
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / G::GL, cl = lane % G::GL;
+    const long long m = a.L.m;
+    long long count, slice_lo = 0, slice_len = 1;
+    if (a.sampling == S_SLICE) {
+        slice_lo = warp * m / a.W;
+        slice_len = (warp + 1) * m / a.W - slice_lo;
+        count = span * slice_len;
+    } else {
+        const long long total = span * m;
+        count = total / a.W + (warp < total % a.W ? 1 : 0);
+    }
+    float* __restrict__ X = a.X;
+    const float gamma = (float)a.gamma;
     for (long long j0 = 0; j0 < count; j0 += 32) {
-        // 32 rows per lane-parallel Philox draw (with replacement)
-        const long long j = j0 + lane;
-        const U4 rr = philox4x32(U4{(uint32_t)j, (uint32_t)(j >> 32), (uint32_t)warp, (uint32_t)epoch}, a.key0,
-                                 a.key1);
-        const long long myrow = (long long)bounded64(((uint64_t)rr.x << 32) | rr.y, (uint64_t)m);
+        const long long myrow = mr_draw(a, warp, epoch, j0 + lane, slice_lo, slice_len);
         const int nq = (int)min(32ll, count - j0);
         for (int q = 0; q < nq; ++q) {
             const long long i = __shfl_sync(FULL, myrow, q);
@@ -62,38 +266,43 @@ __global__ void __launch_bounds__(256) mrhs_worker_kernel(MrhsArgs a) {
             const float* vals = rec_vals<float>(r);
             const int32_t* cols = rec_cols<float>(r);
             const int len = r.len;
-            float2 acc = make_float2(0.f, 0.f);
+            float acc[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
             for (int t0 = 0; t0 < len; t0 += G::S) {
                 const int t = t0 + slot;
                 if (t < len) {
                     const float v = __ldg(vals + t);
-                    const float2 xv = ld_x2(X + (size_t)__ldg(cols + t) * KL + 2 * cl);
-                    acc.x = fmaf(v, xv.x, acc.x);
-                    acc.y = fmaf(v, xv.y, acc.y);
+                    const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
+#pragma unroll
+                    for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
                 }
             }
 #pragma unroll
-            for (int o = G::GL; o < 32; o <<= 1) {
-                acc.x += __shfl_xor_sync(FULL, acc.x, o);
-                acc.y += __shfl_xor_sync(FULL, acc.y, o);
-            }
-            const float2 bv = __ldg(reinterpret_cast<const float2*>(a.B + (size_t)i * KL) + cl);
+            for (int o = G::GL; o < 32; o <<= 1)
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
+            const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
             const float inv = (float)rec_inv(r);
-            const float g = (float)a.gamma;
-            const float cx = g * (acc.x - bv.x) * inv, cy = g * (acc.y - bv.y) * inv;
+            float cf[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[u] - bv.v[u]) * inv;
             for (int t0 = 0; t0 < len; t0 += G::S) {
                 const int t = t0 + slot;
                 if (t < len) {
                     const float v = __ldg(vals + t);
-                    float2* dst = reinterpret_cast<float2*>(X + (size_t)__ldg(cols + t) * KL + 2 * cl);
-                    atomicAdd(dst, make_float2(-cx * v, -cy * v));
+                    MrVec<G::VW> d;
+#pragma unroll
+                    for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                    red_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
                 }
             }
         }
     }
 }
 
-// R = A X - B (fp32 storage, fp64 r^2 block partials)
+// R = A X - B (fp32 storage, fp64 r^2 block partials): warp per row, lanes
+// over the row's KL columns (VW floats each), S nonzeros side by side
 template <int KL>
 __global__ void __launch_bounds__(kMrThreads) mrhs_rows_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
@@ -108,26 +317,31 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_rows_kernel(MrhsArgs a) {
         const RowRef r = row_ref(a.L, i);
         const float* vals = rec_vals<float>(r);
         const int32_t* cols = rec_cols<float>(r);
-        float2 acc = make_float2(0.f, 0.f);
+        float acc[G::VW];
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
         for (int t0 = 0; t0 < r.len; t0 += G::S) {
             const int t = t0 + slot;
             if (t < r.len) {
                 const float v = __ldg(vals + t);
-                const float2 xv = __ldg(reinterpret_cast<const float2*>(a.X + (size_t)__ldg(cols + t) * KL) + cl);
-                acc.x = fmaf(v, xv.x, acc.x);
-                acc.y = fmaf(v, xv.y, acc.y);
+                const MrVec<G::VW> xv = ld_bv<G::VW>(a.X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
             }
         }
 #pragma unroll
-        for (int o = G::GL; o < 32; o <<= 1) {
-            acc.x += __shfl_xor_sync(FULL, acc.x, o);
-            acc.y += __shfl_xor_sync(FULL, acc.y, o);
-        }
+        for (int o = G::GL; o < 32; o <<= 1)
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
         if (slot == 0) {
-            const float2 bv = __ldg(reinterpret_cast<const float2*>(a.B + (size_t)i * KL) + cl);
-            const float2 rv = make_float2(acc.x - bv.x, acc.y - bv.y);
-            reinterpret_cast<float2*>(a.R + (size_t)i * KL)[cl] = rv;
-            mine += (double)rv.x * rv.x + (double)rv.y * rv.y;
+            const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
+            float* rp = a.R + (size_t)i * KL + G::VW * cl;
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) {
+                const float rv = acc[u] - bv.v[u];
+                rp[u] = rv;
+                mine += (double)rv * rv;
+            }
         }
     }
     mine = warp_sum(mine);
@@ -153,25 +367,29 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_cols_kernel(MrhsArgs a, int n
     double g2 = 0.0, d2 = 0.0;
     for (long long j = gw; j < a.L.n; j += nw) {
         const long long e0 = __ldg(a.col_ptr + j), e1 = __ldg(a.col_ptr + j + 1);
-        double gx = 0.0, gy = 0.0;
+        double g[G::VW];
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) g[u] = 0.0;
         for (long long e = e0 + slot; e < e1; e += G::S) {
             const double v = (double)__ldg(a.csc_val + e);
-            const float2 rv = __ldg(reinterpret_cast<const float2*>(a.R + (size_t)__ldg(a.csc_row + e) * KL) + cl);
-            gx += v * rv.x;
-            gy += v * rv.y;
+            const MrVec<G::VW> rv = ld_bv<G::VW>(a.R + (size_t)__ldg(a.csc_row + e) * KL + G::VW * cl);
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) g[u] += v * rv.v[u];
         }
 #pragma unroll
-        for (int o = G::GL; o < 32; o <<= 1) {
-            gx += __shfl_xor_sync(FULL, gx, o);
-            gy += __shfl_xor_sync(FULL, gy, o);
-        }
+        for (int o = G::GL; o < 32; o <<= 1)
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) g[u] += __shfl_xor_sync(FULL, g[u], o);
         if (slot == 0) {
-            g2 += gx * gx + gy * gy;
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) g2 += g[u] * g[u];
             if (a.Xstar) {
-                const float2 xv = __ldg(reinterpret_cast<const float2*>(a.X + (size_t)j * KL) + cl);
-                const double dx = (double)xv.x - a.Xstar[(size_t)j * KL + 2 * cl];
-                const double dy = (double)xv.y - a.Xstar[(size_t)j * KL + 2 * cl + 1];
-                d2 += dx * dx + dy * dy;
+                const MrVec<G::VW> xv = ld_bv<G::VW>(a.X + (size_t)j * KL + G::VW * cl);
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) {
+                    const double d = (double)xv.v[u] - a.Xstar[(size_t)j * KL + G::VW * cl + u];
+                    d2 += d * d;
+                }
             }
         }
     }
@@ -214,14 +432,15 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_reduce_kernel(MrhsArgs a, int
         for (int c = 0; c < 3; ++c) a.norms[c] = red[c][0];
 }
 
-// norms (possibly all-reduced over ranks) -> record + stop (one thread)
-__global__ void mrhs_commit_kernel(MrhsArgs a, int advance) {
+// norms (possibly all-reduced over ranks) -> record + stop (one thread), at
+// boundary set_epoch (epochs are exact per launch: updates = epoch * m); the
+// decision inputs also go to the host mirror for the host-driven schedule
+__global__ void mrhs_commit_kernel(MrhsArgs a, long long set_epoch) {
     DevState* st = a.st;
     if (st->stop) return;
-    if (advance) {
-        const long long sp = chunk_span(st);
-        st->epoch += sp;
-        st->updates += sp * a.L.m;
+    if (set_epoch >= 0) {
+        st->epoch = set_epoch;
+        st->updates = set_epoch * a.L.m;
     }
     const double rs = a.norms[0], gs = a.norms[1], ds = a.norms[2];
     if (!isfinite(rs) || !isfinite(gs)) {
@@ -242,10 +461,18 @@ __global__ void mrhs_commit_kernel(MrhsArgs a, int advance) {
         st->nrec = k + 1;
         if (rs <= st->target || st->epoch >= st->epochs_cap) st->stop = 1;
     }
-    if (st->stop && a.host_flag) {
-        *reinterpret_cast<volatile int*>(a.host_flag) = 1;
-        __threadfence_system();
+    st->go = st->stop ? 0 : 1;
+    if (a.mirror) {
+        volatile HostMirror* hm = a.mirror;
+        hm->epoch = st->epoch;
+        hm->nrec = st->nrec;
+        hm->r_sq = rs;
+        hm->status = st->status;
+        hm->stop = st->stop;
+        hm->seq = hm->seq + 1;
     }
+    if (st->stop && a.host_flag) *reinterpret_cast<volatile int*>(a.host_flag) = 1;
+    __threadfence_system();
 }
 
 static int mr_sms() { return current_sm_count(); }
@@ -262,7 +489,10 @@ int mrhs_col_blocks(long long n) {
 template <int KL>
 static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
     const int blocks = (int)((a.W * 32 + 255) / 256);
-    mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
+    if (a.max_len <= 32)
+        mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
+    else
+        mrhs_worker_long_kernel<KL><<<blocks, 256, 0, s>>>(a);
 }
 template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
@@ -285,6 +515,8 @@ static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
 bool mrhs_supported_kl(long long kl) { return kl >= 2 && kl <= 64 && (kl & (kl - 1)) == 0; }
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s) { MR_DISPATCH(a.KL, mrhs_worker_launch, a, s) }
 void launch_mrhs_monitor(const MrhsArgs& a, cudaStream_t s) { MR_DISPATCH(a.KL, mrhs_monitor_launch, a, s) }
-void launch_mrhs_commit(const MrhsArgs& a, int advance, cudaStream_t s) { mrhs_commit_kernel<<<1, 1, 0, s>>>(a, advance); }
+void launch_mrhs_commit(const MrhsArgs& a, long long set_epoch, cudaStream_t s) {
+    mrhs_commit_kernel<<<1, 1, 0, s>>>(a, set_epoch);
+}
 
 }  // namespace ak

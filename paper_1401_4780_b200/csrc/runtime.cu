@@ -1,6 +1,7 @@
 // Host runtime of the C ABI (runtime.h).
 #include <chrono>
 #include "runtime.h"
+#include "layout.cuh"
 
 #include <algorithm>
 #include <atomic>
@@ -220,6 +221,36 @@ void flag_release(int* host_ptr) {
     if (!host_ptr) return;
     std::lock_guard<std::mutex> lk(g_flag_mu);
     g_flag_free.push_back((int)(host_ptr - g_flag_host));
+}
+
+namespace {
+constexpr int kMirrors = 256;
+std::mutex g_mirror_mu;
+HostMirror* g_mirror_host = nullptr;
+HostMirror* g_mirror_dev = nullptr;
+std::vector<int> g_mirror_free;
+}  // namespace
+
+HostMirror* mirror_acquire(HostMirror** dev_ptr) {
+    std::lock_guard<std::mutex> lk(g_mirror_mu);
+    if (!g_mirror_host) {
+        if (cudaHostAlloc((void**)&g_mirror_host, kMirrors * sizeof(HostMirror), cudaHostAllocMapped) != cudaSuccess)
+            return nullptr;
+        cudaHostGetDevicePointer((void**)&g_mirror_dev, g_mirror_host, 0);
+        std::memset(g_mirror_host, 0, kMirrors * sizeof(HostMirror));
+        for (int k = kMirrors - 1; k >= 0; --k) g_mirror_free.push_back(k);
+    }
+    if (g_mirror_free.empty()) return nullptr;
+    const int k = g_mirror_free.back();
+    g_mirror_free.pop_back();
+    *dev_ptr = g_mirror_dev + k;
+    return g_mirror_host + k;
+}
+
+void mirror_release(HostMirror* host_ptr) {
+    if (!host_ptr) return;
+    std::lock_guard<std::mutex> lk(g_mirror_mu);
+    g_mirror_free.push_back((int)(host_ptr - g_mirror_host));
 }
 
 }  // namespace ak

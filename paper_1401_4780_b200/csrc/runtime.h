@@ -75,4 +75,9 @@ cudaError_t pool_free(void* p, cudaStream_t s);
 int* flag_acquire(int** dev_ptr);
 void flag_release(int* host_ptr);
 
+// pinned, device-mapped record mirrors (layout.cuh HostMirror), same slab scheme
+struct HostMirror;
+HostMirror* mirror_acquire(HostMirror** dev_ptr);
+void mirror_release(HostMirror* host_ptr);
+
 }  // namespace ak

@@ -18,8 +18,12 @@
 #include <thread>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "capi_common.h"
 #include "host_seq.h"
+#include "schedule.h"
 #include "kernels.h"
 
 using namespace ak;
@@ -91,6 +95,8 @@ struct asyrk_system {
     double* scratch = nullptr;
     int* host_flag = nullptr;      // pinned mapped
     int* host_flag_dev = nullptr;
+    HostMirror* mirror = nullptr;  // pinned mapped: latest record for the host-driven monitor schedule
+    HostMirror* mirror_dev = nullptr;
     void* host_scalar = nullptr;   // pinned scratch for small device -> host reads
     // the monitor's structures (row / column SELL, plain CSC) finish on bstream
     // after create returns; every consumer's stream waits on ev_mon_ready
@@ -266,6 +272,8 @@ void free_all(asyrk_system* s) {
         F(s->prep[h].ev_rcp);
     }
     flag_release(s->host_flag);
+    mirror_release(s->mirror);
+    s->mirror = nullptr;
     if (s->host_scalar) cudaFreeHost(s->host_scalar);
     s->host_scalar = nullptr;
     for (int k = 0; k <= kLookahead; ++k) {
@@ -662,6 +670,8 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     // solve buffers
     s->host_flag = flag_acquire(&s->host_flag_dev);
     if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
+    s->mirror = mirror_acquire(&s->mirror_dev);
+    if (!s->mirror) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned record mirror available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
     phase("solve buffers");
@@ -723,6 +733,8 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.rows = s->rsell();
     a.b = s->b;
     a.slot = -1;
+    a.set_epoch = -1;
+    a.mirror = nullptr;
     a.x_alt = nullptr;
     a.force = 0;
     return a;
@@ -786,6 +798,123 @@ struct Timeline {
         }
     }
 };
+
+// Stats, trace and instrument report of a finished solve (the stream is idle).
+asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long long timed, long long launches,
+                          const std::vector<unsigned long long>& chunk_incr, asyrk_trace_out* trace,
+                          asyrk_instrument_out* instr) {
+    cudaStream_t st = s->stream;
+    DevState hs;
+    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+    s->stats.solve_ms = ms;
+    double wms = 0.0;
+    for (long long t = 0; t < timed; ++t) {
+        float w = 0.f;
+        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+        wms += w;
+    }
+    s->stats.worker_ms = wms;
+    s->stats.kernel_launches = launches;
+    s->stats.projections = hs.updates;
+    if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
+
+    write_trace(s, hs, trace, prec);
+    if (instr) {
+        instr->row_updates = hs.updates;
+        unsigned long long inc = 0;
+        if (sp.det) {
+            const long long done = sp.interval > 0 ? (hs.epoch + sp.interval - 1) / sp.interval : 0;
+            for (long long c = 0; c < done && c < (long long)chunk_incr.size(); ++c) inc += chunk_incr[(size_t)c];
+        } else {
+            CK(cudaMemcpy(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost));
+        }
+        instr->increments = (int64_t)inc;
+        launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
+        double mx = 0.0;
+        CK(cudaMemcpyAsync(&mx, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        instr->max_abs_error = mx;
+        instr->tolerance = 1e-9 * (double)std::max<int64_t>(instr->increments, 1);
+        instr->consistent = mx <= instr->tolerance ? 1 : 0;
+    }
+    return ASYRK_OK;
+}
+
+// The async driver with the host-driven monitor schedule (schedule.h). One
+// stream: worker launches of the unmonitored boundaries back to back; at a
+// scheduled boundary the residual monitor (rows + columns/finalize) runs
+// in-stream and writes the record + stop decision; the next boundary's worker
+// launch is enqueued right behind it (it runs only if the record did not stop
+// the solve: st->go) while the host waits for the record's event and reads
+// the mirror to place the next evaluation. So the host's read overlaps a
+// worker epoch, no epoch runs past the stopping boundary, and the returned
+// iterate is the one whose record met the target (parallel.cpp:415-426: the
+// final record is that of the final iterate).
+asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa, int E, int prec, long long max_chunks,
+                           long long launches, asyrk_trace_out* trace, asyrk_instrument_out* instr) {
+    cudaStream_t st = s->stream;
+    mon_wait(s, st);
+    const bool xs = sp.x_star != nullptr;
+    auto epoch_of = [&](long long b) { return std::min<long long>(b * sp.interval, sp.epochs); };
+    cudaEvent_t ev_rec = s->ev_chunk[0];
+    std::memset(s->mirror, 0, sizeof(HostMirror));
+    // boundary 0 (x0)
+    MonitorArgs m0 = monitor_args(s, false, 0, xs);
+    m0.mirror = s->mirror_dev;
+    launch_monitor(m0, prec, st);
+    launches += 2;
+    s->stats.monitor_launches++;
+    CK(cudaEventRecord(ev_rec, st));
+    MonitorSchedule sch;
+    sch.reset(sp.target, sp.every_boundary);
+    long long pending = 0;   // boundary whose record the host has not read yet (-1: none)
+    long long next_mon = 1;  // next boundary to evaluate
+    long long timed = 0;
+    auto enqueue_worker = [&](long long b) {  // chunk b: boundary b -> b + 1
+        wa.epoch0 = epoch_of(b);
+        wa.span0 = epoch_of(b + 1) - wa.epoch0;
+        const bool time_it = timed < kTimedLaunches;
+        if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
+        launch_worker(wa, prec, E, st);
+        if (time_it) {
+            CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed + 1)], st));
+            ++timed;
+        }
+        ++launches;
+        s->stats.worker_launches++;
+    };
+    if (max_chunks > 0) enqueue_worker(0);
+    for (long long b = 0; b < max_chunks; ++b) {
+        // here the worker of chunk b (b -> b + 1) is enqueued; read the pending
+        // record while it runs, then place the next evaluation
+        if (pending >= 0) {
+            CK(cudaEventSynchronize(ev_rec));
+            const volatile HostMirror* hm = s->mirror;
+            if (hm->stop) break;  // the enqueued worker sees go = 0 and exits
+            next_mon = sch.push(pending, hm->r_sq);
+            pending = -1;
+        }
+        const long long b1 = b + 1;
+        if (b1 >= next_mon || b1 == max_chunks) {
+            MonitorArgs ma = monitor_args(s, false, 1, xs);
+            ma.set_epoch = epoch_of(b1);
+            ma.mirror = s->mirror_dev;
+            launch_monitor(ma, prec, st);
+            launches += 2;
+            s->stats.monitor_launches++;
+            CK(cudaEventRecord(ev_rec, st));
+            pending = b1;
+        }
+        if (b1 < max_chunks) enqueue_worker(b1);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(s->ev_end, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    return finish_solve(s, sp, prec, timed, launches, {}, trace, instr);
+}
 
 asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
                        asyrk_instrument_out* instr) {
@@ -888,7 +1017,14 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     }
     CK(cudaGetLastError());
 
-    // async solves overlap the residual monitor with the next epoch's workers
+    // Async solves (default): the host-driven monitor schedule (schedule.h) —
+    // the residual monitor runs in-stream at the boundaries the schedule picks,
+    // the workers of the other boundaries run back to back. ASYRK_OVERLAP=1
+    // selects the round-1 driver instead (a monitor of every boundary it can
+    // take, on its own stream, overlapped with the next epochs).
+    static const bool overlap_env = getenv("ASYRK_OVERLAP") != nullptr;
+    if (!sp.det && !overlap_env)
+        return run_scheduled(s, sp, wa, E, prec, max_chunks, launches, trace, instr);
     static const bool no_overlap = getenv("ASYRK_NO_OVERLAP") != nullptr;
     // (instrumented runs keep the in-stream monitor: restoring the stopping
     // snapshot would desynchronize x from the shadow increments)
@@ -1111,43 +1247,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     CK(cudaStreamSynchronize(st));
     CK(cudaGetLastError());
     tl.dump(tl_path, s->ev_begin);
-
-    DevState hs;
-    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
-    s->stats.solve_ms = ms;
-    double wms = 0.0;
-    for (long long t = 0; t < timed; ++t) {
-        float w = 0.f;
-        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
-        wms += w;
-    }
-    s->stats.worker_ms = wms;
-    s->stats.kernel_launches = launches;
-    s->stats.projections = hs.updates;
-    if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
-
-    write_trace(s, hs, trace, prec);
-    if (instr) {
-        instr->row_updates = hs.updates;
-        unsigned long long inc = 0;
-        if (sp.det) {
-            const long long done = sp.interval > 0 ? (hs.epoch + sp.interval - 1) / sp.interval : 0;
-            for (long long c = 0; c < done && c < (long long)chunk_incr.size(); ++c) inc += chunk_incr[(size_t)c];
-        } else {
-            CK(cudaMemcpy(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost));
-        }
-        instr->increments = (int64_t)inc;
-        launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
-        double mx = 0.0;
-        CK(cudaMemcpyAsync(&mx, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        instr->max_abs_error = mx;
-        instr->tolerance = 1e-9 * (double)std::max<int64_t>(instr->increments, 1);
-        instr->consistent = mx <= instr->tolerance ? 1 : 0;
-    }
-    return ASYRK_OK;
+    return finish_solve(s, sp, prec, timed, launches, chunk_incr, trace, instr);
 }
 
 // validate_config, ref/src/parallel.cpp:56-80 (+ device extensions)
@@ -1880,13 +1980,18 @@ struct asyrk_mrhs {
     int64_t threads = 0;
     double gamma = 1.0;
     uint64_t seed = 0;
-    long long chunks = 0, max_chunks = 0;
+    int sampling = S_UNIFORM;
+    int64_t interval = 1, epochs = 0;
+    long long max_chunks = 0;
+    // host-driven schedule (schedule.h): b = boundaries reached by the enqueued
+    // workers, `due` = the last step ended at an evaluated boundary (its norms
+    // are what the ranks all-reduce), `pending` = boundary of the last commit
+    // whose record the host has not read yet
+    MonitorSchedule sch;
+    long long b = 0, next_mon = 1, pending = -1;
+    bool due = false, stop_seen = false;
+    cudaEvent_t ev_commit = nullptr;
     asyrk_solve_stats stats{};
-    // stop checks one commit behind: commit k records commit_ev[k & 1] on the
-    // solve stream; a chunk queued after a stopping commit sees the device
-    // stop flag and returns at once (same stream), so nothing needs undoing
-    cudaEvent_t commit_ev[2] = {nullptr, nullptr};
-    long long commits = 0;
 };
 
 namespace {
@@ -1914,13 +2019,15 @@ MrhsArgs mrhs_args(asyrk_mrhs* h) {
     a.key0 = (uint32_t)k;
     a.key1 = (uint32_t)(k >> 32);
     a.KL = (int)h->kl;
+    a.sampling = h->sampling;
+    a.mirror = s->mirror_dev;
+    a.max_len = s->max_len;
     return a;
 }
 
 void mrhs_free(asyrk_mrhs* h) {
     if (!h) return;
-    for (cudaEvent_t e : h->commit_ev)
-        if (e) cudaEventDestroy(e);
+    if (h->ev_commit) cudaEventDestroy(h->ev_commit);
     if (h->sys) {
         cudaStream_t st = h->sys->stream;
         for (void* p : {(void*)h->X, (void*)h->B, (void*)h->R, (void*)h->Xstar, (void*)h->part, (void*)h->norms})
@@ -1957,12 +2064,17 @@ asyrk_status mrhs_create_impl(const asyrk_csr_view* A, const float* B, int64_t k
     for (int64_t i = 0; i < s->m; ++i)
         std::memcpy(&bl[(size_t)(i * kl)], B + i * k_total + c0, (size_t)kl * sizeof(float));
     Stager::get().upload(h->B, bl.data(), bl.size() * sizeof(float), s->stream);
+    CK(cudaEventCreateWithFlags(&h->ev_commit, cudaEventDisableTiming));
     CK(cudaStreamSynchronize(s->stream));
     *out = h.release();
     return ASYRK_OK;
 }
 
-// X0 / Xstar are full n x k_total host arrays (row-major); this shard takes its columns
+long long mrhs_epoch_of(const asyrk_mrhs* h, long long b) { return std::min<long long>(b * h->interval, h->epochs); }
+
+// X0 / Xstar are full n x k_total host arrays (row-major); this shard takes its columns.
+// Leaves the initial residual's norms (this shard) in h->norms: the caller
+// all-reduces them, then commits boundary 0.
 asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar) {
     if (!cfg) return fail(ASYRK_E_InvalidArgument, "null config");
     asyrk_system* s = h->sys;
@@ -1972,20 +2084,28 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     if (!(cfg->gamma > 0.0)) return fail(ASYRK_E_InvalidGamma, "gamma must be positive");
     if (cfg->epochs < 0 || cfg->snapshot_interval < 1)
         return fail(ASYRK_E_InvalidArgument, "epochs must be >= 0 and snapshot_interval >= 1");
+    if (cfg->sampling != ASYRK_WITH_REPLACEMENT && cfg->sampling != ASYRK_SLICE_SHUFFLE)
+        return fail(ASYRK_E_InvalidArgument, "mrhs: sampling must be with_replacement or slice_shuffle");
+    if (cfg->sampling == ASYRK_SLICE_SHUFFLE && s->m < cfg->threads)
+        return fail(ASYRK_E_InvalidArgument, "slice_shuffle needs at least one row per worker");
     cudaStream_t st = s->stream;
     mon_wait(s, st);
     AllocStream as(st);
     h->threads = cfg->threads;
     h->gamma = cfg->gamma;
     h->seed = cfg->seed;
-    h->chunks = 0;
-    h->commits = 0;
-    for (cudaEvent_t& e : h->commit_ev)
-        if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->sampling = cfg->sampling == ASYRK_SLICE_SHUFFLE ? S_SLICE : S_UNIFORM;
+    h->interval = cfg->snapshot_interval;
+    h->epochs = cfg->epochs;
     h->max_chunks = cfg->epochs > 0 ? (cfg->epochs + cfg->snapshot_interval - 1) / cfg->snapshot_interval : 0;
+    h->sch.reset(cfg->target_r_sq, cfg->record_every_boundary != 0);
+    h->b = 0;
+    h->next_mon = 1;
+    h->pending = -1;
+    h->stop_seen = false;
     h->stats = asyrk_solve_stats{};
     ensure_records(s, std::max<long long>(256, h->max_chunks + 2));
-    ensure_events(s, 0);
+    ensure_events(s, h->max_chunks);
     const int64_t kl = h->kl;
     if (X0) {
         std::vector<float> xl((size_t)s->n * kl);
@@ -2006,26 +2126,65 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
         CK(cudaStreamSynchronize(st));
     }
     *s->host_flag = 0;
+    std::memset(s->mirror, 0, sizeof(HostMirror));
     CK(cudaEventRecord(s->ev_begin, st));
     launch_state_init(s->st, cfg->epochs, cfg->snapshot_interval, cfg->target_r_sq, st);
     launch_mrhs_monitor(mrhs_args(h), st);  // initial residual -> norms (this shard)
+    h->due = true;
     h->stats.kernel_launches += 4;
     h->stats.monitor_launches++;
     CK(cudaGetLastError());
     return ASYRK_OK;
 }
 
-asyrk_status mrhs_step_impl(asyrk_mrhs* h) {
-    cudaStream_t st = h->sys->stream;
-    const MrhsArgs a = mrhs_args(h);
-    launch_mrhs_worker(a, st);
-    launch_mrhs_monitor(a, st);
-    h->chunks++;
-    h->stats.worker_launches++;
-    h->stats.monitor_launches++;
-    h->stats.kernel_launches += 4;
+// record of the boundary the last step reached (only at evaluated boundaries)
+void mrhs_commit_impl(asyrk_mrhs* h) {
+    if (!h->due) return;
+    launch_mrhs_commit(mrhs_args(h), h->b == 0 ? -1 : mrhs_epoch_of(h, h->b), h->sys->stream);
+    CK(cudaEventRecord(h->ev_commit, h->sys->stream));
+    h->pending = h->b;
+    h->due = false;
+    h->stats.kernel_launches += 1;
     CK(cudaGetLastError());
-    return ASYRK_OK;
+}
+
+// read the pending record (waits for its commit): stop flag + next evaluation
+bool mrhs_read_pending(asyrk_mrhs* h) {
+    if (h->pending < 0) return h->stop_seen;
+    CK(cudaEventSynchronize(h->ev_commit));
+    const volatile HostMirror* hm = h->sys->mirror;
+    if (hm->stop) h->stop_seen = true;
+    else h->next_mon = h->sch.push(h->pending, hm->r_sq);
+    h->pending = -1;
+    return h->stop_seen;
+}
+
+// workers of chunk b (boundary b -> b + 1)
+void mrhs_enqueue_worker(asyrk_mrhs* h) {
+    asyrk_system* s = h->sys;
+    cudaStream_t st = s->stream;
+    MrhsArgs a = mrhs_args(h);
+    a.epoch0 = mrhs_epoch_of(h, h->b);
+    a.span0 = mrhs_epoch_of(h, h->b + 1) - a.epoch0;
+    const long long t = h->stats.worker_launches;
+    const bool time_it = t < kTimedLaunches && (size_t)(2 * t + 1) < s->ev_w.size();
+    if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * t)], st));
+    launch_mrhs_worker(a, st);
+    if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * t + 1)], st));
+    h->b++;
+    h->stats.worker_launches++;
+    h->stats.kernel_launches++;
+    CK(cudaGetLastError());
+}
+
+// the monitor of boundary b if the schedule evaluates it (always the last one)
+void mrhs_maybe_monitor(asyrk_mrhs* h) {
+    h->due = h->b >= h->next_mon || h->b >= h->max_chunks;
+    if (!h->due) return;
+    launch_mrhs_monitor(mrhs_args(h), h->sys->stream);
+    h->stats.monitor_launches++;
+    h->stats.kernel_launches += 3;
+    CK(cudaGetLastError());
 }
 
 asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out) {
@@ -2038,6 +2197,14 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     h->stats.solve_ms = ms;
+    double wms = 0.0;
+    const long long timed = std::min<long long>(h->stats.worker_launches, (long long)s->ev_w.size() / 2);
+    for (long long t = 0; t < timed; ++t) {
+        float w = 0.f;
+        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+        wms += w;
+    }
+    h->stats.worker_ms = wms;
     h->stats.projections = hs.updates;
     h->stats.warps = (int32_t)std::min<int64_t>(h->threads, INT32_MAX);
     if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
@@ -2058,6 +2225,127 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
         }
     }
     if (X_out) CK(cudaMemcpy(X_out, h->X, (size_t)s->n * h->kl * sizeof(float), cudaMemcpyDeviceToHost));
+    return ASYRK_OK;
+}
+
+// ---- NCCL, resolved at run time (libnccl.so.2: the copy already loaded in
+// the process — e.g. PyTorch's — if there is one, else the system library), so
+// the library itself has no link-time NCCL dependency.
+struct NcclApi {
+    bool ok = false;
+    std::string why;
+    decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+    decltype(&ncclCommInitRank) commInitRank = nullptr;
+    decltype(&ncclCommInitAll) commInitAll = nullptr;
+    decltype(&ncclCommDestroy) commDestroy = nullptr;
+    decltype(&ncclAllReduce) allReduce = nullptr;
+    decltype(&ncclGroupStart) groupStart = nullptr;
+    decltype(&ncclGroupEnd) groupEnd = nullptr;
+    decltype(&ncclGetErrorString) errorString = nullptr;
+    decltype(&ncclGetVersion) getVersion = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            api.why = std::string("libnccl.so.2 not loadable: ") + (dlerror() ? dlerror() : "?");
+            return;
+        }
+#define AK_NCCL_SYM(field, name)                                                   \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));            \
+    if (!api.field) {                                                              \
+        api.why = std::string("libnccl.so.2 lacks ") + name;                       \
+        return;                                                                    \
+    }
+        AK_NCCL_SYM(getUniqueId, "ncclGetUniqueId")
+        AK_NCCL_SYM(commInitRank, "ncclCommInitRank")
+        AK_NCCL_SYM(commInitAll, "ncclCommInitAll")
+        AK_NCCL_SYM(commDestroy, "ncclCommDestroy")
+        AK_NCCL_SYM(allReduce, "ncclAllReduce")
+        AK_NCCL_SYM(groupStart, "ncclGroupStart")
+        AK_NCCL_SYM(groupEnd, "ncclGroupEnd")
+        AK_NCCL_SYM(errorString, "ncclGetErrorString")
+        AK_NCCL_SYM(getVersion, "ncclGetVersion")
+#undef AK_NCCL_SYM
+        api.ok = true;
+    });
+    return api;
+}
+
+#define NK(call)                                                                                      \
+    do {                                                                                              \
+        ncclResult_t r_ = (call);                                                                     \
+        if (r_ != ncclSuccess) {                                                                      \
+            ::ak::err_buf() = std::string("NCCL: ") + nccl().errorString(r_) + " at " #call;          \
+            throw ::ak::CudaFail{ASYRK_E_ThreadSpawnFailure};                                         \
+        }                                                                                             \
+    } while (0)
+
+asyrk_status need_nccl() {
+    if (!nccl().ok) return fail(ASYRK_E_ThreadSpawnFailure, nccl().why);
+    return ASYRK_OK;
+}
+
+// The whole sharded solve in C++ for G shards (one per device; G = 1 without
+// NCCL). Per boundary: every shard's workers; at an evaluated boundary the
+// shards' monitors, one all-reduce of {r_sq, g_sq, d_sq} over the shards (a
+// grouped ncclAllReduce on each shard's stream), the commits (identical global
+// record + stop on every shard). The worker launches of the next boundary are
+// enqueued behind the commits before the host reads the record, so the read
+// overlaps an epoch; they run only if the record did not stop the solve.
+asyrk_status mrhs_run(std::vector<asyrk_mrhs*>& hs, const std::vector<int>& devs, const std::vector<ncclComm_t>& comms,
+                      const asyrk_run_config* cfg, const float* X0, const double* Xstar) {
+    const size_t G = hs.size();
+    auto on = [&](size_t g) {
+        if (!devs.empty()) CK(cudaSetDevice(devs[g]));
+    };
+    auto allreduce = [&] {
+        if (comms.empty()) return;
+        NK(nccl().groupStart());
+        for (size_t g = 0; g < G; ++g) {
+            on(g);
+            NK(nccl().allReduce(hs[g]->norms, hs[g]->norms, 3, ncclDouble, ncclSum, comms[g], hs[g]->sys->stream));
+        }
+        NK(nccl().groupEnd());
+    };
+    auto commit_all = [&] {
+        allreduce();
+        for (size_t g = 0; g < G; ++g) {
+            on(g);
+            mrhs_commit_impl(hs[g]);
+        }
+    };
+    for (size_t g = 0; g < G; ++g) {
+        on(g);
+        asyrk_status st = mrhs_begin_impl(hs[g], cfg, X0, Xstar);
+        if (st) return st;
+    }
+    commit_all();  // boundary 0
+    asyrk_mrhs* h0 = hs[0];
+    while (h0->b < h0->max_chunks) {
+        for (size_t g = 0; g < G; ++g) {
+            on(g);
+            mrhs_enqueue_worker(hs[g]);
+        }
+        // the record of the last commit (if any) is read while these workers run
+        on(0);
+        const bool stop = mrhs_read_pending(h0);
+        for (size_t g = 1; g < G; ++g) {
+            hs[g]->stop_seen = stop;
+            hs[g]->next_mon = h0->next_mon;
+            hs[g]->pending = -1;
+        }
+        if (stop) break;  // the workers just enqueued see go = 0 and exit
+        for (size_t g = 0; g < G; ++g) {
+            on(g);
+            mrhs_maybe_monitor(hs[g]);
+        }
+        if (h0->due) commit_all();
+    }
     return ASYRK_OK;
 }
 
@@ -2086,33 +2374,38 @@ asyrk_status asyrk_mrhs_norms(asyrk_mrhs* h, double** dev_norms) {
     return ASYRK_OK;
 }
 
+asyrk_status asyrk_mrhs_due(asyrk_mrhs* h, int32_t* due) {
+    if (!h || !due) return fail(ASYRK_E_InvalidArgument, "null argument");
+    *due = h->due ? 1 : 0;
+    return ASYRK_OK;
+}
+
 asyrk_status asyrk_mrhs_commit(asyrk_mrhs* h, int32_t advance) {
     if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
+    (void)advance;  // the boundary is the one the last step reached (or 0 after begin)
     return guarded([&] {
-        launch_mrhs_commit(mrhs_args(h), advance, h->sys->stream);
-        CK(cudaEventRecord(h->commit_ev[h->commits & 1], h->sys->stream));
-        h->commits++;
-        h->stats.kernel_launches += 1;
-        CK(cudaGetLastError());
+        mrhs_commit_impl(h);
         return ASYRK_OK;
     });
 }
 
 asyrk_status asyrk_mrhs_step(asyrk_mrhs* h) {
     if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
-    return guarded([&] { return mrhs_step_impl(h); });
+    return guarded([&] {
+        mrhs_read_pending(h);
+        mrhs_enqueue_worker(h);
+        mrhs_maybe_monitor(h);
+        return ASYRK_OK;
+    });
 }
 
 asyrk_status asyrk_mrhs_stopped(asyrk_mrhs* h, int32_t* stopped) {
     if (!h || !stopped) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
-        // the previous commit's decision (the latest one right after begin)
-        if (h->commits >= 2)
-            CK(cudaEventSynchronize(h->commit_ev[(h->commits - 2) & 1]));
-        else
-            CK(cudaStreamSynchronize(h->sys->stream));
-        *stopped = *reinterpret_cast<volatile int*>(h->sys->host_flag) ? 1 : 0;
-        if (h->chunks >= h->max_chunks) *stopped = 1;
+        // the decision of the latest commit (each commit's record is read on
+        // its own, after its event): every rank sees the same sequence
+        const bool st = mrhs_read_pending(h);
+        *stopped = (st || h->b >= h->max_chunks) ? 1 : 0;
         return ASYRK_OK;
     });
 }
@@ -2122,26 +2415,13 @@ asyrk_status asyrk_mrhs_finish(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_o
     return guarded([&] { return mrhs_finish_impl(h, trace, X_out); });
 }
 
-// Single-process loop: begin, then chunks of (workers + monitor + commit)
-// with the same bounded lookahead as asyrk_system_solve.
 asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
                               asyrk_trace_out* trace, float* X_out) {
     if (!h) return fail(ASYRK_E_InvalidArgument, "null mrhs");
     return guarded([&] {
-        asyrk_status st = mrhs_begin_impl(h, cfg, X0, Xstar);
+        std::vector<asyrk_mrhs*> hs{h};
+        asyrk_status st = mrhs_run(hs, {}, {}, cfg, X0, Xstar);
         if (st) return st;
-        asyrk_system* s = h->sys;
-        launch_mrhs_commit(mrhs_args(h), 0, s->stream);
-        for (long long k = 0; k < h->max_chunks; ++k) {
-            if (k >= kLookahead) {
-                CK(cudaEventSynchronize(s->ev_chunk[(size_t)(k % (kLookahead + 1))]));
-                if (*reinterpret_cast<volatile int*>(s->host_flag)) break;
-            }
-            st = mrhs_step_impl(h);
-            if (st) return st;
-            launch_mrhs_commit(mrhs_args(h), 1, s->stream);
-            CK(cudaEventRecord(s->ev_chunk[(size_t)(k % (kLookahead + 1))], s->stream));
-        }
         return mrhs_finish_impl(h, trace, X_out);
     });
 }
@@ -2150,6 +2430,121 @@ asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out) 
     if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
     *out = h->stats;
     return ASYRK_OK;
+}
+
+// ---- multi-GPU (NCCL)
+asyrk_status asyrk_nccl_available(int32_t* version) {
+    if (!version) return fail(ASYRK_E_InvalidArgument, "null argument");
+    *version = 0;
+    if (!nccl().ok) return fail(ASYRK_E_ThreadSpawnFailure, nccl().why);
+    int v = 0;
+    nccl().getVersion(&v);
+    *version = v;
+    return ASYRK_OK;
+}
+
+asyrk_status asyrk_nccl_get_unique_id(char* id) {
+    if (!id) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        asyrk_status st = need_nccl();
+        if (st) return st;
+        ncclUniqueId u;
+        NK(nccl().getUniqueId(&u));
+        static_assert(sizeof(ncclUniqueId) == ASYRK_NCCL_UNIQUE_ID_BYTES, "ncclUniqueId size");
+        std::memcpy(id, &u, sizeof(u));
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_nccl_comm_init_rank(void** comm, int32_t nranks, const char* id, int32_t rank) {
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(ASYRK_E_InvalidArgument, "nccl_comm_init_rank: need comm, id and 0 <= rank < nranks");
+    return guarded([&] {
+        asyrk_status st = need_nccl();
+        if (st) return st;
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        ncclComm_t c = nullptr;
+        NK(nccl().commInitRank(&c, nranks, u, rank));
+        *comm = c;
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_nccl_comm_destroy(void* comm) {
+    if (!comm) return ASYRK_OK;
+    return guarded([&] {
+        asyrk_status st = need_nccl();
+        if (st) return st;
+        NK(nccl().commDestroy(static_cast<ncclComm_t>(comm)));
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_mrhs_solve_nccl(asyrk_mrhs* h, const asyrk_run_config* cfg, void* comm, const float* X0,
+                                   const double* Xstar, asyrk_trace_out* trace, float* X_out) {
+    if (!h || !comm) return fail(ASYRK_E_InvalidArgument, "null mrhs or communicator");
+    return guarded([&] {
+        asyrk_status st = need_nccl();
+        if (st) return st;
+        std::vector<asyrk_mrhs*> hs{h};
+        st = mrhs_run(hs, {}, {static_cast<ncclComm_t>(comm)}, cfg, X0, Xstar);
+        if (st) return st;
+        return mrhs_finish_impl(h, trace, X_out);
+    });
+}
+
+asyrk_status asyrk_mrhs_solve_devices(const asyrk_csr_view* A, const float* B, int64_t k_total, const int32_t* devices,
+                                      int32_t ndev, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
+                                      asyrk_trace_out* trace, float* X_out, asyrk_solve_stats* stats) {
+    if (!A || !B || !devices || ndev < 1 || !cfg) return fail(ASYRK_E_InvalidArgument, "null argument or ndev < 1");
+    if (k_total % ndev) return fail(ASYRK_E_InvalidArgument, "mrhs: k_total must split evenly over the devices");
+    return guarded([&] {
+        asyrk_status st = need_nccl();
+        if (st) return st;
+        int prev = 0;
+        CK(cudaGetDevice(&prev));
+        std::vector<int> devs(devices, devices + ndev);
+        std::vector<asyrk_mrhs*> hs((size_t)ndev, nullptr);
+        std::vector<ncclComm_t> comms((size_t)ndev, nullptr);
+        auto cleanup = [&] {
+            for (size_t g = 0; g < hs.size(); ++g) {
+                cudaSetDevice(devs[g]);
+                if (comms[g]) nccl().commDestroy(comms[g]);
+                mrhs_free(hs[g]);
+            }
+            cudaSetDevice(prev);
+        };
+        try {
+            const int64_t kl = k_total / ndev;
+            for (int g = 0; g < ndev; ++g) {
+                CK(cudaSetDevice(devs[(size_t)g]));
+                st = mrhs_create_impl(A, B, k_total, g * kl, (g + 1) * kl, nullptr, &hs[(size_t)g]);
+                if (st) {
+                    cleanup();
+                    return st;
+                }
+            }
+            NK(nccl().commInitAll(comms.data(), ndev, devs.data()));
+            st = mrhs_run(hs, devs, comms, cfg, X0, Xstar);
+            std::vector<float> xl;
+            for (int g = 0; g < ndev && !st; ++g) {
+                CK(cudaSetDevice(devs[(size_t)g]));
+                asyrk_mrhs* h = hs[(size_t)g];
+                xl.assign((size_t)h->sys->n * kl, 0.f);
+                st = mrhs_finish_impl(h, g == 0 ? trace : nullptr, X_out ? xl.data() : nullptr);
+                if (!st && X_out)
+                    for (int64_t j = 0; j < h->sys->n; ++j)
+                        std::memcpy(X_out + j * k_total + g * kl, &xl[(size_t)(j * kl)], (size_t)kl * sizeof(float));
+                if (!st && stats && g == 0) *stats = h->stats;
+            }
+        } catch (...) {
+            cleanup();
+            throw;
+        }
+        cleanup();
+        return st;
+    });
 }
 
 }  // extern "C"

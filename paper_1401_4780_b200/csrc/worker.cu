@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
     using T = X;  // arithmetic type of the projection (x's precision)
     const DevState* st = a.st;
     if (!st->go) return;  // decided on the worker stream before this launch
-    const long long epoch = st->epoch;
-    const long long span = chunk_span(st);
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
     if (span <= 0) return;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (warp >= a.W) return;
@@ -229,8 +229,8 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
     using T = X;
     const DevState* st = a.st;
     if (!st->go) return;
-    const long long epoch = st->epoch;
-    const long long span = chunk_span(st);
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
     if (span <= 0) return;
     const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (warp >= a.W) return;

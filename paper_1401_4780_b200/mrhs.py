@@ -7,6 +7,14 @@ The only collective is the stopping test: after each snapshot the ranks
 all-reduce (sum) their shard's {||R||_F^2, ||A^T R||_F^2, ||X - X*||_F^2}
 (NCCL on the solve stream for CUDA tensors), then every rank's device-side
 commit takes the same global decision ||R||_F^2 <= tol^2 ||B||_F^2.
+Snapshots are taken at the boundaries the host-driven monitor schedule picks
+(csrc/schedule.h); backend.due() says whether a step ended at one.
+
+The same loop runs natively (no Python per epoch) through
+capi.MultiRHS.solve_nccl (one process per GPU, an NCCL communicator the
+library creates from a unique id the ranks share) and capi.mrhs_solve_devices
+(one process, several GPUs); solve_sharded_native below wires the former to
+torch.distributed.
 
 The loop is written against a small backend protocol so that the host logic
 (sharding, the global stop, identical records on every rank) is testable on
@@ -68,6 +76,9 @@ class CudaShardBackend:
     def step(self):
         self.impl.step()
 
+    def due(self):
+        return self.impl.due()
+
     def stopped(self):
         return self.impl.stopped()
 
@@ -102,15 +113,44 @@ def solve_sharded(backend, group=None, all_reduce=None, **cfg):
     epochs = int(cfg.get("epochs", 100))
     interval = max(int(cfg.get("snapshot_interval", 1)), 1)
     max_chunks = (epochs + interval - 1) // interval if epochs > 0 else 0
-    if not backend.stopped():
-        for _ in range(max_chunks):
-            backend.step()
+    for _ in range(max_chunks):
+        if backend.stopped():
+            break
+        backend.step()
+        # only the boundaries the monitor schedule evaluates carry norms; the
+        # schedule is a function of the all-reduced records, so every rank
+        # takes the same branch
+        if backend.due():
             all_reduce(backend.norms())
             backend.commit(True)
-            if backend.stopped():
-                break
     return backend.finish()
 
 
 def relative_residual(trace, B_frob_sq):
     return float(np.sqrt(trace["r_sq"][-1] / B_frob_sq))
+
+
+def solve_sharded_native(shard, group=None, **cfg):
+    """This rank's shard through the native NCCL driver (asyrk_mrhs_solve_nccl):
+    rank 0 creates the NCCL unique id, torch.distributed broadcasts it, the
+    library builds its own communicator on the current device, and the whole
+    loop (workers, monitor, ncclAllReduce, commit) runs in C++. With no
+    process group: a 1-rank communicator."""
+    import torch
+    import torch.distributed as dist
+
+    from . import capi
+
+    if dist.is_available() and dist.is_initialized():
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = capi.nccl_unique_id() if rank == 0 else bytes(capi.NCCL_UNIQUE_ID_BYTES)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, src=0, group=group)
+        uid = bytes(t.cpu().tolist())
+    else:
+        world, rank, uid = 1, 0, capi.nccl_unique_id()
+    comm = capi.NcclComm(world, uid, rank)
+    try:
+        return shard.solve_nccl(comm, **cfg)
+    finally:
+        comm.close()

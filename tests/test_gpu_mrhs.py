@@ -87,20 +87,26 @@ def test_sharded_protocol_global_stop(problem, world):
         ar(s.norms())
     for s in shards:
         s.commit(False)
+    evaluated = 0
     for _ in range(400):
-        for s in shards:
-            s.step()
-        for s in shards:
-            ar(s.norms())
-        for s in shards:
-            s.commit(True)
         stops = [s.stopped() for s in shards]
         assert len(set(stops)) == 1  # identical global decision
         if stops[0]:
             break
+        for s in shards:
+            s.step()
+        dues = [s.due() for s in shards]
+        assert len(set(dues)) == 1  # identical schedule (a function of the all-reduced records)
+        if dues[0]:
+            evaluated += 1
+            for s in shards:
+                ar(s.norms())
+            for s in shards:
+                s.commit(True)
     res = [s.finish() for s in shards]
     assert all(np.array_equal(res[0]["epoch_index"], r["epoch_index"]) for r in res)
     assert all(np.array_equal(res[0]["r_sq"], r["r_sq"]) for r in res)
+    assert len(res[0]["r_sq"]) == evaluated + 1  # boundary 0 + every evaluated boundary
     X = np.concatenate([r["X"] for r in res], axis=1)
     R = _residual(A, X, B)
     assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
@@ -122,3 +128,97 @@ def test_bad_shard_width_rejected(problem):
     A, B, _ = problem
     with pytest.raises(capi.AsyrkError, match="InvalidArgument"):
         capi.MultiRHS(A, B, 0, 48)
+
+
+def test_slice_shuffle_sampling_converges(problem):
+    # the reference's default ParSampling (parallel.cpp:355-363): each worker
+    # reshuffles its slice of the rows every pass
+    A, B, Xs = problem
+    S = capi.MultiRHS(A, B, 0, 64)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    t = S.solve(threads=2048, epochs=400, target=TOL * TOL * bb, seed=4, X_star=Xs, sampling=capi.SLICE_SHUFFLE)
+    S.close()
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+    assert np.linalg.norm(t["X"] - Xs) / np.linalg.norm(Xs) <= 10 * TOL
+    # exact epochs: every launch processes m row events per epoch
+    assert int(t["updates_applied"][-1]) == A.m * int(t["epoch_index"][-1])
+
+
+@pytest.mark.parametrize("kl", [2, 4, 16])
+def test_narrow_shards_converge(problem, kl):
+    # the shard widths of 32 / 16 / 4 GPUs (float2 and float4 lane layouts)
+    A, B, Xs = problem
+    S = capi.MultiRHS(A, B, 0, kl)
+    bb = float((B[:, :kl].astype(np.float64) ** 2).sum())
+    t = S.solve(threads=2048, epochs=400, target=TOL * TOL * bb, seed=5)
+    S.close()
+    R = _residual(A, t["X"], B[:, :kl])
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+
+
+def test_monitor_schedule_records(problem):
+    # tolerance runs evaluate a subset of boundaries (the last one meets the
+    # target, the one before did not); a fixed epoch budget (target 0) and
+    # record_every_boundary evaluate every boundary
+    A, B, Xs = problem
+    bb = float((B.astype(np.float64) ** 2).sum())
+    S = capi.MultiRHS(A, B, 0, 64)
+    t = S.solve(threads=2048, epochs=400, target=TOL * TOL * bb, seed=3)
+    ep = t["epoch_index"]
+    assert ep[0] == 0 and np.all(np.diff(ep) > 0)
+    assert t["r_sq"][-1] <= TOL * TOL * bb < t["r_sq"][-2]
+    assert len(ep) < ep[-1] + 1
+    t2 = S.solve(threads=2048, epochs=7, target=0.0, seed=3)
+    assert list(t2["epoch_index"]) == list(range(8))
+    t3 = S.solve(threads=2048, epochs=400, target=TOL * TOL * bb, seed=3, record_every_boundary=1)
+    assert list(t3["epoch_index"]) == list(range(int(t3["epoch_index"][-1]) + 1))
+    S.close()
+
+
+def test_native_nccl_driver_one_rank(problem):
+    # asyrk_mrhs_solve_nccl with a 1-rank communicator the library builds from
+    # its own unique id: the NCCL all-reduce path of a multi-GPU job, on one GPU
+    A, B, Xs = problem
+    bb = float((B.astype(np.float64) ** 2).sum())
+    assert capi.nccl_version() >= 21800
+    comm = capi.NcclComm(1, capi.nccl_unique_id(), 0)
+    S = capi.MultiRHS(A, B, 0, 64)
+    t = S.solve_nccl(comm, threads=2048, epochs=400, target=TOL * TOL * bb, seed=3, X_star=Xs,
+                     sampling=capi.SLICE_SHUFFLE)
+    S.close()
+    comm.close()
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+    assert np.sqrt(t["dist_sq"][-1]) / np.linalg.norm(Xs) <= 10 * TOL
+
+
+def test_solve_devices_single_process():
+    # asyrk_mrhs_solve_devices: one process, ncclCommInitAll over the listed
+    # GPUs; on a 1-GPU box the device list is [0] (NCCL with one rank)
+    import torch
+
+    A, B, Xs = capi.generate_fixed_theta(20000, 10000, 20, seed=77, k=8)
+    B = B.astype(np.float32)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    devs = list(range(min(torch.cuda.device_count(), 2)))
+    t = capi.mrhs_solve_devices(A, B, devs, threads=1024, epochs=400, target=TOL * TOL * bb, seed=3, X_star=Xs)
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+    assert np.linalg.norm(t["X"] - Xs) / np.linalg.norm(Xs) <= 10 * TOL
+
+
+def test_solve_devices_two_gpus():
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    A, B, Xs = capi.generate_fixed_theta(50000, 25000, 20, seed=1005, k=64)
+    B = B.astype(np.float32)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    t = capi.mrhs_solve_devices(A, B, [0, 1], threads=2048, epochs=400, target=TOL * TOL * bb, seed=3)
+    R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL

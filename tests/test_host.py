@@ -34,7 +34,7 @@ def test_c_abi_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(L, name), f"{name} declared in include/ but not exported"
     assert set(capi.EXPORTED) <= declared
-    assert L.asyrk_abi_version() == 1
+    assert L.asyrk_abi_version() == 2
 
 
 def test_exported_symbols_via_nm():

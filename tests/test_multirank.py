@@ -67,6 +67,9 @@ class NumpyShard:
     def stopped(self):
         return self.stop
 
+    def due(self):
+        return True
+
     def finish(self):
         return dict(epoch_index=np.array([r[0] for r in self.records]), r_sq=np.array([r[1] for r in self.records]),
                     X=self.X, local_r_sq=self.local_r_sq)
