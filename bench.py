@@ -384,7 +384,7 @@ def run_gpu(args):
                              "call": "System.solve(..., instrument=True): the increment audit of "
                                      "solve_parallel's InstrumentReport (parallel.cpp:94-106)"},
             "gpu_launches": launches,
-            "roofline": roofline(W, worker_rate, avg_launch_ms, value),
+            "roofline": roofline(S, W, worker_rate, avg_launch_ms, value),
             "clocks": clk.summary(),
         }
         if c5 is not None:
@@ -400,7 +400,7 @@ def run_gpu(args):
     return 0
 
 
-def roofline(W, worker_rate, avg_launch_ms, step_rate):
+def roofline(S, W, worker_rate, avg_launch_ms, step_rate):
     """The binding ceiling of K2: R_proj = min(BW_HBM / S_A, R_x),
     R_x = the x-side traffic of a projection alone (30 random L2 gathers ->
     warp reduce -> 30 random red.add.f64), measured live at the worker's warp
@@ -409,9 +409,11 @@ def roofline(W, worker_rate, avg_launch_ms, step_rate):
     contract; the proj/s figures sit beside it."""
     from paper_1401_4780_b200 import capi
 
-    rx1 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 1024, 0) for _ in range(3))
-    rx2 = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 1024, 16) for _ in range(3))
+    # on the solver's own x buffer (same address / pages, L2-resident) at the worker's warp count
+    rx1 = max(S.microbench_xside(W, 1024, 0) for _ in range(3))
+    rx2 = max(S.microbench_xside(W, 1024, 16) for _ in range(3))
     rx = max(rx1, rx2)
+    rx_alloc = max(capi.microbench_xside(CFG2["n"], CFG2["theta"], capi.F64, W, 1024, 16) for _ in range(3))
     peak_hbm, hbm_kind = measured_peak_hbm()
     r_hbm = peak_hbm * 1e9 / S_A_F64
     r_proj = min(r_hbm, rx)
@@ -422,11 +424,13 @@ def roofline(W, worker_rate, avg_launch_ms, step_rate):
            "frac": worker_rate / r_proj, "traffic": dram,
            "kernel": "K2 worker_kernel (csrc/worker.cu)",
            "achieved_proj_per_s": worker_rate, "peak_proj_per_s": r_proj,
-           "R_x_proj_per_s": {"rows_in_flight_1": rx1, "rows_in_flight_2": rx2},
+           "R_x_proj_per_s": {"rows_in_flight_1": rx1, "rows_in_flight_2": rx2,
+                              "fresh_buffer_rows_in_flight_2": rx_alloc},
            "R_hbm_proj_per_s": r_hbm,
            "step_frac": step_rate / r_proj,
-           "peak_source": "x-side microbenchmark (asyrk_microbench_xside) measured live in this run, the faster of "
-                          "1 and 2 rows in flight per warp; ncu counters of it in profiles/",
+           "peak_source": "x-side microbenchmark measured live in this run on the solver's own x buffer "
+                          "(asyrk_system_microbench_xside), the faster of 1 and 2 rows in flight per warp; ncu "
+                          "counters of it in profiles/",
            "achieved_source": "credited projections / CUDA-event time of the worker launches (K2) in the timed steps",
            "avg_worker_launch_ms": avg_launch_ms,
            "x_bytes_per_proj": X_BYTES_F64, "alg_bytes_per_proj": BYTES_PER_PROJ_F64}

@@ -16,8 +16,8 @@
  *   asyrk_sweep_threads      sweep_threads           ref/include/asyrk/parallel.hpp:73-75
  *   asyrk_residuals          residuals               ref/include/asyrk/csr.hpp:89-90
  *   asyrk_power_iteration_lambda_max
- *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:131-132
- *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:47-60 (the
+ *                            power_iteration_lambda_max  ref/include/asyrk/stats.hpp:46-47
+ *   asyrk_compute_stats      compute_stats           ref/include/asyrk/stats.hpp:42 (the
  *                                                    structural fields; ref/src/stats.cpp:52-130;
  *                                                    the dense spectrum: include/asyrk_dense.h)
  *   asyrk_simulate           simulate                ref/include/asyrk/delay_sim.hpp:61-71
@@ -185,11 +185,11 @@ asyrk_status asyrk_rk_solve(const asyrk_csr_view* A, const double* b, const doub
 asyrk_status asyrk_residuals(const asyrk_csr_view* A, const double* x, const double* b, double* r_sq,
                              double* grad_sq);
 
-/* power_iteration_lambda_max (stats.hpp:131-132), same start vector. */
+/* power_iteration_lambda_max (stats.hpp:46-47), same start vector. */
 asyrk_status asyrk_power_iteration_lambda_max(const asyrk_csr_view* A, double tol, int64_t max_iters,
                                               double* lambda_max);
 
-/* compute_stats (stats.hpp:47-60, stats.cpp:52-130) with exact_spectral =
+/* compute_stats (stats.hpp:42, stats.cpp:52-130) with exact_spectral =
  * false: every field of SystemStats except lambda_min / sigma_r (those come
  * from asyrk_dense_spectrum). mu, nu, delta, alpha, frob_sq, l_max, l_res and
  * theta are bit-identical to the reference; lambda_max is the device power
@@ -300,6 +300,13 @@ asyrk_status asyrk_system_monte_carlo_ratios(asyrk_system* sys, const double* x0
                                              int64_t runs, double* mean_r_sq, double* ratios);
 /* compute_stats on a resident fp64 system (see asyrk_compute_stats). */
 asyrk_status asyrk_system_compute_stats(asyrk_system* sys, double tol, int64_t max_iters, asyrk_stats_out* out);
+/* The async workers' own row draws (tests and diagnostics): rows_out[w *
+ * per_warp + j] = the row warp w of a `warps`-warp solve with `seed` draws at
+ * position j of epoch `epoch` (sampling: with_replacement, slice_shuffle —
+ * a permutation of the warp's slice per pass — or norm_proportional through
+ * the device alias table, ref kaczmarz.cpp:14-69). */
+asyrk_status asyrk_system_sample_rows(asyrk_system* sys, int32_t sampling, uint64_t seed, int64_t warps, int64_t epoch,
+                                      int64_t per_warp, int32_t* rows_out);
 /* Largest number of worker warps that are co-resident for this system. */
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
 
@@ -382,6 +389,11 @@ asyrk_status asyrk_mrhs_solve_devices(const asyrk_csr_view* A, const float* B, i
  * keeps 2 rows in flight per warp (the K2 worker's shape). */
 asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t precision, int32_t warps,
                                     int64_t proj_per_warp, int32_t mode, double* proj_per_s, double* kernel_ms);
+/* The same on a resident system's own x buffer (address, footprint, its row
+ * length as theta, x's precision) on its stream; x is re-initialised by every
+ * solve, so the ~1e-30 perturbation it leaves does not matter. */
+asyrk_status asyrk_system_microbench_xside(asyrk_system* sys, int32_t warps, int64_t proj_per_warp, int32_t mode,
+                                           double* proj_per_s, double* kernel_ms);
 
 #ifdef __cplusplus
 }

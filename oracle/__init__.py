@@ -256,6 +256,17 @@ class _RefLib(_Lib):
         L.ref_lsq_solve.argtypes = [C_.c_void_p, _f64p, C_.c_double, C_.c_double, C_.c_double, C_.c_int64,
                                     C_.c_double, C_.c_uint64, C_.c_int, _f64p, _f64p, _f64p, C_.POINTER(_Trace)]
 
+    def trace_roundtrip(self, jsonl):
+        """The reference's Trace::from_jsonl then to_jsonl / to_csv (trace.cpp:33-112)."""
+        L = self.L
+        L.ref_trace_roundtrip.argtypes = [C_.c_char_p, C_.c_char_p, C_.c_int64, C_.c_char_p, C_.c_int64, _i64p, _i64p]
+        cap = 4 * len(jsonl) + 4096
+        bj, bc = C_.create_string_buffer(cap), C_.create_string_buffer(cap)
+        lj, lc = C_.c_int64(), C_.c_int64()
+        self._check(L.ref_trace_roundtrip(jsonl.encode(), bj, cap, bc, cap, C_.byref(lj), C_.byref(lc)))
+        assert lj.value <= cap and lc.value <= cap
+        return bj.raw[:lj.value].decode(), bc.raw[:lc.value].decode()
+
     def _check(self, st):
         if st:
             raise OracleError(st, self.L.ref_last_error().decode())

@@ -14,6 +14,7 @@
 //   Matrix Market / vector / instance I/O      (ref/src/io.cpp:41-183)
 //   augment / lsq_solve / optimal_params       (ref/src/lsq.cpp:12-170)
 // Nothing here is shipped; the product never links this library.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -558,6 +559,22 @@ int ref_lsq_solve(void* hp, const double* b, double zeta, double phi, double sig
         scal[2] = r.phi;
         scal[3] = r.sigma_r;
         if (tr) dump_trace(r.trace, tr);
+    });
+}
+
+// Trace serialization (ref/src/trace.cpp:33-112): parse a JSONL trace with
+// the reference's Trace::from_jsonl and write it back with its to_jsonl and
+// to_csv, so the product's serializers can be byte-compared on the same
+// content. out buffers: cap bytes each; *len_* = the full lengths.
+int ref_trace_roundtrip(const char* text, char* out_jsonl, int64_t cap_j, char* out_csv, int64_t cap_c,
+                        int64_t* len_j, int64_t* len_c) {
+    return guarded([&] {
+        const Trace t = Trace::from_jsonl(text);
+        const std::string j = t.to_jsonl(), c = t.to_csv();
+        *len_j = (int64_t)j.size();
+        *len_c = (int64_t)c.size();
+        if (cap_j > 0) std::memcpy(out_jsonl, j.data(), std::min<size_t>(j.size(), (size_t)cap_j));
+        if (cap_c > 0) std::memcpy(out_csv, c.data(), std::min<size_t>(c.size(), (size_t)cap_c));
     });
 }
 

@@ -259,6 +259,8 @@ def lib():
         L.asyrk_mrhs_solve.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p]
         L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_mrhs_due.argtypes = [sp, _i32p]
+        L.asyrk_system_microbench_xside.argtypes = [sp, C.c_int32, C.c_int64, C.c_int32, _f64p, _f64p]
+        L.asyrk_system_sample_rows.argtypes = [sp, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, _i32p]
         L.asyrk_nccl_available.argtypes = [_i32p]
         L.asyrk_nccl_get_unique_id.argtypes = [C.c_char_p]
         L.asyrk_nccl_comm_init_rank.argtypes = [C.POINTER(C.c_void_p), C.c_int32, C.c_char_p, C.c_int32]
@@ -286,7 +288,7 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
+    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
     "asyrk_nccl_comm_init_rank", "asyrk_nccl_comm_destroy", "asyrk_mrhs_solve_nccl", "asyrk_mrhs_solve_devices",
     "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
@@ -302,6 +304,8 @@ class MultiRHS:
 
     def __init__(self, A: "HostCsr", B, c0, c1, stream=None):
         B = np.ascontiguousarray(B, dtype=np.float32)
+        if B.ndim != 2 or B.shape[0] != A.m:
+            raise AsyrkError(6, f"B has shape {B.shape}, expected ({A.m}, k)")
         self.m, self.n = A.m, A.n
         self.k_total = B.shape[1]
         self.c0, self.c1 = c0, c1
@@ -323,8 +327,8 @@ class MultiRHS:
 
     def begin(self, X0=None, X_star=None, **cfg):
         self._cfg = _run_config(**cfg)
-        self._x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
-        self._xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        self._x0 = _mat(X0, (self.n, self.k_total), np.float32, "X0") if X0 is not None else None
+        self._xs = _mat(X_star, (self.n, self.k_total), np.float64, "X_star") if X_star is not None else None
         check(lib().asyrk_mrhs_begin(self.h, C.byref(self._cfg),
                                      self._x0.ctypes.data_as(C.POINTER(C.c_float)) if self._x0 is not None else None,
                                      _ptr(self._xs, _f64p)))
@@ -365,8 +369,8 @@ class MultiRHS:
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
         tr = _Trace(0, cap, want_x=False)
         X = np.zeros((self.n, self.c1 - self.c0), np.float32)
-        x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
-        xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        x0 = _mat(X0, (self.n, self.k_total), np.float32, "X0") if X0 is not None else None
+        xs = _mat(X_star, (self.n, self.k_total), np.float64, "X_star") if X_star is not None else None
         check(lib().asyrk_mrhs_solve(self.h, C.byref(c), x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None
                                      else None, _ptr(xs, _f64p), C.byref(tr.out),
                                      X.ctypes.data_as(C.POINTER(C.c_float))))
@@ -381,8 +385,8 @@ class MultiRHS:
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
         tr = _Trace(0, cap, want_x=False)
         X = np.zeros((self.n, self.c1 - self.c0), np.float32)
-        x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
-        xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+        x0 = _mat(X0, (self.n, self.k_total), np.float32, "X0") if X0 is not None else None
+        xs = _mat(X_star, (self.n, self.k_total), np.float64, "X_star") if X_star is not None else None
         check(lib().asyrk_mrhs_solve_nccl(self.h, C.byref(c), C.c_void_p(comm.handle),
                                           x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None else None,
                                           _ptr(xs, _f64p), C.byref(tr.out), X.ctypes.data_as(C.POINTER(C.c_float))))
@@ -444,9 +448,11 @@ def mrhs_solve_devices(A, B, devices, X0=None, X_star=None, **cfg):
     c = _run_config(**cfg)
     cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
     tr = _Trace(0, cap, want_x=False)
+    if B.ndim != 2 or B.shape[0] != A.m:
+        raise AsyrkError(6, f"B has shape {B.shape}, expected ({A.m}, k)")
     X = np.zeros((A.n, k), np.float32)
-    x0 = np.ascontiguousarray(X0, dtype=np.float32) if X0 is not None else None
-    xs = np.ascontiguousarray(X_star, dtype=np.float64) if X_star is not None else None
+    x0 = _mat(X0, (A.n, k), np.float32, "X0") if X0 is not None else None
+    xs = _mat(X_star, (A.n, k), np.float64, "X_star") if X_star is not None else None
     st = SolveStats()
     check(lib().asyrk_mrhs_solve_devices(C.byref(A.view()), B.ctypes.data_as(C.POINTER(C.c_float)), k,
                                          devs.ctypes.data_as(_i32p), len(devs), C.byref(c),
@@ -465,6 +471,24 @@ def microbench_xside(n, theta, precision=F64, warps=4736, proj_per_warp=256, mod
     check(lib().asyrk_microbench_xside(n, theta, precision, warps, proj_per_warp, mode, C.byref(rate),
                                        C.byref(ms)))
     return rate.value
+
+
+def _mat(a, shape, dtype, name):
+    """Contiguous host matrix of exactly `shape` (DimensionMismatch otherwise)."""
+    v = np.ascontiguousarray(a, dtype=dtype)
+    if v.shape != tuple(shape):
+        raise AsyrkError(6, f"{name} has shape {v.shape}, expected {tuple(shape)}")
+    return v
+
+
+def _vec(a, n, name):
+    """Contiguous float64 host vector of exactly n entries (the C ABI copies n
+    doubles from it): DimensionMismatch otherwise, like the reference
+    (parallel.cpp:57-61)."""
+    v = np.ascontiguousarray(a, dtype=np.float64)
+    if v.ndim != 1 or v.shape[0] != n:
+        raise AsyrkError(6, f"{name} has {v.size} entries, expected {n}")
+    return v
 
 
 def check(status: int):
@@ -561,7 +585,7 @@ class System:
         self.A = A
         self.m, self.n = A.m, A.n
         self.precision = precision
-        self._b = np.ascontiguousarray(b, dtype=np.float64) if b is not None else None
+        self._b = _vec(b, A.m, "b") if b is not None else None
         h = C.c_void_p()
         check(lib().asyrk_system_create(C.byref(A.view()), _ptr(self._b, _f64p), precision,
                                         C.c_void_p(stream) if stream else None, C.byref(h)))
@@ -585,16 +609,16 @@ class System:
             pass
 
     def set_rhs(self, b):
-        self._b = np.ascontiguousarray(b, dtype=np.float64)
+        self._b = _vec(b, self.m, "b")
         check(lib().asyrk_system_set_rhs(self.h, _ptr(self._b, _f64p)))
 
     def solve(self, x0=None, instrument=False, want_x=True, **cfg):
         xs = cfg.pop("x_star", None)
-        xs = np.ascontiguousarray(xs, dtype=np.float64) if xs is not None else None
+        xs = _vec(xs, self.n, "x_star") if xs is not None else None
         c = _run_config(x_star=xs, **cfg)
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
         tr = _Trace(self.n, cap, want_x)
-        x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+        x0a = _vec(x0, self.n, "x0") if x0 is not None else None
         rep = InstrumentOut()
         check(lib().asyrk_system_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out),
                                        C.byref(rep) if instrument else None))
@@ -605,28 +629,41 @@ class System:
                                    consistent=bool(rep.consistent))
         return d
 
+    def microbench_xside(self, warps, proj_per_warp=1024, mode=0):
+        """R_x on this system's own x buffer (asyrk_system_microbench_xside): proj/s."""
+        rate, ms = C.c_double(), C.c_double()
+        check(lib().asyrk_system_microbench_xside(self.h, warps, proj_per_warp, mode, C.byref(rate), C.byref(ms)))
+        return rate.value
+
+    def sample_rows(self, sampling, seed, warps, per_warp, epoch=0):
+        """The async workers' own row draws: (warps, per_warp) int32 array (asyrk_system_sample_rows)."""
+        out = np.zeros((warps, per_warp), np.int32)
+        check(lib().asyrk_system_sample_rows(self.h, sampling, seed, warps, epoch, per_warp,
+                                             out.ctypes.data_as(_i32p)))
+        return out
+
     def rk_solve(self, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):
-        xs = np.ascontiguousarray(x_star, dtype=np.float64) if x_star is not None else None
+        xs = _vec(x_star, self.n, "x_star") if x_star is not None else None
         c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
         tr = _Trace(self.n, max(max_epochs, 0) + 2)
-        x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+        x0a = _vec(x0, self.n, "x0") if x0 is not None else None
         check(lib().asyrk_system_rk_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out)))
         return tr.result(xs is not None)
 
     def residuals(self, x):
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        x = _vec(x, self.n, "x")
         rs, gs = C.c_double(), C.c_double()
         check(lib().asyrk_system_residuals(self.h, _ptr(x, _f64p), C.byref(rs), C.byref(gs)))
         return rs.value, gs.value
 
     def multiply(self, x):
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        x = _vec(x, self.n, "x")
         y = np.zeros(self.m)
         check(lib().asyrk_system_multiply(self.h, _ptr(x, _f64p), _ptr(y, _f64p)))
         return y
 
     def multiply_transpose(self, x):
-        x = np.ascontiguousarray(x, dtype=np.float64)
+        x = _vec(x, self.m, "x")
         y = np.zeros(self.n)
         check(lib().asyrk_system_multiply_transpose(self.h, _ptr(x, _f64p), _ptr(y, _f64p)))
         return y
@@ -638,13 +675,13 @@ class System:
 
     def simulate(self, x0, gamma, tau, delay, iterations, seed, variant, **opts):
         """simulate (ref delay_sim.cpp:71-228) with the system's b."""
-        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        x0 = _vec(x0, self.n, "x0")
         cfg = _sim_config(gamma, tau, delay, iterations, seed, variant, **opts)
         return _sim_call(lambda o: lib().asyrk_system_simulate(self.h, _ptr(x0, _f64p), C.byref(cfg), C.byref(o)),
                          self.n, self.m, cfg)
 
     def monte_carlo_ratios(self, x0, gamma, tau, delay, iterations, runs, base_seed, variant="single_component"):
-        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        x0 = _vec(x0, self.n, "x0")
         cfg = _sim_config(gamma, tau, delay, iterations, base_seed, variant)
         mean, ratios = np.zeros(iterations + 1), np.zeros(max(iterations, 1))
         check(lib().asyrk_system_monte_carlo_ratios(self.h, _ptr(x0, _f64p), C.byref(cfg), runs, _ptr(mean, _f64p),
@@ -674,12 +711,12 @@ class System:
 def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, **cfg):
     """One-shot asyrk_solve_parallel with host buffers (upload, solve, download)."""
     xs = cfg.pop("x_star", None)
-    xs = np.ascontiguousarray(xs, dtype=np.float64) if xs is not None else None
+    xs = _vec(xs, A.n, "x_star") if xs is not None else None
     c = _run_config(x_star=xs, **cfg)
     cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
     tr = _Trace(A.n, cap, want_x)
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None
+    b = _vec(b, A.m, "b")
+    x0a = _vec(x0, A.n, "x0") if x0 is not None else None
     rep = InstrumentOut()
     check(lib().asyrk_solve_parallel(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0a, _f64p), C.byref(c),
                                      C.byref(tr.out), C.byref(rep) if instrument else None))
@@ -691,11 +728,27 @@ def solve_parallel_host(A: HostCsr, b, x0=None, instrument=False, want_x=True, *
     return d
 
 
+def sweep_threads(A: HostCsr, b, thread_list, x0=None, **cfg):
+    """asyrk_sweep_threads (ref parallel.cpp:447-481): one solve per worker count,
+    speedup = wall(threads=1) / wall(threads). Returns a list of entry dicts."""
+    b = _vec(b, A.m, "b")
+    x0a = _vec(x0, A.n, "x0") if x0 is not None else None
+    c = _run_config(**cfg)
+    tl = np.ascontiguousarray(thread_list, dtype=np.int64)
+    k = len(tl)
+    wall, ep, rs, sp = np.zeros(k), np.zeros(k, np.int64), np.zeros(k), np.zeros(k)
+    check(lib().asyrk_sweep_threads(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0a, _f64p), C.byref(c),
+                                    _ptr(tl, _i64p) if k else None, k, _ptr(wall, _f64p), _ptr(ep, _i64p),
+                                    _ptr(rs, _f64p), _ptr(sp, _f64p)))
+    return [dict(threads=int(tl[i]), wall_seconds=float(wall[i]), epochs=int(ep[i]), final_r_sq=float(rs[i]),
+                 speedup=float(sp[i])) for i in range(k)]
+
+
 def simulate(A: HostCsr, b, x0, gamma, tau, delay, iterations, seed, variant, **opts):
     """One-shot asyrk_simulate (ref delay_sim.cpp:71-228); opts = probe_every, probe_r_sq, max_events,
     probe_dist_sq + dist_point (the projector's A^+ b)."""
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    b = _vec(b, A.m, "b")
+    x0 = _vec(x0, A.n, "x0")
     cfg = _sim_config(gamma, tau, delay, iterations, seed, variant, **opts)
     return _sim_call(lambda o: lib().asyrk_simulate(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0, _f64p), C.byref(cfg),
                                                     C.byref(o)), A.n, A.m, cfg)
@@ -704,8 +757,8 @@ def simulate(A: HostCsr, b, x0, gamma, tau, delay, iterations, seed, variant, **
 def monte_carlo_ratios(A: HostCsr, b, x0, gamma, tau, delay, iterations, runs, base_seed,
                        variant="single_component"):
     """One-shot asyrk_monte_carlo_ratios (ref delay_sim.cpp:230-270)."""
-    b = np.ascontiguousarray(b, dtype=np.float64)
-    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    b = _vec(b, A.m, "b")
+    x0 = _vec(x0, A.n, "x0")
     cfg = _sim_config(gamma, tau, delay, iterations, base_seed, variant)
     mean, ratios = np.zeros(iterations + 1), np.zeros(max(iterations, 1))
     check(lib().asyrk_monte_carlo_ratios(C.byref(A.view()), _ptr(b, _f64p), _ptr(x0, _f64p), C.byref(cfg), runs,
@@ -750,7 +803,7 @@ def dense_spectrum(A: "HostCsr"):
 
 def dense_lstsq(A: "HostCsr", b):
     """dense_min_norm_lstsq (ref dense.cpp:110-117): A^+ b from the device SVD."""
-    b = np.ascontiguousarray(b, dtype=np.float64)
+    b = _vec(b, A.m, "b")
     x = np.zeros(A.n)
     check(lib().asyrk_dense_lstsq(C.byref(A.view()), _ptr(b, _f64p), _ptr(x, _f64p)))
     return x

@@ -25,7 +25,7 @@ struct AliasEntry {
 struct WorkerArgs {
     Layout L;
     void* x;                      // X[n]
-    void* shadow;                 // X[n] or nullptr (instrumented run)
+    double* audit;                // kAuditK checksums (instrumented run) or nullptr
     const AliasEntry* alias;      // m entries (S_ALIAS)
     DevState* st;
     unsigned long long* increments;
@@ -38,6 +38,8 @@ struct WorkerArgs {
                                   // solves); span0 = 0: the epoch / span come from st (chunk_span)
 };
 int worker_elems_per_lane(uint32_t max_len);  // 1, 2, 4 or 0 (looped)
+// the workers' row draws for positions [0, per_warp) of every warp (tests)
+void launch_sample_rows(const WorkerArgs& a, long long epoch, long long per_warp, int32_t* out, cudaStream_t s);
 void launch_worker(const WorkerArgs& a, int precision, int E, cudaStream_t s);
 int worker_max_resident_warps(int precision, int E, int full_row);
 
@@ -253,6 +255,9 @@ void launch_x_init(const double* x0, void* x, long long n, int precision, cudaSt
 void launch_x_export(const void* x, double* out, long long n, int precision, cudaStream_t s);
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target,
                        cudaStream_t s);
+// async audit (layout.cuh kAuditK checksums): audit holds 2 kAuditK doubles
+void launch_audit_check(const void* x, const double* x0, long long n, int precision, double* audit, double* out_max,
+                        cudaStream_t s);
 void launch_instrument_check(const void* x, const double* x0, const void* shadow, long long n,
                              int precision, double* out_max, cudaStream_t s);
 

@@ -185,6 +185,26 @@ __host__ __device__ inline uint32_t feistel_half_bits(uint32_t L) {
     return (b + 1) / 2;
 }
 
+// ---- increment audit of the async workers (instrumented solves): K signed
+// checksums of every increment applied, sum_c s_k(c) * d, with s_k(c) = +-1
+// from bit k of a hash of the component; the audit compares them with
+// sum_j s_k(j) (x_j - x0_j) (pack.cu). A lost or repeated increment d on
+// component c moves every checksum by +-d.
+constexpr int kAuditK = 4;
+__host__ __device__ __forceinline__ uint32_t audit_hash(uint32_t c) {
+    c ^= c >> 16;
+    c *= 0x7feb352du;
+    c ^= c >> 15;
+    c *= 0x846ca68bu;
+    c ^= c >> 16;
+    return c;
+}
+__device__ __forceinline__ void audit_add(double (&cs)[kAuditK], int c, double d) {
+    const uint32_t h = audit_hash((uint32_t)c);
+#pragma unroll
+    for (int k = 0; k < kAuditK; ++k) cs[k] += ((h >> k) & 1u) ? d : -d;
+}
+
 // x reads bypass L1 (it is not coherent with other SMs' red.global adds);
 // A is immutable and read through the non-coherent path.
 __device__ __forceinline__ double ld_x(const double* p) { return __ldcg(p); }

@@ -72,11 +72,47 @@ __global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta,
 
 template <class X>
 static void xside_launch(int rows, int blocks, int threads, void* x, int64_t n, int theta, int64_t per_warp, int mode,
-                         unsigned long long* sink) {
+                         unsigned long long* sink, cudaStream_t s) {
     if (rows == 2)
-        xside_kernel<X, 2><<<blocks, threads>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
+        xside_kernel<X, 2><<<blocks, threads, 0, s>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
     else
-        xside_kernel<X, 1><<<blocks, threads>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
+        xside_kernel<X, 1><<<blocks, threads, 0, s>>>((X*)x, (uint32_t)n, theta, per_warp, mode, sink);
+}
+
+}  // namespace ak
+
+namespace ak {
+
+// time one launch (after a warm-up launch) of the x-side kernel on buffer x
+static asyrk_status xside_time(void* x, int64_t n, int32_t theta, int32_t precision, int32_t warps, int64_t& per_warp,
+                               int32_t mode, cudaStream_t stream, float& ms, int& blocks) {
+    // mode + 16: the same traffic with 2 rows in flight per warp (the worker's shape)
+    const int rows = mode >= 16 ? 2 : 1;
+    mode &= 15;
+    if (rows == 2) per_warp += per_warp & 1;
+    unsigned long long* sink = nullptr;
+    if (cudaMalloc(&sink, 8) != cudaSuccess) return ASYRK_E_TooLarge;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int threads = 256;
+    blocks = (warps * 32 + threads - 1) / threads;
+    ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
+        cudaEventRecord(e0, stream);
+        if (precision == P_F32)
+            xside_launch<float>(rows, blocks, threads, x, n, theta, per_warp, mode, sink, stream);
+        else
+            xside_launch<double>(rows, blocks, threads, x, n, theta, per_warp, mode, sink, stream);
+        cudaEventRecord(e1, stream);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    return err == cudaSuccess ? ASYRK_OK : ASYRK_E_ThreadSpawnFailure;
 }
 
 }  // namespace ak
@@ -85,41 +121,39 @@ extern "C" asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t
                                                int64_t proj_per_warp, int32_t mode, double* proj_per_s,
                                                double* kernel_ms) {
     using namespace ak;
-    // mode + 16: the same traffic with 2 rows in flight per warp (the worker's shape)
-    const int rows = mode >= 16 ? 2 : 1;
-    mode &= 15;
-    if (rows == 2) proj_per_warp += proj_per_warp & 1;
     if (n < 1 || theta < 1 || theta > 128 || warps < 1 || proj_per_warp < 1)
         return fail(ASYRK_E_InvalidArgument, "microbench_xside: need n >= 1, 1 <= theta <= 128, warps >= 1");
-    void* x = nullptr;
-    unsigned long long* sink = nullptr;
+    // x on a 2 MB page boundary, like the solver's (system.cu dalloc_page_aligned)
+    void* base = nullptr;
     const size_t xb = (size_t)n * (precision == P_F32 ? 4 : 8);
-    if (cudaMalloc(&x, xb) != cudaSuccess) return ASYRK_E_TooLarge;
-    cudaMalloc(&sink, 8);
+    const size_t page = 2u << 20;
+    if (cudaMalloc(&base, xb + page) != cudaSuccess) return ASYRK_E_TooLarge;
+    void* x = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(base) + page - 1) & ~(uintptr_t)(page - 1));
     cudaMemset(x, 0, xb);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    const int threads = 256;
-    const int blocks = (warps * 32 + threads - 1) / threads;
     float ms = 0.f;
-    for (int rep = 0; rep < 2; ++rep) {  // first launch warms up
-        cudaEventRecord(e0);
-        if (precision == P_F32)
-            xside_launch<float>(rows, blocks, threads, x, n, theta, proj_per_warp, mode, sink);
-        else
-            xside_launch<double>(rows, blocks, threads, x, n, theta, proj_per_warp, mode, sink);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        cudaEventElapsedTime(&ms, e0, e1);
-    }
-    const cudaError_t err = cudaGetLastError();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaFree(x);
-    cudaFree(sink);
-    if (err != cudaSuccess) return ASYRK_E_ThreadSpawnFailure;
-    *proj_per_s = (double)blocks * threads / 32 * (double)proj_per_warp / (ms * 1e-3);
+    int blocks = 0;
+    const asyrk_status st = xside_time(x, n, theta, precision, warps, proj_per_warp, mode, nullptr, ms, blocks);
+    cudaFree(base);
+    if (st) return st;
+    *proj_per_s = (double)blocks * 256 / 32 * (double)proj_per_warp / (ms * 1e-3);
+    if (kernel_ms) *kernel_ms = ms;
+    return ASYRK_OK;
+}
+
+// The same measurement on a resident system's own x buffer (its address,
+// alignment and footprint; the row length of its records as theta) on its
+// stream. Leaves x perturbed by ~1e-30 increments: every solve re-initialises x.
+asyrk_status xside_on_buffer(void* x, int64_t n, int32_t theta, int32_t precision, int32_t warps, int64_t per_warp,
+                             int32_t mode, void* stream, double* proj_per_s, double* kernel_ms) {
+    using namespace ak;
+    if (theta < 1 || theta > 128 || warps < 1 || per_warp < 1)
+        return fail(ASYRK_E_InvalidArgument, "microbench_xside: need rows of 1..128 nonzeros, warps >= 1");
+    float ms = 0.f;
+    int blocks = 0;
+    const asyrk_status st =
+        xside_time(x, n, theta, precision, warps, per_warp, mode, static_cast<cudaStream_t>(stream), ms, blocks);
+    if (st) return st;
+    *proj_per_s = (double)blocks * 256 / 32 * (double)per_warp / (ms * 1e-3);
     if (kernel_ms) *kernel_ms = ms;
     return ASYRK_OK;
 }

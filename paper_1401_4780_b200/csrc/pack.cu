@@ -164,6 +164,36 @@ void launch_instrument_check(const void* x, const double* x0, const void* shadow
                                                                static_cast<const double*>(shadow), n, o);
 }
 
+// Async audit: lhs_k = sum_j s_k(j) (x_j - x0_j) next to the workers'
+// checksums of the increments they applied (audit[0..K) from the workers,
+// audit[K..2K) here); out_max = max_k |lhs_k - audit_k|.
+template <class X>
+__global__ void audit_lhs_kernel(const X* __restrict__ x, const double* __restrict__ x0, long long n, double* audit) {
+    double cs[kAuditK] = {};
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
+        audit_add(cs, (int)k, (double)x[k] - x0[k]);
+#pragma unroll
+    for (int q = 0; q < kAuditK; ++q) {
+        const double v = warp_sum(cs[q]);
+        if ((threadIdx.x & 31) == 0) atomicAdd(audit + kAuditK + q, v);
+    }
+}
+__global__ void audit_final_kernel(const double* audit, double* out_max) {
+    double mx = 0.0;
+    for (int q = 0; q < kAuditK; ++q) mx = fmax(mx, fabs(audit[kAuditK + q] - audit[q]));
+    *out_max = mx;
+}
+void launch_audit_check(const void* x, const double* x0, long long n, int precision, double* audit, double* out_max,
+                        cudaStream_t s) {
+    cudaMemsetAsync(audit + kAuditK, 0, kAuditK * sizeof(double), s);
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+    if (precision == P_F32)
+        audit_lhs_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x), x0, n, audit);
+    else
+        audit_lhs_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), x0, n, audit);
+    audit_final_kernel<<<1, 1, 0, s>>>(audit, out_max);
+}
+
 // CUB radix sort wrapper: stable sort of (col, nnz-index) pairs by column, so
 // each column lists its rows ascending (the order multiply_transpose adds in).
 size_t csc_sort_temp_bytes(long long nnz) {

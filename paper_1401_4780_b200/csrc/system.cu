@@ -28,6 +28,9 @@
 
 using namespace ak;
 
+asyrk_status xside_on_buffer(void* x, int64_t n, int32_t theta, int32_t precision, int32_t warps, int64_t per_warp,
+                             int32_t mode, void* stream, double* proj_per_s, double* kernel_ms);  // microbench.cu
+
 namespace ak {
 std::string& err_buf() {
     static thread_local std::string e;
@@ -831,7 +834,10 @@ asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long l
             CK(cudaMemcpy(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost));
         }
         instr->increments = (int64_t)inc;
-        launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
+        if (sp.det)
+            launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
+        else
+            launch_audit_check(s->x, s->x0d, s->n, prec, s->scratch + 16, s->scratch, st);
         double mx = 0.0;
         CK(cudaMemcpyAsync(&mx, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
@@ -939,8 +945,12 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         CK(cudaMemcpyAsync(s->xstar, sp.x_star, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
     }
     if (instr) {
-        if (!s->shadow) s->shadow = dalloc<unsigned char>((size_t)s->n * 8);
-        CK(cudaMemsetAsync(s->shadow, 0, (size_t)s->n * 8, st));
+        if (sp.det) {  // the reference's per-component shadow (bitwise audit report)
+            if (!s->shadow) s->shadow = dalloc<unsigned char>((size_t)s->n * 8);
+            CK(cudaMemsetAsync(s->shadow, 0, (size_t)s->n * 8, st));
+        } else {  // the workers' signed checksums (layout.cuh kAuditK) in scratch[16..)
+            CK(cudaMemsetAsync(s->scratch + 16, 0, 2 * kAuditK * sizeof(double), st));
+        }
         CK(cudaMemsetAsync(s->incr, 0, sizeof(unsigned long long), st));
     }
     *s->host_flag = 0;
@@ -998,7 +1008,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         E = worker_elems_per_lane(s->max_len);
         wa.L = s->layout();
         wa.x = s->x;
-        wa.shadow = instr ? s->shadow : nullptr;
+        wa.audit = instr ? s->scratch + 16 : nullptr;
         wa.alias = s->alias;
         wa.st = s->st;
         wa.increments = instr ? s->incr : nullptr;
@@ -1842,6 +1852,43 @@ asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x,
         CK(cudaGetLastError());
         return ASYRK_OK;
     });
+}
+
+asyrk_status asyrk_system_sample_rows(asyrk_system* sys, int32_t sampling, uint64_t seed, int64_t warps, int64_t epoch,
+                                      int64_t per_warp, int32_t* rows_out) {
+    if (!sys || !rows_out || warps < 1 || per_warp < 1 || epoch < 0)
+        return fail(ASYRK_E_InvalidArgument, "sample_rows: need a system, warps >= 1, per_warp >= 1, epoch >= 0");
+    if (sampling < 0 || sampling > 2) return fail(ASYRK_E_InvalidArgument, "unknown sampling");
+    if (sampling == ASYRK_SLICE_SHUFFLE && sys->m < warps)
+        return fail(ASYRK_E_InvalidArgument, "slice_shuffle needs at least one row per worker");
+    return guarded([&] {
+        AllocStream as(sys->stream);
+        if (sampling == ASYRK_NORM_PROPORTIONAL) ensure_alias_dev(sys);
+        WorkerArgs wa{};
+        wa.L = sys->layout();
+        wa.alias = sys->alias;
+        wa.W = warps;
+        const uint64_t k = splitmix64(seed ^ 0xA5A5A5A5DEADBEEFull);  // the solve's key derivation
+        wa.key0 = (uint32_t)k;
+        wa.key1 = (uint32_t)(k >> 32);
+        wa.sampling = sampling == ASYRK_SLICE_SHUFFLE ? S_SLICE : sampling == ASYRK_NORM_PROPORTIONAL ? S_ALIAS : S_UNIFORM;
+        const size_t cnt = (size_t)(warps * per_warp);
+        int32_t* d = dalloc<int32_t>(cnt);
+        launch_sample_rows(wa, epoch, per_warp, d, sys->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(rows_out, d, cnt * 4, cudaMemcpyDeviceToHost, sys->stream));
+        CK(cudaStreamSynchronize(sys->stream));
+        pool_free(d, sys->stream);
+        return ASYRK_OK;
+    });
+}
+
+asyrk_status asyrk_system_microbench_xside(asyrk_system* sys, int32_t warps, int64_t proj_per_warp, int32_t mode,
+                                           double* proj_per_s, double* kernel_ms) {
+    if (!sys || !proj_per_s) return fail(ASYRK_E_InvalidArgument, "null argument");
+    const int32_t theta = (int32_t)(sys->uniform ? sys->uniform_len : sys->max_len);
+    const int32_t prec = sys->precision == P_F32 ? P_F32 : P_F64;  // x's element type
+    return xside_on_buffer(sys->x, sys->n, theta, prec, warps, proj_per_warp, mode, sys->stream, proj_per_s, kernel_ms);
 }
 
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out) {

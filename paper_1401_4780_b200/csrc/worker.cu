@@ -63,6 +63,15 @@ __device__ __forceinline__ void load_frag(const Layout& L, long long row, int la
     f.inv = rec_inv(r);
 }
 
+// a warp's audit checksums into the solve's (one fp64 atomic per checksum per warp)
+__device__ __forceinline__ void audit_flush(const WorkerArgs& a, double (&cs)[kAuditK], int lane) {
+#pragma unroll
+    for (int k = 0; k < kAuditK; ++k) {
+        const double v = warp_sum(cs[k]);
+        if (lane == 0) atomicAdd(a.audit + k, v);
+    }
+}
+
 // Lane-parallel draw of the rows for positions [j0, j0+32) of this warp's
 // launch. Also returns 32 random bits per position for single_component picks.
 struct Draw {
@@ -126,7 +135,8 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
     if (count <= 0) return;
 
     X* __restrict__ x = static_cast<X*>(a.x);
-    X* __restrict__ shadow = static_cast<X*>(a.shadow);
+    const bool audit = a.audit != nullptr;
+    double cs[kAuditK] = {};
     const T gamma = (T)a.gamma;
     unsigned long long incr = 0;
 
@@ -192,7 +202,7 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
                         if (cur[r].c[e] >= 0) {
                             const T d = -c * (T)cur[r].v[e];
                             atomicAdd(x + cur[r].c[e], d);
-                            if (shadow) atomicAdd(shadow + cur[r].c[e], d);
+                            if (audit) audit_add(cs, cur[r].c[e], (double)d);
                         }
                     }
                     incr += (unsigned long long)cur[r].len;
@@ -204,7 +214,7 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
                         if (lane + 32 * e == t) {
                             const T d = -gamma * (T)cur[r].len * (T)cur[r].v[e] * res;
                             atomicAdd(x + cur[r].c[e], d);
-                            if (shadow) atomicAdd(shadow + cur[r].c[e], d);
+                            if (audit) audit_add(cs, cur[r].c[e], (double)d);
                         }
                     }
                     incr += 1;
@@ -220,6 +230,7 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
         B0 = B1;
         if (bi + 2 < nb) B1 = draw_row(a, warp, epoch, (bi + 2) * 32 + lane, slice_lo, slice_len);
     }
+    if (audit) audit_flush(a, cs, lane);
     if (a.increments && lane == 0) atomicAdd(a.increments, incr);
 }
 
@@ -246,7 +257,8 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
         count = total / a.W + (warp < total % a.W ? 1 : 0);
     }
     X* __restrict__ x = static_cast<X*>(a.x);
-    X* __restrict__ shadow = static_cast<X*>(a.shadow);
+    const bool audit = a.audit != nullptr;
+    double cs[kAuditK] = {};
     const T gamma = (T)a.gamma;
     unsigned long long incr = 0;
     for (long long j0 = 0; j0 < count; j0 += 32) {
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
                     const T d = -c * (T)__ldg(vals + k);
                     const int col = __ldg(cols + k);
                     atomicAdd(x + col, d);
-                    if (shadow) atomicAdd(shadow + col, d);
+                    if (audit) audit_add(cs, col, (double)d);
                 }
                 incr += (unsigned long long)r.len;
             } else {
@@ -277,13 +289,34 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
                     const T d = -gamma * (T)r.len * (T)__ldg(vals + t) * res;
                     const int col = __ldg(cols + t);
                     atomicAdd(x + col, d);
-                    if (shadow) atomicAdd(shadow + col, d);
+                    if (audit) audit_add(cs, col, (double)d);
                 }
                 incr += 1;
             }
         }
     }
     if (a.increments && lane == 0) atomicAdd(a.increments, incr);
+}
+
+// The workers' own row draws, written out (tests: alias frequencies, slice
+// permutations): warp w's positions [0, per_warp) of epoch `epoch`.
+__global__ void sample_rows_kernel(WorkerArgs a, long long epoch, long long per_warp, int32_t* out) {
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp >= a.W) return;
+    const int lane = threadIdx.x & 31;
+    const long long m = a.L.m;
+    long long slice_lo = 0, slice_len = 1;
+    if (a.sampling == S_SLICE) {
+        slice_lo = warp * m / a.W;
+        slice_len = (warp + 1) * m / a.W - slice_lo;
+    }
+    for (long long j = lane; j < per_warp; j += 32)
+        out[warp * per_warp + j] = (int32_t)draw_row(a, warp, epoch, j, slice_lo, slice_len).row;
+}
+
+void launch_sample_rows(const WorkerArgs& a, long long epoch, long long per_warp, int32_t* out, cudaStream_t s) {
+    const long long threads = a.W * 32;
+    sample_rows_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(a, epoch, per_warp, out);
 }
 
 int worker_elems_per_lane(uint32_t max_len) {

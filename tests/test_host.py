@@ -223,3 +223,24 @@ def test_bench_reference_arm_json_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+
+
+def test_host_vectors_are_length_checked():
+    # the C ABI copies n (or m) doubles from the caller's pointers: short
+    # vectors are rejected before the call with the reference's
+    # DimensionMismatch (parallel.cpp:57-61), no device needed
+    from paper_1401_4780_b200 import capi
+
+    A, b, xs = capi.generate_fixed_theta(200, 100, 5, seed=1)
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.solve_parallel_host(A, b[:-1], threads=4, epochs=2)
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.solve_parallel_host(A, b, x0=np.zeros(99), threads=4, epochs=2)
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.solve_parallel_host(A, b, x_star=xs[:50], threads=4, epochs=2)
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.sweep_threads(A, b[:10], [1, 2])
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.simulate(A, b, np.zeros(3), 1.0, 0, "fixed", 10, 1, "full_row")
+    with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
+        capi.MultiRHS(A, np.zeros((10, 4), np.float32), 0, 4)
