@@ -317,7 +317,7 @@ def run_gpu(args):
 
     # ---- instrumented drop-in call (the reference's Python solve_parallel always
     # passes &rep, module.cpp:190-191): the same solve with the increment audit on
-    instr_ms = []
+    instr_ms, instr_wms = [], []
     for k in range(-1, min(args.steps, 10)):
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -328,6 +328,7 @@ def run_gpu(args):
         torch.cuda.synchronize()
         if k >= 0:
             instr_ms.append(e0.elapsed_time(e1))
+            instr_wms.append(S.stats()["worker_ms"])
         if not ri["instrument"]["consistent"]:
             raise RuntimeError("instrumented solve failed the increment audit")
 
@@ -336,7 +337,7 @@ def run_gpu(args):
     e2e_wall = 0.0
     e2e_proj = 0
     e2e_calls = []
-    for k in range(-1, e2e_steps):
+    for k in range(-3, e2e_steps):  # 3 untimed warm-up calls
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = capi.solve_parallel_host(A, b, threads=W, gamma=1.0, epochs=2000, target=target,
@@ -380,6 +381,8 @@ def run_gpu(args):
             "e2e": {"value": e2e_proj / e2e_wall, "unit": "proj/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_wall / e2e_steps, "calls_ms": e2e_calls},
             "instrumented": {"ms_per_solve": statistics.median(instr_ms),
+                             "worker_ms_per_solve": statistics.median(instr_wms),
+                             "uninstrumented_worker_ms_per_solve": w_ms / args.steps,
                              "ratio_vs_uninstrumented": statistics.median(instr_ms) / statistics.median(step_ms),
                              "call": "System.solve(..., instrument=True): the increment audit of "
                                      "solve_parallel's InstrumentReport (parallel.cpp:94-106)"},
@@ -494,7 +497,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
     for w in range(warmup):
         with torch.cuda.stream(stream):
             flush.zero_()
-        sh.solve_nccl(comm, seed=100 + w, **kw)
+        sh.solve_nccl(comm, seed=100 + w, want_x=False, **kw)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
     if dist:
         dist.barrier()
@@ -505,7 +508,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
             with torch.cuda.stream(stream):
                 flush.zero_()
             ev[k][0].record(stream)
-            t = sh.solve_nccl(comm, seed=1000 + k, **kw)
+            t = sh.solve_nccl(comm, seed=1000 + k, want_x=False, **kw)
             ev[k][1].record(stream)
             st = sh.stats()
             wms += st["worker_ms"]

@@ -307,6 +307,17 @@ asyrk_status asyrk_system_compute_stats(asyrk_system* sys, double tol, int64_t m
  * the device alias table, ref kaczmarz.cpp:14-69). */
 asyrk_status asyrk_system_sample_rows(asyrk_system* sys, int32_t sampling, uint64_t seed, int64_t warps, int64_t epoch,
                                       int64_t per_warp, int32_t* rows_out);
+/* Deterministic multi-RHS rk_solve on a resident fp64 system (SURVEY.md §8c,
+ * config 5's parity definition): B is m x k row-major (k right-hand sides), X0
+ * (or NULL = zeros), cfg->x_star (or NULL) and X_out are n x k row-major. All
+ * columns consume ONE row sequence — the reference rk_solve's
+ * (kaczmarz.cpp:128-227) for cfg->seed / sampling — and column j's iterate is
+ * bit-identical to rk_solve(A, B[:, j], X0[:, j]) with that seed. A record per
+ * epoch: r_sq, grad_sq, dist_sq are the per-column exact values summed in
+ * column order; the stop is global (sum r_sq <= target_r_sq, or max_epochs).
+ * trace->final_x is not written (X_out holds the iterates). */
+asyrk_status asyrk_system_rk_solve_multi(asyrk_system* sys, const double* B, int64_t k, const double* X0,
+                                         const asyrk_rk_config* cfg, double* X_out, asyrk_trace_out* trace);
 /* Largest number of worker warps that are co-resident for this system. */
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out);
 

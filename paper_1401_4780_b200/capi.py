@@ -259,6 +259,8 @@ def lib():
         L.asyrk_mrhs_solve.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p]
         L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_mrhs_due.argtypes = [sp, _i32p]
+        L.asyrk_system_rk_solve_multi.argtypes = [sp, _f64p, C.c_int64, _f64p, C.POINTER(RkConfig), _f64p,
+                                                  C.POINTER(TraceOut)]
         L.asyrk_system_microbench_xside.argtypes = [sp, C.c_int32, C.c_int64, C.c_int32, _f64p, _f64p]
         L.asyrk_system_sample_rows.argtypes = [sp, C.c_int32, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, _i32p]
         L.asyrk_nccl_available.argtypes = [_i32p]
@@ -288,7 +290,7 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
+    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_system_rk_solve_multi", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
     "asyrk_nccl_comm_init_rank", "asyrk_nccl_comm_destroy", "asyrk_mrhs_solve_nccl", "asyrk_mrhs_solve_devices",
     "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
@@ -378,18 +380,18 @@ class MultiRHS:
         d["X"] = X
         return d
 
-    def solve_nccl(self, comm, X0=None, X_star=None, **cfg):
+    def solve_nccl(self, comm, X0=None, X_star=None, want_x=True, **cfg):
         """This rank's shard of a sharded solve, the loop in C++ with one ncclAllReduce of the
         shard norms per evaluated boundary (asyrk_mrhs_solve_nccl); comm from NcclComm."""
         c = _run_config(**cfg)
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
         tr = _Trace(0, cap, want_x=False)
-        X = np.zeros((self.n, self.c1 - self.c0), np.float32)
+        X = np.zeros((self.n, self.c1 - self.c0), np.float32) if want_x else None
         x0 = _mat(X0, (self.n, self.k_total), np.float32, "X0") if X0 is not None else None
         xs = _mat(X_star, (self.n, self.k_total), np.float64, "X_star") if X_star is not None else None
         check(lib().asyrk_mrhs_solve_nccl(self.h, C.byref(c), C.c_void_p(comm.handle),
                                           x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None else None,
-                                          _ptr(xs, _f64p), C.byref(tr.out), X.ctypes.data_as(C.POINTER(C.c_float))))
+                                          _ptr(xs, _f64p), C.byref(tr.out), _ptr(X, C.POINTER(C.c_float))))
         d = tr.result(xs is not None)
         d["X"] = X
         return d
@@ -627,6 +629,24 @@ class System:
             d["instrument"] = dict(row_updates=rep.row_updates, increments=rep.increments,
                                    max_abs_error=rep.max_abs_error, tolerance=rep.tolerance,
                                    consistent=bool(rep.consistent))
+        return d
+
+    def rk_solve_multi(self, B, X0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, X_star=None):
+        """Deterministic multi-RHS rk_solve (asyrk_system_rk_solve_multi): B (m x k); column j
+        of the result is rk_solve(A, B[:, j]) with the same seed, bit for bit."""
+        B = np.ascontiguousarray(B, dtype=np.float64)
+        if B.ndim != 2 or B.shape[0] != self.m:
+            raise AsyrkError(6, f"B has shape {B.shape}, expected ({self.m}, k)")
+        k = B.shape[1]
+        x0 = _mat(X0, (self.n, k), np.float64, "X0") if X0 is not None else None
+        xs = _mat(X_star, (self.n, k), np.float64, "X_star") if X_star is not None else None
+        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+        tr = _Trace(0, max(max_epochs, 0) + 2, want_x=False)
+        X = np.zeros((self.n, k))
+        check(lib().asyrk_system_rk_solve_multi(self.h, _ptr(B, _f64p), k, _ptr(x0, _f64p), C.byref(c),
+                                                _ptr(X, _f64p), C.byref(tr.out)))
+        d = tr.result(xs is not None)
+        d["X"] = X
         return d
 
     def microbench_xside(self, warps, proj_per_warp=1024, mode=0):

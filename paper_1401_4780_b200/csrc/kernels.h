@@ -66,6 +66,12 @@ struct DetArgs {
     long long* dbg;               // optional per-event phase timestamps (diagnostics)
     int poll_ns;                  // dataflow polling back-off (0: spin)
     uint32_t max_len;             // longest row (picks the dataflow kernel's elements per lane)
+    // deterministic multi-RHS (asyrk_system_rk_solve_multi): ncols > 1 runs one
+    // CTA per right-hand side over the same event sequence / prepass; column c's
+    // iterate is x + c * n and its b is b_cols + c * m (b_cols null: one column,
+    // b from the records)
+    int ncols;
+    const double* b_cols;
 };
 void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
@@ -113,8 +119,12 @@ struct MonitorArgs {
     long long set_epoch;          // >= 0: the boundary this record is taken at (host-scheduled solves:
                                   // st->epoch = set_epoch, st->updates = set_epoch * m_rows); -1: unused
     HostMirror* mirror;           // or nullptr: the record's decision inputs for the host
+    double* col_out;              // exact mode: write {r_sq, grad_sq, dist_sq} here instead of recording
 };
 void launch_monitor(const MonitorArgs& a, int precision, cudaStream_t s);
+// deterministic multi-RHS record: sums the per-column exact sums colres[c][3]
+// in column order, then records / decides like the single-RHS finalize
+void launch_multi_commit(const MonitorArgs& a, const double* colres, int ncols, cudaStream_t s);
 // overlapped solves: copy x into snapshot slot xs (if the epoch ran) and
 // advance the coordinator state (epoch, updates, slot meta, next go);
 // advance = 0 takes boundary 0 (x0, before the first workers; sets go)

@@ -349,7 +349,29 @@ __global__ void __launch_bounds__(96) finalize_exact_kernel(MonitorArgs a) {
         res[w] = r;
     }
     __syncthreads();
-    if (threadIdx.x == 0) commit_record(a, res[0], res[1], res[2]);
+    if (threadIdx.x == 0) {
+        if (a.col_out) {
+            a.col_out[0] = res[0];
+            a.col_out[1] = res[1];
+            a.col_out[2] = res[2];
+        } else {
+            commit_record(a, res[0], res[1], res[2]);
+        }
+    }
+}
+
+__global__ void multi_commit_kernel(MonitorArgs a, const double* colres, int ncols) {
+    if (!a.force && a.st->stop) return;
+    double r = 0.0, g = 0.0, d = 0.0;
+    for (int c = 0; c < ncols; ++c) {
+        r = __dadd_rn(r, colres[3 * c]);
+        g = __dadd_rn(g, colres[3 * c + 1]);
+        d = __dadd_rn(d, colres[3 * c + 2]);
+    }
+    commit_record(a, r, g, d);
+}
+void launch_multi_commit(const MonitorArgs& a, const double* colres, int ncols, cudaStream_t s) {
+    multi_commit_kernel<<<1, 1, 0, s>>>(a, colres, ncols);
 }
 
 // ---- finalize, fast: fixed-order sum of the block partials (one block)

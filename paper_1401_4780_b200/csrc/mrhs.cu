@@ -17,6 +17,8 @@
 // per column over a plain CSC, lanes over columns), block partials of
 // ||R||_F^2, ||G||_F^2, ||X - X*||_F^2 in fp64. The partials are what a
 // multi-GPU caller all-reduces (NCCL) before the stop decision.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace ak {
@@ -489,7 +491,9 @@ int mrhs_col_blocks(long long n) {
 template <int KL>
 static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
     const int blocks = (int)((a.W * 32 + 255) / 256);
-    if (a.max_len <= 32)
+    // ASYRK_MRHS_LOOPED=1: the one-row-at-a-time worker for every row length (A/B runs)
+    static const bool looped = getenv("ASYRK_MRHS_LOOPED") != nullptr;
+    if (a.max_len <= 32 && !looped)
         mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
     else
         mrhs_worker_long_kernel<KL><<<blocks, 256, 0, s>>>(a);

@@ -738,6 +738,7 @@ MonitorArgs monitor_args(asyrk_system* s, bool exact, int advance, bool with_xst
     a.slot = -1;
     a.set_epoch = -1;
     a.mirror = nullptr;
+    a.col_out = nullptr;
     a.x_alt = nullptr;
     a.force = 0;
     return a;
@@ -1320,6 +1321,168 @@ asyrk_status system_rk_impl(asyrk_system* s, const double* x0, const asyrk_rk_co
     return run_solve(s, x0, sp, trace, nullptr);
 }
 
+// Deterministic multi-RHS rk_solve (SURVEY.md §8c "config 5 per column"):
+// k right-hand sides, ONE row sequence (the reference's make_stream(seed, 0)
+// stream of rk_solve, kaczmarz.cpp:128-227), column j's iterate bit-identical
+// to rk_solve(A, B[:, j], X0[:, j]) with the same seed. One dataflow CTA per
+// column over the shared event prepass; a record per epoch whose r_sq /
+// grad_sq / dist_sq are the per-column exact sums added in column order; the
+// stop is global (sum r_sq <= target_r_sq or max_epochs).
+asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const double* X0, const asyrk_rk_config* c,
+                           double* X_out, asyrk_trace_out* trace) {
+    if (!c || !B || k < 1) return fail(ASYRK_E_InvalidArgument, "rk_solve_multi: need a config, B and k >= 1");
+    if (s->precision != P_F64) return fail(ASYRK_E_InvalidArgument, "the deterministic path needs an fp64 system");
+    if (c->sampling == ASYRK_RK_UNIFORM && !s->normalized)
+        return fail(ASYRK_E_NotNormalized,
+                    "uniform row sampling is only unbiased on normalized rows; use norm_proportional or normalize first");
+    if (c->max_epochs < 0) return fail(ASYRK_E_InvalidArgument, "max_epochs must be >= 0");
+    if (c->sampling < 0 || c->sampling > 2) return fail(ASYRK_E_InvalidArgument, "unknown sampling");
+    if (k > 65535) return fail(ASYRK_E_TooLarge, "rk_solve_multi: at most 65535 right-hand sides");
+    cudaStream_t st = s->stream;
+    AllocStream alloc_on(st);
+    mon_wait(s, st);
+    const int64_t m = s->m, n = s->n;
+    const int det_mode = c->sampling == ASYRK_RK_UNIFORM ? 0 : (c->sampling == ASYRK_RK_NORM_PROPORTIONAL ? 1 : 2);
+    if (det_mode == 1 && !s->h_alias) {
+        std::vector<double> w(s->h_norm.size());
+        for (size_t i = 0; i < w.size(); ++i) w[i] = s->h_norm[i] * s->h_norm[i];
+        s->h_alias = std::make_unique<HostAlias>();
+        if (!s->h_alias->build(w)) {
+            s->h_alias.reset();
+            return fail(ASYRK_E_InvalidArgument, "alias weights invalid");
+        }
+    }
+    // column-major device copies: column j of X / B / X* contiguous
+    std::vector<double> tmp((size_t)(k * std::max(m, n)));
+    auto to_cols = [&](const double* src, int64_t rows) {
+        for (int64_t i = 0; i < rows; ++i)
+            for (int64_t j = 0; j < k; ++j) tmp[(size_t)(j * rows + i)] = src[i * k + j];
+    };
+    double* Xc = dalloc<double>((size_t)(k * n));
+    double* Bc = dalloc<double>((size_t)(k * m));
+    double* Xs = c->x_star ? dalloc<double>((size_t)(k * n)) : nullptr;
+    double* colres = dalloc<double>((size_t)(3 * k));
+    struct Free {
+        cudaStream_t st;
+        std::vector<void*> p;
+        ~Free() {
+            for (void* q : p) pool_free(q, st);
+        }
+    } fr{st, {Xc, Bc, Xs, colres}};
+    to_cols(B, m);
+    CK(cudaMemcpyAsync(Bc, tmp.data(), (size_t)(k * m) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    if (X0) {
+        to_cols(X0, n);
+        CK(cudaMemcpyAsync(Xc, tmp.data(), (size_t)(k * n) * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    } else {
+        CK(cudaMemsetAsync(Xc, 0, (size_t)(k * n) * 8, st));
+    }
+    if (Xs) {
+        to_cols(c->x_star, n);
+        CK(cudaMemcpyAsync(Xs, tmp.data(), (size_t)(k * n) * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    ensure_records(s, std::max<long long>(256, c->max_epochs + 2));
+    ensure_events(s, 0);
+    ensure_seq(s, (size_t)m);
+    s->stats = asyrk_solve_stats{};
+    std::memset(s->mirror, 0, sizeof(HostMirror));
+    *s->host_flag = 0;
+    CK(cudaEventRecord(s->ev_begin, st));
+    launch_state_init(s->st, c->max_epochs, 1, c->target_r_sq, st);
+    long long launches = 1;
+    auto record = [&](long long epoch) {  // boundary `epoch` of every column -> one record
+        for (int64_t j = 0; j < k; ++j) {
+            MonitorArgs ma = monitor_args(s, true, 0, Xs != nullptr);
+            ma.x = Xc + j * n;
+            ma.b = Bc + j * m;
+            ma.x_star = Xs ? Xs + j * n : nullptr;
+            ma.col_out = colres + 3 * j;
+            launch_monitor(ma, P_F64, st);
+            launches += 3;
+        }
+        MonitorArgs mc = monitor_args(s, true, epoch > 0 ? 1 : 0, Xs != nullptr);
+        mc.set_epoch = epoch;
+        mc.mirror = s->mirror_dev;
+        launch_multi_commit(mc, colres, (int)k, st);
+        launches += 1;
+        s->stats.monitor_launches++;
+        CK(cudaEventRecord(s->ev_chunk[0], st));
+        CK(cudaEventSynchronize(s->ev_chunk[0]));
+        return *const_cast<volatile int*>(&s->mirror->stop) != 0;
+    };
+    SeqGen gen(c->seed, det_mode, m, &s->h_len, s->h_alias.get(), false);
+    DetArgs da{};
+    da.L = s->layout();
+    da.row_norm = s->row_norm;
+    da.x = Xc;
+    da.st = s->st;
+    da.gamma = 1.0;
+    da.full_row = 1;
+    da.x_in_smem = (det_fits_smem(n) && s->max_len <= 128) ? 1 : 0;
+    static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
+    da.poll_ns = poll_ns;
+    da.max_len = s->max_len;
+    da.ncols = (int)k;
+    da.b_cols = Bc;
+    bool stop = record(0);
+    for (long long e = 1; e <= c->max_epochs && !stop; ++e) {
+        int32_t* sq = s->seq_host[0];
+        gen.epoch(sq, s->pick_host[0]);
+        CK(cudaMemcpyAsync(s->seq_dev[0], sq, (size_t)m * 4, cudaMemcpyHostToDevice, st));
+        da.seq = s->seq_dev[0];
+        da.picks = s->pick_dev[0];
+        da.count = m;
+        da.need = s->need[0];
+        da.ev_col = s->prep[0].keys;
+        da.ev_val = s->prep[0].ev_val;
+        da.ev_b = s->prep[0].ev_b;
+        da.ev_nn = s->prep[0].ev_nn;
+        da.ev_rcp = s->prep[0].ev_rcp;
+        long long pairs = m * (long long)s->uniform_len;
+        da.flat_off = nullptr;
+        if (!s->uniform) {
+            long long* fo = s->flat_host[0];
+            fo[0] = 0;
+            for (int64_t q = 0; q < m; ++q) fo[q + 1] = fo[q] + s->h_len[(size_t)sq[q]];
+            pairs = fo[m];
+            CK(cudaMemcpyAsync(s->flat_dev[0], fo, (size_t)(m + 1) * 8, cudaMemcpyHostToDevice, st));
+            da.flat_off = s->flat_dev[0];
+        }
+        if (da.x_in_smem) launch_det_prepare(da, s->prep[0], pairs, st);
+        launch_det(da, 0, st);
+        launches += da.x_in_smem ? 5 : 1;
+        s->stats.worker_launches++;
+        stop = record(e);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(s->ev_end, st));
+    CK(cudaStreamSynchronize(st));
+    DevState hs;
+    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+    s->stats.solve_ms = ms;
+    s->stats.kernel_launches = launches;
+    s->stats.projections = hs.updates;
+    s->stats.warps = (int32_t)std::min<int64_t>(k, INT32_MAX);
+    if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
+    if (trace) {
+        asyrk_trace_out t = *trace;
+        t.final_x = nullptr;
+        write_trace(s, hs, &t, P_F64);
+        trace->count = t.count;
+    }
+    if (X_out) {
+        CK(cudaMemcpy(tmp.data(), Xc, (size_t)(k * n) * 8, cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n; ++i)
+            for (int64_t j = 0; j < k; ++j) X_out[i * k + j] = tmp[(size_t)(j * n + i)];
+    }
+    return ASYRK_OK;
+}
+
 asyrk_status residuals_impl(asyrk_system* s, const double* x, double* r_sq, double* grad_sq) {
     cudaStream_t st = s->stream;
     mon_wait(s, st);
@@ -1889,6 +2052,12 @@ asyrk_status asyrk_system_microbench_xside(asyrk_system* sys, int32_t warps, int
     const int32_t theta = (int32_t)(sys->uniform ? sys->uniform_len : sys->max_len);
     const int32_t prec = sys->precision == P_F32 ? P_F32 : P_F64;  // x's element type
     return xside_on_buffer(sys->x, sys->n, theta, prec, warps, proj_per_warp, mode, sys->stream, proj_per_s, kernel_ms);
+}
+
+asyrk_status asyrk_system_rk_solve_multi(asyrk_system* sys, const double* B, int64_t k, const double* X0,
+                                         const asyrk_rk_config* cfg, double* X_out, asyrk_trace_out* trace) {
+    if (!sys) return fail(ASYRK_E_InvalidArgument, "null system");
+    return guarded([&] { return rk_multi_impl(sys, B, k, X0, cfg, X_out, trace); });
 }
 
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out) {

@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
             }
         }
     }
+    if (audit) audit_flush(a, cs, lane);
     if (a.increments && lane == 0) atomicAdd(a.increments, incr);
 }
 

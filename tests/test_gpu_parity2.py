@@ -177,3 +177,57 @@ def test_config3_fp64x_full_size():
     assert np.sqrt(t["r_sq"][-1] / bb) < 1e-5
     assert np.sqrt(t["dist_sq"][-1] / float(xs @ xs)) < 1e-4
     assert abs(rs - t["r_sq"][-1]) <= 1e-6 * rs  # the record is the returned iterate's residual
+
+
+@pytest.mark.parametrize("sampling,name", [(0, "uniform"), (2, "shuffle"), (1, "norm")])
+def test_deterministic_multi_rhs_columns_equal_reference_rk_solve(sampling, name):
+    # SURVEY.md §8c, config 5's parity definition: column j of the deterministic
+    # multi-RHS run == the reference rk_solve(A, B[:, j]) with the same sequence
+    # (kaczmarz.cpp:128-227), bit for bit, for every sampling; the records are
+    # the per-column exact values summed in column order
+    R = oracle.REF
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    k = 6
+    raw = name == "norm"
+    A, B, Xs = capi.generate_fixed_theta(3000, 1500, 12, seed=1005, k=k, scale_decades=1.0 if raw else 0.0)
+    rows = np.repeat(np.arange(A.m), np.diff(A.row_ptr))
+    Ah, _ = R.build(A.m, A.n, rows, A.col_idx, A.values, normalize=not raw)
+    E = 6
+    with capi.System(A, B[:, 0]) as S:
+        got = S.rk_solve_multi(B, max_epochs=E, target=0.0, seed=17, sampling=sampling, X_star=Xs)
+    assert list(got["epoch_index"]) == list(range(E + 1))
+    r_sum = np.zeros(E + 1)
+    g_sum = np.zeros(E + 1)
+    d_sum = np.zeros(E + 1)
+    for j in range(k):
+        want = R.rk_solve(Ah, np.ascontiguousarray(B[:, j]), np.zeros(A.n), E, 0.0, 17, name,
+                          np.ascontiguousarray(Xs[:, j]))
+        assert np.array_equal(got["X"][:, j], want["final_x"]), j
+        r_sum += want["r_sq"]  # column order, as the device adds them
+        g_sum += want["grad_sq"]
+        d_sum += want["dist_sq"]
+    assert np.array_equal(got["r_sq"], r_sum)
+    assert np.array_equal(got["grad_sq"], g_sum)
+    assert np.array_equal(got["dist_sq"], d_sum)
+    assert np.array_equal(got["updates_applied"], A.m * np.arange(E + 1))
+
+
+def test_deterministic_multi_rhs_global_stop_and_x0():
+    # a global target stops all columns together at the first epoch whose summed
+    # r_sq meets it; a nonzero X0 per column is each column's own start
+    R = oracle.REF
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    k = 4
+    A, B, Xs = capi.generate_fixed_theta(2000, 1000, 10, seed=9, k=k)
+    X0 = np.random.default_rng(1).standard_normal((A.n, k))
+    Ah, _ = R.build(A.m, A.n, np.repeat(np.arange(A.m), np.diff(A.row_ptr)), A.col_idx, A.values, normalize=True)
+    with capi.System(A, B[:, 0]) as S:
+        free = S.rk_solve_multi(B, X0=X0, max_epochs=30, target=0.0, seed=3)
+        tgt = float(free["r_sq"][12]) * 1.0000001
+        got = S.rk_solve_multi(B, X0=X0, max_epochs=30, target=tgt, seed=3)
+    assert int(got["epoch_index"][-1]) == 12
+    for j in range(k):
+        want = R.rk_solve(Ah, np.ascontiguousarray(B[:, j]), np.ascontiguousarray(X0[:, j]), 12, 0.0, 3, "uniform")
+        assert np.array_equal(got["X"][:, j], want["final_x"]), j
