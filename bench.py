@@ -378,6 +378,7 @@ def run_gpu(args):
             "time_to_tolerance_ms": statistics.median(step_ms), "epochs": statistics.median(epochs),
             "records_per_solve": statistics.median(records),
             "worker_launches_per_solve": w_launch / args.steps,
+            "library_solve_ms_per_step": sum(s["solve_ms"] for s in stats) / args.steps,
             "e2e": {"value": e2e_proj / e2e_wall, "unit": "proj/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": 1e3 * e2e_wall / e2e_steps, "calls_ms": e2e_calls},
             "instrumented": {"ms_per_solve": statistics.median(instr_ms),
@@ -502,7 +503,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    rows, epochs, records, wms, wl = 0, [], [], 0.0, 0
+    rows, epochs, records, wms, wl, lib_ms = 0, [], [], 0.0, 0, 0.0
     with ClockSampler(local) as clk:
         for k in range(steps):
             with torch.cuda.stream(stream):
@@ -512,6 +513,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
             ev[k][1].record(stream)
             st = sh.stats()
             wms += st["worker_ms"]
+            lib_ms += st["solve_ms"]
             wl += st["worker_launches"]
             rows += int(t["updates_applied"][-1])
             epochs.append(int(t["epoch_index"][-1]))
@@ -554,6 +556,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
             "ms_per_step": dev_ms / steps, "time_to_tolerance_ms": statistics.median(step_ms),
             "epochs": statistics.median(epochs), "records_per_solve": statistics.median(records),
             "worker_ms_per_solve": wms / steps, "worker_launches_per_solve": wl / steps,
+            "library_solve_ms_per_step": lib_ms / steps,
             "allreduce_us_per_call": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
             "driver": "asyrk_mrhs_solve_nccl (native loop, NCCL all-reduce of the shard norms per evaluated boundary)",
             "sampling": "slice_shuffle",

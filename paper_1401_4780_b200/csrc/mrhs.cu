@@ -123,7 +123,7 @@ __device__ __forceinline__ void mr_load(const MrhsArgs& a, long long i, int lane
 // all KL columns (the next 2 rows' records and B slices are prefetched while
 // the current ones gather / reduce / scatter; K2's structure).
 template <int KL>
-__global__ void __launch_bounds__(256) mrhs_worker_kernel(MrhsArgs a) {
+__global__ void __launch_bounds__(256, 3) mrhs_worker_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
     constexpr int R = 2;
     const DevState* st = a.st;
@@ -491,9 +491,12 @@ int mrhs_col_blocks(long long n) {
 template <int KL>
 static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
     const int blocks = (int)((a.W * 32 + 255) / 256);
-    // ASYRK_MRHS_LOOPED=1: the one-row-at-a-time worker for every row length (A/B runs)
-    static const bool looped = getenv("ASYRK_MRHS_LOOPED") != nullptr;
-    if (a.max_len <= 32 && !looped)
+    // Default: one row at a time (57 registers: 4 blocks / 32 warps per SM), the
+    // faster of the two measured at config 5 (0.64 vs 0.88 ms per epoch at 4096
+    // warps, profiles/r02_cfg5_probe.txt). ASYRK_MRHS_ROWS2=1: 2 rows in flight
+    // with prefetched records (80 registers, 3 blocks per SM).
+    static const bool rows2 = getenv("ASYRK_MRHS_ROWS2") != nullptr;
+    if (a.max_len <= 32 && rows2)
         mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
     else
         mrhs_worker_long_kernel<KL><<<blocks, 256, 0, s>>>(a);

@@ -1404,6 +1404,7 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
             launches += 3;
         }
         MonitorArgs mc = monitor_args(s, true, epoch > 0 ? 1 : 0, Xs != nullptr);
+        mc.x_star = Xs;  // (records dist_sq when given)
         mc.set_epoch = epoch;
         mc.mirror = s->mirror_dev;
         launch_multi_commit(mc, colres, (int)k, st);
@@ -1944,6 +1945,19 @@ asyrk_status asyrk_monte_carlo_ratios(const asyrk_csr_view* A, const double* b, 
         if (s) return s;
         return mc_impl(g.s, x0, cfg, runs, mean_r_sq, ratios);
     });
+}
+
+asyrk_status asyrk_monitor_schedule_next(double target_r_sq, int32_t every, int64_t max_gap, const int64_t* boundaries,
+                                         const double* r_sq, int64_t count, int64_t* next) {
+    if (!next || count < 1 || !boundaries || !r_sq)
+        return fail(ASYRK_E_InvalidArgument, "monitor_schedule_next: need at least one record");
+    MonitorSchedule sch;
+    sch.reset(target_r_sq, every != 0);
+    if (max_gap > 0) sch.max_gap = max_gap;
+    long long nx = 0;
+    for (int64_t i = std::max<int64_t>(0, count - 2); i < count; ++i) nx = sch.push(boundaries[i], r_sq[i]);
+    *next = nx;
+    return ASYRK_OK;
 }
 
 // rate_fit (ref/src/delay_sim.cpp:272-338): least-squares slope of log(y[k])

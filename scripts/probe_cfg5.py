@@ -2,7 +2,7 @@
 
 Runs fixed 6-epoch solves (every boundary evaluated) and full tolerance solves,
 prints per-epoch worker and monitor times from the library's own event timers.
-Set ASYRK_MRHS_LOOPED=1 for the one-row-at-a-time worker (A/B).
+Set ASYRK_MRHS_ROWS2=1 for the 2-rows-in-flight worker (A/B).
 """
 import json
 import os
@@ -33,7 +33,7 @@ for kl in kls:
             t = S.solve(threads=W, epochs=400, target=1e-10 * bbk, seed=3, sampling=samp)
             wall = time.perf_counter() - t0
             st2 = S.stats()
-            print(json.dumps({"kl": kl, "warps": W, "sampling": nm, "looped": bool(os.environ.get("ASYRK_MRHS_LOOPED")),
+            print(json.dumps({"kl": kl, "warps": W, "sampling": nm, "rows2": bool(os.environ.get("ASYRK_MRHS_ROWS2")),
                               "worker_ms_per_epoch": round(per_w, 4), "monitor_ms_per_eval": round(per_m, 4),
                               "solve_ms": round(st2["solve_ms"], 3), "host_wall_ms": round(1e3 * wall, 3),
                               "epochs": int(t["epoch_index"][-1]), "records": len(t["epoch_index"]),

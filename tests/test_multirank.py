@@ -13,11 +13,15 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_1401_4780_b200 import capi
 from paper_1401_4780_b200.mrhs import shard_columns, solve_sharded
 
 
 class NumpyShard:
-    """Serial RK on columns [c0, c1) of X/B; same protocol as CudaShardBackend."""
+    """Serial RK on columns [c0, c1) of X/B; same protocol as CudaShardBackend,
+    including the library's monitor schedule (asyrk_monitor_schedule_next, the
+    host arithmetic the native drivers use): only the boundaries it picks are
+    evaluated and all-reduced."""
 
     def __init__(self, A, B, c0, c1):
         self.A, self.B = A, B[:, c0:c1].copy()
@@ -28,8 +32,10 @@ class NumpyShard:
         m, n = self.A.shape
         self.X = np.zeros((n, self.c1 - self.c0))
         self.target, self.epochs, self.interval = target, epochs, snapshot_interval
+        self.max_chunks = (epochs + snapshot_interval - 1) // snapshot_interval if epochs > 0 else 0
         self.rng = np.random.default_rng(seed)
         self.epoch, self.stop, self.records = 0, False, []
+        self.b, self.next_mon, self.is_due = 0, 1, True
         self._norms = torch.zeros(3, dtype=torch.float64)
         self._measure()
 
@@ -44,14 +50,16 @@ class NumpyShard:
         return self._norms
 
     def commit(self, advance):
-        if self.stop:
+        if self.stop or not self.is_due:
             return
-        if advance:
-            self.epoch += min(self.interval, self.epochs - self.epoch)
+        self.is_due = False
         rs, gs = float(self._norms[0]), float(self._norms[1])
-        self.records.append((self.epoch, rs, gs))
+        self.records.append((self.b, self.epoch, rs, gs))
         if rs <= self.target or self.epoch >= self.epochs:
             self.stop = True
+        bd = [r[0] for r in self.records[-2:]]
+        rq = [r[2] for r in self.records[-2:]]
+        self.next_mon = capi.monitor_schedule_next(self.target, bd, rq)
 
     def step(self):
         if self.stop:
@@ -62,16 +70,20 @@ class NumpyShard:
             a = self.A[i]
             res = a @ self.X - self.B[i]
             self.X -= np.outer(a, res) / (a @ a)
-        self._measure()
-
-    def stopped(self):
-        return self.stop
+        self.epoch += span
+        self.b += 1
+        self.is_due = self.b >= self.next_mon or self.b >= self.max_chunks
+        if self.is_due:
+            self._measure()
 
     def due(self):
-        return True
+        return self.is_due
+
+    def stopped(self):
+        return self.stop or self.b >= self.max_chunks
 
     def finish(self):
-        return dict(epoch_index=np.array([r[0] for r in self.records]), r_sq=np.array([r[1] for r in self.records]),
+        return dict(epoch_index=np.array([r[1] for r in self.records]), r_sq=np.array([r[2] for r in self.records]),
                     X=self.X, local_r_sq=self.local_r_sq)
 
 
@@ -104,6 +116,23 @@ def _free_port():
         return s.getsockname()[1]
 
 
+def test_monitor_schedule_host_arithmetic():
+    # asyrk_monitor_schedule_next (csrc/schedule.h): the next boundary while
+    # fewer than two records exist / the residual did not drop / every boundary
+    # is requested / the target is 0; else 3/4 of the predicted distance to the
+    # target, at least 1 and at most the max gap
+    nx = capi.monitor_schedule_next
+    assert nx(1e-6, [0], [1.0]) == 1
+    assert nx(1e-6, [3, 4], [1.0, 2.0]) == 5
+    assert nx(1e-6, [3, 4], [1.0, 0.5], every=True) == 5
+    assert nx(0.0, [3, 4], [1.0, 0.5]) == 5
+    # r halves per boundary: 20 boundaries to 1e-6 from 1 -> gap min(floor(0.75 * 20), 8)
+    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0]) == 4 + 8
+    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0], max_gap=30) == 4 + 15
+    assert nx(2.0 ** -2, [3, 4], [2.0, 1.0]) == 4 + 1
+    assert nx(0.9, [3, 4], [2.0, 1.0]) == 4 + 1  # below one boundary away: the next one
+
+
 def test_shard_columns_cover_and_split_evenly():
     for world in (1, 2, 4, 8):
         spans = [shard_columns(64, world, r) for r in range(world)]
@@ -126,6 +155,13 @@ def test_two_rank_gloo_global_stop():
     # the all-reduced stop test makes both ranks stop at the same snapshot with identical records
     assert res[0]["epochs"] == res[1]["epochs"]
     assert res[0]["r_sq"] == res[1]["r_sq"]
+    # the monitor schedule (a function of the all-reduced records) evaluated the
+    # same subset of boundaries on both ranks: fewer records than epochs, the
+    # last one meets the target and the one before it did not
+    ep, rq = res[0]["epochs"], res[0]["r_sq"]
+    target = (1e-5) ** 2 * float((B * B).sum())
+    assert ep[0] == 0 and len(ep) < ep[-1] + 1
+    assert rq[-1] <= target < rq[-2]
     # the recorded residual is the global one: sum of the shards' residuals
     assert res[0]["r_sq"][-1] == pytest.approx(res[0]["local"] + res[1]["local"], rel=1e-12)
     X = np.concatenate([res[0]["X"], res[1]["X"]], axis=1)
