@@ -947,14 +947,14 @@ def run_lsq(args):
 
 def run_cfg5_shards(args):
     """Config 5 per-rank work at G = 1, 2, 4, 8 on ONE GPU: the shard a rank of a
-    G-GPU job owns (k/G RHS columns) solved alone with its own stop test. A
-    projection of strong scaling, NOT a multi-GPU measurement: the G-GPU job
-    adds one all-reduce of 3 doubles per epoch (NCCL, not timed here) and its
-    stop is global."""
+    G-GPU job owns (k/G RHS columns) solved alone (native loop, asyrk_mrhs_solve)
+    with its own stop test. A projection of strong scaling, NOT a multi-GPU
+    measurement: the G-GPU job adds one all-reduce of 3 doubles per evaluated
+    boundary (NCCL) and its stop is global."""
     import torch
 
     from paper_1401_4780_b200 import capi
-    from paper_1401_4780_b200.mrhs import CudaShardBackend, shard_columns, solve_sharded
+    from paper_1401_4780_b200.mrhs import shard_columns
 
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
@@ -965,24 +965,26 @@ def run_cfg5_shards(args):
     for G in [1, 2, 4, 8]:
         c0, c1 = shard_columns(CFG5["k"], G, 0)
         bb = float((B[:, c0:c1].astype(np.float64) ** 2).sum())
-        be = CudaShardBackend(A, B, c0, c1)
-        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1)
-        solve_sharded(be, seed=1, **kw)
-        times, epochs, rows = [], [], 0
+        S = capi.MultiRHS(A, B, c0, c1)
+        kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1,
+                  sampling=capi.SLICE_SHUFFLE, want_x=False)
+        S.solve(seed=1, **kw)
+        times, epochs, rows, wms = [], [], 0, 0.0
         for k in range(args.steps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             e0.record()
-            t = solve_sharded(be, seed=100 + k, **kw)
+            t = S.solve(seed=100 + k, **kw)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
             epochs.append(int(t["epoch_index"][-1]))
             rows += int(t["updates_applied"][-1])
-        be.close()
+            wms += S.stats()["worker_ms"]
+        S.close()
         ms = statistics.median(times)
         points.append({"gpus": G, "columns_per_gpu": c1 - c0, "shard_time_to_tolerance_ms": ms,
-                       "epochs": statistics.median(epochs),
+                       "epochs": statistics.median(epochs), "worker_ms_per_solve": wms / args.steps,
                        "shard_column_proj_per_s": rows * (c1 - c0) / (sum(times) * 1e-3)})
     t1 = points[0]["shard_time_to_tolerance_ms"]
     for p in points:
@@ -992,7 +994,8 @@ def run_cfg5_shards(args):
                       "config": {"workload": "config5: m=500000 n=250000 theta=20 k=64 fp32; each point = the "
                                              "k/G-column shard of one rank of a G-GPU job, solved alone on one "
                                              "GPU with a shard-local stop at 1e-5 (the real job all-reduces 3 "
-                                             "doubles per epoch and stops globally)", "warps": W},
+                                             "doubles per evaluated boundary and stops globally)", "warps": W,
+                                 "sampling": "slice_shuffle"},
                       "points": points}))
     return 0
 

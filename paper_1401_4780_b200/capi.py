@@ -259,6 +259,7 @@ def lib():
         L.asyrk_mrhs_solve.argtypes = [sp, C.POINTER(RunConfig), _f32p, _f64p, C.POINTER(TraceOut), _f32p]
         L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_mrhs_due.argtypes = [sp, _i32p]
+        L.asyrk_microbench_xside_mrhs.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _f64p, _f64p]
         L.asyrk_monitor_schedule_next.argtypes = [C.c_double, C.c_int32, C.c_int64, _i64p, _f64p, C.c_int64, _i64p]
         L.asyrk_system_rk_solve_multi.argtypes = [sp, _f64p, C.c_int64, _f64p, C.POINTER(RkConfig), _f64p,
                                                   C.POINTER(TraceOut)]
@@ -291,7 +292,7 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_monitor_schedule_next", "asyrk_system_rk_solve_multi", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
+    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_microbench_xside_mrhs", "asyrk_monitor_schedule_next", "asyrk_system_rk_solve_multi", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
     "asyrk_nccl_comm_init_rank", "asyrk_nccl_comm_destroy", "asyrk_mrhs_solve_nccl", "asyrk_mrhs_solve_devices",
     "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
@@ -367,16 +368,15 @@ class MultiRHS:
         d["X"] = X
         return d
 
-    def solve(self, X0=None, X_star=None, **cfg):
+    def solve(self, X0=None, X_star=None, want_x=True, **cfg):
         c = _run_config(**cfg)
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
         tr = _Trace(0, cap, want_x=False)
-        X = np.zeros((self.n, self.c1 - self.c0), np.float32)
+        X = np.zeros((self.n, self.c1 - self.c0), np.float32) if want_x else None
         x0 = _mat(X0, (self.n, self.k_total), np.float32, "X0") if X0 is not None else None
         xs = _mat(X_star, (self.n, self.k_total), np.float64, "X_star") if X_star is not None else None
         check(lib().asyrk_mrhs_solve(self.h, C.byref(c), x0.ctypes.data_as(C.POINTER(C.c_float)) if x0 is not None
-                                     else None, _ptr(xs, _f64p), C.byref(tr.out),
-                                     X.ctypes.data_as(C.POINTER(C.c_float))))
+                                     else None, _ptr(xs, _f64p), C.byref(tr.out), _ptr(X, C.POINTER(C.c_float))))
         d = tr.result(xs is not None)
         d["X"] = X
         return d
@@ -492,6 +492,13 @@ def _vec(a, n, name):
     if v.ndim != 1 or v.shape[0] != n:
         raise AsyrkError(6, f"{name} has {v.size} entries, expected {n}")
     return v
+
+
+def microbench_xside_mrhs(n, theta, kl, warps=4096, proj_per_warp=64):
+    """R_x of the multi-RHS pattern (asyrk_microbench_xside_mrhs): row projections/s."""
+    rate, ms = C.c_double(), C.c_double()
+    check(lib().asyrk_microbench_xside_mrhs(n, theta, kl, warps, proj_per_warp, C.byref(rate), C.byref(ms)))
+    return rate.value
 
 
 def check(status: int):

@@ -25,10 +25,10 @@ struct AliasEntry {
 struct WorkerArgs {
     Layout L;
     void* x;                      // X[n]
-    double* audit;                // kAuditK checksums (instrumented run) or nullptr
+    double* audit;                // instrumented run: per-warp checksums [W][kAuditK], or nullptr
     const AliasEntry* alias;      // m entries (S_ALIAS)
     DevState* st;
-    unsigned long long* increments;
+    unsigned long long* increments;  // instrumented run: per-warp increment counts [W]
     long long W;                  // worker warps
     double gamma;
     uint32_t key0, key1;          // seed
@@ -265,9 +265,13 @@ void launch_x_init(const double* x0, void* x, long long n, int precision, cudaSt
 void launch_x_export(const void* x, double* out, long long n, int precision, cudaStream_t s);
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target,
                        cudaStream_t s);
-// async audit (layout.cuh kAuditK checksums): audit holds 2 kAuditK doubles
-void launch_audit_check(const void* x, const double* x0, long long n, int precision, double* audit, double* out_max,
-                        cudaStream_t s);
+// async audit (layout.cuh kAuditK checksums): part = the workers' per-warp
+// checksums [W][kAuditK], incr = their per-warp increment counts [W]; lhs =
+// kAuditK scratch doubles; writes max_k |lhs_k - sum_w part[w][k]| to out_max
+// and sum_w incr[w] to out_incr
+void launch_audit_check(const void* x, const double* x0, long long n, int precision, const double* part,
+                        const unsigned long long* incr, long long W, double* lhs, double* out_max,
+                        unsigned long long* out_incr, cudaStream_t s);
 void launch_instrument_check(const void* x, const double* x0, const void* shadow, long long n,
                              int precision, double* out_max, cudaStream_t s);
 

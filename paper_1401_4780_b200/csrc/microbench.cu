@@ -70,6 +70,57 @@ __global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta,
     if (mode == 1 && acc_all == X(12345.678)) atomicAdd(sink, 1ull);  // keep the gathers alive
 }
 
+// Multi-RHS x side (config 5): per "projection" theta random rows of X (KL
+// fp32 columns each) gathered as float4 / float2 lanes, the per-column warp
+// reduction, then theta red.global.add.v4.f32 / .v2 back into the same rows —
+// the K2b worker's X traffic with no A / B stream.
+template <int KL>
+__global__ void __launch_bounds__(256) xside_mrhs_kernel(float* X, uint32_t n, int theta, long long per_warp) {
+    constexpr int VW = KL >= 4 ? 4 : 2, GL = KL / VW, S = 32 / GL;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31, slot = lane / GL, cl = lane % GL;
+    for (long long q = 0; q < per_warp; ++q) {
+        float acc[VW];
+#pragma unroll
+        for (int u = 0; u < VW; ++u) acc[u] = 0.f;
+        for (int t0 = 0; t0 < theta; t0 += S) {
+            const int t = t0 + slot;
+            if (t < theta) {
+                const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)t * 0xC2B2AE35u);
+                const uint32_t row = (uint32_t)(((uint64_t)h * n) >> 32);
+                const float* p = X + (size_t)row * KL + VW * cl;
+                if constexpr (VW == 4) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
+                    acc[0] += v.x, acc[1] += v.y, acc[2] += v.z, acc[3] += v.w;
+                } else {
+                    const float2 v = __ldcg(reinterpret_cast<const float2*>(p));
+                    acc[0] += v.x, acc[1] += v.y;
+                }
+            }
+        }
+#pragma unroll
+        for (int o = GL; o < 32; o <<= 1)
+#pragma unroll
+            for (int u = 0; u < VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
+        for (int t0 = 0; t0 < theta; t0 += S) {
+            const int t = t0 + slot;
+            if (t < theta) {
+                const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)t * 0xC2B2AE35u);
+                const uint32_t row = (uint32_t)(((uint64_t)h * n) >> 32);
+                float* p = X + (size_t)row * KL + VW * cl;
+                if constexpr (VW == 4)
+                    asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                                 "f"(1e-30f * acc[0]), "f"(1e-30f * acc[1]), "f"(1e-30f * acc[2]), "f"(1e-30f * acc[3])
+                                 : "memory");
+                else
+                    asm volatile("red.relaxed.gpu.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(1e-30f * acc[0]),
+                                 "f"(1e-30f * acc[1])
+                                 : "memory");
+            }
+        }
+    }
+}
+
 template <class X>
 static void xside_launch(int rows, int blocks, int threads, void* x, int64_t n, int theta, int64_t per_warp, int mode,
                          unsigned long long* sink, cudaStream_t s) {
@@ -154,6 +205,47 @@ asyrk_status xside_on_buffer(void* x, int64_t n, int32_t theta, int32_t precisio
         xside_time(x, n, theta, precision, warps, per_warp, mode, static_cast<cudaStream_t>(stream), ms, blocks);
     if (st) return st;
     *proj_per_s = (double)blocks * 256 / 32 * (double)per_warp / (ms * 1e-3);
+    if (kernel_ms) *kernel_ms = ms;
+    return ASYRK_OK;
+}
+
+// R_x of the multi-RHS pattern (config 5): X n x kl fp32 on a 2 MB boundary
+extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, int32_t kl, int32_t warps,
+                                                    int64_t proj_per_warp, double* proj_per_s, double* kernel_ms) {
+    using namespace ak;
+    if (n < 1 || theta < 1 || warps < 1 || proj_per_warp < 1 || !(kl == 2 || kl == 4 || kl == 8 || kl == 16 ||
+                                                                   kl == 32 || kl == 64))
+        return fail(ASYRK_E_InvalidArgument, "microbench_xside_mrhs: need n, theta, warps >= 1 and kl in 2..64");
+    void* base = nullptr;
+    const size_t xb = (size_t)n * kl * 4, page = 2u << 20;
+    if (cudaMalloc(&base, xb + page) != cudaSuccess) return ASYRK_E_TooLarge;
+    float* X = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(base) + page - 1) & ~(uintptr_t)(page - 1));
+    cudaMemset(X, 0, xb);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = (warps * 32 + 255) / 256;
+    float ms = 0.f;
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0);
+        switch (kl) {
+            case 2: xside_mrhs_kernel<2><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 4: xside_mrhs_kernel<4><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 8: xside_mrhs_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 16: xside_mrhs_kernel<16><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 32: xside_mrhs_kernel<32><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            default: xside_mrhs_kernel<64><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+        }
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(base);
+    if (err != cudaSuccess) return fail(ASYRK_E_ThreadSpawnFailure, cudaGetErrorString(err));
+    *proj_per_s = (double)blocks * 8 * (double)proj_per_warp / (ms * 1e-3);
     if (kernel_ms) *kernel_ms = ms;
     return ASYRK_OK;
 }

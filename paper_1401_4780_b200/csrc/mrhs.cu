@@ -234,9 +234,30 @@ __global__ void __launch_bounds__(256, 3) mrhs_worker_kernel(MrhsArgs a) {
     }
 }
 
-// Rows longer than 32 nonzeros: one row at a time, record read in the loop.
-template <int KL>
-__global__ void __launch_bounds__(256) mrhs_worker_long_kernel(MrhsArgs a) {
+// One row at a time, the record read in the loop (the default worker; any row
+// length). STREAM: A's records and B's rows are read with the evict-first
+// (streaming) cache policy so the X rows the projections gather and reduce
+// into keep their L2 residency (X is 64 MB at config 5, A + B stream 216 MB
+// per epoch through the 126 MB L2).
+template <class T>
+__device__ __forceinline__ T ld_a(const T* p, bool stream) {
+    return stream ? __ldcs(p) : __ldg(p);
+}
+template <int VW>
+__device__ __forceinline__ MrVec<VW> ld_b_stream(const float* p) {
+    MrVec<VW> r;
+    if constexpr (VW == 4) {
+        const float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        r.v[0] = t.x, r.v[1] = t.y, r.v[2] = t.z, r.v[3] = t.w;
+    } else {
+        const float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+        r.v[0] = t.x, r.v[1] = t.y;
+    }
+    return r;
+}
+
+template <int KL, bool STREAM, int MINB>
+__global__ void __launch_bounds__(256, MINB) mrhs_worker_long_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
     const DevState* st = a.st;
     if (!st->go) return;
@@ -274,8 +295,8 @@ __global__ void __launch_bounds__(256) mrhs_worker_long_kernel(MrhsArgs a) {
             for (int t0 = 0; t0 < len; t0 += G::S) {
                 const int t = t0 + slot;
                 if (t < len) {
-                    const float v = __ldg(vals + t);
-                    const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
+                    const float v = ld_a(vals + t, STREAM);
+                    const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl);
 #pragma unroll
                     for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
                 }
@@ -284,7 +305,8 @@ __global__ void __launch_bounds__(256) mrhs_worker_long_kernel(MrhsArgs a) {
             for (int o = G::GL; o < 32; o <<= 1)
 #pragma unroll
                 for (int u = 0; u < G::VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
-            const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
+            const MrVec<G::VW> bv = STREAM ? ld_b_stream<G::VW>(a.B + (size_t)i * KL + G::VW * cl)
+                                           : ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
             const float inv = (float)rec_inv(r);
             float cf[G::VW];
 #pragma unroll
@@ -292,11 +314,11 @@ __global__ void __launch_bounds__(256) mrhs_worker_long_kernel(MrhsArgs a) {
             for (int t0 = 0; t0 < len; t0 += G::S) {
                 const int t = t0 + slot;
                 if (t < len) {
-                    const float v = __ldg(vals + t);
+                    const float v = ld_a(vals + t, STREAM);
                     MrVec<G::VW> d;
 #pragma unroll
                     for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
-                    red_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
+                    red_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl, d);
                 }
             }
         }
@@ -496,10 +518,16 @@ static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
     // warps, profiles/r02_cfg5_probe.txt). ASYRK_MRHS_ROWS2=1: 2 rows in flight
     // with prefetched records (80 registers, 3 blocks per SM).
     static const bool rows2 = getenv("ASYRK_MRHS_ROWS2") != nullptr;
+    // ASYRK_MRHS_NOSTREAM=1: plain read-only loads for A / B (A/B runs);
+    // ASYRK_MRHS_MINB=5: 5 blocks (40 warps) per SM instead of 4
+    static const bool nostream = getenv("ASYRK_MRHS_NOSTREAM") != nullptr;
+    static const int minb = getenv("ASYRK_MRHS_MINB") ? atoi(getenv("ASYRK_MRHS_MINB")) : 4;
     if (a.max_len <= 32 && rows2)
         mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
+    else if (minb >= 5)
+        (nostream ? mrhs_worker_long_kernel<KL, false, 5> : mrhs_worker_long_kernel<KL, true, 5>)<<<blocks, 256, 0, s>>>(a);
     else
-        mrhs_worker_long_kernel<KL><<<blocks, 256, 0, s>>>(a);
+        (nostream ? mrhs_worker_long_kernel<KL, false, 4> : mrhs_worker_long_kernel<KL, true, 4>)<<<blocks, 256, 0, s>>>(a);
 }
 template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {

@@ -164,34 +164,61 @@ void launch_instrument_check(const void* x, const double* x0, const void* shadow
                                                                static_cast<const double*>(shadow), n, o);
 }
 
-// Async audit: lhs_k = sum_j s_k(j) (x_j - x0_j) next to the workers'
-// checksums of the increments they applied (audit[0..K) from the workers,
-// audit[K..2K) here); out_max = max_k |lhs_k - audit_k|.
+// Async audit: lhs_k = sum_j s_k(j) (x_j - x0_j) beside the workers'
+// per-warp checksums of the increments they applied; out_max = max_k
+// |lhs_k - sum_w part[w][k]| (the partials summed in a fixed order).
 template <class X>
-__global__ void audit_lhs_kernel(const X* __restrict__ x, const double* __restrict__ x0, long long n, double* audit) {
+__global__ void audit_lhs_kernel(const X* __restrict__ x, const double* __restrict__ x0, long long n, double* lhs) {
     double cs[kAuditK] = {};
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x)
         audit_add(cs, (int)k, (double)x[k] - x0[k]);
 #pragma unroll
     for (int q = 0; q < kAuditK; ++q) {
         const double v = warp_sum(cs[q]);
-        if ((threadIdx.x & 31) == 0) atomicAdd(audit + kAuditK + q, v);
+        if ((threadIdx.x & 31) == 0) atomicAdd(lhs + q, v);
     }
 }
-__global__ void audit_final_kernel(const double* audit, double* out_max) {
-    double mx = 0.0;
-    for (int q = 0; q < kAuditK; ++q) mx = fmax(mx, fabs(audit[kAuditK + q] - audit[q]));
-    *out_max = mx;
+__global__ void __launch_bounds__(256) audit_final_kernel(const double* part, const unsigned long long* incr,
+                                                          long long W, const double* lhs, double* out_max,
+                                                          unsigned long long* out_incr) {
+    __shared__ double red[kAuditK][256];
+    __shared__ unsigned long long ired[256];
+    double s[kAuditK] = {};
+    unsigned long long ic = 0;
+    for (long long w = threadIdx.x; w < W; w += 256) {
+#pragma unroll
+        for (int q = 0; q < kAuditK; ++q) s[q] += part[w * kAuditK + q];
+        ic += incr[w];
+    }
+#pragma unroll
+    for (int q = 0; q < kAuditK; ++q) red[q][threadIdx.x] = s[q];
+    ired[threadIdx.x] = ic;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+#pragma unroll
+            for (int q = 0; q < kAuditK; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+            ired[threadIdx.x] += ired[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (int q = 0; q < kAuditK; ++q) mx = fmax(mx, fabs(lhs[q] - red[q][0]));
+        *out_max = mx;
+        *out_incr = ired[0];
+    }
 }
-void launch_audit_check(const void* x, const double* x0, long long n, int precision, double* audit, double* out_max,
-                        cudaStream_t s) {
-    cudaMemsetAsync(audit + kAuditK, 0, kAuditK * sizeof(double), s);
+void launch_audit_check(const void* x, const double* x0, long long n, int precision, const double* part,
+                        const unsigned long long* incr, long long W, double* lhs, double* out_max,
+                        unsigned long long* out_incr, cudaStream_t s) {
+    cudaMemsetAsync(lhs, 0, kAuditK * sizeof(double), s);
     const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
     if (precision == P_F32)
-        audit_lhs_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x), x0, n, audit);
+        audit_lhs_kernel<float><<<blocks, 256, 0, s>>>(static_cast<const float*>(x), x0, n, lhs);
     else
-        audit_lhs_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), x0, n, audit);
-    audit_final_kernel<<<1, 1, 0, s>>>(audit, out_max);
+        audit_lhs_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), x0, n, lhs);
+    audit_final_kernel<<<1, 256, 0, s>>>(part, incr, W, lhs, out_max, out_incr);
 }
 
 // CUB radix sort wrapper: stable sort of (col, nnz-index) pairs by column, so

@@ -8,9 +8,11 @@
 // (two SpMVs over A), so here the coordinator decides WHICH boundaries to
 // evaluate from the records it already has: with the residual decaying
 // geometrically, the last two records give a rate and the number of snapshot
-// intervals left until r_sq <= target; the next evaluation is placed at 3/4 of
-// that distance (never more than max_gap intervals ahead, always the next
-// boundary while fewer than two records exist or the residual did not drop).
+// intervals left until r_sq <= target; the next evaluation is placed one
+// boundary before the predicted crossing (never more than max_gap intervals
+// ahead; the next boundary when the crossing is at most 2 away, while fewer
+// than two records exist, or when the residual did not drop), so an accurate
+// prediction costs two evaluations at the tail.
 // Near the stop every boundary is evaluated, so the stop is taken at the first
 // evaluated boundary that meets the target, and no epoch runs past it. With
 // target <= 0 (a fixed epoch budget) or record_every_boundary, every boundary
@@ -27,13 +29,13 @@ namespace ak {
 struct MonitorSchedule {
     double target = 0.0;
     bool every = false;
-    long long max_gap = 8;
+    long long max_gap = 12;
     long long b_prev = -1, b_last = -1;  // boundaries (in snapshot intervals) of the last two records
     double r_prev = 0.0, r_last = 0.0;
 
     void reset(double tgt, bool every_boundary) {
         target = tgt;
-        static const long long env_gap = getenv("ASYRK_MONITOR_MAX_GAP") ? atoll(getenv("ASYRK_MONITOR_MAX_GAP")) : 8;
+        static const long long env_gap = getenv("ASYRK_MONITOR_MAX_GAP") ? atoll(getenv("ASYRK_MONITOR_MAX_GAP")) : 12;
         static const bool env_every = getenv("ASYRK_MONITOR_EVERY") != nullptr;
         max_gap = env_gap > 0 ? env_gap : 1;
         every = every_boundary || env_every || !(tgt > 0.0);
@@ -55,8 +57,8 @@ struct MonitorSchedule {
         if (!(r_last > target) || !(r_last < r_prev) || !(r_prev > 0.0) || !std::isfinite(r_last)) return 1;
         const double rate = (std::log(r_last) - std::log(r_prev)) / (double)(b_last - b_prev);  // < 0
         const double left = (std::log(target) - std::log(r_last)) / rate;                        // > 0
-        if (!(left > 0.0) || !std::isfinite(left)) return 1;
-        long long g = (long long)std::floor(0.75 * left);
+        if (!(left > 2.0) || !std::isfinite(left)) return 1;
+        long long g = (long long)std::floor(left) - 1;  // one boundary before the predicted crossing
         if (g < 1) g = 1;
         if (g > max_gap) g = max_gap;
         return g;

@@ -95,6 +95,8 @@ struct asyrk_system {
     long long rec_cap = 0;
     DevState* st = nullptr;
     unsigned long long* incr = nullptr;
+    double* audit_part = nullptr;  // instrumented async solves: per-warp checksums [W][kAuditK] + counts [W]
+    long long audit_cap = 0;       // warps audit_part holds
     double* scratch = nullptr;
     int* host_flag = nullptr;      // pinned mapped
     int* host_flag_dev = nullptr;
@@ -260,6 +262,7 @@ void free_all(asyrk_system* s) {
     F(s->recs);
     F(s->st);
     F(s->incr);
+    F(s->audit_part);
     F(s->scratch);
     for (int h = 0; h < 2; ++h) {
         F(s->need[h]);
@@ -831,17 +834,17 @@ asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long l
         if (sp.det) {
             const long long done = sp.interval > 0 ? (hs.epoch + sp.interval - 1) / sp.interval : 0;
             for (long long c = 0; c < done && c < (long long)chunk_incr.size(); ++c) inc += chunk_incr[(size_t)c];
-        } else {
-            CK(cudaMemcpy(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost));
-        }
-        instr->increments = (int64_t)inc;
-        if (sp.det)
             launch_instrument_check(s->x, s->x0d, s->shadow, s->n, prec, s->scratch, st);
-        else
-            launch_audit_check(s->x, s->x0d, s->n, prec, s->scratch + 16, s->scratch, st);
+        } else {
+            launch_audit_check(s->x, s->x0d, s->n, prec, s->audit_part,
+                               reinterpret_cast<const unsigned long long*>(s->audit_part + sp.threads * kAuditK),
+                               sp.threads, s->scratch + 16, s->scratch, s->incr, st);
+            CK(cudaMemcpyAsync(&inc, s->incr, sizeof(inc), cudaMemcpyDeviceToHost, st));
+        }
         double mx = 0.0;
         CK(cudaMemcpyAsync(&mx, s->scratch, sizeof(double), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
+        instr->increments = (int64_t)inc;
         instr->max_abs_error = mx;
         instr->tolerance = 1e-9 * (double)std::max<int64_t>(instr->increments, 1);
         instr->consistent = mx <= instr->tolerance ? 1 : 0;
@@ -949,8 +952,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         if (sp.det) {  // the reference's per-component shadow (bitwise audit report)
             if (!s->shadow) s->shadow = dalloc<unsigned char>((size_t)s->n * 8);
             CK(cudaMemsetAsync(s->shadow, 0, (size_t)s->n * 8, st));
-        } else {  // the workers' signed checksums (layout.cuh kAuditK) in scratch[16..)
-            CK(cudaMemsetAsync(s->scratch + 16, 0, 2 * kAuditK * sizeof(double), st));
+        } else {  // the workers' per-warp signed checksums (layout.cuh kAuditK) and increment counts
+            if (s->audit_cap < sp.threads) {
+                pool_free(s->audit_part, st);
+                s->audit_part = dalloc<double>((size_t)sp.threads * (kAuditK + 1));
+                s->audit_cap = sp.threads;
+            }
+            CK(cudaMemsetAsync(s->audit_part, 0, (size_t)sp.threads * (kAuditK + 1) * sizeof(double), st));
         }
         CK(cudaMemsetAsync(s->incr, 0, sizeof(unsigned long long), st));
     }
@@ -1009,10 +1017,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         E = worker_elems_per_lane(s->max_len);
         wa.L = s->layout();
         wa.x = s->x;
-        wa.audit = instr ? s->scratch + 16 : nullptr;
+        wa.audit = instr ? s->audit_part : nullptr;
         wa.alias = s->alias;
         wa.st = s->st;
-        wa.increments = instr ? s->incr : nullptr;
+        wa.increments = instr ? reinterpret_cast<unsigned long long*>(s->audit_part + wa.W * kAuditK) : nullptr;
         wa.W = sp.threads;
         wa.gamma = sp.gamma;
         const uint64_t k = splitmix64(sp.seed ^ 0xA5A5A5A5DEADBEEFull);

@@ -63,13 +63,17 @@ __device__ __forceinline__ void load_frag(const Layout& L, long long row, int la
     f.inv = rec_inv(r);
 }
 
-// a warp's audit checksums into the solve's (one fp64 atomic per checksum per warp)
-__device__ __forceinline__ void audit_flush(const WorkerArgs& a, double (&cs)[kAuditK], int lane) {
+// a warp's audit checksums and increment count into its own slots (warp w
+// owns audit[w][0..K) and increments[w]; launches are stream-ordered, so a
+// plain read-add-write is race-free and no address is contended)
+__device__ __forceinline__ void audit_flush(const WorkerArgs& a, long long warp, double (&cs)[kAuditK], int lane,
+                                            unsigned long long incr) {
 #pragma unroll
     for (int k = 0; k < kAuditK; ++k) {
         const double v = warp_sum(cs[k]);
-        if (lane == 0) atomicAdd(a.audit + k, v);
+        if (lane == 0) a.audit[warp * kAuditK + k] += v;
     }
+    if (lane == 0) a.increments[warp] += incr;
 }
 
 // Lane-parallel draw of the rows for positions [j0, j0+32) of this warp's
@@ -230,8 +234,7 @@ __global__ void __launch_bounds__(256, kWorkerBlocksPerSM) worker_kernel(WorkerA
         B0 = B1;
         if (bi + 2 < nb) B1 = draw_row(a, warp, epoch, (bi + 2) * 32 + lane, slice_lo, slice_len);
     }
-    if (audit) audit_flush(a, cs, lane);
-    if (a.increments && lane == 0) atomicAdd(a.increments, incr);
+    if (audit) audit_flush(a, warp, cs, lane, incr);
 }
 
 // Rows longer than 128 nonzeros: chunked loop, no record prefetch.
@@ -295,8 +298,7 @@ __global__ void __launch_bounds__(256) worker_kernel_long(WorkerArgs a) {
             }
         }
     }
-    if (audit) audit_flush(a, cs, lane);
-    if (a.increments && lane == 0) atomicAdd(a.increments, incr);
+    if (audit) audit_flush(a, warp, cs, lane, incr);
 }
 
 // The workers' own row draws, written out (tests: alias frequencies, slice
