@@ -466,7 +466,7 @@ CFG5 = dict(m=500000, n=250000, theta=20, k=64, seed=1005)
 TOL5 = 1e-5
 
 
-def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
+def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=0):
     """BASELINE config 5 at this job's N: k=64 right-hand sides split into N
     contiguous column shards, one per rank (A replicated), each rank's
     lock-free warp-workers on its shard, and one NCCL all-reduce of the shard
@@ -493,6 +493,7 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
         uid = capi.nccl_unique_id()
     comm = capi.NcclComm(world, uid, rank)
     sh = capi.MultiRHS(A, B, c0, c1, stream=stream.cuda_stream)
+    W = W or sh.max_resident_warps()  # every co-resident worker warp (4736 at 64 columns on 148 SMs)
     kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1,
               sampling=capi.SLICE_SHUFFLE)
     for w in range(warmup):
@@ -547,16 +548,25 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=4096):
         t = torch.tensor([float(col_proj)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
         col_proj = float(t.item())
+    # the multi-RHS x-side ceiling at this shard's width and warp count (no A / B stream)
+    rx5 = max(capi.microbench_xside_mrhs(CFG5["n"], CFG5["theta"], c1 - c0, W, 64) for _ in range(2))
     sh.close()
     comm.close()
     if rank != 0:
         return None
+    worker_rate = rows / (wms * 1e-3) if wms > 0 else 0.0  # row projections per worker second (this rank)
     return {"metric": "config 5 column projections/sec (row projections x owned RHS columns, all ranks)",
             "value": col_proj / (dev_ms * 1e-3), "unit": "proj/s", "n_gpus": world, "steps": steps,
             "ms_per_step": dev_ms / steps, "time_to_tolerance_ms": statistics.median(step_ms),
             "epochs": statistics.median(epochs), "records_per_solve": statistics.median(records),
             "worker_ms_per_solve": wms / steps, "worker_launches_per_solve": wl / steps,
             "library_solve_ms_per_step": lib_ms / steps,
+            "roofline": {"bound": "l2_x_side", "unit": "row proj/s", "achieved": worker_rate, "peak": rx5,
+                         "frac": worker_rate / rx5 if rx5 else None,
+                         "source": "achieved = rank 0's row projections / its worker-launch time; peak = "
+                                   "asyrk_microbench_xside_mrhs (the K2b worker's X gathers and v4 reds, no A/B "
+                                   "stream) at the same width, warps and n, measured live",
+                         "x_bytes_per_row_proj": 2 * CFG5["theta"] * (c1 - c0) * 4},
             "allreduce_us_per_call": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
             "driver": "asyrk_mrhs_solve_nccl (native loop, NCCL all-reduce of the shard norms per evaluated boundary)",
             "sampling": "slice_shuffle",
@@ -584,7 +594,7 @@ def run_gpu_cfg5(args):
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.Stream()
-    c5 = cfg5_sharded(args.steps, args.warmup, dist, rank, world, local, stream, W=args.warps or 4096)
+    c5 = cfg5_sharded(args.steps, args.warmup, dist, rank, world, local, stream, W=args.warps)
     if rank == 0:
         line = {"metric": METRIC + " (config 5: column projections/sec)", "value": c5["value"], "unit": "proj/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": c5["ms_per_step"],
@@ -960,12 +970,12 @@ def run_cfg5_shards(args):
         return 0
     A, B, Xs = capi.generate_fixed_theta(CFG5["m"], CFG5["n"], CFG5["theta"], seed=CFG5["seed"], k=CFG5["k"])
     B = B.astype(np.float32)
-    W = args.warps or 4096
     points = []
     for G in [1, 2, 4, 8]:
         c0, c1 = shard_columns(CFG5["k"], G, 0)
         bb = float((B[:, c0:c1].astype(np.float64) ** 2).sum())
         S = capi.MultiRHS(A, B, c0, c1)
+        W = args.warps or S.max_resident_warps()
         kw = dict(threads=W, gamma=1.0, epochs=2000, target=TOL5 * TOL5 * bb, snapshot_interval=1,
                   sampling=capi.SLICE_SHUFFLE, want_x=False)
         S.solve(seed=1, **kw)
@@ -983,7 +993,7 @@ def run_cfg5_shards(args):
             wms += S.stats()["worker_ms"]
         S.close()
         ms = statistics.median(times)
-        points.append({"gpus": G, "columns_per_gpu": c1 - c0, "shard_time_to_tolerance_ms": ms,
+        points.append({"gpus": G, "columns_per_gpu": c1 - c0, "warps": W, "shard_time_to_tolerance_ms": ms,
                        "epochs": statistics.median(epochs), "worker_ms_per_solve": wms / args.steps,
                        "shard_column_proj_per_s": rows * (c1 - c0) / (sum(times) * 1e-3)})
     t1 = points[0]["shard_time_to_tolerance_ms"]
@@ -994,8 +1004,8 @@ def run_cfg5_shards(args):
                       "config": {"workload": "config5: m=500000 n=250000 theta=20 k=64 fp32; each point = the "
                                              "k/G-column shard of one rank of a G-GPU job, solved alone on one "
                                              "GPU with a shard-local stop at 1e-5 (the real job all-reduces 3 "
-                                             "doubles per evaluated boundary and stops globally)", "warps": W,
-                                 "sampling": "slice_shuffle"},
+                                             "doubles per evaluated boundary and stops globally)",
+                                 "warps": "all co-resident worker warps per shard width", "sampling": "slice_shuffle"},
                       "points": points}))
     return 0
 

@@ -376,6 +376,8 @@ asyrk_status asyrk_mrhs_finish(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_o
 asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const float* X0, const double* Xstar,
                               asyrk_trace_out* trace, float* X_out);
 asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out);
+/* Largest number of co-resident worker warps for this shard's width. */
+asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out);
 
 /* ---- multi-GPU: NCCL (SURVEY.md §8b "mrhs_shard_solve(..., ncclComm_t)") ----
  * libnccl.so.2 is resolved at run time (the copy already loaded in the

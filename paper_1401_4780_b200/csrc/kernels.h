@@ -167,6 +167,7 @@ struct MrhsArgs {
     uint32_t max_len;             // longest row (> 32: the looped worker)
 };
 bool mrhs_supported_kl(long long kl);
+int mrhs_max_resident_warps(int kl);  // co-resident worker warps (the default worker) on the current device
 int mrhs_row_blocks(long long m);
 int mrhs_col_blocks(long long n);
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s);

@@ -70,25 +70,30 @@ __global__ void __launch_bounds__(256) xside_kernel(X* x, uint32_t n, int theta,
     if (mode == 1 && acc_all == X(12345.678)) atomicAdd(sink, 1ull);  // keep the gathers alive
 }
 
-// Multi-RHS x side (config 5): per "projection" theta random rows of X (KL
-// fp32 columns each) gathered as float4 / float2 lanes, the per-column warp
-// reduction, then theta red.global.add.v4.f32 / .v2 back into the same rows —
-// the K2b worker's X traffic with no A / B stream.
+// Multi-RHS x side (config 5): per "projection" theta (<= 32) random rows of
+// X (KL fp32 columns each) gathered as float4 / float2 lanes, the per-column
+// warp reduction, then theta red.global.add.v4.f32 / .v2 back into the same
+// rows — the K2b worker's X traffic with no A / B stream. Row indices come
+// from one multiply-high of a per-lane LCG per element and stay in registers
+// between the gather and the reduce phases.
 template <int KL>
 __global__ void __launch_bounds__(256) xside_mrhs_kernel(float* X, uint32_t n, int theta, long long per_warp) {
-    constexpr int VW = KL >= 4 ? 4 : 2, GL = KL / VW, S = 32 / GL;
+    constexpr int VW = KL >= 4 ? 4 : 2, GL = KL / VW, S = 32 / GL, T = (32 + S - 1) / S;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, slot = lane / GL, cl = lane % GL;
+    uint32_t rng = hash32(warp * 0x9E3779B9u + (uint32_t)slot * 0x85EBCA6Bu) | 1u;
     for (long long q = 0; q < per_warp; ++q) {
+        uint32_t row[T];
         float acc[VW];
 #pragma unroll
         for (int u = 0; u < VW; ++u) acc[u] = 0.f;
-        for (int t0 = 0; t0 < theta; t0 += S) {
-            const int t = t0 + slot;
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+            rng = rng * 1664525u + 1013904223u;
+            row[j] = __umulhi(rng, n);
+            const int t = j * S + slot;
             if (t < theta) {
-                const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)t * 0xC2B2AE35u);
-                const uint32_t row = (uint32_t)(((uint64_t)h * n) >> 32);
-                const float* p = X + (size_t)row * KL + VW * cl;
+                const float* p = X + (size_t)row[j] * KL + VW * cl;
                 if constexpr (VW == 4) {
                     const float4 v = __ldcg(reinterpret_cast<const float4*>(p));
                     acc[0] += v.x, acc[1] += v.y, acc[2] += v.z, acc[3] += v.w;
@@ -102,12 +107,11 @@ __global__ void __launch_bounds__(256) xside_mrhs_kernel(float* X, uint32_t n, i
         for (int o = GL; o < 32; o <<= 1)
 #pragma unroll
             for (int u = 0; u < VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
-        for (int t0 = 0; t0 < theta; t0 += S) {
-            const int t = t0 + slot;
+#pragma unroll
+        for (int j = 0; j < T; ++j) {
+            const int t = j * S + slot;
             if (t < theta) {
-                const uint32_t h = hash32(warp * 0x9E3779B9u + (uint32_t)q * 0x85EBCA6Bu + (uint32_t)t * 0xC2B2AE35u);
-                const uint32_t row = (uint32_t)(((uint64_t)h * n) >> 32);
-                float* p = X + (size_t)row * KL + VW * cl;
+                float* p = X + (size_t)row[j] * KL + VW * cl;
                 if constexpr (VW == 4)
                     asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
                                  "f"(1e-30f * acc[0]), "f"(1e-30f * acc[1]), "f"(1e-30f * acc[2]), "f"(1e-30f * acc[3])
@@ -213,9 +217,10 @@ asyrk_status xside_on_buffer(void* x, int64_t n, int32_t theta, int32_t precisio
 extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, int32_t kl, int32_t warps,
                                                     int64_t proj_per_warp, double* proj_per_s, double* kernel_ms) {
     using namespace ak;
-    if (n < 1 || theta < 1 || warps < 1 || proj_per_warp < 1 || !(kl == 2 || kl == 4 || kl == 8 || kl == 16 ||
-                                                                   kl == 32 || kl == 64))
-        return fail(ASYRK_E_InvalidArgument, "microbench_xside_mrhs: need n, theta, warps >= 1 and kl in 2..64");
+    if (n < 1 || theta < 1 || theta > 32 || warps < 1 || proj_per_warp < 1 ||
+        !(kl == 2 || kl == 4 || kl == 8 || kl == 16 || kl == 32 || kl == 64))
+        return fail(ASYRK_E_InvalidArgument,
+                    "microbench_xside_mrhs: need n, warps >= 1, 1 <= theta <= 32 and kl a power of two in 2..64");
     void* base = nullptr;
     const size_t xb = (size_t)n * kl * 4, page = 2u << 20;
     if (cudaMalloc(&base, xb + page) != cudaSuccess) return ASYRK_E_TooLarge;

@@ -548,6 +548,16 @@ static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
     }
 
 bool mrhs_supported_kl(long long kl) { return kl >= 2 && kl <= 64 && (kl & (kl - 1)) == 0; }
+
+template <int KL>
+static void mrhs_occupancy(int& per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrhs_worker_long_kernel<KL, true, 4>, 256, 0);
+}
+int mrhs_max_resident_warps(int kl) {
+    int per_sm = 0;
+    MR_DISPATCH(kl, mrhs_occupancy, per_sm)
+    return per_sm * 8 * mr_sms();
+}
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s) { MR_DISPATCH(a.KL, mrhs_worker_launch, a, s) }
 void launch_mrhs_monitor(const MrhsArgs& a, cudaStream_t s) { MR_DISPATCH(a.KL, mrhs_monitor_launch, a, s) }
 void launch_mrhs_commit(const MrhsArgs& a, long long set_epoch, cudaStream_t s) {

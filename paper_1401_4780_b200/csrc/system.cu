@@ -1020,7 +1020,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         wa.audit = instr ? s->audit_part : nullptr;
         wa.alias = s->alias;
         wa.st = s->st;
-        wa.increments = instr ? reinterpret_cast<unsigned long long*>(s->audit_part + wa.W * kAuditK) : nullptr;
+        wa.increments = instr ? reinterpret_cast<unsigned long long*>(s->audit_part + sp.threads * kAuditK) : nullptr;
         wa.W = sp.threads;
         wa.gamma = sp.gamma;
         const uint64_t k = splitmix64(sp.seed ^ 0xA5A5A5A5DEADBEEFull);
@@ -2661,6 +2661,14 @@ asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const 
         asyrk_status st = mrhs_run(hs, {}, {}, cfg, X0, Xstar);
         if (st) return st;
         return mrhs_finish_impl(h, trace, X_out);
+    });
+}
+
+asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out) {
+    if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
+    return guarded([&] {
+        *out = mrhs_max_resident_warps((int)h->kl);
+        return ASYRK_OK;
     });
 }
 

@@ -1,7 +1,11 @@
-"""Copy one profiling round (scripts/profile_round.sh outputs in gpurun_out/)
-into profiles/ under a round tag: bench / reference lines, x-side probe,
-ncu launch-list summary, ncu --set full metric summary, and the worker's
-per-launch DRAM traffic that bench.py reports as roofline.traffic."""
+"""Copy one profiling round (scripts/profile_round2.sh outputs) into profiles/
+under a round tag: bench / reference lines, x-side and config-5 probes, ncu
+launch-list summaries, ncu --set full metric summaries (worker + monitor,
+x-side microbenchmark, config-5 kernels), and the worker's per-launch DRAM
+traffic / L2 requests that bench.py reports (profiles/worker_ncu_summary.json).
+
+  python scripts/save_profiles.py <tag> [source dir (default gpurun_out)]
+"""
 import csv
 import json
 import os
@@ -10,30 +14,47 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-src = os.path.join(ROOT, "gpurun_out")
+tag = sys.argv[1] if len(sys.argv) > 1 else "r02"
+src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
 dst = os.path.join(ROOT, "profiles")
-tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 
 for name, out in [("bench.json", f"{tag}_bench.json"), ("ref.json", f"{tag}_ref.json"),
-                  ("xside.txt", f"{tag}_xside.txt"), ("launches.csv", f"{tag}_launches.csv")]:
+                  ("xside.txt", f"{tag}_xside.txt"), ("probe_cfg5.txt", f"{tag}_cfg5_probe.txt")]:
     p = os.path.join(src, name)
     if os.path.exists(p):
         shutil.copy(p, os.path.join(dst, out))
 
-launches = os.path.join(src, "launches.csv")
-if os.path.exists(launches):
-    txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "launches.py"), launches],
+
+def summary(rep, header):
+    txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), rep],
                          capture_output=True, text=True).stdout
-    open(os.path.join(dst, f"{tag}_launches.txt"), "w").write(
-        "# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialized launches)\n"
-        "# python bench.py --steps 1 --warmup 1 --no-cpu-baseline\n" + txt)
+    return header + txt
+
+
+for name, cmd in [("launches.csv", "python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cfg5"),
+                  ("cfg5_launches.csv", "python scripts/cfg5_once.py")]:
+    p = os.path.join(src, name)
+    if os.path.exists(p):
+        txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "launches.py"), p],
+                             capture_output=True, text=True).stdout
+        base = name.replace(".csv", "")
+        open(os.path.join(dst, f"{tag}_{base}.txt"), "w").write(
+            "# ncu --metrics gpu__time_duration.sum --clock-control none (cold, serialized launches)\n"
+            f"# {cmd}\n" + txt)
+
+for rep, out, hdr in [
+        ("full.ncu-rep", "ncu_full", "# ncu --set full --clock-control none -k regex:worker_kernel|rows_kernel|cols_final_kernel"
+                                     " (config 2 bench, 1 step)\n"),
+        ("xside.ncu-rep", "ncu_xside", "# ncu --set full -k regex:xside_kernel: python scripts/probe_xside.py ncu "
+                                       "(2 rows in flight, then 1; f64, n=100000, theta=30, 3552 warps, 256 proj/warp)\n"),
+        ("mrhs.ncu-rep", "ncu_mrhs", "# ncu --set full -k regex:mrhs_worker|mrhs_rows|mrhs_cols: python scripts/cfg5_once.py "
+                                     "(config 5, 64 columns on one GPU)\n")]:
+    p = os.path.join(src, rep)
+    if os.path.exists(p):
+        open(os.path.join(dst, f"{tag}_{out}.txt"), "w").write(summary(p, hdr))
 
 rep = os.path.join(src, "full.ncu-rep")
 if os.path.exists(rep):
-    txt = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), rep],
-                         capture_output=True, text=True).stdout
-    open(os.path.join(dst, f"{tag}_ncu_full.txt"), "w").write(
-        "# ncu --set full --clock-control none --import-source on -k regex:worker_kernel|rows_kernel|cols_kernel|cols_final_kernel\n" + txt)
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(raw.splitlines()))
     h = rows[0]
@@ -46,15 +67,18 @@ if os.path.exists(rep):
             reqs[key] = float(v[h.index("lts__t_requests.sum")].replace(",", ""))
     for v in rows[2:]:
         if "worker_kernel" in v[h.index("Kernel Name")]:
-            num = lambda k: float(v[h.index(k)].replace(",", ""))  # noqa: E731
-            unit = rows[1][h.index("dram__bytes_read.sum")]
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            def num(k):
+                x = float(v[h.index(k)].replace(",", ""))
+                unit = rows[1][h.index(k)]
+                return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             d = {"kernel": v[h.index("Kernel Name")], "round": tag,
-                 "dram_bytes_per_launch": int((num("dram__bytes_read.sum") + num("dram__bytes_write.sum")) * scale),
+                 "source": f"profiles/{tag}_ncu_full.txt (ncu --set full, cold caches, 1 launch)",
+                 "dram_bytes_per_launch": int(num("dram__bytes_read.sum") + num("dram__bytes_write.sum")),
                  "gpu_time_us": num("gpu__time_duration.sum"),
                  "lts_t_requests": num("lts__t_requests.sum"),
                  "lts_tag_requests_pct_avg": num("lts__t_tag_requests.avg.pct_of_peak_sustained_elapsed"),
                  "lts_tag_requests_pct_max": num("lts__t_tag_requests.max.pct_of_peak_sustained_elapsed"),
+                 "lts_atomic_input_pct_avg": num("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed"),
                  "projections_per_launch": 200000,
                  "lts_requests_per_launch": reqs}
             json.dump(d, open(os.path.join(dst, "worker_ncu_summary.json"), "w"), indent=1)
