@@ -118,9 +118,14 @@ typedef struct {
     /* --- device extensions (zero = reference behaviour) --- */
     int32_t precision;         /* ASYRK_F64 ... */
     int32_t allow_unnormalized; /* 1: async/norm_proportional on raw rows (config 4) */
-    int32_t record_every_boundary; /* async: 1 = a record at every snapshot boundary (the workers
-                                      wait for the residual monitor); 0 = the monitor records the
-                                      latest boundary it can, like the reference coordinator */
+    int32_t record_every_boundary; /* async: 1 = a record at every snapshot boundary; 0 = the
+                                      boundaries the host-driven monitor schedule picks (
+                                      the reference coordinator likewise records only the boundaries
+                                      it catches), always including the stopping one */
+    int32_t det_reassociate;   /* threads == 1: 0 = the reference's floating-point order (bitwise,
+                                  default); 1 = the same row sequence with a warp-tree dot product,
+                                  the precomputed reciprocal and a fused update (iterates within
+                                  1e-12 relative of the reference) */
 } asyrk_run_config;
 
 /* RkConfig (kaczmarz.hpp:95-103) */
@@ -130,6 +135,8 @@ typedef struct {
     uint64_t seed;
     int32_t sampling;          /* ASYRK_RK_* */
     const double* x_star;
+    /* --- device extension (zero = reference behaviour) --- */
+    int32_t det_reassociate;   /* as asyrk_run_config::det_reassociate */
 } asyrk_rk_config;
 
 /* Trace (trace.hpp:11-37), caller-allocated. count receives the number of

@@ -43,12 +43,13 @@ class RunConfig(C.Structure):
     _fields_ = [("threads", C.c_int64), ("gamma", C.c_double), ("epochs", C.c_int64), ("target_r_sq", C.c_double),
                 ("variant", C.c_int32), ("sampling", C.c_int32), ("seed", C.c_uint64),
                 ("snapshot_interval", C.c_int64), ("x_star", _f64p), ("precision", C.c_int32),
-                ("allow_unnormalized", C.c_int32), ("record_every_boundary", C.c_int32)]
+                ("allow_unnormalized", C.c_int32), ("record_every_boundary", C.c_int32),
+                ("det_reassociate", C.c_int32)]
 
 
 class RkConfig(C.Structure):
     _fields_ = [("max_epochs", C.c_int64), ("target_r_sq", C.c_double), ("seed", C.c_uint64),
-                ("sampling", C.c_int32), ("x_star", _f64p)]
+                ("sampling", C.c_int32), ("x_star", _f64p), ("det_reassociate", C.c_int32)]
 
 
 class TraceOut(C.Structure):
@@ -589,9 +590,11 @@ class _Trace:
 
 
 def _run_config(threads=1, gamma=1.0, epochs=100, target=0.0, variant=FULL_ROW, sampling=SLICE_SHUFFLE, seed=0,
-                snapshot_interval=1, x_star=None, precision=F64, allow_unnormalized=0, record_every_boundary=0):
+                snapshot_interval=1, x_star=None, precision=F64, allow_unnormalized=0, record_every_boundary=0,
+                det_reassociate=0):
     return RunConfig(threads, gamma, epochs, target, variant, sampling, seed, snapshot_interval,
-                     _ptr(x_star, _f64p), precision, allow_unnormalized, int(record_every_boundary))
+                     _ptr(x_star, _f64p), precision, allow_unnormalized, int(record_every_boundary),
+                     int(det_reassociate))
 
 
 class System:
@@ -645,7 +648,8 @@ class System:
                                    consistent=bool(rep.consistent))
         return d
 
-    def rk_solve_multi(self, B, X0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, X_star=None):
+    def rk_solve_multi(self, B, X0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, X_star=None,
+                       reassociate=False):
         """Deterministic multi-RHS rk_solve (asyrk_system_rk_solve_multi): B (m x k); column j
         of the result is rk_solve(A, B[:, j]) with the same seed, bit for bit."""
         B = np.ascontiguousarray(B, dtype=np.float64)
@@ -654,7 +658,7 @@ class System:
         k = B.shape[1]
         x0 = _mat(X0, (self.n, k), np.float64, "X0") if X0 is not None else None
         xs = _mat(X_star, (self.n, k), np.float64, "X_star") if X_star is not None else None
-        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p), int(reassociate))
         tr = _Trace(0, max(max_epochs, 0) + 2, want_x=False)
         X = np.zeros((self.n, k))
         check(lib().asyrk_system_rk_solve_multi(self.h, _ptr(B, _f64p), k, _ptr(x0, _f64p), C.byref(c),
@@ -676,9 +680,10 @@ class System:
                                              out.ctypes.data_as(_i32p)))
         return out
 
-    def rk_solve(self, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):
+    def rk_solve(self, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None,
+                 reassociate=False):
         xs = _vec(x_star, self.n, "x_star") if x_star is not None else None
-        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+        c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p), int(reassociate))
         tr = _Trace(self.n, max(max_epochs, 0) + 2)
         x0a = _vec(x0, self.n, "x0") if x0 is not None else None
         check(lib().asyrk_system_rk_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out)))
@@ -987,9 +992,10 @@ def compute_stats(A: HostCsr, tol=1e-9, max_iters=200000):
     return _stats_result(o, theta)
 
 
-def rk_solve_host(A: HostCsr, b, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None):
+def rk_solve_host(A: HostCsr, b, x0=None, max_epochs=100, target=0.0, seed=0, sampling=RK_UNIFORM, x_star=None,
+                  reassociate=False):
     xs = np.ascontiguousarray(x_star, dtype=np.float64) if x_star is not None else None
-    c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p))
+    c = RkConfig(max_epochs, target, seed, sampling, _ptr(xs, _f64p), int(reassociate))
     tr = _Trace(A.n, max(max_epochs, 0) + 2)
     b = np.ascontiguousarray(b, dtype=np.float64)
     x0a = np.ascontiguousarray(x0, dtype=np.float64) if x0 is not None else None

@@ -54,6 +54,7 @@ asyrk_run_config to_c(const RunConfig& cfg, const DeviceOptions& dev) {
     c.precision = dev.precision;
     c.allow_unnormalized = dev.norm_proportional ? 1 : 0;
     c.record_every_boundary = dev.record_every_boundary ? 1 : 0;
+    c.det_reassociate = dev.det_reassociate ? 1 : 0;
     return c;
 }
 

@@ -72,6 +72,7 @@ struct DetArgs {
     // b from the records)
     int ncols;
     const double* b_cols;
+    int reassoc;                  // 1: warp-tree dot, reciprocal coefficient, fused update (tolerance mode)
 };
 void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
@@ -167,7 +168,7 @@ struct MrhsArgs {
     uint32_t max_len;             // longest row (> 32: the looped worker)
 };
 bool mrhs_supported_kl(long long kl);
-int mrhs_max_resident_warps(int kl);  // co-resident worker warps (the default worker) on the current device
+int mrhs_max_resident_warps(int kl, uint32_t max_len);  // co-resident worker warps of the worker used
 int mrhs_row_blocks(long long m);
 int mrhs_col_blocks(long long n);
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s);

@@ -119,13 +119,14 @@ __device__ __forceinline__ void mr_load(const MrhsArgs& a, long long i, int lane
     r.inv = (float)rec_inv(rf);
 }
 
-// K2b: one warp = one lock-free worker projecting R = 2 rows at a time for
-// all KL columns (the next 2 rows' records and B slices are prefetched while
-// the current ones gather / reduce / scatter; K2's structure).
-template <int KL>
-__global__ void __launch_bounds__(256, 3) mrhs_worker_kernel(MrhsArgs a) {
+// K2b, pipelined: one warp = one lock-free worker projecting R rows at a time
+// for all KL columns (the next R rows' records and B slices are prefetched
+// while the current ones gather / reduce / scatter; K2's structure). Pays off
+// on narrow shards (KL <= 16: the multi-GPU widths), where a row's X traffic
+// is small and the per-row latency chain bounds the one-row worker.
+template <int KL, int R>
+__global__ void __launch_bounds__(256, R >= 4 ? 2 : 3) mrhs_worker_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
-    constexpr int R = 2;
     const DevState* st = a.st;
     if (!st->go) return;
     const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
@@ -510,24 +511,34 @@ int mrhs_col_blocks(long long n) {
     return (int)(want < mr_sms() * 8 ? want : mr_sms() * 8);
 }
 
+// rows in flight per warp by shard width (measured, profiles/r02_cfg5_probe.txt)
+static int mrhs_default_rows(int kl) { return kl >= 32 ? 1 : 2; }
+
+// The worker kernel for a shard width: rows in flight per warp from
+// ASYRK_MRHS_ROWS (1, 2 or 4) or the default above; rows of more than 32
+// nonzeros always take the one-row worker. ASYRK_MRHS_NOSTREAM=1: plain
+// read-only loads for A / B; ASYRK_MRHS_MINB=5: the one-row worker at 5 blocks
+// (40 warps) per SM instead of 4 (A/B runs).
+template <int KL>
+static const void* mrhs_worker_fn(uint32_t max_len) {
+    static const int rows_env = getenv("ASYRK_MRHS_ROWS") ? atoi(getenv("ASYRK_MRHS_ROWS")) : 0;
+    static const bool nostream = getenv("ASYRK_MRHS_NOSTREAM") != nullptr;
+    static const int minb = getenv("ASYRK_MRHS_MINB") ? atoi(getenv("ASYRK_MRHS_MINB")) : 4;
+    const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
+    if (max_len <= 32 && rows == 2) return (const void*)mrhs_worker_kernel<KL, 2>;
+    if (max_len <= 32 && rows >= 4) return (const void*)mrhs_worker_kernel<KL, 4>;
+    if (minb >= 5)
+        return nostream ? (const void*)mrhs_worker_long_kernel<KL, false, 5>
+                        : (const void*)mrhs_worker_long_kernel<KL, true, 5>;
+    return nostream ? (const void*)mrhs_worker_long_kernel<KL, false, 4>
+                    : (const void*)mrhs_worker_long_kernel<KL, true, 4>;
+}
+
 template <int KL>
 static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
     const int blocks = (int)((a.W * 32 + 255) / 256);
-    // Default: one row at a time (57 registers: 4 blocks / 32 warps per SM), the
-    // faster of the two measured at config 5 (0.64 vs 0.88 ms per epoch at 4096
-    // warps, profiles/r02_cfg5_probe.txt). ASYRK_MRHS_ROWS2=1: 2 rows in flight
-    // with prefetched records (80 registers, 3 blocks per SM).
-    static const bool rows2 = getenv("ASYRK_MRHS_ROWS2") != nullptr;
-    // ASYRK_MRHS_NOSTREAM=1: plain read-only loads for A / B (A/B runs);
-    // ASYRK_MRHS_MINB=5: 5 blocks (40 warps) per SM instead of 4
-    static const bool nostream = getenv("ASYRK_MRHS_NOSTREAM") != nullptr;
-    static const int minb = getenv("ASYRK_MRHS_MINB") ? atoi(getenv("ASYRK_MRHS_MINB")) : 4;
-    if (a.max_len <= 32 && rows2)
-        mrhs_worker_kernel<KL><<<blocks, 256, 0, s>>>(a);
-    else if (minb >= 5)
-        (nostream ? mrhs_worker_long_kernel<KL, false, 5> : mrhs_worker_long_kernel<KL, true, 5>)<<<blocks, 256, 0, s>>>(a);
-    else
-        (nostream ? mrhs_worker_long_kernel<KL, false, 4> : mrhs_worker_long_kernel<KL, true, 4>)<<<blocks, 256, 0, s>>>(a);
+    void* args[] = {const_cast<MrhsArgs*>(&a)};
+    cudaLaunchKernel(mrhs_worker_fn<KL>(a.max_len), dim3(blocks), dim3(256), args, 0, s);
 }
 template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
@@ -550,12 +561,12 @@ static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
 bool mrhs_supported_kl(long long kl) { return kl >= 2 && kl <= 64 && (kl & (kl - 1)) == 0; }
 
 template <int KL>
-static void mrhs_occupancy(int& per_sm) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrhs_worker_long_kernel<KL, true, 4>, 256, 0);
+static void mrhs_occupancy(int& per_sm, uint32_t max_len) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrhs_worker_fn<KL>(max_len), 256, 0);
 }
-int mrhs_max_resident_warps(int kl) {
+int mrhs_max_resident_warps(int kl, uint32_t max_len) {
     int per_sm = 0;
-    MR_DISPATCH(kl, mrhs_occupancy, per_sm)
+    MR_DISPATCH(kl, mrhs_occupancy, per_sm, max_len)
     return per_sm * 8 * mr_sms();
 }
 void launch_mrhs_worker(const MrhsArgs& a, cudaStream_t s) { MR_DISPATCH(a.KL, mrhs_worker_launch, a, s) }

@@ -761,6 +761,7 @@ struct SolveSpec {
     bool det;               // deterministic sequence path
     int det_mode;           // SeqGen mode
     bool every_boundary;    // async: record every boundary (run config record_every_boundary)
+    bool reassoc;           // deterministic: det_reassociate (tolerance mode)
 };
 
 // ASYRK_TIMELINE=path (diagnostics): timing events around the first chunks'
@@ -1000,6 +1001,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
         da.poll_ns = poll_ns;
         da.max_len = s->max_len;
+        da.reassoc = sp.reassoc ? 1 : 0;
         if (!s->pstream) {
             CK(cudaStreamCreateWithFlags(&s->pstream, cudaStreamNonBlocking));
             for (int h = 0; h < 2; ++h) {
@@ -1304,6 +1306,7 @@ asyrk_status system_solve_impl(asyrk_system* s, const double* x0, const asyrk_ru
     sp.det = c->threads == 1;
     sp.det_mode = c->sampling == ASYRK_SLICE_SHUFFLE ? 2 : (c->sampling == ASYRK_NORM_PROPORTIONAL ? 1 : 0);
     sp.every_boundary = c->record_every_boundary != 0;
+    sp.reassoc = c->det_reassociate != 0;
     return run_solve(s, x0, sp, trace, instr);
 }
 
@@ -1326,6 +1329,7 @@ asyrk_status system_rk_impl(asyrk_system* s, const double* x0, const asyrk_rk_co
     sp.precision = P_F64;
     sp.det = true;
     sp.det_mode = c->sampling == ASYRK_RK_UNIFORM ? 0 : (c->sampling == ASYRK_RK_NORM_PROPORTIONAL ? 1 : 2);
+    sp.reassoc = c->det_reassociate != 0;
     return run_solve(s, x0, sp, trace, nullptr);
 }
 
@@ -1436,6 +1440,7 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     da.max_len = s->max_len;
     da.ncols = (int)k;
     da.b_cols = Bc;
+    da.reassoc = c->det_reassociate ? 1 : 0;
     bool stop = record(0);
     for (long long e = 1; e <= c->max_epochs && !stop; ++e) {
         int32_t* sq = s->seq_host[0];
@@ -2667,7 +2672,7 @@ asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const 
 asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out) {
     if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
-        *out = mrhs_max_resident_warps((int)h->kl);
+        *out = mrhs_max_resident_warps((int)h->kl, h->sys->max_len);
         return ASYRK_OK;
     });
 }

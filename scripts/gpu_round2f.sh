@@ -1,0 +1,11 @@
+#!/bin/bash
+set -u
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity2.py tests/test_gpu_mrhs.py tests/test_gpu_parity.py -q -x --timeout 600 > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/gputest.log
+: > gpurun_out/probe_cfg5.txt
+for R in 1 2 4; do
+  ASYRK_MRHS_ROWS=$R WARPS=2368,3552,4736 KLS=32,16,8 timeout 300 python scripts/probe_cfg5.py >> gpurun_out/probe_cfg5.txt 2>&1
+done
+timeout 600 python bench.py --workload cfg1 --steps 5 --warmup 3 > gpurun_out/cfg1.json 2> gpurun_out/cfg1.err; echo "cfg1 rc=$?"
+timeout 900 python bench.py --workload cfg5shards --steps 5 --warmup 3 > gpurun_out/cfg5shards.json 2> gpurun_out/cfg5shards.err; echo "shards rc=$?"
