@@ -326,6 +326,109 @@ __global__ void __launch_bounds__(256, MINB) mrhs_worker_long_kernel(MrhsArgs a)
     }
 }
 
+// K2b, batched (rows of at most 32 nonzeros): one row per warp at a time, its
+// record (value, column per lane) loaded in one round trip and the next row's
+// prefetched, then the row's X gathers issued in batches of U with no
+// dependent load in between — so a row costs ~2 L2 round trips instead of one
+// (column load -> X load) chain per batch of the looped worker.
+template <int KL, int U>
+__global__ void __launch_bounds__(256, 3) mrhs_worker_batched_kernel(MrhsArgs a) {
+    using G = MrGeom<KL>;
+    constexpr int T = (32 + G::S - 1) / G::S;  // slot iterations covering 32 nonzeros
+    const DevState* st = a.st;
+    if (!st->go) return;
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
+    if (span <= 0) return;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp >= a.W) return;
+    const int lane = threadIdx.x & 31;
+    const int slot = lane / G::GL, cl = lane % G::GL;
+    const long long m = a.L.m;
+    long long count, slice_lo = 0, slice_len = 1;
+    if (a.sampling == S_SLICE) {
+        slice_lo = warp * m / a.W;
+        slice_len = (warp + 1) * m / a.W - slice_lo;
+        count = span * slice_len;
+    } else {
+        const long long total = span * m;
+        count = total / a.W + (warp < total % a.W ? 1 : 0);
+    }
+    if (count <= 0) return;
+    float* __restrict__ X = a.X;
+    const float gamma = (float)a.gamma;
+    const long long nb = (count + 31) >> 5;
+    long long D0 = mr_draw(a, warp, epoch, lane, slice_lo, slice_len);
+    long long D1 = nb > 1 ? mr_draw(a, warp, epoch, 32 + lane, slice_lo, slice_len) : D0;
+    MrRow<G::VW> cur;
+    mr_load<KL>(a, __shfl_sync(FULL, D0, 0), lane, cur);
+    for (long long bi = 0; bi < nb; ++bi) {
+        const int nq = (int)min(32ll, count - bi * 32);
+        const int nq_next = bi + 1 < nb ? (int)min(32ll, count - (bi + 1) * 32) : 0;
+        for (int q = 0; q < nq; ++q) {
+            // ---- prefetch the next row (independent of X)
+            MrRow<G::VW> nxt;
+            const bool in_batch = q + 1 < nq;
+            const bool ok_nxt = in_batch || nq_next > 0;
+            if (ok_nxt) mr_load<KL>(a, __shfl_sync(FULL, in_batch ? D0 : D1, in_batch ? q + 1 : 0), lane, nxt);
+            // ---- a_i^T X: batches of U independent gathers
+            const int len = cur.len;
+            float acc[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
+#pragma unroll
+            for (int jb = 0; jb < T; jb += U) {
+                if (jb * G::S < len) {
+                    MrVec<G::VW> xv[U];
+                    float vv[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const int t = (jb + j) * G::S + slot;
+                        vv[j] = __shfl_sync(FULL, cur.v, t & 31);
+                        const int c = __shfl_sync(FULL, cur.c, t & 31);
+                        if (t < len) {
+                            xv[j] = ld_xv<G::VW>(X + (size_t)c * KL + G::VW * cl);
+                        } else {
+                            vv[j] = 0.f;
+#pragma unroll
+                            for (int u = 0; u < G::VW; ++u) xv[j].v[u] = 0.f;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j)
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(vv[j], xv[j].v[u], acc[u]);
+                }
+            }
+#pragma unroll
+            for (int o = G::GL; o < 32; o <<= 1)
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
+            // ---- X[t, :] -= gamma (a_i^T X - B_i) / ||a_i||^2 * a_it
+            float cf[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[u] - cur.b.v[u]) * cur.inv;
+#pragma unroll
+            for (int jt = 0; jt < T; ++jt) {
+                const int t = jt * G::S + slot;
+                if (jt * G::S < len) {
+                    const float v = __shfl_sync(FULL, cur.v, t & 31);
+                    const int c = __shfl_sync(FULL, cur.c, t & 31);
+                    if (t < len) {
+                        MrVec<G::VW> d;
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                        red_xv<G::VW>(X + (size_t)c * KL + G::VW * cl, d);
+                    }
+                }
+            }
+            if (ok_nxt) cur = nxt;
+        }
+        D0 = D1;
+        if (bi + 2 < nb) D1 = mr_draw(a, warp, epoch, (bi + 2) * 32 + lane, slice_lo, slice_len);
+    }
+}
+
 // R = A X - B (fp32 storage, fp64 r^2 block partials): warp per row, lanes
 // over the row's KL columns (VW floats each), S nonzeros side by side
 template <int KL>
@@ -525,6 +628,11 @@ static const void* mrhs_worker_fn(uint32_t max_len) {
     static const bool nostream = getenv("ASYRK_MRHS_NOSTREAM") != nullptr;
     static const int minb = getenv("ASYRK_MRHS_MINB") ? atoi(getenv("ASYRK_MRHS_MINB")) : 4;
     const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
+    static const int batched = getenv("ASYRK_MRHS_BATCH") ? atoi(getenv("ASYRK_MRHS_BATCH")) : 0;
+    constexpr int T = (32 + MrGeom<KL>::S - 1) / MrGeom<KL>::S;
+    if (max_len <= 32 && batched > 0)
+        return batched >= 8 ? (const void*)mrhs_worker_batched_kernel<KL, (T < 8 ? T : 8)>
+                            : (const void*)mrhs_worker_batched_kernel<KL, (T < 4 ? T : 4)>;
     if (max_len <= 32 && rows == 2) return (const void*)mrhs_worker_kernel<KL, 2>;
     if (max_len <= 32 && rows >= 4) return (const void*)mrhs_worker_kernel<KL, 4>;
     if (minb >= 5)
