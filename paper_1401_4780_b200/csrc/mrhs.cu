@@ -429,6 +429,76 @@ __global__ void __launch_bounds__(256, 3) mrhs_worker_batched_kernel(MrhsArgs a)
     }
 }
 
+// K2b, row-parallel: a warp projects RPW = 32 / GL rows at once, each by its
+// own group of GL = KL / VW lanes (float4 / float2 per lane) that walks the
+// row's nonzeros serially — no cross-lane reduction, one shuffle per row (its
+// index), the nonzeros' value / column loads broadcast within the group, and
+// RPW rows of loads in flight per warp. On narrow shards (the multi-GPU
+// widths) this cuts the instructions per row several-fold against the
+// lane-per-nonzero layout, which spends most of them on the per-row reduction
+// and shuffles (profiles/r02_ncu_mrhs8.txt).
+template <int KL>
+__global__ void __launch_bounds__(256, 4) mrhs_worker_rows_kernel(MrhsArgs a) {
+    using G = MrGeom<KL>;
+    constexpr int RPW = 32 / G::GL;
+    const DevState* st = a.st;
+    if (!st->go) return;
+    const long long epoch = a.span0 > 0 ? a.epoch0 : st->epoch;
+    const long long span = a.span0 > 0 ? a.span0 : chunk_span(st);
+    if (span <= 0) return;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (warp >= a.W) return;
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / G::GL, cl = lane % G::GL;
+    const long long m = a.L.m;
+    long long count, slice_lo = 0, slice_len = 1;
+    if (a.sampling == S_SLICE) {
+        slice_lo = warp * m / a.W;
+        slice_len = (warp + 1) * m / a.W - slice_lo;
+        count = span * slice_len;
+    } else {
+        const long long total = span * m;
+        count = total / a.W + (warp < total % a.W ? 1 : 0);
+    }
+    float* __restrict__ X = a.X;
+    const float gamma = (float)a.gamma;
+    for (long long j0 = 0; j0 < count; j0 += 32) {
+        const long long D = mr_draw(a, warp, epoch, j0 + lane, slice_lo, slice_len);
+        const int nq = (int)min(32ll, count - j0);
+        for (int q0 = 0; q0 < nq; q0 += RPW) {
+            const long long i = __shfl_sync(FULL, D, q0 + grp);
+            if (q0 + grp >= nq) continue;
+            const RowRef r = row_ref(a.L, i);
+            const float* vals = rec_vals<float>(r);
+            const int32_t* cols = rec_cols<float>(r);
+            const int len = r.len;
+            float acc[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
+#pragma unroll 4
+            for (int t = 0; t < len; ++t) {
+                const float v = __ldg(vals + t);
+                const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
+            }
+            const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
+            const float inv = (float)rec_inv(r);
+            float cf[G::VW];
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[u] - bv.v[u]) * inv;
+#pragma unroll 4
+            for (int t = 0; t < len; ++t) {
+                const float v = __ldg(vals + t);
+                MrVec<G::VW> d;
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                red_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
+            }
+        }
+    }
+}
+
 // R = A X - B (fp32 storage, fp64 r^2 block partials): warp per row, lanes
 // over the row's KL columns (VW floats each), S nonzeros side by side
 template <int KL>
@@ -630,6 +700,8 @@ static const void* mrhs_worker_fn(uint32_t max_len) {
     const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
     static const int batched = getenv("ASYRK_MRHS_BATCH") ? atoi(getenv("ASYRK_MRHS_BATCH")) : 0;
     constexpr int T = (32 + MrGeom<KL>::S - 1) / MrGeom<KL>::S;
+    static const bool rowpar = getenv("ASYRK_MRHS_ROWPAR") != nullptr;
+    if (rowpar) return (const void*)mrhs_worker_rows_kernel<KL>;
     if (max_len <= 32 && batched > 0)
         return batched >= 8 ? (const void*)mrhs_worker_batched_kernel<KL, (T < 8 ? T : 8)>
                             : (const void*)mrhs_worker_batched_kernel<KL, (T < 4 ? T : 4)>;

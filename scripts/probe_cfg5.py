@@ -18,7 +18,7 @@ from paper_1401_4780_b200 import capi  # noqa: E402
 
 A, B, Xs = capi.generate_fixed_theta(500000, 250000, 20, seed=1005, k=64)
 B = B.astype(np.float32)
-variant = {k: os.environ[k] for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_NOSTREAM", "ASYRK_MRHS_MINB") if k in os.environ}
+variant = {k: os.environ[k] for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_NOSTREAM", "ASYRK_MRHS_MINB", "ASYRK_MRHS_BATCH", "ASYRK_MRHS_ROWPAR") if k in os.environ}
 kls = [int(v) for v in os.environ.get("KLS", "64").split(",")]
 samps = os.environ.get("SAMPLINGS", "slice_shuffle").split(",")
 for kl in kls:
