@@ -609,6 +609,105 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_cols_kernel(MrhsArgs a, int n
     }
 }
 
+// Row-parallel monitor passes for narrow shards (KL <= 16): a group of GL
+// lanes owns a row (pass 1) or a column (pass 2) and walks its entries
+// serially, as the row-parallel worker does; no cross-lane reduction per row.
+template <int KL>
+__global__ void __launch_bounds__(kMrThreads) mrhs_rows_par_kernel(MrhsArgs a) {
+    using G = MrGeom<KL>;
+    constexpr int RPW = 32 / G::GL;
+    if (a.st->stop) return;
+    __shared__ double red[kMrThreads / 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane / G::GL, cl = lane % G::GL;
+    const long long gw = (long long)blockIdx.x * (kMrThreads / 32) + wib;
+    const long long nw = (long long)gridDim.x * (kMrThreads / 32);
+    double mine = 0.0;
+    for (long long i = gw * RPW + grp; i < a.L.m; i += nw * RPW) {
+        const RowRef r = row_ref(a.L, i);
+        const float* vals = rec_vals<float>(r);
+        const int32_t* cols = rec_cols<float>(r);
+        float acc[G::VW];
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
+#pragma unroll 4
+        for (int t = 0; t < r.len; ++t) {
+            const float v = __ldg(vals + t);
+            const MrVec<G::VW> xv = ld_bv<G::VW>(a.X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
+        }
+        const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
+        float* rp = a.R + (size_t)i * KL + G::VW * cl;
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) {
+            const float rv = acc[u] - bv.v[u];
+            rp[u] = rv;
+            mine += (double)rv * rv;
+        }
+    }
+    mine = warp_sum(mine);
+    if (lane == 0) red[wib] = mine;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kMrThreads / 32; ++w) t += red[w];
+        a.part[blockIdx.x] = t;
+    }
+}
+
+template <int KL>
+__global__ void __launch_bounds__(kMrThreads) mrhs_cols_par_kernel(MrhsArgs a, int nb_rows) {
+    using G = MrGeom<KL>;
+    constexpr int RPW = 32 / G::GL;
+    if (a.st->stop) return;
+    __shared__ double red_g[kMrThreads / 32], red_d[kMrThreads / 32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane / G::GL, cl = lane % G::GL;
+    const long long gw = (long long)blockIdx.x * (kMrThreads / 32) + wib;
+    const long long nw = (long long)gridDim.x * (kMrThreads / 32);
+    double g2 = 0.0, d2 = 0.0;
+    for (long long j = gw * RPW + grp; j < a.L.n; j += nw * RPW) {
+        const long long e0 = __ldg(a.col_ptr + j), e1 = __ldg(a.col_ptr + j + 1);
+        double g[G::VW];
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) g[u] = 0.0;
+#pragma unroll 4
+        for (long long e = e0; e < e1; ++e) {
+            const double v = (double)__ldg(a.csc_val + e);
+            const MrVec<G::VW> rv = ld_bv<G::VW>(a.R + (size_t)__ldg(a.csc_row + e) * KL + G::VW * cl);
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) g[u] += v * rv.v[u];
+        }
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) g2 += g[u] * g[u];
+        if (a.Xstar) {
+            const MrVec<G::VW> xv = ld_bv<G::VW>(a.X + (size_t)j * KL + G::VW * cl);
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) {
+                const double d = (double)xv.v[u] - a.Xstar[(size_t)j * KL + G::VW * cl + u];
+                d2 += d * d;
+            }
+        }
+    }
+    g2 = warp_sum(g2);
+    d2 = warp_sum(d2);
+    if (lane == 0) {
+        red_g[wib] = g2;
+        red_d[wib] = d2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < kMrThreads / 32; ++w) {
+            s0 += red_g[w];
+            s1 += red_d[w];
+        }
+        a.part[nb_rows + blockIdx.x] = s0;
+        a.part[nb_rows + gridDim.x + blockIdx.x] = s1;
+    }
+}
+
 // partials -> norms[0..2] = {r_sq, g_sq, d_sq} of this shard (fixed order)
 __global__ void __launch_bounds__(kMrThreads) mrhs_reduce_kernel(MrhsArgs a, int nb_rows, int nb_cols) {
     if (a.st->stop) return;
@@ -684,7 +783,9 @@ int mrhs_col_blocks(long long n) {
     return (int)(want < mr_sms() * 8 ? want : mr_sms() * 8);
 }
 
-// rows in flight per warp by shard width (measured, profiles/r02_cfg5_probe.txt)
+// rows in flight per warp of the lane-per-nonzero workers (A/B; the defaults
+// below are the measured best: the one-row worker at 32 and 64 columns, the
+// row-parallel one at 16 and fewer, profiles/r02_cfg5_probe.txt)
 static int mrhs_default_rows(int kl) { return kl >= 32 ? 1 : 2; }
 
 // The worker kernel for a shard width: rows in flight per warp from
@@ -700,8 +801,10 @@ static const void* mrhs_worker_fn(uint32_t max_len) {
     const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
     static const int batched = getenv("ASYRK_MRHS_BATCH") ? atoi(getenv("ASYRK_MRHS_BATCH")) : 0;
     constexpr int T = (32 + MrGeom<KL>::S - 1) / MrGeom<KL>::S;
-    static const bool rowpar = getenv("ASYRK_MRHS_ROWPAR") != nullptr;
-    if (rowpar) return (const void*)mrhs_worker_rows_kernel<KL>;
+    // ASYRK_MRHS_ROWPAR=1 / =0 forces the row-parallel worker on / off
+    static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
+    if (rowpar == 1 || (rowpar < 0 && KL <= 16 && rows_env == 0 && batched == 0))
+        return (const void*)mrhs_worker_rows_kernel<KL>;
     if (max_len <= 32 && batched > 0)
         return batched >= 8 ? (const void*)mrhs_worker_batched_kernel<KL, (T < 8 ? T : 8)>
                             : (const void*)mrhs_worker_batched_kernel<KL, (T < 4 ? T : 4)>;
@@ -723,8 +826,15 @@ static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
 template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
     const int nbr = mrhs_row_blocks(a.L.m), nbc = mrhs_col_blocks(a.L.n);
-    mrhs_rows_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
-    mrhs_cols_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
+    // narrow shards: the row-parallel passes (ASYRK_MRHS_ROWPAR=0 keeps the lane-per-entry ones)
+    static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
+    if (rowpar == 1 || (rowpar < 0 && KL <= 16)) {
+        mrhs_rows_par_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
+        mrhs_cols_par_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
+    } else {
+        mrhs_rows_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
+        mrhs_cols_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
+    }
     mrhs_reduce_kernel<<<1, kMrThreads, 0, s>>>(a, nbr, nbc);
 }
 

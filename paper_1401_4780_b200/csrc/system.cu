@@ -997,9 +997,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.gamma = sp.gamma;
         da.full_row = sp.full_row ? 1 : 0;
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
-        // waiting warps back off between polls so they leave issue slots to the running events
-        static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
-        da.poll_ns = poll_ns;
+        // waiting warps back off between polls so they leave issue slots to the running
+        // events (bitwise mode: 32 ns measured best; tolerance mode: spinning, 13.3 vs 13.8 ms)
+        static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
+        da.poll_ns = poll_env >= 0 ? poll_env : (sp.reassoc ? 0 : 32);
         da.max_len = s->max_len;
         da.reassoc = sp.reassoc ? 1 : 0;
         if (!s->pstream) {
@@ -1374,13 +1375,14 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     double* Bc = dalloc<double>((size_t)(k * m));
     double* Xs = c->x_star ? dalloc<double>((size_t)(k * n)) : nullptr;
     double* colres = dalloc<double>((size_t)(3 * k));
+    double* evb = dalloc<double>((size_t)(k * m));  // the prepass's per-column b of each event
     struct Free {
         cudaStream_t st;
         std::vector<void*> p;
         ~Free() {
             for (void* q : p) pool_free(q, st);
         }
-    } fr{st, {Xc, Bc, Xs, colres}};
+    } fr{st, {Xc, Bc, Xs, colres, evb}};
     to_cols(B, m);
     CK(cudaMemcpyAsync(Bc, tmp.data(), (size_t)(k * m) * 8, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
@@ -1435,8 +1437,8 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     da.gamma = 1.0;
     da.full_row = 1;
     da.x_in_smem = (det_fits_smem(n) && s->max_len <= 128) ? 1 : 0;
-    static const int poll_ns = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : 32;
-    da.poll_ns = poll_ns;
+    static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
+    da.poll_ns = poll_env >= 0 ? poll_env : (c->det_reassociate ? 0 : 32);
     da.max_len = s->max_len;
     da.ncols = (int)k;
     da.b_cols = Bc;
@@ -1452,7 +1454,7 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
         da.need = s->need[0];
         da.ev_col = s->prep[0].keys;
         da.ev_val = s->prep[0].ev_val;
-        da.ev_b = s->prep[0].ev_b;
+        da.ev_b = evb;
         da.ev_nn = s->prep[0].ev_nn;
         da.ev_rcp = s->prep[0].ev_rcp;
         long long pairs = m * (long long)s->uniform_len;

@@ -24,7 +24,8 @@ samps = os.environ.get("SAMPLINGS", "slice_shuffle").split(",")
 for kl in kls:
     S = capi.MultiRHS(A, B, 0, kl)
     bbk = float((B[:, :kl].astype(np.float64) ** 2).sum())
-    for W in [int(v) for v in os.environ.get("WARPS", "4096").split(",")]:
+    for W in ([int(v) for v in os.environ["WARPS"].split(",")] if "WARPS" in os.environ
+              else [S.max_resident_warps()]):
         rx = max(capi.microbench_xside_mrhs(A.n, 20, kl, W, 64) for _ in range(2))
         for nm in samps:
             samp = capi.SLICE_SHUFFLE if nm == "slice_shuffle" else capi.WITH_REPLACEMENT
