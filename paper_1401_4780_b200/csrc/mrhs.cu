@@ -793,6 +793,16 @@ static int mrhs_default_rows(int kl) { return kl >= 32 ? 1 : 2; }
 // nonzeros always take the one-row worker. ASYRK_MRHS_NOSTREAM=1: plain
 // read-only loads for A / B; ASYRK_MRHS_MINB=5: the one-row worker at 5 blocks
 // (40 warps) per SM instead of 4 (A/B runs).
+// The row-parallel worker (a lane group per row, RPW rows per warp) on 8- and
+// 16-column shards; ASYRK_MRHS_ROWPAR=1 / =0 forces it on / off (any width),
+// ASYRK_MRHS_ROWS / ASYRK_MRHS_BATCH select the lane-per-nonzero variants.
+template <int KL>
+static bool mrhs_use_rowpar() {
+    static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
+    static const bool other = getenv("ASYRK_MRHS_ROWS") || getenv("ASYRK_MRHS_BATCH");
+    return rowpar == 1 || (rowpar < 0 && !other && (KL == 8 || KL == 16));
+}
+
 template <int KL>
 static const void* mrhs_worker_fn(uint32_t max_len) {
     static const int rows_env = getenv("ASYRK_MRHS_ROWS") ? atoi(getenv("ASYRK_MRHS_ROWS")) : 0;
@@ -801,10 +811,7 @@ static const void* mrhs_worker_fn(uint32_t max_len) {
     const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
     static const int batched = getenv("ASYRK_MRHS_BATCH") ? atoi(getenv("ASYRK_MRHS_BATCH")) : 0;
     constexpr int T = (32 + MrGeom<KL>::S - 1) / MrGeom<KL>::S;
-    // ASYRK_MRHS_ROWPAR=1 / =0 forces the row-parallel worker on / off
-    static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
-    if (rowpar == 1 || (rowpar < 0 && KL <= 16 && rows_env == 0 && batched == 0))
-        return (const void*)mrhs_worker_rows_kernel<KL>;
+    if (mrhs_use_rowpar<KL>()) return (const void*)mrhs_worker_rows_kernel<KL>;
     if (max_len <= 32 && batched > 0)
         return batched >= 8 ? (const void*)mrhs_worker_batched_kernel<KL, (T < 8 ? T : 8)>
                             : (const void*)mrhs_worker_batched_kernel<KL, (T < 4 ? T : 4)>;
@@ -817,18 +824,22 @@ static const void* mrhs_worker_fn(uint32_t max_len) {
                     : (const void*)mrhs_worker_long_kernel<KL, true, 4>;
 }
 
+// a.W = concurrent workers (rows in flight), the reference's `threads`: one
+// per warp for the lane-per-nonzero workers, one per lane group (RPW per
+// warp) for the row-parallel worker, which then launches W / RPW warps
 template <int KL>
-static void mrhs_worker_launch(const MrhsArgs& a, cudaStream_t s) {
+static void mrhs_worker_launch(const MrhsArgs& a0, cudaStream_t s) {
+    MrhsArgs a = a0;
+    if (mrhs_use_rowpar<KL>()) a.W = (a.W + (32 / MrGeom<KL>::GL) - 1) / (32 / MrGeom<KL>::GL);
     const int blocks = (int)((a.W * 32 + 255) / 256);
-    void* args[] = {const_cast<MrhsArgs*>(&a)};
+    void* args[] = {&a};
     cudaLaunchKernel(mrhs_worker_fn<KL>(a.max_len), dim3(blocks), dim3(256), args, 0, s);
 }
 template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
     const int nbr = mrhs_row_blocks(a.L.m), nbc = mrhs_col_blocks(a.L.n);
     // narrow shards: the row-parallel passes (ASYRK_MRHS_ROWPAR=0 keeps the lane-per-entry ones)
-    static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
-    if (rowpar == 1 || (rowpar < 0 && KL <= 16)) {
+    if (mrhs_use_rowpar<KL>()) {
         mrhs_rows_par_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
         mrhs_cols_par_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
     } else {
@@ -853,6 +864,7 @@ bool mrhs_supported_kl(long long kl) { return kl >= 2 && kl <= 64 && (kl & (kl -
 template <int KL>
 static void mrhs_occupancy(int& per_sm, uint32_t max_len) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mrhs_worker_fn<KL>(max_len), 256, 0);
+    if (mrhs_use_rowpar<KL>()) per_sm *= 32 / MrGeom<KL>::GL;  // workers, not warps
 }
 int mrhs_max_resident_warps(int kl, uint32_t max_len) {
     int per_sm = 0;
