@@ -11,7 +11,7 @@ timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/bench.json 2> gpu
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/ref.json 2> gpurun_out/ref.err; echo "ref rc=$?"
 timeout 300 python scripts/probe_xside.py > gpurun_out/xside.txt 2>&1
 timeout 300 python scripts/probe_cfg5.py > gpurun_out/probe_cfg5.txt 2>&1
-ASYRK_MRHS_ROWS2=1 WARPS=3552,4096 timeout 300 python scripts/probe_cfg5.py >> gpurun_out/probe_cfg5.txt 2>&1
+KLS=32,16,8 timeout 300 python scripts/probe_cfg5.py >> gpurun_out/probe_cfg5.txt 2>&1
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cfg5"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
