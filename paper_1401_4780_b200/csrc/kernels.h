@@ -147,7 +147,8 @@ struct MrhsArgs {
     Layout L;                     // fp32 row records (b unused)
     float* X;                     // n x KL row-major
     const float* B;               // m x KL row-major
-    float* R;                     // m x KL residual scratch
+    float* R;                     // m x KL residual scratch (CSC monitor)
+    float* G;                     // n x KL: G = A^T R scattered by the rows pass (scatter monitor), or nullptr
     const double* Xstar;          // n x KL or nullptr
     const long long* col_ptr;     // plain CSC for G = A^T R
     const int32_t* csc_row;

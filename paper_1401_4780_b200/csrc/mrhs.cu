@@ -531,14 +531,29 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_rows_kernel(MrhsArgs a) {
         for (int o = G::GL; o < 32; o <<= 1)
 #pragma unroll
             for (int u = 0; u < G::VW; ++u) acc[u] += __shfl_xor_sync(FULL, acc[u], o);
-        if (slot == 0) {
-            const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
-            float* rp = a.R + (size_t)i * KL + G::VW * cl;
+        const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
+        float rv[G::VW];
 #pragma unroll
-            for (int u = 0; u < G::VW; ++u) {
-                const float rv = acc[u] - bv.v[u];
-                rp[u] = rv;
-                mine += (double)rv * rv;
+        for (int u = 0; u < G::VW; ++u) rv[u] = acc[u] - bv.v[u];
+        if (slot == 0) {
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) mine += (double)rv[u] * rv[u];
+            if (!a.G) {
+                float* rp = a.R + (size_t)i * KL + G::VW * cl;
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) rp[u] = rv[u];
+            }
+        }
+        if (a.G) {  // G += a_i r_i^T (every slot lane holds r_i's columns after the butterfly)
+            for (int t0 = 0; t0 < r.len; t0 += G::S) {
+                const int t = t0 + slot;
+                if (t < r.len) {
+                    const float v = __ldg(vals + t);
+                    MrVec<G::VW> d;
+#pragma unroll
+                    for (int u = 0; u < G::VW; ++u) d.v[u] = v * rv[u];
+                    red_xv<G::VW>(a.G + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
+                }
             }
         }
     }
@@ -638,12 +653,25 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_rows_par_kernel(MrhsArgs a) {
             for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
         }
         const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
-        float* rp = a.R + (size_t)i * KL + G::VW * cl;
+        float rv[G::VW];
 #pragma unroll
         for (int u = 0; u < G::VW; ++u) {
-            const float rv = acc[u] - bv.v[u];
-            rp[u] = rv;
-            mine += (double)rv * rv;
+            rv[u] = acc[u] - bv.v[u];
+            mine += (double)rv[u] * rv[u];
+        }
+        if (a.G) {  // G += a_i r_i^T
+#pragma unroll 4
+            for (int t = 0; t < r.len; ++t) {
+                const float v = __ldg(vals + t);
+                MrVec<G::VW> d;
+#pragma unroll
+                for (int u = 0; u < G::VW; ++u) d.v[u] = v * rv[u];
+                red_xv<G::VW>(a.G + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
+            }
+        } else {
+            float* rp = a.R + (size_t)i * KL + G::VW * cl;
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) rp[u] = rv[u];
         }
     }
     mine = warp_sum(mine);
@@ -692,6 +720,42 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_cols_par_kernel(MrhsArgs a, i
     }
     g2 = warp_sum(g2);
     d2 = warp_sum(d2);
+    if (lane == 0) {
+        red_g[wib] = g2;
+        red_d[wib] = d2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int w = 0; w < kMrThreads / 32; ++w) {
+            s0 += red_g[w];
+            s1 += red_d[w];
+        }
+        a.part[nb_rows + blockIdx.x] = s0;
+        a.part[nb_rows + gridDim.x + blockIdx.x] = s1;
+    }
+}
+
+// Scatter monitor, pass 2: ||G||_F^2 of the G the rows pass accumulated
+// (G = A^T R by fp32 red.add, no CSC gather of R) and ||X - X*||_F^2, fp64
+// block partials in the columns slots of part
+__global__ void __launch_bounds__(kMrThreads) mrhs_gnorm_kernel(MrhsArgs a, int nb_rows) {
+    if (a.st->stop) return;
+    __shared__ double red_g[kMrThreads / 32], red_d[kMrThreads / 32];
+    const long long total = a.L.n * (long long)a.KL;
+    double g2 = 0.0, d2 = 0.0;
+    for (long long e = (long long)blockIdx.x * kMrThreads + threadIdx.x; e < total;
+         e += (long long)gridDim.x * kMrThreads) {
+        const double g = (double)__ldcg(a.G + e);
+        g2 += g * g;
+        if (a.Xstar) {
+            const double d = (double)__ldcg(a.X + e) - a.Xstar[e];
+            d2 += d * d;
+        }
+    }
+    g2 = warp_sum(g2);
+    d2 = warp_sum(d2);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     if (lane == 0) {
         red_g[wib] = g2;
         red_d[wib] = d2;
@@ -839,13 +903,17 @@ template <int KL>
 static void mrhs_monitor_launch(const MrhsArgs& a, cudaStream_t s) {
     const int nbr = mrhs_row_blocks(a.L.m), nbc = mrhs_col_blocks(a.L.n);
     // narrow shards: the row-parallel passes (ASYRK_MRHS_ROWPAR=0 keeps the lane-per-entry ones)
-    if (mrhs_use_rowpar<KL>()) {
+    if (a.G) cudaMemsetAsync(a.G, 0, (size_t)a.L.n * KL * sizeof(float), s);
+    if (mrhs_use_rowpar<KL>())
         mrhs_rows_par_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
-        mrhs_cols_par_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
-    } else {
+    else
         mrhs_rows_kernel<KL><<<nbr, kMrThreads, 0, s>>>(a);
+    if (a.G)
+        mrhs_gnorm_kernel<<<nbc, kMrThreads, 0, s>>>(a, nbr);
+    else if (mrhs_use_rowpar<KL>())
+        mrhs_cols_par_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
+    else
         mrhs_cols_kernel<KL><<<nbc, kMrThreads, 0, s>>>(a, nbr);
-    }
     mrhs_reduce_kernel<<<1, kMrThreads, 0, s>>>(a, nbr, nbc);
 }
 

@@ -2217,7 +2217,8 @@ struct asyrk_mrhs {
     int64_t k_total = 0, c0 = 0, c1 = 0, kl = 0;
     float* X = nullptr;           // n x kl
     float* B = nullptr;           // m x kl
-    float* R = nullptr;           // m x kl
+    float* R = nullptr;           // m x kl (CSC monitor, ASYRK_MRHS_CSC_MONITOR=1)
+    float* G = nullptr;           // n x kl (scatter monitor, default)
     double* Xstar = nullptr;      // n x kl (optional)
     double* part = nullptr;
     double* norms = nullptr;      // device {r_sq, g_sq, d_sq}
@@ -2248,6 +2249,7 @@ MrhsArgs mrhs_args(asyrk_mrhs* h) {
     a.X = h->X;
     a.B = h->B;
     a.R = h->R;
+    a.G = h->G;
     a.Xstar = h->have_xstar ? h->Xstar : nullptr;
     a.col_ptr = s->col_ptr;
     a.csc_row = s->csc_row;
@@ -2275,7 +2277,8 @@ void mrhs_free(asyrk_mrhs* h) {
     if (h->ev_commit) cudaEventDestroy(h->ev_commit);
     if (h->sys) {
         cudaStream_t st = h->sys->stream;
-        for (void* p : {(void*)h->X, (void*)h->B, (void*)h->R, (void*)h->Xstar, (void*)h->part, (void*)h->norms})
+        for (void* p : {(void*)h->X, (void*)h->B, (void*)h->R, (void*)h->G, (void*)h->Xstar, (void*)h->part,
+                        (void*)h->norms})
             pool_free(p, st);
         free_all(h->sys);
         delete h->sys;
@@ -2301,7 +2304,13 @@ asyrk_status mrhs_create_impl(const asyrk_csr_view* A, const float* B, int64_t k
     h->kl = kl;
     h->X = dalloc<float>((size_t)s->n * kl);
     h->B = dalloc<float>((size_t)s->m * kl);
-    h->R = dalloc<float>((size_t)s->m * kl);
+    // the monitor's G = A^T R: scattered by the rows pass into G (n x kl, default:
+    // one pass over A, no CSC gather of R), or gathered from R over the CSC
+    static const bool csc_monitor = getenv("ASYRK_MRHS_CSC_MONITOR") != nullptr;
+    if (csc_monitor)
+        h->R = dalloc<float>((size_t)s->m * kl);
+    else
+        h->G = dalloc<float>((size_t)s->n * kl);
     h->norms = dalloc<double>(4);
     h->part = dalloc<double>((size_t)mrhs_row_blocks(s->m) + 2 * (size_t)mrhs_col_blocks(s->n) + 8);
     // this shard's columns of B, contiguous (host gather, then staged upload)
