@@ -549,7 +549,9 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=0):
         dist.all_reduce(t)
         col_proj = float(t.item())
     # the multi-RHS x-side ceiling at this shard's width and warp count (no A / B stream)
-    rx5 = max(capi.microbench_xside_mrhs(CFG5["n"], CFG5["theta"], c1 - c0, W, 64) for _ in range(2))
+    kl = c1 - c0
+    warps = W // (128 // kl) if kl in (8, 16) else W  # the row-parallel worker runs 128/kl workers per warp
+    rx5 = max(capi.microbench_xside_mrhs(CFG5["n"], CFG5["theta"], kl, warps, 64) for _ in range(2))
     sh.close()
     comm.close()
     if rank != 0:

@@ -18,7 +18,7 @@ from paper_1401_4780_b200 import capi  # noqa: E402
 
 A, B, Xs = capi.generate_fixed_theta(500000, 250000, 20, seed=1005, k=64)
 B = B.astype(np.float32)
-variant = {k: os.environ[k] for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_NOSTREAM", "ASYRK_MRHS_MINB", "ASYRK_MRHS_BATCH", "ASYRK_MRHS_ROWPAR") if k in os.environ}
+variant = {k: os.environ[k] for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_NOSTREAM", "ASYRK_MRHS_MINB", "ASYRK_MRHS_BATCH", "ASYRK_MRHS_ROWPAR", "ASYRK_MRHS_CSC_MONITOR") if k in os.environ}
 kls = [int(v) for v in os.environ.get("KLS", "64").split(",")]
 samps = os.environ.get("SAMPLINGS", "slice_shuffle").split(",")
 for kl in kls:
@@ -26,7 +26,9 @@ for kl in kls:
     bbk = float((B[:, :kl].astype(np.float64) ** 2).sum())
     for W in ([int(v) for v in os.environ["WARPS"].split(",")] if "WARPS" in os.environ
               else [S.max_resident_warps()]):
-        rx = max(capi.microbench_xside_mrhs(A.n, 20, kl, W, 64) for _ in range(2))
+        rowpar = kl in (8, 16) and not any(k in os.environ for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_BATCH")) \
+            and os.environ.get("ASYRK_MRHS_ROWPAR", "") != "0"
+        rx = max(capi.microbench_xside_mrhs(A.n, 20, kl, W // (128 // kl) if rowpar else W, 64) for _ in range(2))
         for nm in samps:
             samp = capi.SLICE_SHUFFLE if nm == "slice_shuffle" else capi.WITH_REPLACEMENT
             S.solve(threads=W, epochs=2, target=0.0, seed=1, sampling=samp, want_x=False)
