@@ -1,6 +1,6 @@
 // Minimal JSON for the trace contract (the reference uses nlohmann/json,
-// which is not vendored here): flat objects with sorted keys, shortest
-// round-trip doubles, and a small parser for Trace::from_jsonl.
+// which is not vendored here): flat objects with sorted keys, doubles as that
+// library prints them (grisu2.hpp), and a small parser for Trace::from_jsonl.
 #pragma once
 
 #include <charconv>
@@ -11,6 +11,8 @@
 #include <string>
 #include <variant>
 #include <vector>
+
+#include "grisu2.hpp"
 
 namespace asyrk::json {
 
@@ -66,11 +68,7 @@ inline void dump_double(double d, std::string& out) {
         out += "null";  // nlohmann's convention for non-finite
         return;
     }
-    char buf[64];
-    auto r = std::to_chars(buf, buf + sizeof(buf), d);
-    std::string s(buf, r.ptr);
-    if (s.find_first_of(".eE") == std::string::npos) s += ".0";
-    out += s;
+    grisu2::to_string(d, out);  // the reference serializer's digits and layout
 }
 
 inline void dump(const Value& v, std::string& out) {

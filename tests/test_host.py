@@ -244,3 +244,42 @@ def test_host_vectors_are_length_checked():
         capi.simulate(A, b, np.zeros(3), 1.0, 0, "fixed", 10, 1, "full_row")
     with pytest.raises(capi.AsyrkError, match="DimensionMismatch"):
         capi.MultiRHS(A, np.zeros((10, 4), np.float32), 0, 4)
+
+
+def test_trace_serializers_match_the_reference_bytes(tmp_path):
+    # Trace::to_jsonl / to_csv (host/trace.cpp, doubles through grisu2.hpp) vs the
+    # reference's (trace.cpp:33-112, nlohmann/json) on the same trace content:
+    # 40000 doubles over many magnitudes, integral values, powers of two,
+    # subnormals, negatives and the fixed / exponent layout boundaries
+    import subprocess
+
+    import oracle
+
+    R = oracle.REF
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(11)
+    vals = [rng.standard_normal(8000) * 10.0 ** rng.integers(-30, 30, 8000),
+            rng.random(8000), np.exp(rng.uniform(-700, 700, 8000)),
+            np.ldexp(1.0, rng.integers(-1070, 1020, 4000)).astype(float),
+            np.round(rng.uniform(-1e6, 1e6, 4000)), rng.uniform(0, 1, 4000) * 1e-310,
+            np.array([1e-4, 1e-5, 9.999e-5, 1e15, 1e16, 123456789012345.0, 1234567890123456.0, 0.1, 1.0, 2.0,
+                      5e-324, 1.7976931348623157e308, 2.2250738585072014e-308, 0.0, -0.0, 3.0, 100.0])]
+    v = np.concatenate(vals)
+    v = v[np.isfinite(v)]
+    src = tmp_path / "v.bin"
+    v.tofile(src)
+    exe = str(tmp_path / "trace_dump")
+    lib = os.path.join(ROOT, "paper_1401_4780_b200")
+    subprocess.run(["g++", "-std=gnu++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "trace_dump.cpp"), "-o", exe, "-L", lib, "-lasyrk_b200",
+                    f"-Wl,-rpath,{lib}"], check=True, capture_output=True)
+    subprocess.run([exe, str(src), str(tmp_path / "t.jsonl"), str(tmp_path / "t.csv")], check=True)
+    ours_j = (tmp_path / "t.jsonl").read_text()
+    ours_c = (tmp_path / "t.csv").read_text()
+    ref_j, ref_c = R.trace_roundtrip(ours_j)
+    if ours_j != ref_j:  # name the first differing number
+        for a, b in zip(ours_j.split(","), ref_j.split(",")):
+            assert a == b
+    assert ours_j == ref_j
+    assert ours_c == ref_c
