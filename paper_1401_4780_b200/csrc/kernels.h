@@ -267,7 +267,7 @@ void launch_col_hist(const int32_t* sorted_cols, long long nnz, long long n, lon
 void launch_x_init(const double* x0, void* x, long long n, int precision, cudaStream_t s);
 void launch_x_export(const void* x, double* out, long long n, int precision, cudaStream_t s);
 void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target,
-                       cudaStream_t s);
+                       cudaStream_t s, int go = 0);
 // async audit (layout.cuh kAuditK checksums): part = the workers' per-warp
 // checksums [W][kAuditK], incr = their per-warp increment counts [W]; lhs =
 // kAuditK scratch doubles; writes max_k |lhs_k - sum_w part[w][k]| to out_max

@@ -116,7 +116,7 @@ void launch_x_export(const void* x, double* out, long long n, int precision, cud
         x_export_kernel<double><<<blocks, 256, 0, s>>>(static_cast<const double*>(x), out, n);
 }
 
-__global__ void state_init_kernel(DevState* st, long long epochs_cap, long long interval, double target) {
+__global__ void state_init_kernel(DevState* st, long long epochs_cap, long long interval, double target, int go) {
     st->epoch = 0;
     st->updates = 0;
     st->nrec = 0;
@@ -126,7 +126,7 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->stop = 0;
     st->status = 0;
     st->increments = 0;
-    st->go = 0;  // set by the initial record's commit
+    st->go = go;  // 0: set by the initial record's commit
     st->snap_valid[0] = st->snap_valid[1] = 0;
     st->stop_slot = -1;
     st->snap_ticket = st->mon_ticket = 0;
@@ -135,8 +135,8 @@ __global__ void state_init_kernel(DevState* st, long long epochs_cap, long long 
     st->snap_target = st->mon_slot = -1;
     st->t0_ns = globaltimer_ns();
 }
-void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s) {
-    state_init_kernel<<<1, 1, 0, s>>>(st, epochs_cap, interval, target);
+void launch_state_init(DevState* st, long long epochs_cap, long long interval, double target, cudaStream_t s, int go) {
+    state_init_kernel<<<1, 1, 0, s>>>(st, epochs_cap, interval, target, go);
 }
 
 // max_t |x_t - x0_t - shadow_t|  (finish_instrument, parallel.cpp:94-106)

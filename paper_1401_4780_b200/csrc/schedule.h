@@ -8,11 +8,11 @@
 // (two SpMVs over A), so here the coordinator decides WHICH boundaries to
 // evaluate from the records it already has: with the residual decaying
 // geometrically, the last two records give a rate and the number of snapshot
-// intervals left until r_sq <= target; the next evaluation is placed one
-// boundary before the predicted crossing (never more than max_gap intervals
-// ahead; the next boundary when the crossing is at most 2 away, while fewer
-// than two records exist, or when the residual did not drop), so an accurate
-// prediction costs two evaluations at the tail.
+// intervals left until r_sq <= target; the next evaluation is placed at the
+// last boundary at or before the predicted crossing (never more than max_gap
+// intervals ahead; the next boundary when the crossing is at most 1 away,
+// while fewer than two records exist, or when the residual did not drop), so
+// an accurate prediction costs one or two evaluations at the tail.
 // Near the stop every boundary is evaluated, so the stop is taken at the first
 // evaluated boundary that meets the target, and no epoch runs past it. With
 // target <= 0 (a fixed epoch budget) or record_every_boundary, every boundary
@@ -57,8 +57,8 @@ struct MonitorSchedule {
         if (!(r_last > target) || !(r_last < r_prev) || !(r_prev > 0.0) || !std::isfinite(r_last)) return 1;
         const double rate = (std::log(r_last) - std::log(r_prev)) / (double)(b_last - b_prev);  // < 0
         const double left = (std::log(target) - std::log(r_last)) / rate;                        // > 0
-        if (!(left > 2.0) || !std::isfinite(left)) return 1;
-        long long g = (long long)std::floor(left) - 1;  // one boundary before the predicted crossing
+        if (!(left > 1.0) || !std::isfinite(left)) return 1;
+        long long g = (long long)std::floor(left);  // the last boundary at or before the predicted crossing
         if (g < 1) g = 1;
         if (g > max_gap) g = max_gap;
         return g;

@@ -866,18 +866,46 @@ asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long l
 asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa, int E, int prec, long long max_chunks,
                            long long launches, asyrk_trace_out* trace, asyrk_instrument_out* instr) {
     cudaStream_t st = s->stream;
-    mon_wait(s, st);
     const bool xs = sp.x_star != nullptr;
     auto epoch_of = [&](long long b) { return std::min<long long>(b * sp.interval, sp.epochs); };
     cudaEvent_t ev_rec = s->ev_chunk[0];
     std::memset(s->mirror, 0, sizeof(HostMirror));
-    // boundary 0 (x0)
-    MonitorArgs m0 = monitor_args(s, false, 0, xs);
-    m0.mirror = s->mirror_dev;
-    launch_monitor(m0, prec, st);
-    launches += 2;
+    // Boundary 0 is x0, which the workers do not read back: its record is taken
+    // from the fp64 copy x0d on the monitor stream while the first workers run
+    // (x is fp64 for P_F64 / P_F32X64 systems), and only the monitors of later
+    // boundaries (on the worker stream) wait for it — and for the monitor
+    // structures create builds on its build stream. fp32 systems record x0 in-stream.
+    const bool side0 = prec != P_F32 && max_chunks > 0 && !instr;  // (an audit must see every increment)
+    if (side0) {
+        if (!s->mstream) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&s->mstream, cudaStreamNonBlocking, hi));
+            for (int q = 0; q < 2; ++q) {
+                CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&s->mon_ev[q], cudaEventDisableTiming));
+            }
+        }
+        launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st, /*go=*/1);
+        CK(cudaEventRecord(s->snap_ev[0], st));
+        CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[0], 0));
+        mon_wait(s, s->mstream);
+        MonitorArgs m0 = monitor_args(s, false, 0, xs);
+        m0.x = s->x0d;
+        m0.mirror = s->mirror_dev;
+        launch_monitor(m0, prec, s->mstream);
+        CK(cudaEventRecord(ev_rec, s->mstream));
+        CK(cudaEventRecord(s->mon_ev[0], s->mstream));
+    } else {
+        mon_wait(s, st);
+        MonitorArgs m0 = monitor_args(s, false, 0, xs);
+        m0.mirror = s->mirror_dev;
+        launch_monitor(m0, prec, st);
+        CK(cudaEventRecord(ev_rec, st));
+    }
+    launches += side0 ? 3 : 2;
     s->stats.monitor_launches++;
-    CK(cudaEventRecord(ev_rec, st));
+    bool waited0 = !side0;  // the worker stream is ordered after record 0
     MonitorSchedule sch;
     sch.reset(sp.target, sp.every_boundary);
     long long pending = 0;   // boundary whose record the host has not read yet (-1: none)
@@ -903,12 +931,24 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         if (pending >= 0) {
             CK(cudaEventSynchronize(ev_rec));
             const volatile HostMirror* hm = s->mirror;
-            if (hm->stop) break;  // the enqueued worker sees go = 0 and exits
+            if (hm->stop) {  // the enqueued worker sees go = 0 and exits
+                if (pending == 0 && side0) {
+                    // x0 met the target (or was non-finite) while the first workers
+                    // already ran: the solve returns x0 (epoch 0, no updates)
+                    CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
+                    launch_x_init(s->x0d, s->x, s->n, prec, st);
+                }
+                break;
+            }
             next_mon = sch.push(pending, hm->r_sq);
             pending = -1;
         }
         const long long b1 = b + 1;
         if (b1 >= next_mon || b1 == max_chunks) {
+            if (!waited0) {  // record 0 (monitor stream) precedes every later record
+                CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
+                waited0 = true;
+            }
             MonitorArgs ma = monitor_args(s, false, 1, xs);
             ma.set_epoch = epoch_of(b1);
             ma.mirror = s->mirror_dev;

@@ -126,11 +126,11 @@ def test_monitor_schedule_host_arithmetic():
     assert nx(1e-6, [3, 4], [1.0, 2.0]) == 5
     assert nx(1e-6, [3, 4], [1.0, 0.5], every=True) == 5
     assert nx(0.0, [3, 4], [1.0, 0.5]) == 5
-    # r halves per boundary: the crossing is 20 boundaries away -> one before it, capped at the max gap (12)
+    # r halves per boundary: the crossing is 20 boundaries away -> there, capped at the max gap (12)
     assert nx(2.0 ** -20, [3, 4], [2.0, 1.0]) == 4 + 12
-    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0], max_gap=30) == 4 + 19
-    assert nx(2.0 ** -5, [3, 4], [2.0, 1.0]) == 4 + 4
-    assert nx(2.0 ** -2, [3, 4], [2.0, 1.0]) == 4 + 1  # at most 2 away: the next one
+    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0], max_gap=30) == 4 + 20
+    assert nx(2.0 ** -5.5, [3, 4], [2.0, 1.0]) == 4 + 5  # the last boundary at or before the crossing
+    assert nx(2.0 ** -1, [3, 4], [2.0, 1.0]) == 4 + 1  # at most 1 away: the next one
     assert nx(0.9, [3, 4], [2.0, 1.0]) == 4 + 1
 
 
