@@ -24,6 +24,7 @@ same shape (seed + rank) — replicas, no data-path collective ("scaling":
 "weak"); timing is the max over ranks.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -337,6 +338,8 @@ def run_gpu(args):
     e2e_wall = 0.0
     e2e_proj = 0
     e2e_calls = []
+    gc.collect()
+    gc.disable()  # no interpreter collection pauses inside the timed host calls
     for k in range(-3, e2e_steps):  # 3 untimed warm-up calls
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -347,6 +350,7 @@ def run_gpu(args):
             e2e_wall += dt
             e2e_proj += int(r["updates_applied"][-1])
             e2e_calls.append(round(1e3 * dt, 2))
+    gc.enable()
     if dist:
         t = torch.tensor([e2e_wall], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

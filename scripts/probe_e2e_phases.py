@@ -12,7 +12,7 @@ from paper_1401_4780_b200 import capi  # noqa: E402
 A, b, xs = capi.generate_fixed_theta(200000, 100000, 30, seed=1002)
 bb = float(b @ b)
 W = 3552
-for k in range(4):
+for k in range(int(os.environ.get('CALLS', '4'))):
     t0 = time.perf_counter()
     r = capi.solve_parallel_host(A, b, threads=W, gamma=1.0, epochs=2000, target=1e-12 * bb,
                                  sampling=capi.SLICE_SHUFFLE, seed=2000 + k)
