@@ -5,10 +5,12 @@
 // (module.cpp:271-279). Statistics use the device compute_stats with the
 // dense spectrum from the device Jacobi SVD (exact_spectral, the reference
 // default) up to ASYRK_DENSE_DEVICE_CAP cells, power iteration beyond.
+#include <pybind11/numpy.h>
 #include <pybind11/pybind11.h>
 #include <pybind11/stl.h>
 
 #include <optional>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -26,10 +28,37 @@
 namespace py = pybind11;
 using namespace asyrk;
 
+// A 1-D host array argument (triplets, b): numpy arrays pass without a
+// per-element Python conversion (the reference's std::vector arguments,
+// module.cpp, convert element by element: ~2 s for config 2's 6M triplets);
+// lists and other sequences are converted by numpy (forcecast).
+template <class T>
+struct Arr {
+    py::array_t<T, py::array::c_style | py::array::forcecast> a;
+    std::size_t size() const { return static_cast<std::size_t>(a.size()); }
+    const T& operator[](std::size_t i) const { return a.data()[i]; }
+    const T* data() const { return a.data(); }
+    operator std::vector<T>() const { return std::vector<T>(a.data(), a.data() + a.size()); }
+    operator std::span<const T>() const { return std::span<const T>(a.data(), size()); }
+};
+
+namespace pybind11::detail {
+template <class T>
+struct type_caster<Arr<T>> {
+    PYBIND11_TYPE_CASTER(Arr<T>, const_name("numpy.ndarray"));
+    bool load(handle src, bool) {
+        auto arr = py::array_t<T, py::array::c_style | py::array::forcecast>::ensure(src);
+        if (!arr || arr.ndim() != 1) return false;
+        value.a = std::move(arr);
+        return true;
+    }
+};
+}  // namespace pybind11::detail
+
 namespace {
 
-CsrMatrix triplets_to_csr(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                          const std::vector<double>& vals) {
+CsrMatrix triplets_to_csr(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                          const Arr<double>& vals) {
     if (rows.size() != cols.size() || rows.size() != vals.size())
         fail(ErrorCode::DimensionMismatch, "triplet lists differ in length");
     std::vector<Triplet> t(rows.size());
@@ -74,8 +103,8 @@ UpdateVariant parse_variant(const std::string& s) {
     fail(ErrorCode::InvalidArgument, "variant: expected full-row|single");
 }
 
-py::dict solve_rk_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                     const std::vector<double>& vals, const std::vector<double>& b, index_t epochs, double target,
+py::dict solve_rk_py(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                     const Arr<double>& vals, const Arr<double>& b, index_t epochs, double target,
                      std::uint64_t seed, const std::string& sampling) {
     CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
     auto [A, bn] = normalize_rows(A0, b);
@@ -93,8 +122,8 @@ py::dict solve_rk_py(index_t m, index_t n, const std::vector<index_t>& rows, con
     return to_dict(tr);
 }
 
-py::dict solve_parallel_core(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                             const std::vector<double>& vals, const std::vector<double>& b, index_t threads,
+py::dict solve_parallel_core(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                             const Arr<double>& vals, const Arr<double>& b, index_t threads,
                              double gamma, index_t epochs, double target, std::uint64_t seed,
                              const std::string& variant, const std::string& sampling, index_t snapshot_interval,
                              int precision, bool instrumented, const std::vector<double>* x_star) {
@@ -151,8 +180,8 @@ SystemStats device_stats(const CsrMatrix& N) {
 }
 
 // module.cpp:113-135
-py::dict system_stats_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                         const std::vector<double>& vals) {
+py::dict system_stats_py(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                         const Arr<double>& vals) {
     CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
     std::vector<double> dummy(static_cast<std::size_t>(m), 0.0);
     auto [N, ignored] = normalize_rows(A, dummy);
@@ -179,8 +208,8 @@ py::dict system_stats_py(index_t m, index_t n, const std::vector<index_t>& rows,
 }
 
 // module.cpp:137-157
-py::dict step_params_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                        const std::vector<double>& vals, index_t tau) {
+py::dict step_params_py(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                        const Arr<double>& vals, index_t tau) {
     CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
     std::vector<double> dummy(static_cast<std::size_t>(m), 0.0);
     auto [N, ignored] = normalize_rows(A, dummy);
@@ -204,8 +233,8 @@ py::dict step_params_py(index_t m, index_t n, const std::vector<index_t>& rows, 
 
 // module.cpp:213-238: step parameters from the statistics, gamma overridden,
 // then the device bounded-delay simulation
-py::dict simulate_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                     const std::vector<double>& vals, const std::vector<double>& b, index_t iterations, index_t tau,
+py::dict simulate_py(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                     const Arr<double>& vals, const Arr<double>& b, index_t iterations, index_t tau,
                      double gamma, const std::string& delay, const std::string& variant, std::uint64_t seed) {
     CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
     auto [A, bn] = normalize_rows(A0, b);
@@ -236,8 +265,8 @@ py::dict simulate_py(index_t m, index_t n, const std::vector<index_t>& rows, con
 
 // module.cpp:227-246: triplets -> normalize_rows(A0, b) -> lsq_solve with the
 // derived (phi, zeta); the augmented solve runs on the device
-py::dict lsq_py(index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-                const std::vector<double>& vals, const std::vector<double>& b, index_t epochs, double target,
+py::dict lsq_py(index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+                const Arr<double>& vals, const Arr<double>& b, index_t epochs, double target,
                 std::uint64_t seed, std::optional<double> sigma_r, index_t threads, double gamma) {
     CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
     auto [A, bn] = normalize_rows(A0, b);
@@ -284,8 +313,8 @@ PYBIND11_MODULE(_asyrk, mod) {
             "bit-identical to the reference).");
     mod.def(
         "solve_parallel",
-        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-           const std::vector<double>& vals, const std::vector<double>& b, index_t threads, double gamma,
+        [](index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+           const Arr<double>& vals, const Arr<double>& b, index_t threads, double gamma,
            index_t epochs, double target, std::uint64_t seed, const std::string& variant) {
             // reference: slice_shuffle, snapshot_interval 1, always instrumented (module.cpp:182-191)
             return solve_parallel_core(m, n, rows, cols, vals, b, threads, gamma, epochs, target, seed, variant,
@@ -297,8 +326,8 @@ PYBIND11_MODULE(_asyrk, mod) {
         "Lock-free solve with `threads` warp-workers; returns the trace plus an instrument report.");
     mod.def(
         "solve_parallel_device",
-        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-           const std::vector<double>& vals, const std::vector<double>& b, index_t threads, double gamma,
+        [](index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+           const Arr<double>& vals, const Arr<double>& b, index_t threads, double gamma,
            index_t epochs, double target, std::uint64_t seed, const std::string& variant, const std::string& sampling,
            index_t snapshot_interval, int precision, bool instrument, std::optional<std::vector<double>> x_star) {
             return solve_parallel_core(m, n, rows, cols, vals, b, threads, gamma, epochs, target, seed, variant,
@@ -329,8 +358,8 @@ PYBIND11_MODULE(_asyrk, mod) {
             "(device rk_solve; threads > 1: async warp workers; sigma_r skips the dense SVD).");
     mod.def(
         "dense_spectrum",
-        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-           const std::vector<double>& vals) {
+        [](index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+           const Arr<double>& vals) {
             CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
             Spectrum sp;
             {
@@ -344,8 +373,8 @@ PYBIND11_MODULE(_asyrk, mod) {
         "Dense spectrum of the raw matrix (device one-sided Jacobi SVD; ref dense_spectrum).");
     mod.def(
         "lambda_max",
-        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-           const std::vector<double>& vals, double tol, index_t max_iters) {
+        [](index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+           const Arr<double>& vals, double tol, index_t max_iters) {
             CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
             auto [A, ignored] = normalize_rows(A0, {});
             py::gil_scoped_release nogil;
@@ -355,8 +384,8 @@ PYBIND11_MODULE(_asyrk, mod) {
         py::arg("max_iters") = 200000, "lambda_max(A^T A) of the row-normalized matrix (device power iteration).");
     mod.def(
         "residuals",
-        [](index_t m, index_t n, const std::vector<index_t>& rows, const std::vector<index_t>& cols,
-           const std::vector<double>& vals, const std::vector<double>& b, const std::vector<double>& x) {
+        [](index_t m, index_t n, const Arr<index_t>& rows, const Arr<index_t>& cols,
+           const Arr<double>& vals, const Arr<double>& b, const std::vector<double>& x) {
             CsrMatrix A = triplets_to_csr(m, n, rows, cols, vals);
             Residuals r = residuals(A, x, b);
             return py::dict(py::arg("r_sq") = r.r_sq, py::arg("grad_sq") = r.grad_sq);
