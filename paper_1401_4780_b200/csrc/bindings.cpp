@@ -32,6 +32,7 @@ using namespace asyrk;
 // per-element Python conversion (the reference's std::vector arguments,
 // module.cpp, convert element by element: ~2 s for config 2's 6M triplets);
 // lists and other sequences are converted by numpy (forcecast).
+namespace {
 template <class T>
 struct Arr {
     py::array_t<T, py::array::c_style | py::array::forcecast> a;
@@ -41,6 +42,7 @@ struct Arr {
     operator std::vector<T>() const { return std::vector<T>(a.data(), a.data() + a.size()); }
     operator std::span<const T>() const { return std::span<const T>(a.data(), size()); }
 };
+}  // namespace
 
 namespace pybind11::detail {
 template <class T>

@@ -91,6 +91,30 @@ CsrMatrix CsrMatrix::from_triplets(std::span<const Triplet> entries, index_t m, 
         if (t.row < 0 || t.row >= m || t.col < 0 || t.col >= n)
             fail(ErrorCode::IndexOutOfRange, "triplet (" + std::to_string(t.row) + "," + std::to_string(t.col) +
                                                  ") outside " + std::to_string(m) + "x" + std::to_string(n));
+    // already in (row, column) order with no repeats — triplets taken from a
+    // CSR, the common case: one pass, same result as the general path below
+    bool sorted = true;
+    for (std::size_t k = 1; k < entries.size() && sorted; ++k) {
+        const Triplet &p = entries[k - 1], &q = entries[k];
+        sorted = q.row > p.row || (q.row == p.row && q.col > p.col);
+    }
+    if (sorted) {
+        CsrMatrix A;
+        A.m_ = m;
+        A.n_ = n;
+        A.row_ptr_.assign(static_cast<std::size_t>(m) + 1, 0);
+        A.col_idx_.reserve(entries.size());
+        A.values_.reserve(entries.size());
+        for (const Triplet& t : entries)
+            if (t.value != 0.0) {
+                A.col_idx_.push_back(t.col);
+                A.values_.push_back(t.value);
+                ++A.row_ptr_[static_cast<std::size_t>(t.row) + 1];
+            }
+        for (index_t i = 0; i < m; ++i) A.row_ptr_[static_cast<std::size_t>(i) + 1] += A.row_ptr_[static_cast<std::size_t>(i)];
+        A.compute_norms();
+        return A;
+    }
     // counting sort by row, then sort each row's columns: O(nnz + rows * theta log theta)
     std::vector<index_t> start(static_cast<std::size_t>(m) + 1, 0);
     for (const Triplet& t : entries) ++start[static_cast<std::size_t>(t.row) + 1];
