@@ -173,9 +173,10 @@ __device__ void run_residuals(const SimArgs& a, const Rows& rw, const double* x,
                               int nthr, double& r_sq, double& g_sq) {
     for (long long i = tid; i < a.m; i += nthr) rt[i] = __dsub_rn(row_dot(rw, i, x), a.b[i]);
     run_sync<CTA>();
-    for (long long j = tid; j < a.n; j += nthr) {
-        const long long c0 = __ldg(a.C.grp_off + (j >> 5)) + (j & 31);
-        const int cl = __ldg(a.C.col_len + j);
+    for (long long q = tid; q < a.n; q += nthr) {  // positions of the sigma-sorted column copy
+        const long long j = a.C.col(q);
+        const long long c0 = __ldg(a.C.grp_off + (q >> 5)) + (q & 31);
+        const int cl = __ldg(a.C.col_len + q);
         const double* cv = static_cast<const double*>(a.C.val);
         double g = 0.0;
         for (int q = 0; q < cl; ++q) {

@@ -87,14 +87,19 @@ size_t det_prepare_temp_bytes(long long total);
 void launch_det_prepare(const DetArgs& a, const DetPrep& p, long long total, cudaStream_t s);
 
 // ---- K3: residual monitor r = Ax - b, g = A^T r, dist = ||x - x*||^2
-// Columns of A in SELL-32 order: the 32 columns of group g interleave their
-// entries, entry t of column 32g+l at grp_off[g] + 32t + l (rows ascending
-// within each column); slots past a column's length are padding.
+// Columns of A in SELL-32 order: the 32 positions of group g interleave their
+// entries, entry t of position 32g+l at grp_off[g] + 32t + l (rows ascending
+// within each column); slots past a column's length are padding. Position p
+// holds column perm[p]: the column copy is sigma-sorted (decreasing length,
+// so a group pads to almost nothing); perm == nullptr (the row copy) is the
+// identity. Consumers walk positions and write per-column results at perm[p].
 struct CscDev {
     const long long* grp_off;     // ceil(n/32)+1
-    const int32_t* col_len;       // n
+    const int32_t* col_len;       // n, by position
     const int32_t* row;           // padded
     const void* val;              // padded (V)
+    const int32_t* perm = nullptr;  // position -> column, or nullptr
+    __device__ __forceinline__ long long col(long long p) const { return perm ? (long long)__ldg(perm + p) : p; }
 };
 struct MonitorArgs {
     Layout L;
@@ -180,10 +185,16 @@ void launch_mrhs_commit(const MrhsArgs& a, long long set_epoch, cudaStream_t s);
 // ---- K4: power iteration building blocks (stats.cpp:15-50)
 void launch_spmv_rows(const CscDev& R, int precision, long long m, const double* v, double* out, cudaStream_t s);
 // SELL-32 columns from a column-sorted CSC: lengths + group sizes, then scatter
-void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s);
+// (perm: position -> column, or nullptr for the identity)
+void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s,
+                     const int32_t* perm = nullptr);
 void launch_sell_scatter(const long long* col_ptr, const int32_t* src_row, const void* src_val, const int32_t* col_len,
                          const long long* grp_off, long long n, int precision, int32_t* dst_row, void* dst_val,
-                         cudaStream_t s);
+                         cudaStream_t s, const int32_t* perm = nullptr);
+// perm = the columns by decreasing length (stable); len_tmp / len_sorted / iota_tmp: n-long scratch
+size_t sigma_sort_temp_bytes(long long n);
+void launch_sigma_sort(const long long* col_ptr, long long n, void* temp, size_t temp_bytes, int32_t* len_tmp,
+                       int32_t* len_sorted, int32_t* iota_tmp, int32_t* perm, cudaStream_t s);
 size_t scan_temp_bytes(long long count);
 void exclusive_scan(void* temp, size_t temp_bytes, const long long* in, long long* out, long long count, cudaStream_t s);
 void launch_spmv_cols(const CscDev& C, int precision, long long n, const double* r, double* out,

@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(kMonThreads) rows_kernel(CscDev R, long long m
     }
 }
 
-// Pass 2 / SpMV columns over SELL-32: lane l of group g owns column 32g + l.
+// Pass 2 / SpMV columns over SELL-32: lane l of group g owns position 32g + l
+// (column C.col(p) of the sigma-sorted copy; results land at the column).
 // out: g (or null), part: {g^2, dist^2} block partials (or null).
 template <class V, class X>
 __device__ __forceinline__ void cols_block(const CscDev& C, long long n, const double* __restrict__ r, double* out,
@@ -125,12 +126,12 @@ __device__ __forceinline__ void cols_block(const CscDev& C, long long n, const d
                                            const double* __restrict__ x_star) {
     __shared__ double red_g[kMonThreads / 32], red_d[kMonThreads / 32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long j = (long long)blockIdx.x * kMonThreads + threadIdx.x;
-    const long long grp = j >> 5;
+    const long long p = (long long)blockIdx.x * kMonThreads + threadIdx.x;  // position (sigma-sorted)
     double g2 = 0.0, d2 = 0.0;
-    if (j < n) {
-        const int len = __ldg(C.col_len + j);
-        const long long base = __ldg(C.grp_off + grp) + lane;
+    if (p < n) {
+        const long long j = C.col(p);
+        const int len = __ldg(C.col_len + p);
+        const long long base = __ldg(C.grp_off + (p >> 5)) + lane;
         const double g = sell_dot<8>(C.row, static_cast<const V*>(C.val), base, len, r);
         if (out) out[j] = g;
         g2 = g * g;

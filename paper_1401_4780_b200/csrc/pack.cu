@@ -247,36 +247,64 @@ void launch_iota_cols(const int32_t* col, long long nnz, int32_t* keys, int32_t*
     iota_cols_kernel<<<blocks, 256, 0, s>>>(col, nnz, keys, idx);
 }
 
-// ---- SELL-32 column layout (see CscDev): one warp per group of 32 columns
-__global__ void sell_len_kernel(const long long* __restrict__ col_ptr, long long n, int32_t* __restrict__ col_len,
-                                long long* __restrict__ grp_size) {
+// ---- SELL-32 column layout (see CscDev): one warp per group of 32 positions;
+// position p holds column perm[p] (perm == nullptr: column p)
+__global__ void sell_len_kernel(const long long* __restrict__ col_ptr, long long n, const int32_t* __restrict__ perm,
+                                int32_t* __restrict__ col_len, long long* __restrict__ grp_size) {
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const long long groups = (n + 31) / 32;
     if (g >= groups) return;
-    const long long j = g * 32 + lane;
-    const int len = j < n ? (int)(col_ptr[j + 1] - col_ptr[j]) : 0;
-    if (j < n) col_len[j] = len;
+    const long long p = g * 32 + lane;
+    const long long j = p < n ? (perm ? (long long)perm[p] : p) : 0;
+    const int len = p < n ? (int)(col_ptr[j + 1] - col_ptr[j]) : 0;
+    if (p < n) col_len[p] = len;
     int mx = len;
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(FULL, mx, o));
     if (lane == 0) grp_size[g] = 32ll * mx;
 }
-void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s) {
+void launch_sell_len(const long long* col_ptr, long long n, int32_t* col_len, long long* grp_size, cudaStream_t s,
+                     const int32_t* perm) {
     const long long groups = (n + 31) / 32;
-    sell_len_kernel<<<(unsigned)((groups * 32 + 255) / 256), 256, 0, s>>>(col_ptr, n, col_len, grp_size);
+    sell_len_kernel<<<(unsigned)((groups * 32 + 255) / 256), 256, 0, s>>>(col_ptr, n, perm, col_len, grp_size);
+}
+
+// sigma-sorting of the columns (SELL-C-sigma with sigma = n): positions in
+// order of decreasing length, ties in column order (a stable radix sort), so
+// the 32 columns of a group have nearly equal lengths and the padding of the
+// column copy (each group padded to its longest column) all but disappears
+__global__ void col_len_iota_kernel(const long long* __restrict__ col_ptr, long long n, int32_t* __restrict__ len,
+                                    int32_t* __restrict__ iota) {
+    for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+        len[j] = (int32_t)(col_ptr[j + 1] - col_ptr[j]);
+        iota[j] = (int32_t)j;
+    }
+}
+size_t sigma_sort_temp_bytes(long long n) {
+    size_t bytes = 0;
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                              (const int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+    return bytes;
+}
+void launch_sigma_sort(const long long* col_ptr, long long n, void* temp, size_t temp_bytes, int32_t* len_tmp,
+                       int32_t* len_sorted, int32_t* iota_tmp, int32_t* perm, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned blocks = (unsigned)std::min<long long>((n + 255) / 256, 148 * 8);
+    col_len_iota_kernel<<<blocks, 256, 0, s>>>(col_ptr, n, len_tmp, iota_tmp);
+    cub::DeviceRadixSort::SortPairsDescending(temp, temp_bytes, len_tmp, len_sorted, iota_tmp, perm, (int)n, 0, 32, s);
 }
 
 template <class V>
 __global__ void sell_scatter_kernel(const long long* __restrict__ ptr, const int32_t* __restrict__ src_idx,
                                     const double* __restrict__ src_val, const int32_t* __restrict__ len_arr,
-                                    const long long* __restrict__ grp_off, long long n, int32_t* __restrict__ dst_idx,
-                                    V* __restrict__ dst_val) {
+                                    const long long* __restrict__ grp_off, long long n, const int32_t* __restrict__ perm,
+                                    int32_t* __restrict__ dst_idx, V* __restrict__ dst_val) {
     const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const long long j = g * 32 + lane;
-    if (g >= (n + 31) / 32 || j >= n) return;
-    const long long src = ptr[j], dst = grp_off[g] + lane;
-    const int len = len_arr[j];
+    const long long p = g * 32 + lane;
+    if (g >= (n + 31) / 32 || p >= n) return;
+    const long long src = ptr[perm ? (long long)perm[p] : p], dst = grp_off[g] + lane;
+    const int len = len_arr[p];
     for (int t = 0; t < len; ++t) {
         dst_idx[dst + 32ll * t] = src_idx[src + t];
         dst_val[dst + 32ll * t] = (V)src_val[src + t];
@@ -285,15 +313,15 @@ __global__ void sell_scatter_kernel(const long long* __restrict__ ptr, const int
 // src_val is fp64 (the reference's values); dst_val gets the device precision
 void launch_sell_scatter(const long long* ptr, const int32_t* src_idx, const void* src_val, const int32_t* len_arr,
                          const long long* grp_off, long long n, int precision, int32_t* dst_idx, void* dst_val,
-                         cudaStream_t s) {
+                         cudaStream_t s, const int32_t* perm) {
     const long long groups = (n + 31) / 32;
     const unsigned blocks = (unsigned)((groups * 32 + 255) / 256);
     const double* sv = static_cast<const double*>(src_val);
     if (precision == P_F64)
-        sell_scatter_kernel<double><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, dst_idx,
+        sell_scatter_kernel<double><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, perm, dst_idx,
                                                            static_cast<double*>(dst_val));
     else
-        sell_scatter_kernel<float><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, dst_idx,
+        sell_scatter_kernel<float><<<blocks, 256, 0, s>>>(ptr, src_idx, sv, len_arr, grp_off, n, perm, dst_idx,
                                                           static_cast<float*>(dst_val));
 }
 

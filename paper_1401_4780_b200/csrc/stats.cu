@@ -33,20 +33,21 @@ __device__ __forceinline__ void max_bits(unsigned long long* dst, double v) {
     atomicMax(dst, (unsigned long long)__double_as_longlong(v));
 }
 
-// lane per column over SELL-32 columns
+// lane per column over SELL-32 columns (positions; results at the column)
 __global__ void __launch_bounds__(kStatThreads) stats_cols_kernel(CscDev C, long long n, const int32_t* __restrict__ row_len,
                                                                   double* __restrict__ col_sq, double* __restrict__ col_norm,
                                                                   StatsDev* out) {
-    const long long j = (long long)blockIdx.x * kStatThreads + threadIdx.x;
-    if (j >= n) return;
-    const int len = __ldg(C.col_len + j);
+    const long long p = (long long)blockIdx.x * kStatThreads + threadIdx.x;  // position
+    if (p >= n) return;
+    const long long j = C.col(p);
+    const int len = __ldg(C.col_len + p);
     if (len == 0) {
         atomicMin(&out->zero_col, j);
         col_sq[j] = 0.0;
         col_norm[j] = 0.0;
         return;
     }
-    const long long base = __ldg(C.grp_off + (j >> 5)) + (j & 31);
+    const long long base = __ldg(C.grp_off + (p >> 5)) + (p & 31);
     const double* cv = static_cast<const double*>(C.val);
     double c = 0.0;
     long long w = 0;
@@ -94,7 +95,7 @@ __global__ void stats_frob_kernel(const double* __restrict__ col_sq, long long n
     if (lane == 0) out->frob_sq = s;
 }
 
-// l_res: warp per column, per-warp hash table {key, acc, order} of `cap` slots
+// l_res: warp per column (walked by position: a maximum, order-free), per-warp hash table {key, acc, order} of `cap` slots
 // (power of two) in shared memory (tables == nullptr) or global scratch.
 __global__ void __launch_bounds__(kStatThreads) stats_lres_kernel(CscDev C, CscDev R, long long n, int cap,
                                                                   unsigned char* tables, StatsDev* out) {

@@ -63,6 +63,7 @@ struct asyrk_system {
     size_t rec_bytes = 0;
     long long* grp_off = nullptr;  // SELL-32 columns (CscDev)
     int32_t* col_len = nullptr;
+    int32_t* col_perm = nullptr;   // sigma-sorted column copy: position -> column
     int32_t* sell_row = nullptr;
     void* sell_val = nullptr;
     long long* rgrp_off = nullptr;  // SELL-32 rows (monitor pass 1)
@@ -144,7 +145,7 @@ struct asyrk_system {
         L.rec_bytes = rec_bytes;
         return L;
     }
-    CscDev csc() const { return CscDev{grp_off, col_len, sell_row, sell_val}; }
+    CscDev csc() const { return CscDev{grp_off, col_len, sell_row, sell_val, col_perm}; }
     CscDev rsell() const { return CscDev{rgrp_off, row_len, rsell_col, rsell_val}; }
     size_t xbytes() const { return precision == P_F32 ? 4 : 8; }
 };
@@ -240,6 +241,7 @@ void free_all(asyrk_system* s) {
     F(s->row_norm);
     F(s->grp_off);
     F(s->col_len);
+    F(s->col_perm);
     F(s->sell_row);
     F(s->sell_val);
     F(s->rgrp_off);
@@ -477,13 +479,17 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     int32_t* keys_s = dalloc<int32_t>((size_t)A->nnz);
     int32_t* idx_s = dalloc<int32_t>((size_t)A->nnz);
     int32_t* row_id = dalloc<int32_t>((size_t)A->nnz);
-    const size_t tb = csc_sort_temp_bytes(A->nnz);
+    const size_t tb = std::max(csc_sort_temp_bytes(A->nnz), sigma_sort_temp_bytes(A->n));
     unsigned char* temp = dalloc<unsigned char>(tb);
     long long* col_ptr = dalloc<long long>((size_t)A->n + 1);
     int32_t* csc_row = dalloc<int32_t>((size_t)A->nnz);
     double* csc_val = dalloc<double>((size_t)A->nnz);
     const long long groups = (A->n + 31) / 32;
     s->col_len = dalloc<int32_t>((size_t)A->n);
+    s->col_perm = dalloc<int32_t>((size_t)A->n);
+    int32_t* len_tmp = dalloc<int32_t>((size_t)A->n);
+    int32_t* len_sorted = dalloc<int32_t>((size_t)A->n);
+    int32_t* iota_tmp = dalloc<int32_t>((size_t)A->n);
     s->grp_off = dalloc<long long>((size_t)groups + 1);
     long long* grp_size = dalloc<long long>((size_t)groups + 1);
     const size_t stb = scan_temp_bytes(groups + 1);
@@ -495,6 +501,12 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     const size_t rstb = scan_temp_bytes(rgroups + 1);
     unsigned char* rstemp = dalloc<unsigned char>(rstb);
     s->b = dalloc<double>((size_t)A->m);
+    // the build's scratch (col_ptr / csc_row / csc_val are nulled when the system keeps them)
+    auto build_temps = [&] {
+        return std::vector<void*>{d_rp,     d_col,   d_val,    d_b,       keys,      idx,       keys_s,
+                                  idx_s,    row_id,  temp,     col_ptr,   csc_row,   csc_val,   grp_size,
+                                  stemp,    rgrp_size, rstemp, len_tmp,   len_sorted, iota_tmp};
+    };
 
     // host scan: row lengths, layout, row-SELL size (sell_len_kernel's 32 * max per group)
     struct Scan {
@@ -581,7 +593,8 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     csc_sort(temp, tb, keys, keys_s, idx, idx_s, A->nnz, end_bit, aux);
     launch_col_hist(keys_s, A->nnz, A->n, col_ptr, aux);
     CK(cudaMemsetAsync(grp_size, 0, ((size_t)groups + 1) * 8, aux));
-    launch_sell_len(col_ptr, A->n, s->col_len, grp_size, aux);
+    launch_sigma_sort(col_ptr, A->n, temp, tb, len_tmp, len_sorted, iota_tmp, s->col_perm, aux);
+    launch_sell_len(col_ptr, A->n, s->col_len, grp_size, aux, s->col_perm);
     exclusive_scan(stemp, stb, grp_size, s->grp_off, groups + 1, aux);
     CK(cudaMemcpyAsync(s->host_scalar, s->grp_off + groups, 8, cudaMemcpyDeviceToHost, aux));  // column-SELL size
     CK(cudaGetLastError());
@@ -599,7 +612,11 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     phase("upload");
 
     scan_thr.join();
-    if (sc.zero_row >= 0 || sc.too_large) cudaStreamSynchronize(aux);  // aux still reads buffers free_all releases
+    if (sc.zero_row >= 0 || sc.too_large) {
+        cudaStreamSynchronize(aux);  // aux still reads buffers free_all releases
+        cudaStreamSynchronize(st);
+        for (void* p : build_temps()) pool_free(p, st);
+    }
     if (sc.zero_row >= 0) {
         free_all(s.get());
         return fail(ASYRK_E_ZeroRow, "row " + std::to_string(sc.zero_row) + " has no nonzeros");
@@ -652,7 +669,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         launch_gather_csc(idx_s, row_id, d_val, A->nnz, P_F64, csc_row, csc_val, aux);
         CK(cudaMemsetAsync(s->sell_row, 0, (size_t)std::max<long long>(sell_total, 1) * 4, aux));
         launch_sell_scatter(col_ptr, csc_row, csc_val, s->col_len, s->grp_off, A->n, precision, s->sell_row,
-                            s->sell_val, aux);
+                            s->sell_val, aux, s->col_perm);
         phase("sell cols");
         CK(cudaGetLastError());
         if (keep_csc || precision == P_F64) {  // plain CSC: multi-RHS monitor, simulator's serial column walks
@@ -663,10 +680,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
             csc_row = nullptr;
             csc_val = nullptr;
         }
-        for (void* p : {(void*)d_rp, (void*)d_col, (void*)d_val, (void*)d_b, (void*)keys, (void*)idx, (void*)keys_s,
-                        (void*)idx_s, (void*)row_id, (void*)temp, (void*)col_ptr, (void*)csc_row, (void*)csc_val,
-                        (void*)grp_size, (void*)stemp, (void*)rgrp_size, (void*)rstemp})
-            pool_free(p, aux);
+        for (void* p : build_temps()) pool_free(p, aux);
         CK(cudaEventCreateWithFlags(&s->ev_mon_ready, cudaEventDisableTiming));
         CK(cudaEventRecord(s->ev_mon_ready, aux));
     }
