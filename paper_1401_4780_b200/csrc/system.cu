@@ -211,6 +211,66 @@ bool kit_put(asyrk_system* s) {
     return true;
 }
 
+// The build (aux) stream and the pinned scalar of create are recycled the
+// same way: a stream creation and a cudaHostAlloc / cudaFreeHost pair per
+// one-shot call cost ~0.2 ms of host time.
+std::vector<std::pair<int, cudaStream_t>> g_aux_streams;
+std::vector<void*> g_scalars;
+
+cudaStream_t aux_stream_take() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_kit_mu);
+        for (size_t i = 0; i < g_aux_streams.size(); ++i)
+            if (g_aux_streams[i].first == dev) {
+                cudaStream_t a = g_aux_streams[i].second;
+                g_aux_streams.erase(g_aux_streams.begin() + (long)i);
+                return a;
+            }
+    }
+    cudaStream_t a = nullptr;
+    CK(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+    return a;
+}
+
+void aux_stream_put(cudaStream_t a) {
+    if (!a) return;
+    cudaStreamSynchronize(a);
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) {
+        std::lock_guard<std::mutex> lk(g_kit_mu);
+        if (g_aux_streams.size() < kMaxKits) {
+            g_aux_streams.emplace_back(dev, a);
+            return;
+        }
+    }
+    cudaStreamDestroy(a);
+}
+
+void* scalar_take() {
+    {
+        std::lock_guard<std::mutex> lk(g_kit_mu);
+        if (!g_scalars.empty()) {
+            void* p = g_scalars.back();
+            g_scalars.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    CK(cudaHostAlloc(&p, 64, cudaHostAllocPortable));
+    return p;
+}
+
+void scalar_put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_kit_mu);
+    if (g_scalars.size() < 4 * kMaxKits) {
+        g_scalars.push_back(p);
+        return;
+    }
+    cudaFreeHost(p);
+}
+
 void destroy_det_streams(asyrk_system* s) {
     if (s->pstream) {
         cudaStreamSynchronize(s->pstream);
@@ -226,8 +286,7 @@ void destroy_det_streams(asyrk_system* s) {
 
 void free_all(asyrk_system* s) {
     if (s->bstream) {
-        cudaStreamSynchronize(s->bstream);
-        cudaStreamDestroy(s->bstream);
+        aux_stream_put(s->bstream);  // synchronizes it
         s->bstream = nullptr;
     }
     if (s->ev_mon_ready) {
@@ -282,7 +341,7 @@ void free_all(asyrk_system* s) {
     flag_release(s->host_flag);
     mirror_release(s->mirror);
     s->mirror = nullptr;
-    if (s->host_scalar) cudaFreeHost(s->host_scalar);
+    scalar_put(s->host_scalar);  // (its last reads were synchronous)
     s->host_scalar = nullptr;
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
@@ -430,7 +489,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         s->own_stream = true;
     }
     AllocStream alloc_on(s->stream);
-    CK(cudaHostAlloc(&s->host_scalar, 64, cudaHostAllocDefault));
+    s->host_scalar = scalar_take();
     // ASYRK_PROFILE_CREATE=1: synchronized phase times on stderr (diagnostics)
     static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
     auto t_prev = std::chrono::steady_clock::now();
@@ -565,15 +624,12 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         cudaStream_t& a;
         cudaEvent_t &e1, &e2;
         ~AuxGuard() {
-            if (a) {
-                cudaStreamSynchronize(a);
-                cudaStreamDestroy(a);
-            }
+            if (a) aux_stream_put(a);
             if (e1) cudaEventDestroy(e1);
             if (e2) cudaEventDestroy(e2);
         }
     } aux_guard{aux, ev_cols, ev_sorted};
-    CK(cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking));
+    aux = aux_stream_take();
     CK(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ev_sorted, cudaEventDisableTiming));
 
