@@ -604,6 +604,7 @@ class System:
         self.A = A
         self.m, self.n = A.m, A.n
         self.precision = precision
+        self._traces = {}
         self._b = _vec(b, A.m, "b") if b is not None else None
         h = C.c_void_p()
         check(lib().asyrk_system_create(C.byref(A.view()), _ptr(self._b, _f64p), precision,
@@ -636,7 +637,13 @@ class System:
         xs = _vec(xs, self.n, "x_star") if xs is not None else None
         c = _run_config(x_star=xs, **cfg)
         cap = max(c.epochs, 0) // max(c.snapshot_interval, 1) + 2
-        tr = _Trace(self.n, cap, want_x)
+        # trace buffers are reused across solves of this system (result() copies them out)
+        key = (cap, bool(want_x))
+        tr = self._traces.get(key) if want_x is False else None
+        if tr is None:
+            tr = _Trace(self.n, cap, want_x)
+            if not want_x:
+                self._traces[key] = tr
         x0a = _vec(x0, self.n, "x0") if x0 is not None else None
         rep = InstrumentOut()
         check(lib().asyrk_system_solve(self.h, _ptr(x0a, _f64p), C.byref(c), C.byref(tr.out),

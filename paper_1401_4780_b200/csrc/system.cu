@@ -103,7 +103,8 @@ struct asyrk_system {
     int* host_flag_dev = nullptr;
     HostMirror* mirror = nullptr;  // pinned mapped: latest record for the host-driven monitor schedule
     HostMirror* mirror_dev = nullptr;
-    void* host_scalar = nullptr;   // pinned scratch for small device -> host reads
+    void* host_scalar = nullptr;   // pinned scratch (kPinBytes): small device -> host reads, the final state + records
+    long long pin_recs = -1;       // records of the last solve already copied into host_scalar (-1: none)
     // the monitor's structures (row / column SELL, plain CSC) finish on bstream
     // after create returns; every consumer's stream waits on ev_mon_ready
     cudaStream_t bstream = nullptr;
@@ -133,6 +134,10 @@ struct asyrk_system {
     void* xs_base[2] = {nullptr, nullptr};
     cudaEvent_t snap_ev[2] = {nullptr, nullptr}, mon_ev[2] = {nullptr, nullptr};
     asyrk_solve_stats stats{};
+    // event timings of the last solve, read when the stats are asked for
+    // (~90 elapsed-time queries at config 2 cost ~0.12 ms of host time that
+    // the solve call itself would otherwise pay): worker launches timed
+    mutable long long stats_timed = -1;  // -1: nothing pending
 
     Layout layout() const {
         Layout L;
@@ -215,6 +220,10 @@ bool kit_put(asyrk_system* s) {
 // same way: a stream creation and a cudaHostAlloc / cudaFreeHost pair per
 // one-shot call cost ~0.2 ms of host time.
 std::vector<std::pair<int, cudaStream_t>> g_aux_streams;
+// pinned scratch per system: [0, 64) small reads; then the solve's DevState and
+// its records, copied behind the last kernel so the host's final read is one
+// stream synchronization (PinLayout)
+constexpr size_t kPinBytes = 64u << 10;
 std::vector<void*> g_scalars;
 
 cudaStream_t aux_stream_take() {
@@ -257,7 +266,7 @@ void* scalar_take() {
         }
     }
     void* p = nullptr;
-    CK(cudaHostAlloc(&p, 64, cudaHostAllocPortable));
+    CK(cudaHostAlloc(&p, kPinBytes, cudaHostAllocPortable));
     return p;
 }
 
@@ -756,11 +765,32 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     return ASYRK_OK;
 }
 
+// host_scalar layout: [0, 64) scratch, then DevState, then records
+constexpr size_t kPinStateOff = 64;
+constexpr size_t kPinRecOff = (kPinStateOff + sizeof(DevState) + 63) / 64 * 64;
+constexpr long long kPinRecCap = (long long)((kPinBytes - kPinRecOff) / sizeof(DevRecord));
+inline DevState* pin_state(asyrk_system* s) {
+    return reinterpret_cast<DevState*>(static_cast<unsigned char*>(s->host_scalar) + kPinStateOff);
+}
+inline DevRecord* pin_records(asyrk_system* s) {
+    return reinterpret_cast<DevRecord*>(static_cast<unsigned char*>(s->host_scalar) + kPinRecOff);
+}
+// enqueue the final state and the first `recs` records into the pinned scratch (stream order)
+void pin_final(asyrk_system* s, long long recs, cudaStream_t st) {
+    recs = std::min<long long>(std::min<long long>(recs, kPinRecCap), s->rec_cap);
+    CK(cudaMemcpyAsync(pin_state(s), s->st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+    if (recs > 0) CK(cudaMemcpyAsync(pin_records(s), s->recs, (size_t)recs * sizeof(DevRecord), cudaMemcpyDeviceToHost, st));
+    s->pin_recs = recs;
+}
+
 void write_trace(asyrk_system* s, const DevState& hs, asyrk_trace_out* trace, int precision) {
     if (!trace) return;
     const long long k = std::min<long long>(hs.nrec, s->rec_cap);
     std::vector<DevRecord> recs((size_t)k);
-    if (k) CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
+    if (k && k <= s->pin_recs)
+        std::memcpy(recs.data(), pin_records(s), (size_t)k * sizeof(DevRecord));
+    else if (k)
+        CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
     trace->count = hs.nrec;
     const long long w = std::min<long long>(k, trace->cap);
     for (long long i = 0; i < w; ++i) {
@@ -878,12 +908,11 @@ struct Timeline {
 };
 
 // Stats, trace and instrument report of a finished solve (the stream is idle).
-asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long long timed, long long launches,
-                          const std::vector<unsigned long long>& chunk_incr, asyrk_trace_out* trace,
-                          asyrk_instrument_out* instr) {
-    cudaStream_t st = s->stream;
-    DevState hs;
-    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+// the last async solve's event timings (its events stay untouched until the next solve)
+void resolve_stats(asyrk_system* s) {
+    if (s->stats_timed < 0) return;
+    const long long timed = s->stats_timed;
+    s->stats_timed = -1;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     s->stats.solve_ms = ms;
@@ -894,11 +923,41 @@ asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long l
         wms += w;
     }
     s->stats.worker_ms = wms;
+}
+
+// ASYRK_PROFILE_SOLVE=1: host timestamps of the async solve's phases on stderr (diagnostics)
+struct SolveClock {
+    bool on = getenv("ASYRK_PROFILE_SOLVE") != nullptr;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(const char* what) const {
+        if (on)
+            fprintf(stderr, "[solve] %-18s %8.1f us\n", what,
+                    std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
+thread_local SolveClock* g_solve_clock = nullptr;
+inline void solve_mark(const char* what) {
+    if (g_solve_clock) g_solve_clock->mark(what);
+}
+
+asyrk_status finish_solve(asyrk_system* s, const SolveSpec& sp, int prec, long long timed, long long launches,
+                          const std::vector<unsigned long long>& chunk_incr, asyrk_trace_out* trace,
+                          asyrk_instrument_out* instr) {
+    cudaStream_t st = s->stream;
+    DevState hs;
+    if (s->pin_recs >= 0)  // copied behind the last kernel (pin_final), the stream is idle
+        std::memcpy(&hs, pin_state(s), sizeof(DevState));
+    else
+        CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
+    solve_mark("state read");
+    s->stats_timed = timed;  // solve_ms / worker_ms: resolve_stats, on demand
     s->stats.kernel_launches = launches;
     s->stats.projections = hs.updates;
+    solve_mark("stats");
     if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
 
     write_trace(s, hs, trace, prec);
+    solve_mark("trace");
     if (instr) {
         instr->row_updates = hs.updates;
         unsigned long long inc = 0;
@@ -946,36 +1005,6 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     // boundaries (on the worker stream) wait for it — and for the monitor
     // structures create builds on its build stream. fp32 systems record x0 in-stream.
     const bool side0 = prec != P_F32 && max_chunks > 0 && !instr;  // (an audit must see every increment)
-    if (side0) {
-        if (!s->mstream) {
-            int lo = 0, hi = 0;
-            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            CK(cudaStreamCreateWithPriority(&s->mstream, cudaStreamNonBlocking, hi));
-            for (int q = 0; q < 2; ++q) {
-                CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
-                CK(cudaEventCreateWithFlags(&s->mon_ev[q], cudaEventDisableTiming));
-            }
-        }
-        launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st, /*go=*/1);
-        CK(cudaEventRecord(s->snap_ev[0], st));
-        CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[0], 0));
-        mon_wait(s, s->mstream);
-        MonitorArgs m0 = monitor_args(s, false, 0, xs);
-        m0.x = s->x0d;
-        m0.mirror = s->mirror_dev;
-        launch_monitor(m0, prec, s->mstream);
-        CK(cudaEventRecord(ev_rec, s->mstream));
-        CK(cudaEventRecord(s->mon_ev[0], s->mstream));
-    } else {
-        mon_wait(s, st);
-        MonitorArgs m0 = monitor_args(s, false, 0, xs);
-        m0.mirror = s->mirror_dev;
-        launch_monitor(m0, prec, st);
-        CK(cudaEventRecord(ev_rec, st));
-    }
-    launches += side0 ? 3 : 2;
-    s->stats.monitor_launches++;
-    bool waited0 = !side0;  // the worker stream is ordered after record 0
     MonitorSchedule sch;
     sch.reset(sp.target, sp.every_boundary);
     long long pending = 0;   // boundary whose record the host has not read yet (-1: none)
@@ -994,12 +1023,45 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         ++launches;
         s->stats.worker_launches++;
     };
-    if (max_chunks > 0) enqueue_worker(0);
+    if (side0) {
+        if (!s->mstream) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&s->mstream, cudaStreamNonBlocking, hi));
+            for (int q = 0; q < 2; ++q) {
+                CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&s->mon_ev[q], cudaEventDisableTiming));
+            }
+        }
+        launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st, /*go=*/1);
+        CK(cudaEventRecord(s->snap_ev[0], st));
+        enqueue_worker(0);  // first: the GPU starts on the workers while the host enqueues record 0
+        CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[0], 0));
+        mon_wait(s, s->mstream);
+        MonitorArgs m0 = monitor_args(s, false, 0, xs);
+        m0.x = s->x0d;
+        m0.mirror = s->mirror_dev;
+        launch_monitor(m0, prec, s->mstream);
+        CK(cudaEventRecord(ev_rec, s->mstream));
+        CK(cudaEventRecord(s->mon_ev[0], s->mstream));
+    } else {
+        mon_wait(s, st);
+        MonitorArgs m0 = monitor_args(s, false, 0, xs);
+        m0.mirror = s->mirror_dev;
+        launch_monitor(m0, prec, st);
+        CK(cudaEventRecord(ev_rec, st));
+        if (max_chunks > 0) enqueue_worker(0);
+    }
+    launches += side0 ? 3 : 2;
+    s->stats.monitor_launches++;
+    bool waited0 = !side0;  // the worker stream is ordered after record 0
+    solve_mark("first worker");
     for (long long b = 0; b < max_chunks; ++b) {
         // here the worker of chunk b (b -> b + 1) is enqueued; read the pending
         // record while it runs, then place the next evaluation
         if (pending >= 0) {
             CK(cudaEventSynchronize(ev_rec));
+            solve_mark("record read");
             const volatile HostMirror* hm = s->mirror;
             if (hm->stop) {  // the enqueued worker sees go = 0 and exits
                 if (pending == 0 && side0) {
@@ -1031,8 +1093,11 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         if (b1 < max_chunks) enqueue_worker(b1);
         CK(cudaGetLastError());
     }
+    solve_mark("loop done");
     CK(cudaEventRecord(s->ev_end, st));
+    pin_final(s, s->stats.monitor_launches, st);  // every record of this solve came from one monitor launch
     CK(cudaStreamSynchronize(st));
+    solve_mark("stream idle");
     CK(cudaGetLastError());
     return finish_solve(s, sp, prec, timed, launches, {}, trace, instr);
 }
@@ -1040,6 +1105,11 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
 asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
                        asyrk_instrument_out* instr) {
     cudaStream_t st = s->stream;
+    SolveClock clk;
+    g_solve_clock = clk.on ? &clk : nullptr;
+    struct ClockReset {
+        ~ClockReset() { g_solve_clock = nullptr; }
+    } clock_reset;
     AllocStream alloc_on(st);
     const int prec = sp.det ? P_F64 : sp.precision;
     if (sp.det && s->precision != P_F64)
@@ -1050,6 +1120,8 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     ensure_records(s, std::max<long long>(256, max_chunks + 2));
     ensure_events(s, max_chunks);
     s->stats = asyrk_solve_stats{};
+    s->stats_timed = -1;
+    s->pin_recs = -1;
 
     // x0, x_star
     if (x0) CK(cudaMemcpyAsync(s->x0d, x0, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
@@ -1075,6 +1147,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     }
     *s->host_flag = 0;
 
+    solve_mark("setup");
     CK(cudaEventRecord(s->ev_begin, st));
     launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st);
     long long launches = 1;
@@ -1512,6 +1585,8 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     ensure_events(s, 0);
     ensure_seq(s, (size_t)m);
     s->stats = asyrk_solve_stats{};
+    s->stats_timed = -1;
+    s->pin_recs = -1;
     std::memset(s->mirror, 0, sizeof(HostMirror));
     *s->host_flag = 0;
     CK(cudaEventRecord(s->ev_begin, st));
@@ -2201,8 +2276,11 @@ asyrk_status asyrk_system_rk_solve_multi(asyrk_system* sys, const double* B, int
 
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out) {
     if (!sys || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
-    *out = sys->stats;
-    return ASYRK_OK;
+    return guarded([&] {
+        resolve_stats(const_cast<asyrk_system*>(sys));
+        *out = sys->stats;
+        return ASYRK_OK;
+    });
 }
 
 asyrk_status asyrk_system_max_resident_warps(const asyrk_system* sys, int32_t precision, int32_t* out) {
@@ -2228,6 +2306,7 @@ asyrk_status asyrk_solve_parallel(const asyrk_csr_view* A, const double* b, cons
             if (s) return s;
             const auto t1 = std::chrono::steady_clock::now();
             s = system_solve_impl(g.s, x0, cfg, trace, instrument);
+            if (prof) resolve_stats(g.s);
             if (prof)
                 fprintf(stderr, "[one-shot] create %.3f ms solve %.3f ms (device %.3f ms)\n",
                         std::chrono::duration<double, std::milli>(t1 - t0).count(),
