@@ -55,6 +55,38 @@ void ThreadPool::run(const std::function<void(int)>& f) {
     done_cv_.wait(lk, [&] { return pending_ == 0; });
 }
 
+HelperThread::HelperThread() {
+    t_ = std::thread([this] {
+        for (;;) {
+            std::packaged_task<void()> task;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return !q_.empty(); });
+                task = std::move(q_.front());
+                q_.pop_front();
+            }
+            task();
+        }
+    });
+    t_.detach();  // process lifetime
+}
+
+HelperThread& HelperThread::get() {
+    static HelperThread* h = new HelperThread();
+    return *h;
+}
+
+std::future<void> HelperThread::submit(std::function<void()> f) {
+    std::packaged_task<void()> task(std::move(f));
+    std::future<void> fut = task.get_future();
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        q_.push_back(std::move(task));
+    }
+    cv_.notify_one();
+    return fut;
+}
+
 static int stager_threads() {
     if (const char* e = getenv("ASYRK_STAGER_THREADS")) return std::max(1, atoi(e));
     const unsigned hc = std::thread::hardware_concurrency();
@@ -184,7 +216,8 @@ cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
         configured.fetch_or(bit, std::memory_order_relaxed);
     }
     const cudaError_t e = no_pool() ? cudaMalloc(p, bytes ? bytes : 1) : cudaMallocAsync(p, bytes ? bytes : 1, s);
-    if (getenv("ASYRK_DEBUG_POOL")) fprintf(stderr, "[pool] alloc %p %zu\n", *p, bytes);
+    static const bool dbg = getenv("ASYRK_DEBUG_POOL") != nullptr;
+    if (dbg) fprintf(stderr, "[pool] alloc %p %zu\n", *p, bytes);
     return e;
 }
 

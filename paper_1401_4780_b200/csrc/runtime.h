@@ -10,8 +10,12 @@
 //    the release threshold lifted, so repeated solves reuse HBM instead of
 //    paying cudaMalloc/cudaFree.
 //  * a pinned, device-mapped flag slab for the coordinators' stop flags.
+//  * HelperThread — one persistent thread for host work that overlaps a
+//    create's uploads (the row-length scan), instead of a thread per call.
 #pragma once
 #include <condition_variable>
+#include <deque>
+#include <future>
 #include <cstddef>
 #include <cstdint>
 #include <functional>
@@ -39,6 +43,20 @@ class ThreadPool {
     long long gen_ = 0;
     int pending_ = 0;
     bool stop_ = false;
+};
+
+class HelperThread {
+  public:
+    static HelperThread& get();
+    // run f on the helper thread; the future reports completion (and rethrows)
+    std::future<void> submit(std::function<void()> f);
+
+  private:
+    HelperThread();
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::packaged_task<void()>> q_;
+    std::thread t_;
 };
 
 // host/stage_copy.cpp: AVX2 streaming-store copies (call only if stage_nt_supported())

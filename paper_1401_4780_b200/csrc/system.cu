@@ -480,6 +480,17 @@ void ensure_alias_dev(asyrk_system* s) {
     CK(cudaStreamSynchronize(s->stream));
 }
 
+// sub-allocations of one block: add() every array, allocate off bytes, then assign
+struct Carve {
+    size_t off = 0;
+    std::vector<std::pair<void**, size_t>> parts;
+    template <class T>
+    void add(T*& p, size_t count) {
+        parts.emplace_back(reinterpret_cast<void**>(&p), off);
+        off += (count * sizeof(T) + 255) / 256 * 256;
+    }
+};
+
 asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t precision, void* stream,
                          asyrk_system** out, bool keep_csc = false) {
     asyrk_status v = check_view(A);
@@ -537,44 +548,52 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     s->st = dalloc<DevState>(1);
     s->incr = dalloc<unsigned long long>(1);
     s->scratch = dalloc<double>(4096);
-    long long* d_rp = dalloc<long long>((size_t)A->m + 1);
-    int32_t* d_col = dalloc<int32_t>((size_t)A->nnz);
-    double* d_val = dalloc<double>((size_t)A->nnz);
-    double* d_b = dalloc<double>((size_t)A->m);
-    s->row_norm = dalloc<double>((size_t)A->m);
-    int32_t* keys = dalloc<int32_t>((size_t)A->nnz);
-    int32_t* idx = dalloc<int32_t>((size_t)A->nnz);
-    int32_t* keys_s = dalloc<int32_t>((size_t)A->nnz);
-    int32_t* idx_s = dalloc<int32_t>((size_t)A->nnz);
-    int32_t* row_id = dalloc<int32_t>((size_t)A->nnz);
+    const long long groups = (A->n + 31) / 32;
+    const long long rgroups = (A->m + 31) / 32;
     const size_t tb = std::max(csc_sort_temp_bytes(A->nnz), sigma_sort_temp_bytes(A->n));
-    unsigned char* temp = dalloc<unsigned char>(tb);
+    const size_t stb = scan_temp_bytes(groups + 1);
+    const size_t rstb = scan_temp_bytes(rgroups + 1);
+    // the build's scratch: one pool allocation carved into its arrays (a pool
+    // call per array measured ~6 us each on the one-shot path)
+    Carve cv;
+    long long *d_rp = nullptr, *grp_size = nullptr, *rgrp_size = nullptr;
+    int32_t *d_col = nullptr, *keys = nullptr, *idx = nullptr, *keys_s = nullptr, *idx_s = nullptr, *row_id = nullptr;
+    int32_t *len_tmp = nullptr, *len_sorted = nullptr, *iota_tmp = nullptr;
+    double *d_val = nullptr, *d_b = nullptr;
+    unsigned char *temp = nullptr, *stemp = nullptr, *rstemp = nullptr;
+    cv.add(d_rp, (size_t)A->m + 1);
+    cv.add(d_col, (size_t)A->nnz);
+    cv.add(d_val, (size_t)A->nnz);
+    cv.add(d_b, (size_t)A->m);
+    cv.add(keys, (size_t)A->nnz);
+    cv.add(idx, (size_t)A->nnz);
+    cv.add(keys_s, (size_t)A->nnz);
+    cv.add(idx_s, (size_t)A->nnz);
+    cv.add(row_id, (size_t)A->nnz);
+    cv.add(temp, tb);
+    cv.add(len_tmp, (size_t)A->n);
+    cv.add(len_sorted, (size_t)A->n);
+    cv.add(iota_tmp, (size_t)A->n);
+    cv.add(grp_size, (size_t)groups + 1);
+    cv.add(stemp, stb);
+    cv.add(rgrp_size, (size_t)rgroups + 1);
+    cv.add(rstemp, rstb);
+    unsigned char* slab = dalloc<unsigned char>(cv.off);
+    for (auto& pr : cv.parts) *pr.first = slab + pr.second;
+    s->row_norm = dalloc<double>((size_t)A->m);
+    // kept by fp64 / multi-RHS systems (plain CSC), so allocated on their own
     long long* col_ptr = dalloc<long long>((size_t)A->n + 1);
     int32_t* csc_row = dalloc<int32_t>((size_t)A->nnz);
     double* csc_val = dalloc<double>((size_t)A->nnz);
-    const long long groups = (A->n + 31) / 32;
     s->col_len = dalloc<int32_t>((size_t)A->n);
     s->col_perm = dalloc<int32_t>((size_t)A->n);
-    int32_t* len_tmp = dalloc<int32_t>((size_t)A->n);
-    int32_t* len_sorted = dalloc<int32_t>((size_t)A->n);
-    int32_t* iota_tmp = dalloc<int32_t>((size_t)A->n);
     s->grp_off = dalloc<long long>((size_t)groups + 1);
-    long long* grp_size = dalloc<long long>((size_t)groups + 1);
-    const size_t stb = scan_temp_bytes(groups + 1);
-    unsigned char* stemp = dalloc<unsigned char>(stb);
-    const long long rgroups = (A->m + 31) / 32;
     s->row_len = dalloc<int32_t>((size_t)A->m);
     s->rgrp_off = dalloc<long long>((size_t)rgroups + 1);
-    long long* rgrp_size = dalloc<long long>((size_t)rgroups + 1);
-    const size_t rstb = scan_temp_bytes(rgroups + 1);
-    unsigned char* rstemp = dalloc<unsigned char>(rstb);
     s->b = dalloc<double>((size_t)A->m);
+    phase("device allocs");
     // the build's scratch (col_ptr / csc_row / csc_val are nulled when the system keeps them)
-    auto build_temps = [&] {
-        return std::vector<void*>{d_rp,     d_col,   d_val,    d_b,       keys,      idx,       keys_s,
-                                  idx_s,    row_id,  temp,     col_ptr,   csc_row,   csc_val,   grp_size,
-                                  stemp,    rgrp_size, rstemp, len_tmp,   len_sorted, iota_tmp};
-    };
+    auto build_temps = [&] { return std::vector<void*>{slab, col_ptr, csc_row, csc_val}; };
 
     // host scan: row lengths, layout, row-SELL size (sell_len_kernel's 32 * max per group)
     struct Scan {
@@ -586,7 +605,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         std::vector<uint2> info;
     } sc;
     s->h_len.resize((size_t)A->m);
-    std::thread scan_thr([&] {
+    std::future<void> scan_done = HelperThread::get().submit([&] {
         s->h_norm.assign(A->row_norm, A->row_norm + A->m);
         for (int64_t g = 0; g < rgroups && sc.zero_row < 0; ++g) {
             uint32_t gmax = 0;
@@ -621,11 +640,12 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
         sc.rec_bytes = (size_t)off * 16u;
     });
     struct Join {
-        std::thread& t;
+        std::future<void>& f;
         ~Join() {
-            if (t.joinable()) t.join();
+            if (f.valid()) f.wait();  // the scan reads A and writes s: never outlive them
         }
-    } join_scan{scan_thr};
+    } join_scan{scan_done};
+    phase("scan thread");
 
     cudaStream_t aux = nullptr;
     cudaEvent_t ev_cols = nullptr, ev_sorted = nullptr;
@@ -676,7 +696,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     }
     phase("upload");
 
-    scan_thr.join();
+    scan_done.get();
     if (sc.zero_row >= 0 || sc.too_large) {
         cudaStreamSynchronize(aux);  // aux still reads buffers free_all releases
         cudaStreamSynchronize(st);
@@ -2403,6 +2423,7 @@ asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const
 // ===========================================================================
 struct asyrk_mrhs {
     asyrk_system* sys = nullptr;  // fp32 records + plain CSC of A
+    mutable long long stats_timed = -1;  // worker launches whose event times are still to be read
     int64_t k_total = 0, c0 = 0, c1 = 0, kl = 0;
     float* X = nullptr;           // n x kl
     float* B = nullptr;           // m x kl
@@ -2547,6 +2568,8 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     h->pending = -1;
     h->stop_seen = false;
     h->stats = asyrk_solve_stats{};
+    h->stats_timed = -1;
+    s->pin_recs = -1;
     ensure_records(s, std::max<long long>(256, h->max_chunks + 2));
     ensure_events(s, h->max_chunks);
     const int64_t kl = h->kl;
@@ -2634,27 +2657,21 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
     asyrk_system* s = h->sys;
     cudaStream_t st = s->stream;
     CK(cudaEventRecord(s->ev_end, st));
+    pin_final(s, h->stats.monitor_launches, st);  // state + records behind the last kernel
     CK(cudaStreamSynchronize(st));
     DevState hs;
-    CK(cudaMemcpy(&hs, s->st, sizeof(DevState), cudaMemcpyDeviceToHost));
-    float ms = 0.f;
-    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
-    h->stats.solve_ms = ms;
-    double wms = 0.0;
-    const long long timed = std::min<long long>(h->stats.worker_launches, (long long)s->ev_w.size() / 2);
-    for (long long t = 0; t < timed; ++t) {
-        float w = 0.f;
-        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
-        wms += w;
-    }
-    h->stats.worker_ms = wms;
+    std::memcpy(&hs, pin_state(s), sizeof(DevState));
+    h->stats_timed = std::min<long long>(h->stats.worker_launches, (long long)s->ev_w.size() / 2);  // mrhs_resolve_stats
     h->stats.projections = hs.updates;
     h->stats.warps = (int32_t)std::min<int64_t>(h->threads, INT32_MAX);
     if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
     if (trace) {
         const long long k = std::min<long long>(hs.nrec, s->rec_cap);
         std::vector<DevRecord> recs((size_t)k);
-        if (k) CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
+        if (k && k <= s->pin_recs)
+            std::memcpy(recs.data(), pin_records(s), (size_t)k * sizeof(DevRecord));
+        else if (k)
+            CK(cudaMemcpy(recs.data(), s->recs, (size_t)k * sizeof(DevRecord), cudaMemcpyDeviceToHost));
         trace->count = hs.nrec;
         const long long w = std::min<long long>(k, trace->cap);
         for (long long i = 0; i < w; ++i) {
@@ -2879,8 +2896,25 @@ asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out) {
 
 asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out) {
     if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
-    *out = h->stats;
-    return ASYRK_OK;
+    return guarded([&] {
+        asyrk_mrhs* hm = const_cast<asyrk_mrhs*>(h);
+        if (hm->stats_timed >= 0) {  // the last solve's event times (its events are untouched until the next)
+            asyrk_system* s = hm->sys;
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+            hm->stats.solve_ms = ms;
+            double wms = 0.0;
+            for (long long t = 0; t < hm->stats_timed; ++t) {
+                float w = 0.f;
+                CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+                wms += w;
+            }
+            hm->stats.worker_ms = wms;
+            hm->stats_timed = -1;
+        }
+        *out = h->stats;
+        return ASYRK_OK;
+    });
 }
 
 // ---- multi-GPU (NCCL)
