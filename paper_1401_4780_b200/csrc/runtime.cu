@@ -162,6 +162,42 @@ void Stager::upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
     });
 }
 
+void Stager::download(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    unsigned char* out = static_cast<unsigned char*>(dst);
+    const unsigned char* in = static_cast<const unsigned char*>(src);
+    const size_t chunks = (bytes + chunk_ - 1) / chunk_;
+    std::vector<int> slot_of(chunks);
+    auto issue = [&](size_t c) {  // DMA chunk c into the next slot
+        const int k = next_;
+        next_ = (next_ + 1) % kSlots;
+        cudaEventSynchronize(ev_[k]);  // the slot's previous transfer is done
+        const size_t o = c * chunk_, nb = std::min(chunk_, bytes - o);
+        if (cudaMemcpyAsync(slot_[k], in + o, nb, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaEventRecord(ev_[k], s) != cudaSuccess)
+            throw std::runtime_error("staged download failed");
+        slot_of[c] = k;
+    };
+    // chunk c + 1 crosses PCIe while chunk c is copied out of its slot
+    if (chunks) issue(0);
+    for (size_t c = 0; c < chunks; ++c) {
+        if (c + 1 < chunks) issue(c + 1);
+        const int k = slot_of[c];
+        if (cudaEventSynchronize(ev_[k]) != cudaSuccess) throw std::runtime_error("staged download failed");
+        const size_t o = c * chunk_, nb = std::min(chunk_, bytes - o);
+        const unsigned char* slot = slot_[k];
+        if (nb >= (1u << 20)) {
+            const int nt = pool_.size();
+            pool_.run([&](int t) {
+                const size_t a = nb * t / nt, b = nb * (t + 1) / nt;
+                if (b > a) std::memcpy(out + o + a, slot + a, b - a);
+            });
+        } else {
+            std::memcpy(out + o, slot, nb);
+        }
+    }
+}
+
 void Stager::upload_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s) {
     const bool nt = have_avx2();
     pipeline(count * 4, 4, s, reinterpret_cast<char*>(dst), [src, nt](unsigned char* out, size_t first, size_t n) {

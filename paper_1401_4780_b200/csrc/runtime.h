@@ -71,6 +71,9 @@ class Stager {
     void upload(void* dst, const void* src, size_t bytes, cudaStream_t s);
     // dst int32 (device) <- src int64 (host), count elements (values must fit)
     void upload_narrow(int32_t* dst, const int64_t* src, size_t count, cudaStream_t s);
+    // dst (host, pageable) <- src (device), bytes, after the work queued on s;
+    // returns when dst is filled (one pinned slot per chunk, threads copy out)
+    void download(void* dst, const void* src, size_t bytes, cudaStream_t s);
 
   private:
     Stager();

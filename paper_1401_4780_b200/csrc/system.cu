@@ -824,8 +824,7 @@ void write_trace(asyrk_system* s, const DevState& hs, asyrk_trace_out* trace, in
     }
     if (trace->final_x) {
         launch_x_export(s->x, s->xd, s->n, precision, s->stream);
-        CK(cudaMemcpyAsync(trace->final_x, s->xd, (size_t)s->n * 8, cudaMemcpyDeviceToHost, s->stream));
-        CK(cudaStreamSynchronize(s->stream));
+        Stager::get().download(trace->final_x, s->xd, (size_t)s->n * 8, s->stream);  // through the pinned slots
     }
 }
 
@@ -2684,7 +2683,7 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
             if (trace->updates_applied) trace->updates_applied[i] = r.updates;
         }
     }
-    if (X_out) CK(cudaMemcpy(X_out, h->X, (size_t)s->n * h->kl * sizeof(float), cudaMemcpyDeviceToHost));
+    if (X_out) Stager::get().download(X_out, h->X, (size_t)s->n * h->kl * sizeof(float), st);
     return ASYRK_OK;
 }
 

@@ -48,7 +48,11 @@ for rep, out, hdr in [
         ("xside.ncu-rep", "ncu_xside", "# ncu --set full -k regex:xside_kernel: python scripts/probe_xside.py ncu "
                                        "(2 rows in flight, then 1; f64, n=100000, theta=30, 3552 warps, 256 proj/warp)\n"),
         ("mrhs.ncu-rep", "ncu_mrhs", "# ncu --set full -k regex:mrhs_worker|mrhs_rows|mrhs_cols: python scripts/cfg5_once.py "
-                                     "(config 5, 64 columns on one GPU)\n")]:
+                                     "(config 5, 64 columns on one GPU)\n"),
+        ("det.ncu-rep", "ncu_det", "# ncu --set full -k regex:det_dataflow -s 2 -c 1: python scripts/ab_det.py "
+                                   "(config 1, bitwise mode: one launch = one epoch, 20 000 row events)\n"),
+        ("det_reassoc.ncu-rep", "ncu_det_reassoc", "# ncu --set full -k regex:det_dataflow -s 2 -c 1: python "
+                                                   "scripts/ab_det.py reassoc (config 1, tolerance mode: one launch = one epoch)\n")]:
     p = os.path.join(src, rep)
     if os.path.exists(p):
         open(os.path.join(dst, f"{tag}_{out}.txt"), "w").write(summary(p, hdr))
