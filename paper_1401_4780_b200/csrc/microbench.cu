@@ -125,6 +125,44 @@ __global__ void __launch_bounds__(256) xside_mrhs_kernel(float* X, uint32_t n, i
     }
 }
 
+// the row-parallel worker's pattern (mrhs.cu mrhs_worker_rows_kernel): a group
+// of GL lanes owns a row and walks its theta X rows serially, four gathers in
+// flight, then theta v4 reds — no cross-lane reduction
+template <int KL>
+__global__ void __launch_bounds__(256) xside_mrhs_rows_kernel(float* X, uint32_t n, int theta, long long per_row) {
+    constexpr int VW = 4, GL = KL / VW;
+    const uint32_t gid = (blockIdx.x * blockDim.x + threadIdx.x) / GL;
+    const int cl = threadIdx.x % GL;
+    uint32_t rng = hash32(gid * 0x9E3779B9u) | 1u;
+    for (long long q = 0; q < per_row; ++q) {
+        const uint32_t r0 = rng;
+        float acc[VW] = {0.f, 0.f, 0.f, 0.f};
+        for (int t = 0; t < theta; t += 4) {
+            uint32_t c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                rng = rng * 1664525u + 1013904223u;
+                c[j] = __umulhi(rng, n);
+            }
+            float4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                v[j] = t + j < theta ? __ldcg(reinterpret_cast<const float4*>(X + (size_t)c[j] * KL + VW * cl))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[0] += v[j].x, acc[1] += v[j].y, acc[2] += v[j].z, acc[3] += v[j].w;
+        }
+        rng = r0;  // the same theta rows again for the reds
+        for (int t = 0; t < theta; ++t) {
+            rng = rng * 1664525u + 1013904223u;
+            float* p = X + (size_t)__umulhi(rng, n) * KL + VW * cl;
+            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(1e-30f * acc[0]),
+                         "f"(1e-30f * acc[1]), "f"(1e-30f * acc[2]), "f"(1e-30f * acc[3])
+                         : "memory");
+        }
+    }
+}
+
 template <class X>
 static void xside_launch(int rows, int blocks, int threads, void* x, int64_t n, int theta, int64_t per_warp, int mode,
                          unsigned long long* sink, cudaStream_t s) {
@@ -231,9 +269,14 @@ extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, in
     cudaEventCreate(&e1);
     const int blocks = (warps * 32 + 255) / 256;
     float ms = 0.f;
+    const bool rows = mrhs_rowpar((int)kl);  // the worker's own shape at this width
     for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(e0);
-        switch (kl) {
+        if (rows && kl == 8)
+            xside_mrhs_rows_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else if (rows && kl == 16)
+            xside_mrhs_rows_kernel<16><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else switch (kl) {
             case 2: xside_mrhs_kernel<2><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
             case 4: xside_mrhs_kernel<4><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
             case 8: xside_mrhs_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
@@ -250,7 +293,9 @@ extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, in
     cudaEventDestroy(e1);
     cudaFree(base);
     if (err != cudaSuccess) return fail(ASYRK_E_ThreadSpawnFailure, cudaGetErrorString(err));
-    *proj_per_s = (double)blocks * 8 * (double)proj_per_warp / (ms * 1e-3);
+    // rows shape: every lane group of a warp projects proj_per_warp rows
+    const double per_warp_rows = rows ? (double)(32 / (kl / 4)) : 1.0;
+    *proj_per_s = (double)blocks * 8 * per_warp_rows * (double)proj_per_warp / (ms * 1e-3);
     if (kernel_ms) *kernel_ms = ms;
     return ASYRK_OK;
 }

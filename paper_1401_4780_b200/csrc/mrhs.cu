@@ -437,6 +437,76 @@ __global__ void __launch_bounds__(256, 3) mrhs_worker_batched_kernel(MrhsArgs a)
 // widths) this cuts the instructions per row several-fold against the
 // lane-per-nonzero layout, which spends most of them on the per-row reduction
 // and shuffles (profiles/r02_ncu_mrhs8.txt).
+#ifndef ASYRK_MRHS_VEC
+#define ASYRK_MRHS_VEC 1
+#endif
+constexpr bool kVec = ASYRK_MRHS_VEC != 0;
+
+// One lane group's walk over a row record (row-parallel kernels): rows of a
+// multiple of 4 nonzeros (the columns then 16-byte aligned in the record) are
+// read as int4 / float4 — each load instruction of the warp touches one line
+// per row, so the record takes a quarter of the L1TEX wavefronts of
+// per-nonzero loads (the unit these kernels saturate at 8 columns:
+// profiles/r02_ncu_mrhs8.txt) — with four X accesses in flight per lane.
+// acc += sum_t v_t X[c_t, lanes]   (CG: L1-bypassing X loads, the worker's)
+template <int KL, bool CG>
+__device__ __forceinline__ void row_gather(const float* vals, const int32_t* cols, int len, const float* X, int cl,
+                                           float* acc) {
+    using G = MrGeom<KL>;
+    auto ld = [&](int c) {
+        const float* p = X + (size_t)c * KL + G::VW * cl;
+        return CG ? ld_xv<G::VW>(p) : ld_bv<G::VW>(p);
+    };
+    if (kVec && (len & 3) == 0) {
+        for (int t = 0; t < len; t += 4) {
+            const int4 c4 = __ldg(reinterpret_cast<const int4*>(cols + t));
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(vals + t));
+            const MrVec<G::VW> x0 = ld(c4.x), x1 = ld(c4.y), x2 = ld(c4.z), x3 = ld(c4.w);
+#pragma unroll
+            for (int u = 0; u < G::VW; ++u) {
+                acc[u] = fmaf(v4.x, x0.v[u], acc[u]);
+                acc[u] = fmaf(v4.y, x1.v[u], acc[u]);
+                acc[u] = fmaf(v4.z, x2.v[u], acc[u]);
+                acc[u] = fmaf(v4.w, x3.v[u], acc[u]);
+            }
+        }
+        return;
+    }
+#pragma unroll 4
+    for (int t = 0; t < len; ++t) {
+        const float v = __ldg(vals + t);
+        const MrVec<G::VW> xv = ld(__ldg(cols + t));
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
+    }
+}
+
+// Y[c_t, lanes] += v_t * f[lanes] for every nonzero t of the row (v4 / v2 reds)
+template <int KL>
+__device__ __forceinline__ void row_scatter(const float* vals, const int32_t* cols, int len, float* Y, int cl,
+                                            const float* f) {
+    using G = MrGeom<KL>;
+    auto red = [&](int c, float v) {
+        MrVec<G::VW> d;
+#pragma unroll
+        for (int u = 0; u < G::VW; ++u) d.v[u] = f[u] * v;
+        red_xv<G::VW>(Y + (size_t)c * KL + G::VW * cl, d);
+    };
+    if (kVec && (len & 3) == 0) {
+        for (int t = 0; t < len; t += 4) {
+            const int4 c4 = __ldg(reinterpret_cast<const int4*>(cols + t));
+            const float4 v4 = __ldg(reinterpret_cast<const float4*>(vals + t));
+            red(c4.x, v4.x);
+            red(c4.y, v4.y);
+            red(c4.z, v4.z);
+            red(c4.w, v4.w);
+        }
+        return;
+    }
+#pragma unroll 4
+    for (int t = 0; t < len; ++t) red(__ldg(cols + t), __ldg(vals + t));
+}
+
 template <int KL>
 __global__ void __launch_bounds__(256, 4) mrhs_worker_rows_kernel(MrhsArgs a) {
     using G = MrGeom<KL>;
@@ -475,26 +545,13 @@ __global__ void __launch_bounds__(256, 4) mrhs_worker_rows_kernel(MrhsArgs a) {
             float acc[G::VW];
 #pragma unroll
             for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
-#pragma unroll 4
-            for (int t = 0; t < len; ++t) {
-                const float v = __ldg(vals + t);
-                const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
-#pragma unroll
-                for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
-            }
+            row_gather<KL, true>(vals, cols, len, X, cl, acc);
             const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
             const float inv = (float)rec_inv(r);
             float cf[G::VW];
 #pragma unroll
             for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[u] - bv.v[u]) * inv;
-#pragma unroll 4
-            for (int t = 0; t < len; ++t) {
-                const float v = __ldg(vals + t);
-                MrVec<G::VW> d;
-#pragma unroll
-                for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
-                red_xv<G::VW>(X + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
-            }
+            row_scatter<KL>(vals, cols, len, X, cl, cf);
         }
     }
 }
@@ -645,13 +702,7 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_rows_par_kernel(MrhsArgs a) {
         float acc[G::VW];
 #pragma unroll
         for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
-#pragma unroll 4
-        for (int t = 0; t < r.len; ++t) {
-            const float v = __ldg(vals + t);
-            const MrVec<G::VW> xv = ld_bv<G::VW>(a.X + (size_t)__ldg(cols + t) * KL + G::VW * cl);
-#pragma unroll
-            for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
-        }
+        row_gather<KL, false>(vals, cols, r.len, a.X, cl, acc);
         const MrVec<G::VW> bv = ld_bv<G::VW>(a.B + (size_t)i * KL + G::VW * cl);
         float rv[G::VW];
 #pragma unroll
@@ -660,14 +711,7 @@ __global__ void __launch_bounds__(kMrThreads) mrhs_rows_par_kernel(MrhsArgs a) {
             mine += (double)rv[u] * rv[u];
         }
         if (a.G) {  // G += a_i r_i^T
-#pragma unroll 4
-            for (int t = 0; t < r.len; ++t) {
-                const float v = __ldg(vals + t);
-                MrVec<G::VW> d;
-#pragma unroll
-                for (int u = 0; u < G::VW; ++u) d.v[u] = v * rv[u];
-                red_xv<G::VW>(a.G + (size_t)__ldg(cols + t) * KL + G::VW * cl, d);
-            }
+            row_scatter<KL>(vals, cols, r.len, a.G, cl, rv);
         } else {
             float* rp = a.R + (size_t)i * KL + G::VW * cl;
 #pragma unroll
@@ -865,6 +909,14 @@ static bool mrhs_use_rowpar() {
     static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
     static const bool other = getenv("ASYRK_MRHS_ROWS") || getenv("ASYRK_MRHS_BATCH");
     return rowpar == 1 || (rowpar < 0 && !other && (KL == 8 || KL == 16));
+}
+
+bool mrhs_rowpar(int kl) {
+    switch (kl) {
+        case 8: return mrhs_use_rowpar<8>();
+        case 16: return mrhs_use_rowpar<16>();
+        default: return false;
+    }
 }
 
 template <int KL>

@@ -255,3 +255,36 @@ def test_config1_reassociated_mode_within_1e12():
     assert np.all(np.abs(fast["r_sq"] - want["r_sq"]) <= 1e-12 * want["r_sq"])
     assert np.array_equal(fast["final_x"], fast2["final_x"])  # reproducible
     assert np.array_equal(exact["final_x"], want["final_x"])  # the default stays bitwise
+
+
+def test_sigma_sorted_columns_bitwise():
+    # the monitor's column copy is sigma-sorted (positions by decreasing column
+    # length, kernels.h CscDev): every column still sums its entries in
+    # ascending row order, so A^T r and the residual records stay bit-identical
+    # to the serial reference (csr.cpp:80-92, 140-160) on skewed column
+    # lengths, empty columns and n not a multiple of 32
+    rng = np.random.default_rng(21)
+    m, n = 3000, 1001
+    pop = rng.pareto(1.2, size=n) + 0.05
+    pop[rng.choice(n, size=60, replace=False)] = 0.0  # empty columns
+    pop /= pop.sum()
+    lens = rng.integers(1, 40, size=m)
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.sort(rng.choice(n, size=k, replace=False, p=pop)) for k in lens]).astype(np.int64)
+    v = rng.standard_normal(rp[-1])
+    v /= np.repeat(np.sqrt(np.add.reduceat(v * v, rp[:-1])), lens)  # unit rows (rk_solve's uniform sampling)
+    A = capi.HostCsr(m, n, rp, ci, v)
+    b = rng.standard_normal(m)
+    x = rng.standard_normal(n)
+    r = rng.standard_normal(m)
+    Ao = oracle.C.from_arrays(m, n, rp, ci, v)
+    with capi.System(A, b) as S:
+        assert np.array_equal(S.multiply_transpose(r), oracle.C.multiply_transpose(Ao, r))
+        assert np.array_equal(S.multiply(x), oracle.C.multiply(Ao, x))
+        assert S.residuals(x) == oracle.C.residuals(Ao, x, b)
+        # the deterministic path's records (exact monitor: serial g^2 in column order)
+        t = S.rk_solve(max_epochs=3, seed=5)
+    ref = oracle.C.rk_solve(Ao, b, np.zeros(n), 3, seed=5)
+    for k in ("r_sq", "grad_sq", "final_x"):
+        assert np.array_equal(t[k], ref[k]), k
