@@ -422,7 +422,7 @@ asyrk_status asyrk_microbench_xside(int64_t n, int32_t theta, int32_t precision,
 /* The multi-RHS x side (config 5): per "projection" theta
  * random rows of an n x kl fp32 X gathered (float4 lanes), a per-column warp
  * reduction, theta red.global.add.v4.f32 back; no A / B stream. At the widths
- * where the row-parallel worker runs (kl 8 / 16) the pattern is that worker's:
+ * where the row-parallel worker runs (kl 8 / 16 / 32) the pattern is that worker's:
  * a group of kl/4 lanes per row, four gathers in flight, no reduction, and
  * every lane group projects proj_per_warp rows. proj_per_s = row projections
  * per second (x kl for column projections). */

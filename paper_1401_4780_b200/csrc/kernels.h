@@ -174,7 +174,7 @@ struct MrhsArgs {
     uint32_t max_len;             // longest row (> 32: the looped worker)
 };
 bool mrhs_supported_kl(long long kl);
-bool mrhs_rowpar(int kl);  // the row-parallel worker runs at this width (KL 8 / 16 by default)
+bool mrhs_rowpar(int kl);  // the row-parallel worker runs at this width (KL 8 / 16 / 32 by default)
 int mrhs_max_resident_warps(int kl, uint32_t max_len);  // co-resident worker warps of the worker used
 int mrhs_row_blocks(long long m);
 int mrhs_col_blocks(long long n);

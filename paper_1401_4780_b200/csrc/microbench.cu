@@ -276,6 +276,8 @@ extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, in
             xside_mrhs_rows_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
         else if (rows && kl == 16)
             xside_mrhs_rows_kernel<16><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else if (rows && kl == 32)
+            xside_mrhs_rows_kernel<32><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
         else switch (kl) {
             case 2: xside_mrhs_kernel<2><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
             case 4: xside_mrhs_kernel<4><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;

@@ -901,20 +901,23 @@ static int mrhs_default_rows(int kl) { return kl >= 32 ? 1 : 2; }
 // nonzeros always take the one-row worker. ASYRK_MRHS_NOSTREAM=1: plain
 // read-only loads for A / B; ASYRK_MRHS_MINB=5: the one-row worker at 5 blocks
 // (40 warps) per SM instead of 4 (A/B runs).
-// The row-parallel worker (a lane group per row, RPW rows per warp) on 8- and
-// 16-column shards; ASYRK_MRHS_ROWPAR=1 / =0 forces it on / off (any width),
+// The row-parallel worker (a lane group per row, RPW rows per warp) on 8-, 16-
+// and 32-column shards (at 32: 0.300 vs 0.316 ms per epoch, its monitor 0.31 vs
+// 0.38 ms; at 64 the one-row worker stays ahead, 0.57 vs 0.60 — A/B in
+// scripts/probe_cfg5.py); ASYRK_MRHS_ROWPAR=1 / =0 forces it on / off (any width),
 // ASYRK_MRHS_ROWS / ASYRK_MRHS_BATCH select the lane-per-nonzero variants.
 template <int KL>
 static bool mrhs_use_rowpar() {
     static const int rowpar = getenv("ASYRK_MRHS_ROWPAR") ? atoi(getenv("ASYRK_MRHS_ROWPAR")) : -1;
     static const bool other = getenv("ASYRK_MRHS_ROWS") || getenv("ASYRK_MRHS_BATCH");
-    return rowpar == 1 || (rowpar < 0 && !other && (KL == 8 || KL == 16));
+    return rowpar == 1 || (rowpar < 0 && !other && (KL == 8 || KL == 16 || KL == 32));
 }
 
 bool mrhs_rowpar(int kl) {
     switch (kl) {
         case 8: return mrhs_use_rowpar<8>();
         case 16: return mrhs_use_rowpar<16>();
+        case 32: return mrhs_use_rowpar<32>();
         default: return false;
     }
 }

@@ -1,5 +1,4 @@
 #!/bin/bash
 set -u
 mkdir -p gpurun_out
-KLS=16,8 timeout 600 python scripts/probe_cfg5.py > gpurun_out/probe_cfg5.txt 2>&1
-timeout 600 python -m pytest tests/test_gpu_mrhs.py -x -q > gpurun_out/t.txt 2>&1; tail -2 gpurun_out/t.txt
+timeout 900 python -m pytest tests/test_gpu_mrhs.py -x -q > gpurun_out/t.txt 2>&1; tail -2 gpurun_out/t.txt

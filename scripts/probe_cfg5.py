@@ -26,7 +26,7 @@ for kl in kls:
     bbk = float((B[:, :kl].astype(np.float64) ** 2).sum())
     for W in ([int(v) for v in os.environ["WARPS"].split(",")] if "WARPS" in os.environ
               else [S.max_resident_warps()]):
-        rowpar = kl in (8, 16) and not any(k in os.environ for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_BATCH")) \
+        rowpar = kl in (8, 16, 32) and not any(k in os.environ for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_BATCH")) \
             and os.environ.get("ASYRK_MRHS_ROWPAR", "") != "0"
         rx = max(capi.microbench_xside_mrhs(A.n, 20, kl, W // (128 // kl) if rowpar else W, 64) for _ in range(2))
         for nm in samps:

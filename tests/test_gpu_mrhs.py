@@ -146,9 +146,10 @@ def test_slice_shuffle_sampling_converges(problem):
     assert int(t["updates_applied"][-1]) == A.m * int(t["epoch_index"][-1])
 
 
-@pytest.mark.parametrize("kl", [2, 4, 16])
+@pytest.mark.parametrize("kl", [2, 4, 8, 16, 32])
 def test_narrow_shards_converge(problem, kl):
-    # the shard widths of 32 / 16 / 4 GPUs (float2 and float4 lane layouts)
+    # the shard widths of 32 / 16 / 8 / 4 / 2 GPUs (float2 and float4 lane layouts;
+    # the row-parallel worker and monitor at 8 / 16 / 32 columns)
     A, B, Xs = problem
     S = capi.MultiRHS(A, B, 0, kl)
     bb = float((B[:, :kl].astype(np.float64) ** 2).sum())
@@ -221,4 +222,33 @@ def test_solve_devices_two_gpus():
     bb = float((B.astype(np.float64) ** 2).sum())
     t = capi.mrhs_solve_devices(A, B, [0, 1], threads=2048, epochs=400, target=TOL * TOL * bb, seed=3)
     R = _residual(A, t["X"], B)
+    assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
+
+
+@pytest.mark.parametrize("kl", [8, 32])
+def test_row_parallel_ragged_rows(kl):
+    # rows of 1..30 nonzeros: the row-parallel kernels read records whose length
+    # is a multiple of 4 as int4 / float4 and the others entry by entry (mrhs.cu
+    # row_gather / row_scatter); both kinds of rows in one system
+    rng = np.random.default_rng(17)
+    m, n = 30000, 12000
+    lens = rng.integers(1, 31, size=m)
+    rp = np.zeros(m + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    ci = np.concatenate([np.sort(rng.choice(n, size=k, replace=False)) for k in lens]).astype(np.int64)
+    v = rng.standard_normal(rp[-1])
+    v /= np.repeat(np.sqrt(np.add.reduceat(v * v, rp[:-1])), lens)
+    A = capi.HostCsr(m, n, rp, ci, v)
+    Xs = rng.standard_normal((n, kl))
+    row = np.repeat(np.arange(m), lens)
+    B = np.zeros((m, kl))
+    np.add.at(B, row, v[:, None] * Xs[ci])
+    B = B.astype(np.float32)
+    bb = float((B.astype(np.float64) ** 2).sum())
+    S = capi.MultiRHS(A, B, 0, kl)
+    t = S.solve(threads=min(S.max_resident_warps(), m // 8), epochs=600, target=TOL * TOL * bb, seed=3)
+    S.close()
+    R = -B.astype(np.float64)
+    np.add.at(R, row, v[:, None] * t["X"][ci].astype(np.float64))
+    assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
     assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
