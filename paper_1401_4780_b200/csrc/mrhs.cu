@@ -41,6 +41,18 @@ struct MrVec {
     float v[VW];
 };
 
+// rows of a multiple of 4 nonzeros: records read as int4 / float4 (row_gather,
+// the one-row worker); ASYRK_MRHS_VEC=0 at build time keeps per-entry loads
+#ifndef ASYRK_MRHS_VEC
+#define ASYRK_MRHS_VEC 1
+#endif
+constexpr bool kVec = ASYRK_MRHS_VEC != 0;
+// element k (0..3, lane-varying) of a 4-vector without a local-memory array
+__device__ __forceinline__ int pick4(const int4& q, int k) { return k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w; }
+__device__ __forceinline__ float pick4(const float4& q, int k) {
+    return k == 0 ? q.x : k == 1 ? q.y : k == 2 ? q.z : q.w;
+}
+
 template <int VW>
 __device__ __forceinline__ MrVec<VW> ld_xv(const float* p) {  // L1-bypassing: X takes other SMs' reds
     MrVec<VW> r;
@@ -293,13 +305,36 @@ __global__ void __launch_bounds__(256, MINB) mrhs_worker_long_kernel(MrhsArgs a)
             float acc[G::VW];
 #pragma unroll
             for (int u = 0; u < G::VW; ++u) acc[u] = 0.f;
-            for (int t0 = 0; t0 < len; t0 += G::S) {
-                const int t = t0 + slot;
-                if (t < len) {
-                    const float v = ld_a(vals + t, STREAM);
-                    const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl);
+            // rows of a multiple of 4 nonzeros (S <= 4): the record as int4 / float4, one
+            // broadcast load per 4 nonzeros (slot s takes entries s, s + S, ...) instead
+            // of one per nonzero — a quarter of the record's L1TEX wavefronts
+            constexpr int PER = G::S <= 4 ? 4 / G::S : 1;  // entries of a chunk per slot
+            const bool vec = kVec && G::S <= 4 && (len & 3) == 0;
+            if (vec) {
+                for (int t0 = 0; t0 < len; t0 += 4) {
+                    const int4 c4 = STREAM ? __ldcs(reinterpret_cast<const int4*>(cols + t0))
+                                           : __ldg(reinterpret_cast<const int4*>(cols + t0));
+                    const float4 v4 = STREAM ? __ldcs(reinterpret_cast<const float4*>(vals + t0))
+                                             : __ldg(reinterpret_cast<const float4*>(vals + t0));
+                    MrVec<G::VW> xv[PER];
 #pragma unroll
-                    for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
+                    for (int j = 0; j < PER; ++j) xv[j] = ld_xv<G::VW>(X + (size_t)pick4(c4, slot + G::S * j) * KL + G::VW * cl);
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) {
+                        const float v = pick4(v4, slot + G::S * j);
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv[j].v[u], acc[u]);
+                    }
+                }
+            } else {
+                for (int t0 = 0; t0 < len; t0 += G::S) {
+                    const int t = t0 + slot;
+                    if (t < len) {
+                        const float v = ld_a(vals + t, STREAM);
+                        const MrVec<G::VW> xv = ld_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl);
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) acc[u] = fmaf(v, xv.v[u], acc[u]);
+                    }
                 }
             }
 #pragma unroll
@@ -312,14 +347,31 @@ __global__ void __launch_bounds__(256, MINB) mrhs_worker_long_kernel(MrhsArgs a)
             float cf[G::VW];
 #pragma unroll
             for (int u = 0; u < G::VW; ++u) cf[u] = -gamma * (acc[u] - bv.v[u]) * inv;
-            for (int t0 = 0; t0 < len; t0 += G::S) {
-                const int t = t0 + slot;
-                if (t < len) {
-                    const float v = ld_a(vals + t, STREAM);
-                    MrVec<G::VW> d;
+            if (vec) {
+                for (int t0 = 0; t0 < len; t0 += 4) {
+                    const int4 c4 = STREAM ? __ldcs(reinterpret_cast<const int4*>(cols + t0))
+                                           : __ldg(reinterpret_cast<const int4*>(cols + t0));
+                    const float4 v4 = STREAM ? __ldcs(reinterpret_cast<const float4*>(vals + t0))
+                                             : __ldg(reinterpret_cast<const float4*>(vals + t0));
 #pragma unroll
-                    for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
-                    red_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl, d);
+                    for (int j = 0; j < PER; ++j) {
+                        const float v = pick4(v4, slot + G::S * j);
+                        MrVec<G::VW> d;
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                        red_xv<G::VW>(X + (size_t)pick4(c4, slot + G::S * j) * KL + G::VW * cl, d);
+                    }
+                }
+            } else {
+                for (int t0 = 0; t0 < len; t0 += G::S) {
+                    const int t = t0 + slot;
+                    if (t < len) {
+                        const float v = ld_a(vals + t, STREAM);
+                        MrVec<G::VW> d;
+#pragma unroll
+                        for (int u = 0; u < G::VW; ++u) d.v[u] = cf[u] * v;
+                        red_xv<G::VW>(X + (size_t)ld_a(cols + t, STREAM) * KL + G::VW * cl, d);
+                    }
                 }
             }
         }
@@ -437,10 +489,6 @@ __global__ void __launch_bounds__(256, 3) mrhs_worker_batched_kernel(MrhsArgs a)
 // widths) this cuts the instructions per row several-fold against the
 // lane-per-nonzero layout, which spends most of them on the per-row reduction
 // and shuffles (profiles/r02_ncu_mrhs8.txt).
-#ifndef ASYRK_MRHS_VEC
-#define ASYRK_MRHS_VEC 1
-#endif
-constexpr bool kVec = ASYRK_MRHS_VEC != 0;
 
 // One lane group's walk over a row record (row-parallel kernels): rows of a
 // multiple of 4 nonzeros (the columns then 16-byte aligned in the record) are
