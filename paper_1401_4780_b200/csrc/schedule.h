@@ -29,13 +29,13 @@ namespace ak {
 struct MonitorSchedule {
     double target = 0.0;
     bool every = false;
-    long long max_gap = 12;
+    long long max_gap = 16;
     long long b_prev = -1, b_last = -1;  // boundaries (in snapshot intervals) of the last two records
     double r_prev = 0.0, r_last = 0.0;
 
     void reset(double tgt, bool every_boundary) {
         target = tgt;
-        static const long long env_gap = getenv("ASYRK_MONITOR_MAX_GAP") ? atoll(getenv("ASYRK_MONITOR_MAX_GAP")) : 12;
+        static const long long env_gap = getenv("ASYRK_MONITOR_MAX_GAP") ? atoll(getenv("ASYRK_MONITOR_MAX_GAP")) : 16;
         static const bool env_every = getenv("ASYRK_MONITOR_EVERY") != nullptr;
         max_gap = env_gap > 0 ? env_gap : 1;
         every = every_boundary || env_every || !(tgt > 0.0);
