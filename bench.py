@@ -573,10 +573,12 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=0):
         t = torch.tensor([float(col_proj)], device="cuda", dtype=torch.float64)
         dist.all_reduce(t)
         col_proj = float(t.item())
-    # the multi-RHS x-side ceiling at this shard's width and warp count (no A / B stream)
+    # the multi-RHS x-side ceiling at this shard's width and warp count (no A / B stream), on the
+    # shard's own X (a fresh buffer measures lower, as config 2's R_x does)
     kl = c1 - c0
-    warps = W // (128 // kl) if kl in (8, 16) else W  # the row-parallel worker runs 128/kl workers per warp
-    rx5 = max(capi.microbench_xside_mrhs(CFG5["n"], CFG5["theta"], kl, warps, 64) for _ in range(2))
+    warps = W // (128 // kl) if kl in (8, 16, 32) else W  # the row-parallel worker runs 128/kl workers per warp
+    rx5 = max(sh.microbench_xside(warps, 64) for _ in range(2))
+    rx5_fresh = capi.microbench_xside_mrhs(CFG5["n"], CFG5["theta"], kl, warps, 64)
     sh.close()
     comm.close()
     if rank != 0:
@@ -590,9 +592,15 @@ def cfg5_sharded(steps, warmup, dist, rank, world, local, stream, W=0):
             "library_solve_ms_per_step": lib_ms / steps,
             "roofline": {"bound": "l2_x_side", "unit": "row proj/s", "achieved": worker_rate, "peak": rx5,
                          "frac": worker_rate / rx5 if rx5 else None,
+                         "peak_fresh_buffer": rx5_fresh,
                          "source": "achieved = rank 0's row projections / its worker-launch time; peak = "
-                                   "asyrk_microbench_xside_mrhs (the K2b worker's X gathers and v4 reds, no A/B "
-                                   "stream) at the same width, warps and n, measured live",
+                                   "asyrk_mrhs_microbench_xside (the K2b worker's X gathers and v4 reds, no A/B "
+                                   "stream) on the shard's own X at the same width and warps, measured live",
+                         "note": "the microbenchmark is the worker's X pattern stripped of the A / B streams, not a "
+                                 "hardware roof: frac ~1.0 (up to 1.05 at 64 columns, where the worker interleaves "
+                                 "its gathers and reds more evenly than the stripped loop) says the worker runs at "
+                                 "the rate of its own X traffic; the saturated unit is the L1TEX pipeline "
+                                 "(ncu: 73% at 64 columns, 90% at 8; profiles/r02_ncu_mrhs*.txt)",
                          "x_bytes_per_row_proj": 2 * CFG5["theta"] * (c1 - c0) * 4},
             "allreduce_us_per_call": ar_us, "scaling": "strong", "columns_per_gpu": c1 - c0,
             "driver": "asyrk_mrhs_solve_nccl (native loop, NCCL all-reduce of the shard norms per evaluated boundary)",

@@ -385,6 +385,12 @@ asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const 
 asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out);
 /* Largest number of co-resident worker warps for this shard's width. */
 asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out);
+/* asyrk_microbench_xside_mrhs on this shard's own X (n x kl, re-initialized
+ * by every solve; the address and pages the worker uses, as
+ * asyrk_system_microbench_xside does for config 2), theta = the rows' length
+ * (at most 32). proj_per_s = row projections per second. */
+asyrk_status asyrk_mrhs_microbench_xside(asyrk_mrhs* h, int32_t warps, int64_t proj_per_warp, double* proj_per_s,
+                                         double* kernel_ms);
 
 /* ---- multi-GPU: NCCL (SURVEY.md §8b "mrhs_shard_solve(..., ncclComm_t)") ----
  * libnccl.so.2 is resolved at run time (the copy already loaded in the

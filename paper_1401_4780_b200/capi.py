@@ -261,6 +261,7 @@ def lib():
         L.asyrk_mrhs_last_stats.argtypes = [sp, C.POINTER(SolveStats)]
         L.asyrk_mrhs_due.argtypes = [sp, _i32p]
         L.asyrk_mrhs_max_resident_warps.argtypes = [sp, _i32p]
+        L.asyrk_mrhs_microbench_xside.argtypes = [sp, C.c_int32, C.c_int64, _f64p, _f64p]
         L.asyrk_microbench_xside_mrhs.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int64, _f64p, _f64p]
         L.asyrk_monitor_schedule_next.argtypes = [C.c_double, C.c_int32, C.c_int64, _i64p, _f64p, C.c_int64, _i64p]
         L.asyrk_system_rk_solve_multi.argtypes = [sp, _f64p, C.c_int64, _f64p, C.POINTER(RkConfig), _f64p,
@@ -294,7 +295,7 @@ EXPORTED = [
     "asyrk_system_last_stats", "asyrk_system_max_resident_warps", "asyrk_generate_fixed_theta",
     "asyrk_microbench_xside", "asyrk_mrhs_create", "asyrk_mrhs_destroy", "asyrk_mrhs_begin", "asyrk_mrhs_norms",
     "asyrk_mrhs_commit", "asyrk_mrhs_step", "asyrk_mrhs_stopped", "asyrk_mrhs_finish", "asyrk_mrhs_solve",
-    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_mrhs_max_resident_warps", "asyrk_microbench_xside_mrhs", "asyrk_monitor_schedule_next", "asyrk_system_rk_solve_multi", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
+    "asyrk_mrhs_last_stats", "asyrk_mrhs_due", "asyrk_mrhs_max_resident_warps", "asyrk_mrhs_microbench_xside", "asyrk_microbench_xside_mrhs", "asyrk_monitor_schedule_next", "asyrk_system_rk_solve_multi", "asyrk_system_microbench_xside", "asyrk_system_sample_rows", "asyrk_nccl_available", "asyrk_nccl_get_unique_id",
     "asyrk_nccl_comm_init_rank", "asyrk_nccl_comm_destroy", "asyrk_mrhs_solve_nccl", "asyrk_mrhs_solve_devices",
     "asyrk_compute_stats", "asyrk_system_compute_stats", "asyrk_simulate",
     "asyrk_system_simulate", "asyrk_monte_carlo_ratios", "asyrk_system_monte_carlo_ratios", "asyrk_rate_fit",
@@ -355,6 +356,12 @@ class MultiRHS:
         w = C.c_int32()
         check(lib().asyrk_mrhs_max_resident_warps(self.h, C.byref(w)))
         return w.value
+
+    def microbench_xside(self, warps, proj_per_warp=64):
+        """R_x of this shard's pattern on its own X (asyrk_mrhs_microbench_xside): row projections/s."""
+        rate, ms = C.c_double(), C.c_double()
+        check(lib().asyrk_mrhs_microbench_xside(self.h, warps, proj_per_warp, C.byref(rate), C.byref(ms)))
+        return rate.value
 
     def due(self):
         """True when the last begin/step ended at an evaluated boundary (all-reduce the norms, then commit)."""

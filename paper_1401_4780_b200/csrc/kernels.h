@@ -174,6 +174,8 @@ struct MrhsArgs {
     uint32_t max_len;             // longest row (> 32: the looped worker)
 };
 bool mrhs_supported_kl(long long kl);
+int32_t xside_mrhs_on_buffer(float* X, int64_t n, int32_t theta, int32_t kl, int32_t warps, int64_t proj_per_warp,
+                                  cudaStream_t stream, double* proj_per_s, double* kernel_ms);  // an asyrk_status
 bool mrhs_rowpar(int kl);  // the row-parallel worker runs at this width (KL 8 / 16 / 32 by default)
 int mrhs_max_resident_warps(int kl, uint32_t max_len);  // co-resident worker warps of the worker used
 int mrhs_row_blocks(long long m);

@@ -252,6 +252,49 @@ asyrk_status xside_on_buffer(void* x, int64_t n, int32_t theta, int32_t precisio
 }
 
 // R_x of the multi-RHS pattern (config 5): X n x kl fp32 on a 2 MB boundary
+namespace ak {
+// the multi-RHS x-side kernel timed on an n x kl X buffer (its contents are
+// perturbed by reds of ~1e-30 x values)
+int32_t xside_mrhs_on_buffer(float* X, int64_t n, int32_t theta, int32_t kl, int32_t warps, int64_t proj_per_warp,
+                                  cudaStream_t stream, double* proj_per_s, double* kernel_ms) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int blocks = (warps * 32 + 255) / 256;
+    float ms = 0.f;
+    const bool rows = mrhs_rowpar((int)kl);  // the worker's own shape at this width
+    for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(e0, stream);
+        if (rows && kl == 8)
+            xside_mrhs_rows_kernel<8><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else if (rows && kl == 16)
+            xside_mrhs_rows_kernel<16><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else if (rows && kl == 32)
+            xside_mrhs_rows_kernel<32><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp);
+        else switch (kl) {
+            case 2: xside_mrhs_kernel<2><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 4: xside_mrhs_kernel<4><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 8: xside_mrhs_kernel<8><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 16: xside_mrhs_kernel<16><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            case 32: xside_mrhs_kernel<32><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+            default: xside_mrhs_kernel<64><<<blocks, 256, 0, stream>>>(X, (uint32_t)n, theta, proj_per_warp); break;
+        }
+        cudaEventRecord(e1, stream);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+    }
+    const cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (err != cudaSuccess) return fail(ASYRK_E_ThreadSpawnFailure, cudaGetErrorString(err));
+    // rows shape: every lane group of a warp projects proj_per_warp rows
+    const double per_warp_rows = rows ? (double)(32 / (kl / 4)) : 1.0;
+    *proj_per_s = (double)blocks * 8 * per_warp_rows * (double)proj_per_warp / (ms * 1e-3);
+    if (kernel_ms) *kernel_ms = ms;
+    return ASYRK_OK;
+}
+}  // namespace ak
+
 extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, int32_t kl, int32_t warps,
                                                     int64_t proj_per_warp, double* proj_per_s, double* kernel_ms) {
     using namespace ak;
@@ -264,40 +307,8 @@ extern "C" asyrk_status asyrk_microbench_xside_mrhs(int64_t n, int32_t theta, in
     if (cudaMalloc(&base, xb + page) != cudaSuccess) return ASYRK_E_TooLarge;
     float* X = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(base) + page - 1) & ~(uintptr_t)(page - 1));
     cudaMemset(X, 0, xb);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    const int blocks = (warps * 32 + 255) / 256;
-    float ms = 0.f;
-    const bool rows = mrhs_rowpar((int)kl);  // the worker's own shape at this width
-    for (int rep = 0; rep < 2; ++rep) {
-        cudaEventRecord(e0);
-        if (rows && kl == 8)
-            xside_mrhs_rows_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
-        else if (rows && kl == 16)
-            xside_mrhs_rows_kernel<16><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
-        else if (rows && kl == 32)
-            xside_mrhs_rows_kernel<32><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp);
-        else switch (kl) {
-            case 2: xside_mrhs_kernel<2><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-            case 4: xside_mrhs_kernel<4><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-            case 8: xside_mrhs_kernel<8><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-            case 16: xside_mrhs_kernel<16><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-            case 32: xside_mrhs_kernel<32><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-            default: xside_mrhs_kernel<64><<<blocks, 256>>>(X, (uint32_t)n, theta, proj_per_warp); break;
-        }
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        cudaEventElapsedTime(&ms, e0, e1);
-    }
-    const cudaError_t err = cudaGetLastError();
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    const asyrk_status st = (asyrk_status)xside_mrhs_on_buffer(X, n, theta, kl, warps, proj_per_warp, 0, proj_per_s, kernel_ms);
+    cudaDeviceSynchronize();
     cudaFree(base);
-    if (err != cudaSuccess) return fail(ASYRK_E_ThreadSpawnFailure, cudaGetErrorString(err));
-    // rows shape: every lane group of a warp projects proj_per_warp rows
-    const double per_warp_rows = rows ? (double)(32 / (kl / 4)) : 1.0;
-    *proj_per_s = (double)blocks * 8 * per_warp_rows * (double)proj_per_warp / (ms * 1e-3);
-    if (kernel_ms) *kernel_ms = ms;
-    return ASYRK_OK;
+    return st;
 }

@@ -2885,6 +2885,20 @@ asyrk_status asyrk_mrhs_solve(asyrk_mrhs* h, const asyrk_run_config* cfg, const 
     });
 }
 
+asyrk_status asyrk_mrhs_microbench_xside(asyrk_mrhs* h, int32_t warps, int64_t proj_per_warp, double* proj_per_s,
+                                         double* kernel_ms) {
+    if (!h || !proj_per_s) return fail(ASYRK_E_InvalidArgument, "null argument");
+    if (warps < 1 || proj_per_warp < 1) return fail(ASYRK_E_InvalidArgument, "warps and proj_per_warp must be >= 1");
+    return guarded([&] {
+        asyrk_system* s = h->sys;
+        const int32_t theta = (int32_t)(s->uniform ? s->uniform_len : s->max_len);
+        if (theta > 32) return fail(ASYRK_E_InvalidArgument, "mrhs microbench: rows of at most 32 nonzeros");
+        // the shard's own X (re-initialized by every solve), as config 2's R_x uses the solver's x
+        return (asyrk_status)xside_mrhs_on_buffer(h->X, s->n, theta, (int32_t)h->kl, warps, proj_per_warp, s->stream, proj_per_s,
+                                    kernel_ms);
+    });
+}
+
 asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out) {
     if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {

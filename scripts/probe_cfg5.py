@@ -28,7 +28,7 @@ for kl in kls:
               else [S.max_resident_warps()]):
         rowpar = kl in (8, 16, 32) and not any(k in os.environ for k in ("ASYRK_MRHS_ROWS", "ASYRK_MRHS_BATCH")) \
             and os.environ.get("ASYRK_MRHS_ROWPAR", "") != "0"
-        rx = max(capi.microbench_xside_mrhs(A.n, 20, kl, W // (128 // kl) if rowpar else W, 64) for _ in range(2))
+        rx = max(S.microbench_xside(W // (128 // kl) if rowpar else W, 64) for _ in range(2))  # on the shard's own X
         for nm in samps:
             samp = capi.SLICE_SHUFFLE if nm == "slice_shuffle" else capi.WITH_REPLACEMENT
             S.solve(threads=W, epochs=2, target=0.0, seed=1, sampling=samp, want_x=False)

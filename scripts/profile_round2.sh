@@ -25,3 +25,11 @@ python scripts/cfg5_once.py > gpurun_out/cfg5_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cfg5_launches.csv python scripts/cfg5_once.py > gpurun_out/cfg5_ncu.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:"mrhs_worker|mrhs_rows|mrhs_cols" -s 40 -c 3 -o gpurun_out/mrhs python scripts/cfg5_once.py > gpurun_out/ncu_mrhs.log 2>&1
 echo "mrhs rc=$?"
+# narrow shard (8 columns, the G = 8 width): the row-parallel worker and monitor, and the x-side
+# microbenchmark in the worker's shape
+KL=8 python scripts/cfg5_once.py > gpurun_out/cfg5_kl8.log 2>&1 && \
+KL=8 ncu --set full --clock-control none --import-source on -k regex:"mrhs_worker|mrhs_rows|mrhs_gnorm" -s 30 -c 3 -o gpurun_out/mrhs8 python scripts/cfg5_once.py > gpurun_out/ncu_mrhs8.log 2>&1
+echo "mrhs8 rc=$?"
+KL=8 python scripts/xside_mrhs_once.py > gpurun_out/xs8.log 2>&1 && \
+KL=8 ncu --set full --clock-control none -k regex:"xside_mrhs" -s 2 -c 1 -o gpurun_out/xside_mrhs8 python scripts/xside_mrhs_once.py > gpurun_out/ncu_xs8.log 2>&1
+echo "xside8 rc=$?"

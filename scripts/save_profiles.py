@@ -49,6 +49,11 @@ for rep, out, hdr in [
                                        "(2 rows in flight, then 1; f64, n=100000, theta=30, 3552 warps, 256 proj/warp)\n"),
         ("mrhs.ncu-rep", "ncu_mrhs", "# ncu --set full -k regex:mrhs_worker|mrhs_rows|mrhs_cols: python scripts/cfg5_once.py "
                                      "(config 5, 64 columns on one GPU)\n"),
+        ("mrhs8.ncu-rep", "ncu_mrhs8", "# ncu --set full -k regex:mrhs_worker|mrhs_rows|mrhs_gnorm: KL=8 python scripts/cfg5_once.py "
+                                       "(config 5, an 8-column shard: the row-parallel worker and monitor)\n"),
+        ("xside_mrhs8.ncu-rep", "ncu_xside_mrhs8", "# ncu --set full -k regex:xside_mrhs: KL=8 python "
+                                                   "scripts/xside_mrhs_once.py (the 8-column x-side pattern, "
+                                                   "row-parallel shape)\n"),
         ("det.ncu-rep", "ncu_det", "# ncu --set full -k regex:det_dataflow -s 2 -c 1: python scripts/ab_det.py "
                                    "(config 1, bitwise mode: one launch = one epoch, 20 000 row events)\n"),
         ("det_reassoc.ncu-rep", "ncu_det_reassoc", "# ncu --set full -k regex:det_dataflow -s 2 -c 1: python "
