@@ -1200,9 +1200,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.full_row = sp.full_row ? 1 : 0;
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
         // waiting warps back off between polls so they leave issue slots to the running
-        // events (bitwise mode: 32 ns measured best; tolerance mode: spinning, 13.3 vs 13.8 ms)
+        // events (bitwise mode: 16 ns, 21.37 vs 21.44 ms at 32 ns; tolerance mode: spinning, 12.23 vs
+        // 12.6 ms with any back-off — scripts/gpu_round2s.sh)
         static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
-        da.poll_ns = poll_env >= 0 ? poll_env : (sp.reassoc ? 0 : 32);
+        da.poll_ns = poll_env >= 0 ? poll_env : (sp.reassoc ? 0 : 16);
         da.max_len = s->max_len;
         da.reassoc = sp.reassoc ? 1 : 0;
         if (!s->pstream) {
@@ -1642,7 +1643,7 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     da.full_row = 1;
     da.x_in_smem = (det_fits_smem(n) && s->max_len <= 128) ? 1 : 0;
     static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
-    da.poll_ns = poll_env >= 0 ? poll_env : (c->det_reassociate ? 0 : 32);
+    da.poll_ns = poll_env >= 0 ? poll_env : (c->det_reassociate ? 0 : 16);
     da.max_len = s->max_len;
     da.ncols = (int)k;
     da.b_cols = Bc;

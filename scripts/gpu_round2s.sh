@@ -2,9 +2,12 @@
 set -u
 mkdir -p gpurun_out
 : > gpurun_out/ab_det.txt
-for L in paper_1401_4780_b200/libasyrk_b200.so; do
-  timeout 300 python scripts/ab_det.py $L >> gpurun_out/ab_det.txt 2>&1
-  timeout 300 python scripts/ab_det.py $L reassoc >> gpurun_out/ab_det.txt 2>&1
+L=paper_1401_4780_b200/libasyrk_b200.so
+for P in 0 2 4 8 16 32; do
+  echo "poll $P" >> gpurun_out/ab_det.txt
+  ASYRK_DET_POLL_NS=$P timeout 300 python scripts/ab_det.py $L reassoc >> gpurun_out/ab_det.txt 2>&1
 done
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.txt 2>&1
-tail -3 gpurun_out/gpu_tests.txt
+for P in 8 16 32 48; do
+  echo "poll $P" >> gpurun_out/ab_det.txt
+  ASYRK_DET_POLL_NS=$P timeout 300 python scripts/ab_det.py $L >> gpurun_out/ab_det.txt 2>&1
+done
