@@ -15,6 +15,7 @@
 #include <vector>
 
 #include "asyrk/delay_sim.hpp"
+#include "host/csr_coo.hpp"
 #include "asyrk/dense.hpp"
 #include "asyrk/lsq.hpp"
 #include "asyrk_dense.h"
@@ -63,9 +64,8 @@ CsrMatrix triplets_to_csr(index_t m, index_t n, const Arr<index_t>& rows, const 
                           const Arr<double>& vals) {
     if (rows.size() != cols.size() || rows.size() != vals.size())
         fail(ErrorCode::DimensionMismatch, "triplet lists differ in length");
-    std::vector<Triplet> t(rows.size());
-    for (std::size_t k = 0; k < rows.size(); ++k) t[k] = Triplet{rows[k], cols[k], vals[k]};
-    return CsrMatrix::from_triplets(t, m, n);
+    // from_triplets' semantics straight from the arrays (host/csr_coo.hpp)
+    return csr_from_coo(m, n, rows.data(), cols.data(), vals.data(), rows.size());
 }
 
 py::dict to_dict(const Trace& tr) {

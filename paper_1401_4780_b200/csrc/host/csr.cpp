@@ -10,6 +10,8 @@
 
 #include "asyrk/csr.hpp"
 #include "asyrk_cuda.h"
+#include "csr_coo.hpp"
+#include "par.hpp"
 
 namespace asyrk {
 
@@ -76,13 +78,24 @@ void CsrMatrix::release_device() const { dev_.reset(); }
 
 void CsrMatrix::compute_norms() {
     row_norm_.resize(static_cast<std::size_t>(m_));
-    for (index_t i = 0; i < m_; ++i) {
-        const index_t b = row_ptr_[static_cast<std::size_t>(i)], e = row_ptr_[static_cast<std::size_t>(i) + 1];
-        if (e == b) fail(ErrorCode::ZeroRow, "row " + std::to_string(i) + " has no nonzeros");
-        double ss = 0.0;  // storage order, like the reference (csr.cpp:53-61)
-        for (index_t k = b; k < e; ++k) ss += values_[static_cast<std::size_t>(k)] * values_[static_cast<std::size_t>(k)];
-        row_norm_[static_cast<std::size_t>(i)] = std::sqrt(ss);
-    }
+    // rows in parallel chunks (each row's sum is serial, so the result is the serial one)
+    const int T = par::threads_for(values_.size() + static_cast<std::size_t>(m_));
+    std::vector<index_t> first_zero(static_cast<std::size_t>(T), -1);
+    par::chunks(static_cast<std::size_t>(m_), T, [&](int t, std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const index_t b = row_ptr_[i], e = row_ptr_[i + 1];
+            if (e == b) {
+                if (first_zero[static_cast<std::size_t>(t)] < 0) first_zero[static_cast<std::size_t>(t)] = static_cast<index_t>(i);
+                continue;
+            }
+            double ss = 0.0;  // storage order, like the reference (csr.cpp:53-61)
+            for (index_t k = b; k < e; ++k)
+                ss += values_[static_cast<std::size_t>(k)] * values_[static_cast<std::size_t>(k)];
+            row_norm_[i] = std::sqrt(ss);
+        }
+    });
+    for (index_t z : first_zero)  // chunks are in row order: the first one found is the first zero row
+        if (z >= 0) fail(ErrorCode::ZeroRow, "row " + std::to_string(z) + " has no nonzeros");
 }
 
 CsrMatrix CsrMatrix::from_triplets(std::span<const Triplet> entries, index_t m, index_t n) {
@@ -210,25 +223,99 @@ void CsrMatrix::flag_normalized() {
 std::pair<CsrMatrix, std::vector<double>> normalize_rows(const CsrMatrix& A, std::span<const double> b) {
     if (!b.empty() && static_cast<index_t>(b.size()) != A.rows())
         fail(ErrorCode::DimensionMismatch, "normalize_rows: b has wrong length");
+    for (index_t i = 0; i < A.rows(); ++i)
+        if (A.row_norm_[static_cast<std::size_t>(i)] == 0.0)
+            fail(ErrorCode::ZeroRow, "row " + std::to_string(i) + " has zero norm");
     CsrMatrix N = A;
     std::vector<double> nb(b.begin(), b.end());
-    for (index_t i = 0; i < A.rows(); ++i) {
-        const std::size_t si = static_cast<std::size_t>(i);
-        const double nrm = A.row_norm_[si];
-        if (nrm == 0.0) fail(ErrorCode::ZeroRow, "row " + std::to_string(i) + " has zero norm");
-        if (std::abs(nrm - 1.0) <= CsrMatrix::kNormTol) continue;  // unit rows stay bit-identical
-        double ss = 0.0;
-        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k) {
-            double& v = N.values_[static_cast<std::size_t>(k)];
-            v /= nrm;
-        }
-        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k)
-            ss += N.values_[static_cast<std::size_t>(k)] * N.values_[static_cast<std::size_t>(k)];
-        if (!nb.empty()) nb[si] /= nrm;
-        N.row_norm_[si] = std::sqrt(ss);  // recomputed, not assumed 1
-    }
+    // rows in parallel chunks: every row is scaled and re-summed on its own
+    par::chunks(static_cast<std::size_t>(A.rows()), par::threads_for(N.values_.size()),
+                [&](int, std::size_t lo, std::size_t hi) {
+                    for (std::size_t si = lo; si < hi; ++si) {
+                        const double nrm = A.row_norm_[si];
+                        if (std::abs(nrm - 1.0) <= CsrMatrix::kNormTol) continue;  // unit rows stay bit-identical
+                        double ss = 0.0;
+                        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k) {
+                            double& v = N.values_[static_cast<std::size_t>(k)];
+                            v /= nrm;
+                        }
+                        for (index_t k = N.row_ptr_[si]; k < N.row_ptr_[si + 1]; ++k)
+                            ss += N.values_[static_cast<std::size_t>(k)] * N.values_[static_cast<std::size_t>(k)];
+                        if (!nb.empty()) nb[si] /= nrm;
+                        N.row_norm_[si] = std::sqrt(ss);  // recomputed, not assumed 1
+                    }
+                });
     N.flag_normalized();
     return {std::move(N), std::move(nb)};
+}
+
+CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
+                       std::size_t nnz) {
+    if (m < 1 || n < 1) fail(ErrorCode::InvalidArgument, "matrix dimensions must be positive");
+    const int T = par::threads_for(nnz);
+    // per chunk: first out-of-range entry, and whether (row, col) strictly increases
+    std::vector<std::size_t> bad(static_cast<std::size_t>(T), SIZE_MAX);
+    std::vector<char> sorted(static_cast<std::size_t>(T), 1);
+    std::vector<std::size_t> kept(static_cast<std::size_t>(T) + 1, 0);
+    par::chunks(nnz, T, [&](int t, std::size_t lo, std::size_t hi) {
+        std::size_t nk = 0;
+        bool srt = true;
+        for (std::size_t k = lo; k < hi; ++k) {
+            if (rows[k] < 0 || rows[k] >= m || cols[k] < 0 || cols[k] >= n) {
+                bad[static_cast<std::size_t>(t)] = k;
+                break;
+            }
+            if (k > 0 && !(rows[k] > rows[k - 1] || (rows[k] == rows[k - 1] && cols[k] > cols[k - 1]))) srt = false;
+            nk += vals[k] != 0.0;
+        }
+        sorted[static_cast<std::size_t>(t)] = srt;
+        kept[static_cast<std::size_t>(t) + 1] = nk;
+    });
+    for (std::size_t k : bad)
+        if (k != SIZE_MAX)
+            fail(ErrorCode::IndexOutOfRange, "triplet (" + std::to_string(rows[k]) + "," + std::to_string(cols[k]) +
+                                                 ") outside " + std::to_string(m) + "x" + std::to_string(n));
+    if (!std::all_of(sorted.begin(), sorted.end(), [](char c) { return c != 0; })) {
+        // general order: the reference path (counting sort by row, duplicates rejected)
+        std::vector<Triplet> t(nnz);
+        for (std::size_t k = 0; k < nnz; ++k) t[k] = Triplet{rows[k], cols[k], vals[k]};
+        return CsrMatrix::from_triplets(t, m, n);
+    }
+    // (row, column) order with no repeats — the common case, e.g. triplets taken
+    // from a CSR: zero values dropped as from_triplets does, chunks write their
+    // kept entries at prefix offsets and the row starts they cross
+    for (int t = 0; t < T; ++t) kept[static_cast<std::size_t>(t) + 1] += kept[static_cast<std::size_t>(t)];
+    const std::size_t total = kept[static_cast<std::size_t>(T)];
+    std::vector<index_t> rp(static_cast<std::size_t>(m) + 1), ci(total);
+    std::vector<double> v(total);
+    // the row of the last kept entry before each chunk (-1: none)
+    std::vector<index_t> last_row(static_cast<std::size_t>(T), -1);
+    par::chunks(nnz, T, [&](int t, std::size_t lo, std::size_t hi) {
+        index_t lr = -1;
+        for (std::size_t k = hi; k > lo; --k)
+            if (vals[k - 1] != 0.0) {
+                lr = rows[k - 1];
+                break;
+            }
+        last_row[static_cast<std::size_t>(t)] = lr;
+    });
+    par::chunks(nnz, T, [&](int t, std::size_t lo, std::size_t hi) {
+        index_t prev = -1;
+        for (int u = t - 1; u >= 0 && prev < 0; --u) prev = last_row[static_cast<std::size_t>(u)];
+        std::size_t p = kept[static_cast<std::size_t>(t)];
+        for (std::size_t k = lo; k < hi; ++k) {
+            if (vals[k] == 0.0) continue;
+            for (index_t i = prev + 1; i <= rows[k]; ++i) rp[static_cast<std::size_t>(i)] = static_cast<index_t>(p);
+            prev = rows[k];
+            ci[p] = cols[k];
+            v[p] = vals[k];
+            ++p;
+        }
+    });
+    index_t lr = -1;
+    for (int t = T - 1; t >= 0 && lr < 0; --t) lr = last_row[static_cast<std::size_t>(t)];
+    for (index_t i = lr + 1; i <= m; ++i) rp[static_cast<std::size_t>(i)] = static_cast<index_t>(total);
+    return CsrMatrix::from_csr(m, n, std::move(rp), std::move(ci), std::move(v));
 }
 
 Residuals residuals(const CsrMatrix& A, std::span<const double> x, std::span<const double> b) {

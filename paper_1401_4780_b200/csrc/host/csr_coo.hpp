@@ -1,0 +1,13 @@
+// CSR from coordinate arrays (the pybind drop-in path): from_triplets'
+// semantics (ref csr.cpp:9-63: bounds, duplicates, zero values dropped, row
+// norms) without the intermediate Triplet vector, with the passes over the
+// entries in parallel when the input is already in (row, column) order.
+#pragma once
+#include <cstddef>
+
+#include "asyrk/csr.hpp"
+
+namespace asyrk {
+CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
+                       std::size_t nnz);
+}

@@ -283,3 +283,19 @@ def test_trace_serializers_match_the_reference_bytes(tmp_path):
             assert a == b
     assert ours_j == ref_j
     assert ours_c == ref_c
+
+
+def test_csr_from_coo_matches_from_triplets(tmp_path):
+    # the pybind drop-in path assembles the CSR straight from the coordinate
+    # arrays (host/csr_coo.hpp, parallel passes when already sorted): same
+    # arrays and row norms as CsrMatrix::from_triplets (ref csr.cpp:9-63), or the
+    # same error, on sorted / unsorted / zero-valued / out-of-range / duplicate input
+    import subprocess
+
+    exe = str(tmp_path / "csr_coo_check")
+    lib = os.path.join(ROOT, "paper_1401_4780_b200")
+    subprocess.run(["g++", "-std=gnu++20", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "csr_coo_check.cpp"), "-o", exe, "-L", lib, "-lasyrk_b200",
+                    f"-Wl,-rpath,{lib}"], check=True, capture_output=True)
+    out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    assert out.startswith("ok 24"), out
