@@ -129,7 +129,6 @@ py::dict solve_parallel_core(index_t m, index_t n, const Arr<index_t>& rows, con
                              double gamma, index_t epochs, double target, std::uint64_t seed,
                              const std::string& variant, const std::string& sampling, index_t snapshot_interval,
                              int precision, bool instrumented, const std::vector<double>* x_star) {
-    CsrMatrix A0 = triplets_to_csr(m, n, rows, cols, vals);
     DeviceOptions dev;
     dev.precision = precision;
     dev.norm_proportional = sampling == "norm" || sampling == "norm-proportional";
@@ -138,10 +137,13 @@ py::dict solve_parallel_core(index_t m, index_t n, const Arr<index_t>& rows, con
     CsrMatrix A;
     std::vector<double> bn;
     if (dev.norm_proportional) {
-        A = std::move(A0);
+        A = triplets_to_csr(m, n, rows, cols, vals);
         bn = b;
     } else {
-        auto pr = normalize_rows(A0, b);
+        if (rows.size() != cols.size() || rows.size() != vals.size())
+            fail(ErrorCode::DimensionMismatch, "triplet lists differ in length");
+        // triplets -> CSR -> normalize_rows, the arrays scaled in place (host/csr_coo.hpp)
+        auto pr = csr_from_coo_normalized(m, n, rows.data(), cols.data(), vals.data(), rows.size(), b);
         A = std::move(pr.first);
         bn = std::move(pr.second);
     }

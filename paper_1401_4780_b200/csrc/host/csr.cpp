@@ -249,8 +249,17 @@ std::pair<CsrMatrix, std::vector<double>> normalize_rows(const CsrMatrix& A, std
     return {std::move(N), std::move(nb)};
 }
 
-CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
-                       std::size_t nnz) {
+namespace {
+struct CooArrays {
+    std::vector<index_t> rp, ci;
+    std::vector<double> v;
+};
+
+// CSR arrays from coordinates already in strictly increasing (row, column)
+// order (false: another order — the caller takes the reference path); bounds
+// are checked first either way, as from_triplets does
+bool assemble_sorted_coo(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
+                         std::size_t nnz, CooArrays& out) {
     if (m < 1 || n < 1) fail(ErrorCode::InvalidArgument, "matrix dimensions must be positive");
     const int T = par::threads_for(nnz);
     // per chunk: first out-of-range entry, and whether (row, col) strictly increases
@@ -275,19 +284,18 @@ CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t*
         if (k != SIZE_MAX)
             fail(ErrorCode::IndexOutOfRange, "triplet (" + std::to_string(rows[k]) + "," + std::to_string(cols[k]) +
                                                  ") outside " + std::to_string(m) + "x" + std::to_string(n));
-    if (!std::all_of(sorted.begin(), sorted.end(), [](char c) { return c != 0; })) {
-        // general order: the reference path (counting sort by row, duplicates rejected)
-        std::vector<Triplet> t(nnz);
-        for (std::size_t k = 0; k < nnz; ++k) t[k] = Triplet{rows[k], cols[k], vals[k]};
-        return CsrMatrix::from_triplets(t, m, n);
-    }
+    if (!std::all_of(sorted.begin(), sorted.end(), [](char c) { return c != 0; })) return false;
     // (row, column) order with no repeats — the common case, e.g. triplets taken
     // from a CSR: zero values dropped as from_triplets does, chunks write their
     // kept entries at prefix offsets and the row starts they cross
     for (int t = 0; t < T; ++t) kept[static_cast<std::size_t>(t) + 1] += kept[static_cast<std::size_t>(t)];
     const std::size_t total = kept[static_cast<std::size_t>(T)];
-    std::vector<index_t> rp(static_cast<std::size_t>(m) + 1), ci(total);
-    std::vector<double> v(total);
+    std::vector<index_t>& rp = out.rp;
+    std::vector<index_t>& ci = out.ci;
+    std::vector<double>& v = out.v;
+    rp.resize(static_cast<std::size_t>(m) + 1);
+    ci.resize(total);
+    v.resize(total);
     // the row of the last kept entry before each chunk (-1: none)
     std::vector<index_t> last_row(static_cast<std::size_t>(T), -1);
     par::chunks(nnz, T, [&](int t, std::size_t lo, std::size_t hi) {
@@ -315,7 +323,66 @@ CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t*
     index_t lr = -1;
     for (int t = T - 1; t >= 0 && lr < 0; --t) lr = last_row[static_cast<std::size_t>(t)];
     for (index_t i = lr + 1; i <= m; ++i) rp[static_cast<std::size_t>(i)] = static_cast<index_t>(total);
-    return CsrMatrix::from_csr(m, n, std::move(rp), std::move(ci), std::move(v));
+    return true;
+}
+
+CsrMatrix coo_reference_path(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
+                             std::size_t nnz) {
+    // general order: counting sort by row, duplicates rejected (from_triplets)
+    std::vector<Triplet> t(nnz);
+    for (std::size_t k = 0; k < nnz; ++k) t[k] = Triplet{rows[k], cols[k], vals[k]};
+    return CsrMatrix::from_triplets(t, m, n);
+}
+}  // namespace
+
+CsrMatrix csr_from_coo(index_t m, index_t n, const index_t* rows, const index_t* cols, const double* vals,
+                       std::size_t nnz) {
+    CooArrays c;
+    if (!assemble_sorted_coo(m, n, rows, cols, vals, nnz, c)) return coo_reference_path(m, n, rows, cols, vals, nnz);
+    return CsrMatrix::from_csr(m, n, std::move(c.rp), std::move(c.ci), std::move(c.v));
+}
+
+std::pair<CsrMatrix, std::vector<double>> csr_from_coo_normalized(index_t m, index_t n, const index_t* rows,
+                                                                  const index_t* cols, const double* vals,
+                                                                  std::size_t nnz, std::span<const double> b) {
+    CooArrays c;
+    if (!assemble_sorted_coo(m, n, rows, cols, vals, nnz, c))
+        return normalize_rows(coo_reference_path(m, n, rows, cols, vals, nnz), b);
+    // normalize_rows on the arrays in place (no copy of A): the row norm as
+    // compute_norms forms it, unit rows left bit-identical, the others scaled;
+    // from_csr then re-forms every norm from the final values, as normalize_rows does
+    const bool b_ok = b.empty() || static_cast<index_t>(b.size()) == m;
+    std::vector<double> nb;
+    if (b_ok) nb.assign(b.begin(), b.end());
+    const int T = par::threads_for(c.v.size());
+    std::vector<index_t> first_empty(static_cast<std::size_t>(T), -1), first_zero(static_cast<std::size_t>(T), -1);
+    par::chunks(static_cast<std::size_t>(m), T, [&](int t, std::size_t lo, std::size_t hi) {
+        for (std::size_t i = lo; i < hi; ++i) {
+            const index_t kb = c.rp[i], ke = c.rp[i + 1];
+            if (kb == ke) {
+                if (first_empty[static_cast<std::size_t>(t)] < 0) first_empty[static_cast<std::size_t>(t)] = static_cast<index_t>(i);
+                continue;
+            }
+            double ss = 0.0;
+            for (index_t k = kb; k < ke; ++k) ss += c.v[static_cast<std::size_t>(k)] * c.v[static_cast<std::size_t>(k)];
+            const double nrm = std::sqrt(ss);
+            if (nrm == 0.0) {
+                if (first_zero[static_cast<std::size_t>(t)] < 0) first_zero[static_cast<std::size_t>(t)] = static_cast<index_t>(i);
+                continue;
+            }
+            if (std::abs(nrm - 1.0) <= CsrMatrix::kNormTol) continue;
+            for (index_t k = kb; k < ke; ++k) c.v[static_cast<std::size_t>(k)] /= nrm;
+            if (!nb.empty()) nb[i] /= nrm;
+        }
+    });
+    for (index_t z : first_empty)  // from_triplets' compute_norms error comes first, then normalize_rows' checks
+        if (z >= 0) fail(ErrorCode::ZeroRow, "row " + std::to_string(z) + " has no nonzeros");
+    if (!b_ok) fail(ErrorCode::DimensionMismatch, "normalize_rows: b has wrong length");
+    for (index_t z : first_zero)
+        if (z >= 0) fail(ErrorCode::ZeroRow, "row " + std::to_string(z) + " has zero norm");
+    CsrMatrix N = CsrMatrix::from_csr(m, n, std::move(c.rp), std::move(c.ci), std::move(c.v));
+    N.flag_normalized();
+    return {std::move(N), std::move(nb)};
 }
 
 Residuals residuals(const CsrMatrix& A, std::span<const double> x, std::span<const double> b) {

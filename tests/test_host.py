@@ -298,4 +298,4 @@ def test_csr_from_coo_matches_from_triplets(tmp_path):
                     os.path.join(ROOT, "tests", "cpp", "csr_coo_check.cpp"), "-o", exe, "-L", lib, "-lasyrk_b200",
                     f"-Wl,-rpath,{lib}"], check=True, capture_output=True)
     out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
-    assert out.startswith("ok 24"), out
+    assert out.startswith("ok 48"), out
