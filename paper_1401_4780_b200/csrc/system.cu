@@ -350,8 +350,6 @@ void free_all(asyrk_system* s) {
     flag_release(s->host_flag);
     mirror_release(s->mirror);
     s->mirror = nullptr;
-    scalar_put(s->host_scalar);  // (its last reads were synchronous)
-    s->host_scalar = nullptr;
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
         F(s->pick_dev[k]);
@@ -363,6 +361,8 @@ void free_all(asyrk_system* s) {
     for (int q = 0; q < 2; ++q) F(s->xs_base[q] ? s->xs_base[q] : s->xs[q]);
     if (s->mstream) cudaStreamSynchronize(s->mstream);
     if (s->stream) cudaStreamSynchronize(s->stream);  // pool frees are stream-ordered
+    scalar_put(s->host_scalar);  // after the streams: no copy into it can still be in flight
+    s->host_scalar = nullptr;
     destroy_det_streams(s);
     if (kit_put(s)) return;
     if (s->ev_begin) cudaEventDestroy(s->ev_begin);
