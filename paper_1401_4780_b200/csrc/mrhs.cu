@@ -18,6 +18,7 @@
 // ||R||_F^2, ||G||_F^2, ||X - X*||_F^2 in fp64. The partials are what a
 // multi-GPU caller all-reduces (NCCL) before the stop decision.
 #include <cstdlib>
+#include "env.h"
 
 #include "kernels.h"
 
@@ -973,7 +974,7 @@ bool mrhs_rowpar(int kl) {
 template <int KL>
 static const void* mrhs_worker_fn(uint32_t max_len) {
     static const int rows_env = getenv("ASYRK_MRHS_ROWS") ? atoi(getenv("ASYRK_MRHS_ROWS")) : 0;
-    static const bool nostream = getenv("ASYRK_MRHS_NOSTREAM") != nullptr;
+    static const bool nostream = env_flag("ASYRK_MRHS_NOSTREAM");
     static const int minb = getenv("ASYRK_MRHS_MINB") ? atoi(getenv("ASYRK_MRHS_MINB")) : 4;
     const int rows = rows_env > 0 ? rows_env : mrhs_default_rows(KL);
     static const int batched = getenv("ASYRK_MRHS_BATCH") ? atoi(getenv("ASYRK_MRHS_BATCH")) : 0;

@@ -1,5 +1,6 @@
 // Host runtime of the C ABI (runtime.h).
 #include <chrono>
+#include "env.h"
 #include "runtime.h"
 #include "layout.cuh"
 
@@ -114,7 +115,7 @@ void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* d
     std::lock_guard<std::mutex> lk(mu_);
     const size_t per_chunk = chunk_ / out_elem;
     const size_t total = out_bytes / out_elem;
-    static const bool prof = getenv("ASYRK_STAGE_PROFILE") != nullptr;  // diagnostics: fill vs wait
+    static const bool prof = env_flag("ASYRK_STAGE_PROFILE");  // diagnostics: fill vs wait
     double t_wait = 0.0, t_fill = 0.0;
     const auto t_start = std::chrono::steady_clock::now();
     for (size_t e0 = 0; e0 < total; e0 += per_chunk) {
@@ -147,7 +148,7 @@ void Stager::pipeline(size_t out_bytes, size_t out_elem, cudaStream_t s, char* d
 }
 
 static bool have_avx2() {
-    static const bool ok = stage_nt_supported() && !getenv("ASYRK_NO_NT_STAGING");
+    static const bool ok = stage_nt_supported() && !env_flag("ASYRK_NO_NT_STAGING");
     return ok;
 }
 
@@ -213,13 +214,13 @@ void Stager::upload_narrow(int32_t* dst, const int64_t* src, size_t count, cudaS
 
 static bool pool_debug() {
     static int d = -1;
-    if (d < 0) d = getenv("ASYRK_DEBUG_POOL") ? 1 : 0;
+    if (d < 0) d = env_flag("ASYRK_DEBUG_POOL") ? 1 : 0;
     return d == 1;
 }
 
 static bool no_pool() {
     static int d = -1;
-    if (d < 0) d = getenv("ASYRK_NO_POOL") ? 1 : 0;
+    if (d < 0) d = env_flag("ASYRK_NO_POOL") ? 1 : 0;
     return d == 1;
 }
 
@@ -252,7 +253,7 @@ cudaError_t pool_alloc(void** p, size_t bytes, cudaStream_t s) {
         configured.fetch_or(bit, std::memory_order_relaxed);
     }
     const cudaError_t e = no_pool() ? cudaMalloc(p, bytes ? bytes : 1) : cudaMallocAsync(p, bytes ? bytes : 1, s);
-    static const bool dbg = getenv("ASYRK_DEBUG_POOL") != nullptr;
+    static const bool dbg = env_flag("ASYRK_DEBUG_POOL");
     if (dbg) fprintf(stderr, "[pool] alloc %p %zu\n", *p, bytes);
     return e;
 }

@@ -22,6 +22,7 @@
 // the all-reduced one — so every rank computes the same schedule.
 #pragma once
 #include <cmath>
+#include "env.h"
 #include <cstdlib>
 
 namespace ak {
@@ -36,7 +37,7 @@ struct MonitorSchedule {
     void reset(double tgt, bool every_boundary) {
         target = tgt;
         static const long long env_gap = getenv("ASYRK_MONITOR_MAX_GAP") ? atoll(getenv("ASYRK_MONITOR_MAX_GAP")) : 16;
-        static const bool env_every = getenv("ASYRK_MONITOR_EVERY") != nullptr;
+        static const bool env_every = env_flag("ASYRK_MONITOR_EVERY");
         max_gap = env_gap > 0 ? env_gap : 1;
         every = every_boundary || env_every || !(tgt > 0.0);
         b_prev = b_last = -1;

@@ -9,6 +9,7 @@
 // and polls a mapped pinned flag; chunks enqueued after the stop decision
 // exit at their first instruction. No host round trip sits between epochs.
 #include <algorithm>
+#include "env.h"
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -511,7 +512,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     AllocStream alloc_on(s->stream);
     s->host_scalar = scalar_take();
     // ASYRK_PROFILE_CREATE=1: synchronized phase times on stderr (diagnostics)
-    static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
+    static const bool prof = env_flag("ASYRK_PROFILE_CREATE");
     auto t_prev = std::chrono::steady_clock::now();
     auto phase = [&](const char* what) {
         if (!prof) return;
@@ -946,7 +947,7 @@ void resolve_stats(asyrk_system* s) {
 
 // ASYRK_PROFILE_SOLVE=1: host timestamps of the async solve's phases on stderr (diagnostics)
 struct SolveClock {
-    bool on = getenv("ASYRK_PROFILE_SOLVE") != nullptr;
+    bool on = env_flag("ASYRK_PROFILE_SOLVE");
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
     void mark(const char* what) const {
         if (on)
@@ -1247,10 +1248,10 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     // the workers of the other boundaries run back to back. ASYRK_OVERLAP=1
     // selects the round-1 driver instead (a monitor of every boundary it can
     // take, on its own stream, overlapped with the next epochs).
-    static const bool overlap_env = getenv("ASYRK_OVERLAP") != nullptr;
+    static const bool overlap_env = env_flag("ASYRK_OVERLAP");
     if (!sp.det && !overlap_env)
         return run_scheduled(s, sp, wa, E, prec, max_chunks, launches, trace, instr);
-    static const bool no_overlap = getenv("ASYRK_NO_OVERLAP") != nullptr;
+    static const bool no_overlap = env_flag("ASYRK_NO_OVERLAP");
     // (instrumented runs keep the in-stream monitor: restoring the stopping
     // snapshot would desynchronize x from the shadow increments)
     // The deterministic path overlaps too: its exact monitor (serial sums,
@@ -1258,13 +1259,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     // stream while the next chunk runs; a chunk that ran past the stopping
     // boundary is undone by restoring that snapshot, so records and the
     // returned iterate are the in-order ones (bit-identical either way).
-    static const bool no_det_overlap = getenv("ASYRK_NO_DET_OVERLAP") != nullptr;
+    static const bool no_det_overlap = env_flag("ASYRK_NO_DET_OVERLAP");
     const bool overlap = !no_overlap && !instr && (!sp.det || !no_det_overlap);
     if (overlap && !s->mstream) {
         // highest priority: monitor blocks take SM slots ahead of queued worker blocks
         int lo = 0, hi = 0;
         CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        static const bool low_prio = getenv("ASYRK_MON_LOWPRIO") != nullptr;
+        static const bool low_prio = env_flag("ASYRK_MON_LOWPRIO");
         CK(cudaStreamCreateWithPriority(&s->mstream, cudaStreamNonBlocking, low_prio ? lo : hi));
         for (int q = 0; q < 2; ++q) {
             CK(cudaEventCreateWithFlags(&s->snap_ev[q], cudaEventDisableTiming));
@@ -1276,7 +1277,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     // record_every_boundary (or ASYRK_EXACT_RECORDS=1): a record at every boundary
     // (the workers wait for the monitor); default: the monitor takes the latest
     // boundary it can, like the reference's coordinator, and the workers never wait
-    static const bool exact_env = getenv("ASYRK_EXACT_RECORDS") != nullptr;
+    static const bool exact_env = env_flag("ASYRK_EXACT_RECORDS");
     const bool exact_records = exact_env || sp.every_boundary || sp.det;  // deterministic: every boundary
     // boundary 0 (x0): the overlapped modes take it through the same snapshot ->
     // monitor-stream path as every later boundary, so the first workers start
@@ -1458,7 +1459,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         CK(cudaMemcpyAsync(s->host_scalar, &s->st->stop_slot, sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         std::memcpy(&stop_slot, s->host_scalar, sizeof(int));
-        static const bool always_final = getenv("ASYRK_ALWAYS_FINAL_RECORD") != nullptr;
+        static const bool always_final = env_flag("ASYRK_ALWAYS_FINAL_RECORD");
         if (stop_slot < 0 || always_final) {
             MonitorArgs fa = monitor_args(s, sp.det, 0, sp.x_star != nullptr);
             fa.force = 1;
@@ -2316,7 +2317,7 @@ asyrk_status asyrk_solve_parallel(const asyrk_csr_view* A, const double* b, cons
                                   asyrk_instrument_out* instrument) {
     if (!cfg) return fail(ASYRK_E_InvalidArgument, "null config");
     return guarded([&] {
-        static const bool prof = getenv("ASYRK_PROFILE_CREATE") != nullptr;
+        static const bool prof = env_flag("ASYRK_PROFILE_CREATE");
         const auto t0 = std::chrono::steady_clock::now();
         asyrk_status s;
         {
@@ -2516,7 +2517,7 @@ asyrk_status mrhs_create_impl(const asyrk_csr_view* A, const float* B, int64_t k
     h->B = dalloc<float>((size_t)s->m * kl);
     // the monitor's G = A^T R: scattered by the rows pass into G (n x kl, default:
     // one pass over A, no CSC gather of R), or gathered from R over the CSC
-    static const bool csc_monitor = getenv("ASYRK_MRHS_CSC_MONITOR") != nullptr;
+    static const bool csc_monitor = env_flag("ASYRK_MRHS_CSC_MONITOR");
     if (csc_monitor)
         h->R = dalloc<float>((size_t)s->m * kl);
     else
