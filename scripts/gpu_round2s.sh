@@ -2,12 +2,12 @@
 set -u
 mkdir -p gpurun_out
 : > gpurun_out/ab_det.txt
-L=paper_1401_4780_b200/libasyrk_b200.so
-for P in 0 2 4 8 16 32; do
-  echo "poll $P" >> gpurun_out/ab_det.txt
-  ASYRK_DET_POLL_NS=$P timeout 300 python scripts/ab_det.py $L reassoc >> gpurun_out/ab_det.txt 2>&1
+for rep in 1 2; do
+for L in scripts/r02c/libasyrk_b200.so paper_1401_4780_b200/libasyrk_b200.so; do
+  timeout 120 python scripts/ab_det.py $L reassoc >> gpurun_out/ab_det.txt 2>&1
+  timeout 120 python scripts/ab_det.py $L >> gpurun_out/ab_det.txt 2>&1
 done
-for P in 8 16 32 48; do
-  echo "poll $P" >> gpurun_out/ab_det.txt
-  ASYRK_DET_POLL_NS=$P timeout 300 python scripts/ab_det.py $L >> gpurun_out/ab_det.txt 2>&1
+echo "dual" >> gpurun_out/ab_det.txt
+ASYRK_DET_DUAL=1 timeout 120 python scripts/ab_det.py paper_1401_4780_b200/libasyrk_b200.so reassoc >> gpurun_out/ab_det.txt 2>&1
+ASYRK_DET_DUAL=1 timeout 120 python scripts/ab_det.py paper_1401_4780_b200/libasyrk_b200.so >> gpurun_out/ab_det.txt 2>&1
 done
