@@ -55,6 +55,7 @@ struct asyrk_system {
     uint32_t max_len = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
+    int dev = 0;  // the device current at create: frees and the stream / scratch pools are per device
 
     // layout
     unsigned char* rec = nullptr;
@@ -295,6 +296,18 @@ void destroy_det_streams(asyrk_system* s) {
 }
 
 void free_all(asyrk_system* s) {
+    // on the system's device (the caller may have another one current), so the
+    // frees and the pooled streams / events land on the right device
+    struct DeviceGuard {
+        int prev = -1;
+        explicit DeviceGuard(int d) {
+            if (cudaGetDevice(&prev) == cudaSuccess && prev != d) cudaSetDevice(d);
+            else prev = -1;
+        }
+        ~DeviceGuard() {
+            if (prev >= 0) cudaSetDevice(prev);
+        }
+    } on_device(s->dev);
     if (s->bstream) {
         aux_stream_put(s->bstream);  // synchronizes it
         s->bstream = nullptr;
@@ -498,6 +511,7 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     if (v) return v;
     if (precision < 0 || precision > 2) return fail(ASYRK_E_InvalidArgument, "unknown precision");
     auto s = std::make_unique<asyrk_system>();
+    CK(cudaGetDevice(&s->dev));
     s->m = A->m;
     s->n = A->n;
     s->nnz = A->nnz;
