@@ -97,7 +97,7 @@ static int stager_threads() {
 Stager::Stager() : pool_(stager_threads()) {
     if (const char* e = getenv("ASYRK_STAGE_CHUNK_KB")) chunk_ = std::max<size_t>(64, strtoull(e, nullptr, 10)) << 10;
     for (int k = 0; k < kSlots; ++k) {
-        if (cudaHostAlloc((void**)&slot_[k], chunk_, cudaHostAllocDefault) != cudaSuccess)
+        if (cudaHostAlloc((void**)&slot_[k], chunk_, cudaHostAllocPortable) != cudaSuccess)
             throw std::runtime_error("pinned staging allocation failed");
         cudaEventCreateWithFlags(&ev_[k], cudaEventDisableTiming);
     }
@@ -275,7 +275,7 @@ constexpr int kFlags = 1024;
 int* flag_acquire(int** dev_ptr) {
     std::lock_guard<std::mutex> lk(g_flag_mu);
     if (!g_flag_host) {
-        if (cudaHostAlloc((void**)&g_flag_host, kFlags * sizeof(int), cudaHostAllocMapped) != cudaSuccess)
+        if (cudaHostAlloc((void**)&g_flag_host, kFlags * sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
             return nullptr;
         cudaHostGetDevicePointer((void**)&g_flag_dev, g_flag_host, 0);
         for (int k = kFlags - 1; k >= 0; --k) g_flag_free.push_back(k);
@@ -304,7 +304,7 @@ std::vector<int> g_mirror_free;
 HostMirror* mirror_acquire(HostMirror** dev_ptr) {
     std::lock_guard<std::mutex> lk(g_mirror_mu);
     if (!g_mirror_host) {
-        if (cudaHostAlloc((void**)&g_mirror_host, kMirrors * sizeof(HostMirror), cudaHostAllocMapped) != cudaSuccess)
+        if (cudaHostAlloc((void**)&g_mirror_host, kMirrors * sizeof(HostMirror), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
             return nullptr;
         cudaHostGetDevicePointer((void**)&g_mirror_dev, g_mirror_host, 0);
         std::memset(g_mirror_host, 0, kMirrors * sizeof(HostMirror));
