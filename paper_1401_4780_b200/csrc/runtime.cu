@@ -13,6 +13,8 @@
 
 namespace ak {
 
+constexpr int kMaxDevices = 64;  // per-device caches and pools
+
 ThreadPool::ThreadPool(int n) {
     for (int t = 1; t < n; ++t) {
         workers_.emplace_back([this, t] {
@@ -103,9 +105,16 @@ Stager::Stager() : pool_(stager_threads()) {
     }
 }
 
+// one Stager per device: its events (and the DMA streams it is used with)
+// belong to that device; process lifetime (pinned memory freed at exit)
 Stager& Stager::get() {
-    static Stager* s = new Stager();  // process lifetime (pinned memory freed at exit)
-    return *s;
+    static std::mutex mu;
+    static Stager* per[kMaxDevices] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!per[dev]) per[dev] = new Stager();
+    return *per[dev];
 }
 
 // Fill pinned chunks with fill(dst_chunk, first_elem, n_elems, thread, nthreads)
@@ -223,8 +232,6 @@ static bool no_pool() {
     if (d < 0) d = env_flag("ASYRK_NO_POOL") ? 1 : 0;
     return d == 1;
 }
-
-constexpr int kMaxDevices = 64;
 
 int current_sm_count() {
     static std::atomic<int> cache[kMaxDevices];
