@@ -2668,6 +2668,23 @@ void mrhs_maybe_monitor(asyrk_mrhs* h) {
     CK(cudaGetLastError());
 }
 
+// the last solve's event times (its events are untouched until the next solve)
+void mrhs_resolve_stats(asyrk_mrhs* h) {
+    if (h->stats_timed < 0) return;
+    asyrk_system* s = h->sys;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
+    h->stats.solve_ms = ms;
+    double wms = 0.0;
+    for (long long t = 0; t < h->stats_timed; ++t) {
+        float w = 0.f;
+        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+        wms += w;
+    }
+    h->stats.worker_ms = wms;
+    h->stats_timed = -1;
+}
+
 asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out) {
     asyrk_system* s = h->sys;
     cudaStream_t st = s->stream;
@@ -2926,21 +2943,7 @@ asyrk_status asyrk_mrhs_max_resident_warps(const asyrk_mrhs* h, int32_t* out) {
 asyrk_status asyrk_mrhs_last_stats(const asyrk_mrhs* h, asyrk_solve_stats* out) {
     if (!h || !out) return fail(ASYRK_E_InvalidArgument, "null argument");
     return guarded([&] {
-        asyrk_mrhs* hm = const_cast<asyrk_mrhs*>(h);
-        if (hm->stats_timed >= 0) {  // the last solve's event times (its events are untouched until the next)
-            asyrk_system* s = hm->sys;
-            float ms = 0.f;
-            CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
-            hm->stats.solve_ms = ms;
-            double wms = 0.0;
-            for (long long t = 0; t < hm->stats_timed; ++t) {
-                float w = 0.f;
-                CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
-                wms += w;
-            }
-            hm->stats.worker_ms = wms;
-            hm->stats_timed = -1;
-        }
+        mrhs_resolve_stats(const_cast<asyrk_mrhs*>(h));
         *out = h->stats;
         return ASYRK_OK;
     });
@@ -3050,7 +3053,10 @@ asyrk_status asyrk_mrhs_solve_devices(const asyrk_csr_view* A, const float* B, i
                 if (!st && X_out)
                     for (int64_t j = 0; j < h->sys->n; ++j)
                         std::memcpy(X_out + j * k_total + g * kl, &xl[(size_t)(j * kl)], (size_t)kl * sizeof(float));
-                if (!st && stats && g == 0) *stats = h->stats;
+                if (!st && stats && g == 0) {
+                    mrhs_resolve_stats(h);
+                    *stats = h->stats;
+                }
             }
         } catch (...) {
             cleanup();
