@@ -207,6 +207,8 @@ def test_solve_devices_single_process():
     devs = list(range(min(torch.cuda.device_count(), 2)))
     t = capi.mrhs_solve_devices(A, B, devs, threads=1024, epochs=400, target=TOL * TOL * bb, seed=3, X_star=Xs)
     assert np.sqrt(t["r_sq"][-1] / bb) <= TOL
+    st = t["stats"]  # device 0's timings and counts
+    assert st["solve_ms"] > 0.0 and 0.0 < st["worker_ms"] <= st["solve_ms"] and st["worker_launches"] >= 1
     R = _residual(A, t["X"], B)
     assert np.sqrt((R * R).sum() / bb) <= 2 * TOL
     assert np.linalg.norm(t["X"] - Xs) / np.linalg.norm(Xs) <= 10 * TOL
