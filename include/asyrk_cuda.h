@@ -309,6 +309,9 @@ asyrk_status asyrk_system_multiply(asyrk_system* sys, const double* x, double* y
 asyrk_status asyrk_system_multiply_transpose(asyrk_system* sys, const double* x, double* y);
 asyrk_status asyrk_system_power_iteration(asyrk_system* sys, double tol, int64_t max_iters, double* lambda_max,
                                           int64_t* iterations);
+/* Counts and device timings of the last solve on this system; the timings are
+ * read from its CUDA events here (not inside the solve call), valid until the
+ * next solve. */
 asyrk_status asyrk_system_last_stats(const asyrk_system* sys, asyrk_solve_stats* out);
 /* simulate / monte_carlo_ratios on a resident fp64 system (b = the system's). */
 asyrk_status asyrk_system_simulate(asyrk_system* sys, const double* x0, const asyrk_sim_config* cfg,
