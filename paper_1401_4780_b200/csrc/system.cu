@@ -105,6 +105,8 @@ struct asyrk_system {
     int* host_flag_dev = nullptr;
     HostMirror* mirror = nullptr;  // pinned mapped: latest record for the host-driven monitor schedule
     HostMirror* mirror_dev = nullptr;
+    HostMirror* mirror0 = nullptr;  // record 0 taken beside the first workers (its own, so it is never overwritten)
+    HostMirror* mirror0_dev = nullptr;
     void* host_scalar = nullptr;   // pinned scratch (kPinBytes): small device -> host reads, the final state + records
     long long pin_recs = -1;       // records of the last solve already copied into host_scalar (-1: none)
     // the monitor's structures (row / column SELL, plain CSC) finish on bstream
@@ -363,6 +365,8 @@ void free_all(asyrk_system* s) {
     }
     flag_release(s->host_flag);
     mirror_release(s->mirror);
+    mirror_release(s->mirror0);
+    s->mirror0 = nullptr;
     s->mirror = nullptr;
     for (int k = 0; k <= kLookahead; ++k) {
         F(s->seq_dev[k]);
@@ -791,7 +795,8 @@ asyrk_status create_impl(const asyrk_csr_view* A, const double* b, int32_t preci
     s->host_flag = flag_acquire(&s->host_flag_dev);
     if (!s->host_flag) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned stop flag available")};
     s->mirror = mirror_acquire(&s->mirror_dev);
-    if (!s->mirror) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned record mirror available")};
+    s->mirror0 = mirror_acquire(&s->mirror0_dev);
+    if (!s->mirror || !s->mirror0) throw CudaFail{fail(ASYRK_E_TooLarge, "no pinned record mirror available")};
     ensure_records(s.get(), 256);
     ensure_events(s.get());
     phase("solve buffers");
@@ -1041,7 +1046,12 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     const bool side0 = prec != P_F32 && max_chunks > 0 && !instr;  // (an audit must see every increment)
     MonitorSchedule sch;
     sch.reset(sp.target, sp.every_boundary);
-    long long pending = 0;   // boundary whose record the host has not read yet (-1: none)
+    // boundary whose record (main mirror) the host has not read yet (-1: none);
+    // with side0, record 0 (its own mirror) is read together with record 1: the
+    // evaluation of boundary 1 is unconditional, so it and the next worker are
+    // enqueued at once instead of after the host has seen record 0
+    long long pending = side0 ? -1 : 0;
+    bool r0_pending = side0;
     long long next_mon = 1;  // next boundary to evaluate
     long long timed = 0;
     auto enqueue_worker = [&](long long b) {  // chunk b: boundary b -> b + 1
@@ -1072,11 +1082,11 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         enqueue_worker(0);  // first: the GPU starts on the workers while the host enqueues record 0
         CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[0], 0));
         mon_wait(s, s->mstream);
+        std::memset(s->mirror0, 0, sizeof(HostMirror));
         MonitorArgs m0 = monitor_args(s, false, 0, xs);
         m0.x = s->x0d;
-        m0.mirror = s->mirror_dev;
+        m0.mirror = s->mirror0_dev;
         launch_monitor(m0, prec, s->mstream);
-        CK(cudaEventRecord(ev_rec, s->mstream));
         CK(cudaEventRecord(s->mon_ev[0], s->mstream));
     } else {
         mon_wait(s, st);
@@ -1094,18 +1104,24 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         // here the worker of chunk b (b -> b + 1) is enqueued; read the pending
         // record while it runs, then place the next evaluation
         if (pending >= 0) {
+            if (r0_pending) {  // record 0 first (long done: boundary 1's evaluation waited for it)
+                CK(cudaEventSynchronize(s->mon_ev[0]));
+                r0_pending = false;
+                const volatile HostMirror* h0 = s->mirror0;
+                if (h0->stop) {
+                    // x0 met the target (or was non-finite) while the first workers
+                    // already ran (their later launches and record 1 skip on the device's
+                    // stop): the solve returns x0 (epoch 0, no updates)
+                    CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
+                    launch_x_init(s->x0d, s->x, s->n, prec, st);
+                    break;
+                }
+                sch.push(0, h0->r_sq);
+            }
             CK(cudaEventSynchronize(ev_rec));
             solve_mark("record read");
             const volatile HostMirror* hm = s->mirror;
-            if (hm->stop) {  // the enqueued worker sees go = 0 and exits
-                if (pending == 0 && side0) {
-                    // x0 met the target (or was non-finite) while the first workers
-                    // already ran: the solve returns x0 (epoch 0, no updates)
-                    CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
-                    launch_x_init(s->x0d, s->x, s->n, prec, st);
-                }
-                break;
-            }
+            if (hm->stop) break;  // the enqueued worker sees go = 0 and exits
             next_mon = sch.push(pending, hm->r_sq);
             pending = -1;
         }
@@ -1126,6 +1142,14 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         }
         if (b1 < max_chunks) enqueue_worker(b1);
         CK(cudaGetLastError());
+    }
+    if (r0_pending) {  // a one-chunk solve ends before the loop reads record 0
+        CK(cudaEventSynchronize(s->mon_ev[0]));
+        const volatile HostMirror* h0 = s->mirror0;
+        if (h0->stop) {
+            CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
+            launch_x_init(s->x0d, s->x, s->n, prec, st);
+        }
     }
     solve_mark("loop done");
     CK(cudaEventRecord(s->ev_end, st));
