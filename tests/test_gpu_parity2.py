@@ -288,3 +288,24 @@ def test_sigma_sorted_columns_bitwise():
     ref = oracle.C.rk_solve(Ao, b, np.zeros(n), 3, seed=5)
     for k in ("r_sq", "grad_sq", "final_x"):
         assert np.array_equal(t[k], ref[k]), k
+
+
+@pytest.mark.parametrize("epochs", [1, 50])
+def test_async_solve_x0_meets_target(epochs):
+    # record 0 (of x0, taken beside the first worker launch, read with record 1 —
+    # system.cu run_scheduled): when x0 already meets the target the solve
+    # returns x0 with one record at epoch 0 and no updates, whatever ran after it
+    # on the device; a one-chunk solve takes the same path after its loop
+    A, b, xs = capi.generate_fixed_theta(20000, 10000, 20, seed=31)
+    bb = float(b @ b)
+    with capi.System(A, b) as S:
+        W = S.max_resident_warps()
+        t = S.solve(x0=xs, threads=W, epochs=epochs, target=1e-6 * bb, seed=1)
+        assert list(t["epoch_index"]) == [0]
+        assert int(t["updates_applied"][-1]) == 0
+        assert np.array_equal(t["final_x"], xs)
+        # from zero, a one-epoch budget records boundaries 0 and 1 and applies m updates
+        t = S.solve(threads=W, epochs=1, target=1e-6 * bb, seed=1)
+        assert list(t["epoch_index"]) == [0, 1]
+        assert int(t["updates_applied"][-1]) == A.m
+        assert t["r_sq"][1] < t["r_sq"][0] == pytest.approx(bb, rel=1e-12)
