@@ -385,7 +385,11 @@ def run_gpu(args):
     # ---- config 5 (the sharded configuration) at this N: k = 64 RHS split over the ranks
     c5 = None
     if not args.no_cfg5:
-        c5 = cfg5_sharded(max(2, min(args.steps, 5)), 1, dist, rank, world, local, stream)
+        try:  # a failure here must not cost the headline line
+            c5 = cfg5_sharded(max(2, min(args.steps, 5)), 1, dist, rank, world, local, stream)
+        except Exception as e:  # noqa: BLE001
+            c5 = {"error": f"{type(e).__name__}: {e}"}
+            print(f"[rank {rank}] cfg5_sharded failed: {c5['error']}", file=sys.stderr, flush=True)
 
     out = None
     if rank == 0:
