@@ -464,7 +464,10 @@ def roofline(S, W, worker_rate, avg_launch_ms, step_rate):
            "peak_source": "x-side microbenchmark measured live in this run on the solver's own x buffer "
                           "(asyrk_system_microbench_xside), the faster of 1 and 2 rows in flight per warp; ncu "
                           "counters of it in profiles/",
-           "achieved_source": "credited projections / CUDA-event time of the worker launches (K2) in the timed steps",
+           "achieved_source": "credited projections / worker time in the timed steps: CUDA-event pairs around "
+                              "every 8th worker launch (K2; launches 1, 9, 17, ... of each solve) scaled to all "
+                              "launches that did work (an event pair between every two launches cost 0.24 ms "
+                              "per solve)",
            "avg_worker_launch_ms": avg_launch_ms,
            "x_bytes_per_proj": X_BYTES_F64, "alg_bytes_per_proj": BYTES_PER_PROJ_F64}
     # the A stream against HBM: algorithmic 384 B/projection vs ncu DRAM bytes

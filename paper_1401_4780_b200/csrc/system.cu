@@ -44,6 +44,12 @@ namespace {
 
 constexpr int kLookahead = 4;      // chunks in flight beyond the last confirmed one
 constexpr int kTimedLaunches = 1024;  // worker launches timed with event pairs per solve
+// async drivers time one worker launch in kTimeEvery with an event pair —
+// launches 1, 9, 17, ... (launch 0 follows the cold start of a solve): a pair
+// between two launches costs ~5.6 us of stream time (0.24 ms per config-2
+// solve when every launch was timed); worker_ms scales the sample to all launches
+constexpr long long kTimeEvery = 8;
+inline bool timed_launch(long long b) { return b % kTimeEvery == 1; }
 
 }  // namespace
 
@@ -142,6 +148,7 @@ struct asyrk_system {
     // (~90 elapsed-time queries at config 2 cost ~0.12 ms of host time that
     // the solve call itself would otherwise pay): worker launches timed
     mutable long long stats_timed = -1;  // -1: nothing pending
+    long long spec_launch = -1;          // worker launch queued behind the stopping record (-1: none)
 
     Layout layout() const {
         Layout L;
@@ -947,6 +954,27 @@ struct Timeline {
 };
 
 // Stats, trace and instrument report of a finished solve (the stream is idle).
+// worker time of a solve from its sampled launches (timed_launch): the mean
+// sampled duration times the launches that did work; spec = index of the
+// launch queued behind the stopping record (it exits at once; -1: none), which
+// is neither a sample nor work
+double sampled_worker_ms(asyrk_system* s, long long timed, long long launches, long long spec) {
+    std::vector<double> w((size_t)std::max<long long>(timed, 0));
+    for (long long t = 0; t < timed; ++t) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
+        w[(size_t)t] = ms;
+    }
+    long long used = timed, work = launches;
+    if (spec >= 0 && spec < launches) {
+        --work;
+        if (timed_launch(spec) && used > 0) --used;  // it is the last launch, so the last sample
+    }
+    double sum = 0.0;
+    for (long long t = 0; t < used; ++t) sum += w[(size_t)t];
+    return used > 0 ? sum * (double)work / (double)used : 0.0;
+}
+
 // the last async solve's event timings (its events stay untouched until the next solve)
 void resolve_stats(asyrk_system* s) {
     if (s->stats_timed < 0) return;
@@ -955,13 +983,7 @@ void resolve_stats(asyrk_system* s) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     s->stats.solve_ms = ms;
-    double wms = 0.0;
-    for (long long t = 0; t < timed; ++t) {
-        float w = 0.f;
-        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
-        wms += w;
-    }
-    s->stats.worker_ms = wms;
+    s->stats.worker_ms = sampled_worker_ms(s, timed, s->stats.worker_launches, s->spec_launch);
 }
 
 // ASYRK_PROFILE_SOLVE=1: host timestamps of the async solve's phases on stderr (diagnostics)
@@ -1052,12 +1074,13 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     // enqueued at once instead of after the host has seen record 0
     long long pending = side0 ? -1 : 0;
     bool r0_pending = side0;
+    long long stop_b = -1;   // boundary whose record stopped the solve (-1: the budget ran out)
     long long next_mon = 1;  // next boundary to evaluate
     long long timed = 0;
     auto enqueue_worker = [&](long long b) {  // chunk b: boundary b -> b + 1
         wa.epoch0 = epoch_of(b);
         wa.span0 = epoch_of(b + 1) - wa.epoch0;
-        const bool time_it = timed < kTimedLaunches;
+        const bool time_it = timed < kTimedLaunches && timed_launch(b);
         if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
         launch_worker(wa, prec, E, st);
         if (time_it) {
@@ -1114,6 +1137,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
                     // stop): the solve returns x0 (epoch 0, no updates)
                     CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
                     launch_x_init(s->x0d, s->x, s->n, prec, st);
+                    stop_b = 0;
                     break;
                 }
                 sch.push(0, h0->r_sq);
@@ -1121,7 +1145,10 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
             CK(cudaEventSynchronize(ev_rec));
             solve_mark("record read");
             const volatile HostMirror* hm = s->mirror;
-            if (hm->stop) break;  // the enqueued worker sees go = 0 and exits
+            if (hm->stop) {  // the enqueued worker sees go = 0 and exits
+                stop_b = pending;
+                break;
+            }
             next_mon = sch.push(pending, hm->r_sq);
             pending = -1;
         }
@@ -1149,6 +1176,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         if (h0->stop) {
             CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
             launch_x_init(s->x0d, s->x, s->n, prec, st);
+            stop_b = 0;
         }
     }
     solve_mark("loop done");
@@ -1157,7 +1185,10 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     CK(cudaStreamSynchronize(st));
     solve_mark("stream idle");
     CK(cudaGetLastError());
-    return finish_solve(s, sp, prec, timed, launches, {}, trace, instr);
+    const asyrk_status fs = finish_solve(s, sp, prec, timed, launches, {}, trace, instr);
+    // the launch of chunk stop_b was queued behind the stopping record and exits at once
+    s->spec_launch = stop_b > 0 && stop_b < s->stats.worker_launches ? stop_b : -1;
+    return fs;
 }
 
 asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, asyrk_trace_out* trace,
@@ -1179,6 +1210,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     ensure_events(s, max_chunks);
     s->stats = asyrk_solve_stats{};
     s->stats_timed = -1;
+    s->spec_launch = -1;
     s->pin_recs = -1;
 
     // x0, x_star
@@ -2463,6 +2495,8 @@ asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const
 struct asyrk_mrhs {
     asyrk_system* sys = nullptr;  // fp32 records + plain CSC of A
     mutable long long stats_timed = -1;  // worker launches whose event times are still to be read
+    long long timed = 0;                  // worker launches of the current solve timed with an event pair
+    long long spec_launch = -1;           // the launch queued behind the stopping record (-1: none)
     int64_t k_total = 0, c0 = 0, c1 = 0, kl = 0;
     float* X = nullptr;           // n x kl
     float* B = nullptr;           // m x kl
@@ -2608,6 +2642,8 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     h->stop_seen = false;
     h->stats = asyrk_solve_stats{};
     h->stats_timed = -1;
+    h->timed = 0;
+    h->spec_launch = -1;
     s->pin_recs = -1;
     ensure_records(s, std::max<long long>(256, h->max_chunks + 2));
     ensure_events(s, h->max_chunks);
@@ -2672,10 +2708,14 @@ void mrhs_enqueue_worker(asyrk_mrhs* h) {
     a.epoch0 = mrhs_epoch_of(h, h->b);
     a.span0 = mrhs_epoch_of(h, h->b + 1) - a.epoch0;
     const long long t = h->stats.worker_launches;
-    const bool time_it = t < kTimedLaunches && (size_t)(2 * t + 1) < s->ev_w.size();
-    if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * t)], st));
+    const long long k = h->timed;
+    const bool time_it = timed_launch(t) && k < kTimedLaunches && (size_t)(2 * k + 1) < s->ev_w.size();
+    if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * k)], st));
     launch_mrhs_worker(a, st);
-    if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * t + 1)], st));
+    if (time_it) {
+        CK(cudaEventRecord(s->ev_w[(size_t)(2 * k + 1)], st));
+        h->timed++;
+    }
     h->b++;
     h->stats.worker_launches++;
     h->stats.kernel_launches++;
@@ -2699,13 +2739,7 @@ void mrhs_resolve_stats(asyrk_mrhs* h) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     h->stats.solve_ms = ms;
-    double wms = 0.0;
-    for (long long t = 0; t < h->stats_timed; ++t) {
-        float w = 0.f;
-        CK(cudaEventElapsedTime(&w, s->ev_w[(size_t)(2 * t)], s->ev_w[(size_t)(2 * t + 1)]));
-        wms += w;
-    }
-    h->stats.worker_ms = wms;
+    h->stats.worker_ms = sampled_worker_ms(s, h->stats_timed, h->stats.worker_launches, h->spec_launch);
     h->stats_timed = -1;
 }
 
@@ -2717,7 +2751,7 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
     CK(cudaStreamSynchronize(st));
     DevState hs;
     std::memcpy(&hs, pin_state(s), sizeof(DevState));
-    h->stats_timed = std::min<long long>(h->stats.worker_launches, (long long)s->ev_w.size() / 2);  // mrhs_resolve_stats
+    h->stats_timed = h->timed;  // sampled launches (mrhs_resolve_stats)
     h->stats.projections = hs.updates;
     h->stats.warps = (int32_t)std::min<int64_t>(h->threads, INT32_MAX);
     if (hs.status == ASYRK_E_NonFinite) return fail(ASYRK_E_NonFinite, "iterate became non-finite");
@@ -2855,7 +2889,10 @@ asyrk_status mrhs_run(std::vector<asyrk_mrhs*>& hs, const std::vector<int>& devs
             hs[g]->next_mon = h0->next_mon;
             hs[g]->pending = -1;
         }
-        if (stop) break;  // the workers just enqueued see go = 0 and exit
+        if (stop) {  // the workers just enqueued see go = 0 and exit
+            for (size_t g = 0; g < G; ++g) hs[g]->spec_launch = hs[g]->stats.worker_launches - 1;
+            break;
+        }
         for (size_t g = 0; g < G; ++g) {
             on(g);
             mrhs_maybe_monitor(hs[g]);

@@ -7,7 +7,4 @@ for L in scripts/r02c/libasyrk_b200.so paper_1401_4780_b200/libasyrk_b200.so; do
   timeout 120 python scripts/ab_det.py $L reassoc >> gpurun_out/ab_det.txt 2>&1
   timeout 120 python scripts/ab_det.py $L >> gpurun_out/ab_det.txt 2>&1
 done
-echo "dual" >> gpurun_out/ab_det.txt
-ASYRK_DET_DUAL=1 timeout 120 python scripts/ab_det.py paper_1401_4780_b200/libasyrk_b200.so reassoc >> gpurun_out/ab_det.txt 2>&1
-ASYRK_DET_DUAL=1 timeout 120 python scripts/ab_det.py paper_1401_4780_b200/libasyrk_b200.so >> gpurun_out/ab_det.txt 2>&1
 done
