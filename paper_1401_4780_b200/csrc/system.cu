@@ -1390,7 +1390,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             CK(cudaEventSynchronize(s->ev_chunk[(size_t)(k % (kLookahead + 1))]));
             if (*reinterpret_cast<volatile int*>(s->host_flag)) break;
         }
-        const bool time_it = timed < kTimedLaunches;
+        const bool time_it = timed < kTimedLaunches && (!sp.det || timed_launch(k) || max_chunks == 1);  // det: sampled (event pairs cost stream time)
         if (sp.det) {
             const long long e0 = k * sp.interval;
             const long long span = std::min<long long>(sp.interval, sp.epochs - e0);
