@@ -851,7 +851,13 @@ void write_trace(asyrk_system* s, const DevState& hs, asyrk_trace_out* trace, in
     }
     if (trace->final_x) {
         launch_x_export(s->x, s->xd, s->n, precision, s->stream);
-        Stager::get().download(trace->final_x, s->xd, (size_t)s->n * 8, s->stream);  // through the pinned slots
+        const size_t xb = (size_t)s->n * 8;
+        if (xb >= (8u << 20)) {
+            Stager::get().download(trace->final_x, s->xd, xb, s->stream);  // large: through the pinned slots
+        } else {  // small (config 2: 0.8 MB): one pageable copy is quicker than the bounce
+            CK(cudaMemcpyAsync(trace->final_x, s->xd, xb, cudaMemcpyDeviceToHost, s->stream));
+            CK(cudaStreamSynchronize(s->stream));
+        }
     }
 }
 
@@ -2774,7 +2780,16 @@ asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_ou
             if (trace->updates_applied) trace->updates_applied[i] = r.updates;
         }
     }
-    if (X_out) Stager::get().download(X_out, h->X, (size_t)s->n * h->kl * sizeof(float), st);
+    if (X_out) {
+        const size_t xb = (size_t)s->n * h->kl * sizeof(float);
+        static const bool plain = env_flag("ASYRK_PLAIN_DOWNLOAD");  // (A/B)
+        if (xb >= (8u << 20) && !plain) {
+            Stager::get().download(X_out, h->X, xb, st);  // large: through the pinned slots
+        } else {
+            CK(cudaMemcpyAsync(X_out, h->X, xb, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
     return ASYRK_OK;
 }
 
