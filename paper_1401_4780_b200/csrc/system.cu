@@ -1278,7 +1278,7 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
         // waiting warps back off between polls so they leave issue slots to the running
         // events (bitwise mode: 16 ns, 21.37 vs 21.44 ms at 32 ns; tolerance mode: spinning, 12.23 vs
-        // 12.6 ms with any back-off — scripts/gpu_round2s.sh)
+        // 12.6 ms with any back-off — scripts/ab_det.py under ASYRK_DET_POLL_NS)
         static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
         da.poll_ns = poll_env >= 0 ? poll_env : (sp.reassoc ? 0 : 16);
         da.max_len = s->max_len;
