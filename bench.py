@@ -1073,7 +1073,19 @@ def run_cfg5_shards(args):
     return 0
 
 
+def _json_stdout():
+    """The driver reads ONE JSON line from stdout, but native libraries print to
+    file descriptor 1 on their own (NCCL's version banner when the box sets
+    NCCL_DEBUG, its INFO log at N > 1): point fd 1 at stderr for everything else
+    and give Python's print a private duplicate of the real stdout."""
+    sys.stdout.flush()
+    real = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(real, "w", buffering=1)
+
+
 def main():
+    _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
