@@ -65,7 +65,6 @@ struct DetArgs {
     double* ev_rcp;               // per event: RN(1 / ev_nn), the division's reciprocal
     long long* dbg;               // optional per-event phase timestamps (diagnostics)
     int poll_ns;                  // dataflow polling back-off (0: spin)
-    int deficit_ns;               // extra back-off per missing update beyond the next one (0: off)
     uint32_t max_len;             // longest row (picks the dataflow kernel's elements per lane)
     // deterministic multi-RHS (asyrk_system_rk_solve_multi): ncols > 1 runs one
     // CTA per right-hand side over the same event sequence / prepass; column c's
@@ -74,29 +73,12 @@ struct DetArgs {
     int ncols;
     const double* b_cols;
     int reassoc;                  // 1: warp-tree dot, reciprocal coefficient, fused update (tolerance mode)
-    // coefficient forwarding (tolerance mode, det.cu det_forward_kernel): per
-    // event its latest in-chunk predecessor P and G = a_P . a_q; per pair the
-    // value of the column's previous update when that update is P's (need
-    // carries kDetFlagP then); coef = per-event coefficients (fallback copy)
-    int forward;                  // 1: det_forward_kernel (the prepass below runs when forward or crit_poll)
-    int crit_poll;                // dataflow kernel: poll the latest predecessor's column first (needs the prepass flags)
-    int ring_mask;                // coefficient ring slots - 1 (power of two, >= 31)
-    const double* ev_pval;
-    const int32_t* ev_p;
-    const double* ev_g;
-    double* coef;
 };
-constexpr int32_t kDetFlagP = 1 << 30;
-// forwarding kernel: ring slots that fit beside x (double-buffered) and the
-// per-column state counters for n columns, 0 if it does not fit
-int det_forward_ring(long long n);
 void launch_det(const DetArgs& a, int n_smem_x, cudaStream_t s);
 bool det_fits_smem(long long n);
 struct DetPrep {
     int32_t *keys, *vals, *keys_s, *vals_s, *start;
     double *ev_val, *ev_b, *ev_nn, *ev_rcp;
-    double *ev_pval, *ev_g, *coef;  // coefficient forwarding (per pair / per event / per event)
-    int32_t* ev_p;
     void* temp;
     size_t temp_bytes;
 };

@@ -369,10 +369,6 @@ void free_all(asyrk_system* s) {
         F(s->prep[h].ev_b);
         F(s->prep[h].ev_nn);
         F(s->prep[h].ev_rcp);
-        F(s->prep[h].ev_pval);
-        F(s->prep[h].ev_g);
-        F(s->prep[h].coef);
-        F(s->prep[h].ev_p);
     }
     flag_release(s->host_flag);
     mirror_release(s->mirror);
@@ -458,13 +454,8 @@ void ensure_seq(asyrk_system* s, size_t count) {
     for (int h = 0; h < 2; ++h) {
         DetPrep& P = s->prep[h];
         for (void* p : {(void*)s->need[h], (void*)P.keys, (void*)P.vals, (void*)P.keys_s, (void*)P.vals_s,
-                        (void*)P.start, P.temp, (void*)P.ev_val, (void*)P.ev_b, (void*)P.ev_nn, (void*)P.ev_rcp,
-                        (void*)P.ev_pval, (void*)P.ev_g, (void*)P.coef, (void*)P.ev_p})
+                        (void*)P.start, P.temp, (void*)P.ev_val, (void*)P.ev_b, (void*)P.ev_nn, (void*)P.ev_rcp})
             pool_free(p, s->stream);
-        P.ev_pval = dalloc<double>(pairs);
-        P.ev_g = dalloc<double>(count);
-        P.coef = dalloc<double>(count);
-        P.ev_p = dalloc<int32_t>(count);
         s->need[h] = dalloc<int32_t>(pairs);
         P.ev_val = dalloc<double>(pairs);
         P.ev_b = dalloc<double>(count);
@@ -1285,26 +1276,13 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
         da.gamma = sp.gamma;
         da.full_row = sp.full_row ? 1 : 0;
         da.x_in_smem = (det_fits_smem(s->n) && s->max_len <= 128) ? 1 : 0;
-        // waiting warps back off between polls so they leave issue slots to the running
-        // events (bitwise mode: 16 ns, 21.37 vs 21.44 ms at 32 ns; tolerance mode: spinning, 12.23 vs
-        // 12.6 ms with any back-off — scripts/ab_det.py under ASYRK_DET_POLL_NS)
+        // waiting warps spin: any polling back-off costs more than the issue slots
+        // it frees (config 1, profiles/r02_det_forward_grid.txt: bitwise 21.0 ms
+        // spinning vs 21.3 at 16 ns; tolerance mode 12.15 vs 12.6 — ASYRK_DET_POLL_NS)
         static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
-        da.poll_ns = poll_env >= 0 ? poll_env : (sp.reassoc ? 0 : 16);
-        static const int deficit_env = getenv("ASYRK_DET_DEFICIT_NS") ? atoi(getenv("ASYRK_DET_DEFICIT_NS")) : 0;
-        da.deficit_ns = deficit_env;
+        da.poll_ns = poll_env >= 0 ? poll_env : 0;
         da.max_len = s->max_len;
         da.reassoc = sp.reassoc ? 1 : 0;
-        // tolerance mode: coefficient forwarding where x fits double-buffered
-        // (ASYRK_DET_FORWARD=0 keeps the reassociated dataflow kernel, for A/B runs)
-        {
-            static const bool fwd = env_flag("ASYRK_DET_FORWARD");
-            static const bool no_crit = getenv("ASYRK_DET_CRIT") && std::string(getenv("ASYRK_DET_CRIT")) == "0";
-            const int R = det_forward_ring(s->n);
-            da.forward = (sp.reassoc && sp.full_row && !instr && da.x_in_smem && R > 0 && fwd &&
-                          !getenv("ASYRK_DET_DEBUG")) ? 1 : 0;
-            da.ring_mask = R > 0 ? R - 1 : 0;
-            da.crit_poll = (da.x_in_smem && !da.forward && !no_crit) ? 1 : 0;
-        }
         if (!s->pstream) {
             CK(cudaStreamCreateWithFlags(&s->pstream, cudaStreamNonBlocking));
             for (int h = 0; h < 2; ++h) {
@@ -1455,10 +1433,6 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
             da.ev_b = s->prep[h].ev_b;
             da.ev_nn = s->prep[h].ev_nn;
             da.ev_rcp = s->prep[h].ev_rcp;
-            da.ev_pval = s->prep[h].ev_pval;
-            da.ev_g = s->prep[h].ev_g;
-            da.ev_p = s->prep[h].ev_p;
-            da.coef = s->prep[h].coef;
             long long pairs = (long long)cnt * (long long)s->uniform_len;
             da.flat_off = nullptr;
             if (!s->uniform) {  // ragged rows: offsets of each event's (event, nonzero) pairs
@@ -1746,7 +1720,7 @@ asyrk_status rk_multi_impl(asyrk_system* s, const double* B, int64_t k, const do
     da.full_row = 1;
     da.x_in_smem = (det_fits_smem(n) && s->max_len <= 128) ? 1 : 0;
     static const int poll_env = getenv("ASYRK_DET_POLL_NS") ? atoi(getenv("ASYRK_DET_POLL_NS")) : -1;
-    da.poll_ns = poll_env >= 0 ? poll_env : (c->det_reassociate ? 0 : 16);
+    da.poll_ns = poll_env >= 0 ? poll_env : 0;
     da.max_len = s->max_len;
     da.ncols = (int)k;
     da.b_cols = Bc;
