@@ -149,6 +149,10 @@ struct asyrk_system {
     // the solve call itself would otherwise pay): worker launches timed
     mutable long long stats_timed = -1;  // -1: nothing pending
     long long spec_launch = -1;          // worker launch queued behind the stopping record (-1: none)
+    // scheduled async solves: epochs of work of each worker launch (0: the launch
+    // behind the stopping record) and its event pair (-1: not timed)
+    std::vector<long long> lw_epochs;
+    std::vector<long long> lw_pair;
 
     Layout layout() const {
         Layout L;
@@ -989,6 +993,20 @@ void resolve_stats(asyrk_system* s) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     s->stats.solve_ms = ms;
+    if (!s->lw_epochs.empty()) {  // scheduled solve: timed launches' ms per epoch x all epochs of work
+        double t_ms = 0.0, t_ep = 0.0, all_ep = 0.0;
+        for (size_t i = 0; i < s->lw_epochs.size(); ++i) {
+            all_ep += (double)s->lw_epochs[i];
+            const long long p = s->lw_pair[i];
+            if (p < 0 || s->lw_epochs[i] <= 0) continue;
+            float lm = 0.f;
+            CK(cudaEventElapsedTime(&lm, s->ev_w[(size_t)(2 * p)], s->ev_w[(size_t)(2 * p + 1)]));
+            t_ms += lm;
+            t_ep += (double)s->lw_epochs[i];
+        }
+        s->stats.worker_ms = t_ep > 0.0 ? t_ms * all_ep / t_ep : 0.0;
+        return;
+    }
     s->stats.worker_ms = sampled_worker_ms(s, timed, s->stats.worker_launches, s->spec_launch);
 }
 
@@ -1083,12 +1101,28 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     long long stop_b = -1;   // boundary whose record stopped the solve (-1: the budget ran out)
     long long next_mon = 1;  // next boundary to evaluate
     long long timed = 0;
-    auto enqueue_worker = [&](long long b) {  // chunk b: boundary b -> b + 1
+    // Worker launches: boundary b -> b_end in one launch. Between the boundary
+    // after an evaluation and the next scheduled evaluation no record is taken,
+    // so those chunks run as ONE launch (each warp walks its slice once per
+    // epoch without waiting for the others at the unrecorded boundaries, as the
+    // reference's workers do, parallel.cpp:306-373; the launch still ends
+    // exactly at the next evaluated boundary): config 2 runs ~10 launches for 42
+    // epochs instead of 43, without the drain and ramp of every epoch. The
+    // launch behind an evaluation is one chunk (the gap after it is not known
+    // until the host has read the record). Fused launches and the first launch
+    // of a solve are timed with event pairs; worker_ms = their ms per epoch x
+    // all epochs of work (resolve_stats).
+    s->lw_epochs.clear();
+    s->lw_pair.clear();
+    static const bool no_fuse = env_flag("ASYRK_NO_FUSE");
+    auto enqueue_worker = [&](long long b, long long b_end) {
         wa.epoch0 = epoch_of(b);
-        wa.span0 = epoch_of(b + 1) - wa.epoch0;
-        const bool time_it = timed < kTimedLaunches && timed_launch(b);
+        wa.span0 = epoch_of(b_end) - wa.epoch0;
+        const bool time_it = timed < kTimedLaunches && (b_end - b > 1 || timed_launch(b));
         if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed)], st));
         launch_worker(wa, prec, E, st);
+        s->lw_epochs.push_back(wa.span0);
+        s->lw_pair.push_back(time_it ? timed : -1);
         if (time_it) {
             CK(cudaEventRecord(s->ev_w[(size_t)(2 * timed + 1)], st));
             ++timed;
@@ -1108,7 +1142,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         }
         launch_state_init(s->st, sp.epochs, sp.interval, sp.target, st, /*go=*/1);
         CK(cudaEventRecord(s->snap_ev[0], st));
-        enqueue_worker(0);  // first: the GPU starts on the workers while the host enqueues record 0
+        enqueue_worker(0, 1);  // first: the GPU starts on the workers while the host enqueues record 0
         CK(cudaStreamWaitEvent(s->mstream, s->snap_ev[0], 0));
         mon_wait(s, s->mstream);
         std::memset(s->mirror0, 0, sizeof(HostMirror));
@@ -1123,7 +1157,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
         m0.mirror = s->mirror_dev;
         launch_monitor(m0, prec, st);
         CK(cudaEventRecord(ev_rec, st));
-        if (max_chunks > 0) enqueue_worker(0);
+        if (max_chunks > 0) enqueue_worker(0, 1);
     }
     launches += side0 ? 3 : 2;
     s->stats.monitor_launches++;
@@ -1144,6 +1178,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
                     CK(cudaStreamWaitEvent(st, s->mon_ev[0], 0));
                     launch_x_init(s->x0d, s->x, s->n, prec, st);
                     stop_b = 0;
+                    for (auto& e : s->lw_epochs) e = 0;  // (their updates are discarded)
                     break;
                 }
                 sch.push(0, h0->r_sq);
@@ -1153,6 +1188,7 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
             const volatile HostMirror* hm = s->mirror;
             if (hm->stop) {  // the enqueued worker sees go = 0 and exits
                 stop_b = pending;
+                if (!s->lw_epochs.empty()) s->lw_epochs.back() = 0;
                 break;
             }
             next_mon = sch.push(pending, hm->r_sq);
@@ -1173,7 +1209,12 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
             CK(cudaEventRecord(ev_rec, st));
             pending = b1;
         }
-        if (b1 < max_chunks) enqueue_worker(b1);
+        if (b1 < max_chunks) {
+            // no record unread: the next evaluation is known, run up to it in one launch
+            const long long b_end = (pending < 0 && !no_fuse) ? std::min(std::max(next_mon, b1 + 1), max_chunks) : b1 + 1;
+            enqueue_worker(b1, b_end);
+            b = b_end - 2;  // (++b: the next iteration handles boundary b_end)
+        }
         CK(cudaGetLastError());
     }
     if (r0_pending) {  // a one-chunk solve ends before the loop reads record 0
@@ -1192,8 +1233,8 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     solve_mark("stream idle");
     CK(cudaGetLastError());
     const asyrk_status fs = finish_solve(s, sp, prec, timed, launches, {}, trace, instr);
-    // the launch of chunk stop_b was queued behind the stopping record and exits at once
-    s->spec_launch = stop_b > 0 && stop_b < s->stats.worker_launches ? stop_b : -1;
+    // the launch queued behind the stopping record exits at once (lw_epochs 0)
+    s->spec_launch = stop_b > 0 ? s->stats.worker_launches - 1 : -1;
     return fs;
 }
 
@@ -1218,6 +1259,8 @@ asyrk_status run_solve(asyrk_system* s, const double* x0, const SolveSpec& sp, a
     s->stats_timed = -1;
     s->spec_launch = -1;
     s->pin_recs = -1;
+    s->lw_epochs.clear();  // (filled by the scheduled driver only)
+    s->lw_pair.clear();
 
     // x0, x_star
     if (x0) CK(cudaMemcpyAsync(s->x0d, x0, (size_t)s->n * 8, cudaMemcpyHostToDevice, st));
@@ -2503,6 +2546,7 @@ struct asyrk_mrhs {
     mutable long long stats_timed = -1;  // worker launches whose event times are still to be read
     long long timed = 0;                  // worker launches of the current solve timed with an event pair
     long long spec_launch = -1;           // the launch queued behind the stopping record (-1: none)
+    std::vector<long long> lw_epochs, lw_pair;  // mrhs_run: epochs of work / event pair of each worker launch
     int64_t k_total = 0, c0 = 0, c1 = 0, kl = 0;
     float* X = nullptr;           // n x kl
     float* B = nullptr;           // m x kl
@@ -2674,6 +2718,8 @@ asyrk_status mrhs_begin_impl(asyrk_mrhs* h, const asyrk_run_config* cfg, const f
     }
     *s->host_flag = 0;
     std::memset(s->mirror, 0, sizeof(HostMirror));
+    h->lw_epochs.clear();
+    h->lw_pair.clear();
     CK(cudaEventRecord(s->ev_begin, st));
     launch_state_init(s->st, cfg->epochs, cfg->snapshot_interval, cfg->target_r_sq, st);
     launch_mrhs_monitor(mrhs_args(h), st);  // initial residual -> norms (this shard)
@@ -2706,23 +2752,32 @@ bool mrhs_read_pending(asyrk_mrhs* h) {
     return h->stop_seen;
 }
 
-// workers of chunk b (boundary b -> b + 1)
-void mrhs_enqueue_worker(asyrk_mrhs* h) {
+// workers of chunks b .. b_end - 1 in one launch (boundary b -> b_end; b_end <= 0:
+// one chunk). mrhs_run fuses the chunks up to the next scheduled evaluation as
+// run_scheduled does (per-launch epochs in lw_epochs; those launches and the
+// sampled single ones are timed)
+void mrhs_enqueue_worker(asyrk_mrhs* h, long long b_end = 0, bool track = false) {
     asyrk_system* s = h->sys;
     cudaStream_t st = s->stream;
+    if (b_end <= h->b) b_end = h->b + 1;
     MrhsArgs a = mrhs_args(h);
     a.epoch0 = mrhs_epoch_of(h, h->b);
-    a.span0 = mrhs_epoch_of(h, h->b + 1) - a.epoch0;
+    a.span0 = mrhs_epoch_of(h, b_end) - a.epoch0;
     const long long t = h->stats.worker_launches;
     const long long k = h->timed;
-    const bool time_it = timed_launch(t) && k < kTimedLaunches && (size_t)(2 * k + 1) < s->ev_w.size();
+    const bool time_it = (timed_launch(t) || (track && b_end - h->b > 1)) && k < kTimedLaunches &&
+                         (size_t)(2 * k + 1) < s->ev_w.size();
     if (time_it) CK(cudaEventRecord(s->ev_w[(size_t)(2 * k)], st));
     launch_mrhs_worker(a, st);
+    if (track) {
+        h->lw_epochs.push_back(a.span0);
+        h->lw_pair.push_back(time_it ? k : -1);
+    }
     if (time_it) {
         CK(cudaEventRecord(s->ev_w[(size_t)(2 * k + 1)], st));
         h->timed++;
     }
-    h->b++;
+    h->b = b_end;
     h->stats.worker_launches++;
     h->stats.kernel_launches++;
     CK(cudaGetLastError());
@@ -2745,8 +2800,23 @@ void mrhs_resolve_stats(asyrk_mrhs* h) {
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, s->ev_begin, s->ev_end));
     h->stats.solve_ms = ms;
-    h->stats.worker_ms = sampled_worker_ms(s, h->stats_timed, h->stats.worker_launches, h->spec_launch);
+    const long long timed = h->stats_timed;
     h->stats_timed = -1;
+    if (!h->lw_epochs.empty()) {  // mrhs_run: timed launches' ms per epoch x all epochs of work
+        double t_ms = 0.0, t_ep = 0.0, all_ep = 0.0;
+        for (size_t i = 0; i < h->lw_epochs.size(); ++i) {
+            all_ep += (double)h->lw_epochs[i];
+            const long long p = h->lw_pair[i];
+            if (p < 0 || h->lw_epochs[i] <= 0) continue;
+            float lm = 0.f;
+            CK(cudaEventElapsedTime(&lm, s->ev_w[(size_t)(2 * p)], s->ev_w[(size_t)(2 * p + 1)]));
+            t_ms += lm;
+            t_ep += (double)h->lw_epochs[i];
+        }
+        h->stats.worker_ms = t_ep > 0.0 ? t_ms * all_ep / t_ep : 0.0;
+        return;
+    }
+    h->stats.worker_ms = sampled_worker_ms(s, timed, h->stats.worker_launches, h->spec_launch);
 }
 
 asyrk_status mrhs_finish_impl(asyrk_mrhs* h, asyrk_trace_out* trace, float* X_out) {
@@ -2891,10 +2961,16 @@ asyrk_status mrhs_run(std::vector<asyrk_mrhs*>& hs, const std::vector<int>& devs
     }
     commit_all();  // boundary 0
     asyrk_mrhs* h0 = hs[0];
+    static const bool no_fuse = env_flag("ASYRK_NO_FUSE");
     while (h0->b < h0->max_chunks) {
+        // with every record read, the next evaluation is known: one launch up to it
+        // (the same on every shard and rank: the schedule follows the all-reduced records)
+        const long long b_end = (h0->pending < 0 && !no_fuse)
+                                    ? std::min(std::max(h0->next_mon, h0->b + 1), h0->max_chunks)
+                                    : h0->b + 1;
         for (size_t g = 0; g < G; ++g) {
             on(g);
-            mrhs_enqueue_worker(hs[g]);
+            mrhs_enqueue_worker(hs[g], b_end, true);
         }
         // the record of the last commit (if any) is read while these workers run
         on(0);
@@ -2905,7 +2981,10 @@ asyrk_status mrhs_run(std::vector<asyrk_mrhs*>& hs, const std::vector<int>& devs
             hs[g]->pending = -1;
         }
         if (stop) {  // the workers just enqueued see go = 0 and exit
-            for (size_t g = 0; g < G; ++g) hs[g]->spec_launch = hs[g]->stats.worker_launches - 1;
+            for (size_t g = 0; g < G; ++g) {
+                hs[g]->spec_launch = hs[g]->stats.worker_launches - 1;
+                if (!hs[g]->lw_epochs.empty()) hs[g]->lw_epochs.back() = 0;
+            }
             break;
         }
         for (size_t g = 0; g < G; ++g) {
