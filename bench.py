@@ -393,7 +393,9 @@ def run_gpu(args):
 
     out = None
     if rank == 0:
-        avg_launch_ms = w_ms / max(w_launch, 1)
+        # worker time per epoch of work (launches span several epochs: the chunks
+        # between two scheduled evaluations run as one launch)
+        avg_launch_ms = w_ms / max(sum(epochs), 1)
         worker_rate = proj / (w_ms * 1e-3)  # credited projections / worker time: discarded epochs count as time
         out = {
             "metric": METRIC, "value": value, "unit": "proj/s", "n_gpus": world, "steps": args.steps,
@@ -465,16 +467,18 @@ def roofline(S, W, worker_rate, avg_launch_ms, step_rate):
                           "(asyrk_system_microbench_xside), the faster of 1 and 2 rows in flight per warp; ncu "
                           "counters of it in profiles/",
            "achieved_source": "credited projections / worker time in the timed steps: CUDA-event pairs around "
-                              "every 8th worker launch (K2; launches 1, 9, 17, ... of each solve) scaled to all "
-                              "launches that did work (an event pair between every two launches cost 0.24 ms "
-                              "per solve)",
-           "avg_worker_launch_ms": avg_launch_ms,
+                              "each multi-epoch worker launch (K2: the epochs between two scheduled evaluations "
+                              "run as one launch) and a sample of the one-epoch ones; their ms per epoch times "
+                              "all epochs of work",
+           "avg_worker_epoch_ms": avg_launch_ms,
            "x_bytes_per_proj": X_BYTES_F64, "alg_bytes_per_proj": BYTES_PER_PROJ_F64}
     # the A stream against HBM: algorithmic 384 B/projection vs ncu DRAM bytes
     alg_launch = S_A_F64 * CFG2["m"]
     out["hbm"] = {"achieved": alg_launch / (avg_launch_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s",
                   "frac": alg_launch / (avg_launch_ms * 1e-3) / 1e9 / peak_hbm, "peak_source": hbm_kind,
-                  "alg_bytes_per_launch": alg_launch, "dram_bytes_per_launch": dram,
+                  "alg_bytes_per_epoch": alg_launch, "dram_bytes_per_epoch": dram,
+                  "dram_source": "ncu --set full of one-epoch worker launches (ASYRK_NO_FUSE=1: same kernel, one "
+                                 "epoch per launch)",
                   "traffic_over_alg": (dram / alg_launch) if dram else None,
                   "source": ncu.get("source") if ncu else None}
     return out

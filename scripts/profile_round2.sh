@@ -16,7 +16,8 @@ CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cfg5"
 $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launch list rc=$?"
-ncu --set full --clock-control none --import-source on -k regex:"worker_kernel|rows_kernel|cols_final_kernel" -s 200 -c 3 -o gpurun_out/full $CMD > gpurun_out/ncu_full.log 2>&1
+# one epoch per worker launch for the capture (ASYRK_NO_FUSE=1), so its DRAM bytes are per epoch
+ASYRK_NO_FUSE=1 ncu --set full --clock-control none --import-source on -k regex:"worker_kernel|rows_kernel|cols_final_kernel" -s 200 -c 3 -o gpurun_out/full $CMD > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
 python scripts/probe_xside.py ncu > gpurun_out/xside_plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:xside_kernel -c 4 -o gpurun_out/xside python scripts/probe_xside.py ncu > gpurun_out/ncu_xside.log 2>&1
