@@ -309,3 +309,25 @@ def test_async_solve_x0_meets_target(epochs):
         assert list(t["epoch_index"]) == [0, 1]
         assert int(t["updates_applied"][-1]) == A.m
         assert t["r_sq"][1] < t["r_sq"][0] == pytest.approx(bb, rel=1e-12)
+
+
+def test_scheduled_solve_fuses_unrecorded_epochs():
+    # the epochs between two scheduled evaluations run as one worker launch
+    # (system.cu run_scheduled): fewer launches than epochs, the records still
+    # sit at exact boundaries (updates = m x epoch at every record), every epoch
+    # of work is credited, and the worker time is a part of the solve time
+    A, b, xs = capi.generate_fixed_theta(40000, 20000, 30, seed=41)
+    bb = float(b @ b)
+    with capi.System(A, b) as S:
+        W = S.max_resident_warps()
+        t = S.solve(threads=W, epochs=500, target=1e-12 * bb, sampling=capi.SLICE_SHUFFLE, seed=2, x_star=xs)
+        st = S.stats()
+    ep = [int(e) for e in t["epoch_index"]]
+    assert ep[0] == 0 and ep == sorted(ep) and t["r_sq"][-1] <= 1e-12 * bb
+    assert all(int(u) == A.m * e for u, e in zip(t["updates_applied"], ep))
+    assert st["projections"] == A.m * ep[-1]
+    assert st["worker_launches"] < ep[-1]
+    assert 0.0 < st["worker_ms"] <= st["solve_ms"]
+    Ao = oracle.C.from_arrays(A.m, A.n, A.row_ptr, A.col_idx, A.values)
+    rs, _ = oracle.C.residuals(Ao, t["final_x"], b)
+    assert abs(rs - t["r_sq"][-1]) <= 1e-9 * rs
