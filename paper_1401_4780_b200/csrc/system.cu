@@ -1114,7 +1114,20 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     // all epochs of work (resolve_stats).
     s->lw_epochs.clear();
     s->lw_pair.clear();
-    static const bool no_fuse = env_flag("ASYRK_NO_FUSE");
+    // Fused only while the records stream within about twice the L2 per epoch:
+    // configs 2 and 4 (77 / 130 MB of records) gain 7% / 3%, config 3 (832 MB
+    // streamed from HBM every epoch) loses 1-2% (profiles/r02_ab_fuse_*.json,
+    // r02_fuse_cfg34.txt) — its epochs are 1.35 ms, so the per-launch drain is
+    // negligible there and warps drifting apart across unrecorded boundaries
+    // scatter the record stream
+    static const bool no_fuse_env = env_flag("ASYRK_NO_FUSE");
+    static const size_t l2_bytes = [] {
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        return (size_t)(l2 > 0 ? l2 : 126 << 20);
+    }();
+    const bool no_fuse = no_fuse_env || s->rec_bytes > 2 * l2_bytes;
     auto enqueue_worker = [&](long long b, long long b_end) {
         wa.epoch0 = epoch_of(b);
         wa.span0 = epoch_of(b_end) - wa.epoch0;
@@ -2961,11 +2974,14 @@ asyrk_status mrhs_run(std::vector<asyrk_mrhs*>& hs, const std::vector<int>& devs
     }
     commit_all();  // boundary 0
     asyrk_mrhs* h0 = hs[0];
-    static const bool no_fuse = env_flag("ASYRK_NO_FUSE");
+    // fused launches up to the next evaluation (ASYRK_MRHS_FUSE=1) are off by
+    // default here: at config 5 (0.57 ms epochs) they measured 22.6 vs 22.2 ms
+    // per solve and the same per-rank shard times (profiles/r02_ab_c5*.json)
+    static const bool fuse = env_flag("ASYRK_MRHS_FUSE") && !env_flag("ASYRK_NO_FUSE");
     while (h0->b < h0->max_chunks) {
         // with every record read, the next evaluation is known: one launch up to it
         // (the same on every shard and rank: the schedule follows the all-reduced records)
-        const long long b_end = (h0->pending < 0 && !no_fuse)
+        const long long b_end = (h0->pending < 0 && fuse)
                                     ? std::min(std::max(h0->next_mon, h0->b + 1), h0->max_chunks)
                                     : h0->b + 1;
         for (size_t g = 0; g < G; ++g) {
