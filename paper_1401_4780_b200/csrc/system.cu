@@ -1109,9 +1109,9 @@ asyrk_status run_scheduled(asyrk_system* s, const SolveSpec& sp, WorkerArgs& wa,
     // exactly at the next evaluated boundary): config 2 runs ~10 launches for 42
     // epochs instead of 43, without the drain and ramp of every epoch. The
     // launch behind an evaluation is one chunk (the gap after it is not known
-    // until the host has read the record). Fused launches and the first launch
-    // of a solve are timed with event pairs; worker_ms = their ms per epoch x
-    // all epochs of work (resolve_stats).
+    // until the host has read the record). Fused launches and a sample of the
+    // one-chunk ones (timed_launch) are timed with event pairs; worker_ms =
+    // their ms per epoch x all epochs of work (resolve_stats).
     s->lw_epochs.clear();
     s->lw_pair.clear();
     // Fused only while the records stream within about twice the L2 per epoch:
