@@ -280,7 +280,7 @@ asyrk_status asyrk_sweep_threads(const asyrk_csr_view* A, const double* b, const
  * csrc/schedule.h), host arithmetic: given the records so far (boundaries in
  * snapshot intervals, ascending, and their r_sq), the next boundary to
  * evaluate. every != 0 (record_every_boundary) or target <= 0: the next one.
- * max_gap <= 0: the default (16, or ASYRK_MONITOR_MAX_GAP). Exposed so that
+ * max_gap <= 0: the default (24, or ASYRK_MONITOR_MAX_GAP). Exposed so that
  * multi-rank drivers in any language take the same decisions. */
 asyrk_status asyrk_monitor_schedule_next(double target_r_sq, int32_t every, int64_t max_gap,
                                          const int64_t* boundaries, const double* r_sq, int64_t count,

@@ -119,17 +119,19 @@ def _free_port():
 def test_monitor_schedule_host_arithmetic():
     # asyrk_monitor_schedule_next (csrc/schedule.h): the next boundary while
     # fewer than two records exist / the residual did not drop / every boundary
-    # is requested / the target is 0; else the last boundary at or before the
+    # is requested / the target is 0; else the first boundary at or after the
     # predicted crossing, at least 1 and at most the max gap
     nx = capi.monitor_schedule_next
     assert nx(1e-6, [0], [1.0]) == 1
     assert nx(1e-6, [3, 4], [1.0, 2.0]) == 5
     assert nx(1e-6, [3, 4], [1.0, 0.5], every=True) == 5
     assert nx(0.0, [3, 4], [1.0, 0.5]) == 5
-    # r halves per boundary: the crossing is 20 boundaries away -> there, capped at the max gap (16)
-    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0]) == 4 + 16
-    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0], max_gap=30) == 4 + 20
-    assert nx(2.0 ** -5.5, [3, 4], [2.0, 1.0]) == 4 + 5  # the last boundary at or before the crossing
+    # r halves per boundary: the crossing is 30 boundaries away -> there, capped at the max gap (24)
+    assert nx(2.0 ** -30, [3, 4], [2.0, 1.0]) == 4 + 24
+    assert nx(2.0 ** -30, [3, 4], [2.0, 1.0], max_gap=40) == 4 + 30
+    assert nx(2.0 ** -20, [3, 4], [2.0, 1.0]) == 4 + 20
+    assert nx(2.0 ** -5.5, [3, 4], [2.0, 1.0]) == 4 + 6  # the first boundary at or after the crossing
+    assert nx(2.0 ** -5, [3, 4], [2.0, 1.0]) == 4 + 5  # (a crossing on a boundary: that boundary)
     assert nx(2.0 ** -1, [3, 4], [2.0, 1.0]) == 4 + 1  # at most 1 away: the next one
     assert nx(0.9, [3, 4], [2.0, 1.0]) == 4 + 1
 
