@@ -1,4 +1,5 @@
-# A/B: x gathers through L1 (build with -DASYRK_X_L1=1, stale until eviction) vs L1-bypassing
+# A/B (history): x gathers through L1 (an experiment build with -DASYRK_X_L1=1, not kept; results in
+# profiles/r02_x_l1_ab.txt and DESIGN §10) vs L1-bypassing
 mkdir -p gpurun_out
 for i in 1 2; do
   timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-cfg5 > gpurun_out/l1_off_$i.json 2>/dev/null; echo "off rc=$?"

@@ -1,5 +1,6 @@
-"""Dev probe: config-1 tolerance-mode solve (coefficient forwarding unless
-ASYRK_DET_FORWARD=0) against the bitwise mode: median solve_ms of 5 after 2
+"""Dev probe (history: the coefficient-forwarding kernel it A/B'd lives in
+commit 4426b6e and was removed as slower; today it times the tolerance mode):
+config-1 tolerance-mode solve against the bitwise mode: median solve_ms of 5 after 2
 warm-ups, relative difference of final_x, run-to-run reproducibility; plus
 ragged-row systems (E = 2, 4 lanes' slots)."""
 import os
